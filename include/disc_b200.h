@@ -1,0 +1,122 @@
+/* disc-b200: B200-native backend for the DISC dynamic-shape compiler's fused-kernel path.
+ *
+ * C ABI (extern "C", plain pointers and sizes, no C++ or torch types).  The reference
+ * artifact (/root/reference/proj) has no FFI -- its boundary is the C++ API -- so each
+ * entry point below cites the reference C++ call it stands in for.  Status codes follow
+ * the reference CLI exit codes (tools/disc_main.cpp:353-366): 0 ok, 2 usage,
+ * 3 parse/validation/compile error, 4 runtime/internal error.  On failure
+ * disc_last_error() holds "error[<class>]: <message>" with the reference's message text.
+ */
+#ifndef DISC_B200_H_
+#define DISC_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct disc_compiler_s* disc_compiler;
+typedef struct disc_plan_s* disc_plan;          /* immutable, shareable across threads */
+typedef struct disc_executor_s* disc_executor;  /* one per (host thread, device, stream) */
+
+/* ---- errors / memory --------------------------------------------------- */
+const char* disc_last_error(void);       /* thread-local; error.hpp:25-63 classes */
+int disc_last_error_class(void);         /* ErrorClass enum value, -1 if none */
+void disc_free(void* p);                 /* frees strings returned through char** */
+const char* disc_version(void);
+
+/* ---- compile side (host) ----------------------------------------------- */
+/* parse_graph + compile_graph (framework.cpp:350, codegen.cpp:688) */
+int disc_compile_graph(const char* graph_json, int inject_constraints, int enable_fusion,
+                       int static_fallback, disc_plan* out);
+/* static_specialize (codegen.cpp:698) */
+int disc_static_specialize(const char* graph_json, disc_plan* out);
+/* Compiler: shape-agnostic plan cache with coalescing (codegen.cpp:762-802) */
+int disc_compiler_create(int inject_constraints, int enable_fusion, int static_fallback,
+                         disc_compiler* out);
+void disc_compiler_destroy(disc_compiler c);
+int disc_compiler_compile(disc_compiler c, const char* graph_json, disc_plan* out);
+void disc_compiler_stats(disc_compiler c, int64_t* compile_count, int64_t* cache_hits);
+/* cache_key (codegen.cpp:703), dump-ir stages (codegen.cpp:624-684), lower_to_dhlo+to_json */
+int disc_cache_key(const char* graph_json, int inject_constraints, int enable_fusion,
+                   int static_fallback, char** out);
+int disc_dump_stage(const char* graph_json, int inject_constraints, int enable_fusion,
+                    const char* stage, char** out);
+int disc_lower_dhlo_json(const char* graph_json, char** out);
+int disc_dhlo_roundtrip(const char* dhlo_json, char** out); /* dhlo_from_json -> to_json */
+
+/* ---- plans ------------------------------------------------------------- */
+/* plan_from_json / plan_to_json / check_plan (runtime_program.cpp:182-575) */
+int disc_plan_from_json(const char* plan_json, disc_plan* out);
+int disc_plan_to_json(disc_plan p, char** out);
+int disc_plan_check(disc_plan p, char** diagnostics_json);
+void disc_plan_retain(disc_plan p);
+void disc_plan_release(disc_plan p);
+int disc_plan_num_inputs(disc_plan p);
+const char* disc_plan_input_name(disc_plan p, int i);
+int disc_plan_input_rank(disc_plan p, int i);
+int disc_plan_num_outputs(disc_plan p);
+const char* disc_plan_output_name(disc_plan p, int i);
+int disc_plan_num_kernels(disc_plan p);
+int64_t disc_plan_eager_op_count(disc_plan p);
+int64_t disc_plan_host_instruction_count(disc_plan p);
+/* Evaluate the host shape program for concrete input dims (EvalShape, executor.cpp:303-341):
+ * writes the register file (up to cap entries) and each output's dims. */
+int disc_plan_eval_shapes(disc_plan p, int n_inputs, const int64_t* const* dims, const int* ranks,
+                          int64_t* regs, int regs_cap, int* n_regs);
+
+/* ---- runtime flow on the device ---------------------------------------- */
+/* Executor (executor.hpp:74-83): owns a stream-ordered device caching allocator that
+ * persists across runs.  `cuda_stream` may be NULL (legacy default stream). */
+int disc_executor_create(int device, void* cuda_stream, disc_executor* out);
+void disc_executor_destroy(disc_executor e);
+int disc_executor_set_stream(disc_executor e, void* cuda_stream);
+/* Executor::run (executor.cpp:221-465).  Inputs are f32, row-major, bound by name; data
+ * pointers are device pointers, or host pointers when inputs_on_host != 0 (copied H2D
+ * inside the call).  Launches are asynchronous on the executor's stream; outputs stay
+ * valid (device-resident) until the next run on this executor. */
+int disc_executor_run(disc_executor e, disc_plan p, int n_inputs, const char* const* names,
+                      const void* const* data, const int64_t* const* dims, const int* ranks,
+                      int inputs_on_host);
+int disc_executor_num_outputs(disc_executor e);
+/* Device pointer + dims of output i of the last run. */
+int disc_executor_output(disc_executor e, int i, const float** dptr, const int64_t** dims,
+                         int* rank);
+/* Copies output i (stream-ordered) to dst (host if dst_on_host, else device); host copies
+ * synchronize the stream. */
+int disc_executor_copy_output(disc_executor e, int i, void* dst, int dst_on_host);
+int disc_executor_synchronize(disc_executor e);
+/* ExecStats (executor.hpp:30-40): launch_count, library_calls, host_instruction_count,
+ * peak_bytes, alloc_calls, allocator_cache_hits, aliased_allocs; ms2 = host_ms, kernel_ms.
+ * kernel_ms is device time (CUDA events) when timing is enabled, else 0. */
+int disc_executor_stats(disc_executor e, int64_t* s7, double* ms2);
+/* BufferEvent list (executor.hpp:44-49): 4 ints per event (logical, physical, alloc_instr,
+ * dealloc_instr). */
+int disc_executor_num_events(disc_executor e);
+int disc_executor_event(disc_executor e, int i, int* four);
+/* Device kernels launched by the last run (CUDA launches, not plan kLaunch count). */
+int64_t disc_executor_device_launches(disc_executor e);
+/* 1: time every kLaunch/kLibraryCall with CUDA events (adds per-launch sync). */
+int disc_executor_set_timing(disc_executor e, int enabled);
+/* Schedule override for testing: "auto" (default), "materialize" (per-member tape),
+ * "fused" (forbid the per-member fallback), "twopass"/"atomic" column reductions. */
+int disc_executor_set_schedule(disc_executor e, const char* schedule);
+/* Allocator byte budget for cached free blocks (0 = unlimited). */
+int disc_executor_set_cache_budget(disc_executor e, int64_t bytes);
+
+/* ---- single-kernel entry (run_kernel, executor.cpp:137-219) ------------- */
+/* Runs artifact `kernel` at version `version` on device externals with the given
+ * register file; outputs are device buffers owned by the executor until the next call. */
+int disc_executor_run_kernel(disc_executor e, disc_plan p, int kernel, int version, int n_ext,
+                             const float* const* ext, const int64_t* const* ext_dims,
+                             const int* ext_ranks, const int64_t* regs, int n_regs);
+/* guard_passes (executor.cpp:78-98) */
+int disc_guard_passes(disc_plan p, int kernel, int version, const int64_t* regs, int n_regs);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DISC_B200_H_ */

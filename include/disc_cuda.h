@@ -1,0 +1,188 @@
+/* disc-b200 device layer: the kernel boundary under the runtime flow.
+ *
+ * Replaces the reference's in-process CPU "device" calls inside Executor::run:
+ *   run_kernel(KernelArtifact, VersionArtifact, externals, regs)  executor.cpp:137-219 (call: 421)
+ *   CachedAllocator::alloc/free/data                               executor.cpp:53-76  (calls: 347,363,457)
+ *   eval_matmul(a, b)                                             kernels.cpp:293-303 (call: 434)
+ * A fused tape is lowered on the host (once per plan) to a small register program and
+ * passed to the kernel BY VALUE (__grid_constant__ parameters); shapes are bound per
+ * launch as gather maps.  Nothing is compiled per shape.
+ */
+#ifndef DISC_CUDA_H_
+#define DISC_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DISC_MAX_RANK 8
+#define DISC_MAX_INSTR 64
+#define DISC_MAX_LOADS 16
+#define DISC_MAX_OUTS 8
+#define DISC_MAX_SLOTS 12
+#define DISC_MAX_CONCAT 8
+
+/* Program opcodes.  Elementwise ops have the reference's f32 semantics (kernels.cpp:26-44):
+ * IEEE add/sub/mul/div (no FMA contraction), max(a,b) = (a<b)?b:a, libdevice expf/tanhf. */
+enum disc_op {
+  DISC_OP_LOAD = 0,   /* acc = ext[load] at map(f) */
+  DISC_OP_ADD, DISC_OP_SUB, DISC_OP_MUL, DISC_OP_DIV, DISC_OP_MAX,
+  DISC_OP_EXP, DISC_OP_TANH, DISC_OP_NEG,
+  DISC_OP_COPY,       /* acc = a */
+  DISC_OP_REDVAL,     /* acc = the current row's reduce result (row schedule only) */
+};
+#define DISC_SRC_ACC 0xFF /* operand is the accumulator register */
+#define DISC_SRC_NONE 0xFE
+
+typedef struct {
+  uint8_t op;
+  uint8_t a, b;   /* operand slots or DISC_SRC_ACC */
+  uint8_t dst;    /* slot to also keep the result in, or DISC_SRC_NONE */
+  int8_t load;    /* LOAD: index into loads[] */
+  int8_t out;     /* >= 0: store result to outs[out][f] */
+  uint8_t pad0, pad1;
+} disc_instr;
+
+/* Gather map: out flat index f -> source flat index
+ *   src = offset + sum_d coord_d(f) * stride[d], coords row-major over dims[0..rank).
+ * rank 0 means identity (src = f).  magic/shift: u32 fast division for dims[d] when
+ * the launch uses 32-bit indexing (dims[d] == 1 -> magic 0). */
+enum disc_load_mode {
+  DISC_LOAD_IDENTITY = 0,  /* contiguous at f */
+  DISC_LOAD_GATHER = 1,    /* general gather */
+  DISC_LOAD_ROWSCALAR = 2, /* row schedule: value depends only on the row (read once/row) */
+};
+typedef struct {
+  const float* ptr;
+  int32_t rank;
+  int32_t mode;
+  int32_t vec_ok;   /* VEC=4 path: 1 = 128-bit load, 2 = splat (inner stride 0), 0 = 4 scalar loads */
+  int32_t pad;
+  int64_t offset;
+  int64_t dims[DISC_MAX_RANK];
+  int64_t strides[DISC_MAX_RANK];
+  uint32_t magic[DISC_MAX_RANK];
+  uint32_t shift[DISC_MAX_RANK];
+} disc_load;
+
+typedef struct {
+  int32_t n_instr;
+  int32_t n_slots;
+  int32_t n_loads;
+  int32_t n_outs;
+  disc_instr code[DISC_MAX_INSTR];
+  disc_load loads[DISC_MAX_LOADS];
+  float* outs[DISC_MAX_OUTS];
+} disc_program;
+
+enum disc_reduce_kind { DISC_REDUCE_SUM = 0, DISC_REDUCE_MAX = 1 };
+
+/* Elementwise (kLoop) schedule: one program over the flat space [0, total). */
+typedef struct {
+  disc_program prog;
+  int64_t total;
+  int32_t vec;      /* 4 or 1 */
+  int32_t wide;     /* 1: 64-bit index math */
+} disc_loop_launch;
+
+/* Reduce schedules over the reduce argument collapsed to [K, R, C] (R reduced). */
+enum disc_reduce_schedule {
+  DISC_SCHED_ROW = 0,       /* C == 1: rows of R, G threads per row (warp / block) */
+  DISC_SCHED_COL_TWOPASS,   /* split-R partials in f64 workspace, ordered finalize */
+  DISC_SCHED_COL_ATOMIC,    /* split-R f64 atomics into workspace, finalize */
+  DISC_SCHED_COL_SINGLE,    /* one pass, no split */
+  DISC_SCHED_GENERIC,       /* non-contiguous reduced axes: thread per output */
+};
+
+typedef struct {
+  disc_program pre;         /* ends with the reduce argument in acc; stores pre outputs */
+  disc_program post;        /* row schedule fused epilogue (REDVAL), n_instr 0 if none */
+  int64_t K, R, C;          /* collapsed geometry (ROW: C == 1) */
+  int32_t kind;             /* disc_reduce_kind */
+  int32_t schedule;         /* disc_reduce_schedule */
+  int32_t vec;              /* 4 or 1 along the contiguous dim */
+  int32_t wide;
+  int32_t group;            /* ROW: threads per row (power of two) */
+  int32_t splits;           /* COL: number of R splits */
+  float* red_out;           /* f32 reduce result [K*C] */
+  double* workspace;        /* COL two-pass/atomic: f64 [splits or 1][K*C] */
+  /* GENERIC: arg dims and reduced-axis mask */
+  int32_t g_rank;
+  int32_t g_mask;
+  int64_t g_dims[DISC_MAX_RANK];
+} disc_reduce_launch;
+
+/* Standalone pad (eval_pad, kernels.cpp:125-147), output-driven gather. */
+typedef struct {
+  const float* in;
+  float* out;
+  int32_t rank;
+  float value;
+  int64_t total;
+  int64_t out_dims[DISC_MAX_RANK];
+  int64_t in_dims[DISC_MAX_RANK];
+  int64_t low[DISC_MAX_RANK];
+  int64_t step[DISC_MAX_RANK];   /* 1 + interior */
+} disc_pad_launch;
+
+/* Standalone concat (eval_concat, kernels.cpp:196-232) of up to DISC_MAX_CONCAT parts. */
+typedef struct {
+  const float* parts[DISC_MAX_CONCAT];
+  int64_t part_axis[DISC_MAX_CONCAT];  /* extent along the axis */
+  int32_t n_parts;
+  int32_t pad;
+  float* out;
+  int64_t outer, inner;   /* out viewed as [outer, axis_total, inner] */
+  int64_t axis_total;
+  int64_t axis_offset;    /* where parts[0] starts along the axis (multi-launch concat) */
+} disc_concat_launch;
+
+/* ---- device management --------------------------------------------------- */
+const char* disc_cuda_last_error(void);
+int disc_cuda_device_count(int* n);
+int disc_cuda_set_device(int device);
+int disc_cuda_device_info(int device, int* sm_count, int64_t* l2_bytes, int64_t* hbm_bytes);
+int disc_cuda_stream_create(void** stream);
+int disc_cuda_stream_destroy(void* stream);
+int disc_cuda_stream_synchronize(void* stream);
+int disc_cuda_device_synchronize(void);
+
+/* ---- memory (raw; the exact-size caching policy lives in the executor) ---- */
+int disc_cuda_malloc(size_t bytes, void* stream, void** dptr);   /* stream-ordered pool */
+int disc_cuda_free(void* dptr, void* stream);
+int disc_cuda_host_alloc(size_t bytes, void** hptr);             /* pinned */
+int disc_cuda_host_free(void* hptr);
+/* kind: 0 h2d, 1 d2h, 2 d2d, 3 default (UVA) */
+int disc_cuda_memcpy(void* dst, const void* src, size_t bytes, int kind, void* stream);
+int disc_cuda_memset(void* dst, int value, size_t bytes, void* stream);
+
+/* ---- events --------------------------------------------------------------- */
+int disc_cuda_event_create(void** ev);
+int disc_cuda_event_destroy(void* ev);
+int disc_cuda_event_record(void* ev, void* stream);
+int disc_cuda_event_synchronize(void* ev);
+int disc_cuda_event_elapsed_ms(void* start, void* stop, float* ms);
+
+/* ---- kernels (asynchronous on `stream`) ----------------------------------- */
+int disc_cuda_launch_loop(const disc_loop_launch* l, void* stream);
+int disc_cuda_launch_reduce(const disc_reduce_launch* l, void* stream);
+int disc_cuda_launch_pad(const disc_pad_launch* l, void* stream);
+int disc_cuda_launch_concat(const disc_concat_launch* l, void* stream);
+/* C[m,n] = A[m,k] B[k,n], f32 in/out, f64 accumulation (eval_matmul semantics). */
+int disc_cuda_gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c,
+                   void* stream);
+/* Fills n floats with uniform [lo, hi) (counter-based; bench/test input synthesis). */
+int disc_cuda_fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, void* stream);
+/* Writes `bytes` to a scratch buffer to evict L2 between timed iterations. */
+int disc_cuda_flush_l2(void* scratch, size_t bytes, void* stream);
+/* Number of kernels this library has launched (process-wide counter). */
+int64_t disc_cuda_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DISC_CUDA_H_ */

@@ -1,0 +1,15 @@
+"""disc-b200: B200-native backend for the DISC dynamic-shape compiler's fused-kernel path.
+
+Host: clean-room C++ compile pipeline (graph -> DHLO -> constraints -> fusion -> plan),
+byte-identical plans to the reference.  Device: sm_100a fused tape kernels behind a
+C ABI (include/disc_b200.h, include/disc_cuda.h).  See DESIGN.md.
+"""
+from .api import (CompileOptions, CompiledPlan, Compiler, DeviceBuffer, DiscError, ExecResult, ExecStats,
+                  Executor, cache_key, compile_graph, cuda_available, dhlo_roundtrip, dump_stage, guard_passes,
+                  kernel_launches, lib, lower_dhlo_json, static_specialize)
+
+__all__ = [
+    "CompileOptions", "CompiledPlan", "Compiler", "DeviceBuffer", "DiscError", "ExecResult", "ExecStats",
+    "Executor", "cache_key", "compile_graph", "cuda_available", "dhlo_roundtrip", "dump_stage", "guard_passes",
+    "kernel_launches", "lib", "lower_dhlo_json", "static_specialize",
+]

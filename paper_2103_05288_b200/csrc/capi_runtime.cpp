@@ -1,0 +1,174 @@
+// C ABI, runtime side: executors over a device + stream (include/disc_b200.h).
+#include <cstring>
+
+#include "capi_common.hpp"
+#include "disc_cuda.h"
+#include "runtime/runtime_flow.hpp"
+#include "runtime/shape_eval.hpp"
+
+using namespace disc;
+using disc_capi::guard;
+
+namespace disc::rt {
+struct PreparedPlan {};  // per-plan device lowering cache (launch binding is per shape)
+std::shared_ptr<const PreparedPlan> prepare_plan(const CompiledPlan&) { return std::make_shared<PreparedPlan>(); }
+}  // namespace disc::rt
+
+struct disc_executor_s {
+  disc_executor_s(int device, void* stream) : ex(device, stream) {}
+  rt::DeviceExecutor ex;
+};
+
+namespace {
+int64_t bytes_of(const int64_t* dims, int rank) {
+  int64_t n = 1;
+  for (int i = 0; i < rank; ++i) n *= dims[i];
+  return n * 4;
+}
+}  // namespace
+
+extern "C" {
+
+int disc_executor_create(int device, void* stream, disc_executor* out) {
+  return guard([&] {
+    int n = 0;
+    if (disc_cuda_device_count(&n) != 0 || n == 0)
+      throw RuntimeError(std::string("no CUDA device available: ") + disc_cuda_last_error());
+    *out = new disc_executor_s(device, stream);
+  });
+}
+
+void disc_executor_destroy(disc_executor e) { delete e; }
+
+int disc_executor_set_stream(disc_executor e, void* stream) {
+  return guard([&] { e->ex.set_stream(stream); });
+}
+
+int disc_executor_run(disc_executor e, disc_plan p, int n, const char* const* names, const void* const* data,
+                      const int64_t* const* dims, const int* ranks, int on_host) {
+  return guard([&] {
+    std::vector<rt::InputBinding> in(n);
+    for (int i = 0; i < n; ++i) {
+      in[i].name = names[i];
+      in[i].dims.assign(dims[i], dims[i] + ranks[i]);
+      in[i].ptr = on_host ? e->ex.stage_input(i, data[i], bytes_of(dims[i], ranks[i]))
+                          : static_cast<const float*>(data[i]);
+    }
+    e->ex.run(*p->plan, in);
+  });
+}
+
+int disc_executor_num_outputs(disc_executor e) { return static_cast<int>(e->ex.outputs().size()); }
+
+int disc_executor_output(disc_executor e, int i, const float** dptr, const int64_t** dims, int* rank) {
+  return guard([&] {
+    const auto& o = e->ex.outputs().at(i);
+    *dptr = o.ptr;
+    *dims = o.dims.data();
+    *rank = static_cast<int>(o.dims.size());
+  });
+}
+
+int disc_executor_copy_output(disc_executor e, int i, void* dst, int dst_on_host) {
+  return guard([&] {
+    const auto& o = e->ex.outputs().at(i);
+    int64_t n = 1;
+    for (int64_t d : o.dims) n *= d;
+    if (n == 0) return;
+    if (disc_cuda_memcpy(dst, o.ptr, static_cast<size_t>(n * 4), dst_on_host ? 1 : 2, e->ex.stream()) != 0)
+      throw RuntimeError(std::string("output copy: ") + disc_cuda_last_error());
+    if (dst_on_host && disc_cuda_stream_synchronize(e->ex.stream()) != 0)
+      throw RuntimeError(std::string("stream sync: ") + disc_cuda_last_error());
+  });
+}
+
+int disc_executor_synchronize(disc_executor e) {
+  return guard([&] {
+    if (disc_cuda_stream_synchronize(e->ex.stream()) != 0)
+      throw RuntimeError(std::string("device error: ") + disc_cuda_last_error());
+  });
+}
+
+int disc_executor_stats(disc_executor e, int64_t* s7, double* ms2) {
+  const auto& s = e->ex.stats();
+  int64_t v[7] = {s.launch_count, s.library_calls, s.host_instruction_count, s.peak_bytes,
+                  s.alloc_calls, s.allocator_cache_hits, s.aliased_allocs};
+  std::memcpy(s7, v, sizeof v);
+  if (ms2) {
+    ms2[0] = s.host_ms;
+    ms2[1] = s.kernel_ms;
+  }
+  return 0;
+}
+
+int disc_executor_num_events(disc_executor e) { return static_cast<int>(e->ex.events().size()); }
+
+int disc_executor_event(disc_executor e, int i, int* four) {
+  const auto& ev = e->ex.events().at(i);
+  four[0] = ev.logical;
+  four[1] = ev.physical;
+  four[2] = ev.alloc_instr;
+  four[3] = ev.dealloc_instr;
+  return 0;
+}
+
+int64_t disc_executor_device_launches(disc_executor e) { return e->ex.device_launches(); }
+
+int disc_executor_set_timing(disc_executor e, int enabled) {
+  e->ex.set_timing(enabled != 0);
+  return 0;
+}
+
+int disc_executor_set_schedule(disc_executor e, const char* s) {
+  return guard([&] {
+    std::string v = s ? s : "auto";
+    rt::SchedulePref p;
+    if (v == "auto") p = rt::SchedulePref::kAuto;
+    else if (v == "materialize") p = rt::SchedulePref::kMaterialize;
+    else if (v == "fused") p = rt::SchedulePref::kFusedOnly;
+    else if (v == "twopass") p = rt::SchedulePref::kTwoPass;
+    else if (v == "atomic") p = rt::SchedulePref::kAtomic;
+    else throw Error(ErrorClass::kUsage, "unknown schedule " + v);
+    e->ex.set_schedule(p);
+  });
+}
+
+int disc_executor_set_cache_budget(disc_executor e, int64_t bytes) {
+  e->ex.set_cache_budget(bytes);
+  return 0;
+}
+
+int disc_executor_run_kernel(disc_executor e, disc_plan p, int kernel, int version, int n_ext, const float* const* ext,
+                             const int64_t* const* ext_dims, const int* ext_ranks, const int64_t* regs, int n_regs) {
+  return guard([&] {
+    const KernelArtifact& art = p->plan->kernels.at(kernel);
+    const VersionArtifact* v = nullptr;
+    for (const auto& x : art.versions)
+      if (x.id == version) v = &x;
+    if (!v) throw InternalError("no such version");
+    std::vector<rt::DevTensor> ex;
+    for (int i = 0; i < n_ext; ++i) ex.push_back({ext[i], std::vector<int64_t>(ext_dims[i], ext_dims[i] + ext_ranks[i])});
+    e->ex.run_kernel(art, *v, ex, std::vector<int64_t>(regs, regs + n_regs));
+  });
+}
+
+int disc_guard_passes(disc_plan p, int kernel, int version, const int64_t* regs, int n_regs) {
+  const KernelArtifact& art = p->plan->kernels.at(kernel);
+  std::vector<int64_t> r(regs, regs + n_regs);
+  for (const auto& v : art.versions) {
+    if (v.id != version) continue;
+    for (const auto& g : v.guards) {
+      if (g.kind == GuardTest::Kind::kNever) return 0;
+      if (g.kind == GuardTest::Kind::kRefEqual && rt::resolve(g.a, r) != rt::resolve(g.b, r)) return 0;
+      if (g.kind == GuardTest::Kind::kTotalDivisibleBy4) {
+        int64_t total = 1;
+        for (const auto& d : art.space_dims) total *= rt::resolve(d, r);
+        if (total % 4 != 0) return 0;
+      }
+    }
+    return 1;
+  }
+  return -1;
+}
+
+}  // extern "C"

@@ -1,0 +1,154 @@
+// Standalone (non-fusible) data-movement artifacts and the library GEMM:
+//   pad    -> output-driven gather (eval_pad, reference kernels.cpp:125-147)
+//   concat -> output-driven gather (eval_concat, kernels.cpp:196-232)
+//   gemm   -> f32 in/out with f64 accumulation (eval_matmul, kernels.cpp:261-303)
+// Transpose and reshape run through the fused loop kernel as single-load programs.
+#include <cstdint>
+
+#include "disc_cuda.h"
+
+namespace disc_dev {
+
+__global__ void __launch_bounds__(256) k_pad(const __grid_constant__ disc_pad_launch P) {
+  for (int64_t f = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; f < P.total;
+       f += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t rem = f, src = 0, in_stride = 1;
+    bool inside = true;
+    for (int d = P.rank - 1; d >= 0; --d) {
+      const int64_t c = rem % P.out_dims[d];
+      rem /= P.out_dims[d];
+      const int64_t t = c - P.low[d];
+      if (t < 0 || t % P.step[d] != 0) {
+        inside = false;
+      } else {
+        const int64_t i = t / P.step[d];
+        if (i >= P.in_dims[d]) inside = false;
+        src += i * in_stride;
+      }
+      in_stride *= P.in_dims[d];
+    }
+    P.out[f] = inside ? __ldg(P.in + src) : P.value;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_concat(const __grid_constant__ disc_concat_launch C) {
+  int64_t span = 0;
+  for (int p = 0; p < C.n_parts; ++p) span += C.part_axis[p];
+  const int64_t total = C.outer * span * C.inner;
+  for (int64_t f = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; f < total;
+       f += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = f % C.inner;
+    const int64_t rest = f / C.inner;
+    int64_t a = rest % span;
+    const int64_t o = rest / span;
+    int p = 0;
+    while (a >= C.part_axis[p]) a -= C.part_axis[p++];
+    const float v = __ldg(C.parts[p] + (o * C.part_axis[p] + a) * C.inner + i);
+    C.out[(o * C.axis_total + C.axis_offset + (f / C.inner) % span) * C.inner + i] = v;
+  }
+}
+
+// 32x32 output tile per 256-thread block (each thread 4 outputs in a column strip),
+// K staged through shared memory in 32-wide slices; f64 accumulation.
+constexpr int kT = 32;
+__global__ void __launch_bounds__(256) k_gemm(int64_t m, int64_t k, int64_t n, const float* __restrict__ a,
+                                              const float* __restrict__ b, float* __restrict__ c) {
+  __shared__ float As[kT][kT + 1];
+  __shared__ float Bs[kT][kT + 1];
+  const int tx = threadIdx.x % kT, ty = threadIdx.x / kT;  // ty in [0, 8)
+  const int64_t row0 = static_cast<int64_t>(blockIdx.y) * kT, col = static_cast<int64_t>(blockIdx.x) * kT + tx;
+  double acc[4] = {0, 0, 0, 0};
+  for (int64_t k0 = 0; k0 < k; k0 += kT) {
+    for (int r = ty; r < kT; r += 8) {
+      const int64_t ar = row0 + r, ac = k0 + tx;
+      As[r][tx] = (ar < m && ac < k) ? a[ar * k + ac] : 0.f;
+      const int64_t br = k0 + r;
+      Bs[r][tx] = (br < k && col < n) ? b[br * n + col] : 0.f;
+    }
+    __syncthreads();
+    const int kk = static_cast<int>(k - k0 < kT ? k - k0 : kT);
+    for (int p = 0; p < kk; ++p) {
+      const double bv = Bs[p][tx];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] += static_cast<double>(As[ty + 8 * i][p]) * bv;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = row0 + ty + 8 * i;
+    if (r < m && col < n) c[r * n + col] = static_cast<float>(acc[i]);
+  }
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi) {
+  const float span = hi - lo;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t r = mix64(seed * 0x9E3779B97F4A7C15ull + static_cast<uint64_t>(i));
+    const float u = static_cast<float>(r >> 40) * (1.0f / 16777216.0f);  // [0, 1)
+    float v = lo + u * span;
+    dst[i] = v < hi ? v : lo;
+  }
+}
+
+__global__ void k_flush(uint4* p, int64_t n, uint32_t salt) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = make_uint4(salt, static_cast<uint32_t>(i), salt, 0u);
+}
+
+}  // namespace disc_dev
+
+namespace disc_launch {
+
+using namespace disc_dev;
+
+static int grid_for(int64_t n, int threads, int cap) {
+  const int64_t want = (n + threads - 1) / threads;
+  return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+cudaError_t pad(const disc_pad_launch& P, cudaStream_t s) {
+  if (P.total <= 0) return cudaSuccess;
+  k_pad<<<grid_for(P.total, 256, 148 * 16), 256, 0, s>>>(P);
+  return cudaGetLastError();
+}
+
+cudaError_t concat(const disc_concat_launch& C, cudaStream_t s) {
+  int64_t span = 0;
+  for (int p = 0; p < C.n_parts; ++p) span += C.part_axis[p];
+  const int64_t total = C.outer * span * C.inner;
+  if (total <= 0) return cudaSuccess;
+  k_concat<<<grid_for(total, 256, 148 * 16), 256, 0, s>>>(C);
+  return cudaGetLastError();
+}
+
+cudaError_t gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c, cudaStream_t s) {
+  if (m <= 0 || n <= 0) return cudaSuccess;
+  dim3 grid(static_cast<unsigned>((n + kT - 1) / kT), static_cast<unsigned>((m + kT - 1) / kT));
+  k_gemm<<<grid, 256, 0, s>>>(m, k, n, a, b, c);
+  return cudaGetLastError();
+}
+
+cudaError_t fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_fill_uniform<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(dst, n, seed, lo, hi);
+  return cudaGetLastError();
+}
+
+cudaError_t flush(void* p, size_t bytes, cudaStream_t s) {
+  static uint32_t salt = 1;
+  const int64_t n = static_cast<int64_t>(bytes / 16);
+  if (n <= 0) return cudaSuccess;
+  k_flush<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(static_cast<uint4*>(p), n, salt++);
+  return cudaGetLastError();
+}
+
+}  // namespace disc_launch

@@ -1,0 +1,1035 @@
+// Tape -> device program binding and schedule selection (see launcher.hpp).
+#include "launcher.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <tuple>
+
+#include "shape_eval.hpp"
+
+namespace disc::rt {
+
+namespace {
+
+void cuda_ok(int rc, const char* what) {
+  if (rc != 0) throw RuntimeError(std::string(what) + ": " + disc_cuda_last_error());
+}
+
+int64_t numel(const std::vector<int64_t>& d) {
+  int64_t n = 1;
+  for (int64_t x : d) n *= x;
+  return n;
+}
+
+std::vector<int64_t> row_major(const std::vector<int64_t>& dims) {
+  std::vector<int64_t> s(dims.size(), 1);
+  for (int i = static_cast<int>(dims.size()) - 2; i >= 0; --i) s[i] = s[i + 1] * dims[i + 1];
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// Gather maps: consumer flat index f -> source flat index.
+
+struct Map {
+  std::vector<int64_t> dims, strides;  // consumer dims (row-major), source stride per dim
+  int64_t offset = 0;
+  bool operator==(const Map& o) const { return dims == o.dims && strides == o.strides && offset == o.offset; }
+};
+
+// Drops extent-1 dims and merges contiguous neighbours; the result is a canonical form
+// (equal canonical forms => equal functions).
+Map canonical(const Map& m) {
+  Map c;
+  c.offset = m.offset;
+  for (size_t i = 0; i < m.dims.size(); ++i) {
+    if (m.dims[i] == 1) continue;
+    if (!c.dims.empty() && c.strides.back() == m.strides[i] * m.dims[i]) {
+      c.dims.back() *= m.dims[i];
+      c.strides.back() = m.strides[i];
+      continue;
+    }
+    c.dims.push_back(m.dims[i]);
+    c.strides.push_back(m.strides[i]);
+  }
+  if (c.dims.empty()) {
+    c.dims = {1};
+    c.strides = {0};
+  }
+  return c;
+}
+
+bool is_identity(const Map& c) {  // c canonical
+  if (c.offset != 0) return false;
+  return c.dims.size() == 1 && (c.strides[0] == 1 || c.dims[0] == 1);
+}
+
+Map identity_map(int64_t n) { return canonical(Map{{n}, {1}, 0}); }
+
+Map broadcast_map(const std::vector<int64_t>& in, const std::vector<int64_t>& out, const std::vector<int64_t>& bdims) {
+  Map m;
+  m.dims = out;
+  m.strides.assign(out.size(), 0);
+  auto st = row_major(in);
+  for (size_t i = 0; i < bdims.size(); ++i)
+    if (in[i] != 1) m.strides[bdims[i]] = st[i];
+  return canonical(m);
+}
+
+Map slice_map(const std::vector<int64_t>& in, const std::vector<int64_t>& starts, const std::vector<int64_t>& steps,
+              const std::vector<int64_t>& out) {
+  Map m;
+  m.dims = out;
+  auto st = row_major(in);
+  for (size_t i = 0; i < in.size(); ++i) {
+    m.offset += starts[i] * st[i];
+    m.strides.push_back(steps[i] * st[i]);
+  }
+  return canonical(m);
+}
+
+Map transpose_map(const std::vector<int64_t>& in, const std::vector<int64_t>& perm) {
+  Map m;
+  auto st = row_major(in);
+  for (int64_t p : perm) {
+    m.dims.push_back(in[p]);
+    m.strides.push_back(st[p]);
+  }
+  return canonical(m);
+}
+
+disc_load make_load(const float* ptr, const Map& c) {
+  disc_load L;
+  std::memset(&L, 0, sizeof L);
+  L.ptr = ptr;
+  if (is_identity(c)) {
+    L.mode = DISC_LOAD_IDENTITY;
+    L.rank = 0;
+    return L;
+  }
+  if (c.dims.size() > DISC_MAX_RANK) throw InternalError("gather map rank exceeds DISC_MAX_RANK");
+  L.mode = DISC_LOAD_GATHER;
+  L.rank = static_cast<int32_t>(c.dims.size());
+  L.offset = c.offset;
+  for (size_t d = 0; d < c.dims.size(); ++d) {
+    L.dims[d] = c.dims[d];
+    L.strides[d] = c.strides[d];
+    if (c.dims[d] < (int64_t{1} << 31)) fast_div_magic(static_cast<uint32_t>(c.dims[d]), &L.magic[d], &L.shift[d]);
+  }
+  return L;
+}
+
+// VEC=4 suitability of one load; sets vec_ok.
+bool vec4_load(disc_load& L) {
+  if (L.mode == DISC_LOAD_IDENTITY) return (reinterpret_cast<uintptr_t>(L.ptr) & 15) == 0;
+  const int r = L.rank;
+  if (L.dims[r - 1] % 4 != 0) return false;
+  const int64_t inner = L.strides[r - 1];
+  if (inner == 0) {
+    L.vec_ok = 2;
+    return true;
+  }
+  bool aligned = inner == 1 && (reinterpret_cast<uintptr_t>(L.ptr) & 15) == 0 && L.offset % 4 == 0;
+  for (int d = 0; d < r - 1 && aligned; ++d) aligned = L.strides[d] % 4 == 0;
+  L.vec_ok = aligned ? 1 : 0;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// Program assembly: SSA values (one per instruction) -> accumulator + slots.
+
+struct NotFusible {
+  const char* why;
+};
+
+class ProgramBuilder {
+ public:
+  int load(const float* ptr, const Map& c) {
+    auto key = std::make_tuple(ptr, c.dims, c.strides, c.offset);
+    auto it = cse_.find(key);
+    if (it != cse_.end()) return it->second;
+    if (loads_.size() >= DISC_MAX_LOADS) throw NotFusible{"too many loads"};
+    loads_.push_back(make_load(ptr, c));
+    int v = push({DISC_OP_LOAD, -1, -1, static_cast<int>(loads_.size()) - 1});
+    cse_[key] = v;
+    return v;
+  }
+  int op(int code, int a, int b = -1) { return push({code, a, b, -1}); }
+  int redval() {
+    if (red_ < 0) red_ = push({DISC_OP_REDVAL, -1, -1, -1});
+    return red_;
+  }
+  void output(int v, float* ptr) { outs_.emplace_back(v, ptr); }
+  bool empty() const { return ins_.empty(); }
+  std::vector<disc_load*> load_refs() {
+    std::vector<disc_load*> r;
+    for (auto& l : loads_) r.push_back(&l);
+    return r;
+  }
+
+  // result >= 0: the program must end with that value in the accumulator.
+  disc_program finish(int result) {
+    // Outputs: tag the producing instruction, or copy when it already stores elsewhere.
+    std::vector<int> out_of(ins_.size(), -1);
+    std::vector<float*> out_ptrs;
+    for (auto [v, ptr] : outs_) {
+      int o = static_cast<int>(out_ptrs.size());
+      if (o >= DISC_MAX_OUTS) throw NotFusible{"too many outputs"};
+      out_ptrs.push_back(ptr);
+      if (out_of[v] < 0) {
+        out_of[v] = o;
+      } else {
+        int c = push({DISC_OP_COPY, v, -1, -1});
+        out_of.push_back(o);
+        (void)c;
+      }
+    }
+    if (result >= 0 && result != static_cast<int>(ins_.size()) - 1) {
+      push({DISC_OP_COPY, result, -1, -1});
+      out_of.push_back(-1);
+    }
+    out_of.resize(ins_.size(), -1);
+    const int n = static_cast<int>(ins_.size());
+    if (n > DISC_MAX_INSTR) throw NotFusible{"program too long"};
+
+    // Operands not produced by the immediately preceding instruction need a slot.
+    std::vector<int> last_use(n, -1);
+    std::vector<char> slotted(n, 0);
+    for (int i = 0; i < n; ++i)
+      for (int v : {ins_[i].a, ins_[i].b})
+        if (v >= 0 && v != i - 1) {
+          slotted[v] = 1;
+          last_use[v] = std::max(last_use[v], i);
+        }
+    std::vector<int> slot_of(n, -1);
+    std::vector<int> holder(DISC_MAX_SLOTS, -1);  // slot -> value
+    int nslots = 0;
+    disc_program P;
+    std::memset(&P, 0, sizeof P);
+    for (int i = 0; i < n; ++i) {
+      // Slots whose value dies at i may be reused as i's destination (reads precede writes).
+      for (int s = 0; s < DISC_MAX_SLOTS; ++s)
+        if (holder[s] >= 0 && last_use[holder[s]] <= i) holder[s] = -1;
+      disc_instr& I = P.code[i];
+      I.op = static_cast<uint8_t>(ins_[i].code);
+      auto src = [&](int v) -> uint8_t {
+        if (v < 0) return DISC_SRC_NONE;
+        return v == i - 1 ? DISC_SRC_ACC : static_cast<uint8_t>(slot_of[v]);
+      };
+      I.a = src(ins_[i].a);
+      I.b = src(ins_[i].b);
+      I.load = static_cast<int8_t>(ins_[i].load);
+      I.out = static_cast<int8_t>(out_of[i]);
+      I.dst = DISC_SRC_NONE;
+      if (slotted[i]) {
+        int s = 0;
+        while (s < DISC_MAX_SLOTS && holder[s] >= 0) ++s;
+        if (s == DISC_MAX_SLOTS) throw NotFusible{"too many live values"};
+        holder[s] = i;
+        slot_of[i] = s;
+        I.dst = static_cast<uint8_t>(s);
+        nslots = std::max(nslots, s + 1);
+      }
+    }
+    P.n_instr = n;
+    P.n_slots = nslots;
+    P.n_loads = static_cast<int32_t>(loads_.size());
+    for (size_t l = 0; l < loads_.size(); ++l) P.loads[l] = loads_[l];
+    P.n_outs = static_cast<int32_t>(out_ptrs.size());
+    for (size_t o = 0; o < out_ptrs.size(); ++o) P.outs[o] = out_ptrs[o];
+    return P;
+  }
+
+ private:
+  struct Ins {
+    int code, a, b, load;
+  };
+  std::vector<Ins> ins_;
+  std::vector<disc_load> loads_;
+  std::map<std::tuple<const float*, std::vector<int64_t>, std::vector<int64_t>, int64_t>, int> cse_;
+  std::vector<std::pair<int, float*>> outs_;
+  int red_ = -1;
+  int push(Ins i) {
+    ins_.push_back(i);
+    return static_cast<int>(ins_.size()) - 1;
+  }
+};
+
+int dhlo_to_op(DhloOpKind k) {
+  switch (k) {
+    case DhloOpKind::kAdd: return DISC_OP_ADD;
+    case DhloOpKind::kSub: return DISC_OP_SUB;
+    case DhloOpKind::kMul: return DISC_OP_MUL;
+    case DhloOpKind::kDiv: return DISC_OP_DIV;
+    case DhloOpKind::kMaximum: return DISC_OP_MAX;
+    case DhloOpKind::kExp: return DISC_OP_EXP;
+    case DhloOpKind::kTanh: return DISC_OP_TANH;
+    case DhloOpKind::kNeg: return DISC_OP_NEG;
+    default: throw InternalError("not an elementwise op");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Binding context for one launch.
+
+struct Binding {
+  const KernelArtifact& art;
+  const VersionArtifact& ver;
+  const std::vector<DevTensor>& ext;
+  const std::vector<int64_t>& regs;
+  std::vector<std::vector<int64_t>> dims;  // per member
+  int red = -1;                            // reduce member
+  std::vector<char> post;                  // reachable from the reduce
+};
+
+// The map through which member t reads its data argument (broadcast/slice only).
+Map arg_map(const Binding& B, int t, const std::vector<int64_t>& arg_dims) {
+  const TapeInstr& ti = B.art.tape[t];
+  const auto& out = B.dims[t];
+  if (ti.kind == DhloOpKind::kDynamicBroadcastInDim)
+    return B.ver.implicit_broadcast ? broadcast_map(arg_dims, out, ti.dims) : identity_map(numel(out));
+  if (ti.kind == DhloOpKind::kDynamicSlice)
+    return slice_map(arg_dims, resolve_all(ti.slice_starts, B.regs), resolve_all(ti.slice_strides, B.regs), out);
+  return identity_map(numel(out));
+}
+
+const std::vector<int64_t>& ref_dims(const Binding& B, const TapeRef& r) {
+  return r.kind == TapeRef::Kind::kExternal ? B.ext.at(r.index).dims : B.dims.at(r.index);
+}
+
+// Lowers members into one program.  `red_ptr`/`row_fused` describe how post members
+// see the reduce result: REDVAL when row-aligned in a fused row kernel, else a load.
+class Lowering {
+ public:
+  Lowering(const Binding& B, ProgramBuilder& pb, const float* red_ptr, const Map* row_map)
+      : B_(B), pb_(pb), red_ptr_(red_ptr), row_map_(row_map) {}
+
+  int value(int t) {
+    auto it = memo_.find(t);
+    if (it != memo_.end()) return it->second;
+    const TapeInstr& ti = B_.art.tape[t];
+    int v;
+    if (t == B_.red) {
+      v = reduce_at(identity_map(numel(B_.dims[t])));
+    } else if (is_elementwise_binary(ti.kind)) {
+      int a = at_identity(ti.args[0]);
+      int b = at_identity(ti.args[1]);
+      v = pb_.op(dhlo_to_op(ti.kind), a, b);
+    } else if (is_elementwise_unary(ti.kind)) {
+      v = pb_.op(dhlo_to_op(ti.kind), at_identity(ti.args[0]));
+    } else if (ti.kind == DhloOpKind::kDynamicBroadcastInDim || ti.kind == DhloOpKind::kDynamicSlice) {
+      const TapeRef& a = ti.args[0];
+      Map m = arg_map(B_, t, ref_dims(B_, a));
+      if (a.kind == TapeRef::Kind::kExternal) v = pb_.load(B_.ext[a.index].ptr, m);
+      else if (is_identity(m)) v = value(a.index);
+      else if (a.index == B_.red) v = reduce_at(m);
+      else throw NotFusible{"member consumed through a gather"};
+    } else {
+      throw NotFusible{"op kind not fusible"};
+    }
+    memo_[t] = v;
+    return v;
+  }
+
+  int at_identity(const TapeRef& r) {
+    if (r.kind == TapeRef::Kind::kExternal) return pb_.load(B_.ext[r.index].ptr, identity_map(numel(B_.ext[r.index].dims)));
+    return value(r.index);
+  }
+
+ private:
+  const Binding& B_;
+  ProgramBuilder& pb_;
+  const float* red_ptr_;
+  const Map* row_map_;
+  std::map<int, int> memo_;
+
+  int reduce_at(const Map& m) {
+    if (row_map_) {
+      if (m == *row_map_) return pb_.redval();
+      throw NotFusible{"reduce read off-row"};
+    }
+    if (!red_ptr_) throw NotFusible{"reduce value unavailable in this phase"};
+    return pb_.load(red_ptr_, m);
+  }
+};
+
+std::vector<int64_t> reduce_out_dims(const std::vector<int64_t>& in, const std::vector<int64_t>& axes) {
+  std::vector<int64_t> out;
+  for (int i = 0; i < static_cast<int>(in.size()); ++i)
+    if (std::find(axes.begin(), axes.end(), i) == axes.end()) out.push_back(in[i]);
+  return out;
+}
+
+// Reduce geometry over the reduce argument's dims.
+struct Geometry {
+  int schedule = DISC_SCHED_ROW;
+  int64_t K = 1, R = 1, C = 1;
+  int rank = 0, mask = 0;
+  std::vector<int64_t> gdims;
+};
+
+Geometry reduce_geometry(const std::vector<int64_t>& dims, const std::vector<int64_t>& axes) {
+  Geometry g;
+  int64_t kept = 1, red = 1;
+  for (int i = 0; i < static_cast<int>(dims.size()); ++i) {
+    bool r = std::find(axes.begin(), axes.end(), i) != axes.end();
+    (r ? red : kept) *= dims[i];
+  }
+  if (kept == 0 || red == 0) {  // empty: identities only (or nothing at all)
+    g.K = kept;
+    g.R = red;
+    return g;
+  }
+  std::vector<std::pair<int64_t, bool>> seg;
+  for (int i = 0; i < static_cast<int>(dims.size()); ++i) {
+    if (dims[i] == 1) continue;
+    bool r = std::find(axes.begin(), axes.end(), i) != axes.end();
+    if (!seg.empty() && seg.back().second == r) seg.back().first *= dims[i];
+    else seg.emplace_back(dims[i], r);
+  }
+  auto pattern = [&](std::initializer_list<bool> p) {
+    if (seg.size() != p.size()) return false;
+    size_t i = 0;
+    for (bool b : p)
+      if (seg[i++].second != b) return false;
+    return true;
+  };
+  if (seg.empty()) return g;
+  if (pattern({true})) {
+    g.R = seg[0].first;
+  } else if (pattern({false})) {
+    g.K = seg[0].first;
+  } else if (pattern({false, true})) {
+    g.K = seg[0].first;
+    g.R = seg[1].first;
+  } else if (pattern({true, false})) {
+    g.schedule = DISC_SCHED_COL_SINGLE;
+    g.R = seg[0].first;
+    g.C = seg[1].first;
+  } else if (pattern({false, true, false})) {
+    g.schedule = DISC_SCHED_COL_SINGLE;
+    g.K = seg[0].first;
+    g.R = seg[1].first;
+    g.C = seg[2].first;
+  } else {
+    g.schedule = DISC_SCHED_GENERIC;
+    g.K = kept;
+    g.R = red;
+    g.rank = static_cast<int>(dims.size());
+    if (g.rank > DISC_MAX_RANK) throw NotFusible{"rank too large for generic reduce"};
+    g.gdims = dims;
+    for (int64_t a : axes) g.mask |= 1 << a;
+  }
+  return g;
+}
+
+int next_pow2(int64_t v) {
+  int p = 1;
+  while (p < v && p < 1024) p <<= 1;
+  return p;
+}
+
+int sm_count() {
+  static int n = [] {
+    int sm = 148;
+    int64_t l2 = 0, hbm = 0;
+    if (disc_cuda_device_info(0, &sm, &l2, &hbm) != 0) sm = 148;
+    return sm;
+  }();
+  return n;
+}
+
+constexpr int64_t kWideLimit = (int64_t{1} << 31) - 64;
+
+// ---------------------------------------------------------------------------
+
+struct Plan {
+  bool is_reduce = false;
+  disc_loop_launch loop;
+  disc_reduce_launch red;
+  bool has_post_pass = false;
+  disc_loop_launch post_pass;
+};
+
+void set_vec(std::vector<disc_program*> progs, int64_t unit, int32_t* vec) {
+  bool ok = unit % 4 == 0;
+  for (disc_program* P : progs) {
+    for (int l = 0; l < P->n_loads && ok; ++l) ok = vec4_load(P->loads[l]);
+    for (int o = 0; o < P->n_outs && ok; ++o) ok = (reinterpret_cast<uintptr_t>(P->outs[o]) & 15) == 0;
+  }
+  *vec = ok ? 4 : 1;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+
+void fast_div_magic(uint32_t d, uint32_t* magic, uint32_t* shift) {
+  if (d <= 1) {
+    *magic = 0;
+    *shift = 0;
+    return;
+  }
+  uint32_t l = 0;
+  while ((uint64_t{1} << l) < d) ++l;  // ceil(log2 d)
+  const uint64_t p = 31 + l;
+  *magic = static_cast<uint32_t>(((uint64_t{1} << p) + d - 1) / d);
+  *shift = static_cast<uint32_t>(p - 32);
+}
+
+Scratch::~Scratch() {
+  for (auto& c : chunks_) disc_cuda_free(c.base, stream_);
+}
+
+void* Scratch::alloc(int64_t bytes) {
+  bytes = (std::max<int64_t>(bytes, 16) + 255) / 256 * 256;
+  while (cur_ < chunks_.size() && used_ + bytes > chunks_[cur_].size) {
+    ++cur_;
+    used_ = 0;
+  }
+  if (cur_ == chunks_.size()) {
+    int64_t size = std::max<int64_t>(bytes, int64_t{64} << 20);
+    void* p = nullptr;
+    cuda_ok(disc_cuda_malloc(static_cast<size_t>(size), stream_, &p), "scratch allocation");
+    chunks_.push_back({static_cast<char*>(p), size});
+    used_ = 0;
+  }
+  void* p = chunks_[cur_].base + used_;
+  used_ += bytes;
+  return p;
+}
+
+void Scratch::reset() {
+  cur_ = 0;
+  used_ = 0;
+}
+
+std::vector<std::vector<int64_t>> simulate_tape(const KernelArtifact& art, const VersionArtifact& ver,
+                                                const std::vector<std::vector<int64_t>>& ext_dims,
+                                                const std::vector<int64_t>& regs) {
+  std::vector<std::vector<int64_t>> dims(art.tape.size());
+  auto arg = [&](const TapeRef& r) -> const std::vector<int64_t>& {
+    return r.kind == TapeRef::Kind::kExternal ? ext_dims.at(r.index) : dims.at(r.index);
+  };
+  for (size_t t = 0; t < art.tape.size(); ++t) {
+    const TapeInstr& ti = art.tape[t];
+    std::vector<int64_t> out = resolve_all(ti.out_dims, regs);
+    const int64_t n = numel(out);
+    switch (ti.kind) {
+      case DhloOpKind::kAdd: case DhloOpKind::kSub: case DhloOpKind::kMul: case DhloOpKind::kDiv:
+      case DhloOpKind::kMaximum: case DhloOpKind::kExp: case DhloOpKind::kTanh: case DhloOpKind::kNeg:
+        for (const auto& a : ti.args)
+          if (numel(arg(a)) != n) throw RuntimeError("fused elementwise operand size mismatch");
+        if (ver.vectorized4 && n % 4 != 0) throw InternalError("vectorized kernel launched with ragged extent");
+        dims[t] = out;
+        break;
+      case DhloOpKind::kReduceSum: case DhloOpKind::kReduceMax:
+        dims[t] = reduce_out_dims(arg(ti.args[0]), ti.dims);
+        break;
+      case DhloOpKind::kDynamicBroadcastInDim: {
+        const auto& in = arg(ti.args[0]);
+        if (ver.implicit_broadcast) {
+          for (size_t i = 0; i < ti.dims.size(); ++i)
+            if (in[i] != 1 && in[i] != out[ti.dims[i]]) throw RuntimeError("broadcast dim incompatible at runtime");
+        } else if (numel(in) != n) {
+          throw InternalError("no-broadcast version launched with non-identity shape");
+        }
+        dims[t] = out;
+        break;
+      }
+      case DhloOpKind::kDynamicSlice: {
+        const auto& in = arg(ti.args[0]);
+        auto starts = resolve_all(ti.slice_starts, regs), steps = resolve_all(ti.slice_strides, regs);
+        for (size_t i = 0; i < in.size(); ++i) {
+          if (steps[i] <= 0) throw RuntimeError("slice stride <= 0");
+          if (starts[i] < 0) throw RuntimeError("slice index out of range");
+          if (out[i] > 0 && starts[i] + (out[i] - 1) * steps[i] >= in[i]) throw RuntimeError("slice index out of range");
+        }
+        dims[t] = out;
+        break;
+      }
+      case DhloOpKind::kTranspose: {
+        const auto& in = arg(ti.args[0]);
+        for (int64_t p : ti.dims) dims[t].push_back(in[p]);
+        break;
+      }
+      case DhloOpKind::kDynamicReshape:
+        if (n != numel(arg(ti.args[0]))) throw RuntimeError("reshape element count mismatch at runtime");
+        dims[t] = out;
+        break;
+      case DhloOpKind::kDynamicPad: {
+        const auto& in = arg(ti.args[0]);
+        auto lo = resolve_all(ti.pad_low, regs), hi = resolve_all(ti.pad_high, regs),
+             it = resolve_all(ti.pad_interior, regs);
+        for (size_t i = 0; i < in.size(); ++i) {
+          if (lo[i] < 0 || hi[i] < 0 || it[i] < 0) throw RuntimeError("negative padding");
+          dims[t].push_back(lo[i] + hi[i] + in[i] + (in[i] > 0 ? (in[i] - 1) * it[i] : 0));
+        }
+        break;
+      }
+      case DhloOpKind::kConcat: {
+        if (ti.args.empty()) throw RuntimeError("concat with no operands");
+        std::vector<int64_t> d = arg(ti.args[0]);
+        int64_t along = 0;
+        for (const auto& a : ti.args) {
+          const auto& p = arg(a);
+          for (size_t i = 0; i < d.size(); ++i)
+            if (static_cast<int64_t>(i) != ti.axis && p[i] != d[i])
+              throw RuntimeError("concat non-axis dim mismatch at runtime");
+          along += p[ti.axis];
+        }
+        d[ti.axis] = along;
+        dims[t] = d;
+        break;
+      }
+      default:
+        throw InternalError("unexpected op in kernel tape");
+    }
+  }
+  return dims;
+}
+
+namespace {
+
+void check_capacity(const std::vector<int64_t>& d, const OutBuf& o) {
+  if (numel(d) * 4 > o.capacity_bytes) throw InternalError("kernel output exceeds planned buffer size");
+}
+
+int64_t algorithmic_bytes(const KernelArtifact& art, const std::vector<DevTensor>& ext,
+                          const std::vector<std::vector<int64_t>>& dims) {
+  int64_t bytes = 0;
+  for (size_t e = 0; e < ext.size(); ++e) {
+    int64_t whole = numel(ext[e].dims), sliced = 0;
+    bool only_slices = true;
+    for (size_t t = 0; t < art.tape.size(); ++t)
+      for (const auto& a : art.tape[t].args)
+        if (a.kind == TapeRef::Kind::kExternal && a.index == static_cast<int>(e)) {
+          if (art.tape[t].kind == DhloOpKind::kDynamicSlice) sliced += numel(dims[t]);
+          else only_slices = false;
+        }
+    bytes += 4 * (only_slices ? std::min(sliced, whole) : whole);
+  }
+  for (int o : art.output_tape_indices) bytes += 4 * numel(dims[o]);
+  return bytes;
+}
+
+// Issues the fused lowering; throws NotFusible when the tape needs materialisation.
+LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& scratch, void* stream,
+                          SchedulePref pref) {
+  const KernelArtifact& art = B.art;
+  const int n = static_cast<int>(art.tape.size());
+  LaunchReport rep;
+
+  // Members whose value is written to an output buffer (first listing wins).
+  auto out_ptr_of = [&](int t) -> std::vector<int> {
+    std::vector<int> idx;
+    for (size_t o = 0; o < art.output_tape_indices.size(); ++o)
+      if (art.output_tape_indices[o] == t) idx.push_back(static_cast<int>(o));
+    return idx;
+  };
+
+  if (B.red < 0) {
+    // kLoop: all members identity-aligned over N elements.
+    const int64_t N = numel(B.dims[art.output_tape_indices.at(0)]);
+    for (int t = 0; t < n; ++t)
+      if (numel(B.dims[t]) != N) throw NotFusible{"member size differs from the space"};
+    ProgramBuilder pb;
+    Lowering lw(B, pb, nullptr, nullptr);
+    for (size_t o = 0; o < art.output_tape_indices.size(); ++o) {
+      int t = art.output_tape_indices[o];
+      pb.output(lw.value(t), outs[o].ptr);
+    }
+    disc_loop_launch L;
+    std::memset(&L, 0, sizeof L);
+    L.prog = pb.finish(-1);
+    L.total = N;
+    L.wide = N > kWideLimit;
+    set_vec({&L.prog}, N, &L.vec);
+    if (N > 0) {
+      cuda_ok(disc_cuda_launch_loop(&L, stream), "fused loop");
+      rep.device_kernels = 1;
+    }
+    rep.schedule = L.vec == 4 ? "loop_v4" : "loop";
+    return rep;
+  }
+
+  // kInput: reduce-rooted.
+  const TapeInstr& rt = art.tape[B.red];
+  const TapeRef& rarg = rt.args[0];
+  const std::vector<int64_t>& adims = ref_dims(B, rarg);
+  const int64_t N = numel(adims);
+  for (int t = 0; t < n; ++t)
+    if (t != B.red && numel(B.dims[t]) != N) throw NotFusible{"member size differs from the space"};
+  Geometry geo = reduce_geometry(adims, rt.dims);
+  const int64_t nout = numel(B.dims[B.red]);
+
+  // Reduce result destination: its output buffer, else scratch when an epilogue needs it.
+  std::vector<int> red_outs = out_ptr_of(B.red);
+  bool has_post = false;
+  for (int o : art.output_tape_indices)
+    if (B.post[o]) has_post = true;
+  float* red_ptr = red_outs.empty() ? nullptr : outs[red_outs[0]].ptr;
+  if (!red_ptr && has_post) red_ptr = static_cast<float*>(scratch.alloc(nout * 4));
+
+  disc_reduce_launch R;
+  std::memset(&R, 0, sizeof R);
+  R.kind = rt.kind == DhloOpKind::kReduceSum ? DISC_REDUCE_SUM : DISC_REDUCE_MAX;
+  R.red_out = red_ptr;
+  R.wide = N > kWideLimit || nout > kWideLimit;
+
+  // Pre program: pre-member outputs, then the reduce argument (left in acc).
+  {
+    ProgramBuilder pb;
+    Lowering lw(B, pb, nullptr, nullptr);
+    for (size_t o = 0; o < art.output_tape_indices.size(); ++o) {
+      int t = art.output_tape_indices[o];
+      if (t == B.red || B.post[t]) continue;
+      pb.output(lw.value(t), outs[o].ptr);
+    }
+    int arg = lw.at_identity(rarg);
+    R.pre = pb.finish(arg);
+  }
+
+  // Geometry -> schedule.
+  R.K = geo.K;
+  R.R = geo.R;
+  R.C = geo.C;
+  R.schedule = geo.schedule;
+  const bool empty = geo.K == 0 || geo.R == 0 || N == 0;
+  if (empty) {
+    R.schedule = DISC_SCHED_ROW;  // identities for every (possibly) non-empty output
+    R.K = nout;
+    R.R = 0;
+    R.C = 1;
+  }
+
+  // Post program: fused into the row kernel when every reduce read is row-aligned.
+  Plan plan;
+  bool post_fused = false;
+  if (has_post) {
+    if (R.schedule == DISC_SCHED_ROW && !empty) {
+      Map row = canonical(Map{{R.K, R.R}, {1, 0}, 0});
+      try {
+        ProgramBuilder pb;
+        Lowering lw(B, pb, nullptr, &row);
+        for (size_t o = 0; o < art.output_tape_indices.size(); ++o) {
+          int t = art.output_tape_indices[o];
+          if (B.post[t]) pb.output(lw.value(t), outs[o].ptr);
+        }
+        R.post = pb.finish(-1);
+        post_fused = true;
+      } catch (const NotFusible&) {
+        std::memset(&R.post, 0, sizeof R.post);
+      }
+    }
+    if (!post_fused) {
+      if (!red_ptr) throw NotFusible{"no reduce buffer"};
+      ProgramBuilder pb;
+      Lowering lw(B, pb, red_ptr, nullptr);
+      int64_t Npost = -1;
+      for (size_t o = 0; o < art.output_tape_indices.size(); ++o) {
+        int t = art.output_tape_indices[o];
+        if (!B.post[t]) continue;
+        pb.output(lw.value(t), outs[o].ptr);
+        Npost = numel(B.dims[t]);
+      }
+      std::memset(&plan.post_pass, 0, sizeof plan.post_pass);
+      plan.post_pass.prog = pb.finish(-1);
+      plan.post_pass.total = Npost;
+      plan.post_pass.wide = Npost > kWideLimit;
+      set_vec({&plan.post_pass.prog}, Npost, &plan.post_pass.vec);
+      plan.has_post_pass = Npost > 0;
+    }
+  }
+
+  // Vector width along the contiguous dimension of the schedule.
+  if (empty) {
+    R.vec = 1;
+  } else if (R.schedule == DISC_SCHED_ROW) {
+    set_vec({&R.pre, &R.post}, R.R, &R.vec);
+  } else if (R.schedule == DISC_SCHED_GENERIC) {
+    R.vec = 1;
+    R.wide = 1;
+    R.g_rank = geo.rank;
+    R.g_mask = geo.mask;
+    for (int d = 0; d < geo.rank; ++d) R.g_dims[d] = geo.gdims[d];
+  } else {
+    set_vec({&R.pre}, R.C, &R.vec);
+  }
+
+  if (R.schedule == DISC_SCHED_ROW) {
+    const int64_t chunks = empty ? 0 : R.R / R.vec;
+    R.group = next_pow2((chunks + 3) / 4);
+    rep.schedule = post_fused ? "row_fused" : "row";
+  } else if (R.schedule != DISC_SCHED_GENERIC) {
+    if (!R.red_out) R.red_out = static_cast<float*>(scratch.alloc(nout * 4));
+    const int64_t tiles = (R.C / R.vec + 31) / 32;
+    const int64_t ctas = R.K * tiles;
+    const int64_t want = (int64_t{sm_count()} * 8 + ctas - 1) / ctas;
+    const int64_t max_split = std::max<int64_t>(1, R.R / 64);
+    int64_t splits = std::min(want, max_split);
+    if (pref == SchedulePref::kTwoPass || pref == SchedulePref::kAtomic) splits = std::max<int64_t>(splits, 2);
+    splits = std::min<int64_t>(std::max<int64_t>(splits, 1), 65535);
+    R.splits = static_cast<int32_t>(splits);
+    if (splits == 1) {
+      R.schedule = DISC_SCHED_COL_SINGLE;
+      rep.schedule = "col_single";
+    } else if (pref == SchedulePref::kAtomic && R.kind == DISC_REDUCE_SUM) {
+      R.schedule = DISC_SCHED_COL_ATOMIC;
+      R.workspace = static_cast<double*>(scratch.alloc(8 * nout));
+      rep.schedule = "col_atomic";
+    } else {
+      R.schedule = DISC_SCHED_COL_TWOPASS;
+      R.workspace = static_cast<double*>(scratch.alloc(8 * nout * splits));
+      rep.schedule = "col_twopass";
+    }
+  } else {
+    if (!R.red_out) R.red_out = static_cast<float*>(scratch.alloc(nout * 4));
+    rep.schedule = "generic";
+  }
+
+  cuda_ok(disc_cuda_launch_reduce(&R, stream), "fused reduce");
+  rep.device_kernels = (R.schedule == DISC_SCHED_COL_TWOPASS || R.schedule == DISC_SCHED_COL_ATOMIC) ? 2 : 1;
+  if (plan.has_post_pass) {
+    cuda_ok(disc_cuda_launch_loop(&plan.post_pass, stream), "epilogue pass");
+    rep.device_kernels += 1;
+    rep.schedule += "+post";
+  }
+  return rep;
+}
+
+// Single-instruction program helpers for materialisation and standalone artifacts.
+void run_copy(const float* src, const Map& m, float* dst, int64_t n, void* stream) {
+  if (n <= 0) return;
+  ProgramBuilder pb;
+  pb.output(pb.load(src, m), dst);
+  disc_loop_launch L;
+  std::memset(&L, 0, sizeof L);
+  L.prog = pb.finish(-1);
+  L.total = n;
+  L.wide = n > kWideLimit;
+  set_vec({&L.prog}, n, &L.vec);
+  cuda_ok(disc_cuda_launch_loop(&L, stream), "gather");
+}
+
+// Reference semantics member by member: every member is materialised in device
+// scratch at its own dims, exactly like run_kernel's scratch tensors.
+LaunchReport launch_materialized(Binding& B, const std::vector<OutBuf>& outs, Scratch& scratch, void* stream) {
+  const KernelArtifact& art = B.art;
+  const int n = static_cast<int>(art.tape.size());
+  LaunchReport rep;
+  rep.materialized = true;
+  rep.schedule = "materialized";
+  std::vector<float*> buf(n, nullptr);
+  auto tensor = [&](const TapeRef& r) -> DevTensor {
+    if (r.kind == TapeRef::Kind::kExternal) return B.ext[r.index];
+    return DevTensor{buf[r.index], B.dims[r.index]};
+  };
+  for (int t = 0; t < n; ++t) {
+    const TapeInstr& ti = art.tape[t];
+    const int64_t cnt = numel(B.dims[t]);
+    buf[t] = static_cast<float*>(scratch.alloc(cnt * 4));
+    if (is_elementwise_binary(ti.kind) || is_elementwise_unary(ti.kind)) {
+      if (cnt == 0) continue;
+      ProgramBuilder pb;
+      std::vector<int> vals;
+      for (const auto& a : ti.args) {
+        DevTensor x = tensor(a);
+        vals.push_back(pb.load(x.ptr, identity_map(numel(x.dims))));
+      }
+      int v = vals.size() == 2 ? pb.op(dhlo_to_op(ti.kind), vals[0], vals[1]) : pb.op(dhlo_to_op(ti.kind), vals[0]);
+      pb.output(v, buf[t]);
+      disc_loop_launch L;
+      std::memset(&L, 0, sizeof L);
+      L.prog = pb.finish(-1);
+      L.total = cnt;
+      L.wide = cnt > kWideLimit;
+      set_vec({&L.prog}, cnt, &L.vec);
+      cuda_ok(disc_cuda_launch_loop(&L, stream), "materialized elementwise");
+      rep.device_kernels++;
+    } else if (ti.kind == DhloOpKind::kDynamicBroadcastInDim || ti.kind == DhloOpKind::kDynamicSlice) {
+      DevTensor x = tensor(ti.args[0]);
+      if (cnt == 0) continue;
+      run_copy(x.ptr, arg_map(B, t, x.dims), buf[t], cnt, stream);
+      rep.device_kernels++;
+    } else if (is_reduce(ti.kind)) {
+      DevTensor x = tensor(ti.args[0]);
+      Geometry geo = reduce_geometry(x.dims, ti.dims);
+      disc_reduce_launch R;
+      std::memset(&R, 0, sizeof R);
+      ProgramBuilder pb;
+      int v = pb.load(x.ptr, identity_map(numel(x.dims)));
+      R.pre = pb.finish(v);
+      R.kind = ti.kind == DhloOpKind::kReduceSum ? DISC_REDUCE_SUM : DISC_REDUCE_MAX;
+      R.red_out = buf[t];
+      R.vec = 1;
+      R.wide = 1;
+      const bool empty = geo.K == 0 || geo.R == 0 || numel(x.dims) == 0;
+      if (empty || geo.schedule != DISC_SCHED_GENERIC) {
+        // Any contiguous pattern also runs correctly as the generic schedule.
+        R.schedule = empty ? DISC_SCHED_ROW : DISC_SCHED_GENERIC;
+        R.K = empty ? cnt : cnt;
+        R.R = empty ? 0 : numel(x.dims) / std::max<int64_t>(cnt, 1);
+        R.group = 1;
+        R.g_rank = static_cast<int>(x.dims.size());
+        if (R.g_rank > DISC_MAX_RANK) throw InternalError("rank too large");
+        for (int d = 0; d < R.g_rank; ++d) R.g_dims[d] = x.dims[d];
+        for (int64_t a : ti.dims) R.g_mask |= 1 << a;
+      } else {
+        R.schedule = DISC_SCHED_GENERIC;
+        R.K = geo.K;
+        R.R = geo.R;
+        R.g_rank = geo.rank;
+        R.g_mask = geo.mask;
+        for (int d = 0; d < geo.rank; ++d) R.g_dims[d] = geo.gdims[d];
+      }
+      if (cnt == 0) continue;
+      cuda_ok(disc_cuda_launch_reduce(&R, stream), "materialized reduce");
+      rep.device_kernels++;
+    } else {
+      throw InternalError("unexpected op in kernel tape");
+    }
+  }
+  for (size_t o = 0; o < art.output_tape_indices.size(); ++o) {
+    int t = art.output_tape_indices[o];
+    const int64_t bytes = numel(B.dims[t]) * 4;
+    if (bytes) cuda_ok(disc_cuda_memcpy(outs[o].ptr, buf[t], static_cast<size_t>(bytes), 2, stream), "output copy");
+  }
+  return rep;
+}
+
+LaunchReport launch_standalone(Binding& B, const std::vector<OutBuf>& outs, void* stream) {
+  const TapeInstr& ti = B.art.tape.at(0);
+  LaunchReport rep;
+  const auto& od = B.dims[0];
+  const int64_t cnt = numel(od);
+  float* dst = outs.at(0).ptr;
+  switch (ti.kind) {
+    case DhloOpKind::kTranspose: {
+      const DevTensor& x = B.ext.at(ti.args[0].index);
+      rep.schedule = "transpose";
+      if (cnt) {
+        run_copy(x.ptr, transpose_map(x.dims, ti.dims), dst, cnt, stream);
+        rep.device_kernels = 1;
+      }
+      return rep;
+    }
+    case DhloOpKind::kDynamicReshape: {
+      const DevTensor& x = B.ext.at(ti.args[0].index);
+      rep.schedule = "reshape";
+      if (cnt) {
+        cuda_ok(disc_cuda_memcpy(dst, x.ptr, static_cast<size_t>(cnt * 4), 2, stream), "reshape copy");
+        rep.device_kernels = 1;
+      }
+      return rep;
+    }
+    case DhloOpKind::kDynamicPad: {
+      const DevTensor& x = B.ext.at(ti.args[0].index);
+      disc_pad_launch P;
+      std::memset(&P, 0, sizeof P);
+      P.in = x.ptr;
+      P.out = dst;
+      P.rank = static_cast<int32_t>(x.dims.size());
+      if (P.rank > DISC_MAX_RANK) throw InternalError("pad rank exceeds DISC_MAX_RANK");
+      P.value = ti.pad_value;
+      P.total = cnt;
+      auto lo = resolve_all(ti.pad_low, B.regs), it = resolve_all(ti.pad_interior, B.regs);
+      for (int d = 0; d < P.rank; ++d) {
+        P.out_dims[d] = od[d];
+        P.in_dims[d] = x.dims[d];
+        P.low[d] = lo[d];
+        P.step[d] = 1 + it[d];
+      }
+      rep.schedule = "pad";
+      if (cnt) {
+        cuda_ok(disc_cuda_launch_pad(&P, stream), "pad");
+        rep.device_kernels = 1;
+      }
+      return rep;
+    }
+    case DhloOpKind::kConcat: {
+      const int ax = static_cast<int>(ti.axis);
+      int64_t outer = 1, inner = 1;
+      for (int d = 0; d < ax; ++d) outer *= od[d];
+      for (size_t d = ax + 1; d < od.size(); ++d) inner *= od[d];
+      rep.schedule = "concat";
+      int64_t offset = 0;
+      for (size_t p0 = 0; p0 < ti.args.size(); p0 += DISC_MAX_CONCAT) {
+        disc_concat_launch C;
+        std::memset(&C, 0, sizeof C);
+        C.out = dst;
+        C.outer = outer;
+        C.inner = inner;
+        C.axis_total = od[ax];
+        C.axis_offset = offset;
+        for (size_t p = p0; p < ti.args.size() && p < p0 + DISC_MAX_CONCAT; ++p) {
+          const DevTensor x = ti.args[p].kind == TapeRef::Kind::kExternal ? B.ext.at(ti.args[p].index) : DevTensor{};
+          C.parts[C.n_parts] = x.ptr;
+          C.part_axis[C.n_parts] = x.dims[ax];
+          offset += x.dims[ax];
+          C.n_parts++;
+        }
+        if (cnt) {
+          cuda_ok(disc_cuda_launch_concat(&C, stream), "concat");
+          rep.device_kernels++;
+        }
+      }
+      return rep;
+    }
+    default:
+      throw InternalError("unexpected standalone kernel kind");
+  }
+}
+
+}  // namespace
+
+LaunchReport launch_kernel(const KernelArtifact& art, const VersionArtifact& ver, const std::vector<DevTensor>& ext,
+                           const std::vector<int64_t>& regs, const std::vector<OutBuf>& outs, Scratch& scratch,
+                           void* stream, SchedulePref pref) {
+  std::vector<std::vector<int64_t>> ext_dims;
+  for (const auto& e : ext) ext_dims.push_back(e.dims);
+  Binding B{art, ver, ext, regs, simulate_tape(art, ver, ext_dims, regs), -1, {}};
+  for (size_t o = 0; o < art.output_tape_indices.size(); ++o)
+    check_capacity(B.dims.at(art.output_tape_indices[o]), outs.at(o));
+
+  LaunchReport rep;
+  if (art.standalone) {
+    rep = launch_standalone(B, outs, stream);
+  } else {
+    const int n = static_cast<int>(art.tape.size());
+    for (int t = 0; t < n; ++t)
+      if (is_reduce(art.tape[t].kind)) B.red = t;
+    B.post.assign(n, 0);
+    if (B.red >= 0)
+      for (int t = B.red + 1; t < n; ++t)
+        for (const auto& a : art.tape[t].args)
+          if (a.kind == TapeRef::Kind::kMember && (a.index == B.red || B.post[a.index])) B.post[t] = 1;
+    bool done = false;
+    if (pref != SchedulePref::kMaterialize) {
+      try {
+        rep = launch_fused(B, outs, scratch, stream, pref);
+        done = true;
+      } catch (const NotFusible& nf) {
+        if (pref == SchedulePref::kFusedOnly) throw InternalError(std::string("not fusible: ") + nf.why);
+      }
+    }
+    if (!done) rep = launch_materialized(B, outs, scratch, stream);
+  }
+  rep.algorithmic_bytes = algorithmic_bytes(art, ext, B.dims);
+  return rep;
+}
+
+void launch_gemm(int64_t m, int64_t k, int64_t n, const DevTensor& a, const DevTensor& b, const OutBuf& c,
+                 void* stream) {
+  if (a.dims.size() != 2 || b.dims.size() != 2) throw RuntimeError("matmul operands must be rank-2");
+  if (a.dims[1] != b.dims[0]) throw RuntimeError("matmul inner dim mismatch at runtime");
+  if (m * n * 4 > c.capacity_bytes) throw InternalError("kernel output exceeds planned buffer size");
+  if (m == 0 || n == 0) return;
+  if (k == 0) {
+    cuda_ok(disc_cuda_memset(c.ptr, 0, static_cast<size_t>(m * n * 4), stream), "gemm zero");
+    return;
+  }
+  cuda_ok(disc_cuda_gemm(m, k, n, a.ptr, b.ptr, c.ptr, stream), "gemm");
+}
+
+}  // namespace disc::rt

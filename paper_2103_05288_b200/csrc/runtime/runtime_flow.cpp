@@ -1,0 +1,349 @@
+// Device runtime flow (see runtime_flow.hpp).
+#include "runtime_flow.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <set>
+
+#include "disc_cuda.h"
+#include "shape_eval.hpp"
+
+namespace disc::rt {
+
+namespace {
+
+void cuda_ok(int rc, const char* what) {
+  if (rc != 0) throw RuntimeError(std::string(what) + ": " + disc_cuda_last_error());
+}
+
+int64_t numel(const std::vector<int64_t>& d) {
+  int64_t n = 1;
+  for (int64_t x : d) n *= x;
+  return n;
+}
+
+using Clock = std::chrono::steady_clock;
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+
+DeviceCachingAllocator::~DeviceCachingAllocator() {
+  for (auto& b : blocks_)
+    if (b.ptr) disc_cuda_free(b.ptr, stream_);
+}
+
+int DeviceCachingAllocator::alloc(int64_t bytes, ExecStats& stats) {
+  auto it = free_.find(bytes);
+  if (it != free_.end() && !it->second.empty()) {
+    int id = it->second.back();
+    it->second.pop_back();
+    cached_ -= bytes;
+    stats.allocator_cache_hits++;
+    return id;
+  }
+  stats.alloc_calls++;
+  void* p = nullptr;
+  // 16-byte granularity like the reference; the pool returns 256-byte aligned blocks.
+  int64_t cap = (std::max<int64_t>(bytes, 1) + 15) / 16 * 16;
+  cuda_ok(disc_cuda_malloc(static_cast<size_t>(cap), stream_, &p), "device allocation");
+  blocks_.push_back({static_cast<float*>(p), bytes});
+  return static_cast<int>(blocks_.size()) - 1;
+}
+
+void DeviceCachingAllocator::free(int block) {
+  free_[blocks_[block].bytes].push_back(block);
+  cached_ += blocks_[block].bytes;
+  if (budget_ > 0 && cached_ > budget_) trim();
+}
+
+void DeviceCachingAllocator::trim() {
+  // Release cached free blocks (largest sizes first) until under budget.  Released ids
+  // are retired, so hit/miss accounting stays exact-size.
+  for (auto it = free_.rbegin(); it != free_.rend() && cached_ > budget_ / 2; ++it) {
+    for (int id : it->second) {
+      disc_cuda_free(blocks_[id].ptr, stream_);
+      blocks_[id].ptr = nullptr;
+      cached_ -= blocks_[id].bytes;
+    }
+    it->second.clear();
+  }
+}
+
+// ---------------------------------------------------------------------------
+
+DeviceExecutor::DeviceExecutor(int device, void* stream)
+    : device_(device), stream_(stream), alloc_(stream), scratch_(stream) {
+  cuda_ok(disc_cuda_set_device(device), "set device");
+  cuda_ok(disc_cuda_event_create(&ev_[0]), "event");
+  cuda_ok(disc_cuda_event_create(&ev_[1]), "event");
+}
+
+DeviceExecutor::~DeviceExecutor() {
+  disc_cuda_stream_synchronize(stream_);
+  for (float* p : passthrough_)
+    if (p) disc_cuda_free(p, stream_);
+  for (auto& s : staging_)
+    if (s.first) disc_cuda_free(s.first, stream_);
+  for (void* e : ev_)
+    if (e) disc_cuda_event_destroy(e);
+}
+
+void DeviceExecutor::set_stream(void* s) {
+  stream_ = s;
+  alloc_.set_stream(s);
+  scratch_.set_stream(s);
+}
+
+const float* DeviceExecutor::stage_input(int slot, const void* host, int64_t bytes) {
+  if (static_cast<int>(staging_.size()) <= slot) staging_.resize(slot + 1, {nullptr, 0});
+  auto& s = staging_[slot];
+  if (s.second < bytes) {
+    if (s.first) disc_cuda_free(s.first, stream_);
+    s.first = nullptr;
+    cuda_ok(disc_cuda_malloc(static_cast<size_t>(std::max<int64_t>(bytes, 16)), stream_, &s.first), "input staging");
+    s.second = bytes;
+  }
+  if (bytes) cuda_ok(disc_cuda_memcpy(s.first, host, static_cast<size_t>(bytes), 0, stream_), "input H2D");
+  return static_cast<const float*>(s.first);
+}
+
+void DeviceExecutor::run_kernel(const KernelArtifact& art, const VersionArtifact& ver, const std::vector<DevTensor>& ext,
+                                const std::vector<int64_t>& regs) {
+  std::vector<std::vector<int64_t>> ed;
+  for (const auto& e : ext) ed.push_back(e.dims);
+  auto dims = simulate_tape(art, ver, ed, regs);
+  std::vector<OutBuf> outs;
+  outputs_.clear();
+  scratch_.reset();
+  for (int t : art.output_tape_indices) {
+    int64_t bytes = numel(dims[t]) * 4;
+    float* p = static_cast<float*>(scratch_.alloc(bytes));
+    outs.push_back({p, bytes});
+    outputs_.push_back({p, dims[t]});
+  }
+  LaunchReport rep = launch_kernel(art, ver, ext, regs, outs, scratch_, stream_, pref_);
+  device_launches_ = rep.device_kernels;
+  schedules_ = {rep.schedule};
+}
+
+void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBinding>& inputs) {
+  ExecStats stats;
+  stats.host_instruction_count = plan.host_instruction_count();
+  const auto t_run = Clock::now();
+  double kernel_ms = 0.0;
+  device_launches_ = 0;
+  algorithmic_bytes_ = 0;
+  schedules_.clear();
+  scratch_.reset();
+
+  std::vector<int64_t> regs(plan.shape_program.num_regs, 0);
+  struct Slot {
+    const InputBinding* input = nullptr;
+    int block = -1;
+    int64_t bytes = 0;
+  };
+  std::vector<Slot> slots(plan.num_buffers);
+  std::map<int, int> version_of;
+  int64_t live = 0;
+  std::map<int, BufferEvent> events;
+  std::vector<const std::vector<int64_t>*> input_dims(plan.inputs.size(), nullptr);
+
+  auto input_asserts = [&] {
+    for (size_t i = 0; i < plan.inputs.size(); ++i) {
+      const auto& pi = plan.inputs[i];
+      const auto& d = slots[i].input->dims;
+      for (size_t k = 0; k < pi.dims.size(); ++k) {
+        int64_t want = resolve(pi.dims[k], regs);
+        if (d[k] != want)
+          throw RuntimeError("input " + pi.id + " dim " + std::to_string(k) + " violates a shape constraint: expected " +
+                             std::to_string(want) + ", got " + std::to_string(d[k]));
+      }
+    }
+  };
+
+  auto view = [&](int buf, const std::vector<int64_t>& dims) -> DevTensor {
+    const Slot& s = slots[buf];
+    if (s.input) {
+      if (numel(dims) > numel(s.input->dims))
+        throw RuntimeError("input " + s.input->name + " is smaller than its planned extent");
+      return {s.input->ptr, dims};
+    }
+    if (numel(dims) * 4 > s.bytes) throw InternalError("read exceeds planned buffer size");
+    return {alloc_.data(s.block), dims};
+  };
+  auto out_buf = [&](int buf) -> OutBuf {
+    const Slot& s = slots[buf];
+    if (s.input) throw InternalError("write into an input buffer");
+    return {alloc_.data(s.block), s.bytes};
+  };
+
+  bool shapes_ready = plan.shape_program.empty();
+  outputs_.assign(plan.outputs.size(), {});
+
+  for (size_t pc = 0; pc < plan.instrs.size(); ++pc) {
+    const Instr& in = plan.instrs[pc];
+    switch (in.kind) {
+      case InstrKind::kBindInput: {
+        const auto& pi = plan.inputs[in.a];
+        const InputBinding* b = nullptr;
+        for (const auto& x : inputs)
+          if (x.name == pi.id) b = &x;
+        if (!b) throw RuntimeError("missing input " + pi.id);
+        if (b->dims.size() != pi.dims.size()) throw RuntimeError("input " + pi.id + " rank mismatch");
+        slots[in.b].input = b;
+        input_dims[in.a] = &b->dims;
+        break;
+      }
+      case InstrKind::kEvalShape:
+        for (size_t i = 0; i < input_dims.size(); ++i)
+          if (!input_dims[i]) throw InternalError("shape evaluation before inputs are bound");
+        eval_shape_range(plan, in.a, in.b, input_dims, regs);
+        shapes_ready = true;
+        input_asserts();
+        break;
+      case InstrKind::kAlloc: {
+        int64_t elems = in.size.const_elems;
+        for (int r : in.size.regs) elems *= regs[r];
+        const int64_t bytes = elems * 4;
+        Slot& s = slots[in.b];
+        s.block = alloc_.alloc(bytes, stats);
+        s.bytes = bytes;
+        live += bytes;
+        stats.peak_bytes = std::max(stats.peak_bytes, live);
+        events[in.b] = {in.b, s.block, static_cast<int>(pc), -1};
+        break;
+      }
+      case InstrKind::kDealloc: {
+        Slot& s = slots[in.b];
+        if (!in.reserve) {  // reserved blocks pass straight to a later alias
+          alloc_.free(s.block);
+          live -= s.bytes;
+        }
+        events[in.b].dealloc_instr = static_cast<int>(pc);
+        break;
+      }
+      case InstrKind::kAlias: {
+        Slot& s = slots[in.b];
+        s.block = slots[in.a].block;
+        s.bytes = slots[in.a].bytes;
+        stats.aliased_allocs++;
+        events[in.b] = {in.b, s.block, static_cast<int>(pc), -1};
+        break;
+      }
+      case InstrKind::kSelectVersion: {
+        const KernelArtifact& art = plan.kernels[in.a];
+        int chosen = -1;
+        for (const auto& v : art.versions) {
+          bool pass = true;
+          for (const auto& g : v.guards) {
+            if (g.kind == GuardTest::Kind::kNever) pass = false;
+            else if (g.kind == GuardTest::Kind::kRefEqual) pass = pass && resolve(g.a, regs) == resolve(g.b, regs);
+            else if (g.kind == GuardTest::Kind::kTotalDivisibleBy4) {
+              int64_t total = 1;
+              for (const auto& d : art.space_dims) total *= resolve(d, regs);
+              pass = pass && total % 4 == 0;
+            }
+            if (!pass) break;
+          }
+          if (pass) {
+            chosen = v.id;
+            break;
+          }
+        }
+        if (chosen < 0) throw RuntimeError("no kernel version guard matched");
+        version_of[in.a] = chosen;
+        break;
+      }
+      case InstrKind::kComputeLaunch:
+        break;  // the reference tile rule (256/1024) is superseded by the schedule selector
+      case InstrKind::kLaunch: {
+        if (!shapes_ready && !plan.shape_program.empty()) throw InternalError("launch before shape evaluation");
+        const KernelArtifact& art = plan.kernels[in.a];
+        const int vid = in.fixed_version >= 0 ? in.fixed_version : version_of.at(in.a);
+        const VersionArtifact* ver = nullptr;
+        for (const auto& v : art.versions)
+          if (v.id == vid) ver = &v;
+        if (!ver) throw InternalError("unknown kernel version selected");
+        std::vector<DevTensor> ext;
+        for (size_t a = 0; a < in.arg_bufs.size(); ++a)
+          ext.push_back(view(in.arg_bufs[a], resolve_all(art.external_input_dims[a], regs)));
+        std::vector<OutBuf> outs;
+        for (int b : in.out_bufs) outs.push_back(out_buf(b));
+        if (timing_) cuda_ok(disc_cuda_event_record(ev_[0], stream_), "event");
+        LaunchReport rep = launch_kernel(art, *ver, ext, regs, outs, scratch_, stream_, pref_);
+        if (timing_) {
+          cuda_ok(disc_cuda_event_record(ev_[1], stream_), "event");
+          cuda_ok(disc_cuda_event_synchronize(ev_[1]), "event sync");
+          float ms = 0;
+          cuda_ok(disc_cuda_event_elapsed_ms(ev_[0], ev_[1], &ms), "event elapsed");
+          kernel_ms += ms;
+        }
+        stats.launch_count++;
+        device_launches_ += rep.device_kernels;
+        algorithmic_bytes_ += rep.algorithmic_bytes;
+        schedules_.push_back(rep.schedule);
+        break;
+      }
+      case InstrKind::kLibraryCall: {
+        const int64_t m = resolve(in.lib_dims[0], regs), k = resolve(in.lib_dims[1], regs),
+                      n = resolve(in.lib_dims[2], regs);
+        DevTensor a = view(in.arg_bufs[0], {m, k}), b = view(in.arg_bufs[1], {k, n});
+        if (timing_) cuda_ok(disc_cuda_event_record(ev_[0], stream_), "event");
+        launch_gemm(m, k, n, a, b, out_buf(in.out_bufs[0]), stream_);
+        if (timing_) {
+          cuda_ok(disc_cuda_event_record(ev_[1], stream_), "event");
+          cuda_ok(disc_cuda_event_synchronize(ev_[1]), "event sync");
+          float ms = 0;
+          cuda_ok(disc_cuda_event_elapsed_ms(ev_[0], ev_[1], &ms), "event elapsed");
+          kernel_ms += ms;
+        }
+        stats.library_calls++;
+        device_launches_ += (m && n) ? 1 : 0;
+        schedules_.push_back("gemm");
+        break;
+      }
+      case InstrKind::kBindOutput: {
+        const auto& po = plan.outputs[in.a];
+        std::vector<int64_t> dims = resolve_all(po.dims, regs);
+        DevTensor t = view(in.b, dims);
+        if (slots[in.b].input) {
+          // Pass-through of a caller input: copy so the output outlives the binding.
+          if (passthrough_.size() <= static_cast<size_t>(in.a)) {
+            passthrough_.resize(in.a + 1, nullptr);
+            passthrough_bytes_.resize(in.a + 1, 0);
+          }
+          const int64_t bytes = numel(dims) * 4;
+          float*& p = passthrough_[in.a];
+          if (passthrough_bytes_[in.a] < bytes) {
+            if (p) disc_cuda_free(p, stream_);
+            void* q = nullptr;
+            cuda_ok(disc_cuda_malloc(static_cast<size_t>(std::max<int64_t>(bytes, 16)), stream_, &q), "output copy");
+            p = static_cast<float*>(q);
+            passthrough_bytes_[in.a] = bytes;
+          }
+          if (bytes) cuda_ok(disc_cuda_memcpy(p, t.ptr, static_cast<size_t>(bytes), 2, stream_), "output copy");
+          outputs_[in.a] = {p, dims};
+        } else {
+          outputs_[in.a] = {t.ptr, dims};
+        }
+        break;
+      }
+    }
+  }
+  if (plan.shape_program.empty()) input_asserts();
+
+  // Every block still held returns to the cache for the next run (outputs stay readable
+  // until then: the next run's work is ordered after them on the stream).
+  std::set<int> returned;
+  for (const auto& [logical, ev] : events)
+    if (ev.dealloc_instr < 0 && returned.insert(ev.physical).second) alloc_.free(ev.physical);
+
+  stats.kernel_ms = kernel_ms;
+  stats.host_ms = std::chrono::duration<double, std::milli>(Clock::now() - t_run).count() - kernel_ms;
+  stats_ = stats;
+  events_.clear();
+  for (const auto& [_, ev] : events) events_.push_back(ev);
+}
+
+}  // namespace disc::rt

@@ -1,0 +1,116 @@
+// The runtime flow on the device: executes a CompiledPlan's host instruction list with
+// stream launches and a stream-ordered device caching allocator.  Instruction semantics,
+// ExecStats and BufferEvents follow the reference Executor::run (executor.cpp:221-465).
+#pragma once
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../host/compiler.hpp"
+#include "launcher.hpp"
+
+namespace disc::rt {
+
+struct ExecStats {
+  int64_t launch_count = 0;
+  int64_t library_calls = 0;
+  int64_t host_instruction_count = 0;
+  int64_t peak_bytes = 0;
+  int64_t alloc_calls = 0;
+  int64_t allocator_cache_hits = 0;
+  int64_t aliased_allocs = 0;
+  double host_ms = 0.0;
+  double kernel_ms = 0.0;
+};
+
+struct BufferEvent {
+  int logical = -1, physical = -1, alloc_instr = -1, dealloc_instr = -1;
+};
+
+// Exact-byte-size free-list allocator over device memory (reference CachedAllocator,
+// executor.cpp:53-76, same hit/miss accounting).  Raw memory comes from the stream-
+// ordered pool; an optional byte budget trims cached free blocks (never hit by parity
+// workloads, bounds memory across >=10k distinct shapes).
+class DeviceCachingAllocator {
+ public:
+  explicit DeviceCachingAllocator(void* stream) : stream_(stream) {}
+  ~DeviceCachingAllocator();
+  int alloc(int64_t bytes, ExecStats& stats);
+  void free(int block);
+  float* data(int block) const { return blocks_[block].ptr; }
+  int64_t bytes(int block) const { return blocks_[block].bytes; }
+  void set_stream(void* s) { stream_ = s; }
+  void set_budget(int64_t b) { budget_ = b; }
+  void trim();
+  int64_t cached_bytes() const { return cached_; }
+
+ private:
+  struct Block {
+    float* ptr = nullptr;
+    int64_t bytes = 0;
+  };
+  void* stream_;
+  std::vector<Block> blocks_;
+  std::map<int64_t, std::vector<int>> free_;
+  int64_t cached_ = 0;
+  int64_t budget_ = 0;
+};
+
+struct OutputView {
+  const float* ptr = nullptr;
+  std::vector<int64_t> dims;
+};
+
+struct InputBinding {
+  std::string name;
+  const float* ptr = nullptr;  // device pointer
+  std::vector<int64_t> dims;
+};
+
+class DeviceExecutor {
+ public:
+  DeviceExecutor(int device, void* stream);
+  ~DeviceExecutor();
+  void set_stream(void* s);
+  void* stream() const { return stream_; }
+  // Runs the plan; outputs remain valid until the next run.
+  void run(const CompiledPlan& plan, const std::vector<InputBinding>& inputs);
+  const std::vector<OutputView>& outputs() const { return outputs_; }
+  const ExecStats& stats() const { return stats_; }
+  const std::vector<BufferEvent>& events() const { return events_; }
+  int64_t device_launches() const { return device_launches_; }
+  int64_t algorithmic_bytes() const { return algorithmic_bytes_; }
+  const std::vector<std::string>& schedules() const { return schedules_; }
+  void set_timing(bool on) { timing_ = on; }
+  void set_schedule(SchedulePref p) { pref_ = p; }
+  void set_cache_budget(int64_t b) { alloc_.set_budget(b); }
+  // Host-staging helper: device copy of host data owned by the executor (not counted in
+  // plan allocator stats).
+  const float* stage_input(int slot, const void* host, int64_t bytes);
+  // run_kernel equivalent on device externals.
+  void run_kernel(const KernelArtifact& art, const VersionArtifact& ver, const std::vector<DevTensor>& ext,
+                  const std::vector<int64_t>& regs);
+  Scratch& scratch() { return scratch_; }
+
+ private:
+  int device_;
+  void* stream_;
+  DeviceCachingAllocator alloc_;
+  Scratch scratch_;
+  std::vector<OutputView> outputs_;
+  std::vector<float*> passthrough_;  // owned copies for input pass-through outputs
+  std::vector<int64_t> passthrough_bytes_;
+  std::vector<std::pair<void*, int64_t>> staging_;
+  ExecStats stats_;
+  std::vector<BufferEvent> events_;
+  int64_t device_launches_ = 0;
+  int64_t algorithmic_bytes_ = 0;
+  std::vector<std::string> schedules_;
+  bool timing_ = false;
+  SchedulePref pref_ = SchedulePref::kAuto;
+  void* ev_[2] = {nullptr, nullptr};
+};
+
+}  // namespace disc::rt
