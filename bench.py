@@ -1,0 +1,510 @@
+#!/usr/bin/env python
+"""disc-b200 benchmark: fused-kernel HBM GB/s across a dynamic-shape sweep, 0 recompiles.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload ln_gelu|softmax|colreduce|bert|stream]
+  python bench.py --impl reference ...     # the reference's own CPU executor, same metric
+
+Workload (BASELINE.json configs[1]): one plan of the LN-like + bias +
+tanh-GELU graph compiled ONCE and run over 192 distinct runtime shapes [T, H] (T
+log-uniform 1..16384, 64 samples x H in {768, 1024, 4096}).  A step = one pass over the
+sweep.  Bytes are the algorithmic boundary bytes of every fused launch (SURVEY §8d:
+4 x (external inputs read + external outputs written), broadcast sources at source size).
+
+  value    = bytes / device time of the K timed steps (CUDA events on the executor's
+             stream, inputs resident in HBM, L2 flushed before each step)
+  e2e      = same bytes / wall time through the public C ABI with host inputs: H2D of
+             every request's inputs from pinned memory and D2H of its outputs inside
+             the timed region
+  roofline = the dominant kernel (largest share of device time): its bytes / its mean
+             CUDA-event launch duration, against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline = the reference executor (oracle/_ref, built from /root/reference) on a
+             bounded sample of the same sweep, 1 host thread
+
+Multi-GPU (torchrun, one process per GPU): every rank runs the same request sweep on its
+own GPU (independent requests, no collective on the data path; weak scaling); the
+timed region is bracketed by barriers and the max over ranks is reported.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused-kernel HBM GB/s (% of peak) across dynamic-shape sweep; 0 recompiles"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# Workloads
+
+def workload(name):
+    from paper_2103_05288_b200 import workloads as W
+    if name == "ln_gelu":
+        return "C2 LN-like+bias+tanh-GELU [T,H], T log-uniform 1..16384 x H {768,1024,4096}", \
+            W.ln_gelu_graph(), W.ln_shapes()
+    if name == "softmax":
+        g = W.softmax_graph_for(0)
+        shapes = [{"S0": s["S0"], "S1": s["_S"]} for s in W.softmax_shapes()]
+        return "C1 softmax [B,S], S 1..4096, B = 2^26/S", g, shapes
+    if name == "colreduce":
+        return "C3 column reduce with prologue [N,C]", W.colreduce_graph(), W.colreduce_shapes()
+    if name == "bert":
+        return "C4 BERT-base non-GEMM subgraphs, S 8..512, B {1,8,32}", W.bert_graph(), W.bert_shapes()
+    raise SystemExit(f"unknown workload {name}")
+
+
+def const_value(name, syms):
+    from paper_2103_05288_b200 import workloads as W
+    if name == "inv_h":
+        return 1.0 / syms.get("H", 1)
+    return W.CONST_INPUTS.get(name)
+
+
+class Requests:
+    """Device-resident inputs for every request of the sweep, bound once."""
+
+    def __init__(self, D, graph, shapes, seed=0):
+        self.D = D
+        self.names = [i["id"] for i in graph["inputs"]]
+        self.bufs, self.dims = [], []
+        self.input_bytes = 0
+        for r, syms in enumerate(shapes):
+            row_b, row_d = [], []
+            for i in graph["inputs"]:
+                shape = tuple(syms[d] if isinstance(d, str) else d for d in i["shape"])
+                b = D.DeviceBuffer(shape)
+                cv = const_value(i["id"], syms)
+                if cv is not None:
+                    b = D.DeviceBuffer.from_numpy(np.full(shape, cv, np.float32))
+                else:
+                    b.fill_uniform(seed * 1000003 + r * 97 + len(row_b))
+                row_b.append(b)
+                row_d.append(np.array(shape, dtype=np.int64))
+                self.input_bytes += b.nbytes
+            self.bufs.append(row_b)
+            self.dims.append(row_d)
+        n, k = len(shapes), len(self.names)
+        self.n = n
+        self.c_names = (C.c_char_p * k)(*[s.encode() for s in self.names])
+        self.c_data = (C.c_void_p * (n * k))(*[b.ptr.value for row in self.bufs for b in row])
+        self.c_dims = (C.c_void_p * (n * k))(*[d.ctypes.data for row in self.dims for d in row])
+        self.c_ranks = (C.c_int * (n * k))(*[d.size for row in self.dims for d in row])
+
+    def run(self, ex, plan):
+        rc = self.D.lib().disc_executor_run_batch(ex._h, plan._h, self.n, len(self.names), self.c_names,
+                                                   self.c_data, self.c_dims, self.c_ranks, 0)
+        self.D.api._check(rc)
+
+
+# ---------------------------------------------------------------------------
+# Clocks during the timed region (B200_PROFILING.md clocks line)
+
+class ClockSampler:
+    def __init__(self, device):
+        self.samples = []
+        self.proc = None
+        self.device = device
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(schedule):
+    """dram bytes per launch for the dominant kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        j = json.load(open(p))
+        return j.get("traffic_per_launch", {}).get(schedule)
+    except Exception:
+        return None
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local, dist
+
+
+def barrier(dist, local):
+    if dist is not None:
+        import torch
+        t = torch.zeros(1, device=f"cuda:{local}")
+        dist.all_reduce(t)
+        torch.cuda.synchronize()
+
+
+def allreduce_max(dist, local, v):
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_baseline(graph, shapes, budget_s=12.0):
+    """Reference executor (oracle/_ref) on a bounded sample of the sweep, 1 thread."""
+    from oracle import ref
+    if not ref.available():
+        return None
+    # sample: mid-sized shapes first, accumulate until the time budget is used
+    plan_json = json.dumps(graph)
+    rp = ref.RefPlan(ref.compile(plan_json))
+    ordered = sorted(shapes, key=lambda s: np.prod([v for k, v in s.items() if not k.startswith("_")]))
+    sample = ordered[len(ordered) // 3: len(ordered) // 3 + 12]
+    rng = np.random.default_rng(0)
+    total_bytes, total_s, used = 0, 0.0, []
+    for syms in sample:
+        inputs = {}
+        for i in graph["inputs"]:
+            shape = tuple(syms[d] if isinstance(d, str) else d for d in i["shape"])
+            cv = const_value(i["id"], syms)
+            inputs[i["id"]] = np.full(shape, cv, np.float32) if cv is not None else \
+                rng.uniform(0.25, 2.0, size=shape).astype(np.float32)
+        rp.run(inputs)  # warm the reference allocator cache
+        reps = 1
+        secs = rp.time(inputs, reps)
+        nbytes = algorithmic_bytes_ref(rp, inputs)
+        total_bytes += nbytes * reps
+        total_s += secs
+        used.append({k: v for k, v in syms.items() if not k.startswith("_")})
+        if total_s > budget_s:
+            break
+    return {"value": total_bytes / total_s / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference",
+            "sample": f"{len(used)} shapes of the same sweep (e.g. {used[0]}..{used[-1]}), reference "
+                      f"Executor::run, 1 thread, {total_s:.1f}s"}
+
+
+def algorithmic_bytes_ref(rp, inputs):
+    """Same byte formula on the reference plan: boundary bytes of every kLaunch."""
+    import paper_2103_05288_b200 as D
+    # The formula depends only on shapes: evaluate it with the product's host shape
+    # program on the (identical) plan -- no device work.
+    plan = D.CompiledPlan.from_json(json.dumps(rp.json))
+    regs = plan.eval_shapes([inputs[i].shape for i in rp.input_ids])
+    from oracle import disc_oracle as O
+    pj = rp.json
+    total = 0
+    for ins in pj["instrs"]:
+        if ins["k"] != "launch":
+            continue
+        art = pj["kernels"][ins["kernel"]]
+        for e, dims in enumerate(art["external_input_dims"]):
+            total += 4 * int(np.prod(O.resolve_dims(dims, regs)))
+        for t in art["outputs"]:
+            total += 4 * int(np.prod(O.resolve_dims(art["tape"][t]["out_dims"], regs)))
+    return total
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's CPU executor, all host threads, same metric."""
+    if world > 1 and rank != 0:
+        return
+    from oracle import ref
+    wname, graph, shapes = workload(args.workload)
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    from concurrent.futures import ThreadPoolExecutor
+    nthreads = os.cpu_count() or 1
+    plan_json = ref.compile(json.dumps(graph))
+    ordered = sorted(shapes, key=lambda s: np.prod([v for k, v in s.items() if not k.startswith("_")]))
+    sample = ordered[len(ordered) // 3: len(ordered) // 3 + max(nthreads, 8)]
+    rng = np.random.default_rng(0)
+    reqs = []
+    for syms in sample:
+        inputs = {}
+        for i in graph["inputs"]:
+            shape = tuple(syms[d] if isinstance(d, str) else d for d in i["shape"])
+            cv = const_value(i["id"], syms)
+            inputs[i["id"]] = np.full(shape, cv, np.float32) if cv is not None else \
+                rng.uniform(0.25, 2.0, size=shape).astype(np.float32)
+        reqs.append(inputs)
+    plans = [ref.RefPlan(plan_json) for _ in range(nthreads)]
+    nbytes = sum(algorithmic_bytes_ref(plans[0], r) for r in reqs)
+
+    def step():
+        def work(t):
+            s = 0.0
+            for i in range(t, len(reqs), nthreads):
+                s += plans[t].time(reqs[i], 1)
+            return s
+        with ThreadPoolExecutor(nthreads) as pool:
+            list(pool.map(work, range(nthreads)))
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    v = nbytes * args.steps / dt / 1e9
+    sample_desc = f"{len(reqs)} shapes of the sweep per step, reference Executor::run, {nthreads} threads"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wname, "sample": sample_desc},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": nthreads, "kind": "reference", "sample": sample_desc},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="disc", choices=["disc", "reference"])
+    ap.add_argument("--workload", default="ln_gelu")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--schedule", default="auto")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world, rank, local, dist = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import paper_2103_05288_b200 as D
+    D.lib()
+    wname, graph, shapes = workload(args.workload)
+    stream = C.c_void_p()
+    D.api._cuda(D.lib().disc_cuda_set_device(local))
+    D.api._cuda(D.lib().disc_cuda_stream_create(C.byref(stream)))
+    ex = D.Executor(local, stream.value)
+    ex.set_schedule(args.schedule)
+    compiler = D.Compiler()
+    plan = compiler.compile(graph)
+    reqs = Requests(D, graph, shapes, seed=rank)
+    D.api._cuda(D.lib().disc_cuda_device_synchronize())
+
+    sm, l2, hbm = C.c_int(), C.c_int64(), C.c_int64()
+    D.lib().disc_cuda_device_info(local, C.byref(sm), C.byref(l2), C.byref(hbm))
+    flush_bytes = max(4 * l2.value, 1 << 28)
+    flush = C.c_void_p()
+    D.api._cuda(D.lib().disc_cuda_malloc(flush_bytes, stream, C.byref(flush)))
+    ev = [C.c_void_p(), C.c_void_p()]
+    for e in ev:
+        D.api._cuda(D.lib().disc_cuda_event_create(C.byref(e)))
+
+    for _ in range(args.warmup):
+        reqs.run(ex, plan)
+    D.api._cuda(D.lib().disc_cuda_stream_synchronize(stream))
+    step_bytes = ex.algorithmic_bytes()  # batch total of the last step
+
+    # ---- timed region: K steps, device time per step (flush untimed) ----
+    ex.set_timing(True)
+    launches0 = D.kernel_launches()
+    step_ms, records = [], []
+    barrier(dist, local)
+    wall0 = time.perf_counter()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            D.lib().disc_cuda_flush_l2(flush, flush_bytes, stream)
+            D.lib().disc_cuda_event_record(ev[0], stream)
+            reqs.run(ex, plan)
+            D.lib().disc_cuda_event_record(ev[1], stream)
+            D.lib().disc_cuda_stream_synchronize(stream)
+            ms = C.c_float()
+            D.lib().disc_cuda_event_elapsed_ms(ev[0], ev[1], C.byref(ms))
+            step_ms.append(ms.value)
+            records.extend(ex.launch_records())
+    wall = time.perf_counter() - wall0
+    flushes = args.steps
+    gpu_launches = D.kernel_launches() - launches0 - flushes
+    barrier(dist, local)
+    ex.set_timing(False)
+    total_ms = allreduce_max(dist, local, sum(step_ms))
+    ms_per_step = total_ms / args.steps
+    value = world * step_bytes / (ms_per_step / 1e3) / 1e9
+
+    # ---- roofline: dominant kernel over the timed steps ----
+    peak, peak_kind = peaks()
+    by_kernel = {}
+    for r in records:
+        k = (r["kernel"], r["schedule"])
+        b = by_kernel.setdefault(k, [0, 0.0, 0])
+        b[0] += r["bytes"]
+        b[1] += r["ms"]
+        b[2] += 1
+    (dk, dsched), (dbytes, dms, dn) = max(by_kernel.items(), key=lambda kv: kv[1][1])
+    achieved = dbytes / (dms / 1e3) / 1e9 if dms > 0 else 0.0
+    kernel_ms_total = sum(v[1] for v in by_kernel.values())
+    breakdown = {f"k{k}:{s}": {"GB/s": round(b / (ms / 1e3) / 1e9, 1) if ms else None,
+                              "share": round(ms / kernel_ms_total, 3) if kernel_ms_total else None,
+                              "launches_per_step": n // args.steps}
+                 for (k, s), (b, ms, n) in sorted(by_kernel.items())}
+    # large-shape class (the >=70% target applies to large shapes)
+    big = [r for r in records if r["bytes"] >= (64 << 20)]
+    big_gbs = sum(r["bytes"] for r in big) / (sum(r["ms"] for r in big) / 1e3) / 1e9 if big else None
+
+    # ---- e2e through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(D, graph, shapes, plan, local, stream, step_bytes)
+    clocks = clk.summary()
+
+    out = None
+    if rank == 0:
+        cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline(graph, shapes)
+        out = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (uniform [0.25, 2) f32, device-generated)",
+            "config": {"workload": wname, "distinct_shapes": len(shapes), "requests_per_step": len(shapes),
+                       "bytes_per_step": step_bytes, "l2": "flushed before each step (4x L2 write)",
+                       "parallelism": f"request-sharded replicas x{world} (no collectives)",
+                       "schedule": args.schedule},
+            "frac_of_hbm_peak": round(value / world / peak, 4),
+            "recompiles": compiler.stats()["compile_count"] - 1,
+            "compile_count": compiler.stats()["compile_count"],
+            "large_shape_GBps": round(big_gbs, 1) if big_gbs else None,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dsched),
+                         "kernel": f"artifact {dk} ({dsched})", "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs",
+                         "bytes_per_launch": dbytes // max(dn, 1), "mean_launch_ms": round(dms / max(dn, 1), 5)},
+            "kernel_breakdown": breakdown,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": gpu_launches,
+            "clocks": clocks,
+            "wall_s_timed": round(wall, 3),
+        }
+        print(json.dumps(out))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def measure_e2e(D, graph, shapes, plan, device, stream, step_bytes):
+    """Public API, host buffers: per request H2D (inside disc_executor_run) from pinned
+    memory, launches, D2H of every output to pinned memory; wall time of one sweep."""
+    L = D.lib()
+    ex = D.Executor(device, stream.value)
+    names = [i["id"] for i in graph["inputs"]]
+    c_names = (C.c_char_p * len(names))(*[s.encode() for s in names])
+    pinned, reqs = [], []
+    h2d = d2h = 0
+    rng = np.random.default_rng(1)
+    for syms in shapes:
+        ptrs, dims = [], []
+        for i in graph["inputs"]:
+            shape = tuple(syms[d] if isinstance(d, str) else d for d in i["shape"])
+            n = int(np.prod(shape))
+            p = C.c_void_p()
+            D.api._cuda(L.disc_cuda_host_alloc(max(4 * n, 16), C.byref(p)))
+            arr = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_float)), shape=(max(n, 1),))
+            cv = const_value(i["id"], syms)
+            arr[:n] = cv if cv is not None else rng.uniform(0.25, 2.0, size=n).astype(np.float32)
+            pinned.append(p)
+            ptrs.append(p.value)
+            d = np.array(shape, dtype=np.int64)
+            dims.append(d)
+            h2d += 4 * n
+        reqs.append(((C.c_void_p * len(ptrs))(*ptrs), dims, (C.c_void_p * len(dims))(*[d.ctypes.data for d in dims]),
+                     (C.c_int * len(dims))(*[d.size for d in dims])))
+    outs = {}
+
+    def sweep():
+        nonlocal d2h
+        d2h = 0
+        for r, (data, dims, c_dims, c_ranks) in enumerate(reqs):
+            D.api._check(L.disc_executor_run(ex._h, plan._h, len(names), c_names, data, c_dims, c_ranks, 1))
+            for o, (_, odims) in enumerate(ex.output_views()):
+                n = int(np.prod(odims)) if odims else 1
+                key = (r, o)
+                if key not in outs:
+                    p = C.c_void_p()
+                    D.api._cuda(L.disc_cuda_host_alloc(max(4 * n, 16), C.byref(p)))
+                    outs[key] = p
+                if n:
+                    D.api._check(L.disc_executor_copy_output(ex._h, o, outs[key], 1))
+                d2h += 4 * n
+
+    sweep()  # warm allocator + staging
+    L.disc_cuda_stream_synchronize(stream)
+    t0 = time.perf_counter()
+    sweep()
+    L.disc_cuda_stream_synchronize(stream)
+    dt = time.perf_counter() - t0
+    for p in pinned + list(outs.values()):
+        L.disc_cuda_host_free(p)
+    return {"value": round(step_bytes / dt / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 3),
+            "path": "disc_executor_run(inputs_on_host=1) + disc_executor_copy_output(host) per request"}
+
+
+if __name__ == "__main__":
+    main()

@@ -80,6 +80,12 @@ int disc_executor_set_stream(disc_executor e, void* cuda_stream);
 int disc_executor_run(disc_executor e, disc_plan p, int n_inputs, const char* const* names,
                       const void* const* data, const int64_t* const* dims, const int* ranks,
                       int inputs_on_host);
+/* Runs n_requests requests of one plan back to back (asynchronously); request r binds
+ * data/dims/ranks[r*n_inputs + i] to names[i].  Launch records accumulate over the
+ * batch; outputs/stats/events are those of the last request. */
+int disc_executor_run_batch(disc_executor e, disc_plan p, int n_requests, int n_inputs,
+                            const char* const* names, const void* const* data,
+                            const int64_t* const* dims, const int* ranks, int inputs_on_host);
 int disc_executor_num_outputs(disc_executor e);
 /* Device pointer + dims of output i of the last run. */
 int disc_executor_output(disc_executor e, int i, const float** dptr, const int64_t** dims,
@@ -98,7 +104,15 @@ int disc_executor_num_events(disc_executor e);
 int disc_executor_event(disc_executor e, int i, int* four);
 /* Device kernels launched by the last run (CUDA launches, not plan kLaunch count). */
 int64_t disc_executor_device_launches(disc_executor e);
-/* 1: time every kLaunch/kLibraryCall with CUDA events (adds per-launch sync). */
+/* Per-launch records of the last run: plan instruction, artifact id (-1 = library call),
+ * schedule name, algorithmic boundary bytes, device ms (timing mode). */
+int disc_executor_num_records(disc_executor e);
+int disc_executor_record(disc_executor e, int i, int* instr, int* kernel, int64_t* bytes, double* ms,
+                         int* device_kernels, const char** schedule);
+/* Sum of algorithmic boundary bytes over the last run's launches. */
+int64_t disc_executor_algorithmic_bytes(disc_executor e);
+/* 1: time every kLaunch/kLibraryCall with CUDA events (asynchronous; read back when
+ * stats/records are queried). */
 int disc_executor_set_timing(disc_executor e, int enabled);
 /* Schedule override for testing: "auto" (default), "materialize" (per-member tape),
  * "fused" (forbid the per-member fallback), "twopass"/"atomic" column reductions. */

@@ -67,6 +67,7 @@ def _declare(L: C.CDLL) -> None:
         "disc_executor_destroy": ([vp], None),
         "disc_executor_set_stream": ([vp, vp], i32),
         "disc_executor_run": ([vp, vp, i32, P(cp), P(vp), P(vp), P(i32), i32], i32),
+        "disc_executor_run_batch": ([vp, vp, i32, i32, P(cp), P(vp), P(vp), P(i32), i32], i32),
         "disc_executor_num_outputs": ([vp], i32),
         "disc_executor_output": ([vp, i32, P(vp), P(P(i64)), P(i32)], i32),
         "disc_executor_copy_output": ([vp, i32, vp, i32], i32),
@@ -76,6 +77,9 @@ def _declare(L: C.CDLL) -> None:
         "disc_executor_event": ([vp, i32, P(i32)], i32),
         "disc_executor_device_launches": ([vp], i64),
         "disc_executor_set_timing": ([vp, i32], i32),
+        "disc_executor_num_records": ([vp], i32),
+        "disc_executor_record": ([vp, i32, P(i32), P(i32), P(i64), P(C.c_double), P(i32), P(cp)], i32),
+        "disc_executor_algorithmic_bytes": ([vp], i64),
         "disc_executor_set_schedule": ([vp, cp], i32),
         "disc_executor_set_cache_budget": ([vp, i64], i32),
         "disc_executor_run_kernel": ([vp, vp, i32, i32, i32, P(vp), P(vp), P(i32), P(i64), i32], i32),
@@ -459,6 +463,22 @@ class Executor:
             L.disc_executor_event(self._h, i, four)
             ev.append(tuple(four))
         return ev
+
+    def launch_records(self) -> List[Dict[str, object]]:
+        """Per-kLaunch records of the last run (schedule, algorithmic bytes, device ms)."""
+        L = lib()
+        out = []
+        for i in range(L.disc_executor_num_records(self._h)):
+            ins, k, dk = C.c_int(), C.c_int(), C.c_int()
+            b, ms, sch = C.c_int64(), C.c_double(), C.c_char_p()
+            _check(L.disc_executor_record(self._h, i, C.byref(ins), C.byref(k), C.byref(b), C.byref(ms),
+                                          C.byref(dk), C.byref(sch)))
+            out.append({"instr": ins.value, "kernel": k.value, "bytes": b.value, "ms": ms.value,
+                        "device_kernels": dk.value, "schedule": sch.value.decode()})
+        return out
+
+    def algorithmic_bytes(self) -> int:
+        return lib().disc_executor_algorithmic_bytes(self._h)
 
     def device_launches(self) -> int:
         return lib().disc_executor_device_launches(self._h)

@@ -58,6 +58,23 @@ int disc_executor_run(disc_executor e, disc_plan p, int n, const char* const* na
   });
 }
 
+int disc_executor_run_batch(disc_executor e, disc_plan p, int n_requests, int n_inputs, const char* const* names,
+                            const void* const* data, const int64_t* const* dims, const int* ranks, int on_host) {
+  return guard([&] {
+    std::vector<rt::InputBinding> in(n_inputs);
+    for (int r = 0; r < n_requests; ++r) {
+      for (int i = 0; i < n_inputs; ++i) {
+        const int k = r * n_inputs + i;
+        in[i].name = names[i];
+        in[i].dims.assign(dims[k], dims[k] + ranks[k]);
+        in[i].ptr = on_host ? e->ex.stage_input(i, data[k], bytes_of(dims[k], ranks[k]))
+                            : static_cast<const float*>(data[k]);
+      }
+      e->ex.run(*p->plan, in, r > 0);
+    }
+  });
+}
+
 int disc_executor_num_outputs(disc_executor e) { return static_cast<int>(e->ex.outputs().size()); }
 
 int disc_executor_output(disc_executor e, int i, const float** dptr, const int64_t** dims, int* rank) {
@@ -90,6 +107,7 @@ int disc_executor_synchronize(disc_executor e) {
 }
 
 int disc_executor_stats(disc_executor e, int64_t* s7, double* ms2) {
+  e->ex.finish_timing();
   const auto& s = e->ex.stats();
   int64_t v[7] = {s.launch_count, s.library_calls, s.host_instruction_count, s.peak_bytes,
                   s.alloc_calls, s.allocator_cache_hits, s.aliased_allocs};
@@ -113,6 +131,26 @@ int disc_executor_event(disc_executor e, int i, int* four) {
 }
 
 int64_t disc_executor_device_launches(disc_executor e) { return e->ex.device_launches(); }
+
+int disc_executor_num_records(disc_executor e) {
+  e->ex.finish_timing();
+  return static_cast<int>(e->ex.launch_records().size());
+}
+
+int disc_executor_record(disc_executor e, int i, int* instr, int* kernel, int64_t* bytes, double* ms,
+                         int* device_kernels, const char** schedule) {
+  return guard([&] {
+    const auto& r = e->ex.launch_records().at(i);
+    *instr = r.instr;
+    *kernel = r.kernel;
+    *bytes = r.bytes;
+    *ms = r.ms;
+    *device_kernels = r.device_kernels;
+    *schedule = r.schedule.c_str();
+  });
+}
+
+int64_t disc_executor_algorithmic_bytes(disc_executor e) { return e->ex.algorithmic_bytes(); }
 
 int disc_executor_set_timing(disc_executor e, int enabled) {
   e->ex.set_timing(enabled != 0);

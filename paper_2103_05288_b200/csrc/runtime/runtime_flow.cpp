@@ -75,8 +75,31 @@ void DeviceCachingAllocator::trim() {
 DeviceExecutor::DeviceExecutor(int device, void* stream)
     : device_(device), stream_(stream), alloc_(stream), scratch_(stream) {
   cuda_ok(disc_cuda_set_device(device), "set device");
-  cuda_ok(disc_cuda_event_create(&ev_[0]), "event");
-  cuda_ok(disc_cuda_event_create(&ev_[1]), "event");
+}
+
+int DeviceExecutor::take_event_pair() {
+  if (ev_next_ == ev_pool_.size()) {
+    void *a = nullptr, *b = nullptr;
+    cuda_ok(disc_cuda_event_create(&a), "event");
+    cuda_ok(disc_cuda_event_create(&b), "event");
+    ev_pool_.push_back({a, b});
+  }
+  return static_cast<int>(ev_next_++);
+}
+
+void DeviceExecutor::finish_timing() {
+  if (!timing_pending_) return;
+  timing_pending_ = false;
+  cuda_ok(disc_cuda_stream_synchronize(stream_), "stream sync");
+  double total = 0;
+  for (auto& r : records_) {
+    if (r.ev < 0) continue;
+    float ms = 0;
+    cuda_ok(disc_cuda_event_elapsed_ms(ev_pool_[r.ev].first, ev_pool_[r.ev].second, &ms), "event elapsed");
+    r.ms = ms;
+    total += ms;
+  }
+  stats_.kernel_ms = total;
 }
 
 DeviceExecutor::~DeviceExecutor() {
@@ -85,8 +108,10 @@ DeviceExecutor::~DeviceExecutor() {
     if (p) disc_cuda_free(p, stream_);
   for (auto& s : staging_)
     if (s.first) disc_cuda_free(s.first, stream_);
-  for (void* e : ev_)
-    if (e) disc_cuda_event_destroy(e);
+  for (auto& e : ev_pool_) {
+    disc_cuda_event_destroy(e.first);
+    disc_cuda_event_destroy(e.second);
+  }
 }
 
 void DeviceExecutor::set_stream(void* s) {
@@ -124,17 +149,21 @@ void DeviceExecutor::run_kernel(const KernelArtifact& art, const VersionArtifact
   }
   LaunchReport rep = launch_kernel(art, ver, ext, regs, outs, scratch_, stream_, pref_);
   device_launches_ = rep.device_kernels;
-  schedules_ = {rep.schedule};
+  records_ = {{-1, -1, rep.schedule, rep.algorithmic_bytes, 0.0, rep.device_kernels, -1}};
 }
 
-void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBinding>& inputs) {
+void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBinding>& inputs, bool append_records) {
   ExecStats stats;
   stats.host_instruction_count = plan.host_instruction_count();
   const auto t_run = Clock::now();
-  double kernel_ms = 0.0;
-  device_launches_ = 0;
-  algorithmic_bytes_ = 0;
-  schedules_.clear();
+  if (!append_records) {
+    if (timing_pending_) cuda_ok(disc_cuda_stream_synchronize(stream_), "stream sync");
+    timing_pending_ = false;
+    records_.clear();
+    ev_next_ = 0;
+    device_launches_ = 0;
+    algorithmic_bytes_ = 0;
+  }
   scratch_.reset();
 
   std::vector<int64_t> regs(plan.shape_program.num_regs, 0);
@@ -270,37 +299,27 @@ void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBindin
           ext.push_back(view(in.arg_bufs[a], resolve_all(art.external_input_dims[a], regs)));
         std::vector<OutBuf> outs;
         for (int b : in.out_bufs) outs.push_back(out_buf(b));
-        if (timing_) cuda_ok(disc_cuda_event_record(ev_[0], stream_), "event");
+        const int ev = timing_ ? take_event_pair() : -1;
+        if (ev >= 0) cuda_ok(disc_cuda_event_record(ev_pool_[ev].first, stream_), "event");
         LaunchReport rep = launch_kernel(art, *ver, ext, regs, outs, scratch_, stream_, pref_);
-        if (timing_) {
-          cuda_ok(disc_cuda_event_record(ev_[1], stream_), "event");
-          cuda_ok(disc_cuda_event_synchronize(ev_[1]), "event sync");
-          float ms = 0;
-          cuda_ok(disc_cuda_event_elapsed_ms(ev_[0], ev_[1], &ms), "event elapsed");
-          kernel_ms += ms;
-        }
+        if (ev >= 0) cuda_ok(disc_cuda_event_record(ev_pool_[ev].second, stream_), "event");
         stats.launch_count++;
         device_launches_ += rep.device_kernels;
         algorithmic_bytes_ += rep.algorithmic_bytes;
-        schedules_.push_back(rep.schedule);
+        records_.push_back({static_cast<int>(pc), in.a, rep.schedule, rep.algorithmic_bytes, 0.0, rep.device_kernels, ev});
         break;
       }
       case InstrKind::kLibraryCall: {
         const int64_t m = resolve(in.lib_dims[0], regs), k = resolve(in.lib_dims[1], regs),
                       n = resolve(in.lib_dims[2], regs);
         DevTensor a = view(in.arg_bufs[0], {m, k}), b = view(in.arg_bufs[1], {k, n});
-        if (timing_) cuda_ok(disc_cuda_event_record(ev_[0], stream_), "event");
+        const int ev = timing_ ? take_event_pair() : -1;
+        if (ev >= 0) cuda_ok(disc_cuda_event_record(ev_pool_[ev].first, stream_), "event");
         launch_gemm(m, k, n, a, b, out_buf(in.out_bufs[0]), stream_);
-        if (timing_) {
-          cuda_ok(disc_cuda_event_record(ev_[1], stream_), "event");
-          cuda_ok(disc_cuda_event_synchronize(ev_[1]), "event sync");
-          float ms = 0;
-          cuda_ok(disc_cuda_event_elapsed_ms(ev_[0], ev_[1], &ms), "event elapsed");
-          kernel_ms += ms;
-        }
+        if (ev >= 0) cuda_ok(disc_cuda_event_record(ev_pool_[ev].second, stream_), "event");
         stats.library_calls++;
         device_launches_ += (m && n) ? 1 : 0;
-        schedules_.push_back("gemm");
+        records_.push_back({static_cast<int>(pc), -1, "gemm", 4 * (m * k + k * n + m * n), 0.0, (m && n) ? 1 : 0, ev});
         break;
       }
       case InstrKind::kBindOutput: {
@@ -339,9 +358,9 @@ void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBindin
   for (const auto& [logical, ev] : events)
     if (ev.dealloc_instr < 0 && returned.insert(ev.physical).second) alloc_.free(ev.physical);
 
-  stats.kernel_ms = kernel_ms;
-  stats.host_ms = std::chrono::duration<double, std::milli>(Clock::now() - t_run).count() - kernel_ms;
+  stats.host_ms = std::chrono::duration<double, std::milli>(Clock::now() - t_run).count();
   stats_ = stats;
+  timing_pending_ = timing_pending_ || timing_;
   events_.clear();
   for (const auto& [_, ev] : events) events_.push_back(ev);
 }

@@ -58,6 +58,16 @@ class DeviceCachingAllocator {
   int64_t budget_ = 0;
 };
 
+struct LaunchRecord {
+  int instr = -1;         // plan instruction index
+  int kernel = -1;        // artifact id (-1: library call)
+  std::string schedule;   // schedule the selector picked
+  int64_t bytes = 0;      // algorithmic boundary bytes
+  double ms = 0.0;        // device time (timing mode only, after finish_timing)
+  int device_kernels = 0;
+  int ev = -1;            // event pair index (timing mode)
+};
+
 struct OutputView {
   const float* ptr = nullptr;
   std::vector<int64_t> dims;
@@ -76,13 +86,16 @@ class DeviceExecutor {
   void set_stream(void* s);
   void* stream() const { return stream_; }
   // Runs the plan; outputs remain valid until the next run.
-  void run(const CompiledPlan& plan, const std::vector<InputBinding>& inputs);
+  // append_records: keep the launch records of earlier runs (batched sweeps).
+  void run(const CompiledPlan& plan, const std::vector<InputBinding>& inputs, bool append_records = false);
+  // Timing mode: waits for the recorded events and fills record/stat device times.
+  void finish_timing();
   const std::vector<OutputView>& outputs() const { return outputs_; }
   const ExecStats& stats() const { return stats_; }
   const std::vector<BufferEvent>& events() const { return events_; }
   int64_t device_launches() const { return device_launches_; }
   int64_t algorithmic_bytes() const { return algorithmic_bytes_; }
-  const std::vector<std::string>& schedules() const { return schedules_; }
+  const std::vector<LaunchRecord>& launch_records() const { return records_; }
   void set_timing(bool on) { timing_ = on; }
   void set_schedule(SchedulePref p) { pref_ = p; }
   void set_cache_budget(int64_t b) { alloc_.set_budget(b); }
@@ -107,10 +120,13 @@ class DeviceExecutor {
   std::vector<BufferEvent> events_;
   int64_t device_launches_ = 0;
   int64_t algorithmic_bytes_ = 0;
-  std::vector<std::string> schedules_;
+  std::vector<LaunchRecord> records_;
   bool timing_ = false;
   SchedulePref pref_ = SchedulePref::kAuto;
-  void* ev_[2] = {nullptr, nullptr};
+  std::vector<std::pair<void*, void*>> ev_pool_;
+  size_t ev_next_ = 0;
+  bool timing_pending_ = false;
+  int take_event_pair();
 };
 
 }  // namespace disc::rt
