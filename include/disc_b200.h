@@ -126,6 +126,10 @@ int disc_executor_set_cache_budget(disc_executor e, int64_t bytes);
 int disc_executor_run_kernel(disc_executor e, disc_plan p, int kernel, int version, int n_ext,
                              const float* const* ext, const int64_t* const* ext_dims,
                              const int* ext_ranks, const int64_t* regs, int n_regs);
+/* Host-only dry run of the runtime flow for the given input shapes: returns the lowered
+ * device programs of every fused launch as JSON (used by tools/gen_patterns.py). */
+int disc_plan_capture_programs(disc_plan p, int n_inputs, const char* const* names,
+                               const int64_t* const* dims, const int* ranks, char** json);
 /* guard_passes (executor.cpp:78-98) */
 int disc_guard_passes(disc_plan p, int kernel, int version, const int64_t* regs, int n_regs);
 

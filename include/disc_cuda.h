@@ -25,43 +25,59 @@ extern "C" {
 #define DISC_MAX_SLOTS 12
 #define DISC_MAX_CONCAT 8
 
-/* Program opcodes.  Elementwise ops have the reference's f32 semantics (kernels.cpp:26-44):
- * IEEE add/sub/mul/div (no FMA contraction), max(a,b) = (a<b)?b:a, libdevice expf/tanhf. */
+/* Tape operations (host-level semantics).  Elementwise ops have the reference's f32
+ * semantics (kernels.cpp:26-44): IEEE add/sub/mul/div (no FMA contraction),
+ * max(a,b) = (a<b)?b:a, libdevice expf/tanhf. */
 enum disc_op {
-  DISC_OP_LOAD = 0,   /* acc = ext[load] at map(f) */
+  DISC_OP_LOAD = 0,
   DISC_OP_ADD, DISC_OP_SUB, DISC_OP_MUL, DISC_OP_DIV, DISC_OP_MAX,
   DISC_OP_EXP, DISC_OP_TANH, DISC_OP_NEG,
-  DISC_OP_COPY,       /* acc = a */
-  DISC_OP_REDVAL,     /* acc = the current row's reduce result (row schedule only) */
+  DISC_OP_COPY,
+  DISC_OP_REDVAL,     /* the current row's reduce result (row schedule only) */
 };
-#define DISC_SRC_ACC 0xFF /* operand is the accumulator register */
-#define DISC_SRC_NONE 0xFE
+
+/* Pre-decoded device opcodes: operand sources (accumulator A / slot S) are folded into
+ * the opcode so the interpreter dispatches once per instruction through one jump table. */
+enum disc_opcode {
+  DISC_I_LOAD_ID = 0,   /* acc = ptr[f]                      (contiguous) */
+  DISC_I_LOAD_AFF = 1,  /* acc = ptr[off + row*rs + col*cs]  (2D affine) */
+  DISC_I_LOAD_GATHER = 2, /* acc = ptr[map(f)]               (general gather) */
+  DISC_I_LOAD_CONST = 3,  /* acc = hoisted scalar (loaded once per block) */
+  DISC_I_REDVAL = 4,
+  DISC_I_COPY = 5,      /* acc = slot[a] */
+  DISC_I_BIN = 8,       /* 8 + 4*(op-ADD) + mode, mode 0 AA, 1 AS, 2 SA, 3 SS (a op b) */
+  DISC_I_UN = 28,       /* 28 + 2*(op-EXP) + mode, mode 0 A, 1 S */
+  DISC_I_END = 34,
+};
+#define DISC_F_SLOT 1   /* also keep acc in slot dst */
+#define DISC_F_OUT 2    /* also store acc to outs[out] */
 
 typedef struct {
-  uint8_t op;
-  uint8_t a, b;   /* operand slots or DISC_SRC_ACC */
-  uint8_t dst;    /* slot to also keep the result in, or DISC_SRC_NONE */
-  int8_t load;    /* LOAD: index into loads[] */
-  int8_t out;     /* >= 0: store result to outs[out][f] */
-  uint8_t pad0, pad1;
+  uint8_t op;      /* disc_opcode */
+  uint8_t a, b;    /* operand slots */
+  uint8_t flags;   /* DISC_F_* */
+  uint8_t dst;     /* slot written when DISC_F_SLOT */
+  uint8_t load;    /* loads[] index for LOAD_* */
+  uint8_t out;     /* outs[] index when DISC_F_OUT */
+  uint8_t pad;
 } disc_instr;
 
-/* Gather map: out flat index f -> source flat index
- *   src = offset + sum_d coord_d(f) * stride[d], coords row-major over dims[0..rank).
- * rank 0 means identity (src = f).  magic/shift: u32 fast division for dims[d] when
- * the launch uses 32-bit indexing (dims[d] == 1 -> magic 0). */
-enum disc_load_mode {
-  DISC_LOAD_IDENTITY = 0,  /* contiguous at f */
-  DISC_LOAD_GATHER = 1,    /* general gather */
-  DISC_LOAD_ROWSCALAR = 2, /* row schedule: value depends only on the row (read once/row) */
-};
+/* A load binds an external operand for one launch.  The launch views its space as
+ * [rows, W] (f = row*W + col); most operands are then 2D-affine in (row, col):
+ *   identity  src = f
+ *   affine    src = offset + row*rs + col*cs   (row/column broadcasts, offsets, strides)
+ *   const     src = offset                      (hoisted: read once per block)
+ *   gather    src = offset + sum_d coord_d(f) * strides[d], coords row-major over dims
+ *             (magic/shift: u32 fast division, magic 0 = divide by 1). */
+enum disc_load_mode { DISC_LOAD_IDENTITY = 0, DISC_LOAD_AFFINE = 1, DISC_LOAD_GATHER = 2, DISC_LOAD_CONST = 3 };
 typedef struct {
   const float* ptr;
-  int32_t rank;
   int32_t mode;
-  int32_t vec_ok;   /* VEC=4 path: 1 = 128-bit load, 2 = splat (inner stride 0), 0 = 4 scalar loads */
+  int32_t rank;     /* gather */
+  int32_t vec_ok;   /* VEC=4: 1 = 128-bit load, 2 = splat (inner stride 0), 0 = 4 scalar loads */
   int32_t pad;
   int64_t offset;
+  int64_t rs, cs;   /* affine */
   int64_t dims[DISC_MAX_RANK];
   int64_t strides[DISC_MAX_RANK];
   uint32_t magic[DISC_MAX_RANK];
@@ -80,12 +96,16 @@ typedef struct {
 
 enum disc_reduce_kind { DISC_REDUCE_SUM = 0, DISC_REDUCE_MAX = 1 };
 
-/* Elementwise (kLoop) schedule: one program over the flat space [0, total). */
+/* Elementwise (kLoop) schedule: one program over the space viewed as [rows, W]. */
 typedef struct {
   disc_program prog;
-  int64_t total;
+  int64_t total;    /* rows * W */
+  int64_t W;        /* row width in elements (multiple of vec) */
+  int64_t rows;
   int32_t vec;      /* 4 or 1 */
   int32_t wide;     /* 1: 64-bit index math */
+  int32_t lpr;      /* lanes per row (power of two <= 32): narrow rows pack several per warp */
+  int32_t pad;
 } disc_loop_launch;
 
 /* Reduce schedules over the reduce argument collapsed to [K, R, C] (R reduced). */
@@ -180,6 +200,17 @@ int disc_cuda_fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float
 int disc_cuda_flush_l2(void* scratch, size_t bytes, void* stream);
 /* Number of kernels this library has launched (process-wide counter). */
 int64_t disc_cuda_kernel_launches(void);
+
+/* Generated fast paths: launches whose lowered program structure matches a pattern
+ * compiled ahead of time (kernels/patterns_gen.cu) run straight-line kernels instead of
+ * the interpreter.  Enabled by default; the counter reports how many launches used one. */
+int disc_cuda_set_specialization(int enabled);
+int64_t disc_cuda_specialized_launches(void);
+int disc_cuda_num_specializations(void);
+/* Capture mode (pattern generator, host only): device calls become no-ops, allocations
+ * return fake addresses and fused launches are recorded as JSON program structures. */
+int disc_cuda_set_capture(int enabled);
+int disc_cuda_capture_records(char** json);   /* free with disc_free */
 
 #ifdef __cplusplus
 }

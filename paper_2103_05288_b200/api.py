@@ -84,6 +84,12 @@ def _declare(L: C.CDLL) -> None:
         "disc_executor_set_cache_budget": ([vp, i64], i32),
         "disc_executor_run_kernel": ([vp, vp, i32, i32, i32, P(vp), P(vp), P(i32), P(i64), i32], i32),
         "disc_guard_passes": ([vp, i32, i32, P(i64), i32], i32),
+        "disc_plan_capture_programs": ([vp, i32, P(cp), P(vp), P(i32), P(vp)], i32),
+        "disc_cuda_set_specialization": ([i32], i32),
+        "disc_cuda_specialized_launches": ([], i64),
+        "disc_cuda_num_specializations": ([], i32),
+        "disc_cuda_set_capture": ([i32], i32),
+        "disc_cuda_capture_records": ([P(vp)], i32),
         # device layer (disc_cuda.h)
         "disc_cuda_last_error": ([], cp),
         "disc_cuda_device_count": ([P(i32)], i32),
@@ -508,6 +514,25 @@ class Executor:
         self.synchronize()
         del bufs
         return outs
+
+
+def capture_programs(plan: CompiledPlan, input_shapes: Dict[str, Sequence[int]]) -> list:
+    """Host-only dry run: the lowered device programs of every fused launch."""
+    names = list(input_shapes)
+    dims = [np.array(input_shapes[n], dtype=np.int64) for n in names]
+    k = len(names)
+    c_names = (C.c_char_p * max(k, 1))(*[n.encode() for n in names])
+    c_dims = (C.c_void_p * max(k, 1))(*[d.ctypes.data for d in dims])
+    c_ranks = (C.c_int * max(k, 1))(*[d.size for d in dims])
+    return json.loads(_str(lib().disc_plan_capture_programs, plan._h, k, c_names, c_dims, c_ranks))
+
+
+def set_specialization(enabled: bool) -> None:
+    lib().disc_cuda_set_specialization(int(enabled))
+
+
+def specialized_launches() -> int:
+    return lib().disc_cuda_specialized_launches()
 
 
 def guard_passes(plan: CompiledPlan, kernel: int, version: int, regs: Sequence[int]) -> bool:

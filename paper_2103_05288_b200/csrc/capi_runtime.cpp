@@ -190,6 +190,26 @@ int disc_executor_run_kernel(disc_executor e, disc_plan p, int kernel, int versi
   });
 }
 
+int disc_plan_capture_programs(disc_plan p, int n, const char* const* names, const int64_t* const* dims,
+                               const int* ranks, char** json) {
+  disc_cuda_set_capture(1);
+  int rc = guard([&] {
+    rt::DeviceExecutor ex(0, nullptr);
+    std::vector<rt::InputBinding> in(n);
+    for (int i = 0; i < n; ++i) {
+      in[i].name = names[i];
+      in[i].dims.assign(dims[i], dims[i] + ranks[i]);
+      void* fake = nullptr;
+      disc_cuda_malloc(static_cast<size_t>(bytes_of(dims[i], ranks[i])), nullptr, &fake);
+      in[i].ptr = static_cast<const float*>(fake);
+    }
+    ex.run(*p->plan, in);
+    disc_cuda_capture_records(json);
+  });
+  disc_cuda_set_capture(0);
+  return rc;
+}
+
 int disc_guard_passes(disc_plan p, int kernel, int version, const int64_t* regs, int n_regs) {
   const KernelArtifact& art = p->plan->kernels.at(kernel);
   std::vector<int64_t> r(regs, regs + n_regs);

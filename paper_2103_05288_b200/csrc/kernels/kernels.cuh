@@ -1,0 +1,296 @@
+// Kernel templates for the fused schedules, parameterised by a "program" functor:
+//   Interp       -- the generic tape interpreter (program.cuh, run_tile), and
+//   generated    -- straight-line code for a known program structure (patterns_gen.cu),
+// so both share one schedule implementation.  See fused.cu for the launchers.
+#pragma once
+
+#include <cfloat>
+#include <cmath>
+
+#include "program.cuh"
+
+namespace disc_dev {
+
+struct Interp {
+  template <int VEC, int CH, bool WIDE>
+  __device__ __forceinline__ static void run(const disc_program& P, const TileCtx& t, typename Vec<VEC>::T (&acc)[CH],
+                                             typename Vec<VEC>::T* slots, int stride, const float* consts, float red) {
+    run_tile<VEC, CH, WIDE>(P, t, acc, slots, stride, consts, red);
+  }
+};
+
+
+constexpr int kLoopThreads = 256;
+constexpr int kCH = 2;  // chunks per thread per dispatch
+
+// ---------------------------------------------------------------------------
+// kLoop: the space viewed as [rows, W].  A warp tile covers 32/lpr rows x (lpr*CH*VEC)
+// columns: lpr lanes share a row (lane l takes chunks l, l+lpr, ... so every access is
+// coalesced), narrow rows pack several per warp.  Grid-stride over warp tiles.
+template <int VEC, bool WIDE, typename Prog>
+__global__ void __launch_bounds__(kLoopThreads) k_loop(const __grid_constant__ disc_loop_launch L) {
+  using T = typename Vec<VEC>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ float consts[DISC_MAX_LOADS];
+  T* slots = reinterpret_cast<T*>(smem_raw) + threadIdx.x;
+  hoist_consts(L.prog, consts);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int lpr = L.lpr;
+  const int rpw = 32 / lpr;
+  const int sub = lane / lpr;
+  const int64_t cstride = static_cast<int64_t>(lpr) * VEC;
+  const int64_t span = cstride * kCH;
+  const int64_t tpr = (L.W + span - 1) / span;
+  const int64_t ntiles = ((L.rows + rpw - 1) / rpw) * tpr;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t tile = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < ntiles;
+       tile += warps) {
+    const int64_t rg = tile / tpr;
+    TileCtx t;
+    t.row = rg * rpw + sub;
+    t.col0 = (tile - rg * tpr) * span + (lane & (lpr - 1)) * VEC;
+    t.W = L.W;
+    t.cstride = cstride;
+    const int64_t left = L.W - t.col0;
+    t.nvalid = (t.row >= L.rows || left <= 0)
+                   ? 0
+                   : static_cast<int>(left >= kCH * cstride ? kCH : (left + cstride - 1) / cstride);
+    T acc[kCH];
+    Prog::template run<VEC, kCH, WIDE>(L.prog, t, acc, slots, kLoopThreads, consts, 0.f);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Reduction helpers (f64, insensitive to order within f64 rounding).
+__device__ __forceinline__ double red_identity(int kind) { return kind == DISC_REDUCE_SUM ? 0.0 : -INFINITY; }
+__device__ __forceinline__ double red_step(int kind, double acc, double v) {
+  return kind == DISC_REDUCE_SUM ? acc + v : ((acc < v) ? v : acc);  // std::max(acc, v)
+}
+__device__ __forceinline__ double red_join(int kind, double a, double b) {
+  return kind == DISC_REDUCE_SUM ? a + b : ((a < b) ? b : a);  // partials never hold NaN for max
+}
+__device__ __forceinline__ double red_accumulate(int kind, double acc, float v) { return red_step(kind, acc, (double)v); }
+__device__ __forceinline__ double red_accumulate(int kind, double acc, float4 v) {
+  acc = red_step(kind, acc, (double)v.x);
+  acc = red_step(kind, acc, (double)v.y);
+  acc = red_step(kind, acc, (double)v.z);
+  return red_step(kind, acc, (double)v.w);
+}
+
+// ---------------------------------------------------------------------------
+// Row schedule: reduce arg collapsed to [K rows, R]; G threads per row (power of two);
+// thread `lane` of a row takes chunks lane, lane+G, ... (coalesced across the group).
+// Optional fused epilogue (post program) re-evaluated per element with the row value.
+template <int VEC, bool WIDE, typename Pre, typename Post>
+__global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduce_launch L) {
+  using T = typename Vec<VEC>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double warp_part[32];
+  __shared__ float row_val[32];
+  __shared__ float consts[2][DISC_MAX_LOADS];
+  T* slots = reinterpret_cast<T*>(smem_raw) + threadIdx.x;
+  hoist_consts(L.pre, consts[0]);
+  hoist_consts(L.post, consts[1]);
+  __syncthreads();
+  const int G = L.group;
+  const int lane = threadIdx.x & (G - 1);
+  const int sub = threadIdx.x / G;
+  const int rpb = blockDim.x / G;
+  const int64_t rows = L.K;
+  const int kind = L.kind;
+  const bool fuse_post = L.post.n_instr > 0;
+  const int64_t cstride = static_cast<int64_t>(G) * VEC;
+  const int64_t span = cstride * kCH;
+
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * rpb; base < rows; base += static_cast<int64_t>(gridDim.x) * rpb) {
+    const int64_t row = base + sub;
+    const bool valid = row < rows;
+    double acc = red_identity(kind);
+    if (valid) {
+      for (int64_t col0 = static_cast<int64_t>(lane) * VEC; col0 < L.R; col0 += span) {
+        TileCtx t{row, col0, L.R, cstride, 0};
+        const int64_t left = L.R - col0;
+        t.nvalid = static_cast<int>(left >= kCH * cstride ? kCH : (left + cstride - 1) / cstride);
+        T v[kCH];
+        Pre::template run<VEC, kCH, WIDE>(L.pre, t, v, slots, blockDim.x, consts[0], 0.f);
+#pragma unroll
+        for (int c = 0; c < kCH; ++c)
+          if (c < t.nvalid) acc = red_accumulate(kind, acc, v[c]);
+      }
+    }
+    const int width = G < 32 ? G : 32;
+    for (int o = width / 2; o > 0; o >>= 1) acc = red_join(kind, acc, __shfl_xor_sync(0xffffffffu, acc, o, width));
+    float result;
+    if (G <= 32) {
+      result = static_cast<float>(acc);
+    } else {
+      const int warp = threadIdx.x >> 5;
+      if ((threadIdx.x & 31) == 0) warp_part[warp] = acc;
+      __syncthreads();
+      const int wpr = G >> 5;
+      if (lane == 0) {
+        double s = warp_part[sub * wpr];
+        for (int w = 1; w < wpr; ++w) s = red_join(kind, s, warp_part[sub * wpr + w]);
+        row_val[sub] = static_cast<float>(s);
+      }
+      __syncthreads();
+      result = row_val[sub];
+    }
+    if (valid) {
+      if (lane == 0 && L.red_out) L.red_out[row] = result;
+      if (fuse_post) {
+        for (int64_t col0 = static_cast<int64_t>(lane) * VEC; col0 < L.R; col0 += span) {
+          TileCtx t{row, col0, L.R, cstride, 0};
+          const int64_t left = L.R - col0;
+          t.nvalid = static_cast<int>(left >= kCH * cstride ? kCH : (left + cstride - 1) / cstride);
+          T v[kCH];
+          Post::template run<VEC, kCH, WIDE>(L.post, t, v, slots, blockDim.x, consts[1], result);
+        }
+      }
+    }
+    if (G > 32) __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Column schedule: reduce arg collapsed to [K, R, C], reduce over R, C contiguous; viewed
+// as rows k*R + r of width C.  Block = 32 (along C) x 8 (along R); a thread owns CH
+// chunks strided by 32*VEC; grid.x = K * ceil(C / (32*CH*VEC)), grid.y = R splits.
+constexpr int kColX = 32, kColY = 8;
+
+template <int VEC, bool WIDE, typename Pre>
+__global__ void __launch_bounds__(kColX* kColY) k_col(const __grid_constant__ disc_reduce_launch L) {
+  using T = typename Vec<VEC>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double part[kColY][kColX][kCH * VEC];
+  __shared__ float consts[DISC_MAX_LOADS];
+  const int tid = threadIdx.y * kColX + threadIdx.x;
+  T* slots = reinterpret_cast<T*>(smem_raw) + tid;
+  hoist_consts(L.pre, consts);
+  __syncthreads();
+  const int kind = L.kind;
+  const int64_t cstride = static_cast<int64_t>(kColX) * VEC;
+  const int64_t span = cstride * kCH;
+  const int64_t tiles = (L.C + span - 1) / span;
+  const int64_t k = blockIdx.x / tiles;
+  const int64_t col0 = (blockIdx.x % tiles) * span + threadIdx.x * VEC;
+  const int64_t per = (L.R + L.splits - 1) / L.splits;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * per;
+  const int64_t r1 = r0 + per < L.R ? r0 + per : L.R;
+  const int64_t left = L.C - col0;
+  const int nvalid = left <= 0 ? 0 : static_cast<int>(left >= kCH * cstride ? kCH : (left + cstride - 1) / cstride);
+
+  double acc[kCH * VEC];
+#pragma unroll
+  for (int i = 0; i < kCH * VEC; ++i) acc[i] = red_identity(kind);
+  if (nvalid > 0) {
+    for (int64_t r = r0 + threadIdx.y; r < r1; r += kColY) {
+      TileCtx t{k * L.R + r, col0, L.C, cstride, nvalid};
+      T v[kCH];
+      Pre::template run<VEC, kCH, WIDE>(L.pre, t, v, slots, kColX * kColY, consts, 0.f);
+#pragma unroll
+      for (int c = 0; c < kCH; ++c) {
+        if constexpr (VEC == 1) {
+          acc[c] = red_step(kind, acc[c], (double)v[c]);
+        } else {
+          acc[c * 4 + 0] = red_step(kind, acc[c * 4 + 0], (double)v[c].x);
+          acc[c * 4 + 1] = red_step(kind, acc[c * 4 + 1], (double)v[c].y);
+          acc[c * 4 + 2] = red_step(kind, acc[c * 4 + 2], (double)v[c].z);
+          acc[c * 4 + 3] = red_step(kind, acc[c * 4 + 3], (double)v[c].w);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kCH * VEC; ++i) part[threadIdx.y][threadIdx.x][i] = acc[i];
+  __syncthreads();
+  if (threadIdx.y == 0) {
+    for (int c = 0; c < nvalid; ++c) {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        double s = part[0][threadIdx.x][c * VEC + i];
+        for (int y = 1; y < kColY; ++y) s = red_join(kind, s, part[y][threadIdx.x][c * VEC + i]);
+        const int64_t o = k * L.C + col0 + c * cstride + i;
+        switch (L.schedule) {
+          case DISC_SCHED_COL_SINGLE:
+            if (L.red_out) L.red_out[o] = static_cast<float>(s);
+            break;
+          case DISC_SCHED_COL_TWOPASS:
+            L.workspace[static_cast<int64_t>(blockIdx.y) * L.K * L.C + o] = s;
+            break;
+          default:  // DISC_SCHED_COL_ATOMIC (sum only)
+            atomicAdd(L.workspace + o, s);
+            break;
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host-side launch configuration shared by the interpreter and generated kernels.
+inline int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+template <typename K>
+inline cudaError_t set_smem(K kernel, size_t bytes) {
+  if (bytes <= 40 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+}
+
+// use_slots = false for generated programs (values live in registers, no slot smem).
+template <typename K>
+inline cudaError_t launch_loop_with(K kernel, const disc_loop_launch& L, cudaStream_t s, bool use_slots = true) {
+  if (L.total <= 0) return cudaSuccess;
+  const int64_t span = static_cast<int64_t>(L.lpr) * kCH * L.vec;
+  const int64_t rpw = 32 / L.lpr;
+  const int64_t tiles = ((L.rows + rpw - 1) / rpw) * ((L.W + span - 1) / span);
+  const int64_t warps_per_block = kLoopThreads / 32;
+  const int64_t want = (tiles + warps_per_block - 1) / warps_per_block;
+  const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
+  const int grid = static_cast<int>(want < cap ? want : cap);
+  const size_t smem = use_slots ? static_cast<size_t>(L.prog.n_slots) * kCH * kLoopThreads * (L.vec == 4 ? 16 : 4) : 0;
+  cudaError_t e = set_smem(kernel, smem);
+  if (e != cudaSuccess) return e;
+  kernel<<<grid, kLoopThreads, smem, s>>>(L);
+  return cudaGetLastError();
+}
+
+template <typename K>
+inline cudaError_t launch_row_with(K kernel, const disc_reduce_launch& L, cudaStream_t s, bool use_slots = true) {
+  if (L.K <= 0) return cudaSuccess;
+  const int slots = L.pre.n_slots > L.post.n_slots ? L.pre.n_slots : L.post.n_slots;
+  const int block = L.group > 256 ? L.group : 256;
+  const int rpb = block / L.group;
+  const int64_t groups = (L.K + rpb - 1) / rpb;
+  const int64_t cap = static_cast<int64_t>(sm_count()) * (2048 / block) * 2;
+  const int grid = static_cast<int>(groups < cap ? groups : cap);
+  const size_t smem = use_slots ? static_cast<size_t>(slots) * kCH * block * (L.vec == 4 ? 16 : 4) : 0;
+  cudaError_t e = set_smem(kernel, smem);
+  if (e != cudaSuccess) return e;
+  kernel<<<grid, block, smem, s>>>(L);
+  return cudaGetLastError();
+}
+
+// Column pass only (the finalize kernel is launched by the caller).
+template <typename K>
+inline cudaError_t launch_col_with(K kernel, const disc_reduce_launch& L, cudaStream_t s, bool use_slots = true) {
+  const int64_t span = static_cast<int64_t>(kColX) * kCH * L.vec;
+  const int64_t tiles = (L.C + span - 1) / span;
+  dim3 grid(static_cast<unsigned>(L.K * tiles), static_cast<unsigned>(L.splits));
+  dim3 block(kColX, kColY);
+  const size_t smem = use_slots ? static_cast<size_t>(L.pre.n_slots) * kCH * kColX * kColY * (L.vec == 4 ? 16 : 4) : 0;
+  cudaError_t e = set_smem(kernel, smem);
+  if (e != cudaSuccess) return e;
+  kernel<<<grid, block, smem, s>>>(L);
+  return cudaGetLastError();
+}
+
+}  // namespace disc_dev

@@ -1,9 +1,13 @@
-// Device-side interpreter for lowered fusion tapes (disc_program).
+// Device interpreter for lowered fusion tapes (disc_program), v2.
 //
-// A thread evaluates the program at one flat index f (VEC=1) or at four consecutive
-// flat indices f..f+3 (VEC=4, float4 lanes).  Values flow through an accumulator
-// register; values needed later live in per-thread shared-memory slots.  Instruction
-// words and gather maps are read from __grid_constant__ parameter space (uniform).
+// One dispatch evaluates an instruction on a TILE of CH chunks x VEC elements of one row
+// of the launch's [rows, W] view (f = row*W + col): the opcode (operand modes folded in)
+// is decoded once per tile through a single jump table, then applied to CH*VEC elements
+// held in registers.  The accumulator lives in registers; values used out of order live
+// in per-thread shared-memory slots.  Loads are mostly 2D-affine in (row, col), so no
+// per-element division is needed; scalar constants are hoisted into shared memory once
+// per block.  Instruction words and load descriptors are read from __grid_constant__
+// parameter space (warp-uniform).
 #pragma once
 
 #include <cstdint>
@@ -25,49 +29,49 @@ struct Vec<4> {
 
 __device__ __forceinline__ float op_max(float a, float b) { return (a < b) ? b : a; }  // std::max(a,b)
 
-__device__ __forceinline__ float apply_bin(int op, float a, float b) {
-  switch (op) {
-    case DISC_OP_ADD: return __fadd_rn(a, b);
-    case DISC_OP_SUB: return __fsub_rn(a, b);
-    case DISC_OP_MUL: return __fmul_rn(a, b);
-    case DISC_OP_DIV: return __fdiv_rn(a, b);
-    default: return op_max(a, b);
-  }
+template <int OP>
+__device__ __forceinline__ float bin1(float a, float b) {
+  if constexpr (OP == 0) return __fadd_rn(a, b);
+  if constexpr (OP == 1) return __fsub_rn(a, b);
+  if constexpr (OP == 2) return __fmul_rn(a, b);
+  if constexpr (OP == 3) return __fdiv_rn(a, b);
+  return op_max(a, b);
 }
-
-__device__ __forceinline__ float apply_un(int op, float a) {
-  switch (op) {
-    case DISC_OP_EXP: return expf(a);
-    case DISC_OP_TANH: return tanhf(a);
-    default: return -a;
-  }
+template <int OP>
+__device__ __forceinline__ float un1(float a) {
+  if constexpr (OP == 0) return expf(a);
+  if constexpr (OP == 1) return tanhf(a);
+  return -a;
 }
-
-__device__ __forceinline__ float4 apply_bin(int op, float4 a, float4 b) {
-  return make_float4(apply_bin(op, a.x, b.x), apply_bin(op, a.y, b.y), apply_bin(op, a.z, b.z),
-                     apply_bin(op, a.w, b.w));
+template <int OP>
+__device__ __forceinline__ float bin(float a, float b) { return bin1<OP>(a, b); }
+template <int OP>
+__device__ __forceinline__ float4 bin(float4 a, float4 b) {
+  return make_float4(bin1<OP>(a.x, b.x), bin1<OP>(a.y, b.y), bin1<OP>(a.z, b.z), bin1<OP>(a.w, b.w));
 }
-__device__ __forceinline__ float4 apply_un(int op, float4 a) {
-  return make_float4(apply_un(op, a.x), apply_un(op, a.y), apply_un(op, a.z), apply_un(op, a.w));
+template <int OP>
+__device__ __forceinline__ float un(float a) { return un1<OP>(a); }
+template <int OP>
+__device__ __forceinline__ float4 un(float4 a) {
+  return make_float4(un1<OP>(a.x), un1<OP>(a.y), un1<OP>(a.z), un1<OP>(a.w));
 }
 
 __device__ __forceinline__ float splat(float v, float) { return v; }
 __device__ __forceinline__ float4 splat(float v, float4) { return make_float4(v, v, v, v); }
 
-// u32 fast division (n < 2^31): q = umulhi(n, magic) >> shift, magic == 0 means d == 1.
+// u32 fast division (n < 2^31): q = umulhi(n, magic) >> shift; magic 0 means d == 1.
 __device__ __forceinline__ uint32_t fdiv(uint32_t n, uint32_t magic, uint32_t shift) {
   return magic ? (__umulhi(n, magic) >> shift) : n;
 }
 
 template <bool WIDE>
-__device__ __forceinline__ int64_t map_index(const disc_load& L, int64_t f) {
-  if (L.rank == 0) return f;
+__device__ __forceinline__ int64_t gather_index(const disc_load& L, int64_t f) {
   int64_t src = L.offset;
   if (WIDE) {
     int64_t rem = f;
     for (int d = L.rank - 1; d > 0; --d) {
-      int64_t dim = L.dims[d];
-      int64_t q = rem / dim;
+      const int64_t dim = L.dims[d];
+      const int64_t q = rem / dim;
       src += (rem - q * dim) * L.strides[d];
       rem = q;
     }
@@ -75,7 +79,7 @@ __device__ __forceinline__ int64_t map_index(const disc_load& L, int64_t f) {
   } else {
     uint32_t rem = static_cast<uint32_t>(f);
     for (int d = L.rank - 1; d > 0; --d) {
-      uint32_t q = fdiv(rem, L.magic[d], L.shift[d]);
+      const uint32_t q = fdiv(rem, L.magic[d], L.shift[d]);
       src += static_cast<int64_t>(rem - q * static_cast<uint32_t>(L.dims[d])) * L.strides[d];
       rem = q;
     }
@@ -86,62 +90,182 @@ __device__ __forceinline__ int64_t map_index(const disc_load& L, int64_t f) {
 
 __device__ __forceinline__ float ldg(const float* p) { return __ldg(p); }
 
-template <int VEC, bool WIDE>
-__device__ __forceinline__ typename Vec<VEC>::T do_load(const disc_load& L, int64_t f) {
+// A tile: CH chunks of VEC elements in row `row`; chunk c starts at column
+// col0 + c*cstride (cstride = warp/group width * VEC keeps every access coalesced).
+struct TileCtx {
+  int64_t row;
+  int64_t col0;
+  int64_t W;
+  int64_t cstride;
+  int nvalid;  // leading chunks inside the row
+};
+
+template <int VEC>
+__device__ __forceinline__ typename Vec<VEC>::T load_row(const disc_load& L, const float* base, int64_t col) {
+  // base already includes offset + row*rs (affine) or row*W (identity)
   if constexpr (VEC == 1) {
-    return ldg(L.ptr + map_index<WIDE>(L, f));
+    return ldg(base + col * L.cs);
   } else {
-    if (L.mode == DISC_LOAD_IDENTITY) return __ldg(reinterpret_cast<const float4*>(L.ptr + f));
-    int64_t s = map_index<WIDE>(L, f);
-    if (L.vec_ok == 1) return __ldg(reinterpret_cast<const float4*>(L.ptr + s));
+    if (L.vec_ok == 1) return __ldg(reinterpret_cast<const float4*>(base + col));
     if (L.vec_ok == 2) {
-      float v = ldg(L.ptr + s);
+      const float v = ldg(base);
       return make_float4(v, v, v, v);
     }
-    // Four consecutive f share the outer coordinates (innermost extent % 4 == 0).
-    int64_t st = L.strides[L.rank - 1];
+    const int64_t cs = L.cs;
+    const float* p = base + col * cs;
+    return make_float4(ldg(p), ldg(p + cs), ldg(p + 2 * cs), ldg(p + 3 * cs));
+  }
+}
+
+template <int VEC, bool WIDE>
+__device__ __forceinline__ typename Vec<VEC>::T load_gather(const disc_load& L, int64_t f) {
+  if constexpr (VEC == 1) {
+    return ldg(L.ptr + gather_index<WIDE>(L, f));
+  } else {
+    const int64_t s = gather_index<WIDE>(L, f);
+    if (L.vec_ok == 1) return __ldg(reinterpret_cast<const float4*>(L.ptr + s));
+    if (L.vec_ok == 2) {
+      const float v = ldg(L.ptr + s);
+      return make_float4(v, v, v, v);
+    }
+    const int64_t st = L.strides[L.rank - 1];
     return make_float4(ldg(L.ptr + s), ldg(L.ptr + s + st), ldg(L.ptr + s + 2 * st), ldg(L.ptr + s + 3 * st));
   }
 }
 
-template <int VEC>
-__device__ __forceinline__ void do_store(float* out, int64_t f, typename Vec<VEC>::T v) {
-  if constexpr (VEC == 1) {
-    out[f] = v;
-  } else {
-    *reinterpret_cast<float4*>(out + f) = v;
+// Hoists CONST loads of `P` into consts[load index] (call from every thread, then sync).
+__device__ __forceinline__ void hoist_consts(const disc_program& P, float* consts) {
+  for (int l = threadIdx.x + threadIdx.y * blockDim.x; l < P.n_loads; l += blockDim.x * blockDim.y)
+    if (P.loads[l].mode == DISC_LOAD_CONST) consts[l] = ldg(P.loads[l].ptr + P.loads[l].offset);
+}
+
+// --- building blocks for generated (straight-line) programs --------------------------
+
+// One load of a tile, dispatched on the load's binding mode (warp-uniform branch).
+template <int VEC, int CH, bool WIDE>
+__device__ __forceinline__ void load_any(const disc_load& L, const TileCtx& t, const float* consts, int l,
+                                         typename Vec<VEC>::T (&v)[CH]) {
+  const int64_t f0 = t.row * t.W + t.col0;
+  switch (L.mode) {
+    case DISC_LOAD_IDENTITY: {
+      const float* base = L.ptr + f0;
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+        if (c < t.nvalid) {
+          if constexpr (VEC == 1) v[c] = ldg(base + c * t.cstride);
+          else v[c] = __ldg(reinterpret_cast<const float4*>(base + c * t.cstride));
+        }
+      break;
+    }
+    case DISC_LOAD_AFFINE: {
+      const float* base = L.ptr + L.offset + t.row * L.rs;
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+        if (c < t.nvalid) v[c] = load_row<VEC>(L, base, t.col0 + c * t.cstride);
+      break;
+    }
+    case DISC_LOAD_GATHER:
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+        if (c < t.nvalid) v[c] = load_gather<VEC, WIDE>(L, f0 + c * t.cstride);
+      break;
+    default: {
+      const float x = consts[l];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) v[c] = splat(x, v[c]);
+    }
   }
 }
 
-// Evaluates `P` at flat index f.  `slots` points at this thread's slot 0; slot k is at
-// slots[k * stride].  `red` is the row's reduce value for DISC_OP_REDVAL.  Returns acc.
-template <int VEC, bool WIDE>
-__device__ __forceinline__ typename Vec<VEC>::T run_program(const disc_program& P, int64_t f,
-                                                            typename Vec<VEC>::T* slots, int stride,
-                                                            float red) {
+template <int VEC, int CH>
+__device__ __forceinline__ void store_tile(float* out, const TileCtx& t, const typename Vec<VEC>::T (&v)[CH]) {
+  float* o = out + t.row * t.W + t.col0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c)
+    if (c < t.nvalid) {
+      if constexpr (VEC == 1) o[c * t.cstride] = v[c];
+      else *reinterpret_cast<float4*>(o + c * t.cstride) = v[c];
+    }
+}
+
+// Evaluates program P on one tile.  slots: this thread's slot base; slot k, chunk c lives
+// at slots[(k * CH + c) * stride].  Returns with acc[] = the last instruction's value.
+template <int VEC, int CH, bool WIDE>
+__device__ __forceinline__ void run_tile(const disc_program& P, const TileCtx& t,
+                                         typename Vec<VEC>::T (&acc)[CH], typename Vec<VEC>::T* slots, int stride,
+                                         const float* consts, float red) {
   using T = typename Vec<VEC>::T;
-  T acc{};
   const int n = P.n_instr;
+  const int64_t f0 = t.row * t.W + t.col0;
+#define DISC_S(k, c) slots[((k) * CH + (c)) * stride]
+#define DISC_FOR_C _Pragma("unroll") for (int c = 0; c < CH; ++c)
+#define DISC_BIN_CASES(OPI)                                                                       \
+  case DISC_I_BIN + 4 * OPI + 0: DISC_FOR_C acc[c] = bin<OPI>(acc[c], acc[c]); break;            \
+  case DISC_I_BIN + 4 * OPI + 1: DISC_FOR_C acc[c] = bin<OPI>(acc[c], DISC_S(in.b, c)); break;   \
+  case DISC_I_BIN + 4 * OPI + 2: DISC_FOR_C acc[c] = bin<OPI>(DISC_S(in.a, c), acc[c]); break;   \
+  case DISC_I_BIN + 4 * OPI + 3: DISC_FOR_C acc[c] = bin<OPI>(DISC_S(in.a, c), DISC_S(in.b, c)); break;
+#define DISC_UN_CASES(OPI)                                                              \
+  case DISC_I_UN + 2 * OPI + 0: DISC_FOR_C acc[c] = un<OPI>(acc[c]); break;             \
+  case DISC_I_UN + 2 * OPI + 1: DISC_FOR_C acc[c] = un<OPI>(DISC_S(in.a, c)); break;
   for (int pc = 0; pc < n; ++pc) {
     const disc_instr in = P.code[pc];
-    const int op = in.op;
-    if (op == DISC_OP_LOAD) {
-      acc = do_load<VEC, WIDE>(P.loads[in.load], f);
-    } else if (op == DISC_OP_REDVAL) {
-      acc = splat(red, acc);
-    } else {
-      T a = in.a == DISC_SRC_ACC ? acc : slots[in.a * stride];
-      if (op >= DISC_OP_EXP) {
-        acc = op == DISC_OP_COPY ? a : apply_un(op, a);
-      } else {
-        T b = in.b == DISC_SRC_ACC ? acc : slots[in.b * stride];
-        acc = apply_bin(op, a, b);
+    switch (in.op) {
+      case DISC_I_LOAD_ID: {
+        const float* base = P.loads[in.load].ptr + f0;
+        DISC_FOR_C if (c < t.nvalid) {
+          if constexpr (VEC == 1) acc[c] = ldg(base + c * t.cstride);
+          else acc[c] = __ldg(reinterpret_cast<const float4*>(base + c * t.cstride));
+        }
+        break;
+      }
+      case DISC_I_LOAD_AFF: {
+        const disc_load& L = P.loads[in.load];
+        const float* base = L.ptr + L.offset + t.row * L.rs;
+        DISC_FOR_C if (c < t.nvalid) acc[c] = load_row<VEC>(L, base, t.col0 + c * t.cstride);
+        break;
+      }
+      case DISC_I_LOAD_GATHER: {
+        const disc_load& L = P.loads[in.load];
+        DISC_FOR_C if (c < t.nvalid) acc[c] = load_gather<VEC, WIDE>(L, f0 + c * t.cstride);
+        break;
+      }
+      case DISC_I_LOAD_CONST: {
+        const float v = consts[in.load];
+        DISC_FOR_C acc[c] = splat(v, acc[c]);
+        break;
+      }
+      case DISC_I_REDVAL:
+        DISC_FOR_C acc[c] = splat(red, acc[c]);
+        break;
+      case DISC_I_COPY:
+        DISC_FOR_C acc[c] = DISC_S(in.a, c);
+        break;
+      DISC_BIN_CASES(0)
+      DISC_BIN_CASES(1)
+      DISC_BIN_CASES(2)
+      DISC_BIN_CASES(3)
+      DISC_BIN_CASES(4)
+      DISC_UN_CASES(0)
+      DISC_UN_CASES(1)
+      DISC_UN_CASES(2)
+      default:
+        break;
+    }
+    if (in.flags & DISC_F_SLOT) {
+      DISC_FOR_C DISC_S(in.dst, c) = acc[c];
+    }
+    if (in.flags & DISC_F_OUT) {
+      float* o = P.outs[in.out] + f0;
+      DISC_FOR_C if (c < t.nvalid) {
+        if constexpr (VEC == 1) o[c * t.cstride] = acc[c];
+        else *reinterpret_cast<T*>(o + c * t.cstride) = acc[c];
       }
     }
-    if (in.dst != DISC_SRC_NONE) slots[in.dst * stride] = acc;
-    if (in.out >= 0) do_store<VEC>(P.outs[in.out], f, acc);
   }
-  return acc;
+#undef DISC_S
+#undef DISC_FOR_C
+#undef DISC_BIN_CASES
+#undef DISC_UN_CASES
 }
 
 }  // namespace disc_dev

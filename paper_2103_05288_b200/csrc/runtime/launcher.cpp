@@ -98,48 +98,24 @@ Map transpose_map(const std::vector<int64_t>& in, const std::vector<int64_t>& pe
   return canonical(m);
 }
 
-disc_load make_load(const float* ptr, const Map& c) {
-  disc_load L;
-  std::memset(&L, 0, sizeof L);
-  L.ptr = ptr;
-  if (is_identity(c)) {
-    L.mode = DISC_LOAD_IDENTITY;
-    L.rank = 0;
-    return L;
-  }
-  if (c.dims.size() > DISC_MAX_RANK) throw InternalError("gather map rank exceeds DISC_MAX_RANK");
-  L.mode = DISC_LOAD_GATHER;
-  L.rank = static_cast<int32_t>(c.dims.size());
-  L.offset = c.offset;
-  for (size_t d = 0; d < c.dims.size(); ++d) {
-    L.dims[d] = c.dims[d];
-    L.strides[d] = c.strides[d];
-    if (c.dims[d] < (int64_t{1} << 31)) fast_div_magic(static_cast<uint32_t>(c.dims[d]), &L.magic[d], &L.shift[d]);
-  }
-  return L;
-}
-
-// VEC=4 suitability of one load; sets vec_ok.
-bool vec4_load(disc_load& L) {
-  if (L.mode == DISC_LOAD_IDENTITY) return (reinterpret_cast<uintptr_t>(L.ptr) & 15) == 0;
-  const int r = L.rank;
-  if (L.dims[r - 1] % 4 != 0) return false;
-  const int64_t inner = L.strides[r - 1];
-  if (inner == 0) {
-    L.vec_ok = 2;
-    return true;
-  }
-  bool aligned = inner == 1 && (reinterpret_cast<uintptr_t>(L.ptr) & 15) == 0 && L.offset % 4 == 0;
-  for (int d = 0; d < r - 1 && aligned; ++d) aligned = L.strides[d] % 4 == 0;
-  L.vec_ok = aligned ? 1 : 0;
+bool is_const_map(const Map& c) {  // c canonical
+  for (int64_t st : c.strides)
+    if (st != 0) return false;
   return true;
 }
 
 // ---------------------------------------------------------------------------
-// Program assembly: SSA values (one per instruction) -> accumulator + slots.
+// Program assembly: SSA values (one per instruction) -> accumulator + slots; loads are
+// bound to the launch's [rows, W] view afterwards (bind_view).
 
 struct NotFusible {
   const char* why;
+};
+
+struct Built {
+  disc_program prog;
+  std::vector<Map> maps;       // per load (canonical, over the consumer's flat index)
+  std::vector<int> load_pc;    // LOAD instruction of each load
 };
 
 class ProgramBuilder {
@@ -148,9 +124,10 @@ class ProgramBuilder {
     auto key = std::make_tuple(ptr, c.dims, c.strides, c.offset);
     auto it = cse_.find(key);
     if (it != cse_.end()) return it->second;
-    if (loads_.size() >= DISC_MAX_LOADS) throw NotFusible{"too many loads"};
-    loads_.push_back(make_load(ptr, c));
-    int v = push({DISC_OP_LOAD, -1, -1, static_cast<int>(loads_.size()) - 1});
+    if (maps_.size() >= DISC_MAX_LOADS) throw NotFusible{"too many loads"};
+    ptrs_.push_back(ptr);
+    maps_.push_back(c);
+    int v = push({DISC_OP_LOAD, -1, -1, static_cast<int>(maps_.size()) - 1});
     cse_[key] = v;
     return v;
   }
@@ -160,16 +137,9 @@ class ProgramBuilder {
     return red_;
   }
   void output(int v, float* ptr) { outs_.emplace_back(v, ptr); }
-  bool empty() const { return ins_.empty(); }
-  std::vector<disc_load*> load_refs() {
-    std::vector<disc_load*> r;
-    for (auto& l : loads_) r.push_back(&l);
-    return r;
-  }
 
   // result >= 0: the program must end with that value in the accumulator.
-  disc_program finish(int result) {
-    // Outputs: tag the producing instruction, or copy when it already stores elsewhere.
+  Built finish(int result) {
     std::vector<int> out_of(ins_.size(), -1);
     std::vector<float*> out_ptrs;
     for (auto [v, ptr] : outs_) {
@@ -179,9 +149,8 @@ class ProgramBuilder {
       if (out_of[v] < 0) {
         out_of[v] = o;
       } else {
-        int c = push({DISC_OP_COPY, v, -1, -1});
+        push({DISC_OP_COPY, v, -1, -1});
         out_of.push_back(o);
-        (void)c;
       }
     }
     if (result >= 0 && result != static_cast<int>(ins_.size()) - 1) {
@@ -192,52 +161,74 @@ class ProgramBuilder {
     const int n = static_cast<int>(ins_.size());
     if (n > DISC_MAX_INSTR) throw NotFusible{"program too long"};
 
-    // Operands not produced by the immediately preceding instruction need a slot.
+    // Operands not produced by the immediately preceding instruction (and every COPY
+    // operand) are read from a slot.
     std::vector<int> last_use(n, -1);
     std::vector<char> slotted(n, 0);
+    auto from_slot = [&](int i, int v) { return v >= 0 && (v != i - 1 || ins_[i].code == DISC_OP_COPY); };
     for (int i = 0; i < n; ++i)
       for (int v : {ins_[i].a, ins_[i].b})
-        if (v >= 0 && v != i - 1) {
+        if (from_slot(i, v)) {
           slotted[v] = 1;
           last_use[v] = std::max(last_use[v], i);
         }
     std::vector<int> slot_of(n, -1);
-    std::vector<int> holder(DISC_MAX_SLOTS, -1);  // slot -> value
+    std::vector<int> holder(DISC_MAX_SLOTS, -1);
     int nslots = 0;
-    disc_program P;
-    std::memset(&P, 0, sizeof P);
+    Built B;
+    std::memset(&B.prog, 0, sizeof B.prog);
+    disc_program& P = B.prog;
+    B.load_pc.assign(maps_.size(), -1);
     for (int i = 0; i < n; ++i) {
-      // Slots whose value dies at i may be reused as i's destination (reads precede writes).
       for (int s = 0; s < DISC_MAX_SLOTS; ++s)
         if (holder[s] >= 0 && last_use[holder[s]] <= i) holder[s] = -1;
+      const Ins& x = ins_[i];
       disc_instr& I = P.code[i];
-      I.op = static_cast<uint8_t>(ins_[i].code);
-      auto src = [&](int v) -> uint8_t {
-        if (v < 0) return DISC_SRC_NONE;
-        return v == i - 1 ? DISC_SRC_ACC : static_cast<uint8_t>(slot_of[v]);
-      };
-      I.a = src(ins_[i].a);
-      I.b = src(ins_[i].b);
-      I.load = static_cast<int8_t>(ins_[i].load);
-      I.out = static_cast<int8_t>(out_of[i]);
-      I.dst = DISC_SRC_NONE;
+      const bool sa = from_slot(i, x.a), sb = from_slot(i, x.b);
+      I.a = sa ? static_cast<uint8_t>(slot_of[x.a]) : 0;
+      I.b = sb ? static_cast<uint8_t>(slot_of[x.b]) : 0;
+      switch (x.code) {
+        case DISC_OP_LOAD:
+          I.op = DISC_I_LOAD_ID;  // patched by bind_view
+          I.load = static_cast<uint8_t>(x.load);
+          B.load_pc[x.load] = i;
+          break;
+        case DISC_OP_REDVAL:
+          I.op = DISC_I_REDVAL;
+          break;
+        case DISC_OP_COPY:
+          I.op = DISC_I_COPY;
+          break;
+        case DISC_OP_EXP: case DISC_OP_TANH: case DISC_OP_NEG:
+          I.op = static_cast<uint8_t>(DISC_I_UN + 2 * (x.code - DISC_OP_EXP) + (sa ? 1 : 0));
+          break;
+        default:
+          I.op = static_cast<uint8_t>(DISC_I_BIN + 4 * (x.code - DISC_OP_ADD) + (sa ? 2 : 0) + (sb ? 1 : 0));
+          break;
+      }
+      if (out_of[i] >= 0) {
+        I.flags |= DISC_F_OUT;
+        I.out = static_cast<uint8_t>(out_of[i]);
+      }
       if (slotted[i]) {
         int s = 0;
         while (s < DISC_MAX_SLOTS && holder[s] >= 0) ++s;
         if (s == DISC_MAX_SLOTS) throw NotFusible{"too many live values"};
         holder[s] = i;
         slot_of[i] = s;
+        I.flags |= DISC_F_SLOT;
         I.dst = static_cast<uint8_t>(s);
         nslots = std::max(nslots, s + 1);
       }
     }
     P.n_instr = n;
     P.n_slots = nslots;
-    P.n_loads = static_cast<int32_t>(loads_.size());
-    for (size_t l = 0; l < loads_.size(); ++l) P.loads[l] = loads_[l];
+    P.n_loads = static_cast<int32_t>(maps_.size());
+    for (size_t l = 0; l < maps_.size(); ++l) P.loads[l].ptr = ptrs_[l];
+    B.maps = maps_;
     P.n_outs = static_cast<int32_t>(out_ptrs.size());
     for (size_t o = 0; o < out_ptrs.size(); ++o) P.outs[o] = out_ptrs[o];
-    return P;
+    return B;
   }
 
  private:
@@ -245,7 +236,8 @@ class ProgramBuilder {
     int code, a, b, load;
   };
   std::vector<Ins> ins_;
-  std::vector<disc_load> loads_;
+  std::vector<const float*> ptrs_;
+  std::vector<Map> maps_;
   std::map<std::tuple<const float*, std::vector<int64_t>, std::vector<int64_t>, int64_t>, int> cse_;
   std::vector<std::pair<int, float*>> outs_;
   int red_ = -1;
@@ -254,6 +246,131 @@ class ProgramBuilder {
     return static_cast<int>(ins_.size()) - 1;
   }
 };
+
+// Binds every load of `b` to the [rows, W] view (f = row*W + col).
+void bind_view(Built& b, int64_t W) {
+  disc_program& P = b.prog;
+  for (size_t l = 0; l < b.maps.size(); ++l) {
+    const Map& c = b.maps[l];
+    disc_load& L = P.loads[l];
+    const float* ptr = L.ptr;
+    std::memset(&L, 0, sizeof L);
+    L.ptr = ptr;
+    int op;
+    if (is_identity(c)) {
+      L.mode = DISC_LOAD_IDENTITY;
+      op = DISC_I_LOAD_ID;
+    } else if (is_const_map(c)) {
+      L.mode = DISC_LOAD_CONST;
+      L.offset = c.offset;
+      op = DISC_I_LOAD_CONST;
+    } else if (c.dims.size() == 1) {  // src = off + f*s = off + row*(W*s) + col*s
+      L.mode = DISC_LOAD_AFFINE;
+      L.offset = c.offset;
+      L.rs = W * c.strides[0];
+      L.cs = c.strides[0];
+      op = DISC_I_LOAD_AFF;
+    } else if (c.dims.size() == 2 && c.dims[1] == W) {
+      L.mode = DISC_LOAD_AFFINE;
+      L.offset = c.offset;
+      L.rs = c.strides[0];
+      L.cs = c.strides[1];
+      op = DISC_I_LOAD_AFF;
+    } else {
+      if (c.dims.size() > DISC_MAX_RANK) throw NotFusible{"gather rank too large"};
+      L.mode = DISC_LOAD_GATHER;
+      L.rank = static_cast<int32_t>(c.dims.size());
+      L.offset = c.offset;
+      for (size_t d = 0; d < c.dims.size(); ++d) {
+        L.dims[d] = c.dims[d];
+        L.strides[d] = c.strides[d];
+        if (c.dims[d] < (int64_t{1} << 31)) fast_div_magic(static_cast<uint32_t>(c.dims[d]), &L.magic[d], &L.shift[d]);
+      }
+      op = DISC_I_LOAD_GATHER;
+    }
+    P.code[b.load_pc[l]].op = static_cast<uint8_t>(op);
+  }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// VEC=4 feasibility for every load/output of the programs on a [*, W] view; sets vec_ok.
+int choose_vec(const std::vector<Built*>& progs, int64_t W) {
+  if (W % 4 != 0) return 1;
+  for (Built* b : progs) {
+    disc_program& P = b->prog;
+    for (int o = 0; o < P.n_outs; ++o)
+      if (!aligned16(P.outs[o])) return 1;
+    for (int l = 0; l < P.n_loads; ++l) {
+      const disc_load& L = P.loads[l];
+      if (L.mode == DISC_LOAD_IDENTITY && !aligned16(L.ptr)) return 1;
+      if (L.mode == DISC_LOAD_GATHER && L.dims[L.rank - 1] % 4 != 0) return 1;
+    }
+  }
+  for (Built* b : progs) {
+    disc_program& P = b->prog;
+    for (int l = 0; l < P.n_loads; ++l) {
+      disc_load& L = P.loads[l];
+      if (L.mode == DISC_LOAD_AFFINE) {
+        L.vec_ok = L.cs == 0 ? 2 : (L.cs == 1 && aligned16(L.ptr) && L.offset % 4 == 0 && L.rs % 4 == 0) ? 1 : 0;
+      } else if (L.mode == DISC_LOAD_GATHER) {
+        const int r = L.rank;
+        const int64_t inner = L.strides[r - 1];
+        bool ok = inner == 1 && aligned16(L.ptr) && L.offset % 4 == 0;
+        for (int d = 0; d < r - 1 && ok; ++d) ok = L.strides[d] % 4 == 0;
+        L.vec_ok = inner == 0 ? 2 : (ok ? 1 : 0);
+      }
+    }
+  }
+  return 4;
+}
+
+// Row width for an elementwise launch: the innermost extent that makes the most loads
+// 2D-affine (no per-element division); the whole space as one row when all loads are
+// contiguous or constant.
+int64_t choose_width(const Built& b, int64_t total) {
+  std::vector<int64_t> cands;
+  for (const Map& c : b.maps)
+    if (!is_identity(c) && !is_const_map(c) && c.dims.size() >= 2) cands.push_back(c.dims.back());
+  int64_t best = total;
+  int best_score = -1;
+  for (int64_t W : cands) {
+    if (W <= 0 || total % W != 0) continue;
+    int score = 0;
+    for (const Map& c : b.maps)
+      score += is_identity(c) || is_const_map(c) || c.dims.size() == 1 || (c.dims.size() == 2 && c.dims[1] == W);
+    score = score * 2 + (W % 4 == 0);
+    if (score > best_score) {
+      best_score = score;
+      best = W;
+    }
+  }
+  return best > 0 ? best : 1;
+}
+
+int lanes_per_row(int64_t W, int vec) {
+  const int64_t per = (W / vec + 1) / 2;  // CH = 2 chunks per lane
+  int l = 1;
+  while (l < per && l < 32) l <<= 1;
+  return l;
+}
+
+constexpr int64_t kWideLimitView = (int64_t{1} << 31) - 64;
+
+disc_loop_launch make_loop(Built& b, int64_t total) {
+  disc_loop_launch L;
+  std::memset(&L, 0, sizeof L);
+  const int64_t W = choose_width(b, total);
+  bind_view(b, W);
+  L.vec = choose_vec({&b}, W);
+  L.prog = b.prog;
+  L.total = total;
+  L.W = W;
+  L.rows = total / W;
+  L.wide = total > kWideLimitView;
+  L.lpr = lanes_per_row(W, L.vec);
+  return L;
+}
 
 int dhlo_to_op(DhloOpKind k) {
   switch (k) {
@@ -451,15 +568,6 @@ struct Plan {
   disc_loop_launch post_pass;
 };
 
-void set_vec(std::vector<disc_program*> progs, int64_t unit, int32_t* vec) {
-  bool ok = unit % 4 == 0;
-  for (disc_program* P : progs) {
-    for (int l = 0; l < P->n_loads && ok; ++l) ok = vec4_load(P->loads[l]);
-    for (int o = 0; o < P->n_outs && ok; ++o) ok = (reinterpret_cast<uintptr_t>(P->outs[o]) & 15) == 0;
-  }
-  *vec = ok ? 4 : 1;
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -620,14 +728,6 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& 
   const int n = static_cast<int>(art.tape.size());
   LaunchReport rep;
 
-  // Members whose value is written to an output buffer (first listing wins).
-  auto out_ptr_of = [&](int t) -> std::vector<int> {
-    std::vector<int> idx;
-    for (size_t o = 0; o < art.output_tape_indices.size(); ++o)
-      if (art.output_tape_indices[o] == t) idx.push_back(static_cast<int>(o));
-    return idx;
-  };
-
   if (B.red < 0) {
     // kLoop: all members identity-aligned over N elements.
     const int64_t N = numel(B.dims[art.output_tape_indices.at(0)]);
@@ -635,16 +735,10 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& 
       if (numel(B.dims[t]) != N) throw NotFusible{"member size differs from the space"};
     ProgramBuilder pb;
     Lowering lw(B, pb, nullptr, nullptr);
-    for (size_t o = 0; o < art.output_tape_indices.size(); ++o) {
-      int t = art.output_tape_indices[o];
-      pb.output(lw.value(t), outs[o].ptr);
-    }
-    disc_loop_launch L;
-    std::memset(&L, 0, sizeof L);
-    L.prog = pb.finish(-1);
-    L.total = N;
-    L.wide = N > kWideLimit;
-    set_vec({&L.prog}, N, &L.vec);
+    for (size_t o = 0; o < art.output_tape_indices.size(); ++o)
+      pb.output(lw.value(art.output_tape_indices[o]), outs[o].ptr);
+    Built b = pb.finish(-1);
+    disc_loop_launch L = make_loop(b, N);
     if (N > 0) {
       cuda_ok(disc_cuda_launch_loop(&L, stream), "fused loop");
       rep.device_kernels = 1;
@@ -664,11 +758,13 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& 
   const int64_t nout = numel(B.dims[B.red]);
 
   // Reduce result destination: its output buffer, else scratch when an epilogue needs it.
-  std::vector<int> red_outs = out_ptr_of(B.red);
+  int red_out_idx = -1;
+  for (size_t o = 0; o < art.output_tape_indices.size(); ++o)
+    if (art.output_tape_indices[o] == B.red && red_out_idx < 0) red_out_idx = static_cast<int>(o);
   bool has_post = false;
   for (int o : art.output_tape_indices)
     if (B.post[o]) has_post = true;
-  float* red_ptr = red_outs.empty() ? nullptr : outs[red_outs[0]].ptr;
+  float* red_ptr = red_out_idx >= 0 ? outs[red_out_idx].ptr : nullptr;
   if (!red_ptr && has_post) red_ptr = static_cast<float*>(scratch.alloc(nout * 4));
 
   disc_reduce_launch R;
@@ -678,6 +774,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& 
   R.wide = N > kWideLimit || nout > kWideLimit;
 
   // Pre program: pre-member outputs, then the reduce argument (left in acc).
+  Built pre;
   {
     ProgramBuilder pb;
     Lowering lw(B, pb, nullptr, nullptr);
@@ -687,10 +784,9 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& 
       pb.output(lw.value(t), outs[o].ptr);
     }
     int arg = lw.at_identity(rarg);
-    R.pre = pb.finish(arg);
+    pre = pb.finish(arg);
   }
 
-  // Geometry -> schedule.
   R.K = geo.K;
   R.R = geo.R;
   R.C = geo.C;
@@ -704,8 +800,11 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& 
   }
 
   // Post program: fused into the row kernel when every reduce read is row-aligned.
-  Plan plan;
-  bool post_fused = false;
+  Built post;
+  std::memset(&post.prog, 0, sizeof post.prog);
+  bool post_fused = false, post_pass = false;
+  disc_loop_launch PL;
+  std::memset(&PL, 0, sizeof PL);
   if (has_post) {
     if (R.schedule == DISC_SCHED_ROW && !empty) {
       Map row = canonical(Map{{R.K, R.R}, {1, 0}, 0});
@@ -716,46 +815,49 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& 
           int t = art.output_tape_indices[o];
           if (B.post[t]) pb.output(lw.value(t), outs[o].ptr);
         }
-        R.post = pb.finish(-1);
+        post = pb.finish(-1);
         post_fused = true;
       } catch (const NotFusible&) {
-        std::memset(&R.post, 0, sizeof R.post);
       }
     }
     if (!post_fused) {
       if (!red_ptr) throw NotFusible{"no reduce buffer"};
       ProgramBuilder pb;
       Lowering lw(B, pb, red_ptr, nullptr);
-      int64_t Npost = -1;
+      int64_t Npost = 0;
       for (size_t o = 0; o < art.output_tape_indices.size(); ++o) {
         int t = art.output_tape_indices[o];
         if (!B.post[t]) continue;
         pb.output(lw.value(t), outs[o].ptr);
         Npost = numel(B.dims[t]);
       }
-      std::memset(&plan.post_pass, 0, sizeof plan.post_pass);
-      plan.post_pass.prog = pb.finish(-1);
-      plan.post_pass.total = Npost;
-      plan.post_pass.wide = Npost > kWideLimit;
-      set_vec({&plan.post_pass.prog}, Npost, &plan.post_pass.vec);
-      plan.has_post_pass = Npost > 0;
+      Built pp = pb.finish(-1);
+      PL = make_loop(pp, Npost);
+      post_pass = Npost > 0;
     }
   }
 
-  // Vector width along the contiguous dimension of the schedule.
+  // Bind loads to the schedule's [rows, W] view and pick the vector width.
   if (empty) {
+    bind_view(pre, 1);
     R.vec = 1;
   } else if (R.schedule == DISC_SCHED_ROW) {
-    set_vec({&R.pre, &R.post}, R.R, &R.vec);
+    bind_view(pre, R.R);
+    if (post_fused) bind_view(post, R.R);
+    R.vec = choose_vec({&pre, &post}, R.R);
   } else if (R.schedule == DISC_SCHED_GENERIC) {
+    bind_view(pre, 1);
     R.vec = 1;
     R.wide = 1;
     R.g_rank = geo.rank;
     R.g_mask = geo.mask;
     for (int d = 0; d < geo.rank; ++d) R.g_dims[d] = geo.gdims[d];
   } else {
-    set_vec({&R.pre}, R.C, &R.vec);
+    bind_view(pre, R.C);
+    R.vec = choose_vec({&pre}, R.C);
   }
+  R.pre = pre.prog;
+  R.post = post.prog;
 
   if (R.schedule == DISC_SCHED_ROW) {
     const int64_t chunks = empty ? 0 : R.R / R.vec;
@@ -763,7 +865,8 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& 
     rep.schedule = post_fused ? "row_fused" : "row";
   } else if (R.schedule != DISC_SCHED_GENERIC) {
     if (!R.red_out) R.red_out = static_cast<float*>(scratch.alloc(nout * 4));
-    const int64_t tiles = (R.C / R.vec + 31) / 32;
+    const int64_t span = 32 * 2 * R.vec;
+    const int64_t tiles = (R.C + span - 1) / span;
     const int64_t ctas = R.K * tiles;
     const int64_t want = (int64_t{sm_count()} * 8 + ctas - 1) / ctas;
     const int64_t max_split = std::max<int64_t>(1, R.R / 64);
@@ -790,25 +893,21 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& 
 
   cuda_ok(disc_cuda_launch_reduce(&R, stream), "fused reduce");
   rep.device_kernels = (R.schedule == DISC_SCHED_COL_TWOPASS || R.schedule == DISC_SCHED_COL_ATOMIC) ? 2 : 1;
-  if (plan.has_post_pass) {
-    cuda_ok(disc_cuda_launch_loop(&plan.post_pass, stream), "epilogue pass");
+  if (post_pass) {
+    cuda_ok(disc_cuda_launch_loop(&PL, stream), "epilogue pass");
     rep.device_kernels += 1;
     rep.schedule += "+post";
   }
   return rep;
 }
 
-// Single-instruction program helpers for materialisation and standalone artifacts.
+// Single-load program helper for materialisation and standalone artifacts.
 void run_copy(const float* src, const Map& m, float* dst, int64_t n, void* stream) {
   if (n <= 0) return;
   ProgramBuilder pb;
   pb.output(pb.load(src, m), dst);
-  disc_loop_launch L;
-  std::memset(&L, 0, sizeof L);
-  L.prog = pb.finish(-1);
-  L.total = n;
-  L.wide = n > kWideLimit;
-  set_vec({&L.prog}, n, &L.vec);
+  Built b = pb.finish(-1);
+  disc_loop_launch L = make_loop(b, n);
   cuda_ok(disc_cuda_launch_loop(&L, stream), "gather");
 }
 
@@ -839,12 +938,8 @@ LaunchReport launch_materialized(Binding& B, const std::vector<OutBuf>& outs, Sc
       }
       int v = vals.size() == 2 ? pb.op(dhlo_to_op(ti.kind), vals[0], vals[1]) : pb.op(dhlo_to_op(ti.kind), vals[0]);
       pb.output(v, buf[t]);
-      disc_loop_launch L;
-      std::memset(&L, 0, sizeof L);
-      L.prog = pb.finish(-1);
-      L.total = cnt;
-      L.wide = cnt > kWideLimit;
-      set_vec({&L.prog}, cnt, &L.vec);
+      Built b = pb.finish(-1);
+      disc_loop_launch L = make_loop(b, cnt);
       cuda_ok(disc_cuda_launch_loop(&L, stream), "materialized elementwise");
       rep.device_kernels++;
     } else if (ti.kind == DhloOpKind::kDynamicBroadcastInDim || ti.kind == DhloOpKind::kDynamicSlice) {
@@ -854,36 +949,32 @@ LaunchReport launch_materialized(Binding& B, const std::vector<OutBuf>& outs, Sc
       rep.device_kernels++;
     } else if (is_reduce(ti.kind)) {
       DevTensor x = tensor(ti.args[0]);
-      Geometry geo = reduce_geometry(x.dims, ti.dims);
+      if (cnt == 0) continue;
       disc_reduce_launch R;
       std::memset(&R, 0, sizeof R);
       ProgramBuilder pb;
       int v = pb.load(x.ptr, identity_map(numel(x.dims)));
-      R.pre = pb.finish(v);
+      Built b = pb.finish(v);
+      bind_view(b, 1);
+      R.pre = b.prog;
       R.kind = ti.kind == DhloOpKind::kReduceSum ? DISC_REDUCE_SUM : DISC_REDUCE_MAX;
       R.red_out = buf[t];
       R.vec = 1;
       R.wide = 1;
-      const bool empty = geo.K == 0 || geo.R == 0 || numel(x.dims) == 0;
-      if (empty || geo.schedule != DISC_SCHED_GENERIC) {
-        // Any contiguous pattern also runs correctly as the generic schedule.
-        R.schedule = empty ? DISC_SCHED_ROW : DISC_SCHED_GENERIC;
-        R.K = empty ? cnt : cnt;
-        R.R = empty ? 0 : numel(x.dims) / std::max<int64_t>(cnt, 1);
-        R.group = 1;
+      R.group = 1;
+      R.K = cnt;
+      if (numel(x.dims) == 0) {  // empty reduced extent: identities
+        R.schedule = DISC_SCHED_ROW;
+        R.R = 0;
+        R.C = 1;
+      } else {
+        R.schedule = DISC_SCHED_GENERIC;
+        R.R = numel(x.dims) / cnt;
         R.g_rank = static_cast<int>(x.dims.size());
         if (R.g_rank > DISC_MAX_RANK) throw InternalError("rank too large");
         for (int d = 0; d < R.g_rank; ++d) R.g_dims[d] = x.dims[d];
         for (int64_t a : ti.dims) R.g_mask |= 1 << a;
-      } else {
-        R.schedule = DISC_SCHED_GENERIC;
-        R.K = geo.K;
-        R.R = geo.R;
-        R.g_rank = geo.rank;
-        R.g_mask = geo.mask;
-        for (int d = 0; d < geo.rank; ++d) R.g_dims[d] = geo.gdims[d];
       }
-      if (cnt == 0) continue;
       cuda_ok(disc_cuda_launch_reduce(&R, stream), "materialized reduce");
       rep.device_kernels++;
     } else {

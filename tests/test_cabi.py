@@ -46,3 +46,12 @@ def test_sass_is_sm100a(disc):
     ptx = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-ptx", disc.api.LIB_PATH],
                          capture_output=True, text=True).stdout
     assert ".ptx" not in ptx
+
+
+def test_generated_patterns_up_to_date(disc):
+    """patterns_gen.cu must match what the current lowering produces for the library."""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "gen_patterns.py"), "--check"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr

@@ -331,3 +331,31 @@ def test_device_inputs_and_large_softmax_property(gpu):
         want = e / e.sum(axis=1, keepdims=True)
         assert np.max(np.abs(y - want) / np.maximum(1.0, np.abs(want))) <= 1e-5
         np.testing.assert_allclose(y.sum(axis=1), 1.0, rtol=1e-4)
+
+
+def test_generated_kernels_match_interpreter(gpu):
+    """Generated straight-line kernels are used for the library patterns and produce
+    results bit-identical to the interpreter (same ops, same order)."""
+    from paper_2103_05288_b200 import workloads as W
+    cases = [(W.ln_gelu_graph(), {"T": 333, "H": 768}), (W.ln_gelu_graph(), {"T": 5, "H": 1000}),
+             (W.softmax_graph_for(0), {"S0": 77, "S1": 4096}), (W.softmax_graph_for(0), {"S0": 300, "S1": 7}),
+             (W.colreduce_graph(), {"N": 5000, "C": 260}), (W.colreduce_graph(), {"N": 100000, "C": 3}),
+             (W.bert_graph(), {"R": 12 * 2 * 64, "S": 64, "T": 128, "H": 768, "F": 3072})]
+    rng = np.random.default_rng(5)
+    for g, syms in cases:
+        plan = gpu.compile_graph(g)
+        inputs = {i["id"]: rng.uniform(0.25, 2.0, size=[syms[d] if isinstance(d, str) else d for d in i["shape"]])
+                  .astype(np.float32) for i in g["inputs"]}
+        ex = gpu.Executor()
+        before = gpu.specialized_launches()
+        fast = ex.run(plan, inputs).outputs
+        assert gpu.specialized_launches() > before, (g["name"], syms)
+        gpu.set_specialization(False)
+        try:
+            slow = ex.run(plan, inputs).outputs
+        finally:
+            gpu.set_specialization(True)
+        for a, b in zip(fast, slow):
+            np.testing.assert_array_equal(a, b)
+        want, _, _ = O.Executor().run(plan.to_json(), inputs)
+        check_outputs(fast, want)

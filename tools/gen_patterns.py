@@ -1,0 +1,171 @@
+"""Generates paper_2103_05288_b200/csrc/kernels/patterns_gen.cu.
+
+For every fused launch of a pattern library (the fixture graphs and the BASELINE config
+graphs C1-C4, each at a few representative shapes), the product's own runtime lowering
+is run in capture mode (host only, no GPU) to obtain the device program structure.  Each
+distinct structure becomes a straight-line device function -- SSA values in registers,
+no interpretation -- instantiated into the same schedule kernels the interpreter uses
+(kernels.cuh).  At runtime the device layer hashes every launch's program structure and
+uses the generated kernel when one exists; any other structure runs the interpreter.
+Nothing is generated or compiled at runtime; kernels are shape-generic (load bindings,
+vector width and geometry stay launch parameters).
+
+  python tools/gen_patterns.py            # rewrite the generated file
+  python tools/gen_patterns.py --check    # exit 1 if it is stale
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+OUT = os.path.join(ROOT, "paper_2103_05288_b200", "csrc", "kernels", "patterns_gen.cu")
+
+I_LOAD_CONST, I_REDVAL, I_COPY, I_BIN, I_UN = 3, 4, 5, 8, 28
+
+
+def library():
+    """(name, graph, [symbol bindings]) of the pattern library."""
+    from paper_2103_05288_b200 import workloads as W
+    lib = []
+    fx = json.load(open(os.path.join(ROOT, "tests", "golden", "fixtures.json")))
+    for name, f in sorted(fx.items()):
+        lib.append((f"fixture:{name}", json.loads(f["graph"]), f["bindings"]))
+    sm = W.softmax_graph_for(0)
+    lib.append(("C1:softmax", sm, [{"S0": 64, "S1": 8}, {"S0": 5, "S1": 7}, {"S0": 16, "S1": 4096},
+                                   {"S0": 2, "S1": 1}]))
+    lib.append(("C2:ln_gelu", W.ln_gelu_graph(), [{"T": 64, "H": 768}, {"T": 1, "H": 1024}, {"T": 7, "H": 4096}]))
+    lib.append(("C3:colreduce", W.colreduce_graph(), [{"N": 1000, "C": 36}, {"N": 64, "C": 4096},
+                                                      {"N": 4096, "C": 3}]))
+    lib.append(("C4:bert", W.bert_graph(), [{"R": 96, "S": 8, "T": 8, "H": 768, "F": 3072},
+                                            {"R": 12 * 8 * 128, "S": 128, "T": 8 * 128, "H": 768, "F": 3072}]))
+    return lib
+
+
+def input_shapes(graph, syms):
+    shapes = {}
+    for i in graph["inputs"]:
+        shapes[i["id"]] = [syms.get(d, 2) if isinstance(d, str) else d for d in i["shape"]]
+    return shapes
+
+
+def collect():
+    import paper_2103_05288_b200 as D
+    seen = {}
+    for name, graph, bindings in library():
+        for opts in (D.CompileOptions(), D.CompileOptions(enable_fusion=False)):
+            plan = D.compile_graph(graph, opts)
+            for syms in bindings:
+                try:
+                    recs = D.capture_programs(plan, input_shapes(graph, syms))
+                except D.DiscError:
+                    continue
+                for r in recs:
+                    seen.setdefault((r["kind"], r["key"]), (r, name))
+    return seen
+
+
+def gen_program(fn, prog):
+    """Straight-line body for one program (code from the capture)."""
+    code = prog["code"]
+    lines = [f"struct {fn} {{",
+             "  template <int VEC, int CH, bool WIDE>",
+             "  __device__ __forceinline__ static void run(const disc_program& P, const TileCtx& t,",
+             "      typename Vec<VEC>::T (&acc)[CH], typename Vec<VEC>::T*, int, const float* consts, float red) {",
+             "    using T = typename Vec<VEC>::T;"]
+    slot_val = {}
+    for i, (op, a, b, flags, dst, load, out) in enumerate(code):
+        v = f"v{i}"
+        lines.append(f"    T {v}[CH];")
+
+        def src(is_slot, s):
+            return f"v{slot_val[s]}" if is_slot else f"v{i - 1}"
+        if op <= I_LOAD_CONST:
+            lines.append(f"    load_any<VEC, CH, WIDE>(P.loads[{load}], t, consts, {load}, {v});")
+        elif op == I_REDVAL:
+            lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = splat(red, {v}[c]);")
+        elif op == I_COPY:
+            lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = {src(True, a)}[c];")
+        elif I_BIN <= op < I_UN:
+            k, mode = divmod(op - I_BIN, 4)
+            x, y = src(mode in (2, 3), a), src(mode in (1, 3), b)
+            lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = bin<{k}>({x}[c], {y}[c]);")
+        else:
+            k, mode = divmod(op - I_UN, 2)
+            lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = un<{k}>({src(mode == 1, a)}[c]);")
+        if flags & 1:
+            slot_val[dst] = i
+        if flags & 2:
+            lines.append(f"    store_tile<VEC, CH>(P.outs[{out}], t, {v});")
+    if code:
+        lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) acc[c] = v{len(code) - 1}[c];")
+    lines += ["  }", "};"]
+    return "\n".join(lines)
+
+
+def generate():
+    seen = collect()
+    parts = ["// GENERATED by tools/gen_patterns.py -- do not edit.",
+             "// Straight-line fused programs for the pattern library (fixtures + BASELINE configs C1-C4);",
+             "// see the generator's docstring.  Source patterns per entry are noted in comments.",
+             '#include "kernels.cuh"', "", "namespace disc_gen {", "using namespace disc_dev;", ""]
+    entries = []
+    for (kind, key), (rec, src_name) in sorted(seen.items()):
+        tag = f"{kind}_{key}"
+        parts.append(f"// {kind} {key} from {src_name}")
+        parts.append(gen_program(f"Pre_{tag}", rec["pre"]))
+        if kind == "row":
+            parts.append(gen_program(f"Post_{tag}", rec["post"]))
+        parts.append(f"cudaError_t launch_{tag}(const void* l, int vec, cudaStream_t s) {{")
+        if kind == "loop":
+            parts.append("  const auto& L = *static_cast<const disc_loop_launch*>(l);")
+            parts.append(f"  return vec == 4 ? launch_loop_with(k_loop<4, false, Pre_{tag}>, L, s, false)"
+                         f" : launch_loop_with(k_loop<1, false, Pre_{tag}>, L, s, false);")
+        elif kind == "row":
+            parts.append("  const auto& L = *static_cast<const disc_reduce_launch*>(l);")
+            parts.append(f"  return vec == 4 ? launch_row_with(k_row<4, false, Pre_{tag}, Post_{tag}>, L, s, false)"
+                         f" : launch_row_with(k_row<1, false, Pre_{tag}, Post_{tag}>, L, s, false);")
+        else:
+            parts.append("  const auto& L = *static_cast<const disc_reduce_launch*>(l);")
+            parts.append(f"  return vec == 4 ? launch_col_with(k_col<4, false, Pre_{tag}>, L, s, false)"
+                         f" : launch_col_with(k_col<1, false, Pre_{tag}>, L, s, false);")
+        parts.append("}")
+        parts.append("")
+        entries.append((["loop", "row", "col"].index(kind), key, f"launch_{tag}"))
+    parts.append("}  // namespace disc_gen")
+    parts.append("")
+    parts.append("namespace disc_spec {")
+    parts.append("struct Entry {\n  int kind;\n  uint64_t key;\n"
+                 "  cudaError_t (*launch)(const void* launch, int vec, cudaStream_t s);\n};")
+    parts.append("static const Entry kEntries[] = {")
+    for kind, key, fn in sorted(entries):
+        parts.append(f"    {{{kind}, 0x{key}ull, disc_gen::{fn}}},")
+    parts.append("};")
+    parts.append("const Entry* lookup(int kind, uint64_t key) {")
+    parts.append("  for (const Entry& e : kEntries)")
+    parts.append("    if (e.kind == kind && e.key == key) return &e;")
+    parts.append("  return nullptr;")
+    parts.append("}")
+    parts.append(f"int count() {{ return {len(entries)}; }}")
+    parts.append("}  // namespace disc_spec")
+    return "\n".join(parts) + "\n", len(entries)
+
+
+def main():
+    text, n = generate()
+    if "--check" in sys.argv:
+        cur = open(OUT).read() if os.path.exists(OUT) else ""
+        if cur != text:
+            print("patterns_gen.cu is stale: run python tools/gen_patterns.py")
+            sys.exit(1)
+        print(f"patterns_gen.cu up to date ({n} patterns)")
+        return
+    with open(OUT, "w") as f:
+        f.write(text)
+    print(f"wrote {OUT}: {n} patterns")
+
+
+if __name__ == "__main__":
+    main()
