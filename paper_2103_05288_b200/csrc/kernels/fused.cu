@@ -7,6 +7,14 @@
 
 namespace disc_dev {
 
+__device__ __forceinline__ double red_identity(int kind) { return kind == DISC_REDUCE_SUM ? 0.0 : -INFINITY; }
+__device__ __forceinline__ double red_step(int kind, double acc, double v) {
+  return kind == DISC_REDUCE_SUM ? acc + v : ((acc < v) ? v : acc);  // std::max(acc, v)
+}
+__device__ __forceinline__ double red_join(int kind, double a, double b) {
+  return kind == DISC_REDUCE_SUM ? a + b : ((a < b) ? b : a);
+}
+
 // Finalize split-R partials: ordered join over splits (two-pass) or cast (atomic).
 __global__ void k_col_finalize(const __grid_constant__ disc_reduce_launch L) {
   const int64_t n = L.K * L.C;
@@ -95,9 +103,7 @@ cudaError_t finalize_columns(const disc_reduce_launch& L, cudaStream_t s) {
 
 cudaError_t reduce(const disc_reduce_launch& L, cudaStream_t s) {
   if (L.schedule == DISC_SCHED_ROW) {
-    if (L.vec == 4)
-      return L.wide ? launch_row_with(k_row<4, true, Interp, Interp>, L, s) : launch_row_with(k_row<4, false, Interp, Interp>, L, s);
-    return L.wide ? launch_row_with(k_row<1, true, Interp, Interp>, L, s) : launch_row_with(k_row<1, false, Interp, Interp>, L, s);
+    return row_pass<Interp, Interp>(L, s, true);
   }
   if (L.schedule == DISC_SCHED_GENERIC) {
     if (L.K <= 0) return cudaSuccess;
@@ -113,9 +119,6 @@ cudaError_t reduce(const disc_reduce_launch& L, cudaStream_t s) {
   return col_pass(L, s);  // column schedules: the device layer adds memset/finalize
 }
 
-cudaError_t col_pass(const disc_reduce_launch& L, cudaStream_t s) {
-  if (L.vec == 4) return L.wide ? launch_col_with(k_col<4, true, Interp>, L, s) : launch_col_with(k_col<4, false, Interp>, L, s);
-  return L.wide ? launch_col_with(k_col<1, true, Interp>, L, s) : launch_col_with(k_col<1, false, Interp>, L, s);
-}
+cudaError_t col_pass(const disc_reduce_launch& L, cudaStream_t s) { return col_pass_t<Interp>(L, s, true); }
 
 }  // namespace disc_launch

@@ -6,6 +6,7 @@
 
 #include <cfloat>
 #include <cmath>
+#include <type_traits>
 
 #include "program.cuh"
 
@@ -19,6 +20,36 @@ struct Interp {
   }
 };
 
+
+// Reduction helpers.  Sums accumulate in f64 (the reference's semantics); max is exact in
+// f32 (max of f32 values cast to f64 == cast of the f32 max), with std::max's NaN rule.
+template <int KIND>
+struct Red {
+  using Acc = typename std::conditional<KIND == DISC_REDUCE_SUM, double, float>::type;
+  __device__ __forceinline__ static Acc identity() {
+    if constexpr (KIND == DISC_REDUCE_SUM) return 0.0;
+    else return -INFINITY;
+  }
+  __device__ __forceinline__ static Acc step(Acc acc, float v) {
+    if constexpr (KIND == DISC_REDUCE_SUM) return acc + static_cast<double>(v);
+    else return (acc < v) ? v : acc;  // std::max(acc, v)
+  }
+  __device__ __forceinline__ static Acc join(Acc a, Acc b) {
+    if constexpr (KIND == DISC_REDUCE_SUM) return a + b;
+    else return (a < b) ? b : a;  // partials never hold NaN
+  }
+  __device__ __forceinline__ static Acc acc(Acc a, float v) { return step(a, v); }
+  __device__ __forceinline__ static Acc acc(Acc a, float4 v) { return step(step(step(step(a, v.x), v.y), v.z), v.w); }
+};
+
+// Chunks of a tile inside the row: CH chunks spaced cstride apart starting at col0.
+template <int CH>
+__device__ __forceinline__ int chunks_in_row(int64_t left, int64_t cstride) {
+  int n = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) n += left > c * cstride;
+  return n;
+}
 
 constexpr int kLoopThreads = 256;
 constexpr int kCH = 2;  // chunks per thread per dispatch
@@ -44,49 +75,41 @@ __global__ void __launch_bounds__(kLoopThreads) k_loop(const __grid_constant__ d
   const int64_t tpr = (L.W + span - 1) / span;
   const int64_t ntiles = ((L.rows + rpw - 1) / rpw) * tpr;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t tile = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < ntiles;
-       tile += warps) {
-    const int64_t rg = tile / tpr;
+  int64_t tile = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // (row group, column tile) advanced incrementally: one division per thread, not per tile.
+  int64_t rg = tile / tpr, tc = tile - rg * tpr;
+  const int64_t drg = warps / tpr, dtc = warps - drg * tpr;
+  const int64_t lane_col = (lane & (lpr - 1)) * VEC;
+  for (; tile < ntiles; tile += warps) {
     TileCtx t;
     t.row = rg * rpw + sub;
-    t.col0 = (tile - rg * tpr) * span + (lane & (lpr - 1)) * VEC;
+    t.col0 = tc * span + lane_col;
     t.W = L.W;
     t.cstride = cstride;
-    const int64_t left = L.W - t.col0;
-    t.nvalid = (t.row >= L.rows || left <= 0)
-                   ? 0
-                   : static_cast<int>(left >= kCH * cstride ? kCH : (left + cstride - 1) / cstride);
+    t.nvalid = t.row >= L.rows ? 0 : chunks_in_row<kCH>(L.W - t.col0, cstride);
     T acc[kCH];
     Prog::template run<VEC, kCH, WIDE>(L.prog, t, acc, slots, kLoopThreads, consts, 0.f);
+    rg += drg;
+    tc += dtc;
+    if (tc >= tpr) {
+      tc -= tpr;
+      ++rg;
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
-// Reduction helpers (f64, insensitive to order within f64 rounding).
-__device__ __forceinline__ double red_identity(int kind) { return kind == DISC_REDUCE_SUM ? 0.0 : -INFINITY; }
-__device__ __forceinline__ double red_step(int kind, double acc, double v) {
-  return kind == DISC_REDUCE_SUM ? acc + v : ((acc < v) ? v : acc);  // std::max(acc, v)
-}
-__device__ __forceinline__ double red_join(int kind, double a, double b) {
-  return kind == DISC_REDUCE_SUM ? a + b : ((a < b) ? b : a);  // partials never hold NaN for max
-}
-__device__ __forceinline__ double red_accumulate(int kind, double acc, float v) { return red_step(kind, acc, (double)v); }
-__device__ __forceinline__ double red_accumulate(int kind, double acc, float4 v) {
-  acc = red_step(kind, acc, (double)v.x);
-  acc = red_step(kind, acc, (double)v.y);
-  acc = red_step(kind, acc, (double)v.z);
-  return red_step(kind, acc, (double)v.w);
-}
-
 // ---------------------------------------------------------------------------
 // Row schedule: reduce arg collapsed to [K rows, R]; G threads per row (power of two);
 // thread `lane` of a row takes chunks lane, lane+G, ... (coalesced across the group).
 // Optional fused epilogue (post program) re-evaluated per element with the row value.
-template <int VEC, bool WIDE, typename Pre, typename Post>
+template <int VEC, bool WIDE, int KIND, typename Pre, typename Post>
 __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduce_launch L) {
+  using RD = Red<KIND>;
+  using Acc = typename RD::Acc;
   using T = typename Vec<VEC>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ double warp_part[32];
+  __shared__ Acc warp_part[32];
   __shared__ float row_val[32];
   __shared__ float consts[2][DISC_MAX_LOADS];
   T* slots = reinterpret_cast<T*>(smem_raw) + threadIdx.x;
@@ -98,7 +121,6 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
   const int sub = threadIdx.x / G;
   const int rpb = blockDim.x / G;
   const int64_t rows = L.K;
-  const int kind = L.kind;
   const bool fuse_post = L.post.n_instr > 0;
   const int64_t cstride = static_cast<int64_t>(G) * VEC;
   const int64_t span = cstride * kCH;
@@ -106,21 +128,19 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
   for (int64_t base = static_cast<int64_t>(blockIdx.x) * rpb; base < rows; base += static_cast<int64_t>(gridDim.x) * rpb) {
     const int64_t row = base + sub;
     const bool valid = row < rows;
-    double acc = red_identity(kind);
+    Acc acc = RD::identity();
     if (valid) {
       for (int64_t col0 = static_cast<int64_t>(lane) * VEC; col0 < L.R; col0 += span) {
-        TileCtx t{row, col0, L.R, cstride, 0};
-        const int64_t left = L.R - col0;
-        t.nvalid = static_cast<int>(left >= kCH * cstride ? kCH : (left + cstride - 1) / cstride);
+        TileCtx t{row, col0, L.R, cstride, chunks_in_row<kCH>(L.R - col0, cstride)};
         T v[kCH];
         Pre::template run<VEC, kCH, WIDE>(L.pre, t, v, slots, blockDim.x, consts[0], 0.f);
 #pragma unroll
         for (int c = 0; c < kCH; ++c)
-          if (c < t.nvalid) acc = red_accumulate(kind, acc, v[c]);
+          if (c < t.nvalid) acc = RD::acc(acc, v[c]);
       }
     }
     const int width = G < 32 ? G : 32;
-    for (int o = width / 2; o > 0; o >>= 1) acc = red_join(kind, acc, __shfl_xor_sync(0xffffffffu, acc, o, width));
+    for (int o = width / 2; o > 0; o >>= 1) acc = RD::join(acc, __shfl_xor_sync(0xffffffffu, acc, o, width));
     float result;
     if (G <= 32) {
       result = static_cast<float>(acc);
@@ -130,8 +150,8 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
       __syncthreads();
       const int wpr = G >> 5;
       if (lane == 0) {
-        double s = warp_part[sub * wpr];
-        for (int w = 1; w < wpr; ++w) s = red_join(kind, s, warp_part[sub * wpr + w]);
+        Acc s = warp_part[sub * wpr];
+        for (int w = 1; w < wpr; ++w) s = RD::join(s, warp_part[sub * wpr + w]);
         row_val[sub] = static_cast<float>(s);
       }
       __syncthreads();
@@ -141,9 +161,7 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
       if (lane == 0 && L.red_out) L.red_out[row] = result;
       if (fuse_post) {
         for (int64_t col0 = static_cast<int64_t>(lane) * VEC; col0 < L.R; col0 += span) {
-          TileCtx t{row, col0, L.R, cstride, 0};
-          const int64_t left = L.R - col0;
-          t.nvalid = static_cast<int>(left >= kCH * cstride ? kCH : (left + cstride - 1) / cstride);
+          TileCtx t{row, col0, L.R, cstride, chunks_in_row<kCH>(L.R - col0, cstride)};
           T v[kCH];
           Post::template run<VEC, kCH, WIDE>(L.post, t, v, slots, blockDim.x, consts[1], result);
         }
@@ -159,17 +177,18 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
 // chunks strided by 32*VEC; grid.x = K * ceil(C / (32*CH*VEC)), grid.y = R splits.
 constexpr int kColX = 32, kColY = 8;
 
-template <int VEC, bool WIDE, typename Pre>
+template <int VEC, bool WIDE, int KIND, typename Pre>
 __global__ void __launch_bounds__(kColX* kColY) k_col(const __grid_constant__ disc_reduce_launch L) {
   using T = typename Vec<VEC>::T;
+  using RD = Red<KIND>;
+  using Acc = typename RD::Acc;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ double part[kColY][kColX][kCH * VEC];
+  __shared__ Acc part[kColY][kColX][kCH * VEC];
   __shared__ float consts[DISC_MAX_LOADS];
   const int tid = threadIdx.y * kColX + threadIdx.x;
   T* slots = reinterpret_cast<T*>(smem_raw) + tid;
   hoist_consts(L.pre, consts);
   __syncthreads();
-  const int kind = L.kind;
   const int64_t cstride = static_cast<int64_t>(kColX) * VEC;
   const int64_t span = cstride * kCH;
   const int64_t tiles = (L.C + span - 1) / span;
@@ -178,12 +197,11 @@ __global__ void __launch_bounds__(kColX* kColY) k_col(const __grid_constant__ di
   const int64_t per = (L.R + L.splits - 1) / L.splits;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * per;
   const int64_t r1 = r0 + per < L.R ? r0 + per : L.R;
-  const int64_t left = L.C - col0;
-  const int nvalid = left <= 0 ? 0 : static_cast<int>(left >= kCH * cstride ? kCH : (left + cstride - 1) / cstride);
+  const int nvalid = chunks_in_row<kCH>(L.C - col0, cstride);
 
-  double acc[kCH * VEC];
+  Acc acc[kCH * VEC];
 #pragma unroll
-  for (int i = 0; i < kCH * VEC; ++i) acc[i] = red_identity(kind);
+  for (int i = 0; i < kCH * VEC; ++i) acc[i] = RD::identity();
   if (nvalid > 0) {
     for (int64_t r = r0 + threadIdx.y; r < r1; r += kColY) {
       TileCtx t{k * L.R + r, col0, L.C, cstride, nvalid};
@@ -192,12 +210,12 @@ __global__ void __launch_bounds__(kColX* kColY) k_col(const __grid_constant__ di
 #pragma unroll
       for (int c = 0; c < kCH; ++c) {
         if constexpr (VEC == 1) {
-          acc[c] = red_step(kind, acc[c], (double)v[c]);
+          acc[c] = RD::step(acc[c], v[c]);
         } else {
-          acc[c * 4 + 0] = red_step(kind, acc[c * 4 + 0], (double)v[c].x);
-          acc[c * 4 + 1] = red_step(kind, acc[c * 4 + 1], (double)v[c].y);
-          acc[c * 4 + 2] = red_step(kind, acc[c * 4 + 2], (double)v[c].z);
-          acc[c * 4 + 3] = red_step(kind, acc[c * 4 + 3], (double)v[c].w);
+          acc[c * 4 + 0] = RD::step(acc[c * 4 + 0], v[c].x);
+          acc[c * 4 + 1] = RD::step(acc[c * 4 + 1], v[c].y);
+          acc[c * 4 + 2] = RD::step(acc[c * 4 + 2], v[c].z);
+          acc[c * 4 + 3] = RD::step(acc[c * 4 + 3], v[c].w);
         }
       }
     }
@@ -209,8 +227,8 @@ __global__ void __launch_bounds__(kColX* kColY) k_col(const __grid_constant__ di
     for (int c = 0; c < nvalid; ++c) {
 #pragma unroll
       for (int i = 0; i < VEC; ++i) {
-        double s = part[0][threadIdx.x][c * VEC + i];
-        for (int y = 1; y < kColY; ++y) s = red_join(kind, s, part[y][threadIdx.x][c * VEC + i]);
+        Acc s = part[0][threadIdx.x][c * VEC + i];
+        for (int y = 1; y < kColY; ++y) s = RD::join(s, part[y][threadIdx.x][c * VEC + i]);
         const int64_t o = k * L.C + col0 + c * cstride + i;
         switch (L.schedule) {
           case DISC_SCHED_COL_SINGLE:
@@ -220,7 +238,7 @@ __global__ void __launch_bounds__(kColX* kColY) k_col(const __grid_constant__ di
             L.workspace[static_cast<int64_t>(blockIdx.y) * L.K * L.C + o] = s;
             break;
           default:  // DISC_SCHED_COL_ATOMIC (sum only)
-            atomicAdd(L.workspace + o, s);
+            atomicAdd(L.workspace + o, static_cast<double>(s));
             break;
         }
       }
@@ -291,6 +309,37 @@ inline cudaError_t launch_col_with(K kernel, const disc_reduce_launch& L, cudaSt
   if (e != cudaSuccess) return e;
   kernel<<<grid, block, smem, s>>>(L);
   return cudaGetLastError();
+}
+
+// Dispatch on (vec, wide, reduce kind) for a given program functor pair.
+template <typename Pre, typename Post>
+inline cudaError_t row_pass(const disc_reduce_launch& L, cudaStream_t s, bool use_slots, bool allow_wide = true) {
+  const bool sum = L.kind == DISC_REDUCE_SUM;
+  if (L.wide && allow_wide) {
+    if (L.vec == 4) return sum ? launch_row_with(k_row<4, true, DISC_REDUCE_SUM, Pre, Post>, L, s, use_slots)
+                               : launch_row_with(k_row<4, true, DISC_REDUCE_MAX, Pre, Post>, L, s, use_slots);
+    return sum ? launch_row_with(k_row<1, true, DISC_REDUCE_SUM, Pre, Post>, L, s, use_slots)
+               : launch_row_with(k_row<1, true, DISC_REDUCE_MAX, Pre, Post>, L, s, use_slots);
+  }
+  if (L.vec == 4) return sum ? launch_row_with(k_row<4, false, DISC_REDUCE_SUM, Pre, Post>, L, s, use_slots)
+                             : launch_row_with(k_row<4, false, DISC_REDUCE_MAX, Pre, Post>, L, s, use_slots);
+  return sum ? launch_row_with(k_row<1, false, DISC_REDUCE_SUM, Pre, Post>, L, s, use_slots)
+             : launch_row_with(k_row<1, false, DISC_REDUCE_MAX, Pre, Post>, L, s, use_slots);
+}
+
+template <typename Pre>
+inline cudaError_t col_pass_t(const disc_reduce_launch& L, cudaStream_t s, bool use_slots, bool allow_wide = true) {
+  const bool sum = L.kind == DISC_REDUCE_SUM;
+  if (L.wide && allow_wide) {
+    if (L.vec == 4) return sum ? launch_col_with(k_col<4, true, DISC_REDUCE_SUM, Pre>, L, s, use_slots)
+                               : launch_col_with(k_col<4, true, DISC_REDUCE_MAX, Pre>, L, s, use_slots);
+    return sum ? launch_col_with(k_col<1, true, DISC_REDUCE_SUM, Pre>, L, s, use_slots)
+               : launch_col_with(k_col<1, true, DISC_REDUCE_MAX, Pre>, L, s, use_slots);
+  }
+  if (L.vec == 4) return sum ? launch_col_with(k_col<4, false, DISC_REDUCE_SUM, Pre>, L, s, use_slots)
+                             : launch_col_with(k_col<4, false, DISC_REDUCE_MAX, Pre>, L, s, use_slots);
+  return sum ? launch_col_with(k_col<1, false, DISC_REDUCE_SUM, Pre>, L, s, use_slots)
+             : launch_col_with(k_col<1, false, DISC_REDUCE_MAX, Pre>, L, s, use_slots);
 }
 
 }  // namespace disc_dev

@@ -860,8 +860,13 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& 
   R.post = post.prog;
 
   if (R.schedule == DISC_SCHED_ROW) {
+    // ~32 chunks per thread (a warp per row for R = 4096: no block barriers), widened
+    // when there are too few rows to fill the machine.
     const int64_t chunks = empty ? 0 : R.R / R.vec;
-    R.group = next_pow2((chunks + 3) / 4);
+    int g = next_pow2((chunks + 31) / 32);
+    const int64_t need = (int64_t{sm_count()} * 1024 + std::max<int64_t>(R.K, 1) - 1) / std::max<int64_t>(R.K, 1);
+    while (g < need && g < 1024 && int64_t{g} * 4 <= chunks) g <<= 1;
+    R.group = g;
     rep.schedule = post_fused ? "row_fused" : "row";
   } else if (R.schedule != DISC_SCHED_GENERIC) {
     if (!R.red_out) R.red_out = static_cast<float*>(scratch.alloc(nout * 4));

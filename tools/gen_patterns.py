@@ -21,7 +21,9 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-OUT = os.path.join(ROOT, "paper_2103_05288_b200", "csrc", "kernels", "patterns_gen.cu")
+KDIR = os.path.join(ROOT, "paper_2103_05288_b200", "csrc", "kernels")
+OUT = os.path.join(KDIR, "patterns_gen.cu")  # registry; kernels in patterns_gen_<k>.cu shards
+SHARDS = 6
 
 I_LOAD_CONST, I_REDVAL, I_COPY, I_BIN, I_UN = 3, 4, 5, 8, 28
 
@@ -106,13 +108,16 @@ def gen_program(fn, prog):
 
 
 def generate():
+    """Returns {path: text} for the registry and the kernel shards."""
     seen = collect()
-    parts = ["// GENERATED by tools/gen_patterns.py -- do not edit.",
-             "// Straight-line fused programs for the pattern library (fixtures + BASELINE configs C1-C4);",
-             "// see the generator's docstring.  Source patterns per entry are noted in comments.",
-             '#include "kernels.cuh"', "", "namespace disc_gen {", "using namespace disc_dev;", ""]
+    header = ["// GENERATED by tools/gen_patterns.py -- do not edit.",
+              "// Straight-line fused programs for the pattern library (fixtures + BASELINE configs C1-C4);",
+              "// see the generator's docstring.  Source patterns per entry are noted in comments."]
+    shards = [header + ['#include "kernels.cuh"', "", "namespace disc_gen {", "using namespace disc_dev;", ""]
+              for _ in range(SHARDS)]
     entries = []
-    for (kind, key), (rec, src_name) in sorted(seen.items()):
+    for n, ((kind, key), (rec, src_name)) in enumerate(sorted(seen.items())):
+        parts = shards[n % SHARDS]
         tag = f"{kind}_{key}"
         parts.append(f"// {kind} {key} from {src_name}")
         parts.append(gen_program(f"Pre_{tag}", rec["pre"]))
@@ -125,46 +130,46 @@ def generate():
                          f" : launch_loop_with(k_loop<1, false, Pre_{tag}>, L, s, false);")
         elif kind == "row":
             parts.append("  const auto& L = *static_cast<const disc_reduce_launch*>(l);")
-            parts.append(f"  return vec == 4 ? launch_row_with(k_row<4, false, Pre_{tag}, Post_{tag}>, L, s, false)"
-                         f" : launch_row_with(k_row<1, false, Pre_{tag}, Post_{tag}>, L, s, false);")
+            parts.append(f"  return row_pass<Pre_{tag}, Post_{tag}>(L, s, false, false);")
         else:
             parts.append("  const auto& L = *static_cast<const disc_reduce_launch*>(l);")
-            parts.append(f"  return vec == 4 ? launch_col_with(k_col<4, false, Pre_{tag}>, L, s, false)"
-                         f" : launch_col_with(k_col<1, false, Pre_{tag}>, L, s, false);")
+            parts.append(f"  return col_pass_t<Pre_{tag}>(L, s, false, false);")
         parts.append("}")
         parts.append("")
         entries.append((["loop", "row", "col"].index(kind), key, f"launch_{tag}"))
-    parts.append("}  // namespace disc_gen")
-    parts.append("")
-    parts.append("namespace disc_spec {")
-    parts.append("struct Entry {\n  int kind;\n  uint64_t key;\n"
-                 "  cudaError_t (*launch)(const void* launch, int vec, cudaStream_t s);\n};")
-    parts.append("static const Entry kEntries[] = {")
+    files = {}
+    for k, parts in enumerate(shards):
+        files[os.path.join(KDIR, f"patterns_gen_{k}.cu")] = "\n".join(parts + ["}  // namespace disc_gen", ""])
+    reg = header + ["#include <cstdint>", "", "#include <cuda_runtime.h>", "", "namespace disc_gen {"]
+    for _, _, fn in sorted(entries):
+        reg.append(f"cudaError_t {fn}(const void* l, int vec, cudaStream_t s);")
+    reg += ["}  // namespace disc_gen", "", "namespace disc_spec {",
+            "struct Entry {\n  int kind;\n  uint64_t key;\n"
+            "  cudaError_t (*launch)(const void* launch, int vec, cudaStream_t s);\n};",
+            "static const Entry kEntries[] = {"]
     for kind, key, fn in sorted(entries):
-        parts.append(f"    {{{kind}, 0x{key}ull, disc_gen::{fn}}},")
-    parts.append("};")
-    parts.append("const Entry* lookup(int kind, uint64_t key) {")
-    parts.append("  for (const Entry& e : kEntries)")
-    parts.append("    if (e.kind == kind && e.key == key) return &e;")
-    parts.append("  return nullptr;")
-    parts.append("}")
-    parts.append(f"int count() {{ return {len(entries)}; }}")
-    parts.append("}  // namespace disc_spec")
-    return "\n".join(parts) + "\n", len(entries)
+        reg.append(f"    {{{kind}, 0x{key}ull, disc_gen::{fn}}},")
+    reg += ["};", "const Entry* lookup(int kind, uint64_t key) {", "  for (const Entry& e : kEntries)",
+            "    if (e.kind == kind && e.key == key) return &e;", "  return nullptr;", "}",
+            f"int count() {{ return {len(entries)}; }}", "}  // namespace disc_spec", ""]
+    files[OUT] = "\n".join(reg)
+    return files, len(entries)
 
 
 def main():
-    text, n = generate()
+    files, n = generate()
     if "--check" in sys.argv:
-        cur = open(OUT).read() if os.path.exists(OUT) else ""
-        if cur != text:
-            print("patterns_gen.cu is stale: run python tools/gen_patterns.py")
-            sys.exit(1)
-        print(f"patterns_gen.cu up to date ({n} patterns)")
+        for path, text in files.items():
+            cur = open(path).read() if os.path.exists(path) else ""
+            if cur != text:
+                print(f"{os.path.basename(path)} is stale: run python tools/gen_patterns.py")
+                sys.exit(1)
+        print(f"generated patterns up to date ({n} patterns)")
         return
-    with open(OUT, "w") as f:
-        f.write(text)
-    print(f"wrote {OUT}: {n} patterns")
+    for path, text in files.items():
+        with open(path, "w") as f:
+            f.write(text)
+    print(f"wrote {len(files)} files: {n} patterns")
 
 
 if __name__ == "__main__":
