@@ -59,7 +59,7 @@ constexpr int kCH = 2;  // chunks per thread per dispatch
 // columns: lpr lanes share a row (lane l takes chunks l, l+lpr, ... so every access is
 // coalesced), narrow rows pack several per warp.  Grid-stride over warp tiles.
 template <int VEC, bool WIDE, typename Prog>
-__global__ void __launch_bounds__(kLoopThreads) k_loop(const __grid_constant__ disc_loop_launch L) {
+__global__ void __launch_bounds__(kLoopThreads, 4) k_loop(const __grid_constant__ disc_loop_launch L) {
   using T = typename Vec<VEC>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ float consts[DISC_MAX_LOADS];
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
 constexpr int kColX = 32, kColY = 8;
 
 template <int VEC, bool WIDE, int KIND, typename Pre>
-__global__ void __launch_bounds__(kColX* kColY) k_col(const __grid_constant__ disc_reduce_launch L) {
+__global__ void __launch_bounds__(kColX* kColY, 4) k_col(const __grid_constant__ disc_reduce_launch L) {
   using T = typename Vec<VEC>::T;
   using RD = Red<KIND>;
   using Acc = typename RD::Acc;
