@@ -84,11 +84,20 @@ typedef struct {
   uint32_t shift[DISC_MAX_RANK];
 } disc_load;
 
+/* Row cache (row schedule with a fused epilogue): contiguous loads shared by the reduce
+ * pass and the epilogue are kept in shared memory.  cache_mode 1: the pre program also
+ * writes the loaded tile to cache slot cache_slot[l]; 2: the post program reads it from
+ * there instead of global memory. */
+enum disc_cache_mode { DISC_CACHE_NONE = 0, DISC_CACHE_FILL = 1, DISC_CACHE_READ = 2 };
+
 typedef struct {
   int32_t n_instr;
   int32_t n_slots;
   int32_t n_loads;
   int32_t n_outs;
+  int32_t cache_mode;
+  int8_t cache_slot[DISC_MAX_LOADS];
+  int32_t pad;
   disc_instr code[DISC_MAX_INSTR];
   disc_load loads[DISC_MAX_LOADS];
   float* outs[DISC_MAX_OUTS];
@@ -127,6 +136,8 @@ typedef struct {
   int32_t wide;
   int32_t group;            /* ROW: threads per row (power of two) */
   int32_t splits;           /* COL: number of R splits */
+  int32_t cache_loads;      /* ROW: number of row-cache slots (0 = no cache) */
+  int32_t pad1;
   float* red_out;           /* f32 reduce result [K*C] */
   double* workspace;        /* COL two-pass/atomic: f64 [splits or 1][K*C] */
   /* GENERIC: arg dims and reduced-axis mask */

@@ -21,8 +21,17 @@ __global__ void k_col_finalize(const __grid_constant__ disc_reduce_launch L) {
   for (int64_t o = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; o < n;
        o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     double t = L.workspace[o];
-    if (L.schedule == DISC_SCHED_COL_TWOPASS)
-      for (int s = 1; s < L.splits; ++s) t = red_join(L.kind, t, L.workspace[static_cast<int64_t>(s) * n + o]);
+    if (L.schedule == DISC_SCHED_COL_TWOPASS) {
+      // Fixed split order; eight partials loaded ahead of each join.
+      for (int s0 = 1; s0 < L.splits; s0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = s0 + u < L.splits ? L.workspace[static_cast<int64_t>(s0 + u) * n + o] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (s0 + u < L.splits) t = red_join(L.kind, t, v[u]);
+      }
+    }
     L.red_out[o] = static_cast<float>(t);
   }
 }

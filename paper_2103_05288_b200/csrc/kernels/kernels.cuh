@@ -58,7 +58,7 @@ constexpr int kCH = 2;  // chunks per thread per dispatch
 // kLoop: the space viewed as [rows, W].  A warp tile covers 32/lpr rows x (lpr*CH*VEC)
 // columns: lpr lanes share a row (lane l takes chunks l, l+lpr, ... so every access is
 // coalesced), narrow rows pack several per warp.  Grid-stride over warp tiles.
-template <int VEC, bool WIDE, typename Prog>
+template <int VEC, bool WIDE, typename Prog, int CH = kCH>
 __global__ void __launch_bounds__(kLoopThreads, 4) k_loop(const __grid_constant__ disc_loop_launch L) {
   using T = typename Vec<VEC>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kLoopThreads, 4) k_loop(const __grid_constant_
   const int rpw = 32 / lpr;
   const int sub = lane / lpr;
   const int64_t cstride = static_cast<int64_t>(lpr) * VEC;
-  const int64_t span = cstride * kCH;
+  const int64_t span = cstride * CH;
   const int64_t tpr = (L.W + span - 1) / span;
   const int64_t ntiles = ((L.rows + rpw - 1) / rpw) * tpr;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
@@ -86,9 +86,9 @@ __global__ void __launch_bounds__(kLoopThreads, 4) k_loop(const __grid_constant_
     t.col0 = tc * span + lane_col;
     t.W = L.W;
     t.cstride = cstride;
-    t.nvalid = t.row >= L.rows ? 0 : chunks_in_row<kCH>(L.W - t.col0, cstride);
-    T acc[kCH];
-    Prog::template run<VEC, kCH, WIDE>(L.prog, t, acc, slots, kLoopThreads, consts, 0.f);
+    t.nvalid = t.row >= L.rows ? 0 : chunks_in_row<CH>(L.W - t.col0, cstride);
+    T acc[CH];
+    Prog::template run<VEC, CH, WIDE>(L.prog, t, acc, slots, kLoopThreads, consts, 0.f);
     rg += drg;
     tc += dtc;
     if (tc >= tpr) {
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kLoopThreads, 4) k_loop(const __grid_constant_
 // Row schedule: reduce arg collapsed to [K rows, R]; G threads per row (power of two);
 // thread `lane` of a row takes chunks lane, lane+G, ... (coalesced across the group).
 // Optional fused epilogue (post program) re-evaluated per element with the row value.
-template <int VEC, bool WIDE, int KIND, typename Pre, typename Post>
+template <int VEC, bool WIDE, int KIND, typename Pre, typename Post, int CH = kCH>
 __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduce_launch L) {
   using RD = Red<KIND>;
   using Acc = typename RD::Acc;
@@ -112,18 +112,21 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
   __shared__ Acc warp_part[32];
   __shared__ float row_val[32];
   __shared__ float consts[2][DISC_MAX_LOADS];
-  T* slots = reinterpret_cast<T*>(smem_raw) + threadIdx.x;
-  hoist_consts(L.pre, consts[0]);
-  hoist_consts(L.post, consts[1]);
-  __syncthreads();
   const int G = L.group;
   const int lane = threadIdx.x & (G - 1);
   const int sub = threadIdx.x / G;
   const int rpb = blockDim.x / G;
+  // Dynamic smem: [row cache: rpb x cache_loads x R floats][interpreter slots].
+  const int64_t cache_floats = (static_cast<int64_t>(rpb) * L.cache_loads * L.R + 3) / 4 * 4;
+  float* row_cache = L.cache_loads ? reinterpret_cast<float*>(smem_raw) + sub * L.cache_loads * L.R : nullptr;
+  T* slots = reinterpret_cast<T*>(reinterpret_cast<float*>(smem_raw) + cache_floats) + threadIdx.x;
+  hoist_consts(L.pre, consts[0]);
+  hoist_consts(L.post, consts[1]);
+  __syncthreads();
   const int64_t rows = L.K;
   const bool fuse_post = L.post.n_instr > 0;
   const int64_t cstride = static_cast<int64_t>(G) * VEC;
-  const int64_t span = cstride * kCH;
+  const int64_t span = cstride * CH;
 
   for (int64_t base = static_cast<int64_t>(blockIdx.x) * rpb; base < rows; base += static_cast<int64_t>(gridDim.x) * rpb) {
     const int64_t row = base + sub;
@@ -131,11 +134,11 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
     Acc acc = RD::identity();
     if (valid) {
       for (int64_t col0 = static_cast<int64_t>(lane) * VEC; col0 < L.R; col0 += span) {
-        TileCtx t{row, col0, L.R, cstride, chunks_in_row<kCH>(L.R - col0, cstride)};
-        T v[kCH];
-        Pre::template run<VEC, kCH, WIDE>(L.pre, t, v, slots, blockDim.x, consts[0], 0.f);
+        TileCtx t{row, col0, L.R, cstride, chunks_in_row<CH>(L.R - col0, cstride), row_cache};
+        T v[CH];
+        Pre::template run<VEC, CH, WIDE>(L.pre, t, v, slots, blockDim.x, consts[0], 0.f);
 #pragma unroll
-        for (int c = 0; c < kCH; ++c)
+        for (int c = 0; c < CH; ++c)
           if (c < t.nvalid) acc = RD::acc(acc, v[c]);
       }
     }
@@ -161,9 +164,9 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
       if (lane == 0 && L.red_out) L.red_out[row] = result;
       if (fuse_post) {
         for (int64_t col0 = static_cast<int64_t>(lane) * VEC; col0 < L.R; col0 += span) {
-          TileCtx t{row, col0, L.R, cstride, chunks_in_row<kCH>(L.R - col0, cstride)};
-          T v[kCH];
-          Post::template run<VEC, kCH, WIDE>(L.post, t, v, slots, blockDim.x, consts[1], result);
+          TileCtx t{row, col0, L.R, cstride, chunks_in_row<CH>(L.R - col0, cstride), row_cache};
+          T v[CH];
+          Post::template run<VEC, CH, WIDE>(L.post, t, v, slots, blockDim.x, consts[1], result);
         }
       }
     }
@@ -173,42 +176,50 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
 
 // ---------------------------------------------------------------------------
 // Column schedule: reduce arg collapsed to [K, R, C], reduce over R, C contiguous; viewed
-// as rows k*R + r of width C.  Block = 32 (along C) x 8 (along R); a thread owns CH
-// chunks strided by 32*VEC; grid.x = K * ceil(C / (32*CH*VEC)), grid.y = R splits.
-constexpr int kColX = 32, kColY = 8;
+// as rows k*R + r of width C.  A warp spans 32/lpc rows x (lpc*CH*VEC) columns (lpc =
+// L.group lanes per row segment, so narrow C packs many rows per warp); 8 warps per
+// block; grid.x = K * ceil(C / span), grid.y = R splits.  Per-thread partials are joined
+// per column through shared memory in a fixed order.
+constexpr int kColThreads = 256;
 
-template <int VEC, bool WIDE, int KIND, typename Pre>
-__global__ void __launch_bounds__(kColX* kColY, 4) k_col(const __grid_constant__ disc_reduce_launch L) {
+template <int VEC, bool WIDE, int KIND, typename Pre, int CH = kCH>
+__global__ void __launch_bounds__(kColThreads, 4) k_col(const __grid_constant__ disc_reduce_launch L) {
   using T = typename Vec<VEC>::T;
   using RD = Red<KIND>;
   using Acc = typename RD::Acc;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ Acc part[kColY][kColX][kCH * VEC];
+  __shared__ Acc part[kColThreads][CH * VEC];
   __shared__ float consts[DISC_MAX_LOADS];
-  const int tid = threadIdx.y * kColX + threadIdx.x;
+  const int tid = threadIdx.x;
   T* slots = reinterpret_cast<T*>(smem_raw) + tid;
   hoist_consts(L.pre, consts);
   __syncthreads();
-  const int64_t cstride = static_cast<int64_t>(kColX) * VEC;
-  const int64_t span = cstride * kCH;
+  const int lpc = L.group;
+  const int rpw = 32 / lpc;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int sub = lane / lpc, lc = lane & (lpc - 1);
+  const int rows_per_pass = (kColThreads / 32) * rpw;
+  const int64_t cstride = static_cast<int64_t>(lpc) * VEC;
+  const int64_t span = cstride * CH;
   const int64_t tiles = (L.C + span - 1) / span;
   const int64_t k = blockIdx.x / tiles;
-  const int64_t col0 = (blockIdx.x % tiles) * span + threadIdx.x * VEC;
+  const int64_t tile0 = (blockIdx.x - k * tiles) * span;
+  const int64_t col0 = tile0 + lc * VEC;
   const int64_t per = (L.R + L.splits - 1) / L.splits;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * per;
   const int64_t r1 = r0 + per < L.R ? r0 + per : L.R;
-  const int nvalid = chunks_in_row<kCH>(L.C - col0, cstride);
+  const int nvalid = chunks_in_row<CH>(L.C - col0, cstride);
 
-  Acc acc[kCH * VEC];
+  Acc acc[CH * VEC];
 #pragma unroll
-  for (int i = 0; i < kCH * VEC; ++i) acc[i] = RD::identity();
+  for (int i = 0; i < CH * VEC; ++i) acc[i] = RD::identity();
   if (nvalid > 0) {
-    for (int64_t r = r0 + threadIdx.y; r < r1; r += kColY) {
+    for (int64_t r = r0 + warp * rpw + sub; r < r1; r += rows_per_pass) {
       TileCtx t{k * L.R + r, col0, L.C, cstride, nvalid};
-      T v[kCH];
-      Pre::template run<VEC, kCH, WIDE>(L.pre, t, v, slots, kColX * kColY, consts, 0.f);
+      T v[CH];
+      Pre::template run<VEC, CH, WIDE>(L.pre, t, v, slots, kColThreads, consts, 0.f);
 #pragma unroll
-      for (int c = 0; c < kCH; ++c) {
+      for (int c = 0; c < CH; ++c) {
         if constexpr (VEC == 1) {
           acc[c] = RD::step(acc[c], v[c]);
         } else {
@@ -221,27 +232,28 @@ __global__ void __launch_bounds__(kColX* kColY, 4) k_col(const __grid_constant__
     }
   }
 #pragma unroll
-  for (int i = 0; i < kCH * VEC; ++i) part[threadIdx.y][threadIdx.x][i] = acc[i];
+  for (int i = 0; i < CH * VEC; ++i) part[tid][i] = acc[i];
   __syncthreads();
-  if (threadIdx.y == 0) {
-    for (int c = 0; c < nvalid; ++c) {
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) {
-        Acc s = part[0][threadIdx.x][c * VEC + i];
-        for (int y = 1; y < kColY; ++y) s = RD::join(s, part[y][threadIdx.x][c * VEC + i]);
-        const int64_t o = k * L.C + col0 + c * cstride + i;
-        switch (L.schedule) {
-          case DISC_SCHED_COL_SINGLE:
-            if (L.red_out) L.red_out[o] = static_cast<float>(s);
-            break;
-          case DISC_SCHED_COL_TWOPASS:
-            L.workspace[static_cast<int64_t>(blockIdx.y) * L.K * L.C + o] = s;
-            break;
-          default:  // DISC_SCHED_COL_ATOMIC (sum only)
-            atomicAdd(L.workspace + o, static_cast<double>(s));
-            break;
-        }
-      }
+  // Column j of the tile: chunk c = (j/VEC)/lpc, lane lc = (j/VEC)%lpc, element j%VEC.
+  for (int j = tid; j < span; j += kColThreads) {
+    const int64_t col = tile0 + j;
+    if (col >= L.C) continue;
+    const int q = j / VEC, e = j % VEC;
+    const int jl = q % lpc, jc = q / lpc;
+    Acc s = RD::identity();
+    for (int w = 0; w < kColThreads / 32; ++w)
+      for (int u = 0; u < rpw; ++u) s = RD::join(s, part[w * 32 + u * lpc + jl][jc * VEC + e]);
+    const int64_t o = k * L.C + col;
+    switch (L.schedule) {
+      case DISC_SCHED_COL_SINGLE:
+        if (L.red_out) L.red_out[o] = static_cast<float>(s);
+        break;
+      case DISC_SCHED_COL_TWOPASS:
+        L.workspace[static_cast<int64_t>(blockIdx.y) * L.K * L.C + o] = static_cast<double>(s);
+        break;
+      default:  // DISC_SCHED_COL_ATOMIC (sum only)
+        atomicAdd(L.workspace + o, static_cast<double>(s));
+        break;
     }
   }
 }
@@ -264,24 +276,24 @@ inline cudaError_t set_smem(K kernel, size_t bytes) {
 }
 
 // use_slots = false for generated programs (values live in registers, no slot smem).
-template <typename K>
+template <int CH = kCH, typename K>
 inline cudaError_t launch_loop_with(K kernel, const disc_loop_launch& L, cudaStream_t s, bool use_slots = true) {
   if (L.total <= 0) return cudaSuccess;
-  const int64_t span = static_cast<int64_t>(L.lpr) * kCH * L.vec;
+  const int64_t span = static_cast<int64_t>(L.lpr) * CH * L.vec;
   const int64_t rpw = 32 / L.lpr;
   const int64_t tiles = ((L.rows + rpw - 1) / rpw) * ((L.W + span - 1) / span);
   const int64_t warps_per_block = kLoopThreads / 32;
   const int64_t want = (tiles + warps_per_block - 1) / warps_per_block;
   const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
   const int grid = static_cast<int>(want < cap ? want : cap);
-  const size_t smem = use_slots ? static_cast<size_t>(L.prog.n_slots) * kCH * kLoopThreads * (L.vec == 4 ? 16 : 4) : 0;
+  const size_t smem = use_slots ? static_cast<size_t>(L.prog.n_slots) * CH * kLoopThreads * (L.vec == 4 ? 16 : 4) : 0;
   cudaError_t e = set_smem(kernel, smem);
   if (e != cudaSuccess) return e;
   kernel<<<grid, kLoopThreads, smem, s>>>(L);
   return cudaGetLastError();
 }
 
-template <typename K>
+template <int CH = kCH, typename K>
 inline cudaError_t launch_row_with(K kernel, const disc_reduce_launch& L, cudaStream_t s, bool use_slots = true) {
   if (L.K <= 0) return cudaSuccess;
   const int slots = L.pre.n_slots > L.post.n_slots ? L.pre.n_slots : L.post.n_slots;
@@ -290,7 +302,8 @@ inline cudaError_t launch_row_with(K kernel, const disc_reduce_launch& L, cudaSt
   const int64_t groups = (L.K + rpb - 1) / rpb;
   const int64_t cap = static_cast<int64_t>(sm_count()) * (2048 / block) * 2;
   const int grid = static_cast<int>(groups < cap ? groups : cap);
-  const size_t smem = use_slots ? static_cast<size_t>(slots) * kCH * block * (L.vec == 4 ? 16 : 4) : 0;
+  const size_t cache = static_cast<size_t>((static_cast<int64_t>(rpb) * L.cache_loads * L.R + 3) / 4 * 4) * 4;
+  const size_t smem = cache + (use_slots ? static_cast<size_t>(slots) * CH * block * (L.vec == 4 ? 16 : 4) : 0);
   cudaError_t e = set_smem(kernel, smem);
   if (e != cudaSuccess) return e;
   kernel<<<grid, block, smem, s>>>(L);
@@ -298,48 +311,47 @@ inline cudaError_t launch_row_with(K kernel, const disc_reduce_launch& L, cudaSt
 }
 
 // Column pass only (the finalize kernel is launched by the caller).
-template <typename K>
+template <int CH = kCH, typename K>
 inline cudaError_t launch_col_with(K kernel, const disc_reduce_launch& L, cudaStream_t s, bool use_slots = true) {
-  const int64_t span = static_cast<int64_t>(kColX) * kCH * L.vec;
+  const int64_t span = static_cast<int64_t>(L.group) * CH * L.vec;
   const int64_t tiles = (L.C + span - 1) / span;
   dim3 grid(static_cast<unsigned>(L.K * tiles), static_cast<unsigned>(L.splits));
-  dim3 block(kColX, kColY);
-  const size_t smem = use_slots ? static_cast<size_t>(L.pre.n_slots) * kCH * kColX * kColY * (L.vec == 4 ? 16 : 4) : 0;
+  const size_t smem = use_slots ? static_cast<size_t>(L.pre.n_slots) * CH * kColThreads * (L.vec == 4 ? 16 : 4) : 0;
   cudaError_t e = set_smem(kernel, smem);
   if (e != cudaSuccess) return e;
-  kernel<<<grid, block, smem, s>>>(L);
+  kernel<<<grid, kColThreads, smem, s>>>(L);
   return cudaGetLastError();
 }
 
 // Dispatch on (vec, wide, reduce kind) for a given program functor pair.
-template <typename Pre, typename Post>
+template <typename Pre, typename Post, int CH = kCH>
 inline cudaError_t row_pass(const disc_reduce_launch& L, cudaStream_t s, bool use_slots, bool allow_wide = true) {
   const bool sum = L.kind == DISC_REDUCE_SUM;
   if (L.wide && allow_wide) {
-    if (L.vec == 4) return sum ? launch_row_with(k_row<4, true, DISC_REDUCE_SUM, Pre, Post>, L, s, use_slots)
-                               : launch_row_with(k_row<4, true, DISC_REDUCE_MAX, Pre, Post>, L, s, use_slots);
-    return sum ? launch_row_with(k_row<1, true, DISC_REDUCE_SUM, Pre, Post>, L, s, use_slots)
-               : launch_row_with(k_row<1, true, DISC_REDUCE_MAX, Pre, Post>, L, s, use_slots);
+    if (L.vec == 4) return sum ? launch_row_with<CH>(k_row<4, true, DISC_REDUCE_SUM, Pre, Post, CH>, L, s, use_slots)
+                               : launch_row_with<CH>(k_row<4, true, DISC_REDUCE_MAX, Pre, Post, CH>, L, s, use_slots);
+    return sum ? launch_row_with<CH>(k_row<1, true, DISC_REDUCE_SUM, Pre, Post, CH>, L, s, use_slots)
+               : launch_row_with<CH>(k_row<1, true, DISC_REDUCE_MAX, Pre, Post, CH>, L, s, use_slots);
   }
-  if (L.vec == 4) return sum ? launch_row_with(k_row<4, false, DISC_REDUCE_SUM, Pre, Post>, L, s, use_slots)
-                             : launch_row_with(k_row<4, false, DISC_REDUCE_MAX, Pre, Post>, L, s, use_slots);
-  return sum ? launch_row_with(k_row<1, false, DISC_REDUCE_SUM, Pre, Post>, L, s, use_slots)
-             : launch_row_with(k_row<1, false, DISC_REDUCE_MAX, Pre, Post>, L, s, use_slots);
+  if (L.vec == 4) return sum ? launch_row_with<CH>(k_row<4, false, DISC_REDUCE_SUM, Pre, Post, CH>, L, s, use_slots)
+                             : launch_row_with<CH>(k_row<4, false, DISC_REDUCE_MAX, Pre, Post, CH>, L, s, use_slots);
+  return sum ? launch_row_with<CH>(k_row<1, false, DISC_REDUCE_SUM, Pre, Post, CH>, L, s, use_slots)
+             : launch_row_with<CH>(k_row<1, false, DISC_REDUCE_MAX, Pre, Post, CH>, L, s, use_slots);
 }
 
-template <typename Pre>
+template <typename Pre, int CH = kCH>
 inline cudaError_t col_pass_t(const disc_reduce_launch& L, cudaStream_t s, bool use_slots, bool allow_wide = true) {
   const bool sum = L.kind == DISC_REDUCE_SUM;
   if (L.wide && allow_wide) {
-    if (L.vec == 4) return sum ? launch_col_with(k_col<4, true, DISC_REDUCE_SUM, Pre>, L, s, use_slots)
-                               : launch_col_with(k_col<4, true, DISC_REDUCE_MAX, Pre>, L, s, use_slots);
-    return sum ? launch_col_with(k_col<1, true, DISC_REDUCE_SUM, Pre>, L, s, use_slots)
-               : launch_col_with(k_col<1, true, DISC_REDUCE_MAX, Pre>, L, s, use_slots);
+    if (L.vec == 4) return sum ? launch_col_with<CH>(k_col<4, true, DISC_REDUCE_SUM, Pre, CH>, L, s, use_slots)
+                               : launch_col_with<CH>(k_col<4, true, DISC_REDUCE_MAX, Pre, CH>, L, s, use_slots);
+    return sum ? launch_col_with<CH>(k_col<1, true, DISC_REDUCE_SUM, Pre, CH>, L, s, use_slots)
+               : launch_col_with<CH>(k_col<1, true, DISC_REDUCE_MAX, Pre, CH>, L, s, use_slots);
   }
-  if (L.vec == 4) return sum ? launch_col_with(k_col<4, false, DISC_REDUCE_SUM, Pre>, L, s, use_slots)
-                             : launch_col_with(k_col<4, false, DISC_REDUCE_MAX, Pre>, L, s, use_slots);
-  return sum ? launch_col_with(k_col<1, false, DISC_REDUCE_SUM, Pre>, L, s, use_slots)
-             : launch_col_with(k_col<1, false, DISC_REDUCE_MAX, Pre>, L, s, use_slots);
+  if (L.vec == 4) return sum ? launch_col_with<CH>(k_col<4, false, DISC_REDUCE_SUM, Pre, CH>, L, s, use_slots)
+                             : launch_col_with<CH>(k_col<4, false, DISC_REDUCE_MAX, Pre, CH>, L, s, use_slots);
+  return sum ? launch_col_with<CH>(k_col<1, false, DISC_REDUCE_SUM, Pre, CH>, L, s, use_slots)
+             : launch_col_with<CH>(k_col<1, false, DISC_REDUCE_MAX, Pre, CH>, L, s, use_slots);
 }
 
 }  // namespace disc_dev

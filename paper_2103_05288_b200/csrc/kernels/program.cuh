@@ -97,8 +97,37 @@ struct TileCtx {
   int64_t col0;
   int64_t W;
   int64_t cstride;
-  int nvalid;  // leading chunks inside the row
+  int nvalid;           // leading chunks inside the row
+  float* cache = nullptr;  // row cache of this row (slot k at cache + k*W), or null
 };
+
+// Row cache: fill on the reduce pass, read on the epilogue (see disc_cache_mode).
+template <int VEC, int CH>
+__device__ __forceinline__ bool cached_load(const disc_program& P, const TileCtx& t, int l,
+                                            typename Vec<VEC>::T (&v)[CH]) {
+  if (P.cache_mode != DISC_CACHE_READ || P.cache_slot[l] < 0 || !t.cache) return false;
+  const float* c0 = t.cache + P.cache_slot[l] * t.W + t.col0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c)
+    if (c < t.nvalid) {
+      if constexpr (VEC == 1) v[c] = c0[c * t.cstride];
+      else v[c] = *reinterpret_cast<const float4*>(c0 + c * t.cstride);
+    }
+  return true;
+}
+
+template <int VEC, int CH>
+__device__ __forceinline__ void cache_fill(const disc_program& P, const TileCtx& t, int l,
+                                           const typename Vec<VEC>::T (&v)[CH]) {
+  if (P.cache_mode != DISC_CACHE_FILL || P.cache_slot[l] < 0 || !t.cache) return;
+  float* c0 = t.cache + P.cache_slot[l] * t.W + t.col0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c)
+    if (c < t.nvalid) {
+      if constexpr (VEC == 1) c0[c * t.cstride] = v[c];
+      else *reinterpret_cast<float4*>(c0 + c * t.cstride) = v[c];
+    }
+}
 
 template <int VEC>
 __device__ __forceinline__ typename Vec<VEC>::T load_row(const disc_load& L, const float* base, int64_t col) {
@@ -143,11 +172,13 @@ __device__ __forceinline__ void hoist_consts(const disc_program& P, float* const
 
 // One load of a tile, dispatched on the load's binding mode (warp-uniform branch).
 template <int VEC, int CH, bool WIDE>
-__device__ __forceinline__ void load_any(const disc_load& L, const TileCtx& t, const float* consts, int l,
+__device__ __forceinline__ void load_any(const disc_program& P, const TileCtx& t, const float* consts, int l,
                                          typename Vec<VEC>::T (&v)[CH]) {
+  const disc_load& L = P.loads[l];
   const int64_t f0 = t.row * t.W + t.col0;
   switch (L.mode) {
     case DISC_LOAD_IDENTITY: {
+      if (cached_load<VEC, CH>(P, t, l, v)) break;
       const float* base = L.ptr + f0;
 #pragma unroll
       for (int c = 0; c < CH; ++c)
@@ -155,6 +186,7 @@ __device__ __forceinline__ void load_any(const disc_load& L, const TileCtx& t, c
           if constexpr (VEC == 1) v[c] = ldg(base + c * t.cstride);
           else v[c] = __ldg(reinterpret_cast<const float4*>(base + c * t.cstride));
         }
+      cache_fill<VEC, CH>(P, t, l, v);
       break;
     }
     case DISC_LOAD_AFFINE: {
@@ -211,11 +243,13 @@ __device__ __forceinline__ void run_tile(const disc_program& P, const TileCtx& t
     const disc_instr in = P.code[pc];
     switch (in.op) {
       case DISC_I_LOAD_ID: {
+        if (cached_load<VEC, CH>(P, t, in.load, acc)) break;
         const float* base = P.loads[in.load].ptr + f0;
         DISC_FOR_C if (c < t.nvalid) {
           if constexpr (VEC == 1) acc[c] = ldg(base + c * t.cstride);
           else acc[c] = __ldg(reinterpret_cast<const float4*>(base + c * t.cstride));
         }
+        cache_fill<VEC, CH>(P, t, in.load, acc);
         break;
       }
       case DISC_I_LOAD_AFF: {

@@ -223,6 +223,8 @@ class ProgramBuilder {
     }
     P.n_instr = n;
     P.n_slots = nslots;
+    P.cache_mode = DISC_CACHE_NONE;
+    for (int l = 0; l < DISC_MAX_LOADS; ++l) P.cache_slot[l] = -1;
     P.n_loads = static_cast<int32_t>(maps_.size());
     for (size_t l = 0; l < maps_.size(); ++l) P.loads[l].ptr = ptrs_[l];
     B.maps = maps_;
@@ -866,15 +868,45 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& 
     int g = next_pow2((chunks + 31) / 32);
     const int64_t need = (int64_t{sm_count()} * 1024 + std::max<int64_t>(R.K, 1) - 1) / std::max<int64_t>(R.K, 1);
     while (g < need && g < 1024 && int64_t{g} * 4 <= chunks) g <<= 1;
+    // Row cache: contiguous loads the epilogue re-reads come from shared memory instead
+    // of a second pass over HBM/L2 (softmax: x is read once).
+    if (post_fused) {
+      int nc = 0;
+      for (int q = 0; q < R.post.n_loads && nc < 2; ++q) {
+        if (R.post.loads[q].mode != DISC_LOAD_IDENTITY) continue;
+        for (int p = 0; p < R.pre.n_loads; ++p)
+          if (R.pre.loads[p].mode == DISC_LOAD_IDENTITY && R.pre.loads[p].ptr == R.post.loads[q].ptr) {
+            if (R.pre.cache_slot[p] < 0) R.pre.cache_slot[p] = static_cast<int8_t>(nc++);
+            R.post.cache_slot[q] = R.pre.cache_slot[p];
+            break;
+          }
+      }
+      const int64_t budget = 48 * 1024;
+      auto bytes = [&](int gg) { return int64_t{std::max(gg, 256) / gg} * nc * R.R * 4; };
+      while (nc && bytes(g) > budget && g < 1024) g <<= 1;
+      if (nc && bytes(g) <= budget) {
+        R.cache_loads = nc;
+        R.pre.cache_mode = DISC_CACHE_FILL;
+        R.post.cache_mode = DISC_CACHE_READ;
+      } else {
+        for (int l = 0; l < DISC_MAX_LOADS; ++l) R.pre.cache_slot[l] = R.post.cache_slot[l] = -1;
+      }
+    }
     R.group = g;
-    rep.schedule = post_fused ? "row_fused" : "row";
+    rep.schedule = post_fused ? (R.cache_loads ? "row_fused_cached" : "row_fused") : "row";
   } else if (R.schedule != DISC_SCHED_GENERIC) {
     if (!R.red_out) R.red_out = static_cast<float*>(scratch.alloc(nout * 4));
-    const int64_t span = 32 * 2 * R.vec;
+    // Lanes per row segment: enough to cover C with two chunks each, up to a warp.
+    const int64_t cchunks = (R.C / R.vec + 1) / 2;
+    int lpc = 1;
+    while (lpc < cchunks && lpc < 32) lpc <<= 1;
+    R.group = lpc;
+    const int64_t span = int64_t{lpc} * 2 * R.vec;
     const int64_t tiles = (R.C + span - 1) / span;
     const int64_t ctas = R.K * tiles;
+    const int64_t rows_per_pass = 8 * (32 / lpc);
     const int64_t want = (int64_t{sm_count()} * 8 + ctas - 1) / ctas;
-    const int64_t max_split = std::max<int64_t>(1, R.R / 64);
+    const int64_t max_split = std::max<int64_t>(1, R.R / (rows_per_pass * 8));
     int64_t splits = std::min(want, max_split);
     if (pref == SchedulePref::kTwoPass || pref == SchedulePref::kAtomic) splits = std::max<int64_t>(splits, 2);
     splits = std::min<int64_t>(std::max<int64_t>(splits, 1), 65535);

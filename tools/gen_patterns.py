@@ -85,7 +85,7 @@ def gen_program(fn, prog):
         def src(is_slot, s):
             return f"v{slot_val[s]}" if is_slot else f"v{i - 1}"
         if op <= I_LOAD_CONST:
-            lines.append(f"    load_any<VEC, CH, WIDE>(P.loads[{load}], t, consts, {load}, {v});")
+            lines.append(f"    load_any<VEC, CH, WIDE>(P, t, consts, {load}, {v});")
         elif op == I_REDVAL:
             lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = splat(red, {v}[c]);")
         elif op == I_COPY:
@@ -113,7 +113,8 @@ def generate():
     header = ["// GENERATED by tools/gen_patterns.py -- do not edit.",
               "// Straight-line fused programs for the pattern library (fixtures + BASELINE configs C1-C4);",
               "// see the generator's docstring.  Source patterns per entry are noted in comments."]
-    shards = [header + ['#include "kernels.cuh"', "", "namespace disc_gen {", "using namespace disc_dev;", ""]
+    shards = [header + ['#include "kernels.cuh"', "", "namespace disc_gen {", "using namespace disc_dev;",
+                        "constexpr int kGenCH = 1;  // generated straight-line code: one chunk per tile", ""]
               for _ in range(SHARDS)]
     entries = []
     for n, ((kind, key), (rec, src_name)) in enumerate(sorted(seen.items())):
@@ -126,14 +127,14 @@ def generate():
         parts.append(f"cudaError_t launch_{tag}(const void* l, int vec, cudaStream_t s) {{")
         if kind == "loop":
             parts.append("  const auto& L = *static_cast<const disc_loop_launch*>(l);")
-            parts.append(f"  return vec == 4 ? launch_loop_with(k_loop<4, false, Pre_{tag}>, L, s, false)"
-                         f" : launch_loop_with(k_loop<1, false, Pre_{tag}>, L, s, false);")
+            parts.append(f"  return vec == 4 ? launch_loop_with<kGenCH>(k_loop<4, false, Pre_{tag}, kGenCH>, L, s, false)"
+                         f" : launch_loop_with<kGenCH>(k_loop<1, false, Pre_{tag}, kGenCH>, L, s, false);")
         elif kind == "row":
             parts.append("  const auto& L = *static_cast<const disc_reduce_launch*>(l);")
-            parts.append(f"  return row_pass<Pre_{tag}, Post_{tag}>(L, s, false, false);")
+            parts.append(f"  return row_pass<Pre_{tag}, Post_{tag}, kGenCH>(L, s, false, false);")
         else:
             parts.append("  const auto& L = *static_cast<const disc_reduce_launch*>(l);")
-            parts.append(f"  return col_pass_t<Pre_{tag}>(L, s, false, false);")
+            parts.append(f"  return col_pass_t<Pre_{tag}, kGenCH>(L, s, false, false);")
         parts.append("}")
         parts.append("")
         entries.append((["loop", "row", "col"].index(kind), key, f"launch_{tag}"))
