@@ -16,23 +16,30 @@ __device__ __forceinline__ double red_join(int kind, double a, double b) {
 }
 
 // Finalize split-R partials: ordered join over splits (two-pass) or cast (atomic).
-__global__ void k_col_finalize(const __grid_constant__ disc_reduce_launch L) {
+// Finalize split-R partials: a block owns 32 outputs x 8 split lanes; lane s joins
+// splits s, s+8, ... in order, then the 8 lane partials are joined in lane order
+// (deterministic); atomic schedules just cast.
+__global__ void __launch_bounds__(256) k_col_finalize(const __grid_constant__ disc_reduce_launch L) {
+  __shared__ double part[8][33];
   const int64_t n = L.K * L.C;
-  for (int64_t o = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; o < n;
-       o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    double t = L.workspace[o];
-    if (L.schedule == DISC_SCHED_COL_TWOPASS) {
-      // Fixed split order; eight partials loaded ahead of each join.
-      for (int s0 = 1; s0 < L.splits; s0 += 8) {
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = s0 + u < L.splits ? L.workspace[static_cast<int64_t>(s0 + u) * n + o] : 0.0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (s0 + u < L.splits) t = red_join(L.kind, t, v[u]);
-      }
+  const int ox = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * 32; base < n; base += static_cast<int64_t>(gridDim.x) * 32) {
+    const int64_t o = base + ox;
+    if (L.schedule != DISC_SCHED_COL_TWOPASS) {
+      if (sl == 0 && o < n) L.red_out[o] = static_cast<float>(L.workspace[o]);
+      continue;
     }
-    L.red_out[o] = static_cast<float>(t);
+    double t = red_identity(L.kind);
+    if (o < n)
+      for (int s = sl; s < L.splits; s += 8) t = red_join(L.kind, t, L.workspace[static_cast<int64_t>(s) * n + o]);
+    part[sl][ox] = t;
+    __syncthreads();
+    if (sl == 0 && o < n) {
+      double r = part[0][ox];
+      for (int u = 1; u < 8; ++u) r = red_join(L.kind, r, part[u][ox]);
+      L.red_out[o] = static_cast<float>(r);
+    }
+    __syncthreads();
   }
 }
 
@@ -105,7 +112,7 @@ cudaError_t col_pass(const disc_reduce_launch& L, cudaStream_t s);
 cudaError_t finalize_columns(const disc_reduce_launch& L, cudaStream_t s) {
   if (L.schedule == DISC_SCHED_COL_SINGLE) return cudaSuccess;
   const int64_t n = L.K * L.C;
-  const int64_t want = (n + 255) / 256;
+  const int64_t want = (n + 31) / 32;
   k_col_finalize<<<static_cast<int>(want < sm_count() * 8 ? want : sm_count() * 8), 256, 0, s>>>(L);
   return cudaGetLastError();
 }

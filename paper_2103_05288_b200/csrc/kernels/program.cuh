@@ -209,6 +209,66 @@ __device__ __forceinline__ void load_any(const disc_program& P, const TileCtx& t
   }
 }
 
+// Load classes (structural: part of a generated pattern's key).
+enum LoadClass { kLcIdentity = 0, kLcConst = 1, kLcSplat = 2, kLcContig = 3, kLcStrided = 4, kLcGather = 5 };
+
+__host__ __device__ inline int load_class(const disc_load& L) {
+  switch (L.mode) {
+    case DISC_LOAD_IDENTITY: return kLcIdentity;
+    case DISC_LOAD_CONST: return kLcConst;
+    case DISC_LOAD_AFFINE: return L.cs == 0 ? kLcSplat : (L.cs == 1 ? kLcContig : kLcStrided);
+    default: return kLcGather;
+  }
+}
+
+// One load of a tile with its binding class known at compile time.
+template <int VEC, int CH, bool WIDE, int CLS>
+__device__ __forceinline__ void load_cls(const disc_program& P, const TileCtx& t, const float* consts, int l,
+                                         typename Vec<VEC>::T (&v)[CH]) {
+  const disc_load& L = P.loads[l];
+  if constexpr (CLS == kLcIdentity) {
+    if (cached_load<VEC, CH>(P, t, l, v)) return;
+    const float* base = L.ptr + (t.row * t.W + t.col0);
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      if (c < t.nvalid) {
+        if constexpr (VEC == 1) v[c] = ldg(base + c * t.cstride);
+        else v[c] = __ldg(reinterpret_cast<const float4*>(base + c * t.cstride));
+      }
+    cache_fill<VEC, CH>(P, t, l, v);
+  } else if constexpr (CLS == kLcConst) {
+    const float x = consts[l];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) v[c] = splat(x, v[c]);
+  } else if constexpr (CLS == kLcSplat) {  // value depends on the row only
+    const float x = ldg(L.ptr + L.offset + t.row * L.rs);
+#pragma unroll
+    for (int c = 0; c < CH; ++c) v[c] = splat(x, v[c]);
+  } else if constexpr (CLS == kLcContig) {
+    const float* base = L.ptr + L.offset + t.row * L.rs + t.col0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      if (c < t.nvalid) {
+        if constexpr (VEC == 1) {
+          v[c] = ldg(base + c * t.cstride);
+        } else {
+          const float* p = base + c * t.cstride;
+          v[c] = L.vec_ok == 1 ? __ldg(reinterpret_cast<const float4*>(p)) : make_float4(ldg(p), ldg(p + 1), ldg(p + 2), ldg(p + 3));
+        }
+      }
+  } else if constexpr (CLS == kLcStrided) {
+    const float* base = L.ptr + L.offset + t.row * L.rs;
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      if (c < t.nvalid) v[c] = load_row<VEC>(L, base, t.col0 + c * t.cstride);
+  } else {
+    const int64_t f0 = t.row * t.W + t.col0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      if (c < t.nvalid) v[c] = load_gather<VEC, WIDE>(L, f0 + c * t.cstride);
+  }
+}
+
 template <int VEC, int CH>
 __device__ __forceinline__ void store_tile(float* out, const TileCtx& t, const typename Vec<VEC>::T (&v)[CH]) {
   float* o = out + t.row * t.W + t.col0;

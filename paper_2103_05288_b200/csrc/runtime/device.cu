@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "disc_cuda.h"
+#include "../kernels/program.cuh"
 
 namespace disc_launch {
 cudaError_t loop(const disc_loop_launch& L, cudaStream_t s);
@@ -66,6 +67,7 @@ uint64_t program_hash(const disc_program& P) {
     h = mix(h, (uint64_t)op | ((uint64_t)I.a << 8) | ((uint64_t)I.b << 16) | ((uint64_t)I.flags << 24) |
                    ((uint64_t)I.dst << 32) | ((uint64_t)I.load << 40) | ((uint64_t)I.out << 48));
   }
+  for (int l = 0; l < P.n_loads; ++l) h = mix(h, 0x100 + disc_dev::load_class(P.loads[l]));
   return h;
 }
 
@@ -79,6 +81,8 @@ std::string program_text(const disc_program& P) {
          std::to_string(I.flags) + "," + std::to_string(I.dst) + "," + std::to_string(I.load) + "," +
          std::to_string(I.out) + "]";
   }
+  s += "],\"lclass\":[";
+  for (int l = 0; l < P.n_loads; ++l) s += (l ? "," : "") + std::to_string(disc_dev::load_class(P.loads[l]));
   return s + "]}";
 }
 

@@ -85,7 +85,7 @@ def gen_program(fn, prog):
         def src(is_slot, s):
             return f"v{slot_val[s]}" if is_slot else f"v{i - 1}"
         if op <= I_LOAD_CONST:
-            lines.append(f"    load_any<VEC, CH, WIDE>(P, t, consts, {load}, {v});")
+            lines.append(f"    load_cls<VEC, CH, WIDE, {prog['lclass'][load]}>(P, t, consts, {load}, {v});")
         elif op == I_REDVAL:
             lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = splat(red, {v}[c]);")
         elif op == I_COPY:
@@ -113,8 +113,7 @@ def generate():
     header = ["// GENERATED by tools/gen_patterns.py -- do not edit.",
               "// Straight-line fused programs for the pattern library (fixtures + BASELINE configs C1-C4);",
               "// see the generator's docstring.  Source patterns per entry are noted in comments."]
-    shards = [header + ['#include "kernels.cuh"', "", "namespace disc_gen {", "using namespace disc_dev;",
-                        "constexpr int kGenCH = 1;  // generated straight-line code: one chunk per tile", ""]
+    shards = [header + ['#include "kernels.cuh"', "", "namespace disc_gen {", "using namespace disc_dev;", ""]
               for _ in range(SHARDS)]
     entries = []
     for n, ((kind, key), (rec, src_name)) in enumerate(sorted(seen.items())):
@@ -124,7 +123,12 @@ def generate():
         parts.append(gen_program(f"Pre_{tag}", rec["pre"]))
         if kind == "row":
             parts.append(gen_program(f"Post_{tag}", rec["post"]))
+        # Chunks per tile: short programs are memory-bound (more loads in flight), long
+        # ones register/issue-bound (keep straight-line code small).
+        n_code = max(len(rec["pre"]["code"]), len(rec.get("post", {}).get("code", [])))
+        ch = 4 if n_code <= 8 else (2 if n_code <= 20 else 1)
         parts.append(f"cudaError_t launch_{tag}(const void* l, int vec, cudaStream_t s) {{")
+        parts.append(f"  constexpr int kGenCH = {ch};")
         if kind == "loop":
             parts.append("  const auto& L = *static_cast<const disc_loop_launch*>(l);")
             parts.append(f"  return vec == 4 ? launch_loop_with<kGenCH>(k_loop<4, false, Pre_{tag}, kGenCH>, L, s, false)"
