@@ -130,6 +130,9 @@ int disc_executor_run_kernel(disc_executor e, disc_plan p, int kernel, int versi
  * device programs of every fused launch as JSON (used by tools/gen_patterns.py). */
 int disc_plan_capture_programs(disc_plan p, int n_inputs, const char* const* names,
                                const int64_t* const* dims, const int* ranks, char** json);
+/* Host-side cost of one run (capture mode: no device work), microseconds per run. */
+int disc_plan_host_overhead(disc_plan p, int n_inputs, const char* const* names,
+                            const int64_t* const* dims, const int* ranks, int iters, double* us_per_run);
 /* guard_passes (executor.cpp:78-98) */
 int disc_guard_passes(disc_plan p, int kernel, int version, const int64_t* regs, int n_regs);
 

@@ -85,6 +85,7 @@ def _declare(L: C.CDLL) -> None:
         "disc_executor_run_kernel": ([vp, vp, i32, i32, i32, P(vp), P(vp), P(i32), P(i64), i32], i32),
         "disc_guard_passes": ([vp, i32, i32, P(i64), i32], i32),
         "disc_plan_capture_programs": ([vp, i32, P(cp), P(vp), P(i32), P(vp)], i32),
+        "disc_plan_host_overhead": ([vp, i32, P(cp), P(vp), P(i32), i32, P(C.c_double)], i32),
         "disc_cuda_set_specialization": ([i32], i32),
         "disc_cuda_specialized_launches": ([], i64),
         "disc_cuda_num_specializations": ([], i32),
@@ -525,6 +526,19 @@ def capture_programs(plan: CompiledPlan, input_shapes: Dict[str, Sequence[int]])
     c_dims = (C.c_void_p * max(k, 1))(*[d.ctypes.data for d in dims])
     c_ranks = (C.c_int * max(k, 1))(*[d.size for d in dims])
     return json.loads(_str(lib().disc_plan_capture_programs, plan._h, k, c_names, c_dims, c_ranks))
+
+
+def host_overhead_us(plan: CompiledPlan, input_shapes: Dict[str, Sequence[int]], iters: int = 2000) -> float:
+    """Host cost of one run of the runtime flow (no device work), in microseconds."""
+    names = list(input_shapes)
+    dims = [np.array(input_shapes[n], dtype=np.int64) for n in names]
+    k = len(names)
+    c_names = (C.c_char_p * max(k, 1))(*[n.encode() for n in names])
+    c_dims = (C.c_void_p * max(k, 1))(*[d.ctypes.data for d in dims])
+    c_ranks = (C.c_int * max(k, 1))(*[d.size for d in dims])
+    us = C.c_double()
+    _check(lib().disc_plan_host_overhead(plan._h, k, c_names, c_dims, c_ranks, iters, C.byref(us)))
+    return us.value
 
 
 def set_specialization(enabled: bool) -> None:

@@ -17,8 +17,13 @@ std::shared_ptr<const PreparedPlan> prepare_plan(const CompiledPlan& plan);
 
 // An immutable compiled plan plus its (lazily built, shape-agnostic) device lowering.
 struct disc_plan_s {
-  explicit disc_plan_s(std::shared_ptr<const disc::CompiledPlan> p) : plan(std::move(p)) {}
+  explicit disc_plan_s(std::shared_ptr<const disc::CompiledPlan> p) : plan(std::move(p)), serial(next_serial()) {}
   std::shared_ptr<const disc::CompiledPlan> plan;
+  uint64_t serial;  // unique per plan object: keys executor launch caches
+  static uint64_t next_serial() {
+    static std::atomic<uint64_t> n{1};
+    return n.fetch_add(1);
+  }
   std::atomic<int> refs{1};
   std::once_flag prepared_once;
   std::shared_ptr<const disc::rt::PreparedPlan> prepared;

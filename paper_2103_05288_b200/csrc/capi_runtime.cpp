@@ -1,4 +1,5 @@
 // C ABI, runtime side: executors over a device + stream (include/disc_b200.h).
+#include <chrono>
 #include <cstring>
 
 #include "capi_common.hpp"
@@ -54,7 +55,7 @@ int disc_executor_run(disc_executor e, disc_plan p, int n, const char* const* na
       in[i].ptr = on_host ? e->ex.stage_input(i, data[i], bytes_of(dims[i], ranks[i]))
                           : static_cast<const float*>(data[i]);
     }
-    e->ex.run(*p->plan, in);
+    e->ex.run(*p->plan, in, false, p->serial);
   });
 }
 
@@ -70,7 +71,7 @@ int disc_executor_run_batch(disc_executor e, disc_plan p, int n_requests, int n_
         in[i].ptr = on_host ? e->ex.stage_input(i, data[k], bytes_of(dims[k], ranks[k]))
                             : static_cast<const float*>(data[k]);
       }
-      e->ex.run(*p->plan, in, r > 0);
+      e->ex.run(*p->plan, in, r > 0, p->serial);
     }
   });
 }
@@ -205,6 +206,28 @@ int disc_plan_capture_programs(disc_plan p, int n, const char* const* names, con
     }
     ex.run(*p->plan, in);
     disc_cuda_capture_records(json);
+  });
+  disc_cuda_set_capture(0);
+  return rc;
+}
+
+int disc_plan_host_overhead(disc_plan p, int n, const char* const* names, const int64_t* const* dims,
+                            const int* ranks, int iters, double* us_per_run) {
+  disc_cuda_set_capture(2);
+  int rc = guard([&] {
+    rt::DeviceExecutor ex(0, nullptr);
+    std::vector<rt::InputBinding> in(n);
+    for (int i = 0; i < n; ++i) {
+      in[i].name = names[i];
+      in[i].dims.assign(dims[i], dims[i] + ranks[i]);
+      void* fake = nullptr;
+      disc_cuda_malloc(static_cast<size_t>(bytes_of(dims[i], ranks[i])), nullptr, &fake);
+      in[i].ptr = static_cast<const float*>(fake);
+    }
+    ex.run(*p->plan, in, false, p->serial);
+    auto t0 = std::chrono::steady_clock::now();
+    for (int k = 0; k < iters; ++k) ex.run(*p->plan, in, false, p->serial);
+    *us_per_run = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count() / iters;
   });
   disc_cuda_set_capture(0);
   return rc;

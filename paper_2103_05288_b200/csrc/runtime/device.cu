@@ -43,6 +43,7 @@ bool g_spec_enabled = true;
 // Capture mode (host-only dry run used by the pattern generator): device calls become
 // no-ops, allocations return fake aligned addresses, launches are recorded.
 bool g_capture = false;
+bool g_capture_record = true;  // capture mode 2: dry run without recording (host timing)
 uint64_t g_fake_next = uint64_t{1} << 36;
 std::vector<std::string> g_records;
 
@@ -94,6 +95,7 @@ uint64_t launch_key(int kind, const disc_program& a, const disc_program* b) {
 }
 
 void record(const std::string& kind, uint64_t key, const std::string& body) {
+  if (!g_capture_record) return;
   char hex[32];
   std::snprintf(hex, sizeof hex, "%016llx", static_cast<unsigned long long>(key));
   g_records.push_back("{\"kind\":\"" + kind + "\",\"key\":\"" + hex + "\"," + body + "}");
@@ -210,7 +212,8 @@ int disc_cuda_launch_loop(const disc_loop_launch* l, void* stream) {
   if (l->total <= 0) return 0;
   const uint64_t key = launch_key(0, l->prog, nullptr);
   if (g_capture) {
-    record("loop", key, "\"vec\":" + std::to_string(l->vec) + ",\"pre\":" + program_text(l->prog));
+    if (g_capture_record) record("loop", key, "\"vec\":" + std::to_string(l->vec) + ",\"pre\":" + program_text(l->prog));
+    else if (g_spec_enabled && !l->wide) (void)disc_spec::lookup(0, key);
     return 0;
   }
   if (g_spec_enabled && !l->wide)
@@ -227,6 +230,10 @@ int disc_cuda_launch_reduce(const disc_reduce_launch* l, void* stream) {
                    l->schedule == DISC_SCHED_COL_ATOMIC;
   const uint64_t key = row ? launch_key(1, l->pre, &l->post) : launch_key(2, l->pre, nullptr);
   if (g_capture) {
+    if (!g_capture_record) {
+      if (g_spec_enabled && (row || col)) (void)disc_spec::lookup(row ? 1 : 2, key);
+      return 0;
+    }
     if (row || col)
       record(row ? "row" : "col", key,
              "\"vec\":" + std::to_string(l->vec) + ",\"pre\":" + program_text(l->pre) +
@@ -277,6 +284,7 @@ int disc_cuda_num_specializations(void) { return disc_spec::count(); }
 
 int disc_cuda_set_capture(int enabled) {
   g_capture = enabled != 0;
+  g_capture_record = enabled == 1;
   if (g_capture) g_records.clear();
   return 0;
 }

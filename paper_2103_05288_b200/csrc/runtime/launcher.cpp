@@ -5,6 +5,7 @@
 #include <cstring>
 #include <map>
 #include <tuple>
+#include <unordered_map>
 
 #include "shape_eval.hpp"
 
@@ -723,9 +724,18 @@ int64_t algorithmic_bytes(const KernelArtifact& art, const std::vector<DevTensor
   return bytes;
 }
 
+// Where the fused lowering sends its work: straight to the device, or into a recipe
+// (cached and replayed with real pointers patched in).
+class Issuer {
+ public:
+  virtual ~Issuer() = default;
+  virtual void* scratch(int64_t bytes) = 0;
+  virtual void loop(const disc_loop_launch& L) = 0;
+  virtual void reduce(const disc_reduce_launch& R) = 0;
+};
+
 // Issues the fused lowering; throws NotFusible when the tape needs materialisation.
-LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& scratch, void* stream,
-                          SchedulePref pref) {
+LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& issue, SchedulePref pref) {
   const KernelArtifact& art = B.art;
   const int n = static_cast<int>(art.tape.size());
   LaunchReport rep;
@@ -742,7 +752,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& 
     Built b = pb.finish(-1);
     disc_loop_launch L = make_loop(b, N);
     if (N > 0) {
-      cuda_ok(disc_cuda_launch_loop(&L, stream), "fused loop");
+      issue.loop(L);
       rep.device_kernels = 1;
     }
     rep.schedule = L.vec == 4 ? "loop_v4" : "loop";
@@ -767,7 +777,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& 
   for (int o : art.output_tape_indices)
     if (B.post[o]) has_post = true;
   float* red_ptr = red_out_idx >= 0 ? outs[red_out_idx].ptr : nullptr;
-  if (!red_ptr && has_post) red_ptr = static_cast<float*>(scratch.alloc(nout * 4));
+  if (!red_ptr && has_post) red_ptr = static_cast<float*>(issue.scratch(nout * 4));
 
   disc_reduce_launch R;
   std::memset(&R, 0, sizeof R);
@@ -895,7 +905,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& 
     R.group = g;
     rep.schedule = post_fused ? (R.cache_loads ? "row_fused_cached" : "row_fused") : "row";
   } else if (R.schedule != DISC_SCHED_GENERIC) {
-    if (!R.red_out) R.red_out = static_cast<float*>(scratch.alloc(nout * 4));
+    if (!R.red_out) R.red_out = static_cast<float*>(issue.scratch(nout * 4));
     // Lanes per row segment: enough to cover C with two chunks each, up to a warp.
     const int64_t cchunks = (R.C / R.vec + 1) / 2;
     int lpc = 1;
@@ -916,22 +926,22 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Scratch& 
       rep.schedule = "col_single";
     } else if (pref == SchedulePref::kAtomic && R.kind == DISC_REDUCE_SUM) {
       R.schedule = DISC_SCHED_COL_ATOMIC;
-      R.workspace = static_cast<double*>(scratch.alloc(8 * nout));
+      R.workspace = static_cast<double*>(issue.scratch(8 * nout));
       rep.schedule = "col_atomic";
     } else {
       R.schedule = DISC_SCHED_COL_TWOPASS;
-      R.workspace = static_cast<double*>(scratch.alloc(8 * nout * splits));
+      R.workspace = static_cast<double*>(issue.scratch(8 * nout * splits));
       rep.schedule = "col_twopass";
     }
   } else {
-    if (!R.red_out) R.red_out = static_cast<float*>(scratch.alloc(nout * 4));
+    if (!R.red_out) R.red_out = static_cast<float*>(issue.scratch(nout * 4));
     rep.schedule = "generic";
   }
 
-  cuda_ok(disc_cuda_launch_reduce(&R, stream), "fused reduce");
+  issue.reduce(R);
   rep.device_kernels = (R.schedule == DISC_SCHED_COL_TWOPASS || R.schedule == DISC_SCHED_COL_ATOMIC) ? 2 : 1;
   if (post_pass) {
-    cuda_ok(disc_cuda_launch_loop(&PL, stream), "epilogue pass");
+    issue.loop(PL);
     rep.device_kernels += 1;
     rep.schedule += "+post";
   }
@@ -1111,9 +1121,146 @@ LaunchReport launch_standalone(Binding& B, const std::vector<OutBuf>& outs, void
 
 }  // namespace
 
+namespace {
+
+class DirectIssuer final : public Issuer {
+ public:
+  DirectIssuer(Scratch& s, void* stream) : scratch_(s), stream_(stream) {}
+  void* scratch(int64_t bytes) override { return scratch_.alloc(bytes); }
+  void loop(const disc_loop_launch& L) override { cuda_ok(disc_cuda_launch_loop(&L, stream_), "fused loop"); }
+  void reduce(const disc_reduce_launch& R) override { cuda_ok(disc_cuda_launch_reduce(&R, stream_), "fused reduce"); }
+
+ private:
+  Scratch& scratch_;
+  void* stream_;
+};
+
+// Tagged pointers: [63:60] kind (1 external, 2 output, 3 scratch), [59:32] index,
+// [3:0] the real pointer's low bits (alignment decisions see the same value).
+constexpr uint64_t kTagExt = 1, kTagOut = 2, kTagScratch = 3;
+inline const void* tag(uint64_t kind, uint64_t index, uintptr_t low) {
+  return reinterpret_cast<const void*>((kind << 60) | (index << 32) | (low & 15));
+}
+
+struct Recipe {
+  std::vector<int64_t> scratch_bytes;
+  std::vector<std::pair<int, std::unique_ptr<disc_loop_launch>>> loops;     // (order, launch)
+  std::vector<std::pair<int, std::unique_ptr<disc_reduce_launch>>> reduces;
+  int steps = 0;
+  LaunchReport rep;
+};
+
+class RecordingIssuer final : public Issuer {
+ public:
+  explicit RecordingIssuer(Recipe& r) : r_(r) {}
+  void* scratch(int64_t bytes) override {
+    r_.scratch_bytes.push_back(bytes);
+    return const_cast<void*>(tag(kTagScratch, r_.scratch_bytes.size() - 1, 0));
+  }
+  void loop(const disc_loop_launch& L) override {
+    r_.loops.emplace_back(r_.steps++, std::make_unique<disc_loop_launch>(L));
+  }
+  void reduce(const disc_reduce_launch& R) override {
+    r_.reduces.emplace_back(r_.steps++, std::make_unique<disc_reduce_launch>(R));
+  }
+
+ private:
+  Recipe& r_;
+};
+
+struct Patch {
+  const std::vector<DevTensor>& ext;
+  const std::vector<OutBuf>& outs;
+  const std::vector<void*>& scratch;
+  template <typename T>
+  void operator()(T*& p) const {
+    const uint64_t v = reinterpret_cast<uint64_t>(p);
+    const uint64_t kind = v >> 60, idx = (v >> 32) & 0x0fffffff;
+    if (kind == kTagExt) p = const_cast<T*>(reinterpret_cast<const T*>(ext.at(idx).ptr));
+    else if (kind == kTagOut) p = reinterpret_cast<T*>(outs.at(idx).ptr);
+    else if (kind == kTagScratch) p = reinterpret_cast<T*>(scratch.at(idx));
+    else if (v) throw InternalError("untagged pointer in a launch recipe");
+  }
+  void program(disc_program& P) const {
+    for (int l = 0; l < P.n_loads; ++l) (*this)(P.loads[l].ptr);
+    for (int o = 0; o < P.n_outs; ++o) (*this)(P.outs[o]);
+  }
+};
+
+void replay(const Recipe& r, const std::vector<DevTensor>& ext, const std::vector<OutBuf>& outs, Scratch& scratch,
+            void* stream) {
+  std::vector<void*> sp;
+  sp.reserve(r.scratch_bytes.size());
+  for (int64_t b : r.scratch_bytes) sp.push_back(scratch.alloc(b));
+  const Patch patch{ext, outs, sp};
+  size_t li = 0, ri = 0;
+  for (int step = 0; step < r.steps; ++step) {
+    if (li < r.loops.size() && r.loops[li].first == step) {
+      disc_loop_launch L = *r.loops[li++].second;
+      patch.program(L.prog);
+      cuda_ok(disc_cuda_launch_loop(&L, stream), "fused loop");
+    } else {
+      disc_reduce_launch R = *r.reduces[ri++].second;
+      patch.program(R.pre);
+      patch.program(R.post);
+      patch(R.red_out);
+      patch(R.workspace);
+      cuda_ok(disc_cuda_launch_reduce(&R, stream), "fused reduce");
+    }
+  }
+}
+
+uint64_t hmix(uint64_t h, uint64_t v) { return (h ^ v) * 0x100000001b3ull + (h >> 29); }
+
+}  // namespace
+
+// Shape-keyed cache of fused launch recipes (one per executor).
+struct LaunchCache {
+  struct Entry {
+    std::vector<int64_t> key;  // full key, compared on hit
+    std::shared_ptr<Recipe> recipe;  // null: the tape needs materialisation
+  };
+  std::unordered_map<uint64_t, std::vector<Entry>> map;
+  size_t entries = 0;
+};
+
+LaunchCache* new_launch_cache() { return new LaunchCache(); }
+void free_launch_cache(LaunchCache* c) { delete c; }
+
 LaunchReport launch_kernel(const KernelArtifact& art, const VersionArtifact& ver, const std::vector<DevTensor>& ext,
                            const std::vector<int64_t>& regs, const std::vector<OutBuf>& outs, Scratch& scratch,
-                           void* stream, SchedulePref pref) {
+                           void* stream, SchedulePref pref, LaunchCache* cache, uint64_t plan_serial) {
+  // Recipe cache: everything the lowering depends on is in the key.
+  std::vector<int64_t> key;
+  uint64_t h = 0;
+  const bool cacheable = cache && plan_serial && !art.standalone && pref != SchedulePref::kMaterialize;
+  if (cacheable) {
+    key.reserve(8 + regs.size() + 4 * ext.size());
+    key.push_back(static_cast<int64_t>(plan_serial));
+    key.push_back(art.kernel_id);
+    key.push_back(ver.id);
+    key.push_back(static_cast<int64_t>(pref));
+    key.insert(key.end(), regs.begin(), regs.end());
+    for (size_t i = 0; i < ext.size(); ++i) {
+      key.push_back(static_cast<int64_t>(ext[i].dims.size()));
+      key.insert(key.end(), ext[i].dims.begin(), ext[i].dims.end());
+      int64_t same = -1;  // aliasing pattern among externals
+      for (size_t j = 0; j < i; ++j)
+        if (ext[j].ptr == ext[i].ptr) same = static_cast<int64_t>(j);
+      key.push_back((reinterpret_cast<uintptr_t>(ext[i].ptr) & 15) | (same << 8));
+    }
+    for (const auto& o : outs) key.push_back((reinterpret_cast<uintptr_t>(o.ptr) & 15) | (o.capacity_bytes << 4));
+    for (int64_t v : key) h = hmix(h, static_cast<uint64_t>(v));
+    auto it = cache->map.find(h);
+    if (it != cache->map.end())
+      for (const auto& e : it->second)
+        if (e.key == key) {
+          if (!e.recipe) break;  // known to need the materialised path
+          replay(*e.recipe, ext, outs, scratch, stream);
+          return e.recipe->rep;
+        }
+  }
+
   std::vector<std::vector<int64_t>> ext_dims;
   for (const auto& e : ext) ext_dims.push_back(e.dims);
   Binding B{art, ver, ext, regs, simulate_tape(art, ver, ext_dims, regs), -1, {}};
@@ -1135,10 +1282,43 @@ LaunchReport launch_kernel(const KernelArtifact& art, const VersionArtifact& ver
     bool done = false;
     if (pref != SchedulePref::kMaterialize) {
       try {
-        rep = launch_fused(B, outs, scratch, stream, pref);
+        if (cacheable) {
+          // Record with tagged pointers, cache, then replay with the real ones.
+          std::vector<DevTensor> text(ext.size());
+          for (size_t i = 0; i < ext.size(); ++i) {
+            size_t first = i;
+            for (size_t j = 0; j < i; ++j)
+              if (ext[j].ptr == ext[i].ptr) {
+                first = j;
+                break;
+              }
+            text[i] = {static_cast<const float*>(tag(kTagExt, first, reinterpret_cast<uintptr_t>(ext[i].ptr))), ext[i].dims};
+          }
+          std::vector<OutBuf> touts(outs.size());
+          for (size_t o = 0; o < outs.size(); ++o)
+            touts[o] = {static_cast<float*>(const_cast<void*>(tag(kTagOut, o, reinterpret_cast<uintptr_t>(outs[o].ptr)))),
+                        outs[o].capacity_bytes};
+          Binding TB{art, ver, text, regs, B.dims, B.red, B.post};
+          auto recipe = std::make_shared<Recipe>();
+          RecordingIssuer rec(*recipe);
+          recipe->rep = launch_fused(TB, touts, rec, pref);
+          recipe->rep.algorithmic_bytes = algorithmic_bytes(art, ext, B.dims);
+          if (cache->entries < 65536) {
+            cache->map[h].push_back({key, recipe});
+            cache->entries++;
+          }
+          replay(*recipe, ext, outs, scratch, stream);
+          return recipe->rep;
+        }
+        DirectIssuer direct(scratch, stream);
+        rep = launch_fused(B, outs, direct, pref);
         done = true;
       } catch (const NotFusible& nf) {
         if (pref == SchedulePref::kFusedOnly) throw InternalError(std::string("not fusible: ") + nf.why);
+        if (cacheable && cache->entries < 65536) {
+          cache->map[h].push_back({key, nullptr});
+          cache->entries++;
+        }
       }
     }
     if (!done) rep = launch_materialized(B, outs, scratch, stream);

@@ -55,11 +55,18 @@ struct LaunchReport {
   int64_t algorithmic_bytes = 0;  // boundary bytes (SURVEY §8d formula)
 };
 
+// Shape-keyed cache of recorded fused launches (owned by an executor).
+struct LaunchCache;
+LaunchCache* new_launch_cache();
+void free_launch_cache(LaunchCache* c);
+
 // Runs one kLaunch.  `ext` are the external inputs bound at the artifact's
-// external_input_dims; `outs` are the planned output buffers.
+// external_input_dims; `outs` are the planned output buffers.  With a cache and a
+// nonzero plan serial, fused lowerings are recorded once per (plan, kernel, version,
+// register file, operand dims, pointer alignment/aliasing) and replayed afterwards.
 LaunchReport launch_kernel(const KernelArtifact& art, const VersionArtifact& ver, const std::vector<DevTensor>& ext,
                            const std::vector<int64_t>& regs, const std::vector<OutBuf>& outs, Scratch& scratch,
-                           void* stream, SchedulePref pref);
+                           void* stream, SchedulePref pref, LaunchCache* cache = nullptr, uint64_t plan_serial = 0);
 
 // Library call (eval_matmul semantics, f64 accumulation).
 void launch_gemm(int64_t m, int64_t k, int64_t n, const DevTensor& a, const DevTensor& b, const OutBuf& c,

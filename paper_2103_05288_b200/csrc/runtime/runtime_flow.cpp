@@ -73,7 +73,7 @@ void DeviceCachingAllocator::trim() {
 // ---------------------------------------------------------------------------
 
 DeviceExecutor::DeviceExecutor(int device, void* stream)
-    : device_(device), stream_(stream), alloc_(stream), scratch_(stream) {
+    : device_(device), stream_(stream), alloc_(stream), scratch_(stream), cache_(new_launch_cache()) {
   cuda_ok(disc_cuda_set_device(device), "set device");
 }
 
@@ -104,6 +104,7 @@ void DeviceExecutor::finish_timing() {
 
 DeviceExecutor::~DeviceExecutor() {
   disc_cuda_stream_synchronize(stream_);
+  free_launch_cache(cache_);
   for (float* p : passthrough_)
     if (p) disc_cuda_free(p, stream_);
   for (auto& s : staging_)
@@ -152,7 +153,8 @@ void DeviceExecutor::run_kernel(const KernelArtifact& art, const VersionArtifact
   records_ = {{-1, -1, rep.schedule, rep.algorithmic_bytes, 0.0, rep.device_kernels, -1}};
 }
 
-void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBinding>& inputs, bool append_records) {
+void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBinding>& inputs, bool append_records,
+                         uint64_t plan_serial) {
   ExecStats stats;
   stats.host_instruction_count = plan.host_instruction_count();
   const auto t_run = Clock::now();
@@ -301,7 +303,7 @@ void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBindin
         for (int b : in.out_bufs) outs.push_back(out_buf(b));
         const int ev = timing_ ? take_event_pair() : -1;
         if (ev >= 0) cuda_ok(disc_cuda_event_record(ev_pool_[ev].first, stream_), "event");
-        LaunchReport rep = launch_kernel(art, *ver, ext, regs, outs, scratch_, stream_, pref_);
+        LaunchReport rep = launch_kernel(art, *ver, ext, regs, outs, scratch_, stream_, pref_, cache_, plan_serial);
         if (ev >= 0) cuda_ok(disc_cuda_event_record(ev_pool_[ev].second, stream_), "event");
         stats.launch_count++;
         device_launches_ += rep.device_kernels;

@@ -87,7 +87,9 @@ class DeviceExecutor {
   void* stream() const { return stream_; }
   // Runs the plan; outputs remain valid until the next run.
   // append_records: keep the launch records of earlier runs (batched sweeps).
-  void run(const CompiledPlan& plan, const std::vector<InputBinding>& inputs, bool append_records = false);
+  // plan_serial: stable id of `plan` (enables the launch recipe cache; 0 disables).
+  void run(const CompiledPlan& plan, const std::vector<InputBinding>& inputs, bool append_records = false,
+           uint64_t plan_serial = 0);
   // Timing mode: waits for the recorded events and fills record/stat device times.
   void finish_timing();
   const std::vector<OutputView>& outputs() const { return outputs_; }
@@ -123,6 +125,7 @@ class DeviceExecutor {
   std::vector<LaunchRecord> records_;
   bool timing_ = false;
   SchedulePref pref_ = SchedulePref::kAuto;
+  LaunchCache* cache_ = nullptr;
   std::vector<std::pair<void*, void*>> ev_pool_;
   size_t ev_next_ = 0;
   bool timing_pending_ = false;
