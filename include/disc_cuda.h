@@ -97,11 +97,15 @@ typedef struct {
   int32_t n_outs;
   int32_t cache_mode;
   int8_t cache_slot[DISC_MAX_LOADS];
-  int32_t pad;
+  int32_t flags;    /* DISC_PROG_* launch flags (not part of the program structure) */
   disc_instr code[DISC_MAX_INSTR];
   disc_load loads[DISC_MAX_LOADS];
   float* outs[DISC_MAX_OUTS];
 } disc_program;
+
+/* disc_program.flags: with programmatic dependent launch, let the next kernel's CTAs
+ * launch as soon as this grid has passed its dependency wait (instead of at its exit). */
+#define DISC_PROG_PDL_EARLY 1
 
 enum disc_reduce_kind { DISC_REDUCE_SUM = 0, DISC_REDUCE_MAX = 1 };
 
@@ -209,9 +213,17 @@ int disc_cuda_gemm(int64_t m, int64_t k, int64_t n, const float* a, const float*
 int disc_cuda_fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, void* stream);
 /* Writes `bytes` to a scratch buffer to evict L2 between timed iterations. */
 int disc_cuda_flush_l2(void* scratch, size_t bytes, void* stream);
+/* Occupies `stream` for the given time (bench/profiling aid: lets the host queue a run
+ * ahead of the device so per-launch events measure device time only). */
+int disc_cuda_spin(uint64_t microseconds, void* stream);
 /* Number of kernels this library has launched (process-wide counter). */
 int64_t disc_cuda_kernel_launches(void);
 
+/* Programmatic dependent launch for fused kernels: 0 plain stream serialisation; 1 (default)
+ * each kernel's launch overlaps the previous kernel and its dependency wait; 2 also lets
+ * the next kernel's CTAs launch early (DISC_PROG_PDL_EARLY, set by the runtime). */
+int disc_cuda_set_pdl(int mode);
+int disc_cuda_pdl_mode(void);
 /* Generated fast paths: launches whose lowered program structure matches a pattern
  * compiled ahead of time (kernels/patterns_gen.cu) run straight-line kernels instead of
  * the interpreter.  Enabled by default; the counter reports how many launches used one. */

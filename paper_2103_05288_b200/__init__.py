@@ -4,12 +4,12 @@ Host: clean-room C++ compile pipeline (graph -> DHLO -> constraints -> fusion ->
 byte-identical plans to the reference.  Device: sm_100a fused tape kernels behind a
 C ABI (include/disc_b200.h, include/disc_cuda.h).  See DESIGN.md.
 """
-from .api import (capture_programs, set_specialization, specialized_launches, CompileOptions, CompiledPlan, Compiler, DeviceBuffer, DiscError, ExecResult, ExecStats,
+from .api import (capture_programs, set_pdl, set_specialization, specialized_launches, CompileOptions, CompiledPlan, Compiler, DeviceBuffer, DiscError, ExecResult, ExecStats,
                   Executor, cache_key, compile_graph, cuda_available, dhlo_roundtrip, dump_stage, guard_passes,
                   kernel_launches, lib, lower_dhlo_json, static_specialize)
 
 __all__ = [
-    "capture_programs", "set_specialization", "specialized_launches",
+    "capture_programs", "set_pdl", "set_specialization", "specialized_launches",
     "CompileOptions", "CompiledPlan", "Compiler", "DeviceBuffer", "DiscError", "ExecResult", "ExecStats",
     "Executor", "cache_key", "compile_graph", "cuda_available", "dhlo_roundtrip", "dump_stage", "guard_passes",
     "kernel_launches", "lib", "lower_dhlo_json", "static_specialize",

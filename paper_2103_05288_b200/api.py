@@ -113,6 +113,9 @@ def _declare(L: C.CDLL) -> None:
         "disc_cuda_event_elapsed_ms": ([vp, vp, P(C.c_float)], i32),
         "disc_cuda_fill_uniform": ([vp, i64, C.c_uint64, C.c_float, C.c_float, vp], i32),
         "disc_cuda_flush_l2": ([vp, C.c_size_t, vp], i32),
+        "disc_cuda_spin": ([C.c_uint64, vp], i32),
+        "disc_cuda_set_pdl": ([i32], i32),
+        "disc_cuda_pdl_mode": ([], i32),
         "disc_cuda_kernel_launches": ([], i64),
     }
     for name, (args, res) in sig.items():
@@ -543,6 +546,12 @@ def host_overhead_us(plan: CompiledPlan, input_shapes: Dict[str, Sequence[int]],
 
 def set_specialization(enabled: bool) -> None:
     lib().disc_cuda_set_specialization(int(enabled))
+
+
+def set_pdl(mode: int) -> None:
+    """Programmatic dependent launch between fused kernels: 0 off, 1 (default) launch
+    overlap + dependency wait, 2 also early launch of the next kernel's CTAs."""
+    lib().disc_cuda_set_pdl(int(mode))
 
 
 def specialized_launches() -> int:

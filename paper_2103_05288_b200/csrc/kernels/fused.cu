@@ -2,6 +2,8 @@
 // live in kernels.cuh.  Memory-bound schedules: no tensor cores; 128-bit coalesced
 // accesses, CH chunks in flight per thread, f64 accumulation for reductions (the
 // reference's reduce semantics, kernels.cpp:46-54, 234-259).
+#include <unordered_map>
+
 #include "kernels.cuh"
 
 
@@ -21,6 +23,7 @@ __device__ __forceinline__ double red_join(int kind, double a, double b) {
 // (deterministic); atomic schedules just cast.
 __global__ void __launch_bounds__(256) k_col_finalize(const __grid_constant__ disc_reduce_launch L) {
   __shared__ double part[8][33];
+  pdl_enter(L.pre);
   const int64_t n = L.K * L.C;
   const int ox = threadIdx.x & 31, sl = threadIdx.x >> 5;
   for (int64_t base = static_cast<int64_t>(blockIdx.x) * 32; base < n; base += static_cast<int64_t>(gridDim.x) * 32) {
@@ -50,6 +53,7 @@ __global__ void __launch_bounds__(kLoopThreads) k_reduce_generic(const __grid_co
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ float consts[DISC_MAX_LOADS];
   float* slots = reinterpret_cast<float*>(smem_raw) + threadIdx.x;
+  pdl_enter(L.pre);
   hoist_consts(L.pre, consts);
   __syncthreads();
   const int r = L.g_rank;
@@ -98,9 +102,32 @@ __global__ void __launch_bounds__(kLoopThreads) k_reduce_generic(const __grid_co
 
 // ---------------------------------------------------------------------------
 // Host launchers (called by the C ABI in runtime/device.cu).
+namespace disc_dev {
+
+static int g_pdl = 1;
+bool pdl_enabled() { return g_pdl != 0; }
+
+int resident_ctas(const void* kernel, int block, size_t smem) {
+  thread_local std::unordered_map<uint64_t, int> cache;
+  const uint64_t key = (reinterpret_cast<uintptr_t>(kernel) * 0x9E3779B97F4A7C15ull) ^
+                       (static_cast<uint64_t>(block) << 40) ^ static_cast<uint64_t>(smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, block, smem) != cudaSuccess || n < 1) n = 1;
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, n);
+  return n;
+}
+
+}  // namespace disc_dev
+
 namespace disc_launch {
 
 using namespace disc_dev;
+
+void set_pdl(int mode) { g_pdl = mode; }
+int pdl_mode() { return g_pdl; }
 
 cudaError_t loop(const disc_loop_launch& L, cudaStream_t s) {
   if (L.vec == 4) return L.wide ? launch_loop_with(k_loop<4, true, Interp>, L, s) : launch_loop_with(k_loop<4, false, Interp>, L, s);
@@ -113,8 +140,9 @@ cudaError_t finalize_columns(const disc_reduce_launch& L, cudaStream_t s) {
   if (L.schedule == DISC_SCHED_COL_SINGLE) return cudaSuccess;
   const int64_t n = L.K * L.C;
   const int64_t want = (n + 31) / 32;
-  k_col_finalize<<<static_cast<int>(want < sm_count() * 8 ? want : sm_count() * 8), 256, 0, s>>>(L);
-  return cudaGetLastError();
+  const cudaError_t e = launch_k(k_col_finalize, dim3(static_cast<int>(want < sm_count() * 8 ? want : sm_count() * 8)),
+                                 dim3(256), 0, s, L);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t reduce(const disc_reduce_launch& L, cudaStream_t s) {
@@ -129,8 +157,8 @@ cudaError_t reduce(const disc_reduce_launch& L, cudaStream_t s) {
     const size_t smem = static_cast<size_t>(slots) * kLoopThreads * 4;
     cudaError_t e = set_smem(k_reduce_generic, smem);
     if (e != cudaSuccess) return e;
-    k_reduce_generic<<<grid, kLoopThreads, smem, s>>>(L);
-    return cudaGetLastError();
+    e = launch_k(k_reduce_generic, dim3(grid), dim3(kLoopThreads), smem, s, L);
+    return e != cudaSuccess ? e : cudaGetLastError();
   }
   return col_pass(L, s);  // column schedules: the device layer adds memset/finalize
 }

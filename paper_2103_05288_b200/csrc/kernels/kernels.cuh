@@ -12,6 +12,16 @@
 
 namespace disc_dev {
 
+// Programmatic dependent launch: every fused kernel is launched with programmatic stream
+// serialization, so its launch overlaps the previous kernel.  The kernel must not touch
+// global memory before pdl_enter()'s wait (which returns once the preceding grid has
+// completed and flushed).  With DISC_PROG_PDL_EARLY it then lets its own dependents
+// launch at once (their CTAs become resident and wait); otherwise as this grid retires.
+__device__ __forceinline__ void pdl_enter(const disc_program& P) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (P.flags & DISC_PROG_PDL_EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 struct Interp {
   template <int VEC, int CH, bool WIDE>
   __device__ __forceinline__ static void run(const disc_program& P, const TileCtx& t, typename Vec<VEC>::T (&acc)[CH],
@@ -64,6 +74,7 @@ __global__ void __launch_bounds__(kLoopThreads, 4) k_loop(const __grid_constant_
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ float consts[DISC_MAX_LOADS];
   T* slots = reinterpret_cast<T*>(smem_raw) + threadIdx.x;
+  pdl_enter(L.prog);
   hoist_consts(L.prog, consts);
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -120,6 +131,7 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
   const int64_t cache_floats = (static_cast<int64_t>(rpb) * L.cache_loads * L.R + 3) / 4 * 4;
   float* row_cache = L.cache_loads ? reinterpret_cast<float*>(smem_raw) + sub * L.cache_loads * L.R : nullptr;
   T* slots = reinterpret_cast<T*>(reinterpret_cast<float*>(smem_raw) + cache_floats) + threadIdx.x;
+  pdl_enter(L.pre);
   hoist_consts(L.pre, consts[0]);
   hoist_consts(L.post, consts[1]);
   __syncthreads();
@@ -192,6 +204,7 @@ __global__ void __launch_bounds__(kColThreads, 4) k_col(const __grid_constant__ 
   __shared__ float consts[DISC_MAX_LOADS];
   const int tid = threadIdx.x;
   T* slots = reinterpret_cast<T*>(smem_raw) + tid;
+  pdl_enter(L.pre);
   hoist_consts(L.pre, consts);
   __syncthreads();
   const int lpc = L.group;
@@ -275,6 +288,28 @@ inline cudaError_t set_smem(K kernel, size_t bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
 }
 
+// Resident CTAs per SM for (kernel, block, dynamic smem); grid-stride kernels are sized
+// to exactly one wave (SM count x this).  Cached per host thread.
+int resident_ctas(const void* kernel, int block, size_t smem);
+
+// PDL mode (disc_cuda_set_pdl); launches go through cudaLaunchKernelEx.
+bool pdl_enabled();
+
+template <typename Arg>
+inline cudaError_t launch_k(void (*kernel)(Arg), dim3 grid, dim3 block, size_t smem, cudaStream_t s, const Arg& a) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
 // use_slots = false for generated programs (values live in registers, no slot smem).
 template <int CH = kCH, typename K>
 inline cudaError_t launch_loop_with(K kernel, const disc_loop_launch& L, cudaStream_t s, bool use_slots = true) {
@@ -284,13 +319,13 @@ inline cudaError_t launch_loop_with(K kernel, const disc_loop_launch& L, cudaStr
   const int64_t tiles = ((L.rows + rpw - 1) / rpw) * ((L.W + span - 1) / span);
   const int64_t warps_per_block = kLoopThreads / 32;
   const int64_t want = (tiles + warps_per_block - 1) / warps_per_block;
-  const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
-  const int grid = static_cast<int>(want < cap ? want : cap);
   const size_t smem = use_slots ? static_cast<size_t>(L.prog.n_slots) * CH * kLoopThreads * (L.vec == 4 ? 16 : 4) : 0;
   cudaError_t e = set_smem(kernel, smem);
   if (e != cudaSuccess) return e;
-  kernel<<<grid, kLoopThreads, smem, s>>>(L);
-  return cudaGetLastError();
+  const int64_t cap = static_cast<int64_t>(sm_count()) * resident_ctas(reinterpret_cast<const void*>(kernel), kLoopThreads, smem);
+  const int grid = static_cast<int>(want < cap ? want : cap);
+  e = launch_k(kernel, dim3(grid), dim3(kLoopThreads), smem, s, L);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int CH = kCH, typename K>
@@ -300,14 +335,14 @@ inline cudaError_t launch_row_with(K kernel, const disc_reduce_launch& L, cudaSt
   const int block = L.group > 256 ? L.group : 256;
   const int rpb = block / L.group;
   const int64_t groups = (L.K + rpb - 1) / rpb;
-  const int64_t cap = static_cast<int64_t>(sm_count()) * (2048 / block) * 2;
-  const int grid = static_cast<int>(groups < cap ? groups : cap);
   const size_t cache = static_cast<size_t>((static_cast<int64_t>(rpb) * L.cache_loads * L.R + 3) / 4 * 4) * 4;
   const size_t smem = cache + (use_slots ? static_cast<size_t>(slots) * CH * block * (L.vec == 4 ? 16 : 4) : 0);
   cudaError_t e = set_smem(kernel, smem);
   if (e != cudaSuccess) return e;
-  kernel<<<grid, block, smem, s>>>(L);
-  return cudaGetLastError();
+  const int64_t cap = static_cast<int64_t>(sm_count()) * resident_ctas(reinterpret_cast<const void*>(kernel), block, smem);
+  const int grid = static_cast<int>(groups < cap ? groups : cap);
+  e = launch_k(kernel, dim3(grid), dim3(block), smem, s, L);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // Column pass only (the finalize kernel is launched by the caller).
@@ -319,8 +354,8 @@ inline cudaError_t launch_col_with(K kernel, const disc_reduce_launch& L, cudaSt
   const size_t smem = use_slots ? static_cast<size_t>(L.pre.n_slots) * CH * kColThreads * (L.vec == 4 ? 16 : 4) : 0;
   cudaError_t e = set_smem(kernel, smem);
   if (e != cudaSuccess) return e;
-  kernel<<<grid, kColThreads, smem, s>>>(L);
-  return cudaGetLastError();
+  e = launch_k(kernel, grid, dim3(kColThreads), smem, s, L);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // Dispatch on (vec, wide, reduce kind) for a given program functor pair.

@@ -104,6 +104,16 @@ __global__ void k_flush(uint4* p, int64_t n, uint32_t salt) {
     p[i] = make_uint4(salt, static_cast<uint32_t>(i), salt, 0u);
 }
 
+// Holds the stream for `ns` nanoseconds (globaltimer), so that host submissions queue up
+// behind it and per-launch events then time device execution only.
+__global__ void k_spin(uint64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 }  // namespace disc_dev
 
 namespace disc_launch {
@@ -148,6 +158,11 @@ cudaError_t flush(void* p, size_t bytes, cudaStream_t s) {
   const int64_t n = static_cast<int64_t>(bytes / 16);
   if (n <= 0) return cudaSuccess;
   k_flush<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(static_cast<uint4*>(p), n, salt++);
+  return cudaGetLastError();
+}
+
+cudaError_t spin(uint64_t ns, cudaStream_t s) {
+  k_spin<<<1, 32, 0, s>>>(ns);
   return cudaGetLastError();
 }
 

@@ -20,6 +20,9 @@ cudaError_t concat(const disc_concat_launch& C, cudaStream_t s);
 cudaError_t gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c, cudaStream_t s);
 cudaError_t fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, cudaStream_t s);
 cudaError_t flush(void* p, size_t bytes, cudaStream_t s);
+cudaError_t spin(uint64_t ns, cudaStream_t s);
+void set_pdl(int mode);
+int pdl_mode();
 }  // namespace disc_launch
 
 // Generated fast paths (patterns_gen.cu): straight-line kernels for known program
@@ -273,7 +276,16 @@ int disc_cuda_fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float
 int disc_cuda_flush_l2(void* scratch, size_t bytes, void* stream) {
   return counted(disc_launch::flush(scratch, bytes, S(stream)), "launch flush");
 }
+int disc_cuda_spin(uint64_t microseconds, void* stream) {
+  return counted(disc_launch::spin(microseconds * 1000ull, S(stream)), "launch spin");
+}
 int64_t disc_cuda_kernel_launches(void) { return g_launches.load(); }
+
+int disc_cuda_set_pdl(int mode) {
+  disc_launch::set_pdl(mode < 0 ? 0 : (mode > 2 ? 2 : mode));
+  return 0;
+}
+int disc_cuda_pdl_mode(void) { return disc_launch::pdl_mode(); }
 
 int disc_cuda_set_specialization(int enabled) {
   g_spec_enabled = enabled != 0;

@@ -225,6 +225,7 @@ class ProgramBuilder {
     P.n_instr = n;
     P.n_slots = nslots;
     P.cache_mode = DISC_CACHE_NONE;
+    P.flags = disc_cuda_pdl_mode() == 2 ? DISC_PROG_PDL_EARLY : 0;
     for (int l = 0; l < DISC_MAX_LOADS; ++l) P.cache_slot[l] = -1;
     P.n_loads = static_cast<int32_t>(maps_.size());
     for (size_t l = 0; l < maps_.size(); ++l) P.loads[l].ptr = ptrs_[l];
