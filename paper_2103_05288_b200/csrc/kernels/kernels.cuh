@@ -22,13 +22,21 @@ __device__ __forceinline__ void pdl_enter(const disc_program& P) {
   if (P.flags & DISC_PROG_PDL_EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Program functors: run<VEC, CH, WIDE>(program, tile, acc, ...).  kSplitFull: the schedule
+// instantiates a guard-free body for full tiles (generated programs); the interpreter
+// keeps one body.
 struct Interp {
-  template <int VEC, int CH, bool WIDE>
-  __device__ __forceinline__ static void run(const disc_program& P, const TileCtx& t, typename Vec<VEC>::T (&acc)[CH],
+  static constexpr bool kSplitFull = false;
+  template <int VEC, int CH, bool WIDE, typename Ctx>
+  __device__ __forceinline__ static void run(const disc_program& P, const Ctx& t, typename Vec<VEC>::T (&acc)[CH],
                                              typename Vec<VEC>::T* slots, int stride, const float* consts, float red) {
-    run_tile<VEC, CH, WIDE>(P, t, acc, slots, stride, consts, red);
+    const TileCtx t64{t.row, t.col0, t.W, t.cstride, t.nvalid, t.cache};
+    run_tile<VEC, CH, WIDE>(P, t64, acc, slots, stride, consts, red);
   }
 };
+
+template <bool WIDE>
+using IndexT = typename std::conditional<WIDE, int64_t, int32_t>::type;
 
 
 // Reduction helpers.  Sums accumulate in f64 (the reference's semantics); max is exact in
@@ -71,6 +79,7 @@ constexpr int kCH = 2;  // chunks per thread per dispatch
 template <int VEC, bool WIDE, typename Prog, int CH = kCH>
 __global__ void __launch_bounds__(kLoopThreads, 4) k_loop(const __grid_constant__ disc_loop_launch L) {
   using T = typename Vec<VEC>::T;
+  using I = IndexT<WIDE>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ float consts[DISC_MAX_LOADS];
   T* slots = reinterpret_cast<T*>(smem_raw) + threadIdx.x;
@@ -81,25 +90,34 @@ __global__ void __launch_bounds__(kLoopThreads, 4) k_loop(const __grid_constant_
   const int lpr = L.lpr;
   const int rpw = 32 / lpr;
   const int sub = lane / lpr;
-  const int64_t cstride = static_cast<int64_t>(lpr) * VEC;
-  const int64_t span = cstride * CH;
-  const int64_t tpr = (L.W + span - 1) / span;
-  const int64_t ntiles = ((L.rows + rpw - 1) / rpw) * tpr;
+  const I W = static_cast<I>(L.W), rows = static_cast<I>(L.rows);
+  const I cstride = static_cast<I>(lpr) * VEC;
+  const I span = cstride * CH;
+  const I tpr = (W + span - 1) / span;
+  const I nrg = (rows + rpw - 1) / rpw;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  int64_t tile = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t tile = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   // (row group, column tile) advanced incrementally: one division per thread, not per tile.
-  int64_t rg = tile / tpr, tc = tile - rg * tpr;
-  const int64_t drg = warps / tpr, dtc = warps - drg * tpr;
-  const int64_t lane_col = (lane & (lpr - 1)) * VEC;
-  for (; tile < ntiles; tile += warps) {
-    TileCtx t;
-    t.row = rg * rpw + sub;
-    t.col0 = tc * span + lane_col;
-    t.W = L.W;
-    t.cstride = cstride;
-    t.nvalid = t.row >= L.rows ? 0 : chunks_in_row<CH>(L.W - t.col0, cstride);
-    T acc[CH];
-    Prog::template run<VEC, CH, WIDE>(L.prog, t, acc, slots, kLoopThreads, consts, 0.f);
+  I rg = static_cast<I>(tile / tpr), tc = static_cast<I>(tile - static_cast<int64_t>(rg) * tpr);
+  const I drg = static_cast<I>(warps / tpr), dtc = static_cast<I>(warps - static_cast<int64_t>(drg) * tpr);
+  const I lane_col = static_cast<I>(lane & (lpr - 1)) * VEC;
+  for (; rg < nrg;) {
+    const I row = rg * rpw + sub;
+    const I col0 = tc * span + lane_col;
+    if (row < rows) {
+      const int nv = chunks_in_row<CH>(W - col0, cstride);
+      T acc[CH];
+      if (!Prog::kSplitFull) {
+        if (nv > 0) Prog::template run<VEC, CH, WIDE>(L.prog, Tile<I, false>{row, col0, W, cstride, nv}, acc, slots,
+                                                       kLoopThreads, consts, 0.f);
+      } else if (nv == CH) {
+        Prog::template run<VEC, CH, WIDE>(L.prog, Tile<I, true>{row, col0, W, cstride, CH}, acc, slots, kLoopThreads,
+                                          consts, 0.f);
+      } else if (CH > 1 && nv > 0) {
+        Prog::template run<VEC, CH, WIDE>(L.prog, Tile<I, false>{row, col0, W, cstride, nv}, acc, slots,
+                                          kLoopThreads, consts, 0.f);
+      }
+    }
     rg += drg;
     tc += dtc;
     if (tc >= tpr) {
@@ -135,23 +153,33 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
   hoist_consts(L.pre, consts[0]);
   hoist_consts(L.post, consts[1]);
   __syncthreads();
+  using I = IndexT<WIDE>;
   const int64_t rows = L.K;
+  const I R = static_cast<I>(L.R);
   const bool fuse_post = L.post.n_instr > 0;
-  const int64_t cstride = static_cast<int64_t>(G) * VEC;
-  const int64_t span = cstride * CH;
+  const I cstride = static_cast<I>(G) * VEC;
+  const I span = cstride * CH;
 
   for (int64_t base = static_cast<int64_t>(blockIdx.x) * rpb; base < rows; base += static_cast<int64_t>(gridDim.x) * rpb) {
-    const int64_t row = base + sub;
-    const bool valid = row < rows;
+    const I row = static_cast<I>(base + sub);
+    const bool valid = base + sub < rows;
     Acc acc = RD::identity();
     if (valid) {
-      for (int64_t col0 = static_cast<int64_t>(lane) * VEC; col0 < L.R; col0 += span) {
-        TileCtx t{row, col0, L.R, cstride, chunks_in_row<CH>(L.R - col0, cstride), row_cache};
+      for (I col0 = static_cast<I>(lane) * VEC; col0 < R; col0 += span) {
+        const int nv = chunks_in_row<CH>(R - col0, cstride);
         T v[CH];
-        Pre::template run<VEC, CH, WIDE>(L.pre, t, v, slots, blockDim.x, consts[0], 0.f);
+        if (Pre::kSplitFull && nv == CH) {
+          Pre::template run<VEC, CH, WIDE>(L.pre, Tile<I, true>{row, col0, R, cstride, CH, row_cache}, v, slots,
+                                           blockDim.x, consts[0], 0.f);
 #pragma unroll
-        for (int c = 0; c < CH; ++c)
-          if (c < t.nvalid) acc = RD::acc(acc, v[c]);
+          for (int c = 0; c < CH; ++c) acc = RD::acc(acc, v[c]);
+        } else {
+          Pre::template run<VEC, CH, WIDE>(L.pre, Tile<I, false>{row, col0, R, cstride, nv, row_cache}, v, slots,
+                                           blockDim.x, consts[0], 0.f);
+#pragma unroll
+          for (int c = 0; c < CH; ++c)
+            if (c < nv) acc = RD::acc(acc, v[c]);
+        }
       }
     }
     const int width = G < 32 ? G : 32;
@@ -175,10 +203,15 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
     if (valid) {
       if (lane == 0 && L.red_out) L.red_out[row] = result;
       if (fuse_post) {
-        for (int64_t col0 = static_cast<int64_t>(lane) * VEC; col0 < L.R; col0 += span) {
-          TileCtx t{row, col0, L.R, cstride, chunks_in_row<CH>(L.R - col0, cstride), row_cache};
+        for (I col0 = static_cast<I>(lane) * VEC; col0 < R; col0 += span) {
+          const int nv = chunks_in_row<CH>(R - col0, cstride);
           T v[CH];
-          Post::template run<VEC, CH, WIDE>(L.post, t, v, slots, blockDim.x, consts[1], result);
+          if (Post::kSplitFull && nv == CH)
+            Post::template run<VEC, CH, WIDE>(L.post, Tile<I, true>{row, col0, R, cstride, CH, row_cache}, v, slots,
+                                              blockDim.x, consts[1], result);
+          else
+            Post::template run<VEC, CH, WIDE>(L.post, Tile<I, false>{row, col0, R, cstride, nv, row_cache}, v, slots,
+                                              blockDim.x, consts[1], result);
         }
       }
     }
@@ -226,11 +259,10 @@ __global__ void __launch_bounds__(kColThreads, 4) k_col(const __grid_constant__ 
   Acc acc[CH * VEC];
 #pragma unroll
   for (int i = 0; i < CH * VEC; ++i) acc[i] = RD::identity();
-  if (nvalid > 0) {
+  auto rows_loop = [&](auto tile_of) {
     for (int64_t r = r0 + warp * rpw + sub; r < r1; r += rows_per_pass) {
-      TileCtx t{k * L.R + r, col0, L.C, cstride, nvalid};
       T v[CH];
-      Pre::template run<VEC, CH, WIDE>(L.pre, t, v, slots, kColThreads, consts, 0.f);
+      Pre::template run<VEC, CH, WIDE>(L.pre, tile_of(k * L.R + r), v, slots, kColThreads, consts, 0.f);
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
         if constexpr (VEC == 1) {
@@ -243,7 +275,16 @@ __global__ void __launch_bounds__(kColThreads, 4) k_col(const __grid_constant__ 
         }
       }
     }
-  }
+  };
+  using I = IndexT<WIDE>;
+  if (Pre::kSplitFull && nvalid == CH)
+    rows_loop([&](int64_t row) {
+      return Tile<I, true>{static_cast<I>(row), static_cast<I>(col0), static_cast<I>(L.C), static_cast<I>(cstride), CH};
+    });
+  else if (nvalid > 0)
+    rows_loop([&](int64_t row) {
+      return Tile<I, false>{static_cast<I>(row), static_cast<I>(col0), static_cast<I>(L.C), static_cast<I>(cstride), nvalid};
+    });
 #pragma unroll
   for (int i = 0; i < CH * VEC; ++i) part[tid][i] = acc[i];
   __syncthreads();
@@ -359,10 +400,12 @@ inline cudaError_t launch_col_with(K kernel, const disc_reduce_launch& L, cudaSt
 }
 
 // Dispatch on (vec, wide, reduce kind) for a given program functor pair.
-template <typename Pre, typename Post, int CH = kCH>
-inline cudaError_t row_pass(const disc_reduce_launch& L, cudaStream_t s, bool use_slots, bool allow_wide = true) {
+// ALLOW_WIDE = false (generated programs, used only on !wide launches) instantiates no
+// 64-bit-index kernels.
+template <typename Pre, typename Post, int CH = kCH, bool ALLOW_WIDE = true>
+inline cudaError_t row_pass(const disc_reduce_launch& L, cudaStream_t s, bool use_slots) {
   const bool sum = L.kind == DISC_REDUCE_SUM;
-  if (L.wide && allow_wide) {
+  if constexpr (ALLOW_WIDE) if (L.wide) {
     if (L.vec == 4) return sum ? launch_row_with<CH>(k_row<4, true, DISC_REDUCE_SUM, Pre, Post, CH>, L, s, use_slots)
                                : launch_row_with<CH>(k_row<4, true, DISC_REDUCE_MAX, Pre, Post, CH>, L, s, use_slots);
     return sum ? launch_row_with<CH>(k_row<1, true, DISC_REDUCE_SUM, Pre, Post, CH>, L, s, use_slots)
@@ -374,10 +417,10 @@ inline cudaError_t row_pass(const disc_reduce_launch& L, cudaStream_t s, bool us
              : launch_row_with<CH>(k_row<1, false, DISC_REDUCE_MAX, Pre, Post, CH>, L, s, use_slots);
 }
 
-template <typename Pre, int CH = kCH>
-inline cudaError_t col_pass_t(const disc_reduce_launch& L, cudaStream_t s, bool use_slots, bool allow_wide = true) {
+template <typename Pre, int CH = kCH, bool ALLOW_WIDE = true>
+inline cudaError_t col_pass_t(const disc_reduce_launch& L, cudaStream_t s, bool use_slots) {
   const bool sum = L.kind == DISC_REDUCE_SUM;
-  if (L.wide && allow_wide) {
+  if constexpr (ALLOW_WIDE) if (L.wide) {
     if (L.vec == 4) return sum ? launch_col_with<CH>(k_col<4, true, DISC_REDUCE_SUM, Pre, CH>, L, s, use_slots)
                                : launch_col_with<CH>(k_col<4, true, DISC_REDUCE_MAX, Pre, CH>, L, s, use_slots);
     return sum ? launch_col_with<CH>(k_col<1, true, DISC_REDUCE_SUM, Pre, CH>, L, s, use_slots)

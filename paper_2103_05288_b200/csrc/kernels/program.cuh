@@ -34,7 +34,7 @@ __device__ __forceinline__ float bin1(float a, float b) {
   if constexpr (OP == 0) return __fadd_rn(a, b);
   if constexpr (OP == 1) return __fsub_rn(a, b);
   if constexpr (OP == 2) return __fmul_rn(a, b);
-  if constexpr (OP == 3) return __fdiv_rn(a, b);
+  if constexpr (OP == 3) return __fdiv_rn(a, b);  // IEEE: unfused plans are bit-exact
   return op_max(a, b);
 }
 template <int OP>
@@ -92,38 +92,44 @@ __device__ __forceinline__ float ldg(const float* p) { return __ldg(p); }
 
 // A tile: CH chunks of VEC elements in row `row`; chunk c starts at column
 // col0 + c*cstride (cstride = warp/group width * VEC keeps every access coalesced).
-struct TileCtx {
-  int64_t row;
-  int64_t col0;
-  int64_t W;
-  int64_t cstride;
-  int nvalid;           // leading chunks inside the row
+// I is the index type: int32_t for launches whose every address fits in 31 bits (!wide),
+// int64_t otherwise; FULL tiles have all CH chunks inside the row (no per-chunk guard).
+template <typename I, bool FULL>
+struct Tile {
+  using Index = I;
+  I row;
+  I col0;
+  I W;
+  I cstride;
+  int nvalid;              // leading chunks inside the row (== CH when FULL)
   float* cache = nullptr;  // row cache of this row (slot k at cache + k*W), or null
+  __device__ __forceinline__ bool has(int c) const { return FULL || c < nvalid; }
 };
+using TileCtx = Tile<int64_t, false>;
 
 // Row cache: fill on the reduce pass, read on the epilogue (see disc_cache_mode).
-template <int VEC, int CH>
-__device__ __forceinline__ bool cached_load(const disc_program& P, const TileCtx& t, int l,
+template <int VEC, int CH, typename Ctx>
+__device__ __forceinline__ bool cached_load(const disc_program& P, const Ctx& t, int l,
                                             typename Vec<VEC>::T (&v)[CH]) {
   if (P.cache_mode != DISC_CACHE_READ || P.cache_slot[l] < 0 || !t.cache) return false;
   const float* c0 = t.cache + P.cache_slot[l] * t.W + t.col0;
 #pragma unroll
   for (int c = 0; c < CH; ++c)
-    if (c < t.nvalid) {
+    if (t.has(c)) {
       if constexpr (VEC == 1) v[c] = c0[c * t.cstride];
       else v[c] = *reinterpret_cast<const float4*>(c0 + c * t.cstride);
     }
   return true;
 }
 
-template <int VEC, int CH>
-__device__ __forceinline__ void cache_fill(const disc_program& P, const TileCtx& t, int l,
+template <int VEC, int CH, typename Ctx>
+__device__ __forceinline__ void cache_fill(const disc_program& P, const Ctx& t, int l,
                                            const typename Vec<VEC>::T (&v)[CH]) {
   if (P.cache_mode != DISC_CACHE_FILL || P.cache_slot[l] < 0 || !t.cache) return;
   float* c0 = t.cache + P.cache_slot[l] * t.W + t.col0;
 #pragma unroll
   for (int c = 0; c < CH; ++c)
-    if (c < t.nvalid) {
+    if (t.has(c)) {
       if constexpr (VEC == 1) c0[c * t.cstride] = v[c];
       else *reinterpret_cast<float4*>(c0 + c * t.cstride) = v[c];
     }
@@ -170,68 +176,35 @@ __device__ __forceinline__ void hoist_consts(const disc_program& P, float* const
 
 // --- building blocks for generated (straight-line) programs --------------------------
 
-// One load of a tile, dispatched on the load's binding mode (warp-uniform branch).
-template <int VEC, int CH, bool WIDE>
-__device__ __forceinline__ void load_any(const disc_program& P, const TileCtx& t, const float* consts, int l,
-                                         typename Vec<VEC>::T (&v)[CH]) {
-  const disc_load& L = P.loads[l];
-  const int64_t f0 = t.row * t.W + t.col0;
-  switch (L.mode) {
-    case DISC_LOAD_IDENTITY: {
-      if (cached_load<VEC, CH>(P, t, l, v)) break;
-      const float* base = L.ptr + f0;
-#pragma unroll
-      for (int c = 0; c < CH; ++c)
-        if (c < t.nvalid) {
-          if constexpr (VEC == 1) v[c] = ldg(base + c * t.cstride);
-          else v[c] = __ldg(reinterpret_cast<const float4*>(base + c * t.cstride));
-        }
-      cache_fill<VEC, CH>(P, t, l, v);
-      break;
-    }
-    case DISC_LOAD_AFFINE: {
-      const float* base = L.ptr + L.offset + t.row * L.rs;
-#pragma unroll
-      for (int c = 0; c < CH; ++c)
-        if (c < t.nvalid) v[c] = load_row<VEC>(L, base, t.col0 + c * t.cstride);
-      break;
-    }
-    case DISC_LOAD_GATHER:
-#pragma unroll
-      for (int c = 0; c < CH; ++c)
-        if (c < t.nvalid) v[c] = load_gather<VEC, WIDE>(L, f0 + c * t.cstride);
-      break;
-    default: {
-      const float x = consts[l];
-#pragma unroll
-      for (int c = 0; c < CH; ++c) v[c] = splat(x, v[c]);
-    }
-  }
-}
-
-// Load classes (structural: part of a generated pattern's key).
-enum LoadClass { kLcIdentity = 0, kLcConst = 1, kLcSplat = 2, kLcContig = 3, kLcStrided = 4, kLcGather = 5 };
+// Load classes (structural: part of a generated pattern's key).  Contiguous row loads
+// split on whether the launch's vector width can load them whole (vec_ok == 1).
+enum LoadClass {
+  kLcIdentity = 0, kLcConst = 1, kLcSplat = 2, kLcContig = 3, kLcStrided = 4, kLcGather = 5, kLcContigU = 6
+};
 
 __host__ __device__ inline int load_class(const disc_load& L) {
   switch (L.mode) {
     case DISC_LOAD_IDENTITY: return kLcIdentity;
     case DISC_LOAD_CONST: return kLcConst;
-    case DISC_LOAD_AFFINE: return L.cs == 0 ? kLcSplat : (L.cs == 1 ? kLcContig : kLcStrided);
+    case DISC_LOAD_AFFINE:
+      return L.cs == 0 ? kLcSplat : (L.cs == 1 ? (L.vec_ok == 1 ? kLcContig : kLcContigU) : kLcStrided);
     default: return kLcGather;
   }
 }
 
-// One load of a tile with its binding class known at compile time.
-template <int VEC, int CH, bool WIDE, int CLS>
-__device__ __forceinline__ void load_cls(const disc_program& P, const TileCtx& t, const float* consts, int l,
+// One load of a tile with its binding class known at compile time.  Index math in the
+// tile's index type (32-bit for !wide launches: one wide multiply-add per pointer).
+template <int VEC, int CH, bool WIDE, int CLS, typename Ctx>
+__device__ __forceinline__ void load_cls(const disc_program& P, const Ctx& t, const float* consts, int l,
                                          typename Vec<VEC>::T (&v)[CH]) {
+  using I = typename Ctx::Index;
   const disc_load& L = P.loads[l];
   if constexpr (CLS == kLcIdentity) {
     if (cached_load<VEC, CH>(P, t, l, v)) return;
     const float* base = L.ptr + (t.row * t.W + t.col0);
 #pragma unroll
     for (int c = 0; c < CH; ++c)
-      if (c < t.nvalid) {
+      if (t.has(c)) {
         if constexpr (VEC == 1) v[c] = ldg(base + c * t.cstride);
         else v[c] = __ldg(reinterpret_cast<const float4*>(base + c * t.cstride));
       }
@@ -241,40 +214,43 @@ __device__ __forceinline__ void load_cls(const disc_program& P, const TileCtx& t
 #pragma unroll
     for (int c = 0; c < CH; ++c) v[c] = splat(x, v[c]);
   } else if constexpr (CLS == kLcSplat) {  // value depends on the row only
-    const float x = ldg(L.ptr + L.offset + t.row * L.rs);
+    const float x = ldg(L.ptr + (static_cast<I>(L.offset) + t.row * static_cast<I>(L.rs)));
 #pragma unroll
     for (int c = 0; c < CH; ++c) v[c] = splat(x, v[c]);
-  } else if constexpr (CLS == kLcContig) {
-    const float* base = L.ptr + L.offset + t.row * L.rs + t.col0;
+  } else if constexpr (CLS == kLcContig || CLS == kLcContigU) {
+    const float* base = L.ptr + (static_cast<I>(L.offset) + t.row * static_cast<I>(L.rs) + t.col0);
 #pragma unroll
     for (int c = 0; c < CH; ++c)
-      if (c < t.nvalid) {
-        if constexpr (VEC == 1) {
-          v[c] = ldg(base + c * t.cstride);
-        } else {
-          const float* p = base + c * t.cstride;
-          v[c] = L.vec_ok == 1 ? __ldg(reinterpret_cast<const float4*>(p)) : make_float4(ldg(p), ldg(p + 1), ldg(p + 2), ldg(p + 3));
-        }
+      if (t.has(c)) {
+        const float* p = base + c * t.cstride;
+        if constexpr (VEC == 1) v[c] = ldg(p);
+        else if constexpr (CLS == kLcContig) v[c] = __ldg(reinterpret_cast<const float4*>(p));
+        else v[c] = make_float4(ldg(p), ldg(p + 1), ldg(p + 2), ldg(p + 3));
       }
-  } else if constexpr (CLS == kLcStrided) {
-    const float* base = L.ptr + L.offset + t.row * L.rs;
+  } else if constexpr (CLS == kLcStrided) {  // cs not in {0, 1}: element loads
+    const I cs = static_cast<I>(L.cs);
+    const float* base = L.ptr + (static_cast<I>(L.offset) + t.row * static_cast<I>(L.rs));
 #pragma unroll
     for (int c = 0; c < CH; ++c)
-      if (c < t.nvalid) v[c] = load_row<VEC>(L, base, t.col0 + c * t.cstride);
+      if (t.has(c)) {
+        const float* p = base + (t.col0 + c * t.cstride) * cs;
+        if constexpr (VEC == 1) v[c] = ldg(p);
+        else v[c] = make_float4(ldg(p), ldg(p + cs), ldg(p + 2 * cs), ldg(p + 3 * cs));
+      }
   } else {
-    const int64_t f0 = t.row * t.W + t.col0;
+    const int64_t f0 = static_cast<int64_t>(t.row) * t.W + t.col0;
 #pragma unroll
     for (int c = 0; c < CH; ++c)
-      if (c < t.nvalid) v[c] = load_gather<VEC, WIDE>(L, f0 + c * t.cstride);
+      if (t.has(c)) v[c] = load_gather<VEC, WIDE>(L, f0 + c * t.cstride);
   }
 }
 
-template <int VEC, int CH>
-__device__ __forceinline__ void store_tile(float* out, const TileCtx& t, const typename Vec<VEC>::T (&v)[CH]) {
-  float* o = out + t.row * t.W + t.col0;
+template <int VEC, int CH, typename Ctx>
+__device__ __forceinline__ void store_tile(float* out, const Ctx& t, const typename Vec<VEC>::T (&v)[CH]) {
+  float* o = out + (t.row * t.W + t.col0);
 #pragma unroll
   for (int c = 0; c < CH; ++c)
-    if (c < t.nvalid) {
+    if (t.has(c)) {
       if constexpr (VEC == 1) o[c * t.cstride] = v[c];
       else *reinterpret_cast<float4*>(o + c * t.cstride) = v[c];
     }

@@ -298,17 +298,18 @@ void bind_view(Built& b, int64_t W) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-// VEC=4 feasibility for every load/output of the programs on a [*, W] view; sets vec_ok.
+// VEC=4 feasibility for every load/output of the programs on a [*, W] view; sets vec_ok
+// (whether each load can be fetched whole at the chosen vector width).
 int choose_vec(const std::vector<Built*>& progs, int64_t W) {
-  if (W % 4 != 0) return 1;
+  bool v4 = W % 4 == 0;
   for (Built* b : progs) {
     disc_program& P = b->prog;
-    for (int o = 0; o < P.n_outs; ++o)
-      if (!aligned16(P.outs[o])) return 1;
-    for (int l = 0; l < P.n_loads; ++l) {
+    for (int o = 0; o < P.n_outs && v4; ++o)
+      if (!aligned16(P.outs[o])) v4 = false;
+    for (int l = 0; l < P.n_loads && v4; ++l) {
       const disc_load& L = P.loads[l];
-      if (L.mode == DISC_LOAD_IDENTITY && !aligned16(L.ptr)) return 1;
-      if (L.mode == DISC_LOAD_GATHER && L.dims[L.rank - 1] % 4 != 0) return 1;
+      if (L.mode == DISC_LOAD_IDENTITY && !aligned16(L.ptr)) v4 = false;
+      if (L.mode == DISC_LOAD_GATHER && L.dims[L.rank - 1] % 4 != 0) v4 = false;
     }
   }
   for (Built* b : progs) {
@@ -316,17 +317,36 @@ int choose_vec(const std::vector<Built*>& progs, int64_t W) {
     for (int l = 0; l < P.n_loads; ++l) {
       disc_load& L = P.loads[l];
       if (L.mode == DISC_LOAD_AFFINE) {
-        L.vec_ok = L.cs == 0 ? 2 : (L.cs == 1 && aligned16(L.ptr) && L.offset % 4 == 0 && L.rs % 4 == 0) ? 1 : 0;
+        const bool ok = !v4 || (aligned16(L.ptr) && L.offset % 4 == 0 && L.rs % 4 == 0);
+        L.vec_ok = L.cs == 0 ? 2 : (L.cs == 1 && ok) ? 1 : 0;
       } else if (L.mode == DISC_LOAD_GATHER) {
         const int r = L.rank;
         const int64_t inner = L.strides[r - 1];
-        bool ok = inner == 1 && aligned16(L.ptr) && L.offset % 4 == 0;
-        for (int d = 0; d < r - 1 && ok; ++d) ok = L.strides[d] % 4 == 0;
+        bool ok = inner == 1 && (!v4 || (aligned16(L.ptr) && L.offset % 4 == 0));
+        for (int d = 0; d < r - 1 && ok && v4; ++d) ok = L.strides[d] % 4 == 0;
         L.vec_ok = inner == 0 ? 2 : (ok ? 1 : 0);
       }
     }
   }
-  return 4;
+  return v4 ? 4 : 1;
+}
+
+// Largest element index any load of P can touch on a [rows, W] view: kernels index in 32
+// bits unless this (or the view itself) reaches 2^31 (the launch's `wide` flag).
+int64_t max_reach(const disc_program& P, int64_t rows, int64_t W) {
+  int64_t m = rows * W;
+  for (int l = 0; l < P.n_loads; ++l) {
+    const disc_load& L = P.loads[l];
+    int64_t r = L.offset;
+    if (L.mode == DISC_LOAD_AFFINE) {
+      r += std::max<int64_t>(rows - 1, 0) * std::abs(L.rs) + std::max<int64_t>(W - 1, 0) * std::abs(L.cs) + 3;
+    } else if (L.mode == DISC_LOAD_GATHER) {
+      for (int d = 0; d < L.rank; ++d) r += std::max<int64_t>(L.dims[d] - 1, 0) * std::abs(L.strides[d]);
+      r += 3;
+    }
+    m = std::max(m, r);
+  }
+  return m;
 }
 
 // Row width for an elementwise launch: the innermost extent that makes the most loads
@@ -371,7 +391,7 @@ disc_loop_launch make_loop(Built& b, int64_t total) {
   L.total = total;
   L.W = W;
   L.rows = total / W;
-  L.wide = total > kWideLimitView;
+  L.wide = total > kWideLimitView || max_reach(L.prog, L.rows, W) > kWideLimitView;
   L.lpr = lanes_per_row(W, L.vec);
   return L;
 }
@@ -871,6 +891,12 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
   }
   R.pre = pre.prog;
   R.post = post.prog;
+  if (!empty && R.schedule != DISC_SCHED_GENERIC) {
+    const bool row_view = R.schedule == DISC_SCHED_ROW;
+    const int64_t vrows = row_view ? R.K : R.K * R.R, vW = row_view ? R.R : R.C;
+    if (max_reach(R.pre, vrows, vW) > kWideLimit || (post_fused && max_reach(R.post, vrows, vW) > kWideLimit))
+      R.wide = 1;
+  }
 
   if (R.schedule == DISC_SCHED_ROW) {
     // ~32 chunks per thread (a warp per row for R = 4096: no block barriers), widened

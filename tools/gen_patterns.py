@@ -73,8 +73,9 @@ def gen_program(fn, prog):
     """Straight-line body for one program (code from the capture)."""
     code = prog["code"]
     lines = [f"struct {fn} {{",
-             "  template <int VEC, int CH, bool WIDE>",
-             "  __device__ __forceinline__ static void run(const disc_program& P, const TileCtx& t,",
+             "  static constexpr bool kSplitFull = true;",
+             "  template <int VEC, int CH, bool WIDE, typename Ctx>",
+             "  __device__ __forceinline__ static void run(const disc_program& P, const Ctx& t,",
              "      typename Vec<VEC>::T (&acc)[CH], typename Vec<VEC>::T*, int, const float* consts, float red) {",
              "    using T = typename Vec<VEC>::T;"]
     slot_val = {}
@@ -135,10 +136,10 @@ def generate():
                          f" : launch_loop_with<kGenCH>(k_loop<1, false, Pre_{tag}, kGenCH>, L, s, false);")
         elif kind == "row":
             parts.append("  const auto& L = *static_cast<const disc_reduce_launch*>(l);")
-            parts.append(f"  return row_pass<Pre_{tag}, Post_{tag}, kGenCH>(L, s, false, false);")
+            parts.append(f"  return row_pass<Pre_{tag}, Post_{tag}, kGenCH, false>(L, s, false);")
         else:
             parts.append("  const auto& L = *static_cast<const disc_reduce_launch*>(l);")
-            parts.append(f"  return col_pass_t<Pre_{tag}, kGenCH>(L, s, false, false);")
+            parts.append(f"  return col_pass_t<Pre_{tag}, kGenCH, false>(L, s, false);")
         parts.append("}")
         parts.append("")
         entries.append((["loop", "row", "col"].index(kind), key, f"launch_{tag}"))
