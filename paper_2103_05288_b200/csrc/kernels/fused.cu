@@ -17,16 +17,23 @@ __device__ __forceinline__ double red_join(int kind, double a, double b) {
   return kind == DISC_REDUCE_SUM ? a + b : ((a < b) ? b : a);
 }
 
-// Finalize split-R partials: ordered join over splits (two-pass) or cast (atomic).
-// Finalize split-R partials: a block owns 32 outputs x 8 split lanes; lane s joins
-// splits s, s+8, ... in order, then the 8 lane partials are joined in lane order
-// (deterministic); atomic schedules just cast.
+// Finalize split-R partials (two-pass) or cast the f64 atomic accumulators.  A block owns
+// 256/lpo outputs with lpo lanes each (lpo grows with the split count, so a few outputs
+// over many splits still spread across the block); lane s joins splits s, s+lpo, ... in
+// order, then the lanes are joined by a fixed tree (deterministic for a given split count).
+__device__ __host__ inline int finalize_lanes(int splits) {
+  int l = 8;
+  while (l < 256 && l * 4 < splits) l <<= 1;
+  return l;
+}
+
 __global__ void __launch_bounds__(256) k_col_finalize(const __grid_constant__ disc_reduce_launch L) {
-  __shared__ double part[8][33];
+  __shared__ double part[256];
   pdl_enter(L.pre);
   const int64_t n = L.K * L.C;
-  const int ox = threadIdx.x & 31, sl = threadIdx.x >> 5;
-  for (int64_t base = static_cast<int64_t>(blockIdx.x) * 32; base < n; base += static_cast<int64_t>(gridDim.x) * 32) {
+  const int lpo = finalize_lanes(L.splits), opb = 256 / lpo;
+  const int ox = threadIdx.x / lpo, sl = threadIdx.x % lpo;
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * opb; base < n; base += static_cast<int64_t>(gridDim.x) * opb) {
     const int64_t o = base + ox;
     if (L.schedule != DISC_SCHED_COL_TWOPASS) {
       if (sl == 0 && o < n) L.red_out[o] = static_cast<float>(L.workspace[o]);
@@ -34,14 +41,14 @@ __global__ void __launch_bounds__(256) k_col_finalize(const __grid_constant__ di
     }
     double t = red_identity(L.kind);
     if (o < n)
-      for (int s = sl; s < L.splits; s += 8) t = red_join(L.kind, t, L.workspace[static_cast<int64_t>(s) * n + o]);
-    part[sl][ox] = t;
+      for (int s = sl; s < L.splits; s += lpo) t = red_join(L.kind, t, L.workspace[static_cast<int64_t>(s) * n + o]);
+    part[threadIdx.x] = t;
     __syncthreads();
-    if (sl == 0 && o < n) {
-      double r = part[0][ox];
-      for (int u = 1; u < 8; ++u) r = red_join(L.kind, r, part[u][ox]);
-      L.red_out[o] = static_cast<float>(r);
+    for (int w = lpo / 2; w > 0; w >>= 1) {
+      if (sl < w) part[threadIdx.x] = red_join(L.kind, part[threadIdx.x], part[threadIdx.x + w]);
+      __syncthreads();
     }
+    if (sl == 0 && o < n) L.red_out[o] = static_cast<float>(part[threadIdx.x]);
     __syncthreads();
   }
 }
@@ -139,7 +146,8 @@ cudaError_t col_pass(const disc_reduce_launch& L, cudaStream_t s);
 cudaError_t finalize_columns(const disc_reduce_launch& L, cudaStream_t s) {
   if (L.schedule == DISC_SCHED_COL_SINGLE) return cudaSuccess;
   const int64_t n = L.K * L.C;
-  const int64_t want = (n + 31) / 32;
+  const int64_t opb = 256 / finalize_lanes(L.splits);
+  const int64_t want = (n + opb - 1) / opb;
   const cudaError_t e = launch_k(k_col_finalize, dim3(static_cast<int>(want < sm_count() * 8 ? want : sm_count() * 8)),
                                  dim3(256), 0, s, L);
   return e != cudaSuccess ? e : cudaGetLastError();

@@ -30,8 +30,18 @@ struct Interp {
   template <int VEC, int CH, bool WIDE, typename Ctx>
   __device__ __forceinline__ static void run(const disc_program& P, const Ctx& t, typename Vec<VEC>::T (&acc)[CH],
                                              typename Vec<VEC>::T* slots, int stride, const float* consts, float red) {
-    const TileCtx t64{t.row, t.col0, t.W, t.cstride, t.nvalid, t.cache};
-    run_tile<VEC, CH, WIDE>(P, t64, acc, slots, stride, consts, red);
+    if constexpr (Ctx::kRows) {  // row tiles: one single-chunk interpreter pass per row
+      using T = typename Vec<VEC>::T;
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+        if (t.has(c)) {
+          const TileCtx t1{t.row + c * t.cstride, t.col0, t.W, t.cstride, 1, nullptr};
+          run_tile<VEC, 1, WIDE>(P, t1, reinterpret_cast<T(&)[1]>(acc[c]), slots, stride, consts, red);
+        }
+    } else {
+      const TileCtx t64{t.row, t.col0, t.W, t.cstride, t.nvalid, t.cache};
+      run_tile<VEC, CH, WIDE>(P, t64, acc, slots, stride, consts, red);
+    }
   }
 };
 
@@ -221,10 +231,12 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
 
 // ---------------------------------------------------------------------------
 // Column schedule: reduce arg collapsed to [K, R, C], reduce over R, C contiguous; viewed
-// as rows k*R + r of width C.  A warp spans 32/lpc rows x (lpc*CH*VEC) columns (lpc =
-// L.group lanes per row segment, so narrow C packs many rows per warp); 8 warps per
-// block; grid.x = K * ceil(C / span), grid.y = R splits.  Per-thread partials are joined
-// per column through shared memory in a fixed order.
+// as rows k*R + r of width C.  A thread owns VEC columns; lpc = L.group lanes span a row
+// segment of lpc*VEC columns and a warp covers 32/lpc rows (narrow C packs many rows per
+// warp).  Each step a thread evaluates CH rows (row tiles: CH loads in flight for the
+// same columns), so only VEC accumulators are live.  8 warps per block; grid.x = K *
+// ceil(C / (lpc*VEC)), grid.y = R splits.  Per-thread partials are joined per column
+// through shared memory in a fixed order (deterministic).
 constexpr int kColThreads = 256;
 
 template <int VEC, bool WIDE, int KIND, typename Pre, int CH = kCH>
@@ -232,8 +244,9 @@ __global__ void __launch_bounds__(kColThreads, 4) k_col(const __grid_constant__ 
   using T = typename Vec<VEC>::T;
   using RD = Red<KIND>;
   using Acc = typename RD::Acc;
+  using I = IndexT<WIDE>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ Acc part[kColThreads][CH * VEC];
+  __shared__ Acc part[kColThreads][VEC];
   __shared__ float consts[DISC_MAX_LOADS];
   const int tid = threadIdx.x;
   T* slots = reinterpret_cast<T*>(smem_raw) + tid;
@@ -245,8 +258,7 @@ __global__ void __launch_bounds__(kColThreads, 4) k_col(const __grid_constant__ 
   const int warp = tid >> 5, lane = tid & 31;
   const int sub = lane / lpc, lc = lane & (lpc - 1);
   const int rows_per_pass = (kColThreads / 32) * rpw;
-  const int64_t cstride = static_cast<int64_t>(lpc) * VEC;
-  const int64_t span = cstride * CH;
+  const int64_t span = static_cast<int64_t>(lpc) * VEC;
   const int64_t tiles = (L.C + span - 1) / span;
   const int64_t k = blockIdx.x / tiles;
   const int64_t tile0 = (blockIdx.x - k * tiles) * span;
@@ -254,49 +266,56 @@ __global__ void __launch_bounds__(kColThreads, 4) k_col(const __grid_constant__ 
   const int64_t per = (L.R + L.splits - 1) / L.splits;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * per;
   const int64_t r1 = r0 + per < L.R ? r0 + per : L.R;
-  const int nvalid = chunks_in_row<CH>(L.C - col0, cstride);
 
-  Acc acc[CH * VEC];
+  Acc acc[VEC];
 #pragma unroll
-  for (int i = 0; i < CH * VEC; ++i) acc[i] = RD::identity();
-  auto rows_loop = [&](auto tile_of) {
-    for (int64_t r = r0 + warp * rpw + sub; r < r1; r += rows_per_pass) {
-      T v[CH];
-      Pre::template run<VEC, CH, WIDE>(L.pre, tile_of(k * L.R + r), v, slots, kColThreads, consts, 0.f);
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        if constexpr (VEC == 1) {
-          acc[c] = RD::step(acc[c], v[c]);
-        } else {
-          acc[c * 4 + 0] = RD::step(acc[c * 4 + 0], v[c].x);
-          acc[c * 4 + 1] = RD::step(acc[c * 4 + 1], v[c].y);
-          acc[c * 4 + 2] = RD::step(acc[c * 4 + 2], v[c].z);
-          acc[c * 4 + 3] = RD::step(acc[c * 4 + 3], v[c].w);
-        }
-      }
+  for (int i = 0; i < VEC; ++i) acc[i] = RD::identity();
+  auto add = [&](const T& v) {
+    if constexpr (VEC == 1) {
+      acc[0] = RD::step(acc[0], v);
+    } else {
+      acc[0] = RD::step(acc[0], v.x);
+      acc[1] = RD::step(acc[1], v.y);
+      acc[2] = RD::step(acc[2], v.z);
+      acc[3] = RD::step(acc[3], v.w);
     }
   };
-  using I = IndexT<WIDE>;
-  if (Pre::kSplitFull && nvalid == CH)
-    rows_loop([&](int64_t row) {
-      return Tile<I, true>{static_cast<I>(row), static_cast<I>(col0), static_cast<I>(L.C), static_cast<I>(cstride), CH};
-    });
-  else if (nvalid > 0)
-    rows_loop([&](int64_t row) {
-      return Tile<I, false>{static_cast<I>(row), static_cast<I>(col0), static_cast<I>(L.C), static_cast<I>(cstride), nvalid};
-    });
+  if (col0 < L.C) {
+    const int64_t step = static_cast<int64_t>(rows_per_pass) * CH;
+    int64_t r = r0 + warp * rpw + sub;
+    // full steps: all CH rows inside [r0, r1)
+    for (; r + (CH - 1) * rows_per_pass < r1; r += step) {
+      T v[CH];
+      Pre::template run<VEC, CH, WIDE>(
+          L.pre, Tile<I, true, true>{static_cast<I>(k * L.R + r), static_cast<I>(col0), static_cast<I>(L.C),
+                                     static_cast<I>(rows_per_pass), CH},
+          v, slots, kColThreads, consts, 0.f);
 #pragma unroll
-  for (int i = 0; i < CH * VEC; ++i) part[tid][i] = acc[i];
+      for (int c = 0; c < CH; ++c) add(v[c]);
+    }
+    if (r < r1) {  // last partial step
+      const int nv = static_cast<int>((r1 - r + rows_per_pass - 1) / rows_per_pass);
+      T v[CH];
+      Pre::template run<VEC, CH, WIDE>(
+          L.pre, Tile<I, false, true>{static_cast<I>(k * L.R + r), static_cast<I>(col0), static_cast<I>(L.C),
+                                      static_cast<I>(rows_per_pass), nv},
+          v, slots, kColThreads, consts, 0.f);
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+        if (c < nv) add(v[c]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) part[tid][i] = acc[i];
   __syncthreads();
-  // Column j of the tile: chunk c = (j/VEC)/lpc, lane lc = (j/VEC)%lpc, element j%VEC.
+  // Column j of the tile: lane lc = j/VEC of each row slot, element j%VEC.
   for (int j = tid; j < span; j += kColThreads) {
     const int64_t col = tile0 + j;
     if (col >= L.C) continue;
-    const int q = j / VEC, e = j % VEC;
-    const int jl = q % lpc, jc = q / lpc;
+    const int jl = j / VEC, e = j % VEC;
     Acc s = RD::identity();
     for (int w = 0; w < kColThreads / 32; ++w)
-      for (int u = 0; u < rpw; ++u) s = RD::join(s, part[w * 32 + u * lpc + jl][jc * VEC + e]);
+      for (int u = 0; u < rpw; ++u) s = RD::join(s, part[w * 32 + u * lpc + jl][e]);
     const int64_t o = k * L.C + col;
     switch (L.schedule) {
       case DISC_SCHED_COL_SINGLE:
@@ -389,7 +408,7 @@ inline cudaError_t launch_row_with(K kernel, const disc_reduce_launch& L, cudaSt
 // Column pass only (the finalize kernel is launched by the caller).
 template <int CH = kCH, typename K>
 inline cudaError_t launch_col_with(K kernel, const disc_reduce_launch& L, cudaStream_t s, bool use_slots = true) {
-  const int64_t span = static_cast<int64_t>(L.group) * CH * L.vec;
+  const int64_t span = static_cast<int64_t>(L.group) * L.vec;
   const int64_t tiles = (L.C + span - 1) / span;
   dim3 grid(static_cast<unsigned>(L.K * tiles), static_cast<unsigned>(L.splits));
   const size_t smem = use_slots ? static_cast<size_t>(L.pre.n_slots) * CH * kColThreads * (L.vec == 4 ? 16 : 4) : 0;

@@ -90,20 +90,25 @@ __device__ __forceinline__ int64_t gather_index(const disc_load& L, int64_t f) {
 
 __device__ __forceinline__ float ldg(const float* p) { return __ldg(p); }
 
-// A tile: CH chunks of VEC elements in row `row`; chunk c starts at column
-// col0 + c*cstride (cstride = warp/group width * VEC keeps every access coalesced).
+// A tile: CH chunks of VEC elements.  Column tiles (ROWS = false): chunk c at
+// (row, col0 + c*cstride) -- cstride = warp/group width * VEC keeps every access
+// coalesced.  Row tiles (ROWS = true, column reductions): chunk c at (row + c*cstride,
+// col0), so a thread keeps CH rows of loads in flight for the same VEC columns.
 // I is the index type: int32_t for launches whose every address fits in 31 bits (!wide),
-// int64_t otherwise; FULL tiles have all CH chunks inside the row (no per-chunk guard).
-template <typename I, bool FULL>
+// int64_t otherwise; FULL tiles have all CH chunks valid (no per-chunk guard).
+template <typename I, bool FULL, bool ROWS = false>
 struct Tile {
   using Index = I;
+  static constexpr bool kRows = ROWS;
   I row;
   I col0;
   I W;
   I cstride;
-  int nvalid;              // leading chunks inside the row (== CH when FULL)
+  int nvalid;              // leading valid chunks (== CH when FULL)
   float* cache = nullptr;  // row cache of this row (slot k at cache + k*W), or null
   __device__ __forceinline__ bool has(int c) const { return FULL || c < nvalid; }
+  // Flat-index distance between consecutive chunks.
+  __device__ __forceinline__ I step() const { return ROWS ? cstride * W : cstride; }
 };
 using TileCtx = Tile<int64_t, false>;
 
@@ -198,61 +203,76 @@ template <int VEC, int CH, bool WIDE, int CLS, typename Ctx>
 __device__ __forceinline__ void load_cls(const disc_program& P, const Ctx& t, const float* consts, int l,
                                          typename Vec<VEC>::T (&v)[CH]) {
   using I = typename Ctx::Index;
+  constexpr bool ROWS = Ctx::kRows;
   const disc_load& L = P.loads[l];
   if constexpr (CLS == kLcIdentity) {
-    if (cached_load<VEC, CH>(P, t, l, v)) return;
+    if constexpr (!ROWS)
+      if (cached_load<VEC, CH>(P, t, l, v)) return;
     const float* base = L.ptr + (t.row * t.W + t.col0);
+    const I step = t.step();
 #pragma unroll
     for (int c = 0; c < CH; ++c)
       if (t.has(c)) {
-        if constexpr (VEC == 1) v[c] = ldg(base + c * t.cstride);
-        else v[c] = __ldg(reinterpret_cast<const float4*>(base + c * t.cstride));
+        if constexpr (VEC == 1) v[c] = ldg(base + c * step);
+        else v[c] = __ldg(reinterpret_cast<const float4*>(base + c * step));
       }
-    cache_fill<VEC, CH>(P, t, l, v);
+    if constexpr (!ROWS) cache_fill<VEC, CH>(P, t, l, v);
   } else if constexpr (CLS == kLcConst) {
     const float x = consts[l];
 #pragma unroll
     for (int c = 0; c < CH; ++c) v[c] = splat(x, v[c]);
   } else if constexpr (CLS == kLcSplat) {  // value depends on the row only
-    const float x = ldg(L.ptr + (static_cast<I>(L.offset) + t.row * static_cast<I>(L.rs)));
+    const I rs = static_cast<I>(L.rs);
+    const float* base = L.ptr + (static_cast<I>(L.offset) + t.row * rs);
+    if constexpr (ROWS) {
 #pragma unroll
-    for (int c = 0; c < CH; ++c) v[c] = splat(x, v[c]);
+      for (int c = 0; c < CH; ++c)
+        if (t.has(c)) v[c] = splat(ldg(base + c * t.cstride * rs), v[c]);
+    } else {
+      const float x = ldg(base);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) v[c] = splat(x, v[c]);
+    }
   } else if constexpr (CLS == kLcContig || CLS == kLcContigU) {
-    const float* base = L.ptr + (static_cast<I>(L.offset) + t.row * static_cast<I>(L.rs) + t.col0);
+    const I rs = static_cast<I>(L.rs);
+    const float* base = L.ptr + (static_cast<I>(L.offset) + t.row * rs + t.col0);
+    const I step = ROWS ? t.cstride * rs : t.cstride;
 #pragma unroll
     for (int c = 0; c < CH; ++c)
       if (t.has(c)) {
-        const float* p = base + c * t.cstride;
+        const float* p = base + c * step;
         if constexpr (VEC == 1) v[c] = ldg(p);
         else if constexpr (CLS == kLcContig) v[c] = __ldg(reinterpret_cast<const float4*>(p));
         else v[c] = make_float4(ldg(p), ldg(p + 1), ldg(p + 2), ldg(p + 3));
       }
   } else if constexpr (CLS == kLcStrided) {  // cs not in {0, 1}: element loads
-    const I cs = static_cast<I>(L.cs);
-    const float* base = L.ptr + (static_cast<I>(L.offset) + t.row * static_cast<I>(L.rs));
+    const I cs = static_cast<I>(L.cs), rs = static_cast<I>(L.rs);
+    const float* base = L.ptr + (static_cast<I>(L.offset) + t.row * rs);
 #pragma unroll
     for (int c = 0; c < CH; ++c)
       if (t.has(c)) {
-        const float* p = base + (t.col0 + c * t.cstride) * cs;
+        const float* p = ROWS ? base + c * t.cstride * rs + t.col0 * cs : base + (t.col0 + c * t.cstride) * cs;
         if constexpr (VEC == 1) v[c] = ldg(p);
         else v[c] = make_float4(ldg(p), ldg(p + cs), ldg(p + 2 * cs), ldg(p + 3 * cs));
       }
   } else {
     const int64_t f0 = static_cast<int64_t>(t.row) * t.W + t.col0;
+    const int64_t step = t.step();
 #pragma unroll
     for (int c = 0; c < CH; ++c)
-      if (t.has(c)) v[c] = load_gather<VEC, WIDE>(L, f0 + c * t.cstride);
+      if (t.has(c)) v[c] = load_gather<VEC, WIDE>(L, f0 + c * step);
   }
 }
 
 template <int VEC, int CH, typename Ctx>
 __device__ __forceinline__ void store_tile(float* out, const Ctx& t, const typename Vec<VEC>::T (&v)[CH]) {
   float* o = out + (t.row * t.W + t.col0);
+  const auto step = t.step();
 #pragma unroll
   for (int c = 0; c < CH; ++c)
     if (t.has(c)) {
-      if constexpr (VEC == 1) o[c * t.cstride] = v[c];
-      else *reinterpret_cast<float4*>(o + c * t.cstride) = v[c];
+      if constexpr (VEC == 1) o[c * step] = v[c];
+      else *reinterpret_cast<float4*>(o + c * step) = v[c];
     }
 }
 

@@ -933,12 +933,13 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     rep.schedule = post_fused ? (R.cache_loads ? "row_fused_cached" : "row_fused") : "row";
   } else if (R.schedule != DISC_SCHED_GENERIC) {
     if (!R.red_out) R.red_out = static_cast<float*>(issue.scratch(nout * 4));
-    // Lanes per row segment: enough to cover C with two chunks each, up to a warp.
-    const int64_t cchunks = (R.C / R.vec + 1) / 2;
+    // Lanes per row segment: one VEC-wide column group each, up to a warp (each thread
+    // keeps its columns and walks rows; narrow C packs 32/lpc rows per warp).
+    const int64_t cchunks = (R.C + R.vec - 1) / R.vec;
     int lpc = 1;
     while (lpc < cchunks && lpc < 32) lpc <<= 1;
     R.group = lpc;
-    const int64_t span = int64_t{lpc} * 2 * R.vec;
+    const int64_t span = int64_t{lpc} * R.vec;
     const int64_t tiles = (R.C + span - 1) / span;
     const int64_t ctas = R.K * tiles;
     const int64_t rows_per_pass = 8 * (32 / lpc);
