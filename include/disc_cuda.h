@@ -84,10 +84,12 @@ typedef struct {
   uint32_t shift[DISC_MAX_RANK];
 } disc_load;
 
-/* Row cache (row schedule with a fused epilogue): contiguous loads shared by the reduce
- * pass and the epilogue are kept in shared memory.  cache_mode 1: the pre program also
- * writes the loaded tile to cache slot cache_slot[l]; 2: the post program reads it from
- * there instead of global memory. */
+/* Row cache (row schedule): identity loads are kept in shared-memory slots; slot k holds
+ * the block's rows back to back (row r at k*slot_stride + r*R).  cache_mode 1: the pre
+ * program also writes the loaded tile to slot cache_slot[l]; 2: the program reads it from
+ * there instead of global memory.  In a staged launch (disc_reduce_launch.stage) the
+ * block copies its rows into the input slots first and programs write output o to slot
+ * out_slot[o]; the block then copies the output slots out (coalesced). */
 enum disc_cache_mode { DISC_CACHE_NONE = 0, DISC_CACHE_FILL = 1, DISC_CACHE_READ = 2 };
 
 typedef struct {
@@ -97,6 +99,7 @@ typedef struct {
   int32_t n_outs;
   int32_t cache_mode;
   int8_t cache_slot[DISC_MAX_LOADS];
+  int8_t out_slot[DISC_MAX_OUTS];   /* staged launches: smem slot of output o, -1 = global */
   int32_t flags;    /* DISC_PROG_* launch flags (not part of the program structure) */
   disc_instr code[DISC_MAX_INSTR];
   disc_load loads[DISC_MAX_LOADS];
@@ -140,8 +143,8 @@ typedef struct {
   int32_t wide;
   int32_t group;            /* ROW: threads per row (power of two) */
   int32_t splits;           /* COL: number of R splits */
-  int32_t cache_loads;      /* ROW: number of row-cache slots (0 = no cache) */
-  int32_t pad1;
+  int32_t cache_loads;      /* ROW: number of shared-memory slots (0 = no cache) */
+  int32_t stage;            /* ROW: 1 = staged block tiles (see disc_program.out_slot) */
   float* red_out;           /* f32 reduce result [K*C] */
   double* workspace;        /* COL two-pass/atomic: f64 [splits or 1][K*C] */
   /* GENERIC: arg dims and reduced-axis mask */

@@ -39,7 +39,7 @@ struct Interp {
           run_tile<VEC, 1, WIDE>(P, t1, reinterpret_cast<T(&)[1]>(acc[c]), slots, stride, consts, red);
         }
     } else {
-      const TileCtx t64{t.row, t.col0, t.W, t.cstride, t.nvalid, t.cache};
+      const Tile<int64_t, false, false, Ctx::kStaged> t64{t.row, t.col0, t.W, t.cstride, t.nvalid, t.cache, t.slot_stride};
       run_tile<VEC, CH, WIDE>(P, t64, acc, slots, stride, consts, red);
     }
   }
@@ -142,7 +142,29 @@ __global__ void __launch_bounds__(kLoopThreads, 4) k_loop(const __grid_constant_
 // Row schedule: reduce arg collapsed to [K rows, R]; G threads per row (power of two);
 // thread `lane` of a row takes chunks lane, lane+G, ... (coalesced across the group).
 // Optional fused epilogue (post program) re-evaluated per element with the row value.
-template <int VEC, bool WIDE, int KIND, typename Pre, typename Post, int CH = kCH>
+// Shared-memory slots hold the block's rpb rows back to back (slot-major):
+//   row cache (FILL/READ)  loads the epilogue re-reads stay on chip;
+//   staged (L.stage)       short rows: the block copies its contiguous span of every
+//                          identity input into the slots (coalesced, 16 B when aligned),
+//                          programs read/write slots, outputs are copied out the same way.
+
+// Copies n floats global -> shared (or back), 16 B per access when both ends allow it.
+__device__ __forceinline__ void copy_span(float* __restrict__ dst, const float* __restrict__ src, int64_t n,
+                                          bool to_global) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+    const int64_t n4 = n >> 2;
+    for (int64_t i = tid; i < n4; i += nt) {
+      const float4 v = to_global ? reinterpret_cast<const float4*>(src)[i] : __ldg(reinterpret_cast<const float4*>(src) + i);
+      reinterpret_cast<float4*>(dst)[i] = v;
+    }
+    for (int64_t i = (n4 << 2) + tid; i < n; i += nt) dst[i] = to_global ? src[i] : __ldg(src + i);
+  } else {
+    for (int64_t i = tid; i < n; i += nt) dst[i] = to_global ? src[i] : __ldg(src + i);
+  }
+}
+
+template <int VEC, bool WIDE, int KIND, typename Pre, typename Post, int CH = kCH, bool STAGED = false>
 __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduce_launch L) {
   using RD = Red<KIND>;
   using Acc = typename RD::Acc;
@@ -155,9 +177,11 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
   const int lane = threadIdx.x & (G - 1);
   const int sub = threadIdx.x / G;
   const int rpb = blockDim.x / G;
-  // Dynamic smem: [row cache: rpb x cache_loads x R floats][interpreter slots].
-  const int64_t cache_floats = (static_cast<int64_t>(rpb) * L.cache_loads * L.R + 3) / 4 * 4;
-  float* row_cache = L.cache_loads ? reinterpret_cast<float*>(smem_raw) + sub * L.cache_loads * L.R : nullptr;
+  // Dynamic smem: [cache_loads slots of slot_stride floats][interpreter slots].
+  const int64_t slot_stride = (static_cast<int64_t>(rpb) * L.R + 3) / 4 * 4;
+  const int64_t cache_floats = slot_stride * L.cache_loads;
+  float* const cache0 = reinterpret_cast<float*>(smem_raw);
+  float* row_cache = L.cache_loads ? cache0 + sub * L.R : nullptr;
   T* slots = reinterpret_cast<T*>(reinterpret_cast<float*>(smem_raw) + cache_floats) + threadIdx.x;
   pdl_enter(L.pre);
   hoist_consts(L.pre, consts[0]);
@@ -166,11 +190,31 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
   using I = IndexT<WIDE>;
   const int64_t rows = L.K;
   const I R = static_cast<I>(L.R);
+  const I sst = static_cast<I>(slot_stride);
   const bool fuse_post = L.post.n_instr > 0;
   const I cstride = static_cast<I>(G) * VEC;
   const I span = cstride * CH;
 
   for (int64_t base = static_cast<int64_t>(blockIdx.x) * rpb; base < rows; base += static_cast<int64_t>(gridDim.x) * rpb) {
+    const int64_t n_el = (rows - base < rpb ? rows - base : rpb) * L.R;
+    if constexpr (STAGED) {  // copy the block's rows of every staged input into its slot
+      uint32_t pre_slots = 0;
+      for (int l = 0; l < L.pre.n_loads; ++l) {
+        const int k = L.pre.cache_slot[l];
+        if (k >= 0 && !((pre_slots >> k) & 1)) {
+          pre_slots |= 1u << k;
+          copy_span(cache0 + k * slot_stride, L.pre.loads[l].ptr + base * L.R, n_el, false);
+        }
+      }
+      for (int l = 0; l < L.post.n_loads; ++l) {
+        const int k = L.post.cache_slot[l];
+        if (k >= 0 && !((pre_slots >> k) & 1)) {
+          pre_slots |= 1u << k;
+          copy_span(cache0 + k * slot_stride, L.post.loads[l].ptr + base * L.R, n_el, false);
+        }
+      }
+      __syncthreads();
+    }
     const I row = static_cast<I>(base + sub);
     const bool valid = base + sub < rows;
     Acc acc = RD::identity();
@@ -179,12 +223,12 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
         const int nv = chunks_in_row<CH>(R - col0, cstride);
         T v[CH];
         if (Pre::kSplitFull && nv == CH) {
-          Pre::template run<VEC, CH, WIDE>(L.pre, Tile<I, true>{row, col0, R, cstride, CH, row_cache}, v, slots,
+          Pre::template run<VEC, CH, WIDE>(L.pre, Tile<I, true, false, STAGED>{row, col0, R, cstride, CH, row_cache, sst}, v, slots,
                                            blockDim.x, consts[0], 0.f);
 #pragma unroll
           for (int c = 0; c < CH; ++c) acc = RD::acc(acc, v[c]);
         } else {
-          Pre::template run<VEC, CH, WIDE>(L.pre, Tile<I, false>{row, col0, R, cstride, nv, row_cache}, v, slots,
+          Pre::template run<VEC, CH, WIDE>(L.pre, Tile<I, false, false, STAGED>{row, col0, R, cstride, nv, row_cache, sst}, v, slots,
                                            blockDim.x, consts[0], 0.f);
 #pragma unroll
           for (int c = 0; c < CH; ++c)
@@ -217,15 +261,26 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
           const int nv = chunks_in_row<CH>(R - col0, cstride);
           T v[CH];
           if (Post::kSplitFull && nv == CH)
-            Post::template run<VEC, CH, WIDE>(L.post, Tile<I, true>{row, col0, R, cstride, CH, row_cache}, v, slots,
-                                              blockDim.x, consts[1], result);
+            Post::template run<VEC, CH, WIDE>(L.post, Tile<I, true, false, STAGED>{row, col0, R, cstride, CH, row_cache, sst}, v,
+                                              slots, blockDim.x, consts[1], result);
           else
-            Post::template run<VEC, CH, WIDE>(L.post, Tile<I, false>{row, col0, R, cstride, nv, row_cache}, v, slots,
-                                              blockDim.x, consts[1], result);
+            Post::template run<VEC, CH, WIDE>(L.post, Tile<I, false, false, STAGED>{row, col0, R, cstride, nv, row_cache, sst}, v,
+                                              slots, blockDim.x, consts[1], result);
         }
       }
     }
-    if (G > 32) __syncthreads();
+    if constexpr (STAGED) {  // copy every staged output slot back, then free the slots
+      __syncthreads();
+      for (int o = 0; o < L.pre.n_outs; ++o)
+        if (L.pre.out_slot[o] >= 0)
+          copy_span(L.pre.outs[o] + base * L.R, cache0 + L.pre.out_slot[o] * slot_stride, n_el, true);
+      for (int o = 0; o < L.post.n_outs; ++o)
+        if (L.post.out_slot[o] >= 0)
+          copy_span(L.post.outs[o] + base * L.R, cache0 + L.post.out_slot[o] * slot_stride, n_el, true);
+      __syncthreads();
+    } else if (G > 32) {
+      __syncthreads();
+    }
   }
 }
 
@@ -395,7 +450,7 @@ inline cudaError_t launch_row_with(K kernel, const disc_reduce_launch& L, cudaSt
   const int block = L.group > 256 ? L.group : 256;
   const int rpb = block / L.group;
   const int64_t groups = (L.K + rpb - 1) / rpb;
-  const size_t cache = static_cast<size_t>((static_cast<int64_t>(rpb) * L.cache_loads * L.R + 3) / 4 * 4) * 4;
+  const size_t cache = static_cast<size_t>((static_cast<int64_t>(rpb) * L.R + 3) / 4 * 4) * L.cache_loads * 4;
   const size_t smem = cache + (use_slots ? static_cast<size_t>(slots) * CH * block * (L.vec == 4 ? 16 : 4) : 0);
   cudaError_t e = set_smem(kernel, smem);
   if (e != cudaSuccess) return e;
@@ -424,16 +479,14 @@ inline cudaError_t launch_col_with(K kernel, const disc_reduce_launch& L, cudaSt
 template <typename Pre, typename Post, int CH = kCH, bool ALLOW_WIDE = true>
 inline cudaError_t row_pass(const disc_reduce_launch& L, cudaStream_t s, bool use_slots) {
   const bool sum = L.kind == DISC_REDUCE_SUM;
-  if constexpr (ALLOW_WIDE) if (L.wide) {
-    if (L.vec == 4) return sum ? launch_row_with<CH>(k_row<4, true, DISC_REDUCE_SUM, Pre, Post, CH>, L, s, use_slots)
-                               : launch_row_with<CH>(k_row<4, true, DISC_REDUCE_MAX, Pre, Post, CH>, L, s, use_slots);
-    return sum ? launch_row_with<CH>(k_row<1, true, DISC_REDUCE_SUM, Pre, Post, CH>, L, s, use_slots)
-               : launch_row_with<CH>(k_row<1, true, DISC_REDUCE_MAX, Pre, Post, CH>, L, s, use_slots);
-  }
-  if (L.vec == 4) return sum ? launch_row_with<CH>(k_row<4, false, DISC_REDUCE_SUM, Pre, Post, CH>, L, s, use_slots)
-                             : launch_row_with<CH>(k_row<4, false, DISC_REDUCE_MAX, Pre, Post, CH>, L, s, use_slots);
-  return sum ? launch_row_with<CH>(k_row<1, false, DISC_REDUCE_SUM, Pre, Post, CH>, L, s, use_slots)
-             : launch_row_with<CH>(k_row<1, false, DISC_REDUCE_MAX, Pre, Post, CH>, L, s, use_slots);
+#define DISC_ROW(V, W, ST)                                                                                   \
+  (sum ? launch_row_with<CH>(k_row<V, W, DISC_REDUCE_SUM, Pre, Post, CH, ST>, L, s, use_slots)              \
+       : launch_row_with<CH>(k_row<V, W, DISC_REDUCE_MAX, Pre, Post, CH, ST>, L, s, use_slots))
+  if constexpr (ALLOW_WIDE)
+    if (L.wide) return L.vec == 4 ? DISC_ROW(4, true, false) : DISC_ROW(1, true, false);
+  if (L.stage) return L.vec == 4 ? DISC_ROW(4, false, true) : DISC_ROW(1, false, true);
+  return L.vec == 4 ? DISC_ROW(4, false, false) : DISC_ROW(1, false, false);
+#undef DISC_ROW
 }
 
 template <typename Pre, int CH = kCH, bool ALLOW_WIDE = true>

@@ -96,16 +96,18 @@ __device__ __forceinline__ float ldg(const float* p) { return __ldg(p); }
 // col0), so a thread keeps CH rows of loads in flight for the same VEC columns.
 // I is the index type: int32_t for launches whose every address fits in 31 bits (!wide),
 // int64_t otherwise; FULL tiles have all CH chunks valid (no per-chunk guard).
-template <typename I, bool FULL, bool ROWS = false>
+template <typename I, bool FULL, bool ROWS = false, bool STAGED = false>
 struct Tile {
   using Index = I;
   static constexpr bool kRows = ROWS;
+  static constexpr bool kStaged = STAGED;  // outputs with an out_slot go to shared memory
   I row;
   I col0;
   I W;
   I cstride;
   int nvalid;              // leading valid chunks (== CH when FULL)
-  float* cache = nullptr;  // row cache of this row (slot k at cache + k*W), or null
+  float* cache = nullptr;  // row cache: this row in slot 0 (slot k at cache + k*slot_stride), or null
+  I slot_stride = 0;
   __device__ __forceinline__ bool has(int c) const { return FULL || c < nvalid; }
   // Flat-index distance between consecutive chunks.
   __device__ __forceinline__ I step() const { return ROWS ? cstride * W : cstride; }
@@ -117,7 +119,7 @@ template <int VEC, int CH, typename Ctx>
 __device__ __forceinline__ bool cached_load(const disc_program& P, const Ctx& t, int l,
                                             typename Vec<VEC>::T (&v)[CH]) {
   if (P.cache_mode != DISC_CACHE_READ || P.cache_slot[l] < 0 || !t.cache) return false;
-  const float* c0 = t.cache + P.cache_slot[l] * t.W + t.col0;
+  const float* c0 = t.cache + P.cache_slot[l] * t.slot_stride + t.col0;
 #pragma unroll
   for (int c = 0; c < CH; ++c)
     if (t.has(c)) {
@@ -131,7 +133,7 @@ template <int VEC, int CH, typename Ctx>
 __device__ __forceinline__ void cache_fill(const disc_program& P, const Ctx& t, int l,
                                            const typename Vec<VEC>::T (&v)[CH]) {
   if (P.cache_mode != DISC_CACHE_FILL || P.cache_slot[l] < 0 || !t.cache) return;
-  float* c0 = t.cache + P.cache_slot[l] * t.W + t.col0;
+  float* c0 = t.cache + P.cache_slot[l] * t.slot_stride + t.col0;
 #pragma unroll
   for (int c = 0; c < CH; ++c)
     if (t.has(c)) {
@@ -276,10 +278,29 @@ __device__ __forceinline__ void store_tile(float* out, const Ctx& t, const typen
     }
 }
 
+// Output o of a tile: its shared-memory slot in a staged launch, else global memory.
+template <int VEC, int CH, typename Ctx>
+__device__ __forceinline__ void store_out(const disc_program& P, int o, const Ctx& t,
+                                          const typename Vec<VEC>::T (&v)[CH]) {
+  if constexpr (Ctx::kStaged) {
+    if (P.out_slot[o] >= 0) {
+      float* s0 = t.cache + P.out_slot[o] * t.slot_stride + t.col0;
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+        if (t.has(c)) {
+          if constexpr (VEC == 1) s0[c * t.cstride] = v[c];
+          else *reinterpret_cast<float4*>(s0 + c * t.cstride) = v[c];
+        }
+      return;
+    }
+  }
+  store_tile<VEC, CH>(P.outs[o], t, v);
+}
+
 // Evaluates program P on one tile.  slots: this thread's slot base; slot k, chunk c lives
 // at slots[(k * CH + c) * stride].  Returns with acc[] = the last instruction's value.
-template <int VEC, int CH, bool WIDE>
-__device__ __forceinline__ void run_tile(const disc_program& P, const TileCtx& t,
+template <int VEC, int CH, bool WIDE, typename Ctx = TileCtx>
+__device__ __forceinline__ void run_tile(const disc_program& P, const Ctx& t,
                                          typename Vec<VEC>::T (&acc)[CH], typename Vec<VEC>::T* slots, int stride,
                                          const float* consts, float red) {
   using T = typename Vec<VEC>::T;
@@ -344,13 +365,7 @@ __device__ __forceinline__ void run_tile(const disc_program& P, const TileCtx& t
     if (in.flags & DISC_F_SLOT) {
       DISC_FOR_C DISC_S(in.dst, c) = acc[c];
     }
-    if (in.flags & DISC_F_OUT) {
-      float* o = P.outs[in.out] + f0;
-      DISC_FOR_C if (c < t.nvalid) {
-        if constexpr (VEC == 1) o[c * t.cstride] = acc[c];
-        else *reinterpret_cast<T*>(o + c * t.cstride) = acc[c];
-      }
-    }
+    if (in.flags & DISC_F_OUT) store_out<VEC, CH>(P, in.out, t, acc);
   }
 #undef DISC_S
 #undef DISC_FOR_C

@@ -2,6 +2,8 @@
 #include "launcher.hpp"
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <tuple>
@@ -227,6 +229,7 @@ class ProgramBuilder {
     P.cache_mode = DISC_CACHE_NONE;
     P.flags = disc_cuda_pdl_mode() == 2 ? DISC_PROG_PDL_EARLY : 0;
     for (int l = 0; l < DISC_MAX_LOADS; ++l) P.cache_slot[l] = -1;
+    for (int o = 0; o < DISC_MAX_OUTS; ++o) P.out_slot[o] = -1;
     P.n_loads = static_cast<int32_t>(maps_.size());
     for (size_t l = 0; l < maps_.size(); ++l) P.loads[l].ptr = ptrs_[l];
     B.maps = maps_;
@@ -380,6 +383,57 @@ int lanes_per_row(int64_t W, int vec) {
 }
 
 constexpr int64_t kWideLimitView = (int64_t{1} << 31) - 64;
+
+int sm_count();
+
+// Threads per row (power of two) for the row schedule over K rows of R elements:
+//  * ~32 chunks per thread, so long rows keep a warp (no block barrier) when rows abound;
+//  * widened while that improves machine fill and wave balance: a one-wave grid of
+//    sm x (1024 / block) CTAs walks groups of 256/G rows, so the score is
+//    min(1, waves) x waves/ceil(waves); wider groups must win by > 3%.
+// Row-schedule policy (DISC_ROW_POLICY, read once; for A/B measurement):
+//   0  ~32 chunks per thread, widened only to fill the machine
+//   1  0 + wave-balance widening
+//   2  1 + staged short rows (16 <= R < 32) (default)
+int row_policy() {
+  static const int p = [] {
+    const char* e = std::getenv("DISC_ROW_POLICY");
+    return e ? std::atoi(e) : 2;
+  }();
+  return p;
+}
+
+int choose_row_group(int64_t K, int64_t R, int vec) {
+  const int64_t chunks = R / vec;
+  if (K <= 0 || chunks <= 0) return 1;
+  auto np2 = [](int64_t x) {
+    int g = 1;
+    while (g < x && g < 1024) g <<= 1;
+    return g;
+  };
+  int g = np2((chunks + 31) / 32);
+  if (row_policy() == 0) {
+    const int64_t need = (int64_t{sm_count()} * 1024 + K - 1) / K;
+    while (g < need && g < 1024 && int64_t{g} * 4 <= chunks) g <<= 1;
+    return g;
+  }
+  auto score = [&](int gg) {
+    const int block = std::max(gg, 256);
+    const int64_t groups = (K + block / gg - 1) / (block / gg);
+    const double slots = double(sm_count()) * std::max(1, 1024 / block);
+    const double waves = double(groups) / slots;
+    return waves < 1 ? waves : waves / std::ceil(waves);
+  };
+  double best = score(g);
+  for (int gg = g * 2; gg <= 1024 && int64_t{gg} * 4 <= chunks; gg <<= 1) {
+    const double sc = score(gg);
+    if (sc > best * 1.03) {
+      best = sc;
+      g = gg;
+    }
+  }
+  return g;
+}
 
 disc_loop_launch make_loop(Built& b, int64_t total) {
   disc_loop_launch L;
@@ -899,15 +953,49 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
   }
 
   if (R.schedule == DISC_SCHED_ROW) {
-    // ~32 chunks per thread (a warp per row for R = 4096: no block barriers), widened
-    // when there are too few rows to fill the machine.
-    const int64_t chunks = empty ? 0 : R.R / R.vec;
-    int g = next_pow2((chunks + 31) / 32);
-    const int64_t need = (int64_t{sm_count()} * 1024 + std::max<int64_t>(R.K, 1) - 1) / std::max<int64_t>(R.K, 1);
-    while (g < need && g < 1024 && int64_t{g} * 4 <= chunks) g <<= 1;
+    int g = choose_row_group(R.K, R.R, R.vec);
+    // Staged short rows (R < 32 floats: even a whole row is under one 128 B line): the
+    // block copies its contiguous span of every identity operand through shared memory,
+    // one thread per row.  Only when that layout is bank-conflict-free (odd R for scalar
+    // rows, odd R/4 for float4 rows); otherwise rows pack 32/G per warp as usual.
+    if (!empty && !R.wide && row_policy() >= 2 && R.R >= 16 && R.R < 32 && (R.vec == 1 ? (R.R & 1) : ((R.R / 4) & 1))) {
+      int n = 0;
+      auto slot_of_ptr = [&](const float* ptr, const disc_program& P) -> int {
+        for (int l = 0; l < P.n_loads; ++l)
+          if (P.loads[l].mode == DISC_LOAD_IDENTITY && P.loads[l].ptr == ptr && P.cache_slot[l] >= 0)
+            return P.cache_slot[l];
+        return -1;
+      };
+      for (int l = 0; l < R.pre.n_loads; ++l)
+        if (R.pre.loads[l].mode == DISC_LOAD_IDENTITY) {
+          const int k = slot_of_ptr(R.pre.loads[l].ptr, R.pre);
+          R.pre.cache_slot[l] = static_cast<int8_t>(k >= 0 ? k : n++);
+        }
+      if (post_fused)
+        for (int l = 0; l < R.post.n_loads; ++l)
+          if (R.post.loads[l].mode == DISC_LOAD_IDENTITY) {
+            int k = slot_of_ptr(R.post.loads[l].ptr, R.pre);
+            if (k < 0) k = slot_of_ptr(R.post.loads[l].ptr, R.post);
+            R.post.cache_slot[l] = static_cast<int8_t>(k >= 0 ? k : n++);
+          }
+      for (int o = 0; o < R.pre.n_outs; ++o) R.pre.out_slot[o] = static_cast<int8_t>(n++);
+      if (post_fused)
+        for (int o = 0; o < R.post.n_outs; ++o) R.post.out_slot[o] = static_cast<int8_t>(n++);
+      const int64_t slot_bytes = (256 * R.R + 3) / 4 * 4 * 4;
+      if (n > 0 && n <= 8 && n * slot_bytes <= 112 * 1024) {
+        R.stage = 1;
+        R.cache_loads = n;
+        R.pre.cache_mode = DISC_CACHE_READ;
+        R.post.cache_mode = DISC_CACHE_READ;
+        g = 1;
+      } else {
+        for (int l = 0; l < DISC_MAX_LOADS; ++l) R.pre.cache_slot[l] = R.post.cache_slot[l] = -1;
+        for (int o = 0; o < DISC_MAX_OUTS; ++o) R.pre.out_slot[o] = R.post.out_slot[o] = -1;
+      }
+    }
     // Row cache: contiguous loads the epilogue re-reads come from shared memory instead
     // of a second pass over HBM/L2 (softmax: x is read once).
-    if (post_fused) {
+    if (post_fused && !R.stage) {
       int nc = 0;
       for (int q = 0; q < R.post.n_loads && nc < 2; ++q) {
         if (R.post.loads[q].mode != DISC_LOAD_IDENTITY) continue;
@@ -930,7 +1018,8 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
       }
     }
     R.group = g;
-    rep.schedule = post_fused ? (R.cache_loads ? "row_fused_cached" : "row_fused") : "row";
+    rep.schedule = R.stage ? (post_fused ? "row_fused_staged" : "row_staged")
+                           : post_fused ? (R.cache_loads ? "row_fused_cached" : "row_fused") : "row";
   } else if (R.schedule != DISC_SCHED_GENERIC) {
     if (!R.red_out) R.red_out = static_cast<float*>(issue.scratch(nout * 4));
     // Lanes per row segment: one VEC-wide column group each, up to a warp (each thread

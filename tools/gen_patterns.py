@@ -101,7 +101,7 @@ def gen_program(fn, prog):
         if flags & 1:
             slot_val[dst] = i
         if flags & 2:
-            lines.append(f"    store_tile<VEC, CH>(P.outs[{out}], t, {v});")
+            lines.append(f"    store_out<VEC, CH>(P, {out}, t, {v});")
     if code:
         lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) acc[c] = v{len(code) - 1}[c];")
     lines += ["  }", "};"]
