@@ -86,6 +86,11 @@ int disc_executor_run(disc_executor e, disc_plan p, int n_inputs, const char* co
 int disc_executor_run_batch(disc_executor e, disc_plan p, int n_requests, int n_inputs,
                             const char* const* names, const void* const* data,
                             const int64_t* const* dims, const int* ranks, int inputs_on_host);
+/* Runs a heterogeneous stream of requests back to back (asynchronously): request r runs
+ * plans[r] on inputs input_offsets[r] .. input_offsets[r+1]-1 of the flat arrays. */
+int disc_executor_run_stream(disc_executor e, int n_requests, const disc_plan* plans, const int* input_offsets,
+                             const char* const* names, const void* const* data, const int64_t* const* dims,
+                             const int* ranks, int inputs_on_host);
 int disc_executor_num_outputs(disc_executor e);
 /* Device pointer + dims of output i of the last run. */
 int disc_executor_output(disc_executor e, int i, const float** dptr, const int64_t** dims,
@@ -133,6 +138,11 @@ int disc_plan_capture_programs(disc_plan p, int n_inputs, const char* const* nam
 /* Host-side cost of one run (capture mode: no device work), microseconds per run. */
 int disc_plan_host_overhead(disc_plan p, int n_inputs, const char* const* names,
                             const int64_t* const* dims, const int* ranks, int iters, double* us_per_run);
+/* Algorithmic boundary bytes (external inputs read + outputs written, per
+ * kLaunch) of one run at the given input shapes -- host only, no device work.  The
+ * multi-GPU dispatcher balances requests by this. */
+int disc_plan_algorithmic_bytes(disc_plan p, int n_inputs, const char* const* names,
+                                const int64_t* const* dims, const int* ranks, int64_t* bytes);
 /* guard_passes (executor.cpp:78-98) */
 int disc_guard_passes(disc_plan p, int kernel, int version, const int64_t* regs, int n_regs);
 

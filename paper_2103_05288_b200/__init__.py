@@ -8,7 +8,11 @@ from .api import (capture_programs, set_pdl, set_specialization, specialized_lau
                   Executor, cache_key, compile_graph, cuda_available, dhlo_roundtrip, dump_stage, guard_passes,
                   kernel_launches, lib, lower_dhlo_json, static_specialize)
 
+from . import dispatch
+from .dispatch import Dispatcher, shard
+
 __all__ = [
+    "Dispatcher", "dispatch", "shard",
     "capture_programs", "set_pdl", "set_specialization", "specialized_launches",
     "CompileOptions", "CompiledPlan", "Compiler", "DeviceBuffer", "DiscError", "ExecResult", "ExecStats",
     "Executor", "cache_key", "compile_graph", "cuda_available", "dhlo_roundtrip", "dump_stage", "guard_passes",

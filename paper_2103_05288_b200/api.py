@@ -68,6 +68,8 @@ def _declare(L: C.CDLL) -> None:
         "disc_executor_set_stream": ([vp, vp], i32),
         "disc_executor_run": ([vp, vp, i32, P(cp), P(vp), P(vp), P(i32), i32], i32),
         "disc_executor_run_batch": ([vp, vp, i32, i32, P(cp), P(vp), P(vp), P(i32), i32], i32),
+        "disc_executor_run_stream": ([vp, i32, P(vp), P(i32), P(cp), P(vp), P(vp), P(i32), i32], i32),
+        "disc_plan_algorithmic_bytes": ([vp, i32, P(cp), P(vp), P(i32), P(i64)], i32),
         "disc_executor_num_outputs": ([vp], i32),
         "disc_executor_output": ([vp, i32, P(vp), P(P(i64)), P(i32)], i32),
         "disc_executor_copy_output": ([vp, i32, vp, i32], i32),
@@ -224,6 +226,18 @@ class CompiledPlan:
     @property
     def host_instruction_count(self) -> int:
         return lib().disc_plan_host_instruction_count(self._h)
+
+    def algorithmic_bytes(self, input_shapes: Dict[str, Sequence[int]]) -> int:
+        """SURVEY §8d boundary bytes of one run at these input shapes (host only)."""
+        names = list(input_shapes)
+        dims = [np.array(input_shapes[n], dtype=np.int64) for n in names]
+        k = len(names)
+        c_names = (C.c_char_p * max(k, 1))(*[n.encode() for n in names])
+        c_dims = (C.c_void_p * max(k, 1))(*[d.ctypes.data for d in dims])
+        c_ranks = (C.c_int * max(k, 1))(*[d.size for d in dims])
+        out = C.c_int64()
+        _check(lib().disc_plan_algorithmic_bytes(self._h, k, c_names, c_dims, c_ranks, C.byref(out)))
+        return out.value
 
     def eval_shapes(self, input_dims: Sequence[Sequence[int]]) -> List[int]:
         arrs = [np.asarray(d, dtype=np.int64) for d in input_dims]
@@ -440,6 +454,31 @@ class Executor:
     def run_device(self, plan: CompiledPlan, inputs: Dict[str, object]) -> None:
         keep, n, names, data, dims, ranks, host = self._bind(inputs)
         _check(lib().disc_executor_run(self._h, plan._h, n, names, data, dims, ranks, int(host)))
+
+    def run_stream(self, requests: Sequence[Tuple[CompiledPlan, Dict[str, object]]]) -> None:
+        """Runs (plan, inputs) requests back to back on this executor's stream (inputs all
+        device-resident or all host); outputs of the last request stay readable."""
+        keep, names, datas, dims, offs, plans = [], [], [], [], [0], []
+        host = None
+        for plan, inputs in requests:
+            k, n, c_names, c_data, c_dims, c_ranks, h = self._bind(inputs)
+            keep.append((k, c_names, c_data, c_dims, c_ranks))
+            if host is None:
+                host = h
+            elif host != h:
+                raise DiscError(2, "inputs must be all host or all device", "usage")
+            names.extend(c_names[i] for i in range(n))
+            datas.extend(c_data[i] for i in range(n))
+            dims.extend(c_dims[i] for i in range(n))
+            keep.append([c_ranks[i] for i in range(n)])
+            offs.append(offs[-1] + n)
+            plans.append(plan._h)
+        ranks = [r for item in keep if isinstance(item, list) for r in item]
+        m = len(requests)
+        t = max(offs[-1], 1)
+        _check(lib().disc_executor_run_stream(
+            self._h, m, (C.c_void_p * max(m, 1))(*plans), (C.c_int * (m + 1))(*offs), (C.c_char_p * t)(*names),
+            (C.c_void_p * t)(*datas), (C.c_void_p * t)(*dims), (C.c_int * t)(*ranks), int(bool(host))))
 
     def output_views(self) -> List[Tuple[int, Tuple[int, ...]]]:
         L = lib()

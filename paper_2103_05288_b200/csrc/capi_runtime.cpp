@@ -5,6 +5,7 @@
 #include "capi_common.hpp"
 #include "disc_cuda.h"
 #include "runtime/runtime_flow.hpp"
+#include "runtime/launcher.hpp"
 #include "runtime/shape_eval.hpp"
 
 using namespace disc;
@@ -72,6 +73,26 @@ int disc_executor_run_batch(disc_executor e, disc_plan p, int n_requests, int n_
                             : static_cast<const float*>(data[k]);
       }
       e->ex.run(*p->plan, in, r > 0, p->serial);
+    }
+  });
+}
+
+int disc_executor_run_stream(disc_executor e, int n_requests, const disc_plan* plans, const int* input_offsets,
+                             const char* const* names, const void* const* data, const int64_t* const* dims,
+                             const int* ranks, int on_host) {
+  return guard([&] {
+    std::vector<rt::InputBinding> in;
+    for (int r = 0; r < n_requests; ++r) {
+      const int i0 = input_offsets[r], n = input_offsets[r + 1] - i0;
+      in.resize(n);
+      for (int i = 0; i < n; ++i) {
+        const int k = i0 + i;
+        in[i].name = names[k];
+        in[i].dims.assign(dims[k], dims[k] + ranks[k]);
+        in[i].ptr = on_host ? e->ex.stage_input(i, data[k], bytes_of(dims[k], ranks[k]))
+                            : static_cast<const float*>(data[k]);
+      }
+      e->ex.run(*plans[r]->plan, in, r > 0, plans[r]->serial);
     }
   });
 }
@@ -231,6 +252,47 @@ int disc_plan_host_overhead(disc_plan p, int n, const char* const* names, const 
   });
   disc_cuda_set_capture(0);
   return rc;
+}
+
+int disc_plan_algorithmic_bytes(disc_plan p, int n, const char* const* names, const int64_t* const* dims,
+                                const int* ranks, int64_t* bytes) {
+  return guard([&] {
+    const CompiledPlan& plan = *p->plan;
+    std::vector<rt::InputBinding> in(n);
+    for (int i = 0; i < n; ++i) {
+      in[i].name = names[i];
+      in[i].dims.assign(dims[i], dims[i] + ranks[i]);
+    }
+    const std::vector<int64_t> regs = disc_capi::eval_shape_program(plan, [&] {
+      std::vector<std::vector<int64_t>> d(plan.inputs.size());
+      for (size_t k = 0; k < plan.inputs.size(); ++k)
+        for (const auto& b : in)
+          if (b.name == plan.inputs[k].id) d[k] = b.dims;
+      return d;
+    }());
+    int64_t total = 0;
+    for (const auto& ins : plan.instrs) {
+      if (ins.kind == InstrKind::kLaunch) {
+        const KernelArtifact& art = plan.kernels.at(ins.a);
+        const VersionArtifact* ver = nullptr;
+        for (const auto& v : art.versions)
+          if (ins.fixed_version >= 0 ? v.id == ins.fixed_version
+                                     : disc_guard_passes(p, ins.a, v.id, regs.data(), static_cast<int>(regs.size())) == 1) {
+            ver = &v;
+            break;
+          }
+        if (!ver) throw RuntimeError("no kernel version guard matched");
+        std::vector<std::vector<int64_t>> ext;
+        for (const auto& d : art.external_input_dims) ext.push_back(rt::resolve_all(d, regs));
+        total += rt::launch_bytes_estimate(art, *ver, ext, regs);
+      } else if (ins.kind == InstrKind::kLibraryCall) {
+        const int64_t m = rt::resolve(ins.lib_dims[0], regs), k = rt::resolve(ins.lib_dims[1], regs),
+                      q = rt::resolve(ins.lib_dims[2], regs);
+        total += 4 * (m * k + k * q + m * q);
+      }
+    }
+    *bytes = total;
+  });
 }
 
 int disc_guard_passes(disc_plan p, int kernel, int version, const int64_t* regs, int n_regs) {

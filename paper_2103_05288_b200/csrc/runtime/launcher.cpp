@@ -799,6 +799,17 @@ int64_t algorithmic_bytes(const KernelArtifact& art, const std::vector<DevTensor
   return bytes;
 }
 
+}  // namespace
+
+int64_t launch_bytes_estimate(const KernelArtifact& art, const VersionArtifact& ver,
+                              const std::vector<std::vector<int64_t>>& ext_dims, const std::vector<int64_t>& regs) {
+  std::vector<DevTensor> ext(ext_dims.size());
+  for (size_t e = 0; e < ext_dims.size(); ++e) ext[e].dims = ext_dims[e];
+  return algorithmic_bytes(art, ext, simulate_tape(art, ver, ext_dims, regs));
+}
+
+namespace {
+
 // Where the fused lowering sends its work: straight to the device, or into a recipe
 // (cached and replayed with real pointers patched in).
 class Issuer {

@@ -77,6 +77,10 @@ std::vector<std::vector<int64_t>> simulate_tape(const KernelArtifact& art, const
                                                 const std::vector<std::vector<int64_t>>& ext_dims,
                                                 const std::vector<int64_t>& regs);
 
+// Algorithmic boundary bytes of one kLaunch at the given shapes, host only.
+int64_t launch_bytes_estimate(const KernelArtifact& art, const VersionArtifact& ver,
+                              const std::vector<std::vector<int64_t>>& ext_dims, const std::vector<int64_t>& regs);
+
 // u32 fast-division constants (exposed for tests).
 void fast_div_magic(uint32_t d, uint32_t* magic, uint32_t* shift);
 

@@ -146,33 +146,71 @@ def softmax_graph_for(s: int) -> dict:
     return g
 
 
-def mixed_stream(n: int = 10000, seed: int = 20261017, max_bytes: int = 1 << 26):
-    """C5: n distinct (graph, shape) requests drawn with mt19937-style seeding (Python's
-    MT19937); bounded to max_bytes of input per request so the stream fits one pass."""
+def mixed_stream(n: int = 10000, seed: int = 20261017, max_bytes: int = 1 << 22, fixtures: Dict[str, tuple] = None,
+                 valid=None):
+    """C5: n distinct (graph, shape) requests, kinds drawn round-robin over C1-C4 plus the
+    given fixtures {name: (graph, example bindings)} (Python's MT19937, seeded); each
+    request's inputs are bounded by max_bytes.  Fixture symbols that are equal in every
+    example binding stay tied (e.g. split's T0 = T1 = S0).  ``valid(kind, syms)``
+    (optional) rejects shapes the caller finds invalid."""
     rng = random.Random(seed)
     graphs = {"softmax": softmax_graph_for(0), "ln_gelu": ln_gelu_graph(), "colreduce": colreduce_graph(),
               "bert": bert_graph()}
-    seen = set()
-    reqs = []
-    while len(reqs) < n:
-        kind = rng.choice(list(graphs))
+    ties = {}
+    for name, (g, bindings) in (fixtures or {}).items():
+        graphs[f"fx_{name}"] = g
+        tie = {}
+        for b in bindings:
+            for x in b:
+                if x not in tie:
+                    tie[x] = next(y for y in b if all(bb.get(y) == bb.get(x) for bb in bindings))
+        ties[f"fx_{name}"] = tie
+    kinds = list(graphs)
+    cap = max(1, max_bytes // 4)
+
+    def draw(kind):
         if kind == "softmax":
             s = rng.randint(1, 4096)
-            syms = {"S0": max(1, rng.randint(1, max(1, (max_bytes // 4) // s))), "S1": s}
-        elif kind == "ln_gelu":
-            syms = {"T": rng.randint(1, 16384), "H": rng.choice([768, 1024, 4096])}
-            syms["T"] = min(syms["T"], max(1, (max_bytes // 4) // syms["H"]))
-        elif kind == "colreduce":
+            return {"S0": rng.randint(1, max(1, cap // s)), "S1": s}
+        if kind == "ln_gelu":
+            h = rng.choice([768, 1024, 4096])
+            return {"T": rng.randint(1, max(1, min(16384, cap // h))), "H": h}
+        if kind == "colreduce":
             c = rng.randint(1, 4096)
-            syms = {"N": rng.randint(1, max(1, (max_bytes // 4) // c)), "C": c}
-        else:
+            return {"N": rng.randint(1, max(1, cap // c)), "C": c}
+        if kind == "bert":
             b, s = rng.choice([1, 8, 32]), rng.randrange(8, 513, 8)
-            if b * 12 * s * s * 4 > max_bytes:
+            if b * 12 * s * s > cap:
+                return None
+            return {"R": b * 12 * s, "S": s, "T": b * s, "H": 768, "F": 3072}
+        g = graphs[kind]  # fixture: every symbolic dim drawn, constant dims kept
+        tie = ties.get(kind, {})
+        syms = {}
+        for i in g["inputs"]:
+            for d in i["shape"]:
+                if isinstance(d, str) and d not in syms:
+                    root = tie.get(d, d)
+                    if root not in syms:
+                        syms[root] = rng.randint(0 if rng.random() < 0.02 else 1, 4096)
+                    syms[d] = syms[root]
+        return syms
+
+    seen = set()
+    reqs = []
+    k = 0
+    while len(reqs) < n:
+        kind = kinds[k % len(kinds)]
+        k += 1
+        for _ in range(64):
+            syms = draw(kind)
+            if syms is None:
                 continue
-            syms = {"R": b * 12 * s, "S": s, "T": b * s, "H": 768, "F": 3072}
-        key = (kind, tuple(sorted(syms.items())))
-        if key in seen:
-            continue
-        seen.add(key)
-        reqs.append((kind, syms))
+            key = (kind, tuple(sorted(syms.items())))
+            if key in seen:
+                continue
+            if valid is not None and not valid(kind, syms):
+                continue
+            seen.add(key)
+            reqs.append((kind, syms))
+            break
     return graphs, reqs

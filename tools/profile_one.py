@@ -20,14 +20,14 @@ def main():
     ap.add_argument("--schedule", default="auto")
     a = ap.parse_args()
     import paper_2103_05288_b200 as D
-    _, graph, _ = bench.workload(a.workload)
+    _, graph, _ = bench.workload_single(a.workload)
     syms = {k: int(v) for k, v in (kv.split("=") for kv in a.shape.split(","))}
     plan = D.compile_graph(graph)
-    reqs = bench.Requests(D, graph, [syms])
+    reqs = bench.Requests(D, {"g": graph}, {"g": plan}, [("g", syms)])
     ex = D.Executor()
     ex.set_schedule(a.schedule)
     for _ in range(a.reps):
-        reqs.run(ex, plan)
+        reqs.run(ex)
     ex.synchronize()
     print("records", ex.launch_records())
 

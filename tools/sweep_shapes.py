@@ -27,7 +27,7 @@ def main():
     a = ap.parse_args()
     import paper_2103_05288_b200 as D
     L = D.lib()
-    _, graph, shapes = bench.workload(a.workload)
+    _, graph, shapes = bench.workload_single(a.workload)
     D.set_pdl(a.pdl)
     plan = D.compile_graph(graph)
     evs = [C.c_void_p(), C.c_void_p()]
@@ -43,8 +43,8 @@ def main():
     rows = []
     tot_b = tot_ms = 0.0
     for syms in shapes:
-        reqs = bench.Requests(D, graph, [syms])
-        reqs.run(ex, plan)  # warm
+        reqs = bench.Requests(D, {"g": graph}, {"g": plan}, [("g", syms)])
+        reqs.run(ex)  # warm
         ex.synchronize()
         if a.request:
             tot = 0.0
@@ -52,7 +52,7 @@ def main():
                 L.disc_cuda_flush_l2(flush, flush_bytes, stream)
                 L.disc_cuda_spin(2000, stream)
                 L.disc_cuda_event_record(evs[0], stream)
-                reqs.run(ex, plan)
+                reqs.run(ex)
                 L.disc_cuda_event_record(evs[1], stream)
                 ex.synchronize()
                 ms = C.c_float()
@@ -71,7 +71,7 @@ def main():
         for _ in range(a.reps):
             L.disc_cuda_flush_l2(flush, flush_bytes, stream)
             L.disc_cuda_spin(2000, stream)  # queue the request: events time the device only
-            reqs.run(ex, plan)
+            reqs.run(ex)
             ex.synchronize()
             for r in ex.launch_records():
                 k = f"k{r['kernel']}:{r['schedule']}"
