@@ -110,6 +110,11 @@ def build(clean: bool = False, verbose: bool = True) -> str:
     cpp, cu = _sources()
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         objs = list(ex.map(lambda s: _compile(s, inc, tag), cpp + cu))
+    keep = set(objs)
+    for f in os.listdir(os.path.join(BUILD, "obj")):  # objects of older header digests
+        path = os.path.join(BUILD, "obj", f)
+        if path not in keep:
+            os.remove(path)
     newest = max(os.path.getmtime(o) for o in objs)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread", "-ldl", "-lrt"]
