@@ -95,8 +95,9 @@ int disc_executor_num_outputs(disc_executor e);
 /* Device pointer + dims of output i of the last run. */
 int disc_executor_output(disc_executor e, int i, const float** dptr, const int64_t** dims,
                          int* rank);
-/* Copies output i (stream-ordered) to dst (host if dst_on_host, else device); host copies
- * synchronize the stream. */
+/* Copies output i (stream-ordered) to dst: dst_on_host 0 device, 1 host (synchronizes the
+ * stream), 2 pinned host, asynchronous (valid after disc_executor_synchronize; lets
+ * requests on several executors overlap H2D, compute and D2H). */
 int disc_executor_copy_output(disc_executor e, int i, void* dst, int dst_on_host);
 int disc_executor_synchronize(disc_executor e);
 /* ExecStats (executor.hpp:30-40): launch_count, library_calls, host_instruction_count,

@@ -116,7 +116,7 @@ int disc_executor_copy_output(disc_executor e, int i, void* dst, int dst_on_host
     if (n == 0) return;
     if (disc_cuda_memcpy(dst, o.ptr, static_cast<size_t>(n * 4), dst_on_host ? 1 : 2, e->ex.stream()) != 0)
       throw RuntimeError(std::string("output copy: ") + disc_cuda_last_error());
-    if (dst_on_host && disc_cuda_stream_synchronize(e->ex.stream()) != 0)
+    if (dst_on_host == 1 && disc_cuda_stream_synchronize(e->ex.stream()) != 0)
       throw RuntimeError(std::string("stream sync: ") + disc_cuda_last_error());
   });
 }
