@@ -121,7 +121,7 @@ typedef struct {
   int32_t vec;      /* 4 or 1 */
   int32_t wide;     /* 1: 64-bit index math */
   int32_t lpr;      /* lanes per row (power of two <= 32): narrow rows pack several per warp */
-  int32_t pad;
+  int32_t prefetch; /* 1: L2-prefetch the next grid-stride tile's streaming operands */
 } disc_loop_launch;
 
 /* Reduce schedules over the reduce argument collapsed to [K, R, C] (R reduced). */

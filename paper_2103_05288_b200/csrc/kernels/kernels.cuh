@@ -27,6 +27,9 @@ __device__ __forceinline__ void pdl_enter(const disc_program& P) {
 // keeps one body.
 struct Interp {
   static constexpr bool kSplitFull = false;
+  static constexpr int kPipe = 0;  // no load/compute split
+  template <int VEC, int CH, typename Ctx>
+  __device__ __forceinline__ static void prefetch(const disc_program&, const Ctx&) {}
   template <int VEC, int CH, bool WIDE, typename Ctx>
   __device__ __forceinline__ static void run(const disc_program& P, const Ctx& t, typename Vec<VEC>::T (&acc)[CH],
                                              typename Vec<VEC>::T* slots, int stride, const float* consts, float red) {
@@ -111,9 +114,57 @@ __global__ void __launch_bounds__(kLoopThreads, 4) k_loop(const __grid_constant_
   I rg = static_cast<I>(tile / tpr), tc = static_cast<I>(tile - static_cast<int64_t>(rg) * tpr);
   const I drg = static_cast<I>(warps / tpr), dtc = static_cast<I>(warps - static_cast<int64_t>(drg) * tpr);
   const I lane_col = static_cast<I>(lane & (lpr - 1)) * VEC;
+  if constexpr (Prog::kPipe > 0) {
+    // Software pipeline: the next grid-stride tile's streaming loads are issued before
+    // the current tile computes (one tile of loads in flight per thread while the
+    // math runs; registers: kPipe x CH x VEC).
+    using LD = typename Prog::template Loads<VEC, CH>;
+    I row = rg * rpw + sub, col0 = tc * span + lane_col;
+    int nv = (rg < nrg && row < rows) ? chunks_in_row<CH>(W - col0, cstride) : 0;
+    LD cur;
+    if (nv > 0) Prog::template load<VEC, CH, WIDE>(L.prog, Tile<I, false>{row, col0, W, cstride, nv}, cur);
+    while (rg < nrg) {
+      I nrg_ = rg + drg, ntc = tc + dtc;
+      if (ntc >= tpr) {
+        ntc -= tpr;
+        ++nrg_;
+      }
+      const I nrow = nrg_ * rpw + sub, ncol0 = ntc * span + lane_col;
+      const int nnv = (nrg_ < nrg && nrow < rows) ? chunks_in_row<CH>(W - ncol0, cstride) : 0;
+      LD nxt;
+      if (nnv > 0) Prog::template load<VEC, CH, WIDE>(L.prog, Tile<I, false>{nrow, ncol0, W, cstride, nnv}, nxt);
+      T acc[CH];
+      if (nv == CH)
+        Prog::template run_loaded<VEC, CH, WIDE>(L.prog, Tile<I, true>{row, col0, W, cstride, CH}, cur, acc, slots,
+                                                 kLoopThreads, consts, 0.f);
+      else if (CH > 1 && nv > 0)
+        Prog::template run_loaded<VEC, CH, WIDE>(L.prog, Tile<I, false>{row, col0, W, cstride, nv}, cur, acc, slots,
+                                                 kLoopThreads, consts, 0.f);
+      cur = nxt;
+      rg = nrg_;
+      tc = ntc;
+      row = nrow;
+      col0 = ncol0;
+      nv = nnv;
+    }
+    return;
+  }
+  const bool prefetch = L.prefetch != 0;
   for (; rg < nrg;) {
     const I row = rg * rpw + sub;
     const I col0 = tc * span + lane_col;
+    if (prefetch) {  // next grid-stride tile of this warp
+      I ntc = tc + dtc, nrg_ = rg + drg;
+      if (ntc >= tpr) {
+        ntc -= tpr;
+        ++nrg_;
+      }
+      const I nrow = nrg_ * rpw + sub, ncol0 = ntc * span + lane_col;
+      if (nrow < rows) {
+        const int nnv = chunks_in_row<CH>(W - ncol0, cstride);
+        Prog::template prefetch<VEC, CH>(L.prog, Tile<I, false>{nrow, ncol0, W, cstride, nnv});
+      }
+    }
     if (row < rows) {
       const int nv = chunks_in_row<CH>(W - col0, cstride);
       T acc[CH];
@@ -217,7 +268,11 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
     }
     const I row = static_cast<I>(base + sub);
     const bool valid = base + sub < rows;
-    Acc acc = RD::identity();
+    // one accumulator per chunk position: CH independent f64 add chains per thread,
+    // joined in a fixed order (deterministic)
+    Acc part[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) part[c] = RD::identity();
     if (valid) {
       for (I col0 = static_cast<I>(lane) * VEC; col0 < R; col0 += span) {
         const int nv = chunks_in_row<CH>(R - col0, cstride);
@@ -226,16 +281,19 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
           Pre::template run<VEC, CH, WIDE>(L.pre, Tile<I, true, false, STAGED>{row, col0, R, cstride, CH, row_cache, sst}, v, slots,
                                            blockDim.x, consts[0], 0.f);
 #pragma unroll
-          for (int c = 0; c < CH; ++c) acc = RD::acc(acc, v[c]);
+          for (int c = 0; c < CH; ++c) part[c] = RD::acc(part[c], v[c]);
         } else {
           Pre::template run<VEC, CH, WIDE>(L.pre, Tile<I, false, false, STAGED>{row, col0, R, cstride, nv, row_cache, sst}, v, slots,
                                            blockDim.x, consts[0], 0.f);
 #pragma unroll
           for (int c = 0; c < CH; ++c)
-            if (c < nv) acc = RD::acc(acc, v[c]);
+            if (c < nv) part[c] = RD::acc(part[c], v[c]);
         }
       }
     }
+    Acc acc = part[0];
+#pragma unroll
+    for (int c = 1; c < CH; ++c) acc = RD::join(acc, part[c]);
     const int width = G < 32 ? G : 32;
     for (int o = width / 2; o > 0; o >>= 1) acc = RD::join(acc, __shfl_xor_sync(0xffffffffu, acc, o, width));
     float result;

@@ -266,6 +266,19 @@ __device__ __forceinline__ void load_cls(const disc_program& P, const Ctx& t, co
   }
 }
 
+// L2 prefetch of a tile's chunks of load l (streaming identity operands: the next
+// grid-stride tile is requested while the current one computes; no registers held).
+template <int VEC, int CH, int CLS, typename Ctx>
+__device__ __forceinline__ void prefetch_cls(const disc_program& P, const Ctx& t, int l) {
+  if constexpr (CLS == kLcIdentity) {
+    const float* p = P.loads[l].ptr + (t.row * t.W + t.col0);
+    const auto step = t.step();
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      if (t.has(c)) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + c * step));
+  }
+}
+
 template <int VEC, int CH, typename Ctx>
 __device__ __forceinline__ void store_tile(float* out, const Ctx& t, const typename Vec<VEC>::T (&v)[CH]) {
   float* o = out + (t.row * t.W + t.col0);

@@ -447,6 +447,11 @@ disc_loop_launch make_loop(Built& b, int64_t total) {
   L.rows = total / W;
   L.wide = total > kWideLimitView || max_reach(L.prog, L.rows, W) > kWideLimitView;
   L.lpr = lanes_per_row(W, L.vec);
+  static const int pf = [] {
+    const char* e = std::getenv("DISC_PREFETCH");
+    return e ? std::atoi(e) : 1;
+  }();
+  L.prefetch = pf;
   return L;
 }
 

@@ -69,13 +69,33 @@ def collect():
     return seen
 
 
-def gen_program(fn, prog):
-    """Straight-line body for one program (code from the capture)."""
+def gen_program(fn, prog, ch=1):
+    """Straight-line body for one program (code from the capture).
+
+    Identity (streaming) loads are split into a load phase (``load`` fills a Loads
+    struct) and the rest (``run_loaded``), so a schedule can issue the next tile's
+    loads before computing the current one (software pipelining); ``run`` = both."""
     code = prog["code"]
+    ident = [i for i, (op, a, b, flags, dst, load, out) in enumerate(code)
+             if op <= I_LOAD_CONST and prog["lclass"][load] == 0]
+    pf = [f"    prefetch_cls<VEC, CH, 0>(P, t, {code[i][5]});" for i in ident]
     lines = [f"struct {fn} {{",
              "  static constexpr bool kSplitFull = true;",
+             # pipelined only while the extra tile of loads fits (<= 16 registers at VEC=4)
+             f"  static constexpr int kPipe = {len(ident) if len(ident) * ch * 4 <= 16 else 0};",
+             "  template <int VEC, int CH>",
+             "  struct Loads {"] + \
+            [f"    typename Vec<VEC>::T l{i}[CH];" for i in ident] + (["    char none;"] if not ident else []) + \
+            ["  };",
+             "  template <int VEC, int CH, typename Ctx>",
+             "  __device__ __forceinline__ static void prefetch(const disc_program& P, const Ctx& t) {"] + pf + \
+            ["  }",
              "  template <int VEC, int CH, bool WIDE, typename Ctx>",
-             "  __device__ __forceinline__ static void run(const disc_program& P, const Ctx& t,",
+             "  __device__ __forceinline__ static void load(const disc_program& P, const Ctx& t, Loads<VEC, CH>& L) {"] + \
+            [f"    load_cls<VEC, CH, WIDE, 0>(P, t, nullptr, {code[i][5]}, L.l{i});" for i in ident] + \
+            ["  }",
+             "  template <int VEC, int CH, bool WIDE, typename Ctx>",
+             "  __device__ __forceinline__ static void run_loaded(const disc_program& P, const Ctx& t, const Loads<VEC, CH>& L,",
              "      typename Vec<VEC>::T (&acc)[CH], typename Vec<VEC>::T*, int, const float* consts, float red) {",
              "    using T = typename Vec<VEC>::T;"]
     slot_val = {}
@@ -86,7 +106,10 @@ def gen_program(fn, prog):
         def src(is_slot, s):
             return f"v{slot_val[s]}" if is_slot else f"v{i - 1}"
         if op <= I_LOAD_CONST:
-            lines.append(f"    load_cls<VEC, CH, WIDE, {prog['lclass'][load]}>(P, t, consts, {load}, {v});")
+            if i in ident:
+                lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = L.l{i}[c];")
+            else:
+                lines.append(f"    load_cls<VEC, CH, WIDE, {prog['lclass'][load]}>(P, t, consts, {load}, {v});")
         elif op == I_REDVAL:
             lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = splat(red, {v}[c]);")
         elif op == I_COPY:
@@ -104,7 +127,15 @@ def gen_program(fn, prog):
             lines.append(f"    store_out<VEC, CH>(P, {out}, t, {v});")
     if code:
         lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) acc[c] = v{len(code) - 1}[c];")
-    lines += ["  }", "};"]
+    lines += ["  }",
+              "  template <int VEC, int CH, bool WIDE, typename Ctx>",
+              "  __device__ __forceinline__ static void run(const disc_program& P, const Ctx& t,",
+              "      typename Vec<VEC>::T (&acc)[CH], typename Vec<VEC>::T* slots, int stride, const float* consts, float red) {",
+              "    Loads<VEC, CH> L;",
+              "    load<VEC, CH, WIDE>(P, t, L);",
+              "    run_loaded<VEC, CH, WIDE>(P, t, L, acc, slots, stride, consts, red);",
+              "  }",
+              "};"]
     return "\n".join(lines)
 
 
@@ -121,13 +152,15 @@ def generate():
         parts = shards[n % SHARDS]
         tag = f"{kind}_{key}"
         parts.append(f"// {kind} {key} from {src_name}")
-        parts.append(gen_program(f"Pre_{tag}", rec["pre"]))
-        if kind == "row":
-            parts.append(gen_program(f"Post_{tag}", rec["post"]))
         # Chunks per tile: short programs are memory-bound (more loads in flight), long
         # ones register/issue-bound (keep straight-line code small).
         n_code = max(len(rec["pre"]["code"]), len(rec.get("post", {}).get("code", [])))
         ch = 4 if n_code <= 8 else (2 if n_code <= 20 else 1)
+        if 5 in rec["pre"]["lclass"] + rec.get("post", {}).get("lclass", []):
+            ch = min(ch, 2)  # gather index math is register-heavy
+        parts.append(gen_program(f"Pre_{tag}", rec["pre"], ch))
+        if kind == "row":
+            parts.append(gen_program(f"Post_{tag}", rec["post"], ch))
         parts.append(f"cudaError_t launch_{tag}(const void* l, int vec, cudaStream_t s) {{")
         parts.append(f"  constexpr int kGenCH = {ch};")
         if kind == "loop":
