@@ -148,6 +148,16 @@ class Requests:
                                                     self.c_data, self.c_dims, self.c_ranks, 0)
         self.D.api._check(rc)
 
+    def run_streams(self, exs, which):
+        """Requests interleaved over executors (own stream each): request r on which[r]."""
+        if self.n == 0:
+            return
+        c_exs = (C.c_void_p * len(exs))(*[e._h for e in exs])
+        c_which = (C.c_int * self.n)(*which)
+        rc = self.D.lib().disc_executors_run_interleaved(c_exs, len(exs), self.n, c_which, self.c_plans, self.c_offs,
+                                                          self.c_names, self.c_data, self.c_dims, self.c_ranks, 0)
+        self.D.api._check(rc)
+
 
 # ---------------------------------------------------------------------------
 # Clocks during the timed region (B200_PROFILING.md clocks line)
@@ -367,6 +377,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--schedule", default="auto")
     ap.add_argument("--e2e-pipes", type=int, default=3, help="executors/streams the e2e pass alternates over")
+    ap.add_argument("--streams", type=int, default=2,
+                    help="executors/streams per GPU the requests are interleaved over (independent requests overlap)")
+    ap.add_argument("--stream-policy", default="lpt", choices=["size", "lpt"],
+                    help="size: requests >= --big-bytes on stream 0, the rest LPT over the others; lpt: LPT over all")
+    ap.add_argument("--big-bytes", type=float, default=256e6)
     ap.add_argument("--pdl", type=int, default=1, choices=[0, 1, 2],
                     help="programmatic dependent launch: 0 off, 1 overlap launch, 2 + early CTA launch")
     args = ap.parse_args()
@@ -388,11 +403,15 @@ def main():
         _, g2, rq2 = workload(args.workload, replica=r)
         graphs.update(g2)
         reqs = reqs + rq2
-    stream = C.c_void_p()
     D.api._cuda(D.lib().disc_cuda_set_device(local))
-    D.api._cuda(D.lib().disc_cuda_stream_create(C.byref(stream)))
-    ex = D.Executor(local, stream.value)
-    ex.set_schedule(args.schedule)
+    streams, exs = [], []
+    for _ in range(max(1, args.streams)):
+        st = C.c_void_p()
+        D.api._cuda(D.lib().disc_cuda_stream_create(C.byref(st)))
+        streams.append(st)
+        exs.append(D.Executor(local, st.value))
+        exs[-1].set_schedule(args.schedule)
+    stream, ex = streams[0], exs[0]
     compiler = D.Compiler()
     plans = {}
     for k, s in reqs:  # every request asks the cache: 1 compile per distinct graph
@@ -401,6 +420,19 @@ def main():
     mine = shard(costs, world)[rank]
     my_reqs = [reqs[i] for i in mine]
     my_bytes = sum(costs[i] for i in mine)
+    which = [0] * len(mine)  # request -> local stream
+    mc = [costs[i] for i in mine]
+    if args.stream_policy == "size" and len(exs) > 1:
+        # large requests serialise on stream 0 (one-wave kernels that fill the GPU);
+        # small/mid ones (latency-bound per kernel) spread over the other streams
+        small = [j for j, c in enumerate(mc) if c < args.big_bytes]
+        for k, part in enumerate(shard([mc[j] for j in small], len(exs) - 1)):
+            for j in part:
+                which[small[j]] = k + 1
+    else:
+        for k, part in enumerate(shard(mc, len(exs))):  # balanced by bytes (LPT)
+            for j in part:
+                which[j] = k
     rq = Requests(D, graphs, plans, my_reqs, seed=rank)
     D.api._cuda(D.lib().disc_cuda_device_synchronize())
 
@@ -412,11 +444,30 @@ def main():
     ev = [C.c_void_p(), C.c_void_p()]
     for e in ev:
         D.api._cuda(D.lib().disc_cuda_event_create(C.byref(e)))
+    join = []
+    for _ in streams:
+        e = C.c_void_p()
+        D.api._cuda(D.lib().disc_cuda_event_create(C.byref(e)))
+        join.append(e)
+    L = D.lib()
+
+    def one_pass():
+        """One pass over this rank's requests, all streams joined back into streams[0]."""
+        if len(exs) == 1:
+            rq.run(ex)
+            return
+        for st in streams[1:]:
+            L.disc_cuda_stream_wait_event(st, ev[0])
+        rq.run_streams(exs, which)
+        for st, e in zip(streams[1:], join[1:]):
+            L.disc_cuda_event_record(e, st)
+            L.disc_cuda_stream_wait_event(stream, e)
 
     for _ in range(args.warmup):
-        rq.run(ex)
-    D.api._cuda(D.lib().disc_cuda_stream_synchronize(stream))
-    step_bytes = ex.algorithmic_bytes()  # executor's own count for the last pass (this rank)
+        L.disc_cuda_event_record(ev[0], stream)
+        one_pass()
+    D.api._cuda(L.disc_cuda_device_synchronize())
+    step_bytes = sum(e.algorithmic_bytes() for e in exs)  # executors' own count for the last pass (this rank)
     if step_bytes != my_bytes:
         log(f"warning: executor bytes {step_bytes} != planned {my_bytes}")
     total_bytes = allreduce(dist, local, step_bytes, "sum")
@@ -428,13 +479,13 @@ def main():
     wall0 = time.perf_counter()
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            D.lib().disc_cuda_flush_l2(flush, flush_bytes, stream)
-            D.lib().disc_cuda_event_record(ev[0], stream)
-            rq.run(ex)
-            D.lib().disc_cuda_event_record(ev[1], stream)
-            D.lib().disc_cuda_stream_synchronize(stream)
+            L.disc_cuda_flush_l2(flush, flush_bytes, stream)
+            L.disc_cuda_event_record(ev[0], stream)
+            one_pass()
+            L.disc_cuda_event_record(ev[1], stream)
+            L.disc_cuda_stream_synchronize(stream)
             ms = C.c_float()
-            D.lib().disc_cuda_event_elapsed_ms(ev[0], ev[1], C.byref(ms))
+            L.disc_cuda_event_elapsed_ms(ev[0], ev[1], C.byref(ms))
             step_ms.append(ms.value)
     wall = time.perf_counter() - wall0
     flushes = args.steps
@@ -501,7 +552,8 @@ def main():
                        "requests_per_step": len(reqs), "graphs": len(graphs), "bytes_per_step": int(total_bytes),
                        "l2": "flushed before each step (4x L2 write)",
                        "parallelism": f"request-sharded x{world} (LPT on algorithmic bytes, no collectives)",
-                       "schedule": args.schedule, "pdl": args.pdl},
+                       "schedule": args.schedule, "pdl": args.pdl, "streams_per_gpu": len(exs),
+                       "stream_policy": args.stream_policy if len(exs) > 1 else None},
             "frac_of_hbm_peak": round(value / world / peak, 4),
             "recompiles": compile_count - len(graphs),
             "compile_count": compile_count,

@@ -91,6 +91,14 @@ int disc_executor_run_batch(disc_executor e, disc_plan p, int n_requests, int n_
 int disc_executor_run_stream(disc_executor e, int n_requests, const disc_plan* plans, const int* input_offsets,
                              const char* const* names, const void* const* data, const int64_t* const* dims,
                              const int* ranks, int inputs_on_host);
+/* Interleaves a request stream over several executors (each with its own stream and
+ * allocator, typically on one device): request r runs on exs[which[r]].  Independent
+ * requests on different streams overlap on the device (small and mid-size requests are
+ * latency-bound per kernel).  Launch records accumulate per executor over the call. */
+int disc_executors_run_interleaved(const disc_executor* exs, int n_exec, int n_requests, const int* which,
+                                   const disc_plan* plans, const int* input_offsets, const char* const* names,
+                                   const void* const* data, const int64_t* const* dims, const int* ranks,
+                                   int inputs_on_host);
 int disc_executor_num_outputs(disc_executor e);
 /* Device pointer + dims of output i of the last run. */
 int disc_executor_output(disc_executor e, int i, const float** dptr, const int64_t** dims,

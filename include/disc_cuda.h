@@ -202,6 +202,7 @@ int disc_cuda_event_create(void** ev);
 int disc_cuda_event_destroy(void* ev);
 int disc_cuda_event_record(void* ev, void* stream);
 int disc_cuda_event_synchronize(void* ev);
+int disc_cuda_stream_wait_event(void* stream, void* ev);  /* later work on stream waits for ev */
 int disc_cuda_event_elapsed_ms(void* start, void* stop, float* ms);
 
 /* ---- kernels (asynchronous on `stream`) ----------------------------------- */

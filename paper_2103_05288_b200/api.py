@@ -70,6 +70,9 @@ def _declare(L: C.CDLL) -> None:
         "disc_executor_run_batch": ([vp, vp, i32, i32, P(cp), P(vp), P(vp), P(i32), i32], i32),
         "disc_executor_run_stream": ([vp, i32, P(vp), P(i32), P(cp), P(vp), P(vp), P(i32), i32], i32),
         "disc_plan_algorithmic_bytes": ([vp, i32, P(cp), P(vp), P(i32), P(i64)], i32),
+        "disc_executors_run_interleaved": ([P(vp), i32, i32, P(i32), P(vp), P(i32), P(cp), P(vp), P(vp), P(i32), i32],
+                                           i32),
+        "disc_cuda_stream_wait_event": ([vp, vp], i32),
         "disc_executor_num_outputs": ([vp], i32),
         "disc_executor_output": ([vp, i32, P(vp), P(P(i64)), P(i32)], i32),
         "disc_executor_copy_output": ([vp, i32, vp, i32], i32),

@@ -97,6 +97,32 @@ int disc_executor_run_stream(disc_executor e, int n_requests, const disc_plan* p
   });
 }
 
+int disc_executors_run_interleaved(const disc_executor* exs, int n_exec, int n_requests, const int* which,
+                                   const disc_plan* plans, const int* input_offsets, const char* const* names,
+                                   const void* const* data, const int64_t* const* dims, const int* ranks,
+                                   int on_host) {
+  return guard([&] {
+    std::vector<rt::InputBinding> in;
+    std::vector<char> started(n_exec, 0);
+    for (int r = 0; r < n_requests; ++r) {
+      const int x = which[r];
+      if (x < 0 || x >= n_exec) throw disc::Error(disc::ErrorClass::kUsage, "executor index out of range");
+      disc_executor e = exs[x];
+      const int i0 = input_offsets[r], n = input_offsets[r + 1] - i0;
+      in.resize(n);
+      for (int i = 0; i < n; ++i) {
+        const int k = i0 + i;
+        in[i].name = names[k];
+        in[i].dims.assign(dims[k], dims[k] + ranks[k]);
+        in[i].ptr = on_host ? e->ex.stage_input(i, data[k], bytes_of(dims[k], ranks[k]))
+                            : static_cast<const float*>(data[k]);
+      }
+      e->ex.run(*plans[r]->plan, in, started[x] != 0, plans[r]->serial);
+      started[x] = 1;
+    }
+  });
+}
+
 int disc_executor_num_outputs(disc_executor e) { return static_cast<int>(e->ex.outputs().size()); }
 
 int disc_executor_output(disc_executor e, int i, const float** dptr, const int64_t** dims, int* rank) {

@@ -204,6 +204,10 @@ int disc_cuda_event_record(void* ev, void* stream) {
   if (g_capture) return 0;
   return check(cudaEventRecord(static_cast<cudaEvent_t>(ev), S(stream)), "cudaEventRecord");
 }
+int disc_cuda_stream_wait_event(void* stream, void* ev) {
+  if (g_capture) return 0;
+  return check(cudaStreamWaitEvent(S(stream), static_cast<cudaEvent_t>(ev), 0), "cudaStreamWaitEvent");
+}
 int disc_cuda_event_synchronize(void* ev) {
   return check(cudaEventSynchronize(static_cast<cudaEvent_t>(ev)), "cudaEventSynchronize");
 }
