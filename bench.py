@@ -148,6 +148,15 @@ class Requests:
                                                     self.c_data, self.c_dims, self.c_ranks, 0)
         self.D.api._check(rc)
 
+    def run_grouped(self, ex):
+        """One grouped call: every request's runtime flow on the host, then the same plan
+        kernel of all requests as one grouped launch (disc_executor_run_grouped)."""
+        if self.n == 0:
+            return
+        rc = self.D.lib().disc_executor_run_grouped(ex._h, self.n, self.c_plans, self.c_offs, self.c_names,
+                                                     self.c_data, self.c_dims, self.c_ranks, 0)
+        self.D.api._check(rc)
+
     def run_streams(self, exs, which):
         """Requests interleaved over executors (own stream each): request r on which[r]."""
         if self.n == 0:
@@ -377,6 +386,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--schedule", default="auto")
     ap.add_argument("--e2e-pipes", type=int, default=3, help="executors/streams the e2e pass alternates over")
+    ap.add_argument("--mode", default="grouped", choices=["grouped", "streams"],
+                    help="grouped: one disc_executor_run_grouped call per step (the same plan kernel of all "
+                         "requests fused into one grouped launch); streams: per-request launches interleaved "
+                         "over --streams executors")
     ap.add_argument("--streams", type=int, default=2,
                     help="executors/streams per GPU the requests are interleaved over (independent requests overlap)")
     ap.add_argument("--stream-policy", default="lpt", choices=["size", "lpt"],
@@ -405,7 +418,7 @@ def main():
         reqs = reqs + rq2
     D.api._cuda(D.lib().disc_cuda_set_device(local))
     streams, exs = [], []
-    for _ in range(max(1, args.streams)):
+    for _ in range(max(1, args.streams) if args.mode == "streams" else 1):
         st = C.c_void_p()
         D.api._cuda(D.lib().disc_cuda_stream_create(C.byref(st)))
         streams.append(st)
@@ -453,6 +466,9 @@ def main():
 
     def one_pass():
         """One pass over this rank's requests, all streams joined back into streams[0]."""
+        if args.mode == "grouped":
+            rq.run_grouped(ex)
+            return
         if len(exs) == 1:
             rq.run(ex)
             return
@@ -466,6 +482,7 @@ def main():
     for _ in range(args.warmup):
         L.disc_cuda_event_record(ev[0], stream)
         one_pass()
+        L.disc_cuda_stream_synchronize(stream)
     D.api._cuda(L.disc_cuda_device_synchronize())
     step_bytes = sum(e.algorithmic_bytes() for e in exs)  # executors' own count for the last pass (this rank)
     if step_bytes != my_bytes:
@@ -475,17 +492,28 @@ def main():
     # ---- timed region: K steps, device time per step (flush untimed) ----
     launches0 = D.kernel_launches()
     step_ms = []
+    step_ev = []
+    for _ in range(2 * args.steps):
+        e = C.c_void_p()
+        D.api._cuda(L.disc_cuda_event_create(C.byref(e)))
+        step_ev.append(e)
     barrier(dist, local)
     wall0 = time.perf_counter()
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
+        # K steps issued back to back (the host prepares step i+1 while the device runs
+        # step i); each step's device time is its own event pair, the L2 flush before it
+        # is outside the pair.
+        for i in range(args.steps):
             L.disc_cuda_flush_l2(flush, flush_bytes, stream)
-            L.disc_cuda_event_record(ev[0], stream)
+            L.disc_cuda_event_record(step_ev[2 * i], stream)
+            if args.mode != "grouped":
+                L.disc_cuda_event_record(ev[0], stream)  # the interleaved streams wait on it
             one_pass()
-            L.disc_cuda_event_record(ev[1], stream)
-            L.disc_cuda_stream_synchronize(stream)
+            L.disc_cuda_event_record(step_ev[2 * i + 1], stream)
+        L.disc_cuda_stream_synchronize(stream)
+        for i in range(args.steps):
             ms = C.c_float()
-            L.disc_cuda_event_elapsed_ms(ev[0], ev[1], C.byref(ms))
+            L.disc_cuda_event_elapsed_ms(step_ev[2 * i], step_ev[2 * i + 1], C.byref(ms))
             step_ms.append(ms.value)
     wall = time.perf_counter() - wall0
     flushes = args.steps
@@ -503,7 +531,10 @@ def main():
     for _ in range(2):
         D.lib().disc_cuda_flush_l2(flush, flush_bytes, stream)
         D.lib().disc_cuda_spin(50000, stream)
-        rq.run(ex)
+        if args.mode == "grouped":
+            rq.run_grouped(ex)  # one record per grouped launch
+        else:
+            rq.run(ex)
         D.lib().disc_cuda_stream_synchronize(stream)
         records.extend(ex.launch_records())
     ex.set_timing(False)
@@ -534,7 +565,8 @@ def main():
     # ---- e2e through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
-        e2e = measure_e2e(D, graphs, plans, my_reqs, [costs[i] for i in mine], local, stream, pipes=args.e2e_pipes)
+        e2e = measure_e2e(D, graphs, plans, my_reqs, [costs[i] for i in mine], local, stream, pipes=args.e2e_pipes,
+                          grouped=args.mode == "grouped")
         if e2e is not None and dist is not None:
             e2e["value"] = round(allreduce(dist, local, e2e["bytes"], "sum") /
                                  allreduce(dist, local, e2e["seconds"], "max") / 1e9, 2)
@@ -552,7 +584,8 @@ def main():
                        "requests_per_step": len(reqs), "graphs": len(graphs), "bytes_per_step": int(total_bytes),
                        "l2": "flushed before each step (4x L2 write)",
                        "parallelism": f"request-sharded x{world} (LPT on algorithmic bytes, no collectives)",
-                       "schedule": args.schedule, "pdl": args.pdl, "streams_per_gpu": len(exs),
+                       "schedule": args.schedule, "pdl": args.pdl, "mode": args.mode,
+                       "streams_per_gpu": len(exs),
                        "stream_policy": args.stream_policy if len(exs) > 1 else None},
             "frac_of_hbm_peak": round(value / world / peak, 4),
             "recompiles": compile_count - len(graphs),
@@ -576,7 +609,8 @@ def main():
         dist.destroy_process_group()
 
 
-def measure_e2e(D, graphs, plans, reqs, costs, device, stream, max_input_bytes=8 << 30, pipes=3):
+def measure_e2e(D, graphs, plans, reqs, costs, device, stream, max_input_bytes=8 << 30, pipes=3, grouped=True,
+                chunk_bytes=1 << 30):
     """Public API, host buffers: every request's inputs go H2D from pinned memory inside
     disc_executor_run(inputs_on_host=1), its outputs D2H into pinned memory
     (disc_executor_copy_output, async); wall time of one pass.  Requests alternate over
@@ -621,8 +655,61 @@ def measure_e2e(D, graphs, plans, reqs, costs, device, stream, max_input_bytes=8
         return None
     outs = {}
 
+    def out_buf(key, n):
+        if key not in outs:
+            p = C.c_void_p()
+            D.api._cuda(L.disc_cuda_host_alloc(max(4 * n, 16), C.byref(p)))
+            outs[key] = p
+        return outs[key]
+
+    # grouped: consecutive requests in chunks of ~chunk_bytes of boundary traffic, one
+    # disc_executor_run_grouped(inputs_on_host=1) call per chunk, chunks alternating over
+    # the pipes (chunk c's H2D overlaps chunk c-1's kernels and chunk c-2's D2H)
+    chunks, cur, acc = [], [], 0
+    for r, cost in enumerate(costs[:len(work)]):
+        cur.append(r)
+        acc += cost
+        if acc >= chunk_bytes:
+            chunks.append(cur)
+            cur, acc = [], 0
+    if cur:
+        chunks.append(cur)
+    cargs = []
+    for ch in chunks:
+        names, datas, dimsp, ranks, offs, hplans = [], [], [], [], [0], []
+        for r in ch:
+            plan, c_names, data, dims, c_dims, c_ranks = work[r]
+            n = len(dims)
+            names += [c_names[i] for i in range(n)]
+            datas += [data[i] for i in range(n)]
+            dimsp += [c_dims[i] for i in range(n)]
+            ranks += [c_ranks[i] for i in range(n)]
+            offs.append(offs[-1] + n)
+            hplans.append(plan._h)
+        t = max(len(names), 1)
+        cargs.append((len(ch), (C.c_void_p * len(ch))(*hplans), (C.c_int * (len(ch) + 1))(*offs),
+                      (C.c_char_p * t)(*names), (C.c_void_p * t)(*datas), (C.c_void_p * t)(*dimsp),
+                      (C.c_int * t)(*ranks)))
+
+    def one_pass_grouped():
+        nonlocal d2h
+        d2h = 0
+        for c, (ch, a) in enumerate(zip(chunks, cargs)):
+            ex = exs[c % pipes]
+            D.api._check(L.disc_executor_run_grouped(ex._h, *a, 1))
+            for j, r in enumerate(ch):
+                for o, (_, odims) in enumerate(ex.request_output_views(j)):
+                    n = int(np.prod(odims)) if odims else 1
+                    if n:
+                        D.api._check(L.disc_executor_copy_request_output(ex._h, j, o, out_buf((r, o), n), 2))
+                    d2h += 4 * n
+        for ex in exs:
+            ex.synchronize()
+
     def one_pass():
         nonlocal d2h
+        if grouped:
+            return one_pass_grouped()
         d2h = 0
         for r, (plan, c_names, data, dims, c_dims, c_ranks) in enumerate(work):
             ex = exs[r % pipes]
@@ -647,11 +734,14 @@ def measure_e2e(D, graphs, plans, reqs, costs, device, stream, max_input_bytes=8
     for p in pinned + list(outs.values()):
         L.disc_cuda_host_free(p)
     del exs
+    path = (f"disc_executor_run_grouped(inputs_on_host=1) per chunk of requests ({len(chunks)} chunks of "
+            f"~{chunk_bytes >> 20} MB) + disc_executor_copy_request_output(pinned host, async), chunks alternating "
+            f"over {pipes} executors/streams") if grouped else \
+        (f"disc_executor_run(inputs_on_host=1) + disc_executor_copy_output(pinned host, async) per "
+         f"request, requests alternating over {pipes} executors/streams")
     return {"value": round(nbytes / dt / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 3), "requests": len(work),
-            "path": f"disc_executor_run(inputs_on_host=1) + disc_executor_copy_output(pinned host, async) per "
-                    f"request, requests alternating over {pipes} executors/streams",
-            "bytes": nbytes, "seconds": dt}
+            "path": path, "bytes": nbytes, "seconds": dt}
 
 
 if __name__ == "__main__":

@@ -91,6 +91,25 @@ int disc_executor_run_batch(disc_executor e, disc_plan p, int n_requests, int n_
 int disc_executor_run_stream(disc_executor e, int n_requests, const disc_plan* plans, const int* input_offsets,
                              const char* const* names, const void* const* data, const int64_t* const* dims,
                              const int* ranks, int inputs_on_host);
+/* Grouped execution of independent requests (same arguments as run_stream).  Every
+ * request's runtime flow -- shape program, buffer plan, version guards, schedule
+ * selection, the reference's runtime checks -- runs on the host exactly as in
+ * disc_executor_run, but its device work is queued; the queue is then issued level by
+ * level with the same fused kernel of ALL requests merged into one grouped launch per
+ * kernel instantiation (disc_cuda_queue_*).  Outputs are bit-identical to running the
+ * requests one by one; no buffer is reused across requests inside the call.  Request r's
+ * outputs: disc_executor_request_output / _copy_request_output, valid until the next run.
+ * Launch records (timing mode) are one per grouped launch.  Replaces a loop of
+ * Executor::run calls (executor.cpp:221-465) for a batch of requests. */
+int disc_executor_run_grouped(disc_executor e, int n_requests, const disc_plan* plans, const int* input_offsets,
+                              const char* const* names, const void* const* data, const int64_t* const* dims,
+                              const int* ranks, int inputs_on_host);
+int disc_executor_num_requests(disc_executor e);
+int disc_executor_num_request_outputs(disc_executor e, int request);  /* -1: no such request */
+int disc_executor_request_output(disc_executor e, int request, int i, const float** dptr, const int64_t** dims,
+                                 int* rank);
+int disc_executor_copy_request_output(disc_executor e, int request, int i, void* dst, int dst_on_host);
+int disc_executor_request_stats(disc_executor e, int request, int64_t* stats7);
 /* Interleaves a request stream over several executors (each with its own stream and
  * allocator, typically on one device): request r runs on exs[which[r]].  Independent
  * requests on different streams overlap on the device (small and mid-size requests are

@@ -234,6 +234,33 @@ int disc_cuda_pdl_mode(void);
 int disc_cuda_set_specialization(int enabled);
 int64_t disc_cuda_specialized_launches(void);
 int disc_cuda_num_specializations(void);
+/* ---- grouped launches and the request queue --------------------------------
+ * A grouped launch issues n independent fused launches as ONE kernel per homogeneous
+ * subgroup (same kernel instantiation: program structure, schedule, vector width, index
+ * width); each member keeps its single-launch grid and its results are bit-identical
+ * to a separate launch.  Descriptors are uploaded through a pinned ring buffer.
+ * (No reference counterpart: the reference runs one request at a time,
+ * executor.cpp:221-465; this is the SURVEY 8(f) rank-3 host-dispatch item.) */
+int disc_cuda_launch_loop_group(const disc_loop_launch* const* launches, int n, void* stream);
+int disc_cuda_launch_reduce_group(const disc_reduce_launch* const* launches, int n, void* stream);
+/* Queue mode (per host thread): launches, copies and memsets on `stream` are recorded
+ * instead of issued (allocations stay immediate, frees on `stream` are deferred until the
+ * flush).  disc_cuda_queue_request() starts the next independent request (a dependency
+ * chain); disc_cuda_queue_mark() attributes the ops queued since the previous mark to
+ * one kLaunch (algorithmic bytes, artifact id, schedule name).  disc_cuda_queue_flush()
+ * issues the k-th op of every request as level k -- fused launches of a level grouped by
+ * kernel instantiation, larger members first -- then the deferred frees, and ends queue
+ * mode.  With timing != 0 every issued group is bracketed by events; the records are
+ * readable after a synchronize through disc_cuda_queue_record(). */
+int disc_cuda_queue_begin(void* stream);
+int disc_cuda_queue_request(void);
+int disc_cuda_queue_mark(int64_t bytes, int kernel, const char* schedule);
+int disc_cuda_queue_flush(int timing);
+int disc_cuda_queue_active(void);
+int disc_cuda_queue_num_records(void);
+int disc_cuda_queue_record(int i, int* level, int* members, int64_t* bytes, int* kernel, const char** schedule,
+                           float* ms);
+
 /* Capture mode (pattern generator, host only): device calls become no-ops, allocations
  * return fake addresses and fused launches are recorded as JSON program structures. */
 int disc_cuda_set_capture(int enabled);

@@ -73,6 +73,13 @@ def _declare(L: C.CDLL) -> None:
         "disc_executors_run_interleaved": ([P(vp), i32, i32, P(i32), P(vp), P(i32), P(cp), P(vp), P(vp), P(i32), i32],
                                            i32),
         "disc_cuda_stream_wait_event": ([vp, vp], i32),
+        "disc_executor_run_grouped": ([vp, i32, P(vp), P(i32), P(cp), P(vp), P(vp), P(i32), i32], i32),
+        "disc_executor_num_requests": ([vp], i32),
+        "disc_executor_num_request_outputs": ([vp, i32], i32),
+        "disc_executor_request_output": ([vp, i32, i32, P(vp), P(P(i64)), P(i32)], i32),
+        "disc_executor_copy_request_output": ([vp, i32, i32, vp, i32], i32),
+        "disc_executor_request_stats": ([vp, i32, P(i64)], i32),
+        "disc_cuda_queue_active": ([], i32),
         "disc_executor_num_outputs": ([vp], i32),
         "disc_executor_output": ([vp, i32, P(vp), P(P(i64)), P(i32)], i32),
         "disc_executor_copy_output": ([vp, i32, vp, i32], i32),
@@ -458,9 +465,12 @@ class Executor:
         keep, n, names, data, dims, ranks, host = self._bind(inputs)
         _check(lib().disc_executor_run(self._h, plan._h, n, names, data, dims, ranks, int(host)))
 
-    def run_stream(self, requests: Sequence[Tuple[CompiledPlan, Dict[str, object]]]) -> None:
-        """Runs (plan, inputs) requests back to back on this executor's stream (inputs all
-        device-resident or all host); outputs of the last request stay readable."""
+    def run_stream(self, requests: Sequence[Tuple[CompiledPlan, Dict[str, object]]], grouped: bool = False) -> None:
+        """Runs (plan, inputs) requests on this executor's stream (inputs all
+        device-resident or all host).  grouped=False: back to back, outputs of the last
+        request stay readable.  grouped=True: disc_executor_run_grouped -- the same plan
+        kernel of all requests runs as one grouped launch; every request's outputs stay
+        readable (request_outputs)."""
         keep, names, datas, dims, offs, plans = [], [], [], [], [0], []
         host = None
         for plan, inputs in requests:
@@ -479,9 +489,44 @@ class Executor:
         ranks = [r for item in keep if isinstance(item, list) for r in item]
         m = len(requests)
         t = max(offs[-1], 1)
-        _check(lib().disc_executor_run_stream(
+        fn = lib().disc_executor_run_grouped if grouped else lib().disc_executor_run_stream
+        _check(fn(
             self._h, m, (C.c_void_p * max(m, 1))(*plans), (C.c_int * (m + 1))(*offs), (C.c_char_p * t)(*names),
             (C.c_void_p * t)(*datas), (C.c_void_p * t)(*dims), (C.c_int * t)(*ranks), int(bool(host))))
+
+    def run_grouped(self, requests: Sequence[Tuple[CompiledPlan, Dict[str, object]]]) -> List[List[np.ndarray]]:
+        """Grouped execution of independent requests; returns every request's host outputs."""
+        self.run_stream(requests, grouped=True)
+        outs = self.fetch_request_outputs()
+        self.synchronize()
+        return outs
+
+    def request_output_views(self, r: int) -> List[Tuple[int, Tuple[int, ...]]]:
+        L = lib()
+        res = []
+        for i in range(L.disc_executor_num_request_outputs(self._h, r)):
+            p, d, k = C.c_void_p(), C.POINTER(C.c_int64)(), C.c_int()
+            _check(L.disc_executor_request_output(self._h, r, i, C.byref(p), C.byref(d), C.byref(k)))
+            res.append((p.value or 0, tuple(d[j] for j in range(k.value))))
+        return res
+
+    def fetch_request_outputs(self) -> List[List[np.ndarray]]:
+        L = lib()
+        out = []
+        for r in range(L.disc_executor_num_requests(self._h)):
+            row = []
+            for i, (_, dims) in enumerate(self.request_output_views(r)):
+                a = np.empty(dims, dtype=np.float32)
+                if a.size:
+                    _check(L.disc_executor_copy_request_output(self._h, r, i, a.ctypes.data, 1))
+                row.append(a)
+            out.append(row)
+        return out
+
+    def request_stats(self, r: int) -> ExecStats:
+        s = (C.c_int64 * 7)()
+        _check(lib().disc_executor_request_stats(self._h, r, s))
+        return ExecStats(*list(s), 0.0, 0.0)
 
     def output_views(self) -> List[Tuple[int, Tuple[int, ...]]]:
         L = lib()

@@ -123,6 +123,76 @@ int disc_executors_run_interleaved(const disc_executor* exs, int n_exec, int n_r
   });
 }
 
+int disc_executor_run_grouped(disc_executor e, int n_requests, const disc_plan* plans, const int* input_offsets,
+                              const char* const* names, const void* const* data, const int64_t* const* dims,
+                              const int* ranks, int on_host) {
+  return guard([&] {
+    e->ex.begin_grouped();
+    try {
+      std::vector<rt::InputBinding> in;
+      for (int r = 0; r < n_requests; ++r) {
+        e->ex.begin_request();
+        const int i0 = input_offsets[r], n = input_offsets[r + 1] - i0;
+        in.resize(n);
+        for (int i = 0; i < n; ++i) {
+          const int k = i0 + i;
+          in[i].name = names[k];
+          in[i].dims.assign(dims[k], dims[k] + ranks[k]);
+          // one staging buffer per (request, input): all of a group's copies are in flight together
+          in[i].ptr = on_host ? e->ex.stage_input(k, data[k], bytes_of(dims[k], ranks[k]))
+                              : static_cast<const float*>(data[k]);
+        }
+        e->ex.run(*plans[r]->plan, in, true, plans[r]->serial);
+      }
+    } catch (...) {
+      try {
+        e->ex.end_grouped();  // issue what was queued (valid work), then report the error
+      } catch (...) {
+      }
+      throw;
+    }
+    e->ex.end_grouped();
+  });
+}
+
+int disc_executor_num_requests(disc_executor e) { return static_cast<int>(e->ex.request_outputs().size()); }
+
+int disc_executor_num_request_outputs(disc_executor e, int r) {
+  const auto& ro = e->ex.request_outputs();
+  return r >= 0 && r < static_cast<int>(ro.size()) ? static_cast<int>(ro[r].size()) : -1;
+}
+
+int disc_executor_request_output(disc_executor e, int r, int i, const float** dptr, const int64_t** dims, int* rank) {
+  return guard([&] {
+    const auto& o = e->ex.request_outputs().at(r).at(i);
+    *dptr = o.ptr;
+    *dims = o.dims.data();
+    *rank = static_cast<int>(o.dims.size());
+  });
+}
+
+int disc_executor_copy_request_output(disc_executor e, int r, int i, void* dst, int dst_on_host) {
+  return guard([&] {
+    const auto& o = e->ex.request_outputs().at(r).at(i);
+    int64_t n = 1;
+    for (int64_t d : o.dims) n *= d;
+    if (n == 0) return;
+    if (disc_cuda_memcpy(dst, o.ptr, static_cast<size_t>(n * 4), dst_on_host ? 1 : 2, e->ex.stream()) != 0)
+      throw RuntimeError(std::string("output copy: ") + disc_cuda_last_error());
+    if (dst_on_host == 1 && disc_cuda_stream_synchronize(e->ex.stream()) != 0)
+      throw RuntimeError(std::string("stream sync: ") + disc_cuda_last_error());
+  });
+}
+
+int disc_executor_request_stats(disc_executor e, int r, int64_t* s7) {
+  return guard([&] {
+    const auto& s = e->ex.request_stats().at(r);
+    int64_t v[7] = {s.launch_count, s.library_calls, s.host_instruction_count, s.peak_bytes,
+                    s.alloc_calls, s.allocator_cache_hits, s.aliased_allocs};
+    std::memcpy(s7, v, sizeof v);
+  });
+}
+
 int disc_executor_num_outputs(disc_executor e) { return static_cast<int>(e->ex.outputs().size()); }
 
 int disc_executor_output(disc_executor e, int i, const float** dptr, const int64_t** dims, int* rank) {

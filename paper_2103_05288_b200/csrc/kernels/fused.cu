@@ -27,13 +27,13 @@ __device__ __host__ inline int finalize_lanes(int splits) {
   return l;
 }
 
-__global__ void __launch_bounds__(256) k_col_finalize(const __grid_constant__ disc_reduce_launch L) {
+__device__ __forceinline__ void finalize_body(const disc_reduce_launch& L, const int bx, const int gx) {
   __shared__ double part[256];
   pdl_enter(L.pre);
   const int64_t n = L.K * L.C;
   const int lpo = finalize_lanes(L.splits), opb = 256 / lpo;
   const int ox = threadIdx.x / lpo, sl = threadIdx.x % lpo;
-  for (int64_t base = static_cast<int64_t>(blockIdx.x) * opb; base < n; base += static_cast<int64_t>(gridDim.x) * opb) {
+  for (int64_t base = static_cast<int64_t>(bx) * opb; base < n; base += static_cast<int64_t>(gx) * opb) {
     const int64_t o = base + ox;
     if (L.schedule != DISC_SCHED_COL_TWOPASS) {
       if (sl == 0 && o < n) L.red_out[o] = static_cast<float>(L.workspace[o]);
@@ -51,6 +51,16 @@ __global__ void __launch_bounds__(256) k_col_finalize(const __grid_constant__ di
     if (sl == 0 && o < n) L.red_out[o] = static_cast<float>(part[threadIdx.x]);
     __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(256) k_col_finalize(const __grid_constant__ disc_reduce_launch L) {
+  finalize_body(L, blockIdx.x, gridDim.x);
+}
+__global__ void __launch_bounds__(256) k_col_finalize_g(const __grid_constant__ disc_group G) {
+  __shared__ __align__(16) unsigned char desc[desc_bytes<disc_reduce_launch>()];
+  const int b = blockIdx.x, g = group_of(G, b);
+  const disc_reduce_launch& L = group_stage<disc_reduce_launch>(G, g, desc);
+  finalize_body(L, b - G.block_off[g], G.block_off[g + 1] - G.block_off[g]);
 }
 
 // ---------------------------------------------------------------------------
@@ -136,28 +146,47 @@ using namespace disc_dev;
 void set_pdl(int mode) { g_pdl = mode; }
 int pdl_mode() { return g_pdl; }
 
-cudaError_t loop(const disc_loop_launch& L, cudaStream_t s) {
-  if (L.vec == 4) return L.wide ? launch_loop_with(k_loop<4, true, Interp>, L, s) : launch_loop_with(k_loop<4, false, Interp>, L, s);
-  return L.wide ? launch_loop_with(k_loop<1, true, Interp>, L, s) : launch_loop_with(k_loop<1, false, Interp>, L, s);
+cudaError_t loop(const disc_loop_launch& L, cudaStream_t s, const HostGroup* g) {
+  return loop_pass<Interp>(L, s, true, g);
 }
 
-cudaError_t col_pass(const disc_reduce_launch& L, cudaStream_t s);
+cudaError_t col_pass(const disc_reduce_launch& L, cudaStream_t s, const HostGroup* g);
 
-cudaError_t finalize_columns(const disc_reduce_launch& L, cudaStream_t s) {
-  if (L.schedule == DISC_SCHED_COL_SINGLE) return cudaSuccess;
+inline int64_t finalize_blocks(const disc_reduce_launch& L) {
   const int64_t n = L.K * L.C;
   const int64_t opb = 256 / finalize_lanes(L.splits);
   const int64_t want = (n + opb - 1) / opb;
-  const cudaError_t e = launch_k(k_col_finalize, dim3(static_cast<int>(want < sm_count() * 8 ? want : sm_count() * 8)),
-                                 dim3(256), 0, s, L);
+  return want < sm_count() * 8 ? want : sm_count() * 8;
+}
+
+cudaError_t finalize_columns(const disc_reduce_launch& L, cudaStream_t s, const HostGroup* g) {
+  if (g) {  // members are two-pass / atomic launches
+    disc_group G;
+    G.table = g->dev_table;
+    G.stride = g->stride;
+    G.n = g->n;
+    int64_t off = 0;
+    for (int i = 0; i < g->n; ++i) {
+      G.block_off[i] = static_cast<int32_t>(off);
+      const disc_reduce_launch& M = g->at<disc_reduce_launch>(i);
+      if (M.K * M.C > 0 && M.schedule != DISC_SCHED_COL_SINGLE) off += finalize_blocks(M);
+    }
+    G.block_off[g->n] = static_cast<int32_t>(off);
+    if (off == 0) return cudaSuccess;
+    const cudaError_t e = launch_k(k_col_finalize_g, dim3(static_cast<unsigned>(off)), dim3(256), 0, s, G);
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
+  if (L.schedule == DISC_SCHED_COL_SINGLE) return cudaSuccess;
+  const cudaError_t e = launch_k(k_col_finalize, dim3(static_cast<int>(finalize_blocks(L))), dim3(256), 0, s, L);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-cudaError_t reduce(const disc_reduce_launch& L, cudaStream_t s) {
+cudaError_t reduce(const disc_reduce_launch& L, cudaStream_t s, const HostGroup* g) {
   if (L.schedule == DISC_SCHED_ROW) {
-    return row_pass<Interp, Interp>(L, s, true);
+    return row_pass<Interp, Interp>(L, s, true, g);
   }
   if (L.schedule == DISC_SCHED_GENERIC) {
+    if (g) return cudaErrorInvalidValue;  // never grouped (device layer issues these one by one)
     if (L.K <= 0) return cudaSuccess;
     const int slots = L.pre.n_slots;
     const int64_t want = (L.K + kLoopThreads - 1) / kLoopThreads;
@@ -168,9 +197,11 @@ cudaError_t reduce(const disc_reduce_launch& L, cudaStream_t s) {
     e = launch_k(k_reduce_generic, dim3(grid), dim3(kLoopThreads), smem, s, L);
     return e != cudaSuccess ? e : cudaGetLastError();
   }
-  return col_pass(L, s);  // column schedules: the device layer adds memset/finalize
+  return col_pass(L, s, g);  // column schedules: the device layer adds memset/finalize
 }
 
-cudaError_t col_pass(const disc_reduce_launch& L, cudaStream_t s) { return col_pass_t<Interp>(L, s, true); }
+cudaError_t col_pass(const disc_reduce_launch& L, cudaStream_t s, const HostGroup* g) {
+  return col_pass_t<Interp>(L, s, true, g);
+}
 
 }  // namespace disc_launch

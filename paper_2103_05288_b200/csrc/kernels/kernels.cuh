@@ -4,6 +4,7 @@
 // so both share one schedule implementation.  See fused.cu for the launchers.
 #pragma once
 
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 #include <type_traits>
@@ -86,11 +87,55 @@ constexpr int kLoopThreads = 256;
 constexpr int kCH = 2;  // chunks per thread per dispatch
 
 // ---------------------------------------------------------------------------
+// Grouped launches: ONE kernel covers n independent launches that share a kernel
+// instantiation (same program structure / schedule template), e.g. the same plan
+// kernel of many variable-shape requests.  Launch g owns CTAs [block_off[g],
+// block_off[g+1]) and runs exactly the single-launch body with (local block, local
+// grid), so results are identical to n separate launches.  Its launch descriptor lives
+// in a device table (uploaded by the device layer) and is staged into shared memory
+// once per CTA; the CTA -> launch map is a binary search over the offsets held in
+// __grid_constant__ parameter space.
+#ifndef DISC_MAX_GROUP
+#define DISC_MAX_GROUP 1024
+#endif
+struct disc_group {
+  const unsigned char* table;  // n descriptors, `stride` bytes apart
+  int32_t stride;
+  int32_t n;
+  int32_t block_off[DISC_MAX_GROUP + 1];
+};
+
+__device__ __forceinline__ int group_of(const disc_group& G, int b) {
+  int lo = 0, hi = G.n;  // block_off[lo] <= b < block_off[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (G.block_off[mid] <= b) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+template <typename Launch>
+constexpr int desc_bytes() { return (static_cast<int>(sizeof(Launch)) + 15) / 16 * 16; }
+
+// Copies descriptor g into shared memory (16 B per thread per step).  The table was
+// written by a copy ordered before the previous kernel in the stream, so it may be read
+// before griddepcontrol.wait.
+template <typename Launch>
+__device__ __forceinline__ const Launch& group_stage(const disc_group& G, int g, unsigned char* buf) {
+  const uint4* src = reinterpret_cast<const uint4*>(G.table + static_cast<int64_t>(g) * G.stride);
+  uint4* dst = reinterpret_cast<uint4*>(buf);
+  for (int i = threadIdx.x; i < desc_bytes<Launch>() / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+  __syncthreads();
+  return *reinterpret_cast<const Launch*>(buf);
+}
+
+// ---------------------------------------------------------------------------
 // kLoop: the space viewed as [rows, W].  A warp tile covers 32/lpr rows x (lpr*CH*VEC)
 // columns: lpr lanes share a row (lane l takes chunks l, l+lpr, ... so every access is
 // coalesced), narrow rows pack several per warp.  Grid-stride over warp tiles.
-template <int VEC, bool WIDE, typename Prog, int CH = kCH>
-__global__ void __launch_bounds__(kLoopThreads, 4) k_loop(const __grid_constant__ disc_loop_launch L) {
+template <int VEC, bool WIDE, typename Prog, int CH>
+__device__ __forceinline__ void loop_body(const disc_loop_launch& L, const int bx, const int gx) {
   using T = typename Vec<VEC>::T;
   using I = IndexT<WIDE>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -108,8 +153,8 @@ __global__ void __launch_bounds__(kLoopThreads, 4) k_loop(const __grid_constant_
   const I span = cstride * CH;
   const I tpr = (W + span - 1) / span;
   const I nrg = (rows + rpw - 1) / rpw;
-  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  const int64_t tile = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t warps = static_cast<int64_t>(gx) * (blockDim.x >> 5);
+  const int64_t tile = static_cast<int64_t>(bx) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   // (row group, column tile) advanced incrementally: one division per thread, not per tile.
   I rg = static_cast<I>(tile / tpr), tc = static_cast<I>(tile - static_cast<int64_t>(rg) * tpr);
   const I drg = static_cast<I>(warps / tpr), dtc = static_cast<I>(warps - static_cast<int64_t>(drg) * tpr);
@@ -215,8 +260,8 @@ __device__ __forceinline__ void copy_span(float* __restrict__ dst, const float* 
   }
 }
 
-template <int VEC, bool WIDE, int KIND, typename Pre, typename Post, int CH = kCH, bool STAGED = false>
-__global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduce_launch L) {
+template <int VEC, bool WIDE, int KIND, typename Pre, typename Post, int CH, bool STAGED>
+__device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int bx, const int gx) {
   using RD = Red<KIND>;
   using Acc = typename RD::Acc;
   using T = typename Vec<VEC>::T;
@@ -246,7 +291,7 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
   const I cstride = static_cast<I>(G) * VEC;
   const I span = cstride * CH;
 
-  for (int64_t base = static_cast<int64_t>(blockIdx.x) * rpb; base < rows; base += static_cast<int64_t>(gridDim.x) * rpb) {
+  for (int64_t base = static_cast<int64_t>(bx) * rpb; base < rows; base += static_cast<int64_t>(gx) * rpb) {
     const int64_t n_el = (rows - base < rpb ? rows - base : rpb) * L.R;
     if constexpr (STAGED) {  // copy the block's rows of every staged input into its slot
       uint32_t pre_slots = 0;
@@ -352,8 +397,8 @@ __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduc
 // through shared memory in a fixed order (deterministic).
 constexpr int kColThreads = 256;
 
-template <int VEC, bool WIDE, int KIND, typename Pre, int CH = kCH>
-__global__ void __launch_bounds__(kColThreads, 4) k_col(const __grid_constant__ disc_reduce_launch L) {
+template <int VEC, bool WIDE, int KIND, typename Pre, int CH>
+__device__ __forceinline__ void col_body(const disc_reduce_launch& L, const int bx, const int by) {
   using T = typename Vec<VEC>::T;
   using RD = Red<KIND>;
   using Acc = typename RD::Acc;
@@ -373,11 +418,11 @@ __global__ void __launch_bounds__(kColThreads, 4) k_col(const __grid_constant__ 
   const int rows_per_pass = (kColThreads / 32) * rpw;
   const int64_t span = static_cast<int64_t>(lpc) * VEC;
   const int64_t tiles = (L.C + span - 1) / span;
-  const int64_t k = blockIdx.x / tiles;
-  const int64_t tile0 = (blockIdx.x - k * tiles) * span;
+  const int64_t k = bx / tiles;
+  const int64_t tile0 = (bx - k * tiles) * span;
   const int64_t col0 = tile0 + lc * VEC;
   const int64_t per = (L.R + L.splits - 1) / L.splits;
-  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * per;
+  const int64_t r0 = static_cast<int64_t>(by) * per;
   const int64_t r1 = r0 + per < L.R ? r0 + per : L.R;
 
   Acc acc[VEC];
@@ -435,13 +480,55 @@ __global__ void __launch_bounds__(kColThreads, 4) k_col(const __grid_constant__ 
         if (L.red_out) L.red_out[o] = static_cast<float>(s);
         break;
       case DISC_SCHED_COL_TWOPASS:
-        L.workspace[static_cast<int64_t>(blockIdx.y) * L.K * L.C + o] = static_cast<double>(s);
+        L.workspace[static_cast<int64_t>(by) * L.K * L.C + o] = static_cast<double>(s);
         break;
       default:  // DISC_SCHED_COL_ATOMIC (sum only)
         atomicAdd(L.workspace + o, static_cast<double>(s));
         break;
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Kernels: single launch (descriptor in parameter space) and grouped launch.
+template <int VEC, bool WIDE, typename Prog, int CH = kCH>
+__global__ void __launch_bounds__(kLoopThreads, 4) k_loop(const __grid_constant__ disc_loop_launch L) {
+  loop_body<VEC, WIDE, Prog, CH>(L, blockIdx.x, gridDim.x);
+}
+template <int VEC, bool WIDE, typename Prog, int CH = kCH>
+__global__ void __launch_bounds__(kLoopThreads, 4) k_loop_g(const __grid_constant__ disc_group G) {
+  __shared__ __align__(16) unsigned char desc[desc_bytes<disc_loop_launch>()];
+  const int b = blockIdx.x, g = group_of(G, b);
+  const disc_loop_launch& L = group_stage<disc_loop_launch>(G, g, desc);
+  loop_body<VEC, WIDE, Prog, CH>(L, b - G.block_off[g], G.block_off[g + 1] - G.block_off[g]);
+}
+
+template <int VEC, bool WIDE, int KIND, typename Pre, typename Post, int CH = kCH, bool STAGED = false>
+__global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduce_launch L) {
+  row_body<VEC, WIDE, KIND, Pre, Post, CH, STAGED>(L, blockIdx.x, gridDim.x);
+}
+template <int VEC, bool WIDE, int KIND, typename Pre, typename Post, int CH = kCH, bool STAGED = false>
+__global__ void __launch_bounds__(1024) k_row_g(const __grid_constant__ disc_group G) {
+  __shared__ __align__(16) unsigned char desc[desc_bytes<disc_reduce_launch>()];
+  const int b = blockIdx.x, g = group_of(G, b);
+  const disc_reduce_launch& L = group_stage<disc_reduce_launch>(G, g, desc);
+  row_body<VEC, WIDE, KIND, Pre, Post, CH, STAGED>(L, b - G.block_off[g], G.block_off[g + 1] - G.block_off[g]);
+}
+
+template <int VEC, bool WIDE, int KIND, typename Pre, int CH = kCH>
+__global__ void __launch_bounds__(kColThreads, 4) k_col(const __grid_constant__ disc_reduce_launch L) {
+  col_body<VEC, WIDE, KIND, Pre, CH>(L, blockIdx.x, blockIdx.y);
+}
+// Grouped column pass: launch g's 2-D grid (K * col tiles, splits) is flattened x-major.
+template <int VEC, bool WIDE, int KIND, typename Pre, int CH = kCH>
+__global__ void __launch_bounds__(kColThreads, 4) k_col_g(const __grid_constant__ disc_group G) {
+  __shared__ __align__(16) unsigned char desc[desc_bytes<disc_reduce_launch>()];
+  const int b = blockIdx.x, g = group_of(G, b);
+  const disc_reduce_launch& L = group_stage<disc_reduce_launch>(G, g, desc);
+  const int local = b - G.block_off[g];
+  const int64_t span = static_cast<int64_t>(L.group) * L.vec;
+  const int gx = static_cast<int>(L.K * ((L.C + span - 1) / span));
+  col_body<VEC, WIDE, KIND, Pre, CH>(L, local % gx, local / gx);
 }
 
 // ---------------------------------------------------------------------------
@@ -456,10 +543,24 @@ inline int sm_count() {
 }
 
 template <typename K>
-inline cudaError_t set_smem(K kernel, size_t bytes) {
-  if (bytes <= 40 * 1024) return cudaSuccess;
+inline cudaError_t set_smem(K kernel, size_t bytes, size_t threshold = 40 * 1024) {
+  if (bytes <= threshold) return cudaSuccess;
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
 }
+
+// Host side of a grouped launch: the uploaded device table and the host copy of the same
+// descriptors (for per-launch grid and shared-memory sizing).
+struct HostGroup {
+  const unsigned char* dev_table;
+  const unsigned char* host_table;
+  int stride;
+  int n;
+  template <typename T>
+  const T& at(int i) const { return *reinterpret_cast<const T*>(host_table + static_cast<size_t>(i) * stride); }
+};
+// Grouped kernels hold a descriptor in static shared memory: opt in to more dynamic
+// shared memory earlier than single launches do.
+constexpr size_t kGroupSmemThreshold = 24 * 1024;
 
 // Resident CTAs per SM for (kernel, block, dynamic smem); grid-stride kernels are sized
 // to exactly one wave (SM count x this).  Cached per host thread.
@@ -483,16 +584,26 @@ inline cudaError_t launch_k(void (*kernel)(Arg), dim3 grid, dim3 block, size_t s
   return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
-// use_slots = false for generated programs (values live in registers, no slot smem).
-template <int CH = kCH, typename K>
-inline cudaError_t launch_loop_with(K kernel, const disc_loop_launch& L, cudaStream_t s, bool use_slots = true) {
-  if (L.total <= 0) return cudaSuccess;
+template <int CH>
+inline int64_t loop_blocks_wanted(const disc_loop_launch& L) {
+  if (L.total <= 0) return 0;
   const int64_t span = static_cast<int64_t>(L.lpr) * CH * L.vec;
   const int64_t rpw = 32 / L.lpr;
   const int64_t tiles = ((L.rows + rpw - 1) / rpw) * ((L.W + span - 1) / span);
   const int64_t warps_per_block = kLoopThreads / 32;
-  const int64_t want = (tiles + warps_per_block - 1) / warps_per_block;
-  const size_t smem = use_slots ? static_cast<size_t>(L.prog.n_slots) * CH * kLoopThreads * (L.vec == 4 ? 16 : 4) : 0;
+  return (tiles + warps_per_block - 1) / warps_per_block;
+}
+template <int CH>
+inline size_t loop_smem(const disc_loop_launch& L, bool use_slots) {
+  return use_slots ? static_cast<size_t>(L.prog.n_slots) * CH * kLoopThreads * (L.vec == 4 ? 16 : 4) : 0;
+}
+
+// use_slots = false for generated programs (values live in registers, no slot smem).
+template <int CH = kCH, typename K>
+inline cudaError_t launch_loop_with(K kernel, const disc_loop_launch& L, cudaStream_t s, bool use_slots = true) {
+  if (L.total <= 0) return cudaSuccess;
+  const int64_t want = loop_blocks_wanted<CH>(L);
+  const size_t smem = loop_smem<CH>(L, use_slots);
   cudaError_t e = set_smem(kernel, smem);
   if (e != cudaSuccess) return e;
   const int64_t cap = static_cast<int64_t>(sm_count()) * resident_ctas(reinterpret_cast<const void*>(kernel), kLoopThreads, smem);
@@ -501,15 +612,23 @@ inline cudaError_t launch_loop_with(K kernel, const disc_loop_launch& L, cudaStr
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+inline int row_block(const disc_reduce_launch& L) { return L.group > 256 ? L.group : 256; }
+template <int CH>
+inline size_t row_smem(const disc_reduce_launch& L, bool use_slots) {
+  const int slots = L.pre.n_slots > L.post.n_slots ? L.pre.n_slots : L.post.n_slots;
+  const int block = row_block(L);
+  const int rpb = block / L.group;
+  const size_t cache = static_cast<size_t>((static_cast<int64_t>(rpb) * L.R + 3) / 4 * 4) * L.cache_loads * 4;
+  return cache + (use_slots ? static_cast<size_t>(slots) * CH * block * (L.vec == 4 ? 16 : 4) : 0);
+}
+
 template <int CH = kCH, typename K>
 inline cudaError_t launch_row_with(K kernel, const disc_reduce_launch& L, cudaStream_t s, bool use_slots = true) {
   if (L.K <= 0) return cudaSuccess;
-  const int slots = L.pre.n_slots > L.post.n_slots ? L.pre.n_slots : L.post.n_slots;
-  const int block = L.group > 256 ? L.group : 256;
+  const int block = row_block(L);
   const int rpb = block / L.group;
   const int64_t groups = (L.K + rpb - 1) / rpb;
-  const size_t cache = static_cast<size_t>((static_cast<int64_t>(rpb) * L.R + 3) / 4 * 4) * L.cache_loads * 4;
-  const size_t smem = cache + (use_slots ? static_cast<size_t>(slots) * CH * block * (L.vec == 4 ? 16 : 4) : 0);
+  const size_t smem = row_smem<CH>(L, use_slots);
   cudaError_t e = set_smem(kernel, smem);
   if (e != cudaSuccess) return e;
   const int64_t cap = static_cast<int64_t>(sm_count()) * resident_ctas(reinterpret_cast<const void*>(kernel), block, smem);
@@ -531,15 +650,104 @@ inline cudaError_t launch_col_with(K kernel, const disc_reduce_launch& L, cudaSt
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// Grouped launches (see disc_group).  Every launch keeps its single-launch grid; the
+// group's CTAs are concatenated in table order.
+template <int CH = kCH, typename K>
+inline cudaError_t launch_loop_group(K kernel, const HostGroup& H, cudaStream_t s, bool use_slots) {
+  disc_group G;
+  G.table = H.dev_table;
+  G.stride = H.stride;
+  G.n = H.n;
+  size_t smem = 0;
+  for (int i = 0; i < H.n; ++i) smem = std::max(smem, loop_smem<CH>(H.at<disc_loop_launch>(i), use_slots));
+  cudaError_t e = set_smem(kernel, smem, kGroupSmemThreshold);
+  if (e != cudaSuccess) return e;
+  const int64_t cap = static_cast<int64_t>(sm_count()) * resident_ctas(reinterpret_cast<const void*>(kernel), kLoopThreads, smem);
+  int64_t off = 0;
+  for (int i = 0; i < H.n; ++i) {
+    G.block_off[i] = static_cast<int32_t>(off);
+    off += std::min(loop_blocks_wanted<CH>(H.at<disc_loop_launch>(i)), cap);
+  }
+  G.block_off[H.n] = static_cast<int32_t>(off);
+  if (off == 0) return cudaSuccess;
+  e = launch_k(kernel, dim3(static_cast<unsigned>(off)), dim3(kLoopThreads), smem, s, G);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+template <int CH = kCH, typename K>
+inline cudaError_t launch_row_group(K kernel, const HostGroup& H, cudaStream_t s, bool use_slots) {
+  disc_group G;
+  G.table = H.dev_table;
+  G.stride = H.stride;
+  G.n = H.n;
+  size_t smem = 0;
+  for (int i = 0; i < H.n; ++i) smem = std::max(smem, row_smem<CH>(H.at<disc_reduce_launch>(i), use_slots));
+  const int block = row_block(H.at<disc_reduce_launch>(0));
+  cudaError_t e = set_smem(kernel, smem, kGroupSmemThreshold);
+  if (e != cudaSuccess) return e;
+  const int64_t cap = static_cast<int64_t>(sm_count()) * resident_ctas(reinterpret_cast<const void*>(kernel), block, smem);
+  int64_t off = 0;
+  for (int i = 0; i < H.n; ++i) {
+    const disc_reduce_launch& L = H.at<disc_reduce_launch>(i);
+    G.block_off[i] = static_cast<int32_t>(off);
+    if (L.K > 0) off += std::min((L.K + block / L.group - 1) / (block / L.group), cap);
+  }
+  G.block_off[H.n] = static_cast<int32_t>(off);
+  if (off == 0) return cudaSuccess;
+  e = launch_k(kernel, dim3(static_cast<unsigned>(off)), dim3(block), smem, s, G);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+template <int CH = kCH, typename K>
+inline cudaError_t launch_col_group(K kernel, const HostGroup& H, cudaStream_t s, bool use_slots) {
+  disc_group G;
+  G.table = H.dev_table;
+  G.stride = H.stride;
+  G.n = H.n;
+  size_t smem = 0;
+  int64_t off = 0;
+  for (int i = 0; i < H.n; ++i) {
+    const disc_reduce_launch& L = H.at<disc_reduce_launch>(i);
+    smem = std::max(smem, use_slots ? static_cast<size_t>(L.pre.n_slots) * CH * kColThreads * (L.vec == 4 ? 16 : 4) : 0);
+    G.block_off[i] = static_cast<int32_t>(off);
+    const int64_t span = static_cast<int64_t>(L.group) * L.vec;
+    if (L.K * L.C > 0) off += L.K * ((L.C + span - 1) / span) * L.splits;
+  }
+  G.block_off[H.n] = static_cast<int32_t>(off);
+  if (off == 0) return cudaSuccess;
+  cudaError_t e = set_smem(kernel, smem, kGroupSmemThreshold);
+  if (e != cudaSuccess) return e;
+  e = launch_k(kernel, dim3(static_cast<unsigned>(off)), dim3(kColThreads), smem, s, G);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+template <typename Prog, int CH = kCH, bool ALLOW_WIDE = true>
+inline cudaError_t loop_pass(const disc_loop_launch& L, cudaStream_t s, bool use_slots, const HostGroup* g) {
+  if (g) {
+    if constexpr (ALLOW_WIDE)
+      if (L.wide) return L.vec == 4 ? launch_loop_group<CH>(k_loop_g<4, true, Prog, CH>, *g, s, use_slots)
+                                    : launch_loop_group<CH>(k_loop_g<1, true, Prog, CH>, *g, s, use_slots);
+    return L.vec == 4 ? launch_loop_group<CH>(k_loop_g<4, false, Prog, CH>, *g, s, use_slots)
+                      : launch_loop_group<CH>(k_loop_g<1, false, Prog, CH>, *g, s, use_slots);
+  }
+  if constexpr (ALLOW_WIDE)
+    if (L.wide) return L.vec == 4 ? launch_loop_with<CH>(k_loop<4, true, Prog, CH>, L, s, use_slots)
+                                  : launch_loop_with<CH>(k_loop<1, true, Prog, CH>, L, s, use_slots);
+  return L.vec == 4 ? launch_loop_with<CH>(k_loop<4, false, Prog, CH>, L, s, use_slots)
+                    : launch_loop_with<CH>(k_loop<1, false, Prog, CH>, L, s, use_slots);
+}
+
 // Dispatch on (vec, wide, reduce kind) for a given program functor pair.
 // ALLOW_WIDE = false (generated programs, used only on !wide launches) instantiates no
 // 64-bit-index kernels.
 template <typename Pre, typename Post, int CH = kCH, bool ALLOW_WIDE = true>
-inline cudaError_t row_pass(const disc_reduce_launch& L, cudaStream_t s, bool use_slots) {
+inline cudaError_t row_pass(const disc_reduce_launch& L, cudaStream_t s, bool use_slots, const HostGroup* g = nullptr) {
   const bool sum = L.kind == DISC_REDUCE_SUM;
 #define DISC_ROW(V, W, ST)                                                                                   \
-  (sum ? launch_row_with<CH>(k_row<V, W, DISC_REDUCE_SUM, Pre, Post, CH, ST>, L, s, use_slots)              \
-       : launch_row_with<CH>(k_row<V, W, DISC_REDUCE_MAX, Pre, Post, CH, ST>, L, s, use_slots))
+  (g ? (sum ? launch_row_group<CH>(k_row_g<V, W, DISC_REDUCE_SUM, Pre, Post, CH, ST>, *g, s, use_slots)      \
+            : launch_row_group<CH>(k_row_g<V, W, DISC_REDUCE_MAX, Pre, Post, CH, ST>, *g, s, use_slots))     \
+     : (sum ? launch_row_with<CH>(k_row<V, W, DISC_REDUCE_SUM, Pre, Post, CH, ST>, L, s, use_slots)          \
+            : launch_row_with<CH>(k_row<V, W, DISC_REDUCE_MAX, Pre, Post, CH, ST>, L, s, use_slots)))
   if constexpr (ALLOW_WIDE)
     if (L.wide) return L.vec == 4 ? DISC_ROW(4, true, false) : DISC_ROW(1, true, false);
   if (L.stage) return L.vec == 4 ? DISC_ROW(4, false, true) : DISC_ROW(1, false, true);
@@ -548,8 +756,16 @@ inline cudaError_t row_pass(const disc_reduce_launch& L, cudaStream_t s, bool us
 }
 
 template <typename Pre, int CH = kCH, bool ALLOW_WIDE = true>
-inline cudaError_t col_pass_t(const disc_reduce_launch& L, cudaStream_t s, bool use_slots) {
+inline cudaError_t col_pass_t(const disc_reduce_launch& L, cudaStream_t s, bool use_slots, const HostGroup* g = nullptr) {
   const bool sum = L.kind == DISC_REDUCE_SUM;
+  if (g) {
+#define DISC_COLG(V, W) (sum ? launch_col_group<CH>(k_col_g<V, W, DISC_REDUCE_SUM, Pre, CH>, *g, s, use_slots) \
+                             : launch_col_group<CH>(k_col_g<V, W, DISC_REDUCE_MAX, Pre, CH>, *g, s, use_slots))
+    if constexpr (ALLOW_WIDE)
+      if (L.wide) return L.vec == 4 ? DISC_COLG(4, true) : DISC_COLG(1, true);
+    return L.vec == 4 ? DISC_COLG(4, false) : DISC_COLG(1, false);
+#undef DISC_COLG
+  }
   if constexpr (ALLOW_WIDE) if (L.wide) {
     if (L.vec == 4) return sum ? launch_col_with<CH>(k_col<4, true, DISC_REDUCE_SUM, Pre, CH>, L, s, use_slots)
                                : launch_col_with<CH>(k_col<4, true, DISC_REDUCE_MAX, Pre, CH>, L, s, use_slots);

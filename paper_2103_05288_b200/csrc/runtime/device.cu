@@ -1,20 +1,28 @@
 // C ABI of the device layer (include/disc_cuda.h): streams, stream-ordered memory,
 // events and the kernel launches the runtime flow issues.
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
+#include <unordered_map>
 #include <vector>
 
 #include "disc_cuda.h"
-#include "../kernels/program.cuh"
+#include "../kernels/kernels.cuh"
+
+using disc_dev::HostGroup;
 
 namespace disc_launch {
-cudaError_t loop(const disc_loop_launch& L, cudaStream_t s);
-cudaError_t reduce(const disc_reduce_launch& L, cudaStream_t s);
-cudaError_t col_pass(const disc_reduce_launch& L, cudaStream_t s);
-cudaError_t finalize_columns(const disc_reduce_launch& L, cudaStream_t s);
+cudaError_t loop(const disc_loop_launch& L, cudaStream_t s, const HostGroup* g = nullptr);
+cudaError_t reduce(const disc_reduce_launch& L, cudaStream_t s, const HostGroup* g = nullptr);
+cudaError_t col_pass(const disc_reduce_launch& L, cudaStream_t s, const HostGroup* g = nullptr);
+cudaError_t finalize_columns(const disc_reduce_launch& L, cudaStream_t s, const HostGroup* g = nullptr);
 cudaError_t pad(const disc_pad_launch& P, cudaStream_t s);
 cudaError_t concat(const disc_concat_launch& C, cudaStream_t s);
 cudaError_t gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c, cudaStream_t s);
@@ -31,7 +39,7 @@ namespace disc_spec {
 struct Entry {
   int kind;        // 0 loop, 1 row (pre+post), 2 column pass (pre)
   uint64_t key;
-  cudaError_t (*launch)(const void* launch, int vec, cudaStream_t s);
+  cudaError_t (*launch)(const void* launch, int vec, cudaStream_t s, const HostGroup* g);
 };
 const Entry* lookup(int kind, uint64_t key);
 int count();
@@ -115,6 +123,250 @@ int counted(cudaError_t e, const char* what, int n = 1) {
   if (e == cudaSuccess) g_launches.fetch_add(n, std::memory_order_relaxed);
   return check(e, what);
 }
+
+// ---------------------------------------------------------------------------
+// Descriptor upload for grouped launches: a pinned host ring mirrored by a device ring
+// per stream.  A region stays reserved until the event recorded after the kernel that
+// reads it; reuse waits for that event (in practice the ring is large enough that the
+// host never waits).
+struct Ring {
+  unsigned char* host = nullptr;
+  unsigned char* dev = nullptr;
+  size_t cap = 0, head = 0;
+  std::deque<std::tuple<size_t, size_t, cudaEvent_t>> inflight;  // [begin, end) until event
+  std::vector<cudaEvent_t> spare;
+};
+std::mutex g_ring_mu;
+std::unordered_map<cudaStream_t, Ring> g_rings;
+
+cudaError_t ring_reserve(Ring& r, size_t n, cudaStream_t st, size_t* off) {
+  n = (n + 255) / 256 * 256;
+  if (n > r.cap) {  // grow: drain everything in flight, then reallocate
+    for (auto& f : r.inflight) {
+      cudaEventSynchronize(std::get<2>(f));
+      r.spare.push_back(std::get<2>(f));
+    }
+    r.inflight.clear();
+    if (r.host) cudaFreeHost(r.host);
+    if (r.dev) cudaFree(r.dev);
+    r.host = r.dev = nullptr;
+    r.cap = std::max<size_t>({n, 2 * r.cap, size_t{16} << 20});
+    r.head = 0;
+    if (cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&r.host), r.cap)) return e;
+    if (cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&r.dev), r.cap)) return e;
+  }
+  if (r.head + n > r.cap) r.head = 0;
+  const size_t b = r.head, e = r.head + n;
+  auto overlaps = [&] {
+    for (auto& f : r.inflight)
+      if (std::get<0>(f) < e && b < std::get<1>(f)) return true;
+    return false;
+  };
+  while (!r.inflight.empty() && overlaps()) {
+    cudaEventSynchronize(std::get<2>(r.inflight.front()));
+    r.spare.push_back(std::get<2>(r.inflight.front()));
+    r.inflight.pop_front();
+  }
+  r.head = e;
+  *off = b;
+  (void)st;
+  return cudaSuccess;
+}
+
+cudaError_t ring_release(Ring& r, size_t off, size_t n, cudaStream_t st) {
+  cudaEvent_t ev;
+  if (r.spare.empty()) {
+    if (cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) return e;
+  } else {
+    ev = r.spare.back();
+    r.spare.pop_back();
+  }
+  r.inflight.emplace_back(off, off + (n + 255) / 256 * 256, ev);
+  return cudaEventRecord(ev, st);
+}
+
+// Kernel instantiation key of a fused launch (members of one grouped launch share it).
+struct GroupKey {
+  int kind = 0;  // 0 loop, 1 row, 2 column pass
+  const disc_spec::Entry* entry = nullptr;
+  int vec = 0, wide = 0, red = 0, stage = 0, block = 0;
+  bool operator<(const GroupKey& o) const {
+    return std::tie(kind, entry, vec, wide, red, stage, block) <
+           std::tie(o.kind, o.entry, o.vec, o.wide, o.red, o.stage, o.block);
+  }
+};
+
+bool is_col(int sched) {
+  return sched == DISC_SCHED_COL_SINGLE || sched == DISC_SCHED_COL_TWOPASS || sched == DISC_SCHED_COL_ATOMIC;
+}
+
+// Grouping key, or false if the launch is issued alone (generic reduce).
+bool group_key(int kind, const void* l, GroupKey* k) {
+  if (kind == 0) {
+    const auto& L = *static_cast<const disc_loop_launch*>(l);
+    k->kind = 0;
+    k->vec = L.vec;
+    k->wide = L.wide;
+    k->entry = (g_spec_enabled && !L.wide) ? disc_spec::lookup(0, launch_key(0, L.prog, nullptr)) : nullptr;
+    return true;
+  }
+  const auto& R = *static_cast<const disc_reduce_launch*>(l);
+  const bool row = R.schedule == DISC_SCHED_ROW;
+  if (!row && !is_col(R.schedule)) return false;
+  k->kind = row ? 1 : 2;
+  k->vec = R.vec;
+  k->wide = R.wide;
+  k->red = R.kind;
+  k->stage = row ? R.stage : 0;
+  k->block = row ? (R.group > 256 ? R.group : 256) : 256;
+  const uint64_t key = row ? launch_key(1, R.pre, &R.post) : launch_key(2, R.pre, nullptr);
+  k->entry = (g_spec_enabled && !R.wide) ? disc_spec::lookup(row ? 1 : 2, key) : nullptr;
+  return true;
+}
+
+int64_t launch_weight(int kind, const void* l) {
+  if (kind == 0) return static_cast<const disc_loop_launch*>(l)->total;
+  const auto& R = *static_cast<const disc_reduce_launch*>(l);
+  return R.K * R.R * (R.C > 0 ? R.C : 1);
+}
+
+// Issues one homogeneous group (<= DISC_MAX_GROUP members, same key) as grouped kernels.
+int issue_group(const GroupKey& k, const std::vector<const void*>& members, cudaStream_t st) {
+  const size_t stride = k.kind == 0 ? disc_dev::desc_bytes<disc_loop_launch>() : disc_dev::desc_bytes<disc_reduce_launch>();
+  const size_t size = k.kind == 0 ? sizeof(disc_loop_launch) : sizeof(disc_reduce_launch);
+  const int n = static_cast<int>(members.size());
+  std::lock_guard<std::mutex> lock(g_ring_mu);
+  Ring& r = g_rings[st];
+  size_t off = 0;
+  if (int rc = check(ring_reserve(r, stride * n, st, &off), "group table")) return rc;
+  for (int i = 0; i < n; ++i) std::memcpy(r.host + off + i * stride, members[i], size);
+  if (int rc = check(cudaMemcpyAsync(r.dev + off, r.host + off, stride * n, cudaMemcpyHostToDevice, st), "group table upload"))
+    return rc;
+  const HostGroup H{r.dev + off, r.host + off, static_cast<int>(stride), n};
+  const void* first = members[0];
+  int rc = 0;
+  if (k.kind == 0) {
+    const auto& L = *static_cast<const disc_loop_launch*>(first);
+    rc = counted(k.entry ? k.entry->launch(first, L.vec, st, &H) : disc_launch::loop(L, st, &H), "grouped loop");
+  } else if (k.kind == 1) {
+    const auto& R = *static_cast<const disc_reduce_launch*>(first);
+    rc = counted(k.entry ? k.entry->launch(first, R.vec, st, &H) : disc_launch::reduce(R, st, &H), "grouped row reduce");
+  } else {
+    bool finalize = false;
+    for (const void* m : members) {
+      const auto& R = *static_cast<const disc_reduce_launch*>(m);
+      if (R.K * R.C <= 0) continue;
+      if (R.schedule == DISC_SCHED_COL_ATOMIC)
+        if ((rc = check(cudaMemsetAsync(R.workspace, 0, sizeof(double) * R.K * R.C, st), "workspace memset"))) return rc;
+      finalize = finalize || R.schedule != DISC_SCHED_COL_SINGLE;
+    }
+    const auto& R = *static_cast<const disc_reduce_launch*>(first);
+    rc = counted(k.entry ? k.entry->launch(first, R.vec, st, &H) : disc_launch::col_pass(R, st, &H), "grouped column pass");
+    if (!rc && finalize) rc = counted(disc_launch::finalize_columns(R, st, &H), "grouped column finalize");
+  }
+  if (rc) return rc;
+  g_spec_launches.fetch_add(k.entry ? n : 0, std::memory_order_relaxed);
+  return check(ring_release(r, off, stride * n, st), "group table release");
+}
+
+// Splits n launches of one kind into homogeneous groups and issues each (largest first).
+int issue_grouped(int kind, const void* const* ls, int n, cudaStream_t st, int* issued = nullptr) {
+  std::map<GroupKey, std::vector<const void*>> groups;
+  std::vector<GroupKey> order;
+  for (int i = 0; i < n; ++i) {
+    GroupKey k;
+    if (!group_key(kind, ls[i], &k)) {  // issued alone
+      if (int rc = kind == 0 ? disc_cuda_launch_loop(static_cast<const disc_loop_launch*>(ls[i]), st)
+                             : disc_cuda_launch_reduce(static_cast<const disc_reduce_launch*>(ls[i]), st))
+        return rc;
+      continue;
+    }
+    auto it = groups.find(k);
+    if (it == groups.end()) {
+      order.push_back(k);
+      it = groups.emplace(k, std::vector<const void*>()).first;
+    }
+    it->second.push_back(ls[i]);
+  }
+  for (const GroupKey& k : order) {
+    auto& m = groups[k];
+    std::stable_sort(m.begin(), m.end(),
+                     [&](const void* a, const void* b) { return launch_weight(kind, a) > launch_weight(kind, b); });
+    for (size_t i = 0; i < m.size(); i += DISC_MAX_GROUP) {
+      std::vector<const void*> chunk(m.begin() + i, m.begin() + std::min(m.size(), i + DISC_MAX_GROUP));
+      if (int rc = issue_group(k, chunk, st)) return rc;
+      if (issued) ++*issued;
+    }
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Per-thread request queue (disc_cuda_queue_*).
+enum QKind { kQLoop = 0, kQReduce, kQPad, kQConcat, kQGemm, kQMemcpy, kQMemset };
+struct QMemcpy {
+  void* dst;
+  const void* src;
+  size_t bytes;
+  int kind;
+};
+struct QMemset {
+  void* dst;
+  int value;
+  size_t bytes;
+};
+struct QGemm {
+  int64_t m, k, n;
+  const float *a, *b;
+  float* c;
+};
+struct QOp {
+  int kind;
+  size_t off;  // payload offset in the arena
+  int64_t bytes = 0;
+  int kernel = -1;
+  int sched = -1;  // index into Queue::names
+};
+struct QRecord {
+  int level, members, kernel, sched;
+  int64_t bytes;
+  cudaEvent_t a = nullptr, b = nullptr;
+  float ms = 0.f;
+};
+struct Queue {
+  bool active = false;
+  cudaStream_t stream = nullptr;
+  std::vector<unsigned char> arena;
+  std::vector<std::vector<QOp>> reqs;
+  size_t mark_from = 0;
+  std::vector<void*> frees;
+  std::vector<std::string> names;
+  std::vector<QRecord> records;
+  std::vector<cudaEvent_t> events;  // pool for timing
+  size_t next_event = 0;
+};
+thread_local Queue t_q;
+
+bool queued(void* stream) { return t_q.active && S(stream) == t_q.stream; }
+
+template <typename T>
+void enqueue(int kind, const T& payload) {
+  if (t_q.reqs.empty()) t_q.reqs.emplace_back();
+  const size_t off = (t_q.arena.size() + 15) / 16 * 16;
+  t_q.arena.resize(off + sizeof(T));
+  std::memcpy(t_q.arena.data() + off, &payload, sizeof(T));
+  t_q.reqs.back().push_back({kind, off});
+}
+
+cudaEvent_t queue_event() {
+  if (t_q.next_event == t_q.events.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    t_q.events.push_back(e);
+  }
+  return t_q.events[t_q.next_event++];
+}
+
 }  // namespace
 
 extern "C" {
@@ -171,6 +423,10 @@ int disc_cuda_malloc(size_t bytes, void* stream, void** dptr) {
 }
 int disc_cuda_free(void* dptr, void* stream) {
   if (g_capture) return 0;
+  if (queued(stream)) {  // queued work may still read it: free after the flush
+    t_q.frees.push_back(dptr);
+    return 0;
+  }
   return check(cudaFreeAsync(dptr, S(stream)), "cudaFreeAsync");
 }
 int disc_cuda_host_alloc(size_t bytes, void** hptr) { return check(cudaMallocHost(hptr, bytes ? bytes : 16), "cudaMallocHost"); }
@@ -178,12 +434,20 @@ int disc_cuda_host_free(void* hptr) { return check(cudaFreeHost(hptr), "cudaFree
 
 int disc_cuda_memcpy(void* dst, const void* src, size_t bytes, int kind, void* stream) {
   if (!bytes || g_capture) return 0;
+  if (queued(stream)) {
+    enqueue(kQMemcpy, QMemcpy{dst, src, bytes, kind});
+    return 0;
+  }
   static const cudaMemcpyKind kinds[] = {cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost, cudaMemcpyDeviceToDevice,
                                          cudaMemcpyDefault};
   return check(cudaMemcpyAsync(dst, src, bytes, kinds[kind & 3], S(stream)), "cudaMemcpyAsync");
 }
 int disc_cuda_memset(void* dst, int value, size_t bytes, void* stream) {
   if (g_capture) return 0;
+  if (queued(stream)) {
+    if (bytes) enqueue(kQMemset, QMemset{dst, value, bytes});
+    return 0;
+  }
   return check(cudaMemsetAsync(dst, value, bytes, S(stream)), "cudaMemsetAsync");
 }
 
@@ -217,6 +481,10 @@ int disc_cuda_event_elapsed_ms(void* a, void* b, float* ms) {
 
 int disc_cuda_launch_loop(const disc_loop_launch* l, void* stream) {
   if (l->total <= 0) return 0;
+  if (queued(stream) && !g_capture) {
+    enqueue(kQLoop, *l);
+    return 0;
+  }
   const uint64_t key = launch_key(0, l->prog, nullptr);
   if (g_capture) {
     if (g_capture_record) record("loop", key, "\"vec\":" + std::to_string(l->vec) + ",\"pre\":" + program_text(l->prog));
@@ -226,12 +494,16 @@ int disc_cuda_launch_loop(const disc_loop_launch* l, void* stream) {
   if (g_spec_enabled && !l->wide)
     if (const disc_spec::Entry* e = disc_spec::lookup(0, key)) {
       g_spec_launches.fetch_add(1, std::memory_order_relaxed);
-      return counted(e->launch(l, l->vec, S(stream)), "launch loop (generated)");
+      return counted(e->launch(l, l->vec, S(stream), nullptr), "launch loop (generated)");
     }
   return counted(disc_launch::loop(*l, S(stream)), "launch loop");
 }
 
 int disc_cuda_launch_reduce(const disc_reduce_launch* l, void* stream) {
+  if (queued(stream) && !g_capture) {
+    enqueue(kQReduce, *l);
+    return 0;
+  }
   const bool row = l->schedule == DISC_SCHED_ROW;
   const bool col = l->schedule == DISC_SCHED_COL_SINGLE || l->schedule == DISC_SCHED_COL_TWOPASS ||
                    l->schedule == DISC_SCHED_COL_ATOMIC;
@@ -249,13 +521,13 @@ int disc_cuda_launch_reduce(const disc_reduce_launch* l, void* stream) {
   }
   const disc_spec::Entry* e = (g_spec_enabled && !l->wide && (row || col)) ? disc_spec::lookup(row ? 1 : 2, key) : nullptr;
   if (e) g_spec_launches.fetch_add(1, std::memory_order_relaxed);
-  if (!col) return counted(e ? e->launch(l, l->vec, S(stream)) : disc_launch::reduce(*l, S(stream)), "launch reduce");
+  if (!col) return counted(e ? e->launch(l, l->vec, S(stream), nullptr) : disc_launch::reduce(*l, S(stream)), "launch reduce");
   if (l->K * l->C <= 0) return 0;
   if (l->schedule == DISC_SCHED_COL_ATOMIC) {
     if (int rc = check(cudaMemsetAsync(l->workspace, 0, sizeof(double) * l->K * l->C, S(stream)), "workspace memset"))
       return rc;
   }
-  if (int rc = counted(e ? e->launch(l, l->vec, S(stream)) : disc_launch::col_pass(*l, S(stream)), "launch column pass"))
+  if (int rc = counted(e ? e->launch(l, l->vec, S(stream), nullptr) : disc_launch::col_pass(*l, S(stream)), "launch column pass"))
     return rc;
   if (l->schedule == DISC_SCHED_COL_SINGLE) return 0;
   return counted(disc_launch::finalize_columns(*l, S(stream)), "launch column finalize");
@@ -264,14 +536,26 @@ int disc_cuda_launch_reduce(const disc_reduce_launch* l, void* stream) {
 int disc_cuda_launch_pad(const disc_pad_launch* l, void* stream) {
   if (g_capture) return 0;
   if (l->total <= 0) return 0;
+  if (queued(stream)) {
+    enqueue(kQPad, *l);
+    return 0;
+  }
   return counted(disc_launch::pad(*l, S(stream)), "launch pad");
 }
 int disc_cuda_launch_concat(const disc_concat_launch* l, void* stream) {
   if (g_capture) return 0;
+  if (queued(stream)) {
+    enqueue(kQConcat, *l);
+    return 0;
+  }
   return counted(disc_launch::concat(*l, S(stream)), "launch concat");
 }
 int disc_cuda_gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c, void* stream) {
   if (g_capture) return 0;
+  if (queued(stream)) {
+    enqueue(kQGemm, QGemm{m, k, n, a, b, c});
+    return 0;
+  }
   return counted(disc_launch::gemm(m, k, n, a, b, c, S(stream)), "launch gemm");
 }
 int disc_cuda_fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, void* stream) {
@@ -297,6 +581,193 @@ int disc_cuda_set_specialization(int enabled) {
 }
 int64_t disc_cuda_specialized_launches(void) { return g_spec_launches.load(); }
 int disc_cuda_num_specializations(void) { return disc_spec::count(); }
+
+int disc_cuda_launch_loop_group(const disc_loop_launch* const* launches, int n, void* stream) {
+  if (g_capture || n <= 0) return 0;
+  return issue_grouped(0, reinterpret_cast<const void* const*>(launches), n, S(stream));
+}
+int disc_cuda_launch_reduce_group(const disc_reduce_launch* const* launches, int n, void* stream) {
+  if (g_capture || n <= 0) return 0;
+  return issue_grouped(1, reinterpret_cast<const void* const*>(launches), n, S(stream));
+}
+
+int disc_cuda_queue_begin(void* stream) {
+  if (t_q.active) {
+    t_err = "disc_cuda_queue_begin: a queue is already active on this thread";
+    return 5;
+  }
+  t_q.active = true;
+  t_q.stream = S(stream);
+  t_q.arena.clear();
+  t_q.reqs.clear();
+  t_q.frees.clear();
+  t_q.mark_from = 0;
+  return 0;
+}
+int disc_cuda_queue_active(void) { return t_q.active ? 1 : 0; }
+int disc_cuda_queue_request(void) {
+  if (!t_q.active) return 0;
+  if (t_q.reqs.empty() || !t_q.reqs.back().empty()) t_q.reqs.emplace_back();
+  t_q.mark_from = 0;
+  return 0;
+}
+int disc_cuda_queue_mark(int64_t bytes, int kernel, const char* schedule) {
+  if (!t_q.active || t_q.reqs.empty()) return 0;
+  auto& ops = t_q.reqs.back();
+  if (t_q.mark_from < ops.size()) {
+    int name = -1;
+    const std::string sched = schedule ? schedule : "";
+    for (size_t i = 0; i < t_q.names.size(); ++i)
+      if (t_q.names[i] == sched) name = static_cast<int>(i);
+    if (name < 0) {
+      t_q.names.push_back(sched);
+      name = static_cast<int>(t_q.names.size()) - 1;
+    }
+    ops[t_q.mark_from].bytes = bytes;
+    for (size_t i = t_q.mark_from; i < ops.size(); ++i) {
+      ops[i].kernel = kernel;
+      ops[i].sched = name;
+    }
+  }
+  t_q.mark_from = ops.size();
+  return 0;
+}
+
+int disc_cuda_queue_flush(int timing) {
+  if (!t_q.active) return 0;
+  t_q.active = false;  // everything below issues for real
+  const cudaStream_t st = t_q.stream;
+  t_q.records.clear();
+  t_q.next_event = 0;
+  size_t levels = 0;
+  for (const auto& r : t_q.reqs) levels = std::max(levels, r.size());
+  const unsigned char* A = t_q.arena.data();
+  auto begin_rec = [&](int level, int members, int64_t bytes, int kernel, int sched) {
+    QRecord rec{level, members, kernel, sched, bytes};
+    if (timing) {
+      rec.a = queue_event();
+      rec.b = queue_event();
+      cudaEventRecord(rec.a, st);
+    }
+    t_q.records.push_back(rec);
+  };
+  auto end_rec = [&] {
+    if (timing) cudaEventRecord(t_q.records.back().b, st);
+  };
+  int rc = 0;
+  for (size_t lv = 0; lv < levels && !rc; ++lv) {
+    // fused launches of this level, by kind; everything else issued in request order
+    std::vector<const QOp*> fused[2];
+    for (const auto& r : t_q.reqs) {
+      if (lv >= r.size()) continue;
+      const QOp& op = r[lv];
+      const void* p = A + op.off;
+      if (op.kind == kQLoop || op.kind == kQReduce) {
+        fused[op.kind == kQLoop ? 0 : 1].push_back(&op);
+        continue;
+      }
+      begin_rec(static_cast<int>(lv), 1, op.bytes, op.kernel, op.sched);
+      switch (op.kind) {
+        case kQPad: rc = counted(disc_launch::pad(*static_cast<const disc_pad_launch*>(p), st), "launch pad"); break;
+        case kQConcat:
+          rc = counted(disc_launch::concat(*static_cast<const disc_concat_launch*>(p), st), "launch concat");
+          break;
+        case kQGemm: {
+          const auto& g = *static_cast<const QGemm*>(p);
+          rc = counted(disc_launch::gemm(g.m, g.k, g.n, g.a, g.b, g.c, st), "launch gemm");
+          break;
+        }
+        case kQMemcpy: {
+          static const cudaMemcpyKind kinds[] = {cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost,
+                                                 cudaMemcpyDeviceToDevice, cudaMemcpyDefault};
+          const auto& c = *static_cast<const QMemcpy*>(p);
+          rc = check(cudaMemcpyAsync(c.dst, c.src, c.bytes, kinds[c.kind & 3], st), "cudaMemcpyAsync");
+          break;
+        }
+        case kQMemset: {
+          const auto& m = *static_cast<const QMemset*>(p);
+          rc = check(cudaMemsetAsync(m.dst, m.value, m.bytes, st), "cudaMemsetAsync");
+          break;
+        }
+      }
+      end_rec();
+      if (rc) break;
+    }
+    for (int kind = 0; kind < 2 && !rc; ++kind) {
+      if (fused[kind].empty()) continue;
+      // group by kernel instantiation; one record per grouped launch
+      std::map<GroupKey, std::vector<const QOp*>> groups;
+      std::vector<GroupKey> order;
+      for (const QOp* op : fused[kind]) {
+        const void* p = A + op->off;
+        GroupKey k;
+        if (!group_key(kind, p, &k)) {
+          begin_rec(static_cast<int>(lv), 1, op->bytes, op->kernel, op->sched);
+          rc = kind == 0 ? disc_cuda_launch_loop(static_cast<const disc_loop_launch*>(p), st)
+                         : disc_cuda_launch_reduce(static_cast<const disc_reduce_launch*>(p), st);
+          end_rec();
+          if (rc) break;
+          continue;
+        }
+        auto it = groups.find(k);
+        if (it == groups.end()) {
+          order.push_back(k);
+          it = groups.emplace(k, std::vector<const QOp*>()).first;
+        }
+        it->second.push_back(op);
+      }
+      for (const GroupKey& k : order) {
+        if (rc) break;
+        auto& m = groups[k];
+        std::stable_sort(m.begin(), m.end(), [&](const QOp* a, const QOp* b) {
+          return launch_weight(kind, A + a->off) > launch_weight(kind, A + b->off);
+        });
+        for (size_t i = 0; i < m.size() && !rc; i += DISC_MAX_GROUP) {
+          const size_t e = std::min(m.size(), i + DISC_MAX_GROUP);
+          std::vector<const void*> chunk;
+          int64_t bytes = 0;
+          int kernel = m[i]->kernel, sched = m[i]->sched;
+          for (size_t j = i; j < e; ++j) {
+            chunk.push_back(A + m[j]->off);
+            bytes += m[j]->bytes;
+            if (m[j]->kernel != kernel) kernel = -1;
+            if (m[j]->sched != sched) sched = -1;
+          }
+          begin_rec(static_cast<int>(lv), static_cast<int>(chunk.size()), bytes, kernel, sched);
+          rc = issue_group(k, chunk, st);
+          end_rec();
+        }
+      }
+    }
+  }
+  for (void* p : t_q.frees)
+    if (!rc) rc = check(cudaFreeAsync(p, st), "cudaFreeAsync");
+  t_q.frees.clear();
+  t_q.reqs.clear();
+  t_q.arena.clear();
+  return rc;
+}
+
+int disc_cuda_queue_num_records(void) { return static_cast<int>(t_q.records.size()); }
+int disc_cuda_queue_record(int i, int* level, int* members, int64_t* bytes, int* kernel, const char** schedule,
+                           float* ms) {
+  if (i < 0 || i >= static_cast<int>(t_q.records.size())) {
+    t_err = "disc_cuda_queue_record: index out of range";
+    return 5;
+  }
+  QRecord& r = t_q.records[i];
+  if (r.a && r.b && r.ms == 0.f) {
+    if (int rc = check(cudaEventSynchronize(r.b), "cudaEventSynchronize")) return rc;
+    if (int rc = check(cudaEventElapsedTime(&r.ms, r.a, r.b), "cudaEventElapsedTime")) return rc;
+  }
+  *level = r.level;
+  *members = r.members;
+  *bytes = r.bytes;
+  *kernel = r.kernel;
+  *schedule = r.sched >= 0 ? t_q.names[r.sched].c_str() : "mixed";
+  *ms = r.ms;
+  return 0;
+}
 
 int disc_cuda_set_capture(int enabled) {
   g_capture = enabled != 0;

@@ -52,6 +52,22 @@ int DeviceCachingAllocator::alloc(int64_t bytes, ExecStats& stats) {
 }
 
 void DeviceCachingAllocator::free(int block) {
+  if (defer_) {
+    deferred_.push_back(block);
+    return;
+  }
+  release(block);
+}
+
+void DeviceCachingAllocator::set_defer(bool on) {
+  defer_ = on;
+  if (!on) {
+    for (int b : deferred_) release(b);
+    deferred_.clear();
+  }
+}
+
+void DeviceCachingAllocator::release(int block) {
   free_[blocks_[block].bytes].push_back(block);
   cached_ += blocks_[block].bytes;
   if (budget_ > 0 && cached_ > budget_) trim();
@@ -87,9 +103,77 @@ int DeviceExecutor::take_event_pair() {
   return static_cast<int>(ev_next_++);
 }
 
+void DeviceExecutor::begin_grouped() {
+  if (grouped_) throw InternalError("grouped execution already in progress");
+  if (timing_pending_) cuda_ok(disc_cuda_stream_synchronize(stream_), "stream sync");
+  timing_pending_ = false;
+  records_.clear();
+  ev_next_ = 0;
+  device_launches_ = 0;
+  algorithmic_bytes_ = 0;
+  req_outputs_.clear();
+  req_stats_.clear();
+  scratch_.reset();
+  records_grouped_ = false;
+  cuda_ok(disc_cuda_queue_begin(stream_), "queue begin");
+  alloc_.set_defer(true);
+  grouped_ = true;
+  group_timing_ = timing_;
+  request_ = -1;
+}
+
+void DeviceExecutor::begin_request() {
+  if (!grouped_) throw InternalError("begin_request outside grouped execution");
+  cuda_ok(disc_cuda_queue_request(), "queue request");
+  ++request_;
+}
+
+void DeviceExecutor::end_grouped() {
+  if (!grouped_) return;
+  grouped_ = false;
+  const int rc = disc_cuda_queue_flush(group_timing_ ? 1 : 0);
+  alloc_.set_defer(false);
+  cuda_ok(rc, "grouped launch");
+  // one record per issued group; device times are read in finish_timing (timing mode)
+  const int n = disc_cuda_queue_num_records();
+  records_.clear();
+  device_launches_ = 0;
+  for (int i = 0; i < n; ++i) {
+    int level = 0, members = 0, kernel = -1;
+    int64_t bytes = 0;
+    const char* sched = nullptr;
+    float ms = 0.f;
+    if (group_timing_) {
+      // metadata only here (the event query would synchronize): read in finish_timing
+      records_.push_back({i, -1, "", 0, 0.0, 1, -1});
+    } else {
+      cuda_ok(disc_cuda_queue_record(i, &level, &members, &bytes, &kernel, &sched, &ms), "group record");
+      records_.push_back({level, kernel, std::string("group:") + (sched ? sched : ""), bytes, 0.0, members, -1});
+    }
+    device_launches_ += 1;
+  }
+  records_grouped_ = true;
+  timing_pending_ = group_timing_;
+}
+
 void DeviceExecutor::finish_timing() {
   if (!timing_pending_) return;
   timing_pending_ = false;
+  if (records_grouped_) {
+    double total = 0;
+    for (size_t i = 0; i < records_.size(); ++i) {
+      int level = 0, members = 0, kernel = -1;
+      int64_t bytes = 0;
+      const char* sched = nullptr;
+      float ms = 0.f;
+      cuda_ok(disc_cuda_queue_record(static_cast<int>(i), &level, &members, &bytes, &kernel, &sched, &ms),
+              "group record");
+      records_[i] = {level, kernel, std::string("group:") + (sched ? sched : ""), bytes, ms, members, -1};
+      total += ms;
+    }
+    stats_.kernel_ms = total;
+    return;
+  }
   cuda_ok(disc_cuda_stream_synchronize(stream_), "stream sync");
   double total = 0;
   for (auto& r : records_) {
@@ -158,15 +242,17 @@ void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBindin
   ExecStats stats;
   stats.host_instruction_count = plan.host_instruction_count();
   const auto t_run = Clock::now();
-  if (!append_records) {
+  if (!append_records && !grouped_) {
     if (timing_pending_) cuda_ok(disc_cuda_stream_synchronize(stream_), "stream sync");
     timing_pending_ = false;
     records_.clear();
+    records_grouped_ = false;
     ev_next_ = 0;
     device_launches_ = 0;
     algorithmic_bytes_ = 0;
   }
-  scratch_.reset();
+  if (!grouped_) scratch_.reset();  // grouped: scratch of every request stays live until the flush
+  if (grouped_) cuda_ok(disc_cuda_queue_mark(0, -1, "h2d"), "queue mark");  // input staging copies
 
   std::vector<int64_t> regs(plan.shape_program.num_regs, 0);
   struct Slot {
@@ -301,13 +387,17 @@ void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBindin
           ext.push_back(view(in.arg_bufs[a], resolve_all(art.external_input_dims[a], regs)));
         std::vector<OutBuf> outs;
         for (int b : in.out_bufs) outs.push_back(out_buf(b));
-        const int ev = timing_ ? take_event_pair() : -1;
+        const int ev = timing_ && !grouped_ ? take_event_pair() : -1;
         if (ev >= 0) cuda_ok(disc_cuda_event_record(ev_pool_[ev].first, stream_), "event");
         LaunchReport rep = launch_kernel(art, *ver, ext, regs, outs, scratch_, stream_, pref_, cache_, plan_serial);
         if (ev >= 0) cuda_ok(disc_cuda_event_record(ev_pool_[ev].second, stream_), "event");
         stats.launch_count++;
-        device_launches_ += rep.device_kernels;
         algorithmic_bytes_ += rep.algorithmic_bytes;
+        if (grouped_) {  // the queued ops of this kLaunch carry its bytes / artifact / schedule
+          cuda_ok(disc_cuda_queue_mark(rep.algorithmic_bytes, in.a, rep.schedule.c_str()), "queue mark");
+          break;
+        }
+        device_launches_ += rep.device_kernels;
         records_.push_back({static_cast<int>(pc), in.a, rep.schedule, rep.algorithmic_bytes, 0.0, rep.device_kernels, ev});
         break;
       }
@@ -315,11 +405,16 @@ void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBindin
         const int64_t m = resolve(in.lib_dims[0], regs), k = resolve(in.lib_dims[1], regs),
                       n = resolve(in.lib_dims[2], regs);
         DevTensor a = view(in.arg_bufs[0], {m, k}), b = view(in.arg_bufs[1], {k, n});
-        const int ev = timing_ ? take_event_pair() : -1;
+        const int ev = timing_ && !grouped_ ? take_event_pair() : -1;
         if (ev >= 0) cuda_ok(disc_cuda_event_record(ev_pool_[ev].first, stream_), "event");
         launch_gemm(m, k, n, a, b, out_buf(in.out_bufs[0]), stream_);
         if (ev >= 0) cuda_ok(disc_cuda_event_record(ev_pool_[ev].second, stream_), "event");
         stats.library_calls++;
+        if (grouped_) {
+          cuda_ok(disc_cuda_queue_mark(4 * (m * k + k * n + m * n), -1, "gemm"), "queue mark");
+          algorithmic_bytes_ += 4 * (m * k + k * n + m * n);
+          break;
+        }
         device_launches_ += (m && n) ? 1 : 0;
         records_.push_back({static_cast<int>(pc), -1, "gemm", 4 * (m * k + k * n + m * n), 0.0, (m && n) ? 1 : 0, ev});
         break;
@@ -328,7 +423,13 @@ void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBindin
         const auto& po = plan.outputs[in.a];
         std::vector<int64_t> dims = resolve_all(po.dims, regs);
         DevTensor t = view(in.b, dims);
-        if (slots[in.b].input) {
+        if (slots[in.b].input && grouped_) {
+          // Pass-through in a group: a per-request copy (scratch lives until the next run).
+          const int64_t bytes = numel(dims) * 4;
+          float* p = static_cast<float*>(scratch_.alloc(bytes));
+          if (bytes) cuda_ok(disc_cuda_memcpy(p, t.ptr, static_cast<size_t>(bytes), 2, stream_), "output copy");
+          outputs_[in.a] = {p, dims};
+        } else if (slots[in.b].input) {
           // Pass-through of a caller input: copy so the output outlives the binding.
           if (passthrough_.size() <= static_cast<size_t>(in.a)) {
             passthrough_.resize(in.a + 1, nullptr);
@@ -353,6 +454,7 @@ void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBindin
     }
   }
   if (plan.shape_program.empty()) input_asserts();
+  if (grouped_) cuda_ok(disc_cuda_queue_mark(0, -1, "copy"), "queue mark");  // pass-through output copies
 
   // Every block still held returns to the cache for the next run (outputs stay readable
   // until then: the next run's work is ordered after them on the stream).
@@ -362,7 +464,12 @@ void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBindin
 
   stats.host_ms = std::chrono::duration<double, std::milli>(Clock::now() - t_run).count();
   stats_ = stats;
-  timing_pending_ = timing_pending_ || timing_;
+  if (grouped_) {
+    req_outputs_.push_back(outputs_);
+    req_stats_.push_back(stats);
+  } else {
+    timing_pending_ = timing_pending_ || timing_;
+  }
   events_.clear();
   for (const auto& [_, ev] : events) events_.push_back(ev);
 }

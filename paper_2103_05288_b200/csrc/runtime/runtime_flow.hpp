@@ -43,6 +43,9 @@ class DeviceCachingAllocator {
   int64_t bytes(int block) const { return blocks_[block].bytes; }
   void set_stream(void* s) { stream_ = s; }
   void set_budget(int64_t b) { budget_ = b; }
+  // Grouped execution: frees are held back until release_deferred() (work queued for
+  // later issue may still use the blocks), so no block is reused inside one group.
+  void set_defer(bool on);
   void trim();
   int64_t cached_bytes() const { return cached_; }
 
@@ -56,6 +59,9 @@ class DeviceCachingAllocator {
   std::map<int64_t, std::vector<int>> free_;
   int64_t cached_ = 0;
   int64_t budget_ = 0;
+  bool defer_ = false;
+  std::vector<int> deferred_;
+  void release(int block);
 };
 
 struct LaunchRecord {
@@ -90,6 +96,18 @@ class DeviceExecutor {
   // plan_serial: stable id of `plan` (enables the launch recipe cache; 0 disables).
   void run(const CompiledPlan& plan, const std::vector<InputBinding>& inputs, bool append_records = false,
            uint64_t plan_serial = 0);
+  // Grouped execution of independent requests (disc_executor_run_grouped):
+  //   begin_grouped(); { begin_request(); [stage_input...]; run(...); } x n; end_grouped();
+  // Each run() evaluates its request's runtime flow on the host (shapes, buffers,
+  // versions, schedules) while the device work is queued; end_grouped() issues it level
+  // by level with the same plan kernel of all requests fused into grouped launches.
+  // Request outputs stay valid until the next run.
+  void begin_grouped();
+  void begin_request();
+  void end_grouped();
+  bool grouped() const { return grouped_; }
+  const std::vector<std::vector<OutputView>>& request_outputs() const { return req_outputs_; }
+  const std::vector<ExecStats>& request_stats() const { return req_stats_; }
   // Timing mode: waits for the recorded events and fills record/stat device times.
   void finish_timing();
   const std::vector<OutputView>& outputs() const { return outputs_; }
@@ -129,6 +147,12 @@ class DeviceExecutor {
   std::vector<std::pair<void*, void*>> ev_pool_;
   size_t ev_next_ = 0;
   bool timing_pending_ = false;
+  bool grouped_ = false;
+  bool group_timing_ = false;
+  bool records_grouped_ = false;  // records_ describe grouped launches
+  int request_ = -1;
+  std::vector<std::vector<OutputView>> req_outputs_;
+  std::vector<ExecStats> req_stats_;
   int take_event_pair();
 };
 

@@ -161,30 +161,32 @@ def generate():
         parts.append(gen_program(f"Pre_{tag}", rec["pre"], ch))
         if kind == "row":
             parts.append(gen_program(f"Post_{tag}", rec["post"], ch))
-        parts.append(f"cudaError_t launch_{tag}(const void* l, int vec, cudaStream_t s) {{")
+        parts.append(f"cudaError_t launch_{tag}(const void* l, int vec, cudaStream_t s, const HostGroup* g) {{")
         parts.append(f"  constexpr int kGenCH = {ch};")
         if kind == "loop":
             parts.append("  const auto& L = *static_cast<const disc_loop_launch*>(l);")
-            parts.append(f"  return vec == 4 ? launch_loop_with<kGenCH>(k_loop<4, false, Pre_{tag}, kGenCH>, L, s, false)"
-                         f" : launch_loop_with<kGenCH>(k_loop<1, false, Pre_{tag}, kGenCH>, L, s, false);")
+            parts.append(f"  return loop_pass<Pre_{tag}, kGenCH, false>(L, s, false, g);")
         elif kind == "row":
             parts.append("  const auto& L = *static_cast<const disc_reduce_launch*>(l);")
-            parts.append(f"  return row_pass<Pre_{tag}, Post_{tag}, kGenCH, false>(L, s, false);")
+            parts.append(f"  return row_pass<Pre_{tag}, Post_{tag}, kGenCH, false>(L, s, false, g);")
         else:
             parts.append("  const auto& L = *static_cast<const disc_reduce_launch*>(l);")
-            parts.append(f"  return col_pass_t<Pre_{tag}, kGenCH, false>(L, s, false);")
+            parts.append(f"  return col_pass_t<Pre_{tag}, kGenCH, false>(L, s, false, g);")
         parts.append("}")
         parts.append("")
         entries.append((["loop", "row", "col"].index(kind), key, f"launch_{tag}"))
     files = {}
     for k, parts in enumerate(shards):
         files[os.path.join(KDIR, f"patterns_gen_{k}.cu")] = "\n".join(parts + ["}  // namespace disc_gen", ""])
-    reg = header + ["#include <cstdint>", "", "#include <cuda_runtime.h>", "", "namespace disc_gen {"]
+    reg = header + ["#include <cstdint>", "", "#include <cuda_runtime.h>", "",
+                    "namespace disc_dev {", "struct HostGroup;", "}  // namespace disc_dev", "", "namespace disc_gen {",
+                    "using disc_dev::HostGroup;"]
     for _, _, fn in sorted(entries):
-        reg.append(f"cudaError_t {fn}(const void* l, int vec, cudaStream_t s);")
+        reg.append(f"cudaError_t {fn}(const void* l, int vec, cudaStream_t s, const HostGroup* g);")
     reg += ["}  // namespace disc_gen", "", "namespace disc_spec {",
             "struct Entry {\n  int kind;\n  uint64_t key;\n"
-            "  cudaError_t (*launch)(const void* launch, int vec, cudaStream_t s);\n};",
+            "  // g != nullptr: grouped launch of g->n descriptors (l = the first)\n"
+            "  cudaError_t (*launch)(const void* launch, int vec, cudaStream_t s, const disc_dev::HostGroup* g);\n};",
             "static const Entry kEntries[] = {"]
     for kind, key, fn in sorted(entries):
         reg.append(f"    {{{kind}, 0x{key}ull, disc_gen::{fn}}},")
