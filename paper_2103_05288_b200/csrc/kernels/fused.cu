@@ -2,6 +2,7 @@
 // live in kernels.cuh.  Memory-bound schedules: no tensor cores; 128-bit coalesced
 // accesses, CH chunks in flight per thread, f64 accumulation for reductions (the
 // reference's reduce semantics, kernels.cpp:46-54, 234-259).
+#include <cstdlib>
 #include <unordered_map>
 
 #include "kernels.cuh"
@@ -124,6 +125,15 @@ namespace disc_dev {
 static int g_pdl = 1;
 bool pdl_enabled() { return g_pdl != 0; }
 
+int group_waves() {
+  static const int w = [] {
+    const char* e = std::getenv("DISC_GROUP_WAVES");
+    const int v = e ? std::atoi(e) : 16;
+    return v > 0 ? v : 16;
+  }();
+  return w;
+}
+
 int resident_ctas(const void* kernel, int block, size_t smem) {
   thread_local std::unordered_map<uint64_t, int> cache;
   const uint64_t key = (reinterpret_cast<uintptr_t>(kernel) * 0x9E3779B97F4A7C15ull) ^
@@ -165,6 +175,9 @@ cudaError_t finalize_columns(const disc_reduce_launch& L, cudaStream_t s, const 
     G.table = g->dev_table;
     G.stride = g->stride;
     G.n = g->n;
+    G.nseg = 1;  // finalize reads only the reduce geometry and pointers (and pre.flags)
+    G.seg[0][0] = 0;
+    G.seg[0][1] = static_cast<uint16_t>(desc_bytes<disc_reduce_launch>() / 16);
     int64_t off = 0;
     for (int i = 0; i < g->n; ++i) {
       G.block_off[i] = static_cast<int32_t>(off);

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstddef>
 #include <cfloat>
 #include <cmath>
 #include <type_traits>
@@ -98,10 +99,13 @@ constexpr int kCH = 2;  // chunks per thread per dispatch
 #ifndef DISC_MAX_GROUP
 #define DISC_MAX_GROUP 1024
 #endif
+#define DISC_GROUP_SEGS 8
 struct disc_group {
   const unsigned char* table;  // n descriptors, `stride` bytes apart
   int32_t stride;
   int32_t n;
+  int32_t nseg;                       // descriptor byte ranges a CTA stages, in 16 B units:
+  uint16_t seg[DISC_GROUP_SEGS][2];   // (offset, count); the members share program structure
   int32_t block_off[DISC_MAX_GROUP + 1];
 };
 
@@ -125,9 +129,48 @@ template <typename Launch>
 __device__ __forceinline__ const Launch& group_stage(const disc_group& G, int g, unsigned char* buf) {
   const uint4* src = reinterpret_cast<const uint4*>(G.table + static_cast<int64_t>(g) * G.stride);
   uint4* dst = reinterpret_cast<uint4*>(buf);
-  for (int i = threadIdx.x; i < desc_bytes<Launch>() / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+  for (int k = 0; k < G.nseg; ++k) {  // only the ranges the kernel reads (unused loads/code skipped)
+    const int o = G.seg[k][0], c = G.seg[k][1];
+    for (int i = threadIdx.x; i < c; i += blockDim.x) dst[o + i] = __ldg(src + o + i);
+  }
   __syncthreads();
   return *reinterpret_cast<const Launch*>(buf);
+}
+
+// Host: the staged ranges of a group's descriptors (from its first member; members of a
+// generated group share n_loads / n_outs; interpreter groups stage whole programs).
+namespace detail {
+inline void seg_add(disc_group& G, size_t begin, size_t end) {
+  const int o = static_cast<int>(begin / 16), e = static_cast<int>((end + 15) / 16);
+  if (G.nseg > 0 && G.seg[G.nseg - 1][0] + G.seg[G.nseg - 1][1] >= o) {  // merge adjacent
+    const int s0 = G.seg[G.nseg - 1][0];
+    G.seg[G.nseg - 1][1] = static_cast<uint16_t>(std::max(e, s0 + G.seg[G.nseg - 1][1]) - s0);
+    return;
+  }
+  G.seg[G.nseg][0] = static_cast<uint16_t>(o);
+  G.seg[G.nseg][1] = static_cast<uint16_t>(e - o);
+  ++G.nseg;
+}
+inline void seg_program(disc_group& G, size_t base, const disc_program& P, bool whole) {
+  if (whole) {
+    seg_add(G, base, base + sizeof(disc_program));
+    return;
+  }
+  seg_add(G, base, base + offsetof(disc_program, code));
+  seg_add(G, base + offsetof(disc_program, loads), base + offsetof(disc_program, loads) + P.n_loads * sizeof(disc_load));
+  seg_add(G, base + offsetof(disc_program, outs), base + sizeof(disc_program));
+}
+}  // namespace detail
+inline void group_segments(disc_group& G, const disc_loop_launch& L, bool whole) {
+  G.nseg = 0;
+  detail::seg_program(G, offsetof(disc_loop_launch, prog), L.prog, whole);
+  detail::seg_add(G, offsetof(disc_loop_launch, prog) + sizeof(disc_program), sizeof(disc_loop_launch));
+}
+inline void group_segments(disc_group& G, const disc_reduce_launch& L, bool whole) {
+  G.nseg = 0;
+  detail::seg_program(G, offsetof(disc_reduce_launch, pre), L.pre, whole);
+  detail::seg_program(G, offsetof(disc_reduce_launch, post), L.post, whole);
+  detail::seg_add(G, offsetof(disc_reduce_launch, post) + sizeof(disc_program), sizeof(disc_reduce_launch));
 }
 
 // ---------------------------------------------------------------------------
@@ -650,25 +693,44 @@ inline cudaError_t launch_col_with(K kernel, const disc_reduce_launch& L, cudaSt
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-// Grouped launches (see disc_group).  Every launch keeps its single-launch grid; the
-// group's CTAs are concatenated in table order.
+// Grouped launches (see disc_group).  The group's CTAs are concatenated in table order.
+// CTA budget: a few waves of the kernel shared by all members in proportion to their
+// work units (warp tiles / row groups), every member >= 1 CTA and never more than it can
+// use or than one wave (its single-launch grid).  Members grid-stride over their units,
+// so per-CTA startup (descriptor staging, dependency wait) is amortised over many units
+// instead of every member paying a full wave.
+int group_waves();  // DISC_GROUP_WAVES (default 16; A/B on C2: 1 -> 3453, 4 -> 4855, 8 -> 5211, 16 -> 5225 GB/s)
+
+inline void group_blocks(const int64_t* units, int n, int64_t cap, int32_t* off) {
+  int64_t total = 0;
+  for (int i = 0; i < n; ++i) total += units[i] > 0 ? units[i] : 0;
+  const int64_t budget = static_cast<int64_t>(group_waves()) * cap;
+  int64_t o = 0;
+  for (int i = 0; i < n; ++i) {
+    off[i] = static_cast<int32_t>(o);
+    if (units[i] <= 0) continue;
+    int64_t b = total <= budget ? units[i] : (budget * units[i] + total - 1) / total;
+    b = std::max<int64_t>(1, std::min({b, units[i], cap}));
+    o += b;
+  }
+  off[n] = static_cast<int32_t>(o);
+}
 template <int CH = kCH, typename K>
 inline cudaError_t launch_loop_group(K kernel, const HostGroup& H, cudaStream_t s, bool use_slots) {
   disc_group G;
   G.table = H.dev_table;
   G.stride = H.stride;
   G.n = H.n;
+  group_segments(G, H.at<disc_loop_launch>(0), use_slots);
   size_t smem = 0;
   for (int i = 0; i < H.n; ++i) smem = std::max(smem, loop_smem<CH>(H.at<disc_loop_launch>(i), use_slots));
   cudaError_t e = set_smem(kernel, smem, kGroupSmemThreshold);
   if (e != cudaSuccess) return e;
   const int64_t cap = static_cast<int64_t>(sm_count()) * resident_ctas(reinterpret_cast<const void*>(kernel), kLoopThreads, smem);
-  int64_t off = 0;
-  for (int i = 0; i < H.n; ++i) {
-    G.block_off[i] = static_cast<int32_t>(off);
-    off += std::min(loop_blocks_wanted<CH>(H.at<disc_loop_launch>(i)), cap);
-  }
-  G.block_off[H.n] = static_cast<int32_t>(off);
+  int64_t units[DISC_MAX_GROUP];
+  for (int i = 0; i < H.n; ++i) units[i] = loop_blocks_wanted<CH>(H.at<disc_loop_launch>(i));
+  group_blocks(units, H.n, cap, G.block_off);
+  const int64_t off = G.block_off[H.n];
   if (off == 0) return cudaSuccess;
   e = launch_k(kernel, dim3(static_cast<unsigned>(off)), dim3(kLoopThreads), smem, s, G);
   return e != cudaSuccess ? e : cudaGetLastError();
@@ -680,19 +742,20 @@ inline cudaError_t launch_row_group(K kernel, const HostGroup& H, cudaStream_t s
   G.table = H.dev_table;
   G.stride = H.stride;
   G.n = H.n;
+  group_segments(G, H.at<disc_reduce_launch>(0), use_slots);
   size_t smem = 0;
   for (int i = 0; i < H.n; ++i) smem = std::max(smem, row_smem<CH>(H.at<disc_reduce_launch>(i), use_slots));
   const int block = row_block(H.at<disc_reduce_launch>(0));
   cudaError_t e = set_smem(kernel, smem, kGroupSmemThreshold);
   if (e != cudaSuccess) return e;
   const int64_t cap = static_cast<int64_t>(sm_count()) * resident_ctas(reinterpret_cast<const void*>(kernel), block, smem);
-  int64_t off = 0;
+  int64_t units[DISC_MAX_GROUP];
   for (int i = 0; i < H.n; ++i) {
     const disc_reduce_launch& L = H.at<disc_reduce_launch>(i);
-    G.block_off[i] = static_cast<int32_t>(off);
-    if (L.K > 0) off += std::min((L.K + block / L.group - 1) / (block / L.group), cap);
+    units[i] = L.K > 0 ? (L.K + block / L.group - 1) / (block / L.group) : 0;
   }
-  G.block_off[H.n] = static_cast<int32_t>(off);
+  group_blocks(units, H.n, cap, G.block_off);
+  const int64_t off = G.block_off[H.n];
   if (off == 0) return cudaSuccess;
   e = launch_k(kernel, dim3(static_cast<unsigned>(off)), dim3(block), smem, s, G);
   return e != cudaSuccess ? e : cudaGetLastError();
@@ -704,6 +767,7 @@ inline cudaError_t launch_col_group(K kernel, const HostGroup& H, cudaStream_t s
   G.table = H.dev_table;
   G.stride = H.stride;
   G.n = H.n;
+  group_segments(G, H.at<disc_reduce_launch>(0), use_slots);
   size_t smem = 0;
   int64_t off = 0;
   for (int i = 0; i < H.n; ++i) {
