@@ -151,6 +151,11 @@ typedef struct {
   int32_t g_rank;
   int32_t g_mask;
   int64_t g_dims[DISC_MAX_RANK];
+  /* ROW with a fused epilogue: shared-memory slot that keeps the reduce ARGUMENT (the
+   * pre program's per-element value) for the epilogue, which reads it as a cached
+   * identity load instead of recomputing it (softmax: exp(x - max)); -1 = none */
+  int32_t arg_slot;
+  int32_t pad_;
 } disc_reduce_launch;
 
 /* Standalone pad (eval_pad, kernels.cpp:125-147), output-driven gather. */

@@ -21,6 +21,9 @@ import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libdisc_b200.so")
+# A/B experiments (tools/ab_*.sh): an alternative in-tree build of the same library
+if os.environ.get("DISC_LIB_VARIANT"):
+    LIB_PATH = os.path.join(os.path.dirname(LIB_PATH), f"libdisc_b200_{os.environ['DISC_LIB_VARIANT']}.so")
 _lib: Optional[C.CDLL] = None
 
 ERROR_CLASSES = ("usage", "parse", "validation", "compile", "runtime", "internal")

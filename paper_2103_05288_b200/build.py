@@ -24,6 +24,12 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libdisc_b200.so")
+# A/B experiment builds: DISC_BUILD_VARIANT=<name> DISC_NVCC_DEFS="-DKNOB=0" builds
+# libdisc_b200_<name>.so in its own object dir (selected at run time by DISC_LIB_VARIANT).
+_VARIANT = os.environ.get("DISC_BUILD_VARIANT")
+if _VARIANT:
+    BUILD = os.path.join(PKG, f"_build_{_VARIANT}")
+    LIB = os.path.join(PKG, f"libdisc_b200_{_VARIANT}.so")
 
 CXX = shutil.which("g++", path="/usr/bin") or "g++"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -31,7 +37,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CXXFLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-Wno-unused-parameter",
             "-ffp-contract=off"]
 NVCCFLAGS = ["-std=c++17", "-O3", "-lineinfo", "--fmad=false", "-prec-div=true", "-prec-sqrt=true",
-             "-Xcompiler", "-fPIC", "-Xptxas", "-O3", "--expt-relaxed-constexpr"] + ARCH
+             "-Xcompiler", "-fPIC", "-Xptxas", "-O3", "--expt-relaxed-constexpr"] + ARCH + \
+    os.environ.get("DISC_NVCC_DEFS", "").split()
 
 
 def _json_header() -> str:

@@ -96,6 +96,9 @@ constexpr int kCH = 2;  // chunks per thread per dispatch
 // in a device table (uploaded by the device layer) and is staged into shared memory
 // once per CTA; the CTA -> launch map is a binary search over the offsets held in
 // __grid_constant__ parameter space.
+#ifndef DISC_ROW_PIPE
+#define DISC_ROW_PIPE 0  // software-pipelined reduce pass in row kernels (A/B on B200: slower, off)
+#endif
 #ifndef DISC_MAX_GROUP
 #define DISC_MAX_GROUP 1024
 #endif
@@ -361,7 +364,50 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
     Acc part[CH];
 #pragma unroll
     for (int c = 0; c < CH; ++c) part[c] = RD::identity();
-    if (valid) {
+    if constexpr (DISC_ROW_PIPE && Pre::kPipe > 0 && !STAGED) {
+      // Software pipeline (generated programs): the next span's loads are issued before
+      // the current span is evaluated and accumulated.
+      using LD = typename Pre::template Loads<VEC, CH>;
+      if (valid) {
+        I col0 = static_cast<I>(lane) * VEC;
+        int nv = col0 < R ? chunks_in_row<CH>(R - col0, cstride) : 0;
+        LD cur;
+        if (nv == CH) Pre::template load<VEC, CH, WIDE>(L.pre, Tile<I, true>{row, col0, R, cstride, CH, row_cache, sst}, cur);
+        else if (nv > 0) Pre::template load<VEC, CH, WIDE>(L.pre, Tile<I, false>{row, col0, R, cstride, nv, row_cache, sst}, cur);
+        while (nv > 0) {
+          const I ncol = col0 + span;
+          const int nnv = ncol < R ? chunks_in_row<CH>(R - ncol, cstride) : 0;
+          LD nxt;
+          if (nnv == CH)
+            Pre::template load<VEC, CH, WIDE>(L.pre, Tile<I, true>{row, ncol, R, cstride, CH, row_cache, sst}, nxt);
+          else if (nnv > 0)
+            Pre::template load<VEC, CH, WIDE>(L.pre, Tile<I, false>{row, ncol, R, cstride, nnv, row_cache, sst}, nxt);
+          T v[CH];
+          if (nv == CH) {
+            Pre::template run_loaded<VEC, CH, WIDE>(L.pre, Tile<I, true>{row, col0, R, cstride, CH, row_cache, sst}, cur, v,
+                                                    slots, blockDim.x, consts[0], 0.f);
+#pragma unroll
+            for (int c = 0; c < CH; ++c) part[c] = RD::acc(part[c], v[c]);
+          } else {
+            Pre::template run_loaded<VEC, CH, WIDE>(L.pre, Tile<I, false>{row, col0, R, cstride, nv, row_cache, sst}, cur, v,
+                                                    slots, blockDim.x, consts[0], 0.f);
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+              if (c < nv) part[c] = RD::acc(part[c], v[c]);
+          }
+          if (L.arg_slot >= 0 && row_cache) {
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+              if (c < nv) *reinterpret_cast<T*>(row_cache + L.arg_slot * sst + col0 + c * cstride) = v[c];
+          }
+          cur = nxt;
+          col0 = ncol;
+          nv = nnv;
+        }
+      }
+    } else if (valid) {
+      // reduce-argument cache (fused epilogue reads the pre value back from smem)
+      float* const arg_cache = (!STAGED && L.arg_slot >= 0 && row_cache) ? row_cache + L.arg_slot * sst : nullptr;
       for (I col0 = static_cast<I>(lane) * VEC; col0 < R; col0 += span) {
         const int nv = chunks_in_row<CH>(R - col0, cstride);
         T v[CH];
@@ -376,6 +422,11 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
 #pragma unroll
           for (int c = 0; c < CH; ++c)
             if (c < nv) part[c] = RD::acc(part[c], v[c]);
+        }
+        if (arg_cache) {
+#pragma unroll
+          for (int c = 0; c < CH; ++c)
+            if (c < nv) *reinterpret_cast<T*>(arg_cache + col0 + c * cstride) = v[c];
         }
       }
     }

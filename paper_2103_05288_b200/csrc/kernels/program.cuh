@@ -266,6 +266,25 @@ __device__ __forceinline__ void load_cls(const disc_program& P, const Ctx& t, co
   }
 }
 
+// Per-row scalar of a splat-class load (value depends on the row only): one register
+// per chunk (column tiles: the same row, loaded once).
+template <int CH, typename Ctx>
+__device__ __forceinline__ void load_splat(const disc_program& P, const Ctx& t, int l, float (&s)[CH]) {
+  using I = typename Ctx::Index;
+  const disc_load& L = P.loads[l];
+  const I rs = static_cast<I>(L.rs);
+  const float* base = L.ptr + (static_cast<I>(L.offset) + t.row * rs);
+  if constexpr (Ctx::kRows) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      if (t.has(c)) s[c] = ldg(base + c * t.cstride * rs);
+  } else {
+    const float x = ldg(base);
+#pragma unroll
+    for (int c = 0; c < CH; ++c) s[c] = x;
+  }
+}
+
 // L2 prefetch of a tile's chunks of load l (streaming identity operands: the next
 // grid-stride tile is requested while the current one computes; no registers held).
 template <int VEC, int CH, int CLS, typename Ctx>

@@ -384,6 +384,19 @@ int lanes_per_row(int64_t W, int vec) {
 
 constexpr int64_t kWideLimitView = (int64_t{1} << 31) - 64;
 
+// Placeholder pointer of the reduce-argument cache load (16 B aligned, never dereferenced:
+// the load is always served from shared memory, see disc_reduce_launch.arg_slot).
+const float* const kArgCachePtr = reinterpret_cast<const float*>(uintptr_t{0xA5C0} << 4);
+
+// DISC_ARG_CACHE=0 disables the reduce-argument cache (A/B).
+bool arg_cache_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DISC_ARG_CACHE");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 int sm_count();
 
 // Threads per row (power of two) for the row schedule over K rows of R elements:
@@ -504,9 +517,15 @@ class Lowering {
   Lowering(const Binding& B, ProgramBuilder& pb, const float* red_ptr, const Map* row_map)
       : B_(B), pb_(pb), red_ptr_(red_ptr), row_map_(row_map) {}
 
+  // Member t is read through an identity load of `ptr` instead of being recomputed
+  // (the reduce-argument cache of a fused row epilogue).
+  void substitute(int t, const float* ptr) { subst_[t] = ptr; }
+
   int value(int t) {
     auto it = memo_.find(t);
     if (it != memo_.end()) return it->second;
+    auto sb = subst_.find(t);
+    if (sb != subst_.end()) return memo_[t] = pb_.load(sb->second, identity_map(numel(B_.dims[t])));
     const TapeInstr& ti = B_.art.tape[t];
     int v;
     if (t == B_.red) {
@@ -542,6 +561,7 @@ class Lowering {
   const float* red_ptr_;
   const Map* row_map_;
   std::map<int, int> memo_;
+  std::map<int, const float*> subst_;
 
   int reduce_at(const Map& m) {
     if (row_map_) {
@@ -872,6 +892,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
 
   disc_reduce_launch R;
   std::memset(&R, 0, sizeof R);
+  R.arg_slot = -1;
   R.kind = rt.kind == DhloOpKind::kReduceSum ? DISC_REDUCE_SUM : DISC_REDUCE_MAX;
   R.red_out = red_ptr;
   R.wide = N > kWideLimit || nout > kWideLimit;
@@ -914,6 +935,11 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
       try {
         ProgramBuilder pb;
         Lowering lw(B, pb, nullptr, &row);
+        // The epilogue reads the reduce argument back from shared memory (written by the
+        // reduce pass) instead of recomputing it; rows up to 4096 keep every cache slot
+        // within the 48 KB budget (never staged: R >= 32).
+        if (arg_cache_enabled() && rarg.kind == TapeRef::Kind::kMember && R.R >= 32 && R.R <= 4096)
+          lw.substitute(rarg.index, kArgCachePtr);
         for (size_t o = 0; o < art.output_tape_indices.size(); ++o) {
           int t = art.output_tape_indices[o];
           if (B.post[t]) pb.output(lw.value(t), outs[o].ptr);
@@ -1013,8 +1039,13 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     // of a second pass over HBM/L2 (softmax: x is read once).
     if (post_fused && !R.stage) {
       int nc = 0;
-      for (int q = 0; q < R.post.n_loads && nc < 2; ++q) {
-        if (R.post.loads[q].mode != DISC_LOAD_IDENTITY) continue;
+      for (int q = 0; q < R.post.n_loads; ++q)
+        if (R.post.loads[q].ptr == kArgCachePtr) {
+          R.arg_slot = nc;
+          R.post.cache_slot[q] = static_cast<int8_t>(nc++);
+        }
+      for (int q = 0; q < R.post.n_loads && nc < 2 + (R.arg_slot >= 0); ++q) {
+        if (R.post.loads[q].mode != DISC_LOAD_IDENTITY || R.post.loads[q].ptr == kArgCachePtr) continue;
         for (int p = 0; p < R.pre.n_loads; ++p)
           if (R.pre.loads[p].mode == DISC_LOAD_IDENTITY && R.pre.loads[p].ptr == R.post.loads[q].ptr) {
             if (R.pre.cache_slot[p] < 0) R.pre.cache_slot[p] = static_cast<int8_t>(nc++);
@@ -1030,6 +1061,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
         R.pre.cache_mode = DISC_CACHE_FILL;
         R.post.cache_mode = DISC_CACHE_READ;
       } else {
+        if (R.arg_slot >= 0) throw InternalError("reduce-argument cache over budget");
         for (int l = 0; l < DISC_MAX_LOADS; ++l) R.pre.cache_slot[l] = R.post.cache_slot[l] = -1;
       }
     }
@@ -1132,6 +1164,7 @@ LaunchReport launch_materialized(Binding& B, const std::vector<OutBuf>& outs, Sc
       if (cnt == 0) continue;
       disc_reduce_launch R;
       std::memset(&R, 0, sizeof R);
+      R.arg_slot = -1;
       ProgramBuilder pb;
       int v = pb.load(x.ptr, identity_map(numel(x.dims)));
       Built b = pb.finish(v);
@@ -1312,7 +1345,8 @@ struct Patch {
     if (kind == kTagExt) p = const_cast<T*>(reinterpret_cast<const T*>(ext.at(idx).ptr));
     else if (kind == kTagOut) p = reinterpret_cast<T*>(outs.at(idx).ptr);
     else if (kind == kTagScratch) p = reinterpret_cast<T*>(scratch.at(idx));
-    else if (v) throw InternalError("untagged pointer in a launch recipe");
+    else if (v && reinterpret_cast<const float*>(p) != kArgCachePtr)
+      throw InternalError("untagged pointer in a launch recipe");
   }
   void program(disc_program& P) const {
     for (int l = 0; l < P.n_loads; ++l) (*this)(P.loads[l].ptr);

@@ -26,6 +26,7 @@ OUT = os.path.join(KDIR, "patterns_gen.cu")  # registry; kernels in patterns_gen
 SHARDS = 6
 
 I_LOAD_CONST, I_REDVAL, I_COPY, I_BIN, I_UN = 3, 4, 5, 8, 28
+LC_SPLAT, LC_CONTIG, LC_CONTIGU = 2, 3, 6  # program.cuh LoadClass
 
 
 def library():
@@ -69,30 +70,42 @@ def collect():
     return seen
 
 
-def gen_program(fn, prog, ch=1):
+def gen_program(fn, prog, ch=1, early_splat=True):
     """Straight-line body for one program (code from the capture).
 
     Identity (streaming) loads are split into a load phase (``load`` fills a Loads
     struct) and the rest (``run_loaded``), so a schedule can issue the next tile's
     loads before computing the current one (software pipelining); ``run`` = both."""
     code = prog["code"]
-    ident = [i for i, (op, a, b, flags, dst, load, out) in enumerate(code)
-             if op <= I_LOAD_CONST and prog["lclass"][load] == 0]
-    pf = [f"    prefetch_cls<VEC, CH, 0>(P, t, {code[i][5]});" for i in ident]
+    loads = [(i, prog["lclass"][load]) for i, (op, a, b, flags, dst, load, out) in enumerate(code) if op <= I_LOAD_CONST]
+    ident = [i for i, c in loads if c == 0]
+    # Loads issued in the load phase (and, in a pipelined schedule, one tile ahead):
+    # streaming identity operands, per-row scalars (splat: one register) and, while the
+    # register budget allows, the L2-resident contiguous [W] vectors (bias/gamma/...).
+    splat = [i for i, c in loads if c == LC_SPLAT] if early_splat else []
+    contig = [i for i, c in loads if c in (LC_CONTIG, LC_CONTIGU)]
+    regs = len(ident) * ch * 4 + len(splat) * ch
+    if regs + len(contig) * ch * 4 <= 16:
+        ident = ident + contig
+        regs += len(contig) * ch * 4
+    early = sorted(ident + splat)
+    pf = [f"    prefetch_cls<VEC, CH, 0>(P, t, {code[i][5]});" for i, c in loads if c == 0]
     lines = [f"struct {fn} {{",
              "  static constexpr bool kSplitFull = true;",
              # pipelined only while the extra tile of loads fits (<= 16 registers at VEC=4)
-             f"  static constexpr int kPipe = {len(ident) if len(ident) * ch * 4 <= 16 else 0};",
+             f"  static constexpr int kPipe = {len(early) if regs <= 16 else 0};",
              "  template <int VEC, int CH>",
              "  struct Loads {"] + \
-            [f"    typename Vec<VEC>::T l{i}[CH];" for i in ident] + (["    char none;"] if not ident else []) + \
+            [f"    typename Vec<VEC>::T l{i}[CH];" for i in ident] + [f"    float s{i}[CH];" for i in splat] + \
+            (["    char none;"] if not early else []) + \
             ["  };",
              "  template <int VEC, int CH, typename Ctx>",
              "  __device__ __forceinline__ static void prefetch(const disc_program& P, const Ctx& t) {"] + pf + \
             ["  }",
              "  template <int VEC, int CH, bool WIDE, typename Ctx>",
              "  __device__ __forceinline__ static void load(const disc_program& P, const Ctx& t, Loads<VEC, CH>& L) {"] + \
-            [f"    load_cls<VEC, CH, WIDE, 0>(P, t, nullptr, {code[i][5]}, L.l{i});" for i in ident] + \
+            [f"    load_cls<VEC, CH, WIDE, {prog['lclass'][code[i][5]]}>(P, t, nullptr, {code[i][5]}, L.l{i});"
+             if i in ident else f"    load_splat<CH>(P, t, {code[i][5]}, L.s{i});" for i in early] + \
             ["  }",
              "  template <int VEC, int CH, bool WIDE, typename Ctx>",
              "  __device__ __forceinline__ static void run_loaded(const disc_program& P, const Ctx& t, const Loads<VEC, CH>& L,",
@@ -108,6 +121,8 @@ def gen_program(fn, prog, ch=1):
         if op <= I_LOAD_CONST:
             if i in ident:
                 lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = L.l{i}[c];")
+            elif i in splat:
+                lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = splat(L.s{i}[c], {v}[c]);")
             else:
                 lines.append(f"    load_cls<VEC, CH, WIDE, {prog['lclass'][load]}>(P, t, consts, {load}, {v});")
         elif op == I_REDVAL:
@@ -158,9 +173,11 @@ def generate():
         ch = 4 if n_code <= 8 else (2 if n_code <= 20 else 1)
         if 5 in rec["pre"]["lclass"] + rec.get("post", {}).get("lclass", []):
             ch = min(ch, 2)  # gather index math is register-heavy
-        parts.append(gen_program(f"Pre_{tag}", rec["pre"], ch))
+        # early (pipelined) per-row scalars only pay off in the loop schedule (A/B: the row
+        # schedule's reduce pass is faster with loads in program order)
+        parts.append(gen_program(f"Pre_{tag}", rec["pre"], ch, early_splat=kind == "loop"))
         if kind == "row":
-            parts.append(gen_program(f"Post_{tag}", rec["post"], ch))
+            parts.append(gen_program(f"Post_{tag}", rec["post"], ch, early_splat=False))
         parts.append(f"cudaError_t launch_{tag}(const void* l, int vec, cudaStream_t s, const HostGroup* g) {{")
         parts.append(f"  constexpr int kGenCH = {ch};")
         if kind == "loop":
