@@ -34,6 +34,8 @@ enum disc_op {
   DISC_OP_EXP, DISC_OP_TANH, DISC_OP_NEG,
   DISC_OP_COPY,
   DISC_OP_REDVAL,     /* the current row's reduce result (row schedule only) */
+  DISC_OP_RCPVAL,     /* 1 / REDVAL (IEEE reciprocal, once per row): x / REDVAL is lowered
+                         to x * RCPVAL in fused epilogues (<= 1.5 ulp from the quotient) */
 };
 
 /* Pre-decoded device opcodes: operand sources (accumulator A / slot S) are folded into
@@ -45,6 +47,7 @@ enum disc_opcode {
   DISC_I_LOAD_CONST = 3,  /* acc = hoisted scalar (loaded once per block) */
   DISC_I_REDVAL = 4,
   DISC_I_COPY = 5,      /* acc = slot[a] */
+  DISC_I_RCPVAL = 6,    /* acc = 1 / row reduce result */
   DISC_I_BIN = 8,       /* 8 + 4*(op-ADD) + mode, mode 0 AA, 1 AS, 2 SA, 3 SS (a op b) */
   DISC_I_UN = 28,       /* 28 + 2*(op-EXP) + mode, mode 0 A, 1 S */
   DISC_I_END = 34,

@@ -380,6 +380,11 @@ __device__ __forceinline__ void run_tile(const disc_program& P, const Ctx& t,
       case DISC_I_REDVAL:
         DISC_FOR_C acc[c] = splat(red, acc[c]);
         break;
+      case DISC_I_RCPVAL: {
+        const float r = __frcp_rn(red);
+        DISC_FOR_C acc[c] = splat(r, acc[c]);
+        break;
+      }
       case DISC_I_COPY:
         DISC_FOR_C acc[c] = DISC_S(in.a, c);
         break;

@@ -134,10 +134,26 @@ class ProgramBuilder {
     cse_[key] = v;
     return v;
   }
-  int op(int code, int a, int b = -1) { return push({code, a, b, -1}); }
+  int op(int code, int a, int b = -1) {
+    // Fused row epilogue: x / REDVAL -> x * (1 / REDVAL), the reciprocal once per row
+    // (softmax normalisation; within 1.5 ulp of the IEEE quotient).  Unfused plans never
+    // see REDVAL, so their IEEE division stays bit-exact.
+    if (code == DISC_OP_DIV && b >= 0 && b == red_ && rcp_enabled()) {
+      if (rcp_ < 0) rcp_ = push({DISC_OP_RCPVAL, -1, -1, -1});
+      return push({DISC_OP_MUL, a, rcp_, -1});
+    }
+    return push({code, a, b, -1});
+  }
   int redval() {
     if (red_ < 0) red_ = push({DISC_OP_REDVAL, -1, -1, -1});
     return red_;
+  }
+  static bool rcp_enabled() {
+    static const bool on = [] {
+      const char* e = std::getenv("DISC_RCP_REDVAL");
+      return !e || std::atoi(e) != 0;
+    }();
+    return on;
   }
   void output(int v, float* ptr) { outs_.emplace_back(v, ptr); }
 
@@ -199,6 +215,9 @@ class ProgramBuilder {
         case DISC_OP_REDVAL:
           I.op = DISC_I_REDVAL;
           break;
+        case DISC_OP_RCPVAL:
+          I.op = DISC_I_RCPVAL;
+          break;
         case DISC_OP_COPY:
           I.op = DISC_I_COPY;
           break;
@@ -248,6 +267,7 @@ class ProgramBuilder {
   std::map<std::tuple<const float*, std::vector<int64_t>, std::vector<int64_t>, int64_t>, int> cse_;
   std::vector<std::pair<int, float*>> outs_;
   int red_ = -1;
+  int rcp_ = -1;
   int push(Ins i) {
     ins_.push_back(i);
     return static_cast<int>(ins_.size()) - 1;

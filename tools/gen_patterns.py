@@ -25,7 +25,7 @@ KDIR = os.path.join(ROOT, "paper_2103_05288_b200", "csrc", "kernels")
 OUT = os.path.join(KDIR, "patterns_gen.cu")  # registry; kernels in patterns_gen_<k>.cu shards
 SHARDS = 6
 
-I_LOAD_CONST, I_REDVAL, I_COPY, I_BIN, I_UN = 3, 4, 5, 8, 28
+I_LOAD_CONST, I_REDVAL, I_COPY, I_RCPVAL, I_BIN, I_UN = 3, 4, 5, 6, 8, 28
 LC_SPLAT, LC_CONTIG, LC_CONTIGU = 2, 3, 6  # program.cuh LoadClass
 
 
@@ -127,6 +127,8 @@ def gen_program(fn, prog, ch=1, early_splat=True):
                 lines.append(f"    load_cls<VEC, CH, WIDE, {prog['lclass'][load]}>(P, t, consts, {load}, {v});")
         elif op == I_REDVAL:
             lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = splat(red, {v}[c]);")
+        elif op == I_RCPVAL:
+            lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = splat(__frcp_rn(red), {v}[c]);")
         elif op == I_COPY:
             lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = {src(True, a)}[c];")
         elif I_BIN <= op < I_UN:
@@ -160,7 +162,8 @@ def generate():
     header = ["// GENERATED by tools/gen_patterns.py -- do not edit.",
               "// Straight-line fused programs for the pattern library (fixtures + BASELINE configs C1-C4);",
               "// see the generator's docstring.  Source patterns per entry are noted in comments."]
-    shards = [header + ['#include "kernels.cuh"', "", "namespace disc_gen {", "using namespace disc_dev;", ""]
+    shards = [header + ['#include "kernels.cuh"', "", "#ifndef DISC_ROWX_CH", "#define DISC_ROWX_CH 2", "#endif", "",
+                        "namespace disc_gen {", "using namespace disc_dev;", ""]
               for _ in range(SHARDS)]
     entries = []
     for n, ((kind, key), (rec, src_name)) in enumerate(sorted(seen.items())):
@@ -179,7 +182,13 @@ def generate():
         if kind == "row":
             parts.append(gen_program(f"Post_{tag}", rec["post"], ch, early_splat=False))
         parts.append(f"cudaError_t launch_{tag}(const void* l, int vec, cudaStream_t s, const HostGroup* g) {{")
-        parts.append(f"  constexpr int kGenCH = {ch};")
+        trans = any(I_UN <= c[0] < I_UN + 4 for p_ in ("pre", "post") for c in rec.get(p_, {}).get("code", []))
+        if kind == "row" and trans and ch > 1:
+            # transcendental row programs: fewer chunks in flight per thread (register
+            # pressure under the 64-register cap spills the f64 accumulators)
+            parts.append(f"  constexpr int kGenCH = DISC_ROWX_CH < {ch} ? DISC_ROWX_CH : {ch};")
+        else:
+            parts.append(f"  constexpr int kGenCH = {ch};")
         if kind == "loop":
             parts.append("  const auto& L = *static_cast<const disc_loop_launch*>(l);")
             parts.append(f"  return loop_pass<Pre_{tag}, kGenCH, false>(L, s, false, g);")
