@@ -836,20 +836,28 @@ inline cudaError_t launch_col_group(K kernel, const HostGroup& H, cudaStream_t s
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// Scalar (VEC=1) instantiations keep as many bytes in flight per thread as the float4
+// ones: DISC_VEC1_CH_SCALE x the chunks (capped at 8).
+#ifndef DISC_VEC1_CH_SCALE
+#define DISC_VEC1_CH_SCALE 1  // A/B: 4 (CH 8 at VEC=1) is 1.4-2.8x slower on odd-width softmax rows
+#endif
+constexpr int vec1_ch(int ch) { return ch * DISC_VEC1_CH_SCALE < 8 ? ch * DISC_VEC1_CH_SCALE : (ch > 8 ? ch : 8); }
+
 template <typename Prog, int CH = kCH, bool ALLOW_WIDE = true>
 inline cudaError_t loop_pass(const disc_loop_launch& L, cudaStream_t s, bool use_slots, const HostGroup* g) {
+  constexpr int C1 = vec1_ch(CH);
   if (g) {
     if constexpr (ALLOW_WIDE)
       if (L.wide) return L.vec == 4 ? launch_loop_group<CH>(k_loop_g<4, true, Prog, CH>, *g, s, use_slots)
-                                    : launch_loop_group<CH>(k_loop_g<1, true, Prog, CH>, *g, s, use_slots);
+                                    : launch_loop_group<C1>(k_loop_g<1, true, Prog, C1>, *g, s, use_slots);
     return L.vec == 4 ? launch_loop_group<CH>(k_loop_g<4, false, Prog, CH>, *g, s, use_slots)
-                      : launch_loop_group<CH>(k_loop_g<1, false, Prog, CH>, *g, s, use_slots);
+                      : launch_loop_group<C1>(k_loop_g<1, false, Prog, C1>, *g, s, use_slots);
   }
   if constexpr (ALLOW_WIDE)
     if (L.wide) return L.vec == 4 ? launch_loop_with<CH>(k_loop<4, true, Prog, CH>, L, s, use_slots)
-                                  : launch_loop_with<CH>(k_loop<1, true, Prog, CH>, L, s, use_slots);
+                                  : launch_loop_with<C1>(k_loop<1, true, Prog, C1>, L, s, use_slots);
   return L.vec == 4 ? launch_loop_with<CH>(k_loop<4, false, Prog, CH>, L, s, use_slots)
-                    : launch_loop_with<CH>(k_loop<1, false, Prog, CH>, L, s, use_slots);
+                    : launch_loop_with<C1>(k_loop<1, false, Prog, C1>, L, s, use_slots);
 }
 
 // Dispatch on (vec, wide, reduce kind) for a given program functor pair.
@@ -858,15 +866,16 @@ inline cudaError_t loop_pass(const disc_loop_launch& L, cudaStream_t s, bool use
 template <typename Pre, typename Post, int CH = kCH, bool ALLOW_WIDE = true>
 inline cudaError_t row_pass(const disc_reduce_launch& L, cudaStream_t s, bool use_slots, const HostGroup* g = nullptr) {
   const bool sum = L.kind == DISC_REDUCE_SUM;
-#define DISC_ROW(V, W, ST)                                                                                   \
-  (g ? (sum ? launch_row_group<CH>(k_row_g<V, W, DISC_REDUCE_SUM, Pre, Post, CH, ST>, *g, s, use_slots)      \
-            : launch_row_group<CH>(k_row_g<V, W, DISC_REDUCE_MAX, Pre, Post, CH, ST>, *g, s, use_slots))     \
-     : (sum ? launch_row_with<CH>(k_row<V, W, DISC_REDUCE_SUM, Pre, Post, CH, ST>, L, s, use_slots)          \
-            : launch_row_with<CH>(k_row<V, W, DISC_REDUCE_MAX, Pre, Post, CH, ST>, L, s, use_slots)))
+  constexpr int C1 = vec1_ch(CH);
+#define DISC_ROW(V, W, ST, C)                                                                                \
+  (g ? (sum ? launch_row_group<C>(k_row_g<V, W, DISC_REDUCE_SUM, Pre, Post, C, ST>, *g, s, use_slots)        \
+            : launch_row_group<C>(k_row_g<V, W, DISC_REDUCE_MAX, Pre, Post, C, ST>, *g, s, use_slots))       \
+     : (sum ? launch_row_with<C>(k_row<V, W, DISC_REDUCE_SUM, Pre, Post, C, ST>, L, s, use_slots)            \
+            : launch_row_with<C>(k_row<V, W, DISC_REDUCE_MAX, Pre, Post, C, ST>, L, s, use_slots)))
   if constexpr (ALLOW_WIDE)
-    if (L.wide) return L.vec == 4 ? DISC_ROW(4, true, false) : DISC_ROW(1, true, false);
-  if (L.stage) return L.vec == 4 ? DISC_ROW(4, false, true) : DISC_ROW(1, false, true);
-  return L.vec == 4 ? DISC_ROW(4, false, false) : DISC_ROW(1, false, false);
+    if (L.wide) return L.vec == 4 ? DISC_ROW(4, true, false, CH) : DISC_ROW(1, true, false, C1);
+  if (L.stage) return L.vec == 4 ? DISC_ROW(4, false, true, CH) : DISC_ROW(1, false, true, CH);
+  return L.vec == 4 ? DISC_ROW(4, false, false, CH) : DISC_ROW(1, false, false, C1);
 #undef DISC_ROW
 }
 
