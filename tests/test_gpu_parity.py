@@ -359,3 +359,23 @@ def test_generated_kernels_match_interpreter(gpu):
             np.testing.assert_array_equal(a, b)
         want, _, _ = O.Executor().run(plan.to_json(), inputs)
         check_outputs(fast, want)
+
+
+def test_transcendental_accuracy(gpu):
+    """exp/tanh on the device against float64 numpy over a dense argument sweep (incl.
+    subnormal/tiny, large and saturating arguments): tanh within 4e-7 absolute (the
+    MUFU-based formulation, program.cuh tanh_fast), exp within 2 ulp-relative."""
+    for op, ref_fn, tol in (("Tanh", np.tanh, 4e-7), ("Exp", np.exp, 2.5e-7)):
+        g = json.dumps({"name": "t", "inputs": [{"id": "x", "shape": ["N"]}], "outputs": ["y"],
+                        "nodes": [{"id": "y", "op": op, "inputs": ["x"]}]})
+        lim = 20.0 if op == "Tanh" else 80.0
+        x = np.concatenate([np.linspace(-lim, lim, 2_000_003, dtype=np.float32),
+                            np.float32(1e-30) * np.arange(-50, 50, dtype=np.float32),
+                            np.array([0.0, -0.0, 1e-7, -1e-7, 0.59999, 0.6, 0.60001, 9.0, 9.02, 88.0], np.float32)])
+        y = gpu.Executor().run(gpu.compile_graph(g), {"x": x}).outputs[0].astype(np.float64)
+        want = ref_fn(x.astype(np.float64))
+        err = np.abs(y - want) / np.maximum(1.0, np.abs(want)) if op == "Tanh" else np.abs(y - want) / np.abs(want)
+        assert float(err.max()) <= tol, (op, float(err.max()), float(x[np.argmax(err)]))
+        if op == "Tanh":  # tiny arguments are returned exactly (sign and value)
+            tiny = np.abs(x) < 2.44140625e-4
+            np.testing.assert_array_equal(y[tiny], x[tiny].astype(np.float64))
