@@ -162,7 +162,9 @@ def generate():
     header = ["// GENERATED by tools/gen_patterns.py -- do not edit.",
               "// Straight-line fused programs for the pattern library (fixtures + BASELINE configs C1-C4);",
               "// see the generator's docstring.  Source patterns per entry are noted in comments."]
-    shards = [header + ['#include "kernels.cuh"', "", "#ifndef DISC_ROWX_CH", "#define DISC_ROWX_CH 2", "#endif", "",
+    shards = [header + ['#include "kernels.cuh"', "", "#ifndef DISC_ROWX_CH", "#define DISC_ROWX_CH 2", "#endif",
+                        "#ifndef DISC_ROW_READ_CH", "#define DISC_ROW_READ_CH 2", "#endif",
+                        "#ifndef DISC_ROW_MAX_CH", "#define DISC_ROW_MAX_CH 2", "#endif", "",
                         "namespace disc_gen {", "using namespace disc_dev;", ""]
               for _ in range(SHARDS)]
     entries = []
@@ -183,10 +185,16 @@ def generate():
             parts.append(gen_program(f"Post_{tag}", rec["post"], ch, early_splat=False))
         parts.append(f"cudaError_t launch_{tag}(const void* l, int vec, cudaStream_t s, const HostGroup* g) {{")
         trans = any(I_UN <= c[0] < I_UN + 4 for p_ in ("pre", "post") for c in rec.get(p_, {}).get("code", []))
-        if kind == "row" and trans and ch > 1:
+        trivial = kind == "row" and len(rec["pre"]["code"]) <= 1 and not rec.get("post", {}).get("code")
+        if trivial:
+            # a plain row reduce of one input (read-only stream): more loads in flight
+            parts.append(f"  constexpr int kGenCH = DISC_ROW_READ_CH;")
+        elif kind == "row" and trans and ch > 1:
             # transcendental row programs: fewer chunks in flight per thread (register
             # pressure under the 64-register cap spills the f64 accumulators)
             parts.append(f"  constexpr int kGenCH = DISC_ROWX_CH < {ch} ? DISC_ROWX_CH : {ch};")
+        elif kind == "row" and ch > 1:
+            parts.append(f"  constexpr int kGenCH = DISC_ROW_MAX_CH < {ch} ? DISC_ROW_MAX_CH : {ch};")
         else:
             parts.append(f"  constexpr int kGenCH = {ch};")
         if kind == "loop":
