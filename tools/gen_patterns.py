@@ -164,7 +164,8 @@ def generate():
               "// see the generator's docstring.  Source patterns per entry are noted in comments."]
     shards = [header + ['#include "kernels.cuh"', "", "#ifndef DISC_ROWX_CH", "#define DISC_ROWX_CH 2", "#endif",
                         "#ifndef DISC_ROW_READ_CH", "#define DISC_ROW_READ_CH 2", "#endif",
-                        "#ifndef DISC_ROW_MAX_CH", "#define DISC_ROW_MAX_CH 2", "#endif", "",
+                        "#ifndef DISC_ROW_MAX_CH", "#define DISC_ROW_MAX_CH 2", "#endif",
+                        "#ifndef DISC_COL_MAX_CH", "#define DISC_COL_MAX_CH 4", "#endif", "",
                         "namespace disc_gen {", "using namespace disc_dev;", ""]
               for _ in range(SHARDS)]
     entries = []
@@ -195,6 +196,8 @@ def generate():
             parts.append(f"  constexpr int kGenCH = DISC_ROWX_CH < {ch} ? DISC_ROWX_CH : {ch};")
         elif kind == "row" and ch > 1:
             parts.append(f"  constexpr int kGenCH = DISC_ROW_MAX_CH < {ch} ? DISC_ROW_MAX_CH : {ch};")
+        elif kind == "col" and ch > 1:
+            parts.append(f"  constexpr int kGenCH = DISC_COL_MAX_CH < {ch} ? DISC_COL_MAX_CH : {ch};")
         else:
             parts.append(f"  constexpr int kGenCH = {ch};")
         if kind == "loop":
