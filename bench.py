@@ -233,10 +233,14 @@ def ncu_traffic(schedule):
     if not os.path.exists(p):
         return None
     try:
-        j = json.load(open(p))
-        return j.get("traffic_per_launch", {}).get(schedule)
+        t = json.load(open(p)).get("traffic_per_launch", {})
     except Exception:
         return None
+    while schedule:  # "group:row_fused_cached" -> "group:row_fused" -> "group:row"
+        if schedule in t:
+            return t[schedule]
+        schedule = schedule.rsplit("_", 1)[0] if "_" in schedule else ""
+    return None
 
 
 def dist_setup(args):

@@ -30,6 +30,16 @@ SCRATCH = os.path.join(ROOT, "gpurun_out")
 
 def schedule_of(name):
     """bench.py schedule label of a kernel name (roofline.kernel uses these)."""
+    if "k_loop_g<4" in name:
+        return "group:loop_v4"
+    if "k_loop_g<" in name:
+        return "group:loop"
+    if "k_row_g<" in name:
+        return "group:row_staged" if name.rstrip(")").split(",")[-1].strip().startswith("true") else "group:row"
+    if "k_col_finalize_g" in name:
+        return "group:col_finalize"
+    if "k_col_g<" in name:
+        return "group:col"
     if name.startswith("void disc_dev::k_loop<4") or name.startswith("void k_loop<4"):
         return "loop_v4"
     if "k_loop<" in name:
@@ -63,7 +73,7 @@ def main(tag):
         p[2] += v.get("dram__bytes_read.sum", 0.0) + v.get("dram__bytes_write.sum", 0.0)
     ours = {n: p for n, p in per.items() if "disc_dev" in n or n.startswith("void k_") or "k_col_finalize" in n}
     total_ns = sum(p[1] for p in ours.values())
-    lines = [f"# {tag}: ncu launch list of `python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e`",
+    lines = [f"# {tag}: ncu launch list of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e`",
              "# (--metrics gpu__time_duration.sum,dram__bytes_{read,write}.sum --clock-control none; cold-cache,",
              "#  serialised launches: shares are comparable with the bench, absolute times are not)",
              f"# {sum(p[0] for p in per.values())} launches, {sum(p[0] for p in ours.values())} of them disc kernels",
@@ -82,16 +92,19 @@ def main(tag):
 
     fulls = {}
     for fn in sorted(os.listdir(SCRATCH)):
-        m = re.match(rf"full_{tag}_(\w+)\.ncu-rep$", fn)
-        if not m:
+        m = re.match(rf"full_{tag}_(\w+)\.(ncu-rep|txt)$", fn)
+        if not m or (m.group(2) == "ncu-rep" and os.path.exists(os.path.join(SCRATCH, f"full_{tag}_{m.group(1)}.txt"))):
             continue
-        text = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), os.path.join(SCRATCH, fn),
-                               "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
-                               "sm__throughput.avg.pct_of_peak_sustained_elapsed"],
-                              capture_output=True, text=True).stdout
+        if m.group(2) == "txt":  # summarised on the GPU box (tools/profile_round.sh)
+            text = open(os.path.join(SCRATCH, fn)).read()
+        else:
+            text = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"),
+                                   os.path.join(SCRATCH, fn), "dram__bytes_read.sum", "dram__bytes_write.sum",
+                                   "smsp__inst_executed.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed"],
+                                  capture_output=True, text=True).stdout
         with open(os.path.join(OUT, f"{tag}_full_{m.group(1)}.txt"), "w") as f:
-            f.write(f"# {tag}: ncu --set full --import-source on --clock-control none, tools/profile_one.py "
-                    f"({m.group(1)}, see tools/profile_round.sh for the shape)\n" + text)
+            f.write(f"# {tag}: ncu --set full --import-source on --clock-control none of the grouped kernels of one "
+                    f"pass of the {m.group(1)} sweep (tools/profile_grouped.py, see tools/profile_round.sh)\n" + text)
         fulls[m.group(1)] = fn
     summary = {"round": tag,
                "traffic_per_launch": {s: round(b / n) for s, (b, n) in traffic.items()},
