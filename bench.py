@@ -254,15 +254,23 @@ def dist_setup(args):
         if args.impl == "reference":
             dist.init_process_group("gloo")
         else:
+            # BENCH_DEVICES_OVERRIDE=1: ranks share the visible GPUs round-robin over gloo
+            # (exercises the multi-rank path on a 1-GPU box; not a scaling measurement)
+            if os.environ.get("BENCH_DEVICES_OVERRIDE"):
+                local = local % max(1, torch.cuda.device_count())
             torch.cuda.set_device(local)
-            dist.init_process_group("nccl")
+            dist.init_process_group("gloo" if os.environ.get("BENCH_DEVICES_OVERRIDE") else "nccl")
     return world, rank, local, dist
+
+
+def _dev(dist, local):
+    return "cpu" if dist is not None and dist.get_backend() == "gloo" else f"cuda:{local}"
 
 
 def barrier(dist, local):
     if dist is not None:
         import torch
-        t = torch.zeros(1, device=f"cuda:{local}")
+        t = torch.zeros(1, device=_dev(dist, local))
         dist.all_reduce(t)
         torch.cuda.synchronize()
 
@@ -271,7 +279,7 @@ def allreduce(dist, local, v, op="max"):
     if dist is None:
         return v
     import torch
-    t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([v], dtype=torch.float64, device=_dev(dist, local))
     dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return float(t.item())
 
