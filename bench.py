@@ -398,6 +398,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--schedule", default="auto")
     ap.add_argument("--e2e-pipes", type=int, default=3, help="executors/streams the e2e pass alternates over")
+    ap.add_argument("--e2e-chunk-mb", type=int, default=256,
+                    help="grouped e2e: boundary bytes per disc_executor_run_grouped call")
     ap.add_argument("--mode", default="grouped", choices=["grouped", "streams"],
                     help="grouped: one disc_executor_run_grouped call per step (the same plan kernel of all "
                          "requests fused into one grouped launch); streams: per-request launches interleaved "
@@ -578,7 +580,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         e2e = measure_e2e(D, graphs, plans, my_reqs, [costs[i] for i in mine], local, stream, pipes=args.e2e_pipes,
-                          grouped=args.mode == "grouped")
+                          grouped=args.mode == "grouped", chunk_bytes=args.e2e_chunk_mb << 20)
         if e2e is not None and dist is not None:
             e2e["value"] = round(allreduce(dist, local, e2e["bytes"], "sum") /
                                  allreduce(dist, local, e2e["seconds"], "max") / 1e9, 2)

@@ -201,7 +201,9 @@ int disc_cuda_malloc(size_t bytes, void* stream, void** dptr);   /* stream-order
 int disc_cuda_free(void* dptr, void* stream);
 int disc_cuda_host_alloc(size_t bytes, void** hptr);             /* pinned */
 int disc_cuda_host_free(void* hptr);
-/* kind: 0 h2d, 1 d2h, 2 d2d, 3 default (UVA) */
+/* kind: 0 h2d, 1 d2h, 2 d2d, 3 default (UVA); | DISC_MEMCPY_NOW issues the copy even while
+ * this thread queues work for `stream` (it then precedes every queued op). */
+#define DISC_MEMCPY_NOW 4
 int disc_cuda_memcpy(void* dst, const void* src, size_t bytes, int kind, void* stream);
 int disc_cuda_memset(void* dst, int value, size_t bytes, void* stream);
 

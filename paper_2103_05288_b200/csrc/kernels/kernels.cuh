@@ -11,6 +11,7 @@
 #include <type_traits>
 
 #include "program.cuh"
+#include "../desc_ranges.hpp"
 
 namespace disc_dev {
 
@@ -112,6 +113,13 @@ struct disc_group {
   int32_t block_off[DISC_MAX_GROUP + 1];
 };
 
+// Item of a grouped 2-D copy (reshape copies, concat parts): rows x cols floats.
+struct disc_copy2d {
+  const float* src;
+  float* dst;
+  int64_t rows, cols, src_ld, dst_ld;
+};
+
 __device__ __forceinline__ int group_of(const disc_group& G, int b) {
   int lo = 0, hi = G.n;  // block_off[lo] <= b < block_off[hi]
   while (hi - lo > 1) {
@@ -140,40 +148,38 @@ __device__ __forceinline__ const Launch& group_stage(const disc_group& G, int g,
   return *reinterpret_cast<const Launch*>(buf);
 }
 
-// Host: the staged ranges of a group's descriptors (from its first member; members of a
-// generated group share n_loads / n_outs; interpreter groups stage whole programs).
-namespace detail {
-inline void seg_add(disc_group& G, size_t begin, size_t end) {
-  const int o = static_cast<int>(begin / 16), e = static_cast<int>((end + 15) / 16);
-  if (G.nseg > 0 && G.seg[G.nseg - 1][0] + G.seg[G.nseg - 1][1] >= o) {  // merge adjacent
-    const int s0 = G.seg[G.nseg - 1][0];
-    G.seg[G.nseg - 1][1] = static_cast<uint16_t>(std::max(e, s0 + G.seg[G.nseg - 1][1]) - s0);
-    return;
-  }
-  G.seg[G.nseg][0] = static_cast<uint16_t>(o);
-  G.seg[G.nseg][1] = static_cast<uint16_t>(e - o);
-  ++G.nseg;
+// Host: the staged ranges of a group's descriptors (desc_ranges.hpp): the union over the
+// members -- their used prefixes -- so interpreter groups, whose members may differ in
+// program length, stage every member's instructions and loads.
+inline void max_counts(disc_program& m, const disc_program& p) {
+  m.n_instr = std::max(m.n_instr, p.n_instr);
+  m.n_loads = std::max(m.n_loads, p.n_loads);
 }
-inline void seg_program(disc_group& G, size_t base, const disc_program& P, bool whole) {
-  if (whole) {
-    seg_add(G, base, base + sizeof(disc_program));
-    return;
-  }
-  seg_add(G, base, base + offsetof(disc_program, code));
-  seg_add(G, base + offsetof(disc_program, loads), base + offsetof(disc_program, loads) + P.n_loads * sizeof(disc_load));
-  seg_add(G, base + offsetof(disc_program, outs), base + sizeof(disc_program));
+inline void group_counts(disc_loop_launch& m, const disc_loop_launch& L) { max_counts(m.prog, L.prog); }
+inline void group_counts(disc_reduce_launch& m, const disc_reduce_launch& L) {
+  max_counts(m.pre, L.pre);
+  max_counts(m.post, L.post);
 }
-}  // namespace detail
-inline void group_segments(disc_group& G, const disc_loop_launch& L, bool whole) {
+template <typename Launch, typename HG>
+inline void group_segments(disc_group& G, const HG& H) {
+  Launch m;
+  disc_desc::copy_used(&m, H.template at<Launch>(0));
+  for (int i = 1; i < H.n; ++i) group_counts(m, H.template at<Launch>(i));
+  disc_desc::Range r[disc_desc::kMaxRanges];
+  const int n = disc_desc::ranges(m, r);
   G.nseg = 0;
-  detail::seg_program(G, offsetof(disc_loop_launch, prog), L.prog, whole);
-  detail::seg_add(G, offsetof(disc_loop_launch, prog) + sizeof(disc_program), sizeof(disc_loop_launch));
-}
-inline void group_segments(disc_group& G, const disc_reduce_launch& L, bool whole) {
-  G.nseg = 0;
-  detail::seg_program(G, offsetof(disc_reduce_launch, pre), L.pre, whole);
-  detail::seg_program(G, offsetof(disc_reduce_launch, post), L.post, whole);
-  detail::seg_add(G, offsetof(disc_reduce_launch, post) + sizeof(disc_program), sizeof(disc_reduce_launch));
+  for (int i = 0; i < n; ++i) {
+    if (!r[i].len) continue;
+    const int o = static_cast<int>(r[i].off / 16), e = static_cast<int>((r[i].off + r[i].len + 15) / 16);
+    if (G.nseg > 0 && G.seg[G.nseg - 1][0] + G.seg[G.nseg - 1][1] >= o) {  // merge adjacent
+      const int s0 = G.seg[G.nseg - 1][0];
+      G.seg[G.nseg - 1][1] = static_cast<uint16_t>(std::max(e, s0 + G.seg[G.nseg - 1][1]) - s0);
+      continue;
+    }
+    G.seg[G.nseg][0] = static_cast<uint16_t>(o);
+    G.seg[G.nseg][1] = static_cast<uint16_t>(e - o);
+    ++G.nseg;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -772,7 +778,7 @@ inline cudaError_t launch_loop_group(K kernel, const HostGroup& H, cudaStream_t 
   G.table = H.dev_table;
   G.stride = H.stride;
   G.n = H.n;
-  group_segments(G, H.at<disc_loop_launch>(0), use_slots);
+  group_segments<disc_loop_launch>(G, H);
   size_t smem = 0;
   for (int i = 0; i < H.n; ++i) smem = std::max(smem, loop_smem<CH>(H.at<disc_loop_launch>(i), use_slots));
   cudaError_t e = set_smem(kernel, smem, kGroupSmemThreshold);
@@ -793,7 +799,7 @@ inline cudaError_t launch_row_group(K kernel, const HostGroup& H, cudaStream_t s
   G.table = H.dev_table;
   G.stride = H.stride;
   G.n = H.n;
-  group_segments(G, H.at<disc_reduce_launch>(0), use_slots);
+  group_segments<disc_reduce_launch>(G, H);
   size_t smem = 0;
   for (int i = 0; i < H.n; ++i) smem = std::max(smem, row_smem<CH>(H.at<disc_reduce_launch>(i), use_slots));
   const int block = row_block(H.at<disc_reduce_launch>(0));
@@ -818,7 +824,7 @@ inline cudaError_t launch_col_group(K kernel, const HostGroup& H, cudaStream_t s
   G.table = H.dev_table;
   G.stride = H.stride;
   G.n = H.n;
-  group_segments(G, H.at<disc_reduce_launch>(0), use_slots);
+  group_segments<disc_reduce_launch>(G, H);
   size_t smem = 0;
   int64_t off = 0;
   for (int i = 0; i < H.n; ++i) {

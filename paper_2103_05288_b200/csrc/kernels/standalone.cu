@@ -6,8 +6,36 @@
 #include <cstdint>
 
 #include "disc_cuda.h"
+#include "kernels.cuh"
 
 namespace disc_dev {
+
+// Grouped 2-D copies (request-queue flush, device.cu): reshape D2D copies and concat
+// parts of many requests in ONE launch.  Item g copies rows x cols floats from src (row
+// stride src_ld) to dst (row stride dst_ld); CTAs [block_off[g], block_off[g+1]) stride
+// over its float4 (or float) elements.
+__global__ void __launch_bounds__(256) k_copy2d_g(const __grid_constant__ disc_group G) {
+  const int b = blockIdx.x, g = group_of(G, b);
+  const disc_copy2d* items = reinterpret_cast<const disc_copy2d*>(G.table);
+  const disc_copy2d it = items[g];
+  const int lb = b - G.block_off[g], nb = G.block_off[g + 1] - G.block_off[g];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const bool v4 = ((it.cols | it.src_ld | it.dst_ld) & 3) == 0 &&
+                  ((reinterpret_cast<uintptr_t>(it.src) | reinterpret_cast<uintptr_t>(it.dst)) & 15) == 0;
+  if (v4) {
+    const int64_t c4 = it.cols >> 2, n = it.rows * c4;
+    for (int64_t f = static_cast<int64_t>(lb) * blockDim.x + threadIdx.x; f < n; f += static_cast<int64_t>(nb) * blockDim.x) {
+      const int64_t r = it.rows == 1 ? 0 : f / c4, c = f - r * c4;
+      reinterpret_cast<float4*>(it.dst + r * it.dst_ld)[c] = __ldg(reinterpret_cast<const float4*>(it.src + r * it.src_ld) + c);
+    }
+  } else {
+    const int64_t n = it.rows * it.cols;
+    for (int64_t f = static_cast<int64_t>(lb) * blockDim.x + threadIdx.x; f < n; f += static_cast<int64_t>(nb) * blockDim.x) {
+      const int64_t r = it.rows == 1 ? 0 : f / it.cols, c = f - r * it.cols;
+      it.dst[r * it.dst_ld + c] = __ldg(it.src + r * it.src_ld + c);
+    }
+  }
+}
 
 __global__ void __launch_bounds__(256) k_pad(const __grid_constant__ disc_pad_launch P) {
   for (int64_t f = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; f < P.total;
@@ -138,6 +166,26 @@ cudaError_t concat(const disc_concat_launch& C, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
   k_concat<<<grid_for(total, 256, 148 * 16), 256, 0, s>>>(C);
   return cudaGetLastError();
+}
+
+// Grouped copies: the table (H.dev_table) holds H.n disc_copy2d items.
+cudaError_t copy2d_group(const HostGroup& H, cudaStream_t s) {
+  disc_group G;
+  G.table = H.dev_table;
+  G.stride = H.stride;
+  G.n = H.n;
+  G.nseg = 0;
+  int64_t off = 0;
+  for (int i = 0; i < H.n; ++i) {
+    const disc_copy2d& it = H.at<disc_copy2d>(i);
+    G.block_off[i] = static_cast<int32_t>(off);
+    const int64_t n = it.rows * it.cols;
+    if (n > 0) off += std::min<int64_t>((n + 4095) / 4096, 256);
+  }
+  G.block_off[H.n] = static_cast<int32_t>(off);
+  if (off == 0) return cudaSuccess;
+  const cudaError_t e = launch_k(k_copy2d_g, dim3(static_cast<unsigned>(off)), dim3(256), 0, s, G);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c, cudaStream_t s) {

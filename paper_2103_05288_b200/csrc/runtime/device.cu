@@ -7,6 +7,8 @@
 #include <cstring>
 #include <deque>
 #include <map>
+#include <memory>
+#include <type_traits>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -15,6 +17,7 @@
 
 #include "disc_cuda.h"
 #include "../kernels/kernels.cuh"
+#include "../desc_ranges.hpp"
 
 using disc_dev::HostGroup;
 
@@ -25,6 +28,7 @@ cudaError_t col_pass(const disc_reduce_launch& L, cudaStream_t s, const HostGrou
 cudaError_t finalize_columns(const disc_reduce_launch& L, cudaStream_t s, const HostGroup* g = nullptr);
 cudaError_t pad(const disc_pad_launch& P, cudaStream_t s);
 cudaError_t concat(const disc_concat_launch& C, cudaStream_t s);
+cudaError_t copy2d_group(const HostGroup& H, cudaStream_t s);
 cudaError_t gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c, cudaStream_t s);
 cudaError_t fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, cudaStream_t s);
 cudaError_t flush(void* p, size_t bytes, cudaStream_t s);
@@ -239,7 +243,15 @@ int issue_group(const GroupKey& k, const std::vector<const void*>& members, cuda
   Ring& r = g_rings[st];
   size_t off = 0;
   if (int rc = check(ring_reserve(r, stride * n, st, &off), "group table")) return rc;
-  for (int i = 0; i < n; ++i) std::memcpy(r.host + off + i * stride, members[i], size);
+  for (int i = 0; i < n; ++i) {  // only the byte ranges the kernels read (desc_ranges.hpp)
+    if (k.kind == 0)
+      disc_desc::copy_used(reinterpret_cast<disc_loop_launch*>(r.host + off + i * stride),
+                           *static_cast<const disc_loop_launch*>(members[i]));
+    else
+      disc_desc::copy_used(reinterpret_cast<disc_reduce_launch*>(r.host + off + i * stride),
+                           *static_cast<const disc_reduce_launch*>(members[i]));
+  }
+  (void)size;
   if (int rc = check(cudaMemcpyAsync(r.dev + off, r.host + off, stride * n, cudaMemcpyHostToDevice, st), "group table upload"))
     return rc;
   const HostGroup H{r.dev + off, r.host + off, static_cast<int>(stride), n};
@@ -267,6 +279,36 @@ int issue_group(const GroupKey& k, const std::vector<const void*>& members, cuda
   if (rc) return rc;
   g_spec_launches.fetch_add(k.entry ? n : 0, std::memory_order_relaxed);
   return check(ring_release(r, off, stride * n, st), "group table release");
+}
+
+// Issues D2D copy items (reshape copies, concat parts) as grouped copy kernels.
+int issue_copies(const std::vector<disc_dev::disc_copy2d>& items, cudaStream_t st) {
+  for (size_t i0 = 0; i0 < items.size(); i0 += DISC_MAX_GROUP) {
+    const int n = static_cast<int>(std::min<size_t>(items.size() - i0, DISC_MAX_GROUP));
+    const size_t bytes = sizeof(disc_dev::disc_copy2d) * n;
+    std::lock_guard<std::mutex> lock(g_ring_mu);
+    Ring& r = g_rings[st];
+    size_t off = 0;
+    if (int rc = check(ring_reserve(r, bytes, st, &off), "copy table")) return rc;
+    std::memcpy(r.host + off, items.data() + i0, bytes);
+    if (int rc = check(cudaMemcpyAsync(r.dev + off, r.host + off, bytes, cudaMemcpyHostToDevice, st), "copy table upload"))
+      return rc;
+    const HostGroup H{r.dev + off, r.host + off, static_cast<int>(sizeof(disc_dev::disc_copy2d)), n};
+    if (int rc = counted(disc_launch::copy2d_group(H, st), "grouped copy")) return rc;
+    if (int rc = check(ring_release(r, off, bytes, st), "copy table release")) return rc;
+  }
+  return 0;
+}
+
+// Concat (eval_concat) as one 2-D copy per part.
+void concat_items(const disc_concat_launch& C, std::vector<disc_dev::disc_copy2d>& out) {
+  int64_t a = C.axis_offset;
+  for (int p = 0; p < C.n_parts; ++p) {
+    const int64_t cols = C.part_axis[p] * C.inner;
+    if (C.outer > 0 && cols > 0)
+      out.push_back({C.parts[p], C.out + a * C.inner, C.outer, cols, cols, C.axis_total * C.inner});
+    a += C.part_axis[p];
+  }
 }
 
 // Splits n launches of one kind into homogeneous groups and issues each (largest first).
@@ -333,10 +375,30 @@ struct QRecord {
   cudaEvent_t a = nullptr, b = nullptr;
   float ms = 0.f;
 };
+// Growable byte arena without zero-fill (descriptors are copied in by used ranges).
+struct Arena {
+  std::unique_ptr<unsigned char[]> buf;
+  size_t cap = 0, used = 0;
+  unsigned char* data() { return buf.get(); }
+  void clear() { used = 0; }
+  size_t take(size_t n) {  // 16 B aligned offset of n fresh bytes
+    const size_t off = (used + 15) / 16 * 16;
+    if (off + n > cap) {
+      const size_t nc = std::max(off + n, 2 * cap + (size_t{1} << 20));
+      std::unique_ptr<unsigned char[]> nb(new unsigned char[nc]);
+      if (used) std::memcpy(nb.get(), buf.get(), used);
+      buf = std::move(nb);
+      cap = nc;
+    }
+    used = off + n;
+    return off;
+  }
+};
+
 struct Queue {
   bool active = false;
   cudaStream_t stream = nullptr;
-  std::vector<unsigned char> arena;
+  Arena arena;
   std::vector<std::vector<QOp>> reqs;
   size_t mark_from = 0;
   std::vector<void*> frees;
@@ -352,9 +414,11 @@ bool queued(void* stream) { return t_q.active && S(stream) == t_q.stream; }
 template <typename T>
 void enqueue(int kind, const T& payload) {
   if (t_q.reqs.empty()) t_q.reqs.emplace_back();
-  const size_t off = (t_q.arena.size() + 15) / 16 * 16;
-  t_q.arena.resize(off + sizeof(T));
-  std::memcpy(t_q.arena.data() + off, &payload, sizeof(T));
+  const size_t off = t_q.arena.take(sizeof(T));
+  if constexpr (std::is_same<T, disc_loop_launch>::value || std::is_same<T, disc_reduce_launch>::value)
+    disc_desc::copy_used(reinterpret_cast<T*>(t_q.arena.data() + off), payload);
+  else
+    std::memcpy(t_q.arena.data() + off, &payload, sizeof(T));
   t_q.reqs.back().push_back({kind, off});
 }
 
@@ -434,7 +498,7 @@ int disc_cuda_host_free(void* hptr) { return check(cudaFreeHost(hptr), "cudaFree
 
 int disc_cuda_memcpy(void* dst, const void* src, size_t bytes, int kind, void* stream) {
   if (!bytes || g_capture) return 0;
-  if (queued(stream)) {
+  if (queued(stream) && !(kind & DISC_MEMCPY_NOW)) {
     enqueue(kQMemcpy, QMemcpy{dst, src, bytes, kind});
     return 0;
   }
@@ -658,12 +722,27 @@ int disc_cuda_queue_flush(int timing) {
   for (size_t lv = 0; lv < levels && !rc; ++lv) {
     // fused launches of this level, by kind; everything else issued in request order
     std::vector<const QOp*> fused[2];
+    std::vector<disc_dev::disc_copy2d> copies;  // D2D copies and concats of this level
+    int64_t copy_bytes = 0;
     for (const auto& r : t_q.reqs) {
       if (lv >= r.size()) continue;
       const QOp& op = r[lv];
       const void* p = A + op.off;
       if (op.kind == kQLoop || op.kind == kQReduce) {
         fused[op.kind == kQLoop ? 0 : 1].push_back(&op);
+        continue;
+      }
+      if (op.kind == kQConcat ||
+          (op.kind == kQMemcpy && (static_cast<const QMemcpy*>(p)->kind & 3) == 2 &&
+           static_cast<const QMemcpy*>(p)->bytes % 4 == 0)) {
+        if (op.kind == kQConcat) {
+          concat_items(*static_cast<const disc_concat_launch*>(p), copies);
+        } else {
+          const auto& c = *static_cast<const QMemcpy*>(p);
+          const int64_t n = static_cast<int64_t>(c.bytes / 4);
+          copies.push_back({static_cast<const float*>(c.src), static_cast<float*>(c.dst), 1, n, n, n});
+        }
+        copy_bytes += op.bytes;
         continue;
       }
       begin_rec(static_cast<int>(lv), 1, op.bytes, op.kernel, op.sched);
@@ -692,6 +771,18 @@ int disc_cuda_queue_flush(int timing) {
       }
       end_rec();
       if (rc) break;
+    }
+    if (!rc && !copies.empty()) {
+      int copy_name = -1;
+      for (size_t i = 0; i < t_q.names.size(); ++i)
+        if (t_q.names[i] == "copy") copy_name = static_cast<int>(i);
+      if (copy_name < 0) {
+        t_q.names.push_back("copy");
+        copy_name = static_cast<int>(t_q.names.size()) - 1;
+      }
+      begin_rec(static_cast<int>(lv), static_cast<int>(copies.size()), copy_bytes, -1, copy_name);
+      rc = issue_copies(copies, st);
+      end_rec();
     }
     for (int kind = 0; kind < 2 && !rc; ++kind) {
       if (fused[kind].empty()) continue;

@@ -1,6 +1,8 @@
 // Tape -> device program binding and schedule selection (see launcher.hpp).
 #include "launcher.hpp"
 
+#include "../desc_ranges.hpp"
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -1383,11 +1385,13 @@ void replay(const Recipe& r, const std::vector<DevTensor>& ext, const std::vecto
   size_t li = 0, ri = 0;
   for (int step = 0; step < r.steps; ++step) {
     if (li < r.loops.size() && r.loops[li].first == step) {
-      disc_loop_launch L = *r.loops[li++].second;
+      disc_loop_launch L;  // only the used byte ranges are copied (desc_ranges.hpp)
+      disc_desc::copy_used(&L, *r.loops[li++].second);
       patch.program(L.prog);
       cuda_ok(disc_cuda_launch_loop(&L, stream), "fused loop");
     } else {
-      disc_reduce_launch R = *r.reduces[ri++].second;
+      disc_reduce_launch R;
+      disc_desc::copy_used(&R, *r.reduces[ri++].second);
       patch.program(R.pre);
       patch.program(R.post);
       patch(R.red_out);

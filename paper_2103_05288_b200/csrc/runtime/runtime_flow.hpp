@@ -3,6 +3,7 @@
 // ExecStats and BufferEvents follow the reference Executor::run (executor.cpp:221-465).
 #pragma once
 
+#include <chrono>
 #include <map>
 #include <memory>
 #include <string>
@@ -150,6 +151,18 @@ class DeviceExecutor {
   bool grouped_ = false;
   bool group_timing_ = false;
   bool records_grouped_ = false;  // records_ describe grouped launches
+  std::chrono::steady_clock::time_point t_group_;
+  // grouped calls: small host inputs packed into one pinned arena (one H2D per group)
+  static constexpr int64_t kSmallInput = 64 << 10;
+  struct SmallChunk {
+    void* host = nullptr;   // pinned
+    void* dev = nullptr;
+    int64_t cap = 0, used = 0;
+    void* event = nullptr;  // after the chunk's H2D copy
+    bool pending = false;
+  };
+  std::vector<SmallChunk> small_;
+  size_t small_cur_ = 0;
   int request_ = -1;
   std::vector<std::vector<OutputView>> req_outputs_;
   std::vector<ExecStats> req_stats_;
