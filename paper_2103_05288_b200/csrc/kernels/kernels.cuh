@@ -31,6 +31,7 @@ __device__ __forceinline__ void pdl_enter(const disc_program& P) {
 struct Interp {
   static constexpr bool kSplitFull = false;
   static constexpr int kPipe = 0;  // no load/compute split
+  static constexpr bool kXuHeavy = false;
   template <int VEC, int CH, typename Ctx>
   __device__ __forceinline__ static void prefetch(const disc_program&, const Ctx&) {}
   template <int VEC, int CH, bool WIDE, typename Ctx>
@@ -75,6 +76,46 @@ struct Red {
   __device__ __forceinline__ static Acc acc(Acc a, float v) { return step(a, v); }
   __device__ __forceinline__ static Acc acc(Acc a, float4 v) { return step(step(step(step(a, v.x), v.y), v.z), v.w); }
 };
+
+// Per-thread partial accumulator of a reduce pass.  Default: the Red accumulator (f64
+// sum: one f32->f64 conversion + DADD per element).  COMP (programs heavy on the XU pipe,
+// which also executes the f32->f64 conversions, e.g. tanh/exp prologues): a compensated
+// f32 pair (Knuth TwoSum, error <= eps|sum| + O(n eps^2) sum|v|, i.e. f64-grade for these
+// lengths) on the FMA pipe, converted to f64 once when the pass ends.
+#ifndef DISC_COMP_SUM
+#define DISC_COMP_SUM 0  // A/B on B200: no gain on the tanh column reduce, -3% softmax
+#endif
+template <int KIND, bool COMP>
+struct PartAcc {
+  using RD = Red<KIND>;
+  using T = typename RD::Acc;
+  __device__ __forceinline__ static T identity() { return RD::identity(); }
+  __device__ __forceinline__ static T add(T a, float v) { return RD::step(a, v); }
+  __device__ __forceinline__ static T add(T a, float4 v) { return RD::acc(a, v); }
+  __device__ __forceinline__ static typename RD::Acc to(T a) { return a; }
+};
+struct F2 {
+  float s, c;
+};
+template <>
+struct PartAcc<DISC_REDUCE_SUM, true> {
+  using T = F2;
+  __device__ __forceinline__ static T identity() { return {0.f, 0.f}; }
+  __device__ __forceinline__ static T add(T a, float v) {
+    const float t = __fadd_rn(a.s, v);
+    const float bp = __fsub_rn(t, a.s);
+    const float ap = __fsub_rn(t, bp);
+    const float err = __fadd_rn(__fsub_rn(a.s, ap), __fsub_rn(v, bp));
+    return {t, __fadd_rn(a.c, err)};
+  }
+  __device__ __forceinline__ static T add(T a, float4 v) { return add(add(add(add(a, v.x), v.y), v.z), v.w); }
+  __device__ __forceinline__ static double to(T a) { return static_cast<double>(a.s) + static_cast<double>(a.c); }
+};
+template <typename Prog>
+constexpr bool comp_sum() {
+  if constexpr (DISC_COMP_SUM == 0) return false;
+  else return Prog::kXuHeavy;
+}
 
 // Chunks of a tile inside the row: CH chunks spaced cstride apart starting at col0.
 template <int CH>
@@ -367,9 +408,10 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
     const bool valid = base + sub < rows;
     // one accumulator per chunk position: CH independent f64 add chains per thread,
     // joined in a fixed order (deterministic)
-    Acc part[CH];
+    using PA = PartAcc<KIND, comp_sum<Pre>()>;
+    typename PA::T part[CH];
 #pragma unroll
-    for (int c = 0; c < CH; ++c) part[c] = RD::identity();
+    for (int c = 0; c < CH; ++c) part[c] = PA::identity();
     if constexpr (DISC_ROW_PIPE && Pre::kPipe > 0 && !STAGED) {
       // Software pipeline (generated programs): the next span's loads are issued before
       // the current span is evaluated and accumulated.
@@ -393,13 +435,13 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
             Pre::template run_loaded<VEC, CH, WIDE>(L.pre, Tile<I, true>{row, col0, R, cstride, CH, row_cache, sst}, cur, v,
                                                     slots, blockDim.x, consts[0], 0.f);
 #pragma unroll
-            for (int c = 0; c < CH; ++c) part[c] = RD::acc(part[c], v[c]);
+            for (int c = 0; c < CH; ++c) part[c] = PA::add(part[c], v[c]);
           } else {
             Pre::template run_loaded<VEC, CH, WIDE>(L.pre, Tile<I, false>{row, col0, R, cstride, nv, row_cache, sst}, cur, v,
                                                     slots, blockDim.x, consts[0], 0.f);
 #pragma unroll
             for (int c = 0; c < CH; ++c)
-              if (c < nv) part[c] = RD::acc(part[c], v[c]);
+              if (c < nv) part[c] = PA::add(part[c], v[c]);
           }
           if (L.arg_slot >= 0 && row_cache) {
 #pragma unroll
@@ -421,13 +463,13 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
           Pre::template run<VEC, CH, WIDE>(L.pre, Tile<I, true, false, STAGED>{row, col0, R, cstride, CH, row_cache, sst}, v, slots,
                                            blockDim.x, consts[0], 0.f);
 #pragma unroll
-          for (int c = 0; c < CH; ++c) part[c] = RD::acc(part[c], v[c]);
+          for (int c = 0; c < CH; ++c) part[c] = PA::add(part[c], v[c]);
         } else {
           Pre::template run<VEC, CH, WIDE>(L.pre, Tile<I, false, false, STAGED>{row, col0, R, cstride, nv, row_cache, sst}, v, slots,
                                            blockDim.x, consts[0], 0.f);
 #pragma unroll
           for (int c = 0; c < CH; ++c)
-            if (c < nv) part[c] = RD::acc(part[c], v[c]);
+            if (c < nv) part[c] = PA::add(part[c], v[c]);
         }
         if (arg_cache) {
 #pragma unroll
@@ -436,9 +478,9 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
         }
       }
     }
-    Acc acc = part[0];
+    Acc acc = PA::to(part[0]);
 #pragma unroll
-    for (int c = 1; c < CH; ++c) acc = RD::join(acc, part[c]);
+    for (int c = 1; c < CH; ++c) acc = RD::join(acc, PA::to(part[c]));
     const int width = G < 32 ? G : 32;
     for (int o = width / 2; o > 0; o >>= 1) acc = RD::join(acc, __shfl_xor_sync(0xffffffffu, acc, o, width));
     float result;
@@ -525,17 +567,18 @@ __device__ __forceinline__ void col_body(const disc_reduce_launch& L, const int 
   const int64_t r0 = static_cast<int64_t>(by) * per;
   const int64_t r1 = r0 + per < L.R ? r0 + per : L.R;
 
-  Acc acc[VEC];
+  using PA = PartAcc<KIND, comp_sum<Pre>()>;
+  typename PA::T acc[VEC];
 #pragma unroll
-  for (int i = 0; i < VEC; ++i) acc[i] = RD::identity();
+  for (int i = 0; i < VEC; ++i) acc[i] = PA::identity();
   auto add = [&](const T& v) {
     if constexpr (VEC == 1) {
-      acc[0] = RD::step(acc[0], v);
+      acc[0] = PA::add(acc[0], v);
     } else {
-      acc[0] = RD::step(acc[0], v.x);
-      acc[1] = RD::step(acc[1], v.y);
-      acc[2] = RD::step(acc[2], v.z);
-      acc[3] = RD::step(acc[3], v.w);
+      acc[0] = PA::add(acc[0], v.x);
+      acc[1] = PA::add(acc[1], v.y);
+      acc[2] = PA::add(acc[2], v.z);
+      acc[3] = PA::add(acc[3], v.w);
     }
   };
   if (col0 < L.C) {
@@ -564,7 +607,7 @@ __device__ __forceinline__ void col_body(const disc_reduce_launch& L, const int 
     }
   }
 #pragma unroll
-  for (int i = 0; i < VEC; ++i) part[tid][i] = acc[i];
+  for (int i = 0; i < VEC; ++i) part[tid][i] = PA::to(acc[i]);
   __syncthreads();
   // Column j of the tile: lane lc = j/VEC of each row slot, element j%VEC.
   for (int j = tid; j < span; j += kColThreads) {

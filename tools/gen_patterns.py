@@ -90,8 +90,10 @@ def gen_program(fn, prog, ch=1, early_splat=True):
         regs += len(contig) * ch * 4
     early = sorted(ident + splat)
     pf = [f"    prefetch_cls<VEC, CH, 0>(P, t, {code[i][5]});" for i, c in loads if c == 0]
+    xu = any(I_UN <= c[0] < I_UN + 4 for c in code)  # exp / tanh (MUFU) in the program
     lines = [f"struct {fn} {{",
              "  static constexpr bool kSplitFull = true;",
+             f"  static constexpr bool kXuHeavy = {'true' if xu else 'false'};",
              # pipelined only while the extra tile of loads fits (<= 16 registers at VEC=4)
              f"  static constexpr int kPipe = {len(early) if regs <= 16 else 0};",
              "  template <int VEC, int CH>",
