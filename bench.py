@@ -404,6 +404,8 @@ def main():
                     help="grouped: one disc_executor_run_grouped call per step (the same plan kernel of all "
                          "requests fused into one grouped launch); streams: per-request launches interleaved "
                          "over --streams executors")
+    ap.add_argument("--host-threads", type=int, default=min(8, os.cpu_count() or 1),
+                    help="grouped mode: host threads running the requests' runtime flows")
     ap.add_argument("--streams", type=int, default=2,
                     help="executors/streams per GPU the requests are interleaved over (independent requests overlap)")
     ap.add_argument("--stream-policy", default="lpt", choices=["size", "lpt"],
@@ -438,6 +440,8 @@ def main():
         streams.append(st)
         exs.append(D.Executor(local, st.value))
         exs[-1].set_schedule(args.schedule)
+        if args.mode == "grouped":
+            exs[-1].set_host_threads(args.host_threads)
     stream, ex = streams[0], exs[0]
     compiler = D.Compiler()
     plans = {}
@@ -599,6 +603,7 @@ def main():
                        "l2": "flushed before each step (4x L2 write)",
                        "parallelism": f"request-sharded x{world} (LPT on algorithmic bytes, no collectives)",
                        "schedule": args.schedule, "pdl": args.pdl, "mode": args.mode,
+                       "host_threads": args.host_threads if args.mode == "grouped" else 1,
                        "streams_per_gpu": len(exs),
                        "stream_policy": args.stream_policy if len(exs) > 1 else None},
             "frac_of_hbm_peak": round(value / world / peak, 4),

@@ -104,6 +104,10 @@ int disc_executor_run_stream(disc_executor e, int n_requests, const disc_plan* p
 int disc_executor_run_grouped(disc_executor e, int n_requests, const disc_plan* plans, const int* input_offsets,
                               const char* const* names, const void* const* data, const int64_t* const* dims,
                               const int* ranks, int inputs_on_host);
+/* Host threads for disc_executor_run_grouped (default 1): calls with >= 64 requests per
+ * thread run contiguous request ranges' runtime flows on worker threads (own sub-executor
+ * each: allocator, scratch, recipe cache) and merge their queues into one grouped flush. */
+int disc_executor_set_host_threads(disc_executor e, int n);
 int disc_executor_num_requests(disc_executor e);
 int disc_executor_num_request_outputs(disc_executor e, int request);  /* -1: no such request */
 int disc_executor_request_output(disc_executor e, int request, int i, const float** dptr, const int64_t** dims,

@@ -267,6 +267,12 @@ int disc_cuda_queue_request(void);
 int disc_cuda_queue_mark(int64_t bytes, int kernel, const char* schedule);
 int disc_cuda_queue_flush(int timing);
 int disc_cuda_queue_active(void);
+/* Multi-threaded host flow: a worker thread detaches its queue (the handle owns the
+ * recorded ops; the thread's queue ends) and one thread flushes its own active queue (if
+ * any) together with the detached ones -- their requests merged level by level and
+ * grouped as if queued by one thread; the handles are consumed. */
+void* disc_cuda_queue_detach(void);
+int disc_cuda_queue_flush_detached(void* const* queues, int n, int timing);
 int disc_cuda_queue_num_records(void);
 int disc_cuda_queue_record(int i, int* level, int* members, int64_t* bytes, int* kernel, const char** schedule,
                            float* ms);

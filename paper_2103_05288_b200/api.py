@@ -78,6 +78,7 @@ def _declare(L: C.CDLL) -> None:
         "disc_cuda_stream_wait_event": ([vp, vp], i32),
         "disc_executor_run_grouped": ([vp, i32, P(vp), P(i32), P(cp), P(vp), P(vp), P(i32), i32], i32),
         "disc_executor_num_requests": ([vp], i32),
+        "disc_executor_set_host_threads": ([vp, i32], i32),
         "disc_executor_num_request_outputs": ([vp, i32], i32),
         "disc_executor_request_output": ([vp, i32, i32, P(vp), P(P(i64)), P(i32)], i32),
         "disc_executor_copy_request_output": ([vp, i32, i32, vp, i32], i32),
@@ -429,6 +430,10 @@ class Executor:
 
     def set_schedule(self, schedule: str) -> None:
         _check(lib().disc_executor_set_schedule(self._h, schedule.encode()))
+
+    def set_host_threads(self, n: int) -> None:
+        """Worker threads for the host flow of grouped calls (run_grouped)."""
+        _check(lib().disc_executor_set_host_threads(self._h, int(n)))
 
     def set_cache_budget(self, nbytes: int) -> None:
         lib().disc_executor_set_cache_budget(self._h, int(nbytes))

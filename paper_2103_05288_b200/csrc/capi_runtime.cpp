@@ -127,32 +127,19 @@ int disc_executor_run_grouped(disc_executor e, int n_requests, const disc_plan* 
                               const char* const* names, const void* const* data, const int64_t* const* dims,
                               const int* ranks, int on_host) {
   return guard([&] {
-    e->ex.begin_grouped();
-    try {
-      std::vector<rt::InputBinding> in;
-      for (int r = 0; r < n_requests; ++r) {
-        e->ex.begin_request();
-        const int i0 = input_offsets[r], n = input_offsets[r + 1] - i0;
-        in.resize(n);
-        for (int i = 0; i < n; ++i) {
-          const int k = i0 + i;
-          in[i].name = names[k];
-          in[i].dims.assign(dims[k], dims[k] + ranks[k]);
-          // one staging buffer per (request, input): all of a group's copies are in flight together
-          in[i].ptr = on_host ? e->ex.stage_input(k, data[k], bytes_of(dims[k], ranks[k]))
-                              : static_cast<const float*>(data[k]);
-        }
-        e->ex.run(*plans[r]->plan, in, true, plans[r]->serial);
-      }
-    } catch (...) {
-      try {
-        e->ex.end_grouped();  // issue what was queued (valid work), then report the error
-      } catch (...) {
-      }
-      throw;
+    std::vector<const CompiledPlan*> ps(n_requests);
+    std::vector<uint64_t> serials(n_requests);
+    for (int r = 0; r < n_requests; ++r) {
+      ps[r] = plans[r]->plan.get();
+      serials[r] = plans[r]->serial;
     }
-    e->ex.end_grouped();
+    e->ex.run_grouped_batch(n_requests, ps.data(), serials.data(), input_offsets, names, data, dims, ranks,
+                            on_host != 0);
   });
+}
+
+int disc_executor_set_host_threads(disc_executor e, int n) {
+  return guard([&] { e->ex.set_host_threads(n); });
 }
 
 int disc_executor_num_requests(disc_executor e) { return static_cast<int>(e->ex.request_outputs().size()); }

@@ -368,6 +368,8 @@ struct QOp {
   int64_t bytes = 0;
   int kernel = -1;
   int sched = -1;  // index into Queue::names
+  int grouped = 0;  // fused launch: 1 = groupable (gk valid), 0 = issued alone
+  GroupKey gk;      // computed when queued (on the thread that runs the request's flow)
 };
 struct QRecord {
   int level, members, kernel, sched;
@@ -415,11 +417,14 @@ template <typename T>
 void enqueue(int kind, const T& payload) {
   if (t_q.reqs.empty()) t_q.reqs.emplace_back();
   const size_t off = t_q.arena.take(sizeof(T));
-  if constexpr (std::is_same<T, disc_loop_launch>::value || std::is_same<T, disc_reduce_launch>::value)
+  QOp op{kind, off};
+  if constexpr (std::is_same<T, disc_loop_launch>::value || std::is_same<T, disc_reduce_launch>::value) {
     disc_desc::copy_used(reinterpret_cast<T*>(t_q.arena.data() + off), payload);
-  else
+    op.grouped = group_key(kind == kQLoop ? 0 : 1, &payload, &op.gk) ? 1 : 0;
+  } else {
     std::memcpy(t_q.arena.data() + off, &payload, sizeof(T));
-  t_q.reqs.back().push_back({kind, off});
+  }
+  t_q.reqs.back().push_back(op);
 }
 
 cudaEvent_t queue_event() {
@@ -697,15 +702,38 @@ int disc_cuda_queue_mark(int64_t bytes, int kernel, const char* schedule) {
   return 0;
 }
 
-int disc_cuda_queue_flush(int timing) {
-  if (!t_q.active) return 0;
-  t_q.active = false;  // everything below issues for real
-  const cudaStream_t st = t_q.stream;
+}  // extern "C"
+
+namespace {
+
+// Issues the queued work of `qs` (the calling thread's queue and/or detached ones) level
+// by level on qs[0]'s stream; records go to the calling thread.
+int flush_queues(const std::vector<Queue*>& qs, int timing) {
+  const cudaStream_t st = qs[0]->stream;
   t_q.records.clear();
   t_q.next_event = 0;
+  // schedule names of every queue, interned into the calling thread's table
+  std::vector<std::vector<int>> remap(qs.size());
+  auto intern = [&](const std::string& n) {
+    for (size_t i = 0; i < t_q.names.size(); ++i)
+      if (t_q.names[i] == n) return static_cast<int>(i);
+    t_q.names.push_back(n);
+    return static_cast<int>(t_q.names.size()) - 1;
+  };
+  for (size_t k = 0; k < qs.size(); ++k)
+    for (const auto& n : qs[k]->names) remap[k].push_back(intern(n));
+  auto name_of = [&](size_t k, int sched) { return sched >= 0 ? remap[k][sched] : -1; };
+  struct ReqRef {
+    size_t q;
+    const std::vector<QOp>* ops;
+  };
+  std::vector<ReqRef> reqs;
   size_t levels = 0;
-  for (const auto& r : t_q.reqs) levels = std::max(levels, r.size());
-  const unsigned char* A = t_q.arena.data();
+  for (size_t k = 0; k < qs.size(); ++k)
+    for (const auto& r : qs[k]->reqs) {
+      reqs.push_back({k, &r});
+      levels = std::max(levels, r.size());
+    }
   auto begin_rec = [&](int level, int members, int64_t bytes, int kernel, int sched) {
     QRecord rec{level, members, kernel, sched, bytes};
     if (timing) {
@@ -718,53 +746,69 @@ int disc_cuda_queue_flush(int timing) {
   auto end_rec = [&] {
     if (timing) cudaEventRecord(t_q.records.back().b, st);
   };
+  const int copy_name = intern("copy");
+  struct FOp {
+    const QOp* op;
+    const unsigned char* p;
+    size_t q;
+  };
   int rc = 0;
   for (size_t lv = 0; lv < levels && !rc; ++lv) {
-    // fused launches of this level, by kind; everything else issued in request order
-    std::vector<const QOp*> fused[2];
-    std::vector<disc_dev::disc_copy2d> copies;  // D2D copies and concats of this level
+    // fused launches of this level, grouped by kernel instantiation; D2D copies and
+    // concats as one grouped copy; everything else issued in request order
+    std::map<GroupKey, std::vector<FOp>> groups[2];
+    std::vector<GroupKey> order[2];
+    std::vector<FOp> alone[2];
+    std::vector<disc_dev::disc_copy2d> copies;
     int64_t copy_bytes = 0;
-    for (const auto& r : t_q.reqs) {
-      if (lv >= r.size()) continue;
-      const QOp& op = r[lv];
-      const void* p = A + op.off;
+    for (const ReqRef& rr : reqs) {
+      if (lv >= rr.ops->size()) continue;
+      const QOp& op = (*rr.ops)[lv];
+      const unsigned char* p = qs[rr.q]->arena.data() + op.off;
       if (op.kind == kQLoop || op.kind == kQReduce) {
-        fused[op.kind == kQLoop ? 0 : 1].push_back(&op);
+        const int kind = op.kind == kQLoop ? 0 : 1;
+        if (!op.grouped) {
+          alone[kind].push_back({&op, p, rr.q});
+          continue;
+        }
+        auto it = groups[kind].find(op.gk);
+        if (it == groups[kind].end()) {
+          order[kind].push_back(op.gk);
+          it = groups[kind].emplace(op.gk, std::vector<FOp>()).first;
+        }
+        it->second.push_back({&op, p, rr.q});
         continue;
       }
       if (op.kind == kQConcat ||
-          (op.kind == kQMemcpy && (static_cast<const QMemcpy*>(p)->kind & 3) == 2 &&
-           static_cast<const QMemcpy*>(p)->bytes % 4 == 0)) {
+          (op.kind == kQMemcpy && (reinterpret_cast<const QMemcpy*>(p)->kind & 3) == 2 &&
+           reinterpret_cast<const QMemcpy*>(p)->bytes % 4 == 0)) {
         if (op.kind == kQConcat) {
-          concat_items(*static_cast<const disc_concat_launch*>(p), copies);
+          concat_items(*reinterpret_cast<const disc_concat_launch*>(p), copies);
         } else {
-          const auto& c = *static_cast<const QMemcpy*>(p);
+          const auto& c = *reinterpret_cast<const QMemcpy*>(p);
           const int64_t n = static_cast<int64_t>(c.bytes / 4);
           copies.push_back({static_cast<const float*>(c.src), static_cast<float*>(c.dst), 1, n, n, n});
         }
         copy_bytes += op.bytes;
         continue;
       }
-      begin_rec(static_cast<int>(lv), 1, op.bytes, op.kernel, op.sched);
+      begin_rec(static_cast<int>(lv), 1, op.bytes, op.kernel, name_of(rr.q, op.sched));
       switch (op.kind) {
-        case kQPad: rc = counted(disc_launch::pad(*static_cast<const disc_pad_launch*>(p), st), "launch pad"); break;
-        case kQConcat:
-          rc = counted(disc_launch::concat(*static_cast<const disc_concat_launch*>(p), st), "launch concat");
-          break;
+        case kQPad: rc = counted(disc_launch::pad(*reinterpret_cast<const disc_pad_launch*>(p), st), "launch pad"); break;
         case kQGemm: {
-          const auto& g = *static_cast<const QGemm*>(p);
+          const auto& g = *reinterpret_cast<const QGemm*>(p);
           rc = counted(disc_launch::gemm(g.m, g.k, g.n, g.a, g.b, g.c, st), "launch gemm");
           break;
         }
         case kQMemcpy: {
           static const cudaMemcpyKind kinds[] = {cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost,
                                                  cudaMemcpyDeviceToDevice, cudaMemcpyDefault};
-          const auto& c = *static_cast<const QMemcpy*>(p);
+          const auto& c = *reinterpret_cast<const QMemcpy*>(p);
           rc = check(cudaMemcpyAsync(c.dst, c.src, c.bytes, kinds[c.kind & 3], st), "cudaMemcpyAsync");
           break;
         }
         case kQMemset: {
-          const auto& m = *static_cast<const QMemset*>(p);
+          const auto& m = *reinterpret_cast<const QMemset*>(p);
           rc = check(cudaMemsetAsync(m.dst, m.value, m.bytes, st), "cudaMemsetAsync");
           break;
         }
@@ -773,56 +817,34 @@ int disc_cuda_queue_flush(int timing) {
       if (rc) break;
     }
     if (!rc && !copies.empty()) {
-      int copy_name = -1;
-      for (size_t i = 0; i < t_q.names.size(); ++i)
-        if (t_q.names[i] == "copy") copy_name = static_cast<int>(i);
-      if (copy_name < 0) {
-        t_q.names.push_back("copy");
-        copy_name = static_cast<int>(t_q.names.size()) - 1;
-      }
       begin_rec(static_cast<int>(lv), static_cast<int>(copies.size()), copy_bytes, -1, copy_name);
       rc = issue_copies(copies, st);
       end_rec();
     }
     for (int kind = 0; kind < 2 && !rc; ++kind) {
-      if (fused[kind].empty()) continue;
-      // group by kernel instantiation; one record per grouped launch
-      std::map<GroupKey, std::vector<const QOp*>> groups;
-      std::vector<GroupKey> order;
-      for (const QOp* op : fused[kind]) {
-        const void* p = A + op->off;
-        GroupKey k;
-        if (!group_key(kind, p, &k)) {
-          begin_rec(static_cast<int>(lv), 1, op->bytes, op->kernel, op->sched);
-          rc = kind == 0 ? disc_cuda_launch_loop(static_cast<const disc_loop_launch*>(p), st)
-                         : disc_cuda_launch_reduce(static_cast<const disc_reduce_launch*>(p), st);
-          end_rec();
-          if (rc) break;
-          continue;
-        }
-        auto it = groups.find(k);
-        if (it == groups.end()) {
-          order.push_back(k);
-          it = groups.emplace(k, std::vector<const QOp*>()).first;
-        }
-        it->second.push_back(op);
-      }
-      for (const GroupKey& k : order) {
+      for (const FOp& f : alone[kind]) {
+        begin_rec(static_cast<int>(lv), 1, f.op->bytes, f.op->kernel, name_of(f.q, f.op->sched));
+        rc = kind == 0 ? disc_cuda_launch_loop(reinterpret_cast<const disc_loop_launch*>(f.p), st)
+                       : disc_cuda_launch_reduce(reinterpret_cast<const disc_reduce_launch*>(f.p), st);
+        end_rec();
         if (rc) break;
-        auto& m = groups[k];
-        std::stable_sort(m.begin(), m.end(), [&](const QOp* a, const QOp* b) {
-          return launch_weight(kind, A + a->off) > launch_weight(kind, A + b->off);
+      }
+      for (const GroupKey& k : order[kind]) {
+        if (rc) break;
+        auto& m = groups[kind][k];
+        std::stable_sort(m.begin(), m.end(), [&](const FOp& a, const FOp& b) {
+          return launch_weight(kind, a.p) > launch_weight(kind, b.p);
         });
         for (size_t i = 0; i < m.size() && !rc; i += DISC_MAX_GROUP) {
           const size_t e = std::min(m.size(), i + DISC_MAX_GROUP);
           std::vector<const void*> chunk;
           int64_t bytes = 0;
-          int kernel = m[i]->kernel, sched = m[i]->sched;
+          int kernel = m[i].op->kernel, sched = name_of(m[i].q, m[i].op->sched);
           for (size_t j = i; j < e; ++j) {
-            chunk.push_back(A + m[j]->off);
-            bytes += m[j]->bytes;
-            if (m[j]->kernel != kernel) kernel = -1;
-            if (m[j]->sched != sched) sched = -1;
+            chunk.push_back(m[j].p);
+            bytes += m[j].op->bytes;
+            if (m[j].op->kernel != kernel) kernel = -1;
+            if (name_of(m[j].q, m[j].op->sched) != sched) sched = -1;
           }
           begin_rec(static_cast<int>(lv), static_cast<int>(chunk.size()), bytes, kernel, sched);
           rc = issue_group(k, chunk, st);
@@ -831,11 +853,53 @@ int disc_cuda_queue_flush(int timing) {
       }
     }
   }
-  for (void* p : t_q.frees)
-    if (!rc) rc = check(cudaFreeAsync(p, st), "cudaFreeAsync");
-  t_q.frees.clear();
+  for (Queue* q : qs) {
+    for (void* p : q->frees)
+      if (!rc) rc = check(cudaFreeAsync(p, st), "cudaFreeAsync");
+    q->frees.clear();
+    q->reqs.clear();
+    q->arena.clear();
+  }
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int disc_cuda_queue_flush(int timing) {
+  if (!t_q.active) return 0;
+  t_q.active = false;  // everything below issues for real
+  return flush_queues({&t_q}, timing);
+}
+
+void* disc_cuda_queue_detach(void) {
+  if (!t_q.active) return nullptr;
+  Queue* q = new Queue();
+  q->active = false;
+  q->stream = t_q.stream;
+  std::swap(q->arena, t_q.arena);
+  std::swap(q->reqs, t_q.reqs);
+  std::swap(q->frees, t_q.frees);
+  std::swap(q->names, t_q.names);
+  t_q.active = false;
   t_q.reqs.clear();
   t_q.arena.clear();
+  t_q.frees.clear();
+  return q;
+}
+
+int disc_cuda_queue_flush_detached(void* const* queues, int n, int timing) {
+  std::vector<Queue*> qs;
+  if (t_q.active) {
+    t_q.active = false;
+    qs.push_back(&t_q);
+  }
+  for (int i = 0; i < n; ++i)
+    if (queues[i]) qs.push_back(static_cast<Queue*>(queues[i]));
+  int rc = 0;
+  if (!qs.empty()) rc = flush_queues(qs, timing);
+  for (int i = 0; i < n; ++i) delete static_cast<Queue*>(queues[i]);
   return rc;
 }
 

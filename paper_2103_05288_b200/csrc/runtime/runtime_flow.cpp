@@ -3,6 +3,11 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <exception>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -132,9 +137,7 @@ void DeviceExecutor::begin_request() {
   ++request_;
 }
 
-void DeviceExecutor::end_grouped() {
-  if (!grouped_) return;
-  grouped_ = false;
+int DeviceExecutor::issue_small_inputs() {
   int rc = 0;
   for (auto& c : small_) {  // packed small inputs: one H2D per chunk ahead of every queued op
     if (c.used == 0) continue;
@@ -144,6 +147,199 @@ void DeviceExecutor::end_grouped() {
     c.used = 0;
   }
   small_cur_ = 0;
+  return rc;
+}
+
+void* DeviceExecutor::detach_grouped() {
+  grouped_ = false;
+  const int rc = issue_small_inputs();
+  void* q = disc_cuda_queue_detach();
+  cuda_ok(rc, "small-input copy");
+  return q;
+}
+
+void DeviceExecutor::finish_detached() { alloc_.set_defer(false); }
+
+// Persistent worker threads for run_grouped_batch.
+struct DeviceExecutor::Pool {
+  std::vector<std::thread> threads;
+  std::mutex mu;
+  std::condition_variable cv, done;
+  std::function<void(int)> job;
+  uint64_t gen = 0;
+  int pending = 0;
+  bool stop = false;
+  Pool(int n, int device) {
+    for (int w = 0; w < n; ++w)
+      threads.emplace_back([this, w, device] {
+        disc_cuda_set_device(device);
+        uint64_t seen = 0;
+        for (;;) {
+          std::function<void(int)> f;
+          {
+            std::unique_lock<std::mutex> l(mu);
+            cv.wait(l, [&] { return stop || gen != seen; });
+            if (stop) return;
+            seen = gen;
+            f = job;
+          }
+          f(w);
+          std::lock_guard<std::mutex> l(mu);
+          if (--pending == 0) done.notify_all();
+        }
+      });
+  }
+  void run(const std::function<void(int)>& f) {  // f(w) on every worker; returns when all finished
+    std::unique_lock<std::mutex> l(mu);
+    job = f;
+    pending = static_cast<int>(threads.size());
+    ++gen;
+    cv.notify_all();
+    done.wait(l, [&] { return pending == 0; });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> l(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& t : threads) t.join();
+  }
+};
+
+void DeviceExecutor::set_host_threads(int n) {
+  n = std::max(1, std::min(n, 64));
+  if (n == host_threads_) return;
+  pool_.reset();
+  subs_.clear();
+  host_threads_ = n;
+  if (n > 1) {
+    for (int w = 1; w < n; ++w) {
+      subs_.push_back(std::make_unique<DeviceExecutor>(device_, stream_));
+      subs_.back()->set_schedule(pref_);
+    }
+    pool_ = std::make_unique<Pool>(n - 1, device_);
+  }
+}
+
+void DeviceExecutor::run_requests(int r0, int r1, const CompiledPlan* const* plans, const uint64_t* serials,
+                                  const int* offs, const char* const* names, const void* const* data,
+                                  const int64_t* const* dims, const int* ranks, bool on_host) {
+  std::vector<InputBinding> in;
+  for (int r = r0; r < r1; ++r) {
+    begin_request();
+    const int i0 = offs[r], n = offs[r + 1] - i0;
+    in.resize(n);
+    for (int i = 0; i < n; ++i) {
+      const int k = i0 + i;
+      in[i].name = names[k];
+      in[i].dims.assign(dims[k], dims[k] + ranks[k]);
+      int64_t bytes = 4;
+      for (int64_t d : in[i].dims) bytes *= d;
+      // one staging buffer per (request, input): all of a group's copies are in flight together
+      in[i].ptr = on_host ? stage_input(k, data[k], bytes) : static_cast<const float*>(data[k]);
+    }
+    run(*plans[r], in, true, serials[r]);
+  }
+}
+
+void DeviceExecutor::run_grouped_batch(int n, const CompiledPlan* const* plans, const uint64_t* serials,
+                                       const int* offs, const char* const* names, const void* const* data,
+                                       const int64_t* const* dims, const int* ranks, bool on_host) {
+  constexpr int kMinPerThread = 64;
+  const int T = std::max(1, std::min(host_threads_, n / kMinPerThread));
+  if (T <= 1) {
+    begin_grouped();
+    try {
+      run_requests(0, n, plans, serials, offs, names, data, dims, ranks, on_host);
+    } catch (...) {
+      try {
+        end_grouped();  // issue what was queued (valid work), then report the error
+      } catch (...) {
+      }
+      throw;
+    }
+    end_grouped();
+    return;
+  }
+  // contiguous request ranges: [bounds[w], bounds[w+1]) on worker w (w = 0: this thread)
+  std::vector<int> bounds(T + 1);
+  for (int w = 0; w <= T; ++w) bounds[w] = static_cast<int>(int64_t{n} * w / T);
+  std::vector<void*> handles(T, nullptr);
+  std::vector<std::exception_ptr> errs(T);
+  for (int w = 1; w < T; ++w) subs_[w - 1]->set_timing(false);
+  pool_->run([&](int w) {
+    if (w + 1 >= T) return;
+    DeviceExecutor& ex = *subs_[w];
+    try {
+      ex.begin_grouped();
+      ex.run_requests(bounds[w + 1], bounds[w + 2], plans, serials, offs, names, data, dims, ranks, on_host);
+    } catch (...) {
+      errs[w + 1] = std::current_exception();
+    }
+    try {
+      if (ex.grouped()) handles[w + 1] = ex.detach_grouped();
+    } catch (...) {
+      if (!errs[w + 1]) errs[w + 1] = std::current_exception();
+    }
+  });
+  begin_grouped();
+  try {
+    run_requests(bounds[0], bounds[1], plans, serials, offs, names, data, dims, ranks, on_host);
+  } catch (...) {
+    errs[0] = std::current_exception();
+  }
+  // merged flush: this thread's queue + the workers' detached ones
+  grouped_ = false;
+  int rc = issue_small_inputs();
+  const auto t_flush = Clock::now();
+  std::vector<void*> hs;
+  for (int w = 1; w < T; ++w)
+    if (handles[w]) hs.push_back(handles[w]);
+  const int frc = disc_cuda_queue_flush_detached(hs.data(), static_cast<int>(hs.size()), group_timing_ ? 1 : 0);
+  if (rc == 0) rc = frc;
+  static const bool prof = std::getenv("DISC_HOST_PROFILE") != nullptr;
+  if (prof)
+    std::fprintf(stderr, "[disc host] grouped call: %d requests on %d threads, flow %.3f ms, flush %.3f ms\n", n, T,
+                 std::chrono::duration<double, std::milli>(t_flush - t_group_).count(),
+                 std::chrono::duration<double, std::milli>(Clock::now() - t_flush).count());
+  alloc_.set_defer(false);
+  for (int w = 1; w < T; ++w) subs_[w - 1]->finish_detached();
+  // request outputs / stats in request order
+  for (int w = 1; w < T; ++w) {
+    const auto& ro = subs_[w - 1]->request_outputs();
+    const auto& rs = subs_[w - 1]->request_stats();
+    req_outputs_.insert(req_outputs_.end(), ro.begin(), ro.end());
+    req_stats_.insert(req_stats_.end(), rs.begin(), rs.end());
+  }
+  for (const auto& e : errs)
+    if (e) std::rethrow_exception(e);
+  cuda_ok(rc, "grouped launch");
+  const int nrec = disc_cuda_queue_num_records();
+  records_.clear();
+  device_launches_ = 0;
+  for (int i = 0; i < nrec; ++i) {
+    int level = 0, members = 0, kernel = -1;
+    int64_t bytes = 0;
+    const char* sched = nullptr;
+    float ms = 0.f;
+    if (group_timing_) {
+      records_.push_back({i, -1, "", 0, 0.0, 1, -1});
+    } else {
+      cuda_ok(disc_cuda_queue_record(i, &level, &members, &bytes, &kernel, &sched, &ms), "group record");
+      records_.push_back({level, kernel, std::string("group:") + (sched ? sched : ""), bytes, 0.0, members, -1});
+    }
+    device_launches_ += 1;
+  }
+  for (int w = 1; w < T; ++w) algorithmic_bytes_ += subs_[w - 1]->algorithmic_bytes();
+  records_grouped_ = true;
+  timing_pending_ = group_timing_;
+}
+
+void DeviceExecutor::end_grouped() {
+  if (!grouped_) return;
+  grouped_ = false;
+  int rc = issue_small_inputs();
   const auto t_flush = Clock::now();
   if (rc == 0) rc = disc_cuda_queue_flush(group_timing_ ? 1 : 0);
   else disc_cuda_queue_flush(0);

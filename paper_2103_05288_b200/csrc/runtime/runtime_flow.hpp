@@ -106,6 +106,15 @@ class DeviceExecutor {
   void begin_grouped();
   void begin_request();
   void end_grouped();
+  // Whole grouped call over raw C-ABI arrays (request r: plans[r], inputs offs[r] ..
+  // offs[r+1]-1).  With host threads > 1 and enough requests, contiguous request ranges
+  // run their host flow on worker threads (each with its own sub-executor: allocator,
+  // scratch, recipe cache, queue); the queues are merged into one grouped flush.
+  void run_grouped_batch(int n, const CompiledPlan* const* plans, const uint64_t* serials, const int* offs,
+                         const char* const* names, const void* const* data, const int64_t* const* dims,
+                         const int* ranks, bool on_host);
+  void set_host_threads(int n);
+  int host_threads() const { return host_threads_; }
   bool grouped() const { return grouped_; }
   const std::vector<std::vector<OutputView>>& request_outputs() const { return req_outputs_; }
   const std::vector<ExecStats>& request_stats() const { return req_stats_; }
@@ -118,8 +127,14 @@ class DeviceExecutor {
   int64_t algorithmic_bytes() const { return algorithmic_bytes_; }
   const std::vector<LaunchRecord>& launch_records() const { return records_; }
   void set_timing(bool on) { timing_ = on; }
-  void set_schedule(SchedulePref p) { pref_ = p; }
-  void set_cache_budget(int64_t b) { alloc_.set_budget(b); }
+  void set_schedule(SchedulePref p) {
+    pref_ = p;
+    for (auto& x : subs_) x->set_schedule(p);
+  }
+  void set_cache_budget(int64_t b) {
+    alloc_.set_budget(b);
+    for (auto& x : subs_) x->set_cache_budget(b);
+  }
   // Host-staging helper: device copy of host data owned by the executor (not counted in
   // plan allocator stats).
   const float* stage_input(int slot, const void* host, int64_t bytes);
@@ -151,6 +166,17 @@ class DeviceExecutor {
   bool grouped_ = false;
   bool group_timing_ = false;
   bool records_grouped_ = false;  // records_ describe grouped launches
+  // multi-threaded host flow (run_grouped_batch)
+  int host_threads_ = 1;
+  struct Pool;
+  std::unique_ptr<Pool> pool_;
+  std::vector<std::unique_ptr<DeviceExecutor>> subs_;
+  void run_requests(int r0, int r1, const CompiledPlan* const* plans, const uint64_t* serials, const int* offs,
+                    const char* const* names, const void* const* data, const int64_t* const* dims, const int* ranks,
+                    bool on_host);
+  void* detach_grouped();      // worker: issue packed small inputs, hand the queue over
+  void finish_detached();      // after the merged flush
+  int issue_small_inputs();
   std::chrono::steady_clock::time_point t_group_;
   // grouped calls: small host inputs packed into one pinned arena (one H2D per group)
   static constexpr int64_t kSmallInput = 64 << 10;

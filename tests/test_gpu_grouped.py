@@ -179,3 +179,36 @@ def test_grouped_errors_are_reported(gpu, fixtures):
     got = ex.run_grouped([(plan, good)])
     want = gpu.Executor().run(plan, good).outputs
     _assert_same(got, [want], "after error")
+
+
+@pytest.mark.parametrize("threads", [2, 4])
+def test_grouped_host_threads_identical(gpu, ref, threads):
+    """Multi-threaded host flow (worker sub-executors, merged queues): outputs and
+    per-request stats identical to the single-threaded grouped call and to sequential runs."""
+    rng = ref.RefRng(99)
+    reqs = []
+    for seed in range(60):
+        g = ref.random_graph(seed, 10)
+        plan = gpu.compile_graph(g)
+        for b in range(5):
+            reqs.append((plan, ref.make_binding(g, rng.random_symbols(g), seed * 7 + b)))
+    seq = _sequential(gpu, reqs)
+    one = gpu.Executor()
+    base = one.run_grouped(reqs)
+    _assert_same(base, seq, "1 thread")
+    ex = gpu.Executor()
+    ex.set_host_threads(threads)
+    for _ in range(2):  # the second call reuses sub-executor caches
+        _assert_same(ex.run_grouped(reqs), seq, f"{threads} threads")
+    for r in range(len(reqs)):
+        assert ex.request_stats(r).launch_count == one.request_stats(r).launch_count
+    # the merged flush issues the same groups as one thread queueing everything
+    one.set_timing(True)
+    one.run_stream(reqs, grouped=True)
+    one.synchronize()
+    ex.set_timing(True)
+    ex.run_stream(reqs, grouped=True)
+    ex.synchronize()
+    assert ex.algorithmic_bytes() == one.algorithmic_bytes()
+    key = lambda recs: sorted((r["instr"], r["schedule"], r["bytes"], r["device_kernels"]) for r in recs)
+    assert key(ex.launch_records()) == key(one.launch_records())
