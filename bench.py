@@ -404,7 +404,7 @@ def main():
                     help="grouped: one disc_executor_run_grouped call per step (the same plan kernel of all "
                          "requests fused into one grouped launch); streams: per-request launches interleaved "
                          "over --streams executors")
-    ap.add_argument("--host-threads", type=int, default=min(8, os.cpu_count() or 1),
+    ap.add_argument("--host-threads", type=int, default=min(16, os.cpu_count() or 1),
                     help="grouped mode: host threads running the requests' runtime flows")
     ap.add_argument("--streams", type=int, default=2,
                     help="executors/streams per GPU the requests are interleaved over (independent requests overlap)")

@@ -272,6 +272,8 @@ int disc_cuda_queue_active(void);
  * any) together with the detached ones -- their requests merged level by level and
  * grouped as if queued by one thread; the handles are consumed. */
 void* disc_cuda_queue_detach(void);
+/* Host profile: ns spent packing grouped-launch descriptor tables since the last call. */
+int64_t disc_cuda_host_profile(int64_t* table_bytes);
 int disc_cuda_queue_flush_detached(void* const* queues, int n, int timing);
 int disc_cuda_queue_num_records(void);
 int disc_cuda_queue_record(int i, int* level, int* members, int64_t* bytes, int* kernel, const char** schedule,

@@ -172,12 +172,7 @@ inline int64_t finalize_blocks(const disc_reduce_launch& L) {
 cudaError_t finalize_columns(const disc_reduce_launch& L, cudaStream_t s, const HostGroup* g) {
   if (g) {  // members are two-pass / atomic launches
     disc_group G;
-    G.table = g->dev_table;
-    G.stride = g->stride;
-    G.n = g->n;
-    G.nseg = 1;  // finalize reads only the reduce geometry and pointers (and pre.flags)
-    G.seg[0][0] = 0;
-    G.seg[0][1] = static_cast<uint16_t>(desc_bytes<disc_reduce_launch>() / 16);
+    g->fill(G);  // the column pass's records: reduce geometry, pointers and pre.flags included
     int64_t off = 0;
     for (int i = 0; i < g->n; ++i) {
       G.block_off[i] = static_cast<int32_t>(off);

@@ -149,8 +149,8 @@ struct disc_group {
   const unsigned char* table;  // n descriptors, `stride` bytes apart
   int32_t stride;
   int32_t n;
-  int32_t nseg;                       // descriptor byte ranges a CTA stages, in 16 B units:
-  uint16_t seg[DISC_GROUP_SEGS][2];   // (offset, count); the members share program structure
+  int32_t nseg;                       // descriptor ranges a CTA stages, in 16 B units:
+  uint16_t seg[DISC_GROUP_SEGS][3];   // (offset in the descriptor, count, offset in the record)
   int32_t block_off[DISC_MAX_GROUP + 1];
 };
 
@@ -179,11 +179,13 @@ constexpr int desc_bytes() { return (static_cast<int>(sizeof(Launch)) + 15) / 16
 // before griddepcontrol.wait.
 template <typename Launch>
 __device__ __forceinline__ const Launch& group_stage(const disc_group& G, int g, unsigned char* buf) {
+  // member g's record holds only the descriptor ranges the kernel reads (desc_ranges.hpp),
+  // packed back to back; they are unpacked to their offsets in the descriptor
   const uint4* src = reinterpret_cast<const uint4*>(G.table + static_cast<int64_t>(g) * G.stride);
   uint4* dst = reinterpret_cast<uint4*>(buf);
-  for (int k = 0; k < G.nseg; ++k) {  // only the ranges the kernel reads (unused loads/code skipped)
-    const int o = G.seg[k][0], c = G.seg[k][1];
-    for (int i = threadIdx.x; i < c; i += blockDim.x) dst[o + i] = __ldg(src + o + i);
+  for (int k = 0; k < G.nseg; ++k) {
+    const int o = G.seg[k][0], c = G.seg[k][1], so = G.seg[k][2];
+    for (int i = threadIdx.x; i < c; i += blockDim.x) dst[o + i] = __ldg(src + so + i);
   }
   __syncthreads();
   return *reinterpret_cast<const Launch*>(buf);
@@ -201,26 +203,32 @@ inline void group_counts(disc_reduce_launch& m, const disc_reduce_launch& L) {
   max_counts(m.pre, L.pre);
   max_counts(m.post, L.post);
 }
-template <typename Launch, typename HG>
-inline void group_segments(disc_group& G, const HG& H) {
+// Fills (nseg, seg, stride) of a compact member record for `n` descriptors.
+template <typename Launch>
+inline void group_segments(const void* const* members, int n, int32_t* nseg, uint16_t (*seg)[3], int32_t* stride) {
   Launch m;
-  disc_desc::copy_used(&m, H.template at<Launch>(0));
-  for (int i = 1; i < H.n; ++i) group_counts(m, H.template at<Launch>(i));
+  disc_desc::copy_used(&m, *static_cast<const Launch*>(members[0]));
+  for (int i = 1; i < n; ++i) group_counts(m, *static_cast<const Launch*>(members[i]));
   disc_desc::Range r[disc_desc::kMaxRanges];
-  const int n = disc_desc::ranges(m, r);
-  G.nseg = 0;
-  for (int i = 0; i < n; ++i) {
+  const int nr = disc_desc::ranges(m, r);
+  int ns = 0, rec = 0;
+  for (int i = 0; i < nr; ++i) {
     if (!r[i].len) continue;
     const int o = static_cast<int>(r[i].off / 16), e = static_cast<int>((r[i].off + r[i].len + 15) / 16);
-    if (G.nseg > 0 && G.seg[G.nseg - 1][0] + G.seg[G.nseg - 1][1] >= o) {  // merge adjacent
-      const int s0 = G.seg[G.nseg - 1][0];
-      G.seg[G.nseg - 1][1] = static_cast<uint16_t>(std::max(e, s0 + G.seg[G.nseg - 1][1]) - s0);
+    if (ns > 0 && seg[ns - 1][0] + seg[ns - 1][1] >= o) {  // merge adjacent
+      const int s0 = seg[ns - 1][0], add = std::max(e, s0 + seg[ns - 1][1]) - (s0 + seg[ns - 1][1]);
+      seg[ns - 1][1] = static_cast<uint16_t>(seg[ns - 1][1] + add);
+      rec += add;
       continue;
     }
-    G.seg[G.nseg][0] = static_cast<uint16_t>(o);
-    G.seg[G.nseg][1] = static_cast<uint16_t>(e - o);
-    ++G.nseg;
+    seg[ns][0] = static_cast<uint16_t>(o);
+    seg[ns][1] = static_cast<uint16_t>(e - o);
+    seg[ns][2] = static_cast<uint16_t>(rec);
+    rec += e - o;
+    ++ns;
   }
+  *nseg = ns;
+  *stride = rec * 16;
 }
 
 // ---------------------------------------------------------------------------
@@ -691,15 +699,25 @@ inline cudaError_t set_smem(K kernel, size_t bytes, size_t threshold = 40 * 1024
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
 }
 
-// Host side of a grouped launch: the uploaded device table and the host copy of the same
-// descriptors (for per-launch grid and shared-memory sizing).
+// Host side of a grouped launch: the members' host descriptors (full layout, for grid and
+// shared-memory sizing) and the uploaded device table of compact member records.
 struct HostGroup {
-  const unsigned char* dev_table;
-  const unsigned char* host_table;
-  int stride;
+  const void* const* members;
   int n;
+  const unsigned char* dev_table;
+  int32_t stride;               // record bytes
+  int32_t nseg;
+  uint16_t seg[DISC_GROUP_SEGS][3];
   template <typename T>
-  const T& at(int i) const { return *reinterpret_cast<const T*>(host_table + static_cast<size_t>(i) * stride); }
+  const T& at(int i) const { return *static_cast<const T*>(members[i]); }
+  void fill(disc_group& G) const {
+    G.table = dev_table;
+    G.stride = stride;
+    G.n = n;
+    G.nseg = nseg;
+    for (int k = 0; k < nseg; ++k)
+      for (int j = 0; j < 3; ++j) G.seg[k][j] = seg[k][j];
+  }
 };
 // Grouped kernels hold a descriptor in static shared memory: opt in to more dynamic
 // shared memory earlier than single launches do.
@@ -818,10 +836,7 @@ inline void group_blocks(const int64_t* units, int n, int64_t cap, int32_t* off)
 template <int CH = kCH, typename K>
 inline cudaError_t launch_loop_group(K kernel, const HostGroup& H, cudaStream_t s, bool use_slots) {
   disc_group G;
-  G.table = H.dev_table;
-  G.stride = H.stride;
-  G.n = H.n;
-  group_segments<disc_loop_launch>(G, H);
+  H.fill(G);
   size_t smem = 0;
   for (int i = 0; i < H.n; ++i) smem = std::max(smem, loop_smem<CH>(H.at<disc_loop_launch>(i), use_slots));
   cudaError_t e = set_smem(kernel, smem, kGroupSmemThreshold);
@@ -839,10 +854,7 @@ inline cudaError_t launch_loop_group(K kernel, const HostGroup& H, cudaStream_t 
 template <int CH = kCH, typename K>
 inline cudaError_t launch_row_group(K kernel, const HostGroup& H, cudaStream_t s, bool use_slots) {
   disc_group G;
-  G.table = H.dev_table;
-  G.stride = H.stride;
-  G.n = H.n;
-  group_segments<disc_reduce_launch>(G, H);
+  H.fill(G);
   size_t smem = 0;
   for (int i = 0; i < H.n; ++i) smem = std::max(smem, row_smem<CH>(H.at<disc_reduce_launch>(i), use_slots));
   const int block = row_block(H.at<disc_reduce_launch>(0));
@@ -864,10 +876,7 @@ inline cudaError_t launch_row_group(K kernel, const HostGroup& H, cudaStream_t s
 template <int CH = kCH, typename K>
 inline cudaError_t launch_col_group(K kernel, const HostGroup& H, cudaStream_t s, bool use_slots) {
   disc_group G;
-  G.table = H.dev_table;
-  G.stride = H.stride;
-  G.n = H.n;
-  group_segments<disc_reduce_launch>(G, H);
+  H.fill(G);
   size_t smem = 0;
   int64_t off = 0;
   for (int i = 0; i < H.n; ++i) {

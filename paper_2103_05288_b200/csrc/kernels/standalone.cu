@@ -171,10 +171,7 @@ cudaError_t concat(const disc_concat_launch& C, cudaStream_t s) {
 // Grouped copies: the table (H.dev_table) holds H.n disc_copy2d items.
 cudaError_t copy2d_group(const HostGroup& H, cudaStream_t s) {
   disc_group G;
-  G.table = H.dev_table;
-  G.stride = H.stride;
-  G.n = H.n;
-  G.nseg = 0;
+  H.fill(G);  // records are disc_copy2d items read in place (no staging)
   int64_t off = 0;
   for (int i = 0; i < H.n; ++i) {
     const disc_copy2d& it = H.at<disc_copy2d>(i);

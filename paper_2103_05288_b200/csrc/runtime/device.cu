@@ -2,6 +2,7 @@
 // events and the kernel launches the runtime flow issues.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -139,12 +140,64 @@ struct Ring {
   size_t cap = 0, head = 0;
   std::deque<std::tuple<size_t, size_t, cudaEvent_t>> inflight;  // [begin, end) until event
   std::vector<cudaEvent_t> spare;
+  // outgrown buffers, freed once the last event recorded while they were current is done
+  std::vector<std::tuple<unsigned char*, unsigned char*, cudaEvent_t>> retired;
 };
+constexpr size_t kRingMax = size_t{1} << 30;
+
+// Outgrown ring buffers are released without blocking the host: the device part
+// stream-ordered (cudaFreeAsync), the pinned host part only once its last user is done
+// and then kept for the process (cudaFreeHost would synchronise the device); growth is
+// geometric (x4 from 64 MB), so this happens a handful of times at most.
+void ring_collect(Ring& r, cudaStream_t st) {
+  for (size_t i = 0; i < r.retired.size();) {
+    auto& [h, d, ev] = r.retired[i];
+    if (d) {
+      cudaFreeAsync(d, st);
+      d = nullptr;
+    }
+    if (cudaEventQuery(ev) == cudaSuccess) {
+      r.spare.push_back(ev);
+      r.retired[i] = r.retired.back();
+      r.retired.pop_back();
+    } else {
+      ++i;
+    }
+  }
+}
 std::mutex g_ring_mu;
+int64_t g_copy_ns = 0, g_copy_bytes = 0;  // host profile (DISC_HOST_PROFILE)
 std::unordered_map<cudaStream_t, Ring> g_rings;
 
 cudaError_t ring_reserve(Ring& r, size_t n, cudaStream_t st, size_t* off) {
   n = (n + 255) / 256 * 256;
+  ring_collect(r, st);
+  {
+    // Would the next region have to wait for work still in flight?  Then grow instead
+    // (up to kRingMax): the host keeps running ahead of the device.
+    size_t b = r.head, e = r.head + n;
+    if (e > r.cap) {
+      b = 0;
+      e = n;
+    }
+    bool busy = false;
+    for (auto& f : r.inflight)
+      if (std::get<0>(f) < e && b < std::get<1>(f) && cudaEventQuery(std::get<2>(f)) != cudaSuccess) busy = true;
+    if (busy && r.cap < kRingMax && !r.inflight.empty()) {
+      cudaEvent_t last = std::get<2>(r.inflight.back());
+      r.retired.emplace_back(r.host, r.dev, last);  // 'last' is recorded after every user
+      r.inflight.pop_back();
+      for (auto& f : r.inflight) r.spare.push_back(std::get<2>(f));
+      r.inflight.clear();
+      const size_t nc = std::min(kRingMax, std::max(4 * r.cap, n));
+      r.host = r.dev = nullptr;
+      r.cap = 0;
+      r.head = 0;
+      if (cudaError_t x = cudaMallocHost(reinterpret_cast<void**>(&r.host), nc)) return x;
+      if (cudaError_t x = cudaMallocAsync(reinterpret_cast<void**>(&r.dev), nc, st)) return x;
+      r.cap = nc;
+    }
+  }
   if (n > r.cap) {  // grow: drain everything in flight, then reallocate
     for (auto& f : r.inflight) {
       cudaEventSynchronize(std::get<2>(f));
@@ -154,7 +207,7 @@ cudaError_t ring_reserve(Ring& r, size_t n, cudaStream_t st, size_t* off) {
     if (r.host) cudaFreeHost(r.host);
     if (r.dev) cudaFree(r.dev);
     r.host = r.dev = nullptr;
-    r.cap = std::max<size_t>({n, 2 * r.cap, size_t{16} << 20});
+    r.cap = std::max<size_t>({n, 4 * r.cap, size_t{64} << 20});
     r.head = 0;
     if (cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&r.host), r.cap)) return e;
     if (cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&r.dev), r.cap)) return e;
@@ -234,28 +287,28 @@ int64_t launch_weight(int kind, const void* l) {
   return R.K * R.R * (R.C > 0 ? R.C : 1);
 }
 
-// Issues one homogeneous group (<= DISC_MAX_GROUP members, same key) as grouped kernels.
-int issue_group(const GroupKey& k, const std::vector<const void*>& members, cudaStream_t st) {
-  const size_t stride = k.kind == 0 ? disc_dev::desc_bytes<disc_loop_launch>() : disc_dev::desc_bytes<disc_reduce_launch>();
-  const size_t size = k.kind == 0 ? sizeof(disc_loop_launch) : sizeof(disc_reduce_launch);
-  const int n = static_cast<int>(members.size());
-  std::lock_guard<std::mutex> lock(g_ring_mu);
-  Ring& r = g_rings[st];
-  size_t off = 0;
-  if (int rc = check(ring_reserve(r, stride * n, st, &off), "group table")) return rc;
-  for (int i = 0; i < n; ++i) {  // only the byte ranges the kernels read (desc_ranges.hpp)
-    if (k.kind == 0)
-      disc_desc::copy_used(reinterpret_cast<disc_loop_launch*>(r.host + off + i * stride),
-                           *static_cast<const disc_loop_launch*>(members[i]));
-    else
-      disc_desc::copy_used(reinterpret_cast<disc_reduce_launch*>(r.host + off + i * stride),
-                           *static_cast<const disc_reduce_launch*>(members[i]));
+// Grouped launch of one homogeneous group (<= DISC_MAX_GROUP members, same key) in three
+// steps: plan (compact record layout), pack (records into a pinned table), launch.
+void plan_group(const GroupKey& k, HostGroup& H) {
+  if (k.kind == 0)
+    disc_dev::group_segments<disc_loop_launch>(H.members, H.n, &H.nseg, H.seg, &H.stride);
+  else
+    disc_dev::group_segments<disc_reduce_launch>(H.members, H.n, &H.nseg, H.seg, &H.stride);
+}
+
+void pack_group(const HostGroup& H, unsigned char* dst) {  // compact records: only the ranges kernels read
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int i = 0; i < H.n; ++i) {
+    unsigned char* rec = dst + static_cast<size_t>(i) * H.stride;
+    const unsigned char* src = static_cast<const unsigned char*>(H.members[i]);
+    for (int s = 0; s < H.nseg; ++s) std::memcpy(rec + H.seg[s][2] * 16, src + H.seg[s][0] * 16, H.seg[s][1] * 16);
   }
-  (void)size;
-  if (int rc = check(cudaMemcpyAsync(r.dev + off, r.host + off, stride * n, cudaMemcpyHostToDevice, st), "group table upload"))
-    return rc;
-  const HostGroup H{r.dev + off, r.host + off, static_cast<int>(stride), n};
-  const void* first = members[0];
+  g_copy_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+  g_copy_bytes += static_cast<int64_t>(H.stride) * H.n;
+}
+
+int launch_group(const GroupKey& k, const HostGroup& H, cudaStream_t st) {
+  const void* first = H.members[0];
   int rc = 0;
   if (k.kind == 0) {
     const auto& L = *static_cast<const disc_loop_launch*>(first);
@@ -265,8 +318,8 @@ int issue_group(const GroupKey& k, const std::vector<const void*>& members, cuda
     rc = counted(k.entry ? k.entry->launch(first, R.vec, st, &H) : disc_launch::reduce(R, st, &H), "grouped row reduce");
   } else {
     bool finalize = false;
-    for (const void* m : members) {
-      const auto& R = *static_cast<const disc_reduce_launch*>(m);
+    for (int i = 0; i < H.n; ++i) {
+      const auto& R = *static_cast<const disc_reduce_launch*>(H.members[i]);
       if (R.K * R.C <= 0) continue;
       if (R.schedule == DISC_SCHED_COL_ATOMIC)
         if ((rc = check(cudaMemsetAsync(R.workspace, 0, sizeof(double) * R.K * R.C, st), "workspace memset"))) return rc;
@@ -277,27 +330,39 @@ int issue_group(const GroupKey& k, const std::vector<const void*>& members, cuda
     if (!rc && finalize) rc = counted(disc_launch::finalize_columns(R, st, &H), "grouped column finalize");
   }
   if (rc) return rc;
-  g_spec_launches.fetch_add(k.entry ? n : 0, std::memory_order_relaxed);
-  return check(ring_release(r, off, stride * n, st), "group table release");
+  g_spec_launches.fetch_add(k.entry ? H.n : 0, std::memory_order_relaxed);
+  return 0;
 }
 
-// Issues D2D copy items (reshape copies, concat parts) as grouped copy kernels.
-int issue_copies(const std::vector<disc_dev::disc_copy2d>& items, cudaStream_t st) {
-  for (size_t i0 = 0; i0 < items.size(); i0 += DISC_MAX_GROUP) {
-    const int n = static_cast<int>(std::min<size_t>(items.size() - i0, DISC_MAX_GROUP));
-    const size_t bytes = sizeof(disc_dev::disc_copy2d) * n;
-    std::lock_guard<std::mutex> lock(g_ring_mu);
-    Ring& r = g_rings[st];
-    size_t off = 0;
-    if (int rc = check(ring_reserve(r, bytes, st, &off), "copy table")) return rc;
-    std::memcpy(r.host + off, items.data() + i0, bytes);
-    if (int rc = check(cudaMemcpyAsync(r.dev + off, r.host + off, bytes, cudaMemcpyHostToDevice, st), "copy table upload"))
-      return rc;
-    const HostGroup H{r.dev + off, r.host + off, static_cast<int>(sizeof(disc_dev::disc_copy2d)), n};
-    if (int rc = counted(disc_launch::copy2d_group(H, st), "grouped copy")) return rc;
-    if (int rc = check(ring_release(r, off, bytes, st), "copy table release")) return rc;
-  }
-  return 0;
+// Stand-alone grouped launch (disc_cuda_launch_*_group): its own table upload.
+int issue_group(const GroupKey& k, const std::vector<const void*>& members, cudaStream_t st) {
+  HostGroup H{};
+  H.members = members.data();
+  H.n = static_cast<int>(members.size());
+  plan_group(k, H);
+  const size_t bytes = static_cast<size_t>(H.stride) * H.n;
+  std::lock_guard<std::mutex> lock(g_ring_mu);
+  Ring& r = g_rings[st];
+  size_t off = 0;
+  if (int rc = check(ring_reserve(r, bytes, st, &off), "group table")) return rc;
+  pack_group(H, r.host + off);
+  if (int rc = check(cudaMemcpyAsync(r.dev + off, r.host + off, bytes, cudaMemcpyHostToDevice, st), "group table upload"))
+    return rc;
+  H.dev_table = r.dev + off;
+  if (int rc = launch_group(k, H, st)) return rc;
+  return check(ring_release(r, off, bytes, st), "group table release");
+}
+
+// Grouped copy kernel over a table of disc_copy2d items already on the device.
+int launch_copies(const disc_dev::disc_copy2d* host_items, const unsigned char* dev_items, int n, cudaStream_t st) {
+  std::vector<const void*> ptrs(n);
+  for (int i = 0; i < n; ++i) ptrs[i] = host_items + i;
+  HostGroup H{};
+  H.members = ptrs.data();
+  H.n = n;
+  H.dev_table = dev_items;
+  H.stride = static_cast<int32_t>(sizeof(disc_dev::disc_copy2d));
+  return counted(disc_launch::copy2d_group(H, st), "grouped copy");
 }
 
 // Concat (eval_concat) as one 2-D copy per part.
@@ -383,7 +448,8 @@ struct Arena {
   size_t cap = 0, used = 0;
   unsigned char* data() { return buf.get(); }
   void clear() { used = 0; }
-  size_t take(size_t n) {  // 16 B aligned offset of n fresh bytes
+  size_t take(size_t n) {  // 16 B aligned offset of n fresh bytes (16 B granules: readable in whole granules)
+    n = (n + 15) / 16 * 16;
     const size_t off = (used + 15) / 16 * 16;
     if (off + n > cap) {
       const size_t nc = std::max(off + n, 2 * cap + (size_t{1} << 20));
@@ -707,12 +773,16 @@ int disc_cuda_queue_mark(int64_t bytes, int kernel, const char* schedule) {
 namespace {
 
 // Issues the queued work of `qs` (the calling thread's queue and/or detached ones) level
-// by level on qs[0]'s stream; records go to the calling thread.
+// by level on qs[0]'s stream; records go to the calling thread.  Three phases: plan every
+// level's actions (groups keyed by kernel instantiation, grouped copies, single ops) and
+// the size of every group's record table; pack all tables into ONE pinned ring region and
+// upload it with one copy; issue the actions -- so consecutive grouped kernels follow each
+// other directly (programmatic dependent launch chains them) instead of each waiting
+// behind its own table copy.
 int flush_queues(const std::vector<Queue*>& qs, int timing) {
   const cudaStream_t st = qs[0]->stream;
   t_q.records.clear();
   t_q.next_event = 0;
-  // schedule names of every queue, interned into the calling thread's table
   std::vector<std::vector<int>> remap(qs.size());
   auto intern = [&](const std::string& n) {
     for (size_t i = 0; i < t_q.names.size(); ++i)
@@ -723,6 +793,7 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
   for (size_t k = 0; k < qs.size(); ++k)
     for (const auto& n : qs[k]->names) remap[k].push_back(intern(n));
   auto name_of = [&](size_t k, int sched) { return sched >= 0 ? remap[k][sched] : -1; };
+  const int copy_name = intern("copy");
   struct ReqRef {
     size_t q;
     const std::vector<QOp>* ops;
@@ -734,33 +805,38 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
       reqs.push_back({k, &r});
       levels = std::max(levels, r.size());
     }
-  auto begin_rec = [&](int level, int members, int64_t bytes, int kernel, int sched) {
-    QRecord rec{level, members, kernel, sched, bytes};
-    if (timing) {
-      rec.a = queue_event();
-      rec.b = queue_event();
-      cudaEventRecord(rec.a, st);
-    }
-    t_q.records.push_back(rec);
-  };
-  auto end_rec = [&] {
-    if (timing) cudaEventRecord(t_q.records.back().b, st);
-  };
-  const int copy_name = intern("copy");
   struct FOp {
     const QOp* op;
     const unsigned char* p;
     size_t q;
   };
-  int rc = 0;
-  for (size_t lv = 0; lv < levels && !rc; ++lv) {
-    // fused launches of this level, grouped by kernel instantiation; D2D copies and
-    // concats as one grouped copy; everything else issued in request order
+  // ---- phase 1: plan ----
+  enum AKind { kSingle, kAlone, kGroup, kCopies };
+  struct Action {
+    AKind kind;
+    int level, members = 1, kernel = -1, sched = -1;
+    int64_t bytes = 0;
+    FOp f{};                                   // kSingle / kAlone
+    int fkind = 0;                             // kAlone: 0 loop, 1 reduce
+    GroupKey gk;                               // kGroup
+    std::vector<const void*> ptrs;             // kGroup members
+    HostGroup H{};                             // kGroup (members/n set when issued)
+    std::vector<disc_dev::disc_copy2d> items;  // kCopies
+    size_t table = 0, table_bytes = 0;         // offset in the uploaded region
+  };
+  std::vector<Action> acts;
+  size_t total = 0;
+  auto place = [&](Action& a, size_t bytes) {
+    a.table = total;
+    a.table_bytes = bytes;
+    total += (bytes + 255) / 256 * 256;
+  };
+  for (size_t lv = 0; lv < levels; ++lv) {
     std::map<GroupKey, std::vector<FOp>> groups[2];
     std::vector<GroupKey> order[2];
     std::vector<FOp> alone[2];
-    std::vector<disc_dev::disc_copy2d> copies;
-    int64_t copy_bytes = 0;
+    Action copies{kCopies, static_cast<int>(lv)};
+    copies.sched = copy_name;
     for (const ReqRef& rr : reqs) {
       if (lv >= rr.ops->size()) continue;
       const QOp& op = (*rr.ops)[lv];
@@ -783,75 +859,149 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
           (op.kind == kQMemcpy && (reinterpret_cast<const QMemcpy*>(p)->kind & 3) == 2 &&
            reinterpret_cast<const QMemcpy*>(p)->bytes % 4 == 0)) {
         if (op.kind == kQConcat) {
-          concat_items(*reinterpret_cast<const disc_concat_launch*>(p), copies);
+          concat_items(*reinterpret_cast<const disc_concat_launch*>(p), copies.items);
         } else {
           const auto& c = *reinterpret_cast<const QMemcpy*>(p);
           const int64_t n = static_cast<int64_t>(c.bytes / 4);
-          copies.push_back({static_cast<const float*>(c.src), static_cast<float*>(c.dst), 1, n, n, n});
+          copies.items.push_back({static_cast<const float*>(c.src), static_cast<float*>(c.dst), 1, n, n, n});
         }
-        copy_bytes += op.bytes;
+        copies.bytes += op.bytes;
         continue;
       }
-      begin_rec(static_cast<int>(lv), 1, op.bytes, op.kernel, name_of(rr.q, op.sched));
-      switch (op.kind) {
-        case kQPad: rc = counted(disc_launch::pad(*reinterpret_cast<const disc_pad_launch*>(p), st), "launch pad"); break;
-        case kQGemm: {
-          const auto& g = *reinterpret_cast<const QGemm*>(p);
-          rc = counted(disc_launch::gemm(g.m, g.k, g.n, g.a, g.b, g.c, st), "launch gemm");
-          break;
-        }
-        case kQMemcpy: {
-          static const cudaMemcpyKind kinds[] = {cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost,
-                                                 cudaMemcpyDeviceToDevice, cudaMemcpyDefault};
-          const auto& c = *reinterpret_cast<const QMemcpy*>(p);
-          rc = check(cudaMemcpyAsync(c.dst, c.src, c.bytes, kinds[c.kind & 3], st), "cudaMemcpyAsync");
-          break;
-        }
-        case kQMemset: {
-          const auto& m = *reinterpret_cast<const QMemset*>(p);
-          rc = check(cudaMemsetAsync(m.dst, m.value, m.bytes, st), "cudaMemsetAsync");
-          break;
-        }
-      }
-      end_rec();
-      if (rc) break;
+      Action a{kSingle, static_cast<int>(lv)};
+      a.f = {&op, p, rr.q};
+      a.bytes = op.bytes;
+      a.kernel = op.kernel;
+      a.sched = name_of(rr.q, op.sched);
+      acts.push_back(std::move(a));
     }
-    if (!rc && !copies.empty()) {
-      begin_rec(static_cast<int>(lv), static_cast<int>(copies.size()), copy_bytes, -1, copy_name);
-      rc = issue_copies(copies, st);
-      end_rec();
+    for (size_t i0 = 0; i0 < copies.items.size(); i0 += DISC_MAX_GROUP) {
+      Action c{kCopies, static_cast<int>(lv)};
+      c.sched = copy_name;
+      c.bytes = i0 == 0 ? copies.bytes : 0;
+      c.items.assign(copies.items.begin() + i0,
+                     copies.items.begin() + std::min(copies.items.size(), i0 + DISC_MAX_GROUP));
+      c.members = static_cast<int>(c.items.size());
+      place(c, sizeof(disc_dev::disc_copy2d) * c.items.size());
+      acts.push_back(std::move(c));
     }
-    for (int kind = 0; kind < 2 && !rc; ++kind) {
+    for (int kind = 0; kind < 2; ++kind) {
       for (const FOp& f : alone[kind]) {
-        begin_rec(static_cast<int>(lv), 1, f.op->bytes, f.op->kernel, name_of(f.q, f.op->sched));
-        rc = kind == 0 ? disc_cuda_launch_loop(reinterpret_cast<const disc_loop_launch*>(f.p), st)
-                       : disc_cuda_launch_reduce(reinterpret_cast<const disc_reduce_launch*>(f.p), st);
-        end_rec();
-        if (rc) break;
+        Action a{kAlone, static_cast<int>(lv)};
+        a.f = f;
+        a.fkind = kind;
+        a.bytes = f.op->bytes;
+        a.kernel = f.op->kernel;
+        a.sched = name_of(f.q, f.op->sched);
+        acts.push_back(std::move(a));
       }
       for (const GroupKey& k : order[kind]) {
-        if (rc) break;
         auto& m = groups[kind][k];
-        std::stable_sort(m.begin(), m.end(), [&](const FOp& a, const FOp& b) {
-          return launch_weight(kind, a.p) > launch_weight(kind, b.p);
+        std::stable_sort(m.begin(), m.end(), [&](const FOp& x, const FOp& y) {
+          return launch_weight(kind, x.p) > launch_weight(kind, y.p);
         });
-        for (size_t i = 0; i < m.size() && !rc; i += DISC_MAX_GROUP) {
+        for (size_t i = 0; i < m.size(); i += DISC_MAX_GROUP) {
           const size_t e = std::min(m.size(), i + DISC_MAX_GROUP);
-          std::vector<const void*> chunk;
-          int64_t bytes = 0;
-          int kernel = m[i].op->kernel, sched = name_of(m[i].q, m[i].op->sched);
+          Action g{kGroup, static_cast<int>(lv)};
+          g.gk = k;
+          g.kernel = m[i].op->kernel;
+          g.sched = name_of(m[i].q, m[i].op->sched);
           for (size_t j = i; j < e; ++j) {
-            chunk.push_back(m[j].p);
-            bytes += m[j].op->bytes;
-            if (m[j].op->kernel != kernel) kernel = -1;
-            if (name_of(m[j].q, m[j].op->sched) != sched) sched = -1;
+            g.ptrs.push_back(m[j].p);
+            g.bytes += m[j].op->bytes;
+            if (m[j].op->kernel != g.kernel) g.kernel = -1;
+            if (name_of(m[j].q, m[j].op->sched) != g.sched) g.sched = -1;
           }
-          begin_rec(static_cast<int>(lv), static_cast<int>(chunk.size()), bytes, kernel, sched);
-          rc = issue_group(k, chunk, st);
-          end_rec();
+          g.members = static_cast<int>(g.ptrs.size());
+          g.H.members = g.ptrs.data();
+          g.H.n = g.members;
+          plan_group(k, g.H);
+          place(g, static_cast<size_t>(g.H.stride) * g.H.n);
+          acts.push_back(std::move(g));
         }
       }
     }
+  }
+  // ---- phase 2: pack every table into one ring region, one upload ----
+  std::unique_lock<std::mutex> lock(g_ring_mu);
+  Ring& ring = g_rings[st];
+  size_t base = 0;
+  int rc = 0;
+  if (total > 0) {
+    rc = check(ring_reserve(ring, total, st, &base), "group tables");
+    if (!rc) {
+      for (Action& a : acts) {
+        if (a.kind == kGroup) {
+          a.H.members = a.ptrs.data();  // (vector moved into acts)
+          pack_group(a.H, ring.host + base + a.table);
+        } else if (a.kind == kCopies) {
+          std::memcpy(ring.host + base + a.table, a.items.data(), a.table_bytes);
+        }
+      }
+      rc = check(cudaMemcpyAsync(ring.dev + base, ring.host + base, total, cudaMemcpyHostToDevice, st),
+                 "group tables upload");
+    }
+  }
+  lock.unlock();
+  // ---- phase 3: issue ----
+  auto begin_rec = [&](const Action& a) {
+    QRecord rec{a.level, a.members, a.kernel, a.sched, a.bytes};
+    if (timing) {
+      rec.a = queue_event();
+      rec.b = queue_event();
+      cudaEventRecord(rec.a, st);
+    }
+    t_q.records.push_back(rec);
+  };
+  auto end_rec = [&] {
+    if (timing) cudaEventRecord(t_q.records.back().b, st);
+  };
+  for (Action& a : acts) {
+    if (rc) break;
+    begin_rec(a);
+    switch (a.kind) {
+      case kGroup:
+        a.H.members = a.ptrs.data();
+        a.H.dev_table = ring.dev + base + a.table;
+        rc = launch_group(a.gk, a.H, st);
+        break;
+      case kCopies:
+        rc = launch_copies(a.items.data(), ring.dev + base + a.table, a.members, st);
+        break;
+      case kAlone:
+        rc = a.fkind == 0 ? disc_cuda_launch_loop(reinterpret_cast<const disc_loop_launch*>(a.f.p), st)
+                          : disc_cuda_launch_reduce(reinterpret_cast<const disc_reduce_launch*>(a.f.p), st);
+        break;
+      case kSingle: {
+        const unsigned char* p = a.f.p;
+        switch (a.f.op->kind) {
+          case kQPad: rc = counted(disc_launch::pad(*reinterpret_cast<const disc_pad_launch*>(p), st), "launch pad"); break;
+          case kQGemm: {
+            const auto& g = *reinterpret_cast<const QGemm*>(p);
+            rc = counted(disc_launch::gemm(g.m, g.k, g.n, g.a, g.b, g.c, st), "launch gemm");
+            break;
+          }
+          case kQMemcpy: {
+            static const cudaMemcpyKind kinds[] = {cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost,
+                                                   cudaMemcpyDeviceToDevice, cudaMemcpyDefault};
+            const auto& c = *reinterpret_cast<const QMemcpy*>(p);
+            rc = check(cudaMemcpyAsync(c.dst, c.src, c.bytes, kinds[c.kind & 3], st), "cudaMemcpyAsync");
+            break;
+          }
+          case kQMemset: {
+            const auto& m = *reinterpret_cast<const QMemset*>(p);
+            rc = check(cudaMemsetAsync(m.dst, m.value, m.bytes, st), "cudaMemsetAsync");
+            break;
+          }
+        }
+        break;
+      }
+    }
+    end_rec();
+  }
+  if (total > 0) {
+    std::lock_guard<std::mutex> l2(g_ring_mu);
+    if (!rc) rc = check(ring_release(ring, base, total, st), "group tables release");
   }
   for (Queue* q : qs) {
     for (void* p : q->frees)
@@ -887,6 +1037,13 @@ void* disc_cuda_queue_detach(void) {
   t_q.arena.clear();
   t_q.frees.clear();
   return q;
+}
+
+int64_t disc_cuda_host_profile(int64_t* table_bytes) {
+  if (table_bytes) *table_bytes = g_copy_bytes;
+  const int64_t ns = g_copy_ns;
+  g_copy_ns = g_copy_bytes = 0;
+  return ns;
 }
 
 int disc_cuda_queue_flush_detached(void* const* queues, int n, int timing) {

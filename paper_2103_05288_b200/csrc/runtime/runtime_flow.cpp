@@ -189,12 +189,15 @@ struct DeviceExecutor::Pool {
         }
       });
   }
-  void run(const std::function<void(int)>& f) {  // f(w) on every worker; returns when all finished
-    std::unique_lock<std::mutex> l(mu);
+  void start(const std::function<void(int)>& f) {  // f(w) on every worker, asynchronously
+    std::lock_guard<std::mutex> l(mu);
     job = f;
     pending = static_cast<int>(threads.size());
     ++gen;
     cv.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> l(mu);
     done.wait(l, [&] { return pending == 0; });
   }
   ~Pool() {
@@ -268,7 +271,8 @@ void DeviceExecutor::run_grouped_batch(int n, const CompiledPlan* const* plans, 
   std::vector<void*> handles(T, nullptr);
   std::vector<std::exception_ptr> errs(T);
   for (int w = 1; w < T; ++w) subs_[w - 1]->set_timing(false);
-  pool_->run([&](int w) {
+  const auto t_start = Clock::now();
+  pool_->start([&](int w) {
     if (w + 1 >= T) return;
     DeviceExecutor& ex = *subs_[w];
     try {
@@ -283,12 +287,14 @@ void DeviceExecutor::run_grouped_batch(int n, const CompiledPlan* const* plans, 
       if (!errs[w + 1]) errs[w + 1] = std::current_exception();
     }
   });
-  begin_grouped();
-  try {
+  try {  // this thread's range, concurrently with the workers
+    begin_grouped();
     run_requests(bounds[0], bounds[1], plans, serials, offs, names, data, dims, ranks, on_host);
   } catch (...) {
     errs[0] = std::current_exception();
   }
+  pool_->wait();
+  t_group_ = t_start;
   // merged flush: this thread's queue + the workers' detached ones
   grouped_ = false;
   int rc = issue_small_inputs();
@@ -299,10 +305,15 @@ void DeviceExecutor::run_grouped_batch(int n, const CompiledPlan* const* plans, 
   const int frc = disc_cuda_queue_flush_detached(hs.data(), static_cast<int>(hs.size()), group_timing_ ? 1 : 0);
   if (rc == 0) rc = frc;
   static const bool prof = std::getenv("DISC_HOST_PROFILE") != nullptr;
-  if (prof)
-    std::fprintf(stderr, "[disc host] grouped call: %d requests on %d threads, flow %.3f ms, flush %.3f ms\n", n, T,
-                 std::chrono::duration<double, std::milli>(t_flush - t_group_).count(),
-                 std::chrono::duration<double, std::milli>(Clock::now() - t_flush).count());
+  if (prof) {
+    int64_t tb = 0;
+    const int64_t cns = disc_cuda_host_profile(&tb);
+    std::fprintf(stderr,
+                 "[disc host] grouped call: %d requests on %d threads, flow %.3f ms, flush %.3f ms "
+                 "(tables %.3f ms, %.1f MB)\n",
+                 n, T, std::chrono::duration<double, std::milli>(t_flush - t_group_).count(),
+                 std::chrono::duration<double, std::milli>(Clock::now() - t_flush).count(), cns / 1e6, tb / 1e6);
+  }
   alloc_.set_defer(false);
   for (int w = 1; w < T; ++w) subs_[w - 1]->finish_detached();
   // request outputs / stats in request order
