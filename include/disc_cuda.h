@@ -36,6 +36,8 @@ enum disc_op {
   DISC_OP_REDVAL,     /* the current row's reduce result (row schedule only) */
   DISC_OP_RCPVAL,     /* 1 / REDVAL (IEEE reciprocal, once per row): x / REDVAL is lowered
                          to x * RCPVAL in fused epilogues (<= 1.5 ulp from the quotient) */
+  DISC_OP_FDIV,       /* a * rcp.approx(b): Div inside multi-member (fused) groups, <= 2 ulp
+                         (IEEE a / b stays the single-op plans' semantics, bit-exact) */
 };
 
 /* Pre-decoded device opcodes: operand sources (accumulator A / slot S) are folded into
@@ -50,7 +52,8 @@ enum disc_opcode {
   DISC_I_RCPVAL = 6,    /* acc = 1 / row reduce result */
   DISC_I_BIN = 8,       /* 8 + 4*(op-ADD) + mode, mode 0 AA, 1 AS, 2 SA, 3 SS (a op b) */
   DISC_I_UN = 28,       /* 28 + 2*(op-EXP) + mode, mode 0 A, 1 S */
-  DISC_I_END = 34,
+  DISC_I_FDIV = 34,     /* 34 + mode (as DISC_I_BIN): fused-group division */
+  DISC_I_END = 38,
 };
 #define DISC_F_SLOT 1   /* also keep acc in slot dst */
 #define DISC_F_OUT 2    /* also store acc to outs[out] */

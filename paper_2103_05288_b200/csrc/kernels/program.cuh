@@ -29,12 +29,19 @@ struct Vec<4> {
 
 __device__ __forceinline__ float op_max(float a, float b) { return (a < b) ? b : a; }  // std::max(a,b)
 
+__device__ __forceinline__ float rcp_approx(float b) {
+  float r;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(b));  // rel. error 2^-23; 1/0 = inf, 1/inf = 0
+  return r;
+}
+
 template <int OP>
 __device__ __forceinline__ float bin1(float a, float b) {
   if constexpr (OP == 0) return __fadd_rn(a, b);
   if constexpr (OP == 1) return __fsub_rn(a, b);
   if constexpr (OP == 2) return __fmul_rn(a, b);
   if constexpr (OP == 3) return __fdiv_rn(a, b);  // IEEE: unfused plans are bit-exact
+  if constexpr (OP == 5) return __fmul_rn(a, rcp_approx(b));  // DISC_OP_FDIV (fused groups)
   return op_max(a, b);
 }
 #ifndef DISC_FAST_TANH
@@ -421,6 +428,10 @@ __device__ __forceinline__ void run_tile(const disc_program& P, const Ctx& t,
       DISC_UN_CASES(0)
       DISC_UN_CASES(1)
       DISC_UN_CASES(2)
+      case DISC_I_FDIV + 0: DISC_FOR_C acc[c] = bin<5>(acc[c], acc[c]); break;
+      case DISC_I_FDIV + 1: DISC_FOR_C acc[c] = bin<5>(acc[c], DISC_S(in.b, c)); break;
+      case DISC_I_FDIV + 2: DISC_FOR_C acc[c] = bin<5>(DISC_S(in.a, c), acc[c]); break;
+      case DISC_I_FDIV + 3: DISC_FOR_C acc[c] = bin<5>(DISC_S(in.a, c), DISC_S(in.b, c)); break;
       default:
         break;
     }

@@ -144,7 +144,18 @@ class ProgramBuilder {
       if (rcp_ < 0) rcp_ = push({DISC_OP_RCPVAL, -1, -1, -1});
       return push({DISC_OP_MUL, a, rcp_, -1});
     }
+    if (code == DISC_OP_DIV && fast_div_) return push({DISC_OP_FDIV, a, b, -1});
     return push({code, a, b, -1});
+  }
+  // Programs of multi-member (fused) groups divide with a * rcp.approx(b) (<= 2 ulp;
+  // the north-star tolerance is 1e-5); single-op plans keep IEEE division (bit-exact
+  // against the reference, test_executor.cpp:317-332).  DISC_FAST_DIV=0 disables.
+  void set_fast_div(bool on) {
+    static const bool enabled = [] {
+      const char* e = std::getenv("DISC_FAST_DIV");
+      return !e || std::atoi(e) != 0;
+    }();
+    fast_div_ = on && enabled;
   }
   int redval() {
     if (red_ < 0) red_ = push({DISC_OP_REDVAL, -1, -1, -1});
@@ -226,6 +237,9 @@ class ProgramBuilder {
         case DISC_OP_EXP: case DISC_OP_TANH: case DISC_OP_NEG:
           I.op = static_cast<uint8_t>(DISC_I_UN + 2 * (x.code - DISC_OP_EXP) + (sa ? 1 : 0));
           break;
+        case DISC_OP_FDIV:
+          I.op = static_cast<uint8_t>(DISC_I_FDIV + (sa ? 2 : 0) + (sb ? 1 : 0));
+          break;
         default:
           I.op = static_cast<uint8_t>(DISC_I_BIN + 4 * (x.code - DISC_OP_ADD) + (sa ? 2 : 0) + (sb ? 1 : 0));
           break;
@@ -270,6 +284,7 @@ class ProgramBuilder {
   std::vector<std::pair<int, float*>> outs_;
   int red_ = -1;
   int rcp_ = -1;
+  bool fast_div_ = false;
   int push(Ins i) {
     ins_.push_back(i);
     return static_cast<int>(ins_.size()) - 1;
@@ -879,6 +894,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     for (int t = 0; t < n; ++t)
       if (numel(B.dims[t]) != N) throw NotFusible{"member size differs from the space"};
     ProgramBuilder pb;
+    pb.set_fast_div(B.art.tape.size() > 1);
     Lowering lw(B, pb, nullptr, nullptr);
     for (size_t o = 0; o < art.output_tape_indices.size(); ++o)
       pb.output(lw.value(art.output_tape_indices[o]), outs[o].ptr);
@@ -923,6 +939,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
   Built pre;
   {
     ProgramBuilder pb;
+    pb.set_fast_div(B.art.tape.size() > 1);
     Lowering lw(B, pb, nullptr, nullptr);
     for (size_t o = 0; o < art.output_tape_indices.size(); ++o) {
       int t = art.output_tape_indices[o];
@@ -956,6 +973,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
       Map row = canonical(Map{{R.K, R.R}, {1, 0}, 0});
       try {
         ProgramBuilder pb;
+    pb.set_fast_div(B.art.tape.size() > 1);
         Lowering lw(B, pb, nullptr, &row);
         // The epilogue reads the reduce argument back from shared memory (written by the
         // reduce pass) instead of recomputing it; rows up to 4096 keep every cache slot
@@ -974,6 +992,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     if (!post_fused) {
       if (!red_ptr) throw NotFusible{"no reduce buffer"};
       ProgramBuilder pb;
+    pb.set_fast_div(B.art.tape.size() > 1);
       Lowering lw(B, pb, red_ptr, nullptr);
       int64_t Npost = 0;
       for (size_t o = 0; o < art.output_tape_indices.size(); ++o) {

