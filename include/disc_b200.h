@@ -167,6 +167,12 @@ int disc_executor_run_kernel(disc_executor e, disc_plan p, int kernel, int versi
  * device programs of every fused launch as JSON (used by tools/gen_patterns.py). */
 int disc_plan_capture_programs(disc_plan p, int n_inputs, const char* const* names,
                                const int64_t* const* dims, const int* ranks, char** json);
+/* Grouping dry run (host only, no device): runs disc_executor_run_grouped's host flow for
+ * the requests (device-resident inputs of the given dims) in capture mode and returns the
+ * flush plan as JSON: one entry per issued action {level, action: group|copies|single|alone,
+ * members, bytes, kernel, schedule[, table_bytes, generated, order]}.  Free with disc_free. */
+int disc_plan_group_dry_run(int n_requests, const disc_plan* plans, const int* input_offsets, const char* const* names,
+                            const int64_t* const* dims, const int* ranks, int host_threads, char** json);
 /* Host-side cost of one run (capture mode: no device work), microseconds per run. */
 int disc_plan_host_overhead(disc_plan p, int n_inputs, const char* const* names,
                             const int64_t* const* dims, const int* ranks, int iters, double* us_per_run);

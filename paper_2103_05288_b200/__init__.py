@@ -4,7 +4,7 @@ Host: clean-room C++ compile pipeline (graph -> DHLO -> constraints -> fusion ->
 byte-identical plans to the reference.  Device: sm_100a fused tape kernels behind a
 C ABI (include/disc_b200.h, include/disc_cuda.h).  See DESIGN.md.
 """
-from .api import (capture_programs, set_pdl, set_specialization, specialized_launches, CompileOptions, CompiledPlan, Compiler, DeviceBuffer, DiscError, ExecResult, ExecStats,
+from .api import (capture_programs, group_dry_run, set_pdl, set_specialization, specialized_launches, CompileOptions, CompiledPlan, Compiler, DeviceBuffer, DiscError, ExecResult, ExecStats,
                   Executor, cache_key, compile_graph, cuda_available, dhlo_roundtrip, dump_stage, guard_passes,
                   kernel_launches, lib, lower_dhlo_json, static_specialize)
 
@@ -13,7 +13,7 @@ from .dispatch import Dispatcher, shard
 
 __all__ = [
     "Dispatcher", "dispatch", "shard",
-    "capture_programs", "set_pdl", "set_specialization", "specialized_launches",
+    "capture_programs", "group_dry_run", "set_pdl", "set_specialization", "specialized_launches",
     "CompileOptions", "CompiledPlan", "Compiler", "DeviceBuffer", "DiscError", "ExecResult", "ExecStats",
     "Executor", "cache_key", "compile_graph", "cuda_available", "dhlo_roundtrip", "dump_stage", "guard_passes",
     "kernel_launches", "lib", "lower_dhlo_json", "static_specialize",

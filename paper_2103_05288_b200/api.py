@@ -102,6 +102,7 @@ def _declare(L: C.CDLL) -> None:
         "disc_guard_passes": ([vp, i32, i32, P(i64), i32], i32),
         "disc_plan_capture_programs": ([vp, i32, P(cp), P(vp), P(i32), P(vp)], i32),
         "disc_plan_host_overhead": ([vp, i32, P(cp), P(vp), P(i32), i32, P(C.c_double)], i32),
+        "disc_plan_group_dry_run": ([i32, P(vp), P(i32), P(cp), P(vp), P(i32), i32, P(vp)], i32),
         "disc_cuda_set_specialization": ([i32], i32),
         "disc_cuda_specialized_launches": ([], i64),
         "disc_cuda_num_specializations": ([], i32),
@@ -637,6 +638,28 @@ def host_overhead_us(plan: CompiledPlan, input_shapes: Dict[str, Sequence[int]],
     us = C.c_double()
     _check(lib().disc_plan_host_overhead(plan._h, k, c_names, c_dims, c_ranks, iters, C.byref(us)))
     return us.value
+
+
+def group_dry_run(requests: Sequence[Tuple[CompiledPlan, Dict[str, Sequence[int]]]], host_threads: int = 1) -> list:
+    """Host-only flush plan of disc_executor_run_grouped for (plan, {input: shape}) requests
+    (no device needed): one dict per issued action (grouped launches with their members'
+    work in issue order, grouped copies, single ops)."""
+    names, dims, ranks, offs, plans, keep = [], [], [], [0], [], []
+    for plan, shapes in requests:
+        for k, shp in shapes.items():
+            d = np.array(shp, dtype=np.int64)
+            keep.append(d)
+            names.append(k.encode())
+            dims.append(d.ctypes.data)
+            ranks.append(d.size)
+        offs.append(len(names))
+        plans.append(plan._h)
+    m, t = len(requests), max(len(names), 1)
+    out = C.c_void_p()
+    _check(lib().disc_plan_group_dry_run(m, (C.c_void_p * max(m, 1))(*plans), (C.c_int * (m + 1))(*offs),
+                                         (C.c_char_p * t)(*names), (C.c_void_p * t)(*dims), (C.c_int * t)(*ranks),
+                                         int(host_threads), C.byref(out)))
+    return json.loads(_take(out))
 
 
 def set_specialization(enabled: bool) -> None:

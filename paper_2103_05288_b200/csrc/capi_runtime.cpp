@@ -315,6 +315,33 @@ int disc_plan_capture_programs(disc_plan p, int n, const char* const* names, con
   return rc;
 }
 
+int disc_plan_group_dry_run(int n_requests, const disc_plan* plans, const int* input_offsets, const char* const* names,
+                            const int64_t* const* dims, const int* ranks, int host_threads, char** json) {
+  disc_cuda_set_capture(1);
+  int rc = guard([&] {
+    rt::DeviceExecutor ex(0, nullptr);
+    ex.set_host_threads(host_threads);
+    const int total = input_offsets[n_requests];
+    std::vector<const void*> data(std::max(total, 1));
+    for (int k = 0; k < total; ++k) {
+      void* fake = nullptr;
+      disc_cuda_malloc(static_cast<size_t>(bytes_of(dims[k], ranks[k])), nullptr, &fake);
+      data[k] = fake;
+    }
+    std::vector<const CompiledPlan*> ps(n_requests);
+    std::vector<uint64_t> serials(n_requests);
+    for (int r = 0; r < n_requests; ++r) {
+      ps[r] = plans[r]->plan.get();
+      serials[r] = plans[r]->serial;
+    }
+    disc_cuda_set_capture(1);  // drop the programs recorded so far: only the flush plan
+    ex.run_grouped_batch(n_requests, ps.data(), serials.data(), input_offsets, names, data.data(), dims, ranks, false);
+    disc_cuda_capture_records(json);
+  });
+  disc_cuda_set_capture(0);
+  return rc;
+}
+
 int disc_plan_host_overhead(disc_plan p, int n, const char* const* names, const int64_t* const* dims,
                             const int* ranks, int iters, double* us_per_run) {
   disc_cuda_set_capture(2);

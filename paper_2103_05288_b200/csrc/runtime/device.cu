@@ -60,7 +60,7 @@ bool g_spec_enabled = true;
 // no-ops, allocations return fake aligned addresses, launches are recorded.
 bool g_capture = false;
 bool g_capture_record = true;  // capture mode 2: dry run without recording (host timing)
-uint64_t g_fake_next = uint64_t{1} << 36;
+std::atomic<uint64_t> g_fake_next{uint64_t{1} << 36};
 std::vector<std::string> g_records;
 
 uint64_t mix(uint64_t h, uint64_t v) {
@@ -550,8 +550,7 @@ int disc_cuda_device_synchronize(void) { return check(cudaDeviceSynchronize(), "
 
 int disc_cuda_malloc(size_t bytes, void* stream, void** dptr) {
   if (g_capture) {
-    *dptr = reinterpret_cast<void*>(g_fake_next);
-    g_fake_next += (bytes + 4095) / 4096 * 4096 + 4096;
+    *dptr = reinterpret_cast<void*>(g_fake_next.fetch_add((bytes + 4095) / 4096 * 4096 + 4096));
     return 0;
   }
   return check(cudaMallocAsync(dptr, bytes ? bytes : 16, S(stream)), "cudaMallocAsync");
@@ -568,27 +567,28 @@ int disc_cuda_host_alloc(size_t bytes, void** hptr) { return check(cudaMallocHos
 int disc_cuda_host_free(void* hptr) { return check(cudaFreeHost(hptr), "cudaFreeHost"); }
 
 int disc_cuda_memcpy(void* dst, const void* src, size_t bytes, int kind, void* stream) {
-  if (!bytes || g_capture) return 0;
+  if (!bytes) return 0;
   if (queued(stream) && !(kind & DISC_MEMCPY_NOW)) {
     enqueue(kQMemcpy, QMemcpy{dst, src, bytes, kind});
     return 0;
   }
+  if (g_capture) return 0;
   static const cudaMemcpyKind kinds[] = {cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost, cudaMemcpyDeviceToDevice,
                                          cudaMemcpyDefault};
   return check(cudaMemcpyAsync(dst, src, bytes, kinds[kind & 3], S(stream)), "cudaMemcpyAsync");
 }
 int disc_cuda_memset(void* dst, int value, size_t bytes, void* stream) {
-  if (g_capture) return 0;
   if (queued(stream)) {
     if (bytes) enqueue(kQMemset, QMemset{dst, value, bytes});
     return 0;
   }
+  if (g_capture) return 0;
   return check(cudaMemsetAsync(dst, value, bytes, S(stream)), "cudaMemsetAsync");
 }
 
 int disc_cuda_event_create(void** ev) {
   if (g_capture) {
-    *ev = reinterpret_cast<void*>(g_fake_next++);
+    *ev = reinterpret_cast<void*>(g_fake_next.fetch_add(16));
     return 0;
   }
   cudaEvent_t e;
@@ -616,7 +616,7 @@ int disc_cuda_event_elapsed_ms(void* a, void* b, float* ms) {
 
 int disc_cuda_launch_loop(const disc_loop_launch* l, void* stream) {
   if (l->total <= 0) return 0;
-  if (queued(stream) && !g_capture) {
+  if (queued(stream)) {  // (capture mode too: the grouping dry run)
     enqueue(kQLoop, *l);
     return 0;
   }
@@ -635,7 +635,7 @@ int disc_cuda_launch_loop(const disc_loop_launch* l, void* stream) {
 }
 
 int disc_cuda_launch_reduce(const disc_reduce_launch* l, void* stream) {
-  if (queued(stream) && !g_capture) {
+  if (queued(stream)) {
     enqueue(kQReduce, *l);
     return 0;
   }
@@ -669,28 +669,28 @@ int disc_cuda_launch_reduce(const disc_reduce_launch* l, void* stream) {
 }
 
 int disc_cuda_launch_pad(const disc_pad_launch* l, void* stream) {
-  if (g_capture) return 0;
   if (l->total <= 0) return 0;
   if (queued(stream)) {
     enqueue(kQPad, *l);
     return 0;
   }
+  if (g_capture) return 0;
   return counted(disc_launch::pad(*l, S(stream)), "launch pad");
 }
 int disc_cuda_launch_concat(const disc_concat_launch* l, void* stream) {
-  if (g_capture) return 0;
   if (queued(stream)) {
     enqueue(kQConcat, *l);
     return 0;
   }
+  if (g_capture) return 0;
   return counted(disc_launch::concat(*l, S(stream)), "launch concat");
 }
 int disc_cuda_gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c, void* stream) {
-  if (g_capture) return 0;
   if (queued(stream)) {
     enqueue(kQGemm, QGemm{m, k, n, a, b, c});
     return 0;
   }
+  if (g_capture) return 0;
   return counted(disc_launch::gemm(m, k, n, a, b, c, S(stream)), "launch gemm");
 }
 int disc_cuda_fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, void* stream) {
@@ -921,6 +921,29 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
         }
       }
     }
+  }
+  if (g_capture) {  // grouping dry run (host only): describe the actions, issue nothing
+    static const char* kinds[] = {"single", "alone", "group", "copies"};
+    for (const Action& a : acts) {
+      std::string sched = a.sched >= 0 ? t_q.names[a.sched] : "mixed";
+      std::string j = "{\"level\":" + std::to_string(a.level) + ",\"action\":\"" + kinds[a.kind] +
+                      "\",\"members\":" + std::to_string(a.members) + ",\"bytes\":" + std::to_string(a.bytes) +
+                      ",\"kernel\":" + std::to_string(a.kernel) + ",\"schedule\":\"" + sched + "\"";
+      if (a.kind == kGroup) {
+        j += ",\"table_bytes\":" + std::to_string(a.table_bytes) + ",\"generated\":" + (a.gk.entry ? "true" : "false") +
+             ",\"order\":[";
+        for (size_t i = 0; i < a.ptrs.size(); ++i)
+          j += (i ? "," : "") + std::to_string(launch_weight(a.gk.kind == 0 ? 0 : 1, a.ptrs[i]));
+        j += "]";
+      }
+      g_records.push_back(j + "}");
+    }
+    for (Queue* q : qs) {
+      q->frees.clear();
+      q->reqs.clear();
+      q->arena.clear();
+    }
+    return 0;
   }
   // ---- phase 2: pack every table into one ring region, one upload ----
   std::unique_lock<std::mutex> lock(g_ring_mu);

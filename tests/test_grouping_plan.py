@@ -1,0 +1,90 @@
+"""Grouped execution's flush plan, host only (no device): disc_plan_group_dry_run runs the
+requests' runtime flows in capture mode and returns the actions the level-synchronous
+flush would issue.  Pins the grouping rules of DESIGN.md §2.4 on CPU; the device-side
+equivalence (bit-identical outputs) is tests/test_gpu_grouped.py."""
+import json
+
+import pytest
+
+
+@pytest.fixture(scope="module")
+def D():
+    import paper_2103_05288_b200 as D
+    D.lib()
+    return D
+
+
+def _reqs(D, graph, shape_list):
+    from paper_2103_05288_b200 import workloads as W
+    plan = D.compile_graph(graph)
+    return plan, [(plan, W.input_shapes(graph, s)) for s in shape_list]
+
+
+def test_c2_sweep_is_three_grouped_launches(D):
+    """192 variable-shape LN+GELU requests -> one grouped launch per plan kernel, members
+    ordered by work (largest first), bytes = the requests' algorithmic bytes."""
+    from paper_2103_05288_b200 import workloads as W
+    g = W.ln_gelu_graph()
+    plan, reqs = _reqs(D, g, W.ln_shapes())
+    acts = D.group_dry_run(reqs)
+    assert [a["action"] for a in acts] == ["group"] * 3
+    assert [a["level"] for a in acts] == [0, 1, 2]
+    assert [a["kernel"] for a in acts] == [0, 1, 2]
+    assert all(a["members"] == len(reqs) and a["generated"] for a in acts)
+    for a in acts:
+        assert a["order"] == sorted(a["order"], reverse=True)
+        # compact member records: well under the full descriptor (4.6 / 9.3 KB)
+        assert a["table_bytes"] / a["members"] < 4096
+    want = sum(plan.algorithmic_bytes(shapes) for _, shapes in reqs)
+    assert sum(a["bytes"] for a in acts) == want
+
+
+def test_groups_split_by_kernel_instantiation(D):
+    """Softmax over S = 1..4096: vec4 and scalar rows, staged short rows -- one group per
+    kernel instantiation and level, every fused launch in exactly one group."""
+    from paper_2103_05288_b200 import workloads as W
+    g = W.softmax_graph_for(0)
+    shapes = [{"S0": 64, "S1": s} for s in (1, 2, 3, 7, 8, 17, 31, 64, 100, 255, 256, 777, 1024, 4096)]
+    plan, reqs = _reqs(D, g, shapes)
+    acts = D.group_dry_run(reqs)
+    fused = [a for a in acts if a["action"] in ("group", "alone")]
+    for lv in (0, 1):
+        assert sum(a["members"] for a in fused if a["level"] == lv) == len(reqs)
+    # more than one instantiation per level (vector width / staging differ), fewer than requests
+    assert 1 < sum(1 for a in fused if a["level"] == 0) < len(reqs)
+
+
+def test_mixed_fixtures_and_host_threads_identical(D, fixtures):
+    """Heterogeneous requests over every fixture graph, 20 bindings each: the plan is the
+    same whether one thread or several worker threads queue them (merged queues)."""
+    reqs = []
+    for name in sorted(fixtures):
+        f = fixtures[name]
+        graph = json.loads(f["graph"]) if isinstance(f["graph"], str) else f["graph"]
+        plan = D.compile_graph(graph)
+        for syms in (f["bindings"] * 20)[:20]:
+            shapes = {i["id"]: [syms.get(d, 2) if isinstance(d, str) else d for d in i["shape"]] for i in graph["inputs"]}
+            reqs.append((plan, shapes))
+    one = D.group_dry_run(reqs, host_threads=1)
+    assert len(reqs) >= 128
+    for t in (2, 4):
+        assert D.group_dry_run(reqs, host_threads=t) == one
+    kinds = {a["action"] for a in one}
+    assert "group" in kinds
+    # library calls and other non-fusible work are issued one by one, never grouped
+    assert all(a["members"] == 1 for a in one if a["action"] == "single")
+
+
+def test_stream_of_10k_requests_collapses(D):
+    """C5: 10 000 distinct (graph, shape) requests over 10 graphs, one compile per graph;
+    the flush issues a few hundred actions, not one launch per request kernel."""
+    import bench
+    _, graphs, reqs = bench.workload("stream")
+    compiler = D.Compiler()
+    plans = {k: compiler.compile(g) for k, g in graphs.items()}
+    rq = [(plans[k], {i["id"]: bench.input_shape(i, s) for i in graphs[k]["inputs"]}) for k, s in reqs]
+    assert compiler.stats()["compile_count"] == len(graphs)
+    acts = D.group_dry_run(rq, host_threads=4)
+    fused = sum(a["members"] for a in acts if a["action"] in ("group", "alone"))
+    assert fused >= len(reqs)
+    assert len(acts) < 600, len(acts)
