@@ -4,6 +4,9 @@
 //   gemm   -> f32 in/out with f64 accumulation (eval_matmul, kernels.cpp:261-303)
 // Transpose and reshape run through the fused loop kernel as single-load programs.
 #include <cstdint>
+#include <cstdlib>
+#include <dlfcn.h>
+#include <string>
 
 #include "disc_cuda.h"
 #include "kernels.cuh"
@@ -109,6 +112,17 @@ __global__ void __launch_bounds__(256) k_gemm(int64_t m, int64_t k, int64_t n, c
   }
 }
 
+__global__ void k_widen(const float* __restrict__ in, double* __restrict__ out, int64_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<double>(__ldg(in + i));
+}
+__global__ void k_narrow(const double* __restrict__ in, float* __restrict__ out, int64_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<float>(in[i]);
+}
+
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
   z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
@@ -185,8 +199,65 @@ cudaError_t copy2d_group(const HostGroup& H, cudaStream_t s) {
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// kLibraryCall GEMM with the reference's numerics: eval_matmul
+// (kernels.cpp:261-303) accumulates f32 products in f64.  Operands are widened to f64 on the
+// device and multiplied by cuBLAS DGEMM (B200 FP64 tensor cores), the product rounded back
+// to f32 -- the same exact f64 products and f64 sums as the reference, in another order.
+// (SGEMM's f32 accumulation misses the 1e-5 floored tolerance under cancellation at K=768:
+// 4.9e-5 measured.)  cuBLAS is loaded lazily with dlopen, so the library only needs it when
+// a plan has a library call; DISC_GEMM=simt selects the f64-accumulating SIMT kernel below
+// (also used when cuBLAS cannot be loaded).
+namespace {
+struct Cublas {
+  void* handle = nullptr;  // cublasHandle_t
+  int (*create)(void**) = nullptr;
+  int (*set_stream)(void*, cudaStream_t) = nullptr;
+  int (*dgemm)(void*, int, int, int, int, int, const double*, const double*, int, const double*, int, const double*,
+               double*, int) = nullptr;
+  bool ok = false;
+};
+Cublas* cublas() {
+  thread_local Cublas c;
+  thread_local bool tried = false;
+  if (tried) return c.ok ? &c : nullptr;
+  tried = true;
+  const char* mode = std::getenv("DISC_GEMM");
+  if (mode && std::string(mode) == "simt") return nullptr;
+  void* lib = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) return nullptr;
+  c.create = reinterpret_cast<int (*)(void**)>(dlsym(lib, "cublasCreate_v2"));
+  c.set_stream = reinterpret_cast<int (*)(void*, cudaStream_t)>(dlsym(lib, "cublasSetStream_v2"));
+  c.dgemm = reinterpret_cast<decltype(c.dgemm)>(dlsym(lib, "cublasDgemm_v2"));
+  if (!c.create || !c.set_stream || !c.dgemm || c.create(&c.handle) != 0) return nullptr;
+  c.ok = true;
+  return &c;
+}
+}  // namespace
+
+bool gemm_uses_cublas() { return cublas() != nullptr; }
+
 cudaError_t gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c, cudaStream_t s) {
   if (m <= 0 || n <= 0) return cudaSuccess;
+  if (Cublas* cb = cublas(); cb && k > 0 && m < (int64_t{1} << 31) && n < (int64_t{1} << 31) && k < (int64_t{1} << 31)) {
+    double *a64 = nullptr, *b64 = nullptr, *c64 = nullptr;
+    if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&a64), sizeof(double) * m * k, s)) return e;
+    if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&b64), sizeof(double) * k * n, s)) return e;
+    if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&c64), sizeof(double) * m * n, s)) return e;
+    k_widen<<<grid_for(m * k, 256, 148 * 16), 256, 0, s>>>(a, a64, m * k);
+    k_widen<<<grid_for(k * n, 256, 148 * 16), 256, 0, s>>>(b, b64, k * n);
+    // row-major C[m,n] = A[m,k] B[k,n]  ==  column-major C^T = B^T A^T
+    const double one = 1.0, zero = 0.0;
+    int st = cb->set_stream(cb->handle, s);
+    if (st == 0)
+      st = cb->dgemm(cb->handle, 0 /*N*/, 0 /*N*/, static_cast<int>(n), static_cast<int>(m), static_cast<int>(k), &one,
+                     b64, static_cast<int>(n), a64, static_cast<int>(k), &zero, c64, static_cast<int>(n));
+    k_narrow<<<grid_for(m * n, 256, 148 * 16), 256, 0, s>>>(c64, c, m * n);
+    cudaFreeAsync(a64, s);
+    cudaFreeAsync(b64, s);
+    cudaFreeAsync(c64, s);
+    if (st != 0) return cudaErrorUnknown;
+    return cudaGetLastError();
+  }
   dim3 grid(static_cast<unsigned>((n + kT - 1) / kT), static_cast<unsigned>((m + kT - 1) / kT));
   k_gemm<<<grid, 256, 0, s>>>(m, k, n, a, b, c);
   return cudaGetLastError();

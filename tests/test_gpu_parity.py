@@ -381,3 +381,18 @@ def test_transcendental_accuracy(gpu):
         if op == "Tanh":  # tiny arguments are returned exactly (sign and value)
             tiny = np.abs(x) < 2.44140625e-4
             np.testing.assert_array_equal(y[tiny], x[tiny].astype(np.float64))
+
+
+def test_gemm_library_call(gpu, ref):
+    """kLibraryCall (eval_matmul, kernels.cpp:261-303) at transformer sizes: within 1e-5
+    of the f64-accumulated product (floored rel_err), and the matmul fixture plan against
+    the reference executor."""
+    rng = np.random.default_rng(3)
+    for m, k, n in ((512, 768, 3072), (333, 3072, 768), (1, 5, 7), (64, 0, 16)):
+        g = json.dumps({"name": "mm", "inputs": [{"id": "a", "shape": ["M", k]}, {"id": "b", "shape": [k, "N"]}],
+                        "outputs": ["c"], "nodes": [{"id": "c", "op": "MatMul", "inputs": ["a", "b"]}]})
+        a = rng.uniform(0.25, 2.0, size=(m, k)).astype(np.float32)
+        b = rng.uniform(-1.0, 1.0, size=(k, n)).astype(np.float32)
+        got = gpu.Executor().run(gpu.compile_graph(g), {"a": a, "b": b}).outputs[0]
+        want = (a.astype(np.float64) @ b.astype(np.float64)).astype(np.float32)
+        assert O.rel_err(got, want) <= 1e-5, (m, k, n, O.rel_err(got, want))
