@@ -108,6 +108,11 @@ int disc_executor_run_grouped(disc_executor e, int n_requests, const disc_plan* 
  * thread run contiguous request ranges' runtime flows on worker threads (own sub-executor
  * each: allocator, scratch, recipe cache) and merge their queues into one grouped flush. */
 int disc_executor_set_host_threads(disc_executor e, int n);
+/* Static plans (no shape program, e.g. disc_static_specialize) run as CUDA graphs: a run
+ * whose device work (launch parameters and pointers included) hashes like the previous
+ * run's is captured, later identical runs replay it.  Default on. */
+int disc_executor_set_graphs(disc_executor e, int on);
+int64_t disc_executor_graph_replays(disc_executor e);
 int disc_executor_num_requests(disc_executor e);
 int disc_executor_num_request_outputs(disc_executor e, int request);  /* -1: no such request */
 int disc_executor_request_output(disc_executor e, int request, int i, const float** dptr, const int64_t** dims,

@@ -275,6 +275,15 @@ int disc_cuda_queue_active(void);
  * any) together with the detached ones -- their requests merged level by level and
  * grouped as if queued by one thread; the handles are consumed. */
 void* disc_cuda_queue_detach(void);
+/* Static plans as CUDA graphs: the executor queues a run, hashes the queued ops (0 = not
+ * capturable) and either replays the graph captured for the same hash or issues the queue
+ * under stream capture (disc_cuda_queue_issue_graph: ops in order, no grouping) and keeps
+ * the instantiated graph; graph_exec == nullptr issues the ops directly, no capture. */
+uint64_t disc_cuda_queue_hash(void* queue);
+void disc_cuda_queue_discard(void* queue);
+int disc_cuda_queue_issue_graph(void* queue, void** graph_exec);
+int disc_cuda_graph_launch(void* graph_exec, void* stream);
+int disc_cuda_graph_destroy(void* graph_exec);
 /* Host profile: ns spent packing grouped-launch descriptor tables since the last call. */
 int64_t disc_cuda_host_profile(int64_t* table_bytes);
 int disc_cuda_queue_flush_detached(void* const* queues, int n, int timing);

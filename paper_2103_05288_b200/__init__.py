@@ -6,7 +6,7 @@ C ABI (include/disc_b200.h, include/disc_cuda.h).  See DESIGN.md.
 """
 from .api import (capture_programs, group_dry_run, set_pdl, set_specialization, specialized_launches, CompileOptions, CompiledPlan, Compiler, DeviceBuffer, DiscError, ExecResult, ExecStats,
                   Executor, cache_key, compile_graph, cuda_available, dhlo_roundtrip, dump_stage, guard_passes,
-                  kernel_launches, lib, lower_dhlo_json, static_specialize)
+                  kernel_launches, lib, lower_dhlo_json, new_stream, static_specialize)
 
 from . import dispatch
 from .dispatch import Dispatcher, shard
@@ -16,5 +16,5 @@ __all__ = [
     "capture_programs", "group_dry_run", "set_pdl", "set_specialization", "specialized_launches",
     "CompileOptions", "CompiledPlan", "Compiler", "DeviceBuffer", "DiscError", "ExecResult", "ExecStats",
     "Executor", "cache_key", "compile_graph", "cuda_available", "dhlo_roundtrip", "dump_stage", "guard_passes",
-    "kernel_launches", "lib", "lower_dhlo_json", "static_specialize",
+    "kernel_launches", "lib", "lower_dhlo_json", "new_stream", "static_specialize",
 ]

@@ -79,6 +79,8 @@ def _declare(L: C.CDLL) -> None:
         "disc_executor_run_grouped": ([vp, i32, P(vp), P(i32), P(cp), P(vp), P(vp), P(i32), i32], i32),
         "disc_executor_num_requests": ([vp], i32),
         "disc_executor_set_host_threads": ([vp, i32], i32),
+        "disc_executor_set_graphs": ([vp, i32], i32),
+        "disc_executor_graph_replays": ([vp], i64),
         "disc_executor_num_request_outputs": ([vp, i32], i32),
         "disc_executor_request_output": ([vp, i32, i32, P(vp), P(P(i64)), P(i32)], i32),
         "disc_executor_copy_request_output": ([vp, i32, i32, vp, i32], i32),
@@ -436,6 +438,13 @@ class Executor:
         """Worker threads for the host flow of grouped calls (run_grouped)."""
         _check(lib().disc_executor_set_host_threads(self._h, int(n)))
 
+    def set_graphs(self, on: bool) -> None:
+        """Static plans as CUDA graphs (captured on the second identical run, then replayed)."""
+        _check(lib().disc_executor_set_graphs(self._h, int(on)))
+
+    def graph_replays(self) -> int:
+        return lib().disc_executor_graph_replays(self._h)
+
     def set_cache_budget(self, nbytes: int) -> None:
         lib().disc_executor_set_cache_budget(self._h, int(nbytes))
 
@@ -638,6 +647,13 @@ def host_overhead_us(plan: CompiledPlan, input_shapes: Dict[str, Sequence[int]],
     us = C.c_double()
     _check(lib().disc_plan_host_overhead(plan._h, k, c_names, c_dims, c_ranks, iters, C.byref(us)))
     return us.value
+
+
+def new_stream() -> int:
+    """A non-blocking CUDA stream (disc_cuda_stream_create), e.g. for Executor(0, stream)."""
+    st = C.c_void_p()
+    _cuda(lib().disc_cuda_stream_create(C.byref(st)))
+    return st.value
 
 
 def group_dry_run(requests: Sequence[Tuple[CompiledPlan, Dict[str, Sequence[int]]]], host_threads: int = 1) -> list:

@@ -138,6 +138,12 @@ int disc_executor_run_grouped(disc_executor e, int n_requests, const disc_plan* 
   });
 }
 
+int disc_executor_set_graphs(disc_executor e, int on) {
+  return guard([&] { e->ex.set_graphs(on != 0); });
+}
+
+int64_t disc_executor_graph_replays(disc_executor e) { return e->ex.graph_replays(); }
+
 int disc_executor_set_host_threads(disc_executor e, int n) {
   return guard([&] { e->ex.set_host_threads(n); });
 }

@@ -123,7 +123,9 @@ __global__ void __launch_bounds__(kLoopThreads) k_reduce_generic(const __grid_co
 namespace disc_dev {
 
 static int g_pdl = 1;
-bool pdl_enabled() { return g_pdl != 0; }
+static thread_local bool t_capturing = false;  // stream capture in progress on this thread
+bool pdl_enabled() { return g_pdl != 0 && !t_capturing; }
+void set_capturing(bool on) { t_capturing = on; }
 
 int group_waves() {
   static const int w = [] {

@@ -727,8 +727,10 @@ constexpr size_t kGroupSmemThreshold = 24 * 1024;
 // to exactly one wave (SM count x this).  Cached per host thread.
 int resident_ctas(const void* kernel, int block, size_t smem);
 
-// PDL mode (disc_cuda_set_pdl); launches go through cudaLaunchKernelEx.
+// PDL mode (disc_cuda_set_pdl); launches go through cudaLaunchKernelEx.  Off while this
+// thread captures a CUDA graph (set_capturing).
 bool pdl_enabled();
+void set_capturing(bool on);
 
 template <typename Arg>
 inline cudaError_t launch_k(void (*kernel)(Arg), dim3 grid, dim3 block, size_t smem, cudaStream_t s, const Arg& a) {

@@ -446,7 +446,7 @@ struct QRecord {
 struct Arena {
   std::unique_ptr<unsigned char[]> buf;
   size_t cap = 0, used = 0;
-  unsigned char* data() { return buf.get(); }
+  unsigned char* data() const { return buf.get(); }
   void clear() { used = 0; }
   size_t take(size_t n) {  // 16 B aligned offset of n fresh bytes (16 B granules: readable in whole granules)
     n = (n + 15) / 16 * 16;
@@ -1060,6 +1060,132 @@ void* disc_cuda_queue_detach(void) {
   t_q.arena.clear();
   t_q.frees.clear();
   return q;
+}
+
+// ---- static plans as CUDA graphs ------------------------
+uint64_t disc_cuda_queue_hash(void* queue) {
+  const Queue* q = static_cast<const Queue*>(queue);
+  uint64_t h = 1469598103934665603ull;
+  auto mixb = [&](const void* p, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  };
+  for (const auto& r : q->reqs)
+    for (const QOp& op : r) {
+      mixb(&op.kind, sizeof op.kind);
+      const unsigned char* p = q->arena.data() + op.off;
+      if (op.kind == kQLoop || op.kind == kQReduce) {
+        disc_desc::Range rg[disc_desc::kMaxRanges];
+        const int n = op.kind == kQLoop ? disc_desc::ranges(*reinterpret_cast<const disc_loop_launch*>(p), rg)
+                                        : disc_desc::ranges(*reinterpret_cast<const disc_reduce_launch*>(p), rg);
+        for (int i = 0; i < n; ++i) mixb(p + rg[i].off, rg[i].len);
+      } else {
+        const size_t sz = op.kind == kQPad ? sizeof(disc_pad_launch)
+                          : op.kind == kQConcat ? sizeof(disc_concat_launch)
+                          : op.kind == kQGemm ? sizeof(QGemm)
+                          : op.kind == kQMemcpy ? sizeof(QMemcpy) : sizeof(QMemset);
+        mixb(p, sz);
+      }
+    }
+  return q->frees.empty() ? h : 0;  // 0: not capturable (frees inside the run)
+}
+
+void disc_cuda_queue_discard(void* queue) { delete static_cast<Queue*>(queue); }
+
+// Issues a detached queue's ops in order (no grouping) inside a stream capture, then
+// instantiates and launches the graph; *graph_exec receives it (nullptr if the queue could
+// not be captured, in which case the ops were issued directly).  Consumes the queue.
+int disc_cuda_queue_issue_graph(void* queue, void** graph_exec) {
+  Queue* q = static_cast<Queue*>(queue);
+  const bool want = graph_exec != nullptr;
+  if (want) *graph_exec = nullptr;
+  const cudaStream_t st = q->stream;
+  auto issue_all = [&]() -> int {
+    for (const auto& r : q->reqs)
+      for (const QOp& op : r) {
+        const unsigned char* p = q->arena.data() + op.off;
+        int rc = 0;
+        switch (op.kind) {
+          case kQLoop: rc = disc_cuda_launch_loop(reinterpret_cast<const disc_loop_launch*>(p), st); break;
+          case kQReduce: rc = disc_cuda_launch_reduce(reinterpret_cast<const disc_reduce_launch*>(p), st); break;
+          case kQPad: rc = disc_cuda_launch_pad(reinterpret_cast<const disc_pad_launch*>(p), st); break;
+          case kQConcat: rc = disc_cuda_launch_concat(reinterpret_cast<const disc_concat_launch*>(p), st); break;
+          case kQGemm: {
+            const auto& g = *reinterpret_cast<const QGemm*>(p);
+            rc = disc_cuda_gemm(g.m, g.k, g.n, g.a, g.b, g.c, st);
+            break;
+          }
+          case kQMemcpy: {
+            const auto& c = *reinterpret_cast<const QMemcpy*>(p);
+            rc = disc_cuda_memcpy(c.dst, c.src, c.bytes, c.kind & 3, st);
+            break;
+          }
+          case kQMemset: {
+            const auto& m = *reinterpret_cast<const QMemset*>(p);
+            rc = disc_cuda_memset(m.dst, m.value, m.bytes, st);
+            break;
+          }
+        }
+        if (rc) {
+          if (std::getenv("DISC_GRAPH_DEBUG"))
+            std::fprintf(stderr, "[disc graph] op kind %d failed: %s\n", op.kind, t_err.c_str());
+          return rc;
+        }
+      }
+    return 0;
+  };
+  int rc = 0;
+  bool done = false;
+  // (the legacy default stream cannot be captured; a failed begin leaves its error to clear)
+  bool capturing = false;
+  if (want && q->frees.empty() && st != nullptr) {
+    capturing = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (!capturing) cudaGetLastError();
+  }
+  if (capturing) {
+    disc_dev::set_capturing(true);
+    const int irc = issue_all();
+    disc_dev::set_capturing(false);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(st, &g);
+    cudaGraphExec_t ex = nullptr;
+    if (irc == 0 && e == cudaSuccess && g && cudaGraphInstantiate(&ex, g, 0) == cudaSuccess) {
+      rc = check(cudaGraphLaunch(ex, st), "cudaGraphLaunch");
+      if (!rc) {
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        *graph_exec = ex;
+      } else {
+        cudaGraphExecDestroy(ex);
+      }
+      done = true;
+    }
+    if (g) cudaGraphDestroy(g);
+    if (!done) {  // capture not possible: issue directly below
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+        cudaGraph_t junk = nullptr;
+        cudaStreamEndCapture(st, &junk);
+        if (junk) cudaGraphDestroy(junk);
+      }
+      cudaGetLastError();
+    }
+  }
+  if (!done) {
+    rc = issue_all();
+    for (void* f : q->frees)
+      if (!rc) rc = check(cudaFreeAsync(f, st), "cudaFreeAsync");
+  }
+  delete q;
+  return rc;
+}
+
+int disc_cuda_graph_launch(void* graph_exec, void* stream) {
+  const int rc = check(cudaGraphLaunch(static_cast<cudaGraphExec_t>(graph_exec), S(stream)), "cudaGraphLaunch");
+  if (!rc) g_launches.fetch_add(1, std::memory_order_relaxed);
+  return rc;
+}
+int disc_cuda_graph_destroy(void* graph_exec) {
+  return check(cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph_exec)), "cudaGraphExecDestroy");
 }
 
 int64_t disc_cuda_host_profile(int64_t* table_bytes) {

@@ -415,6 +415,8 @@ void DeviceExecutor::finish_timing() {
 
 DeviceExecutor::~DeviceExecutor() {
   disc_cuda_stream_synchronize(stream_);
+  for (auto& [_, g] : graph_cache_)
+    for (auto& [h, exec] : g.graphs) disc_cuda_graph_destroy(exec);
   for (auto& c : small_) {
     disc_cuda_host_free(c.host);
     disc_cuda_free(c.dev, stream_);
@@ -497,6 +499,56 @@ void DeviceExecutor::run_kernel(const KernelArtifact& art, const VersionArtifact
 
 void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBinding>& inputs, bool append_records,
                          uint64_t plan_serial) {
+  static const bool env_on = [] {
+    const char* e = std::getenv("DISC_GRAPHS");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool graph = env_on && graphs_ && !grouped_ && !timing_ && plan_serial != 0 && plan.shape_program.empty() &&
+                     stream_ != nullptr && !disc_cuda_queue_active();
+  if (!graph) return run_impl(plan, inputs, append_records, plan_serial);
+  cuda_ok(disc_cuda_queue_begin(stream_), "queue begin");
+  cuda_ok(disc_cuda_queue_request(), "queue request");
+  try {
+    run_impl(plan, inputs, append_records, plan_serial);
+  } catch (...) {
+    if (void* q = disc_cuda_queue_detach()) disc_cuda_queue_issue_graph(q, nullptr);  // valid work before the error
+    throw;
+  }
+  void* q = disc_cuda_queue_detach();
+  if (!q) return;
+  const uint64_t h = disc_cuda_queue_hash(q);
+  GraphEntry& g = graph_cache_[plan_serial];
+  for (auto& [gh, exec] : g.graphs)
+    if (h && gh == h) {  // same launches, same pointers: replay
+      disc_cuda_queue_discard(q);
+      cuda_ok(disc_cuda_graph_launch(exec, stream_), "graph replay");
+      ++graph_replays_;
+      device_launches_ = 1;
+      return;
+    }
+  // capture work seen before (buffer placement can cycle between a few states)
+  const bool repeat = h && std::find(g.seen.begin(), g.seen.end(), h) != g.seen.end();
+  if (repeat) {
+    void* exec = nullptr;
+    cuda_ok(disc_cuda_queue_issue_graph(q, &exec), "graph capture");
+    if (exec) {
+      if (g.graphs.size() >= 4) {
+        disc_cuda_graph_destroy(g.graphs.front().second);
+        g.graphs.erase(g.graphs.begin());
+      }
+      g.graphs.emplace_back(h, exec);
+    }
+  } else {
+    cuda_ok(disc_cuda_queue_issue_graph(q, nullptr), "issue");
+    if (h) {
+      if (g.seen.size() >= 8) g.seen.erase(g.seen.begin());
+      g.seen.push_back(h);
+    }
+  }
+}
+
+void DeviceExecutor::run_impl(const CompiledPlan& plan, const std::vector<InputBinding>& inputs, bool append_records,
+                              uint64_t plan_serial) {
   ExecStats stats;
   stats.host_instruction_count = plan.host_instruction_count();
   const auto t_run = Clock::now();

@@ -97,6 +97,11 @@ class DeviceExecutor {
   // plan_serial: stable id of `plan` (enables the launch recipe cache; 0 disables).
   void run(const CompiledPlan& plan, const std::vector<InputBinding>& inputs, bool append_records = false,
            uint64_t plan_serial = 0);
+  // Static plans (no shape program) run as CUDA graphs: a run whose queued device work
+  // hashes like the previous run's is captured once and replayed afterwards
+  // (SURVEY 8(f) rank 2).  On by default; DISC_GRAPHS=0 or set_graphs(false) disables.
+  void set_graphs(bool on) { graphs_ = on; }
+  int64_t graph_replays() const { return graph_replays_; }
   // Grouped execution of independent requests (disc_executor_run_grouped):
   //   begin_grouped(); { begin_request(); [stage_input...]; run(...); } x n; end_grouped();
   // Each run() evaluates its request's runtime flow on the host (shapes, buffers,
@@ -166,6 +171,15 @@ class DeviceExecutor {
   bool grouped_ = false;
   bool group_timing_ = false;
   bool records_grouped_ = false;  // records_ describe grouped launches
+  void run_impl(const CompiledPlan& plan, const std::vector<InputBinding>& inputs, bool append_records,
+                uint64_t plan_serial);
+  struct GraphEntry {
+    std::vector<uint64_t> seen;                      // recent work hashes (capture on a repeat)
+    std::vector<std::pair<uint64_t, void*>> graphs;  // captured graphs by hash (<= 4)
+  };
+  std::map<uint64_t, GraphEntry> graph_cache_;
+  bool graphs_ = true;
+  int64_t graph_replays_ = 0;
   // multi-threaded host flow (run_grouped_batch)
   int host_threads_ = 1;
   struct Pool;

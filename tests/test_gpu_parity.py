@@ -396,3 +396,33 @@ def test_gemm_library_call(gpu, ref):
         got = gpu.Executor().run(gpu.compile_graph(g), {"a": a, "b": b}).outputs[0]
         want = (a.astype(np.float64) @ b.astype(np.float64)).astype(np.float32)
         assert O.rel_err(got, want) <= 1e-5, (m, k, n, O.rel_err(got, want))
+
+
+def test_static_plans_replay_as_cuda_graphs(gpu, ref, fixtures):
+    """Static plans (static_specialize: no shape program) are captured on the second
+    identical run and replayed afterwards (one graph launch per run); outputs equal the
+    graph-free executor's and the reference's, with new input values each run."""
+    from test_compiler_parity import _static_variant
+    for name in ("softmax", "transformer", "chain"):
+        g = _static_variant(fixtures, name)
+        plan = gpu.static_specialize(g)
+        ex, plain = gpu.Executor(0, gpu.new_stream()), gpu.Executor(0, gpu.new_stream())
+        plain.set_graphs(False)
+        for it in range(7):
+            inputs = ref.make_binding(g, {}, 100 + it)
+            before = gpu.kernel_launches()
+            got = ex.run(plan, inputs)
+            launched = gpu.kernel_launches() - before
+            want = plain.run(plan, inputs)
+            for a, b in zip(got.outputs, want.outputs):
+                np.testing.assert_array_equal(a, b)
+            assert got.stats.as_dict() == want.stats.as_dict()
+            if it >= 4:
+                assert launched == 1, (name, it, launched)
+        assert ex.graph_replays() >= 1, name
+    # dynamic plans never use graphs
+    dyn = gpu.compile_graph(fixtures["softmax"]["graph"])
+    ex = gpu.Executor(0, gpu.new_stream())
+    for it in range(3):
+        ex.run(dyn, ref.make_binding(fixtures["softmax"]["graph"], {"S0": 5}, it))
+    assert ex.graph_replays() == 0
