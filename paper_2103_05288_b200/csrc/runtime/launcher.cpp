@@ -1094,7 +1094,10 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
             break;
           }
       }
-      const int64_t budget = 48 * 1024;
+      static const int64_t budget = [] {  // row-cache bytes per block (DISC_ROW_CACHE_KB, A/B)
+        const char* e = std::getenv("DISC_ROW_CACHE_KB");
+        return int64_t{e ? std::atoi(e) : 48} * 1024;
+      }();
       auto bytes = [&](int gg) { return int64_t{std::max(gg, 256) / gg} * nc * R.R * 4; };
       while (nc && bytes(g) > budget && g < 1024) g <<= 1;
       if (nc && bytes(g) <= budget) {
