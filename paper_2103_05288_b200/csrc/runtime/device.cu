@@ -12,6 +12,7 @@
 #include <type_traits>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <unordered_map>
 #include <vector>
@@ -290,10 +291,12 @@ int64_t launch_weight(int kind, const void* l) {
 // Grouped launch of one homogeneous group (<= DISC_MAX_GROUP members, same key) in three
 // steps: plan (compact record layout), pack (records into a pinned table), launch.
 void plan_group(const GroupKey& k, HostGroup& H) {
+  // generated groups share one program structure: the first member's ranges cover all
+  const int n = k.entry ? 1 : H.n;
   if (k.kind == 0)
-    disc_dev::group_segments<disc_loop_launch>(H.members, H.n, &H.nseg, H.seg, &H.stride);
+    disc_dev::group_segments<disc_loop_launch>(H.members, n, &H.nseg, H.seg, &H.stride);
   else
-    disc_dev::group_segments<disc_reduce_launch>(H.members, H.n, &H.nseg, H.seg, &H.stride);
+    disc_dev::group_segments<disc_reduce_launch>(H.members, n, &H.nseg, H.seg, &H.stride);
 }
 
 void pack_group(const HostGroup& H, unsigned char* dst) {  // compact records: only the ranges kernels read
@@ -780,6 +783,7 @@ namespace {
 // other directly (programmatic dependent launch chains them) instead of each waiting
 // behind its own table copy.
 int flush_queues(const std::vector<Queue*>& qs, int timing) {
+  const auto t_start = std::chrono::steady_clock::now();
   const cudaStream_t st = qs[0]->stream;
   t_q.records.clear();
   t_q.next_event = 0;
@@ -831,9 +835,9 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
     a.table_bytes = bytes;
     total += (bytes + 255) / 256 * 256;
   };
-  for (size_t lv = 0; lv < levels; ++lv) {
-    std::map<GroupKey, std::vector<FOp>> groups[2];
-    std::vector<GroupKey> order[2];
+  auto plan_level = [&](size_t lv, std::vector<Action>& acts) {
+    // few distinct kernel instantiations per level: a linear key table beats a map
+    std::vector<std::pair<GroupKey, std::vector<FOp>>> groups[2];
     std::vector<FOp> alone[2];
     Action copies{kCopies, static_cast<int>(lv)};
     copies.sched = copy_name;
@@ -847,12 +851,12 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
           alone[kind].push_back({&op, p, rr.q});
           continue;
         }
-        auto it = groups[kind].find(op.gk);
-        if (it == groups[kind].end()) {
-          order[kind].push_back(op.gk);
-          it = groups[kind].emplace(op.gk, std::vector<FOp>()).first;
-        }
-        it->second.push_back({&op, p, rr.q});
+        auto& gs = groups[kind];
+        size_t gi = 0;
+        auto same = [](const GroupKey& a, const GroupKey& b) { return !(a < b) && !(b < a); };
+        while (gi < gs.size() && !same(gs[gi].first, op.gk)) ++gi;
+        if (gi == gs.size()) gs.emplace_back(op.gk, std::vector<FOp>());
+        gs[gi].second.push_back({&op, p, rr.q});
         continue;
       }
       if (op.kind == kQConcat ||
@@ -882,7 +886,7 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
       c.items.assign(copies.items.begin() + i0,
                      copies.items.begin() + std::min(copies.items.size(), i0 + DISC_MAX_GROUP));
       c.members = static_cast<int>(c.items.size());
-      place(c, sizeof(disc_dev::disc_copy2d) * c.items.size());
+      c.table_bytes = sizeof(disc_dev::disc_copy2d) * c.items.size();
       acts.push_back(std::move(c));
     }
     for (int kind = 0; kind < 2; ++kind) {
@@ -895,11 +899,15 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
         a.sched = name_of(f.q, f.op->sched);
         acts.push_back(std::move(a));
       }
-      for (const GroupKey& k : order[kind]) {
-        auto& m = groups[kind][k];
-        std::stable_sort(m.begin(), m.end(), [&](const FOp& x, const FOp& y) {
-          return launch_weight(kind, x.p) > launch_weight(kind, y.p);
-        });
+      for (auto& [k, m] : groups[kind]) {
+        {  // larger members first (weights computed once)
+          std::vector<std::pair<int64_t, size_t>> w(m.size());
+          for (size_t i = 0; i < m.size(); ++i) w[i] = {-launch_weight(kind, m[i].p), i};
+          std::stable_sort(w.begin(), w.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+          std::vector<FOp> sorted(m.size());
+          for (size_t i = 0; i < m.size(); ++i) sorted[i] = m[w[i].second];
+          m.swap(sorted);
+        }
         for (size_t i = 0; i < m.size(); i += DISC_MAX_GROUP) {
           const size_t e = std::min(m.size(), i + DISC_MAX_GROUP);
           Action g{kGroup, static_cast<int>(lv)};
@@ -916,12 +924,37 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
           g.H.members = g.ptrs.data();
           g.H.n = g.members;
           plan_group(k, g.H);
-          place(g, static_cast<size_t>(g.H.stride) * g.H.n);
+          g.table_bytes = static_cast<size_t>(g.H.stride) * g.H.n;
           acts.push_back(std::move(g));
         }
       }
     }
+  };
+  // levels are planned independently (in parallel for large flushes), then concatenated
+  std::vector<std::vector<Action>> per(levels);
+  {
+    size_t ops = 0;
+    for (const ReqRef& rr : reqs) ops += rr.ops->size();
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const size_t nt = ops >= 8192 ? std::min<size_t>(hw, levels) : 1;
+    if (nt <= 1) {
+      for (size_t lv = 0; lv < levels; ++lv) plan_level(lv, per[lv]);
+    } else {
+      std::atomic<size_t> next{0};
+      auto worker = [&] {
+        for (size_t lv; (lv = next.fetch_add(1)) < levels;) plan_level(lv, per[lv]);
+      };
+      std::vector<std::thread> th;
+      for (size_t w = 1; w < nt; ++w) th.emplace_back(worker);
+      worker();
+      for (auto& t : th) t.join();
+    }
   }
+  for (auto& v : per)
+    for (Action& x : v) {
+      if (x.kind == kGroup || x.kind == kCopies) place(x, x.table_bytes);
+      acts.push_back(std::move(x));
+    }
   if (g_capture) {  // grouping dry run (host only): describe the actions, issue nothing
     static const char* kinds[] = {"single", "alone", "group", "copies"};
     for (const Action& a : acts) {
@@ -946,6 +979,7 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
     return 0;
   }
   // ---- phase 2: pack every table into one ring region, one upload ----
+  const auto t_plan = std::chrono::steady_clock::now();
   std::unique_lock<std::mutex> lock(g_ring_mu);
   Ring& ring = g_rings[st];
   size_t base = 0;
@@ -953,19 +987,51 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
   if (total > 0) {
     rc = check(ring_reserve(ring, total, st, &base), "group tables");
     if (!rc) {
+      // pack the member records; large flushes split the packing over threads
+      struct Task {
+        Action* a;
+        int i0, i1;
+      };
+      std::vector<Task> tasks;
+      size_t members = 0;
       for (Action& a : acts) {
         if (a.kind == kGroup) {
           a.H.members = a.ptrs.data();  // (vector moved into acts)
-          pack_group(a.H, ring.host + base + a.table);
+          for (int i = 0; i < a.H.n; i += 256) tasks.push_back({&a, i, std::min(a.H.n, i + 256)});
+          members += a.H.n;
         } else if (a.kind == kCopies) {
           std::memcpy(ring.host + base + a.table, a.items.data(), a.table_bytes);
         }
+      }
+      auto pack_range = [&](size_t t0, size_t t1) {
+        for (size_t t = t0; t < t1; ++t) {
+          const HostGroup& H = tasks[t].a->H;
+          unsigned char* dst = ring.host + base + tasks[t].a->table;
+          for (int i = tasks[t].i0; i < tasks[t].i1; ++i) {
+            unsigned char* rec = dst + static_cast<size_t>(i) * H.stride;
+            const unsigned char* src = static_cast<const unsigned char*>(H.members[i]);
+            for (int sg = 0; sg < H.nseg; ++sg)
+              std::memcpy(rec + H.seg[sg][2] * 16, src + H.seg[sg][0] * 16, H.seg[sg][1] * 16);
+          }
+        }
+      };
+      const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+      const size_t nt = members >= 4096 ? std::min<size_t>(hw, tasks.size()) : 1;
+      if (nt <= 1) {
+        pack_range(0, tasks.size());
+      } else {
+        std::vector<std::thread> th;
+        for (size_t w = 1; w < nt; ++w)
+          th.emplace_back(pack_range, tasks.size() * w / nt, tasks.size() * (w + 1) / nt);
+        pack_range(0, tasks.size() / nt);
+        for (auto& t : th) t.join();
       }
       rc = check(cudaMemcpyAsync(ring.dev + base, ring.host + base, total, cudaMemcpyHostToDevice, st),
                  "group tables upload");
     }
   }
   lock.unlock();
+  const auto t_pack = std::chrono::steady_clock::now();
   // ---- phase 3: issue ----
   auto begin_rec = [&](const Action& a) {
     QRecord rec{a.level, a.members, a.kernel, a.sched, a.bytes};
@@ -1025,6 +1091,13 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
   if (total > 0) {
     std::lock_guard<std::mutex> l2(g_ring_mu);
     if (!rc) rc = check(ring_release(ring, base, total, st), "group tables release");
+  }
+  static const bool prof = std::getenv("DISC_HOST_PROFILE") != nullptr;
+  if (prof) {
+    const auto t_end = std::chrono::steady_clock::now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[disc flush] %zu actions: plan %.3f ms, pack+upload %.3f ms, issue %.3f ms\n", acts.size(),
+                 ms(t_start, t_plan), ms(t_plan, t_pack), ms(t_pack, t_end));
   }
   for (Queue* q : qs) {
     for (void* p : q->frees)
