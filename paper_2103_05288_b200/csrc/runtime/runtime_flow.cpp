@@ -7,6 +7,7 @@
 #include <exception>
 #include <functional>
 #include <mutex>
+#include <numeric>
 #include <thread>
 #include <cstdio>
 #include <cstdlib>
@@ -131,6 +132,14 @@ void DeviceExecutor::begin_grouped() {
   request_ = -1;
 }
 
+// Next phase of the same grouped call: a new queue, nothing reset (outputs, scratch and
+// deferred frees of earlier phases stay).
+void DeviceExecutor::begin_phase() {
+  if (grouped_) throw InternalError("grouped execution already in progress");
+  cuda_ok(disc_cuda_queue_begin(stream_), "queue begin");
+  grouped_ = true;
+}
+
 void DeviceExecutor::begin_request() {
   if (!grouped_) throw InternalError("begin_request outside grouped execution");
   cuda_ok(disc_cuda_queue_request(), "queue request");
@@ -225,11 +234,12 @@ void DeviceExecutor::set_host_threads(int n) {
   }
 }
 
-void DeviceExecutor::run_requests(int r0, int r1, const CompiledPlan* const* plans, const uint64_t* serials,
+void DeviceExecutor::run_requests(const int* ids, int count, const CompiledPlan* const* plans, const uint64_t* serials,
                                   const int* offs, const char* const* names, const void* const* data,
                                   const int64_t* const* dims, const int* ranks, bool on_host) {
   std::vector<InputBinding> in;
-  for (int r = r0; r < r1; ++r) {
+  for (int j = 0; j < count; ++j) {
+    const int r = ids[j];
     begin_request();
     const int i0 = offs[r], n = offs[r + 1] - i0;
     in.resize(n);
@@ -242,7 +252,26 @@ void DeviceExecutor::run_requests(int r0, int r1, const CompiledPlan* const* pla
       // one staging buffer per (request, input): all of a group's copies are in flight together
       in[i].ptr = on_host ? stage_input(k, data[k], bytes) : static_cast<const float*>(data[k]);
     }
+    req_ids_.push_back(r);
     run(*plans[r], in, true, serials[r]);
+  }
+}
+
+// Reads the records of the flush just issued (non-timing: metadata only) into records_.
+void DeviceExecutor::append_group_records() {
+  const int nrec = disc_cuda_queue_num_records();
+  for (int i = 0; i < nrec; ++i) {
+    int level = 0, members = 0, kernel = -1;
+    int64_t bytes = 0;
+    const char* sched = nullptr;
+    float ms = 0.f;
+    if (group_timing_) {
+      records_.push_back({i, -1, "", 0, 0.0, 1, -1});  // device times read in finish_timing
+    } else {
+      cuda_ok(disc_cuda_queue_record(i, &level, &members, &bytes, &kernel, &sched, &ms), "group record");
+      records_.push_back({level, kernel, std::string("group:") + (sched ? sched : ""), bytes, 0.0, members, -1});
+    }
+    device_launches_ += 1;
   }
 }
 
@@ -250,99 +279,123 @@ void DeviceExecutor::run_grouped_batch(int n, const CompiledPlan* const* plans, 
                                        const int* offs, const char* const* names, const void* const* data,
                                        const int64_t* const* dims, const int* ranks, bool on_host) {
   constexpr int kMinPerThread = 64;
-  const int T = std::max(1, std::min(host_threads_, n / kMinPerThread));
-  if (T <= 1) {
-    begin_grouped();
-    try {
-      run_requests(0, n, plans, serials, offs, names, data, dims, ranks, on_host);
-    } catch (...) {
-      try {
-        end_grouped();  // issue what was queued (valid work), then report the error
-      } catch (...) {
+  // Phases: with enough requests, the largest eighth (by input size) is flushed first, so
+  // the device starts on the long kernels while the host runs the other flows
+  // (DISC_GROUP_PHASES=1: one flush).  Timing mode keeps one flush (per-launch events).
+  static const int max_phases = [] {
+    const char* e = std::getenv("DISC_GROUP_PHASES");
+    return e ? std::max(1, std::atoi(e)) : 2;
+  }();
+  std::vector<std::vector<int>> phases;
+  if (!timing_ && max_phases >= 2 && n >= 128) {
+    std::vector<std::pair<int64_t, int>> w(n);
+    for (int r = 0; r < n; ++r) {
+      int64_t e = 0;
+      for (int k = offs[r]; k < offs[r + 1]; ++k) {
+        int64_t m = 1;
+        for (int d = 0; d < ranks[k]; ++d) m *= dims[k][d];
+        e += m;
       }
-      throw;
+      w[r] = {-e, r};
     }
-    end_grouped();
-    return;
+    const int k = std::max(1, n / 8);
+    std::nth_element(w.begin(), w.begin() + k, w.end());
+    std::vector<char> first(n, 0);
+    for (int i = 0; i < k; ++i) first[w[i].second] = 1;
+    phases.resize(2);
+    for (int r = 0; r < n; ++r) phases[first[r] ? 0 : 1].push_back(r);
+  } else {
+    phases.emplace_back(n);
+    std::iota(phases[0].begin(), phases[0].end(), 0);
   }
-  // contiguous request ranges: [bounds[w], bounds[w+1]) on worker w (w = 0: this thread)
-  std::vector<int> bounds(T + 1);
-  for (int w = 0; w <= T; ++w) bounds[w] = static_cast<int>(int64_t{n} * w / T);
-  std::vector<void*> handles(T, nullptr);
-  std::vector<std::exception_ptr> errs(T);
-  for (int w = 1; w < T; ++w) subs_[w - 1]->set_timing(false);
+  // session
+  begin_grouped();  // resets outputs, records, scratch; defers frees
+  req_ids_.clear();
+  std::vector<char> sub_used(subs_.size(), 0);
+  std::vector<std::exception_ptr> errs;
+  int rc = 0;
   const auto t_start = Clock::now();
-  pool_->start([&](int w) {
-    if (w + 1 >= T) return;
-    DeviceExecutor& ex = *subs_[w];
-    try {
-      ex.begin_grouped();
-      ex.run_requests(bounds[w + 1], bounds[w + 2], plans, serials, offs, names, data, dims, ranks, on_host);
-    } catch (...) {
-      errs[w + 1] = std::current_exception();
+  double flush_ms = 0;
+  for (size_t ph = 0; ph < phases.size(); ++ph) {
+    const std::vector<int>& P = phases[ph];
+    const int m = static_cast<int>(P.size());
+    const int T = std::max(1, std::min(host_threads_, m / kMinPerThread));
+    std::vector<int> bounds(T + 1);
+    for (int w = 0; w <= T; ++w) bounds[w] = static_cast<int>(int64_t{m} * w / T);
+    std::vector<void*> handles(T, nullptr);
+    std::vector<std::exception_ptr> perr(T);
+    if (ph > 0) begin_phase();
+    if (T > 1) {
+      pool_->start([&](int w) {
+        if (w + 1 >= T) return;
+        DeviceExecutor& ex = *subs_[w];
+        try {
+          if (!sub_used[w]) {
+            ex.set_timing(false);
+            ex.begin_grouped();
+            ex.req_ids_.clear();
+            sub_used[w] = 1;
+          } else {
+            ex.begin_phase();
+          }
+          ex.run_requests(P.data() + bounds[w + 1], bounds[w + 2] - bounds[w + 1], plans, serials, offs, names, data,
+                          dims, ranks, on_host);
+        } catch (...) {
+          perr[w + 1] = std::current_exception();
+        }
+        try {
+          if (ex.grouped()) handles[w + 1] = ex.detach_grouped();
+        } catch (...) {
+          if (!perr[w + 1]) perr[w + 1] = std::current_exception();
+        }
+      });
     }
-    try {
-      if (ex.grouped()) handles[w + 1] = ex.detach_grouped();
+    try {  // this thread's range, concurrently with the workers
+      run_requests(P.data() + bounds[0], bounds[1] - bounds[0], plans, serials, offs, names, data, dims, ranks, on_host);
     } catch (...) {
-      if (!errs[w + 1]) errs[w + 1] = std::current_exception();
+      perr[0] = std::current_exception();
     }
-  });
-  try {  // this thread's range, concurrently with the workers
-    begin_grouped();
-    run_requests(bounds[0], bounds[1], plans, serials, offs, names, data, dims, ranks, on_host);
-  } catch (...) {
-    errs[0] = std::current_exception();
+    if (T > 1) pool_->wait();
+    // merged flush of this phase: this thread's queue + the workers' detached ones
+    grouped_ = false;
+    const int src = issue_small_inputs();
+    const auto t_flush = Clock::now();
+    std::vector<void*> hs;
+    for (int w = 1; w < T; ++w)
+      if (handles[w]) hs.push_back(handles[w]);
+    const int frc = disc_cuda_queue_flush_detached(hs.data(), static_cast<int>(hs.size()), group_timing_ ? 1 : 0);
+    flush_ms += std::chrono::duration<double, std::milli>(Clock::now() - t_flush).count();
+    if (rc == 0) rc = src ? src : frc;
+    if (rc == 0) append_group_records();
+    for (auto& e : perr)
+      if (e) errs.push_back(e);
+    if (!errs.empty() || rc) break;
   }
-  pool_->wait();
-  t_group_ = t_start;
-  // merged flush: this thread's queue + the workers' detached ones
-  grouped_ = false;
-  int rc = issue_small_inputs();
-  const auto t_flush = Clock::now();
-  std::vector<void*> hs;
-  for (int w = 1; w < T; ++w)
-    if (handles[w]) hs.push_back(handles[w]);
-  const int frc = disc_cuda_queue_flush_detached(hs.data(), static_cast<int>(hs.size()), group_timing_ ? 1 : 0);
-  if (rc == 0) rc = frc;
   static const bool prof = std::getenv("DISC_HOST_PROFILE") != nullptr;
-  if (prof) {
-    int64_t tb = 0;
-    const int64_t cns = disc_cuda_host_profile(&tb);
-    std::fprintf(stderr,
-                 "[disc host] grouped call: %d requests on %d threads, flow %.3f ms, flush %.3f ms "
-                 "(tables %.3f ms, %.1f MB)\n",
-                 n, T, std::chrono::duration<double, std::milli>(t_flush - t_group_).count(),
-                 std::chrono::duration<double, std::milli>(Clock::now() - t_flush).count(), cns / 1e6, tb / 1e6);
-  }
+  if (prof)
+    std::fprintf(stderr, "[disc host] grouped call: %d requests, %zu phases, host %.3f ms (flush %.3f ms)\n", n,
+                 phases.size(), std::chrono::duration<double, std::milli>(Clock::now() - t_start).count(), flush_ms);
+  // end of session: frees released, outputs / stats in request order
   alloc_.set_defer(false);
-  for (int w = 1; w < T; ++w) subs_[w - 1]->finish_detached();
-  // request outputs / stats in request order
-  for (int w = 1; w < T; ++w) {
-    const auto& ro = subs_[w - 1]->request_outputs();
-    const auto& rs = subs_[w - 1]->request_stats();
-    req_outputs_.insert(req_outputs_.end(), ro.begin(), ro.end());
-    req_stats_.insert(req_stats_.end(), rs.begin(), rs.end());
-  }
-  for (const auto& e : errs)
-    if (e) std::rethrow_exception(e);
-  cuda_ok(rc, "grouped launch");
-  const int nrec = disc_cuda_queue_num_records();
-  records_.clear();
-  device_launches_ = 0;
-  for (int i = 0; i < nrec; ++i) {
-    int level = 0, members = 0, kernel = -1;
-    int64_t bytes = 0;
-    const char* sched = nullptr;
-    float ms = 0.f;
-    if (group_timing_) {
-      records_.push_back({i, -1, "", 0, 0.0, 1, -1});
-    } else {
-      cuda_ok(disc_cuda_queue_record(i, &level, &members, &bytes, &kernel, &sched, &ms), "group record");
-      records_.push_back({level, kernel, std::string("group:") + (sched ? sched : ""), bytes, 0.0, members, -1});
+  std::vector<std::vector<OutputView>> outs(n);
+  std::vector<ExecStats> sts(n);
+  auto gather = [&](DeviceExecutor& ex) {
+    for (size_t j = 0; j < ex.req_ids_.size() && j < ex.req_outputs_.size(); ++j) {
+      outs[ex.req_ids_[j]] = ex.req_outputs_[j];
+      sts[ex.req_ids_[j]] = ex.req_stats_[j];
     }
-    device_launches_ += 1;
-  }
-  for (int w = 1; w < T; ++w) algorithmic_bytes_ += subs_[w - 1]->algorithmic_bytes();
+  };
+  gather(*this);
+  for (size_t w = 0; w < subs_.size(); ++w)
+    if (sub_used[w]) {
+      subs_[w]->finish_detached();
+      gather(*subs_[w]);
+      algorithmic_bytes_ += subs_[w]->algorithmic_bytes();
+    }
+  req_outputs_.swap(outs);
+  req_stats_.swap(sts);
+  for (const auto& e : errs) std::rethrow_exception(e);
+  cuda_ok(rc, "grouped launch");
   records_grouped_ = true;
   timing_pending_ = group_timing_;
 }

@@ -185,9 +185,12 @@ class DeviceExecutor {
   struct Pool;
   std::unique_ptr<Pool> pool_;
   std::vector<std::unique_ptr<DeviceExecutor>> subs_;
-  void run_requests(int r0, int r1, const CompiledPlan* const* plans, const uint64_t* serials, const int* offs,
-                    const char* const* names, const void* const* data, const int64_t* const* dims, const int* ranks,
-                    bool on_host);
+  void run_requests(const int* ids, int count, const CompiledPlan* const* plans, const uint64_t* serials,
+                    const int* offs, const char* const* names, const void* const* data, const int64_t* const* dims,
+                    const int* ranks, bool on_host);
+  void begin_phase();
+  void append_group_records();
+  std::vector<int> req_ids_;  // request id of each req_outputs_ entry (grouped calls)
   void* detach_grouped();      // worker: issue packed small inputs, hand the queue over
   void finish_detached();      // after the merged flush
   int issue_small_inputs();

@@ -20,17 +20,21 @@ def _reqs(D, graph, shape_list):
     return plan, [(plan, W.input_shapes(graph, s)) for s in shape_list]
 
 
-def test_c2_sweep_is_three_grouped_launches(D):
-    """192 variable-shape LN+GELU requests -> one grouped launch per plan kernel, members
-    ordered by work (largest first), bytes = the requests' algorithmic bytes."""
+def test_c2_sweep_is_three_grouped_launches_per_phase(D):
+    """192 variable-shape LN+GELU requests -> one grouped launch per plan kernel in each of
+    the two flush phases (the largest eighth of the requests first, so the device starts
+    while the host runs the other flows), members ordered by work (largest first), bytes =
+    the requests' algorithmic bytes."""
     from paper_2103_05288_b200 import workloads as W
     g = W.ln_gelu_graph()
     plan, reqs = _reqs(D, g, W.ln_shapes())
     acts = D.group_dry_run(reqs)
-    assert [a["action"] for a in acts] == ["group"] * 3
-    assert [a["level"] for a in acts] == [0, 1, 2]
-    assert [a["kernel"] for a in acts] == [0, 1, 2]
-    assert all(a["members"] == len(reqs) and a["generated"] for a in acts)
+    assert [a["action"] for a in acts] == ["group"] * 6
+    assert [a["level"] for a in acts] == [0, 1, 2] * 2
+    assert [a["kernel"] for a in acts] == [0, 1, 2] * 2
+    assert [a["members"] for a in acts] == [len(reqs) // 8] * 3 + [len(reqs) - len(reqs) // 8] * 3
+    assert all(a["generated"] for a in acts)
+    assert min(acts[0]["order"]) >= max(acts[3]["order"])  # phase 1 = the largest requests
     for a in acts:
         assert a["order"] == sorted(a["order"], reverse=True)
         # compact member records: well under the full descriptor (4.6 / 9.3 KB)
