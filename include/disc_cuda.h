@@ -193,6 +193,7 @@ typedef struct {
 const char* disc_cuda_last_error(void);
 int disc_cuda_device_count(int* n);
 int disc_cuda_set_device(int device);
+int disc_cuda_get_device(int* device);
 int disc_cuda_device_info(int device, int* sm_count, int64_t* l2_bytes, int64_t* hbm_bytes);
 int disc_cuda_stream_create(void** stream);
 int disc_cuda_stream_destroy(void* stream);
@@ -295,6 +296,7 @@ int disc_cuda_queue_record(int i, int* level, int* members, int64_t* bytes, int*
  * return fake addresses and fused launches are recorded as JSON program structures. */
 int disc_cuda_set_capture(int enabled);
 int disc_cuda_capture_records(char** json);   /* free with disc_free */
+int disc_cuda_capturing(void);
 
 #ifdef __cplusplus
 }

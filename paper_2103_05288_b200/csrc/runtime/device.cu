@@ -518,6 +518,13 @@ int disc_cuda_device_count(int* n) {
   }
   return check(cudaGetDeviceCount(n), "cudaGetDeviceCount");
 }
+int disc_cuda_get_device(int* device) {
+  if (g_capture) {
+    *device = 0;
+    return 0;
+  }
+  return check(cudaGetDevice(device), "cudaGetDevice");
+}
 int disc_cuda_set_device(int device) {
   if (g_capture) return 0;
   return check(cudaSetDevice(device), "cudaSetDevice");
@@ -1309,6 +1316,8 @@ int disc_cuda_set_capture(int enabled) {
   if (g_capture) g_records.clear();
   return 0;
 }
+int disc_cuda_capturing(void) { return g_capture ? 1 : 0; }
+
 int disc_cuda_capture_records(char** json) {
   std::string s = "[";
   for (size_t i = 0; i < g_records.size(); ++i) s += (i ? ",\n" : "\n") + g_records[i];

@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <tuple>
 #include <unordered_map>
 
@@ -425,6 +426,34 @@ constexpr int64_t kWideLimitView = (int64_t{1} << 31) - 64;
 // the load is always served from shared memory, see disc_reduce_launch.arg_slot).
 const float* const kArgCachePtr = reinterpret_cast<const float*>(uintptr_t{0xA5C0} << 4);
 
+// DISC_SINGLE_ROWS=0 keeps single-element rows on the row schedule (A/B).
+bool single_rows_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DISC_SINGLE_ROWS");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+// A device float holding -inf (the MAX identity as a hoisted constant load), one per
+// device layer (capture mode: a fake address that is never read).
+const float* neg_inf_ptr() {
+  if (disc_cuda_capturing()) return reinterpret_cast<const float*>(uintptr_t{0xA5D0} << 4);  // dry runs: never read
+  static std::mutex mu;
+  static std::map<int, const float*> per_device;
+  int dev = 0;
+  disc_cuda_get_device(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = per_device.find(dev);
+  if (it != per_device.end()) return it->second;
+  void* d = nullptr;
+  const float v = -INFINITY;
+  if (disc_cuda_malloc(sizeof(float), nullptr, &d) != 0 ||
+      disc_cuda_memcpy(d, &v, sizeof v, 0 | DISC_MEMCPY_NOW, nullptr) != 0 || disc_cuda_stream_synchronize(nullptr) != 0)
+    throw RuntimeError(std::string("constant allocation: ") + disc_cuda_last_error());
+  return per_device[dev] = static_cast<const float*>(d);
+}
+
 // DISC_ARG_CACHE=0 disables the reduce-argument cache (A/B).
 bool arg_cache_enabled() {
   static const bool on = [] {
@@ -557,6 +586,11 @@ class Lowering {
   // Member t is read through an identity load of `ptr` instead of being recomputed
   // (the reduce-argument cache of a fused row epilogue).
   void substitute(int t, const float* ptr) { subst_[t] = ptr; }
+  // Rows of one element: the reduce member is the SSA value v (see launch_fused).
+  void set_reduce_value(int v) {
+    red_value_ = v;
+    memo_[B_.red] = v;
+  }
 
   int value(int t) {
     auto it = memo_.find(t);
@@ -599,8 +633,13 @@ class Lowering {
   const Map* row_map_;
   std::map<int, int> memo_;
   std::map<int, const float*> subst_;
+  int red_value_ = -1;
 
   int reduce_at(const Map& m) {
+    if (red_value_ >= 0) {  // single-element rows: the reduce is an elementwise value
+      if (m == identity_map(numel(B_.dims[B_.red]))) return red_value_;
+      throw NotFusible{"reduce read off-row"};
+    }
     if (row_map_) {
       if (m == *row_map_) return pb_.redval();
       throw NotFusible{"reduce read off-row"};
@@ -960,6 +999,26 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     R.K = nout;
     R.R = 0;
     R.C = 1;
+  }
+
+  // Rows of a single element (softmax over S = 1, ...): the reduce is elementwise -- SUM
+  // gives the value itself (exact through the f64 accumulator), MAX gives std::max(-inf, v)
+  // (v, or -inf for NaN, as the reference's reduce_step) -- so the whole group runs as ONE
+  // vectorised elementwise program instead of a thread-per-row reduction.
+  if (R.schedule == DISC_SCHED_ROW && !empty && R.R == 1 && single_rows_enabled()) {
+    ProgramBuilder pb;
+    pb.set_fast_div(B.art.tape.size() > 1);
+    Lowering lw(B, pb, nullptr, nullptr);
+    int v = lw.at_identity(rarg);
+    if (R.kind == DISC_REDUCE_MAX) v = pb.op(DISC_OP_MAX, pb.load(neg_inf_ptr(), canonical(Map{{geo.K}, {0}, 0})), v);
+    lw.set_reduce_value(v);
+    for (size_t o = 0; o < art.output_tape_indices.size(); ++o) pb.output(lw.value(art.output_tape_indices[o]), outs[o].ptr);
+    Built b = pb.finish(-1);
+    disc_loop_launch L = make_loop(b, geo.K);
+    issue.loop(L);
+    rep.device_kernels = 1;
+    rep.schedule = "row1_loop";
+    return rep;
   }
 
   // Post program: fused into the row kernel when every reduce read is row-aligned.
@@ -1389,8 +1448,8 @@ struct Patch {
     if (kind == kTagExt) p = const_cast<T*>(reinterpret_cast<const T*>(ext.at(idx).ptr));
     else if (kind == kTagOut) p = reinterpret_cast<T*>(outs.at(idx).ptr);
     else if (kind == kTagScratch) p = reinterpret_cast<T*>(scratch.at(idx));
-    else if (v && reinterpret_cast<const float*>(p) != kArgCachePtr)
-      throw InternalError("untagged pointer in a launch recipe");
+    else if (v && reinterpret_cast<const float*>(p) != kArgCachePtr && reinterpret_cast<const float*>(p) != neg_inf_ptr())
+      throw InternalError("untagged pointer in a launch recipe");  // (device constants stay as they are)
   }
   void program(disc_program& P) const {
     for (int l = 0; l < P.n_loads; ++l) (*this)(P.loads[l].ptr);
