@@ -161,7 +161,10 @@ typedef struct {
    * pre program's per-element value) for the epilogue, which reads it as a cached
    * identity load instead of recomputing it (softmax: exp(x - max)); -1 = none */
   int32_t arg_slot;
-  int32_t pad_;
+  /* ROW, vec 4, R % 4 != 0 (only identity / row-splat / const operands): each row runs a
+   * float4 body from its first 16 B-aligned column plus a scalar head and tail; row-cache
+   * rows are padded to R + 3 and shifted so the body stays aligned in shared memory */
+  int32_t unaligned;
 } disc_reduce_launch;
 
 /* Standalone pad (eval_pad, kernels.cpp:125-147), output-driven gather. */

@@ -375,10 +375,12 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
   const int sub = threadIdx.x / G;
   const int rpb = blockDim.x / G;
   // Dynamic smem: [cache_loads slots of slot_stride floats][interpreter slots].
-  const int64_t slot_stride = (static_cast<int64_t>(rpb) * L.R + 3) / 4 * 4;
+  const bool unal = VEC == 4 && L.unaligned;  // float4 body + scalar head/tail per row
+  const int64_t rrow = unal ? (L.R + 6) / 4 * 4 : L.R;  // row pitch in the row cache
+  const int64_t slot_stride = (static_cast<int64_t>(rpb) * rrow + 3) / 4 * 4;
   const int64_t cache_floats = slot_stride * L.cache_loads;
   float* const cache0 = reinterpret_cast<float*>(smem_raw);
-  float* row_cache = L.cache_loads ? cache0 + sub * L.R : nullptr;
+  float* row_cache = L.cache_loads ? cache0 + sub * rrow : nullptr;
   T* slots = reinterpret_cast<T*>(reinterpret_cast<float*>(smem_raw) + cache_floats) + threadIdx.x;
   pdl_enter(L.pre);
   hoist_consts(L.pre, consts[0]);
@@ -414,6 +416,13 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
     }
     const I row = static_cast<I>(base + sub);
     const bool valid = base + sub < rows;
+    // body columns [h, Rb): h = first column whose flat index is 16 B aligned
+    I h = 0, Rb = R;
+    if (unal) {
+      h = static_cast<I>((4 - (static_cast<int64_t>(base + sub) * L.R) % 4) % 4);
+      Rb = h + (R - h) / 4 * 4;
+      if (L.cache_loads) row_cache = cache0 + sub * rrow + ((4 - h) & 3);  // body aligned in smem too
+    }
     // one accumulator per chunk position: CH independent f64 add chains per thread,
     // joined in a fixed order (deterministic)
     using PA = PartAcc<KIND, comp_sum<Pre>()>;
@@ -464,8 +473,8 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
     } else if (valid) {
       // reduce-argument cache (fused epilogue reads the pre value back from smem)
       float* const arg_cache = (!STAGED && L.arg_slot >= 0 && row_cache) ? row_cache + L.arg_slot * sst : nullptr;
-      for (I col0 = static_cast<I>(lane) * VEC; col0 < R; col0 += span) {
-        const int nv = chunks_in_row<CH>(R - col0, cstride);
+      for (I col0 = h + static_cast<I>(lane) * VEC; col0 < Rb; col0 += span) {
+        const int nv = chunks_in_row<CH>(Rb - col0, cstride);
         T v[CH];
         if (Pre::kSplitFull && nv == CH) {
           Pre::template run<VEC, CH, WIDE>(L.pre, Tile<I, true, false, STAGED>{row, col0, R, cstride, CH, row_cache, sst}, v, slots,
@@ -483,6 +492,18 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
 #pragma unroll
           for (int c = 0; c < CH; ++c)
             if (c < nv) *reinterpret_cast<T*>(arg_cache + col0 + c * cstride) = v[c];
+        }
+      }
+      if constexpr (VEC == 4 && !STAGED) {
+        if (unal) {  // scalar head [0, h) and tail [Rb, R)
+          for (I e = static_cast<I>(lane); e < h + (R - Rb); e += static_cast<I>(G)) {
+            const I c = e < h ? e : Rb + (e - h);
+            float vs[1];
+            Pre::template run<1, 1, WIDE>(L.pre, Tile<I, false>{row, c, R, 1, 1, row_cache, sst}, vs,
+                                          reinterpret_cast<float*>(slots), blockDim.x * 4, consts[0], 0.f);
+            part[0] = PA::add(part[0], vs[0]);
+            if (arg_cache) arg_cache[c] = vs[0];
+          }
         }
       }
     }
@@ -510,8 +531,8 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
     if (valid) {
       if (lane == 0 && L.red_out) L.red_out[row] = result;
       if (fuse_post) {
-        for (I col0 = static_cast<I>(lane) * VEC; col0 < R; col0 += span) {
-          const int nv = chunks_in_row<CH>(R - col0, cstride);
+        for (I col0 = h + static_cast<I>(lane) * VEC; col0 < Rb; col0 += span) {
+          const int nv = chunks_in_row<CH>(Rb - col0, cstride);
           T v[CH];
           if (Post::kSplitFull && nv == CH)
             Post::template run<VEC, CH, WIDE>(L.post, Tile<I, true, false, STAGED>{row, col0, R, cstride, CH, row_cache, sst}, v,
@@ -519,6 +540,16 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
           else
             Post::template run<VEC, CH, WIDE>(L.post, Tile<I, false, false, STAGED>{row, col0, R, cstride, nv, row_cache, sst}, v,
                                               slots, blockDim.x, consts[1], result);
+        }
+        if constexpr (VEC == 4 && !STAGED) {
+          if (unal) {
+            for (I e = static_cast<I>(lane); e < h + (R - Rb); e += static_cast<I>(G)) {
+              const I c = e < h ? e : Rb + (e - h);
+              float vs[1];
+              Post::template run<1, 1, WIDE>(L.post, Tile<I, false>{row, c, R, 1, 1, row_cache, sst}, vs,
+                                             reinterpret_cast<float*>(slots), blockDim.x * 4, consts[1], result);
+            }
+          }
         }
       }
     }
@@ -781,7 +812,8 @@ inline size_t row_smem(const disc_reduce_launch& L, bool use_slots) {
   const int slots = L.pre.n_slots > L.post.n_slots ? L.pre.n_slots : L.post.n_slots;
   const int block = row_block(L);
   const int rpb = block / L.group;
-  const size_t cache = static_cast<size_t>((static_cast<int64_t>(rpb) * L.R + 3) / 4 * 4) * L.cache_loads * 4;
+  const int64_t rrow = (L.vec == 4 && L.unaligned) ? (L.R + 6) / 4 * 4 : L.R;
+  const size_t cache = static_cast<size_t>((static_cast<int64_t>(rpb) * rrow + 3) / 4 * 4) * L.cache_loads * 4;
   return cache + (use_slots ? static_cast<size_t>(slots) * CH * block * (L.vec == 4 ? 16 : 4) : 0);
 }
 

@@ -426,6 +426,15 @@ constexpr int64_t kWideLimitView = (int64_t{1} << 31) - 64;
 // the load is always served from shared memory, see disc_reduce_launch.arg_slot).
 const float* const kArgCachePtr = reinterpret_cast<const float*>(uintptr_t{0xA5C0} << 4);
 
+// DISC_UNALIGNED_ROWS=0 keeps odd-width rows on the scalar (vec 1) row kernel (A/B).
+bool unaligned_rows_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DISC_UNALIGNED_ROWS");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 // DISC_SINGLE_ROWS=0 keeps single-element rows on the row schedule (A/B).
 bool single_rows_enabled() {
   static const bool on = [] {
@@ -1074,6 +1083,24 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     bind_view(pre, R.R);
     if (post_fused) bind_view(post, R.R);
     R.vec = choose_vec({&pre, &post}, R.R);
+    // Odd-width rows: float4 body from each row's first 16 B-aligned column + scalar
+    // head/tail, when every operand is a 16 B-aligned identity, a row splat or a constant.
+    if (R.vec == 1 && R.R % 4 != 0 && R.R >= 32 && unaligned_rows_enabled()) {
+      bool ok = true;
+      for (const Built* b : {&pre, &post}) {
+        const disc_program& P = b->prog;
+        for (int l = 0; l < P.n_loads && ok; ++l) {
+          const disc_load& Ld = P.loads[l];
+          ok = (Ld.mode == DISC_LOAD_IDENTITY && aligned16(Ld.ptr)) || Ld.mode == DISC_LOAD_CONST ||
+               (Ld.mode == DISC_LOAD_AFFINE && Ld.cs == 0);
+        }
+        for (int o = 0; o < P.n_outs && ok; ++o) ok = aligned16(P.outs[o]);
+      }
+      if (ok) {
+        R.vec = 4;
+        R.unaligned = 1;
+      }
+    }
   } else if (R.schedule == DISC_SCHED_GENERIC) {
     bind_view(pre, 1);
     R.vec = 1;
@@ -1157,7 +1184,8 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
         const char* e = std::getenv("DISC_ROW_CACHE_KB");
         return int64_t{e ? std::atoi(e) : 48} * 1024;
       }();
-      auto bytes = [&](int gg) { return int64_t{std::max(gg, 256) / gg} * nc * R.R * 4; };
+      const int64_t rrow = R.unaligned ? (R.R + 6) / 4 * 4 : R.R;  // padded rows (kernels.cuh row_body)
+      auto bytes = [&](int gg) { return int64_t{std::max(gg, 256) / gg} * nc * rrow * 4; };
       while (nc && bytes(g) > budget && g < 1024) g <<= 1;
       if (nc && bytes(g) <= budget) {
         R.cache_loads = nc;
