@@ -400,42 +400,6 @@ void DeviceExecutor::run_grouped_batch(int n, const CompiledPlan* const* plans, 
   timing_pending_ = group_timing_;
 }
 
-void DeviceExecutor::end_grouped() {
-  if (!grouped_) return;
-  grouped_ = false;
-  int rc = issue_small_inputs();
-  const auto t_flush = Clock::now();
-  if (rc == 0) rc = disc_cuda_queue_flush(group_timing_ ? 1 : 0);
-  else disc_cuda_queue_flush(0);
-  static const bool prof = std::getenv("DISC_HOST_PROFILE") != nullptr;
-  if (prof)
-    std::fprintf(stderr, "[disc host] grouped call: %zu requests, flow %.3f ms, flush %.3f ms\n", req_outputs_.size(),
-                 std::chrono::duration<double, std::milli>(t_flush - t_group_).count(),
-                 std::chrono::duration<double, std::milli>(Clock::now() - t_flush).count());
-  alloc_.set_defer(false);
-  cuda_ok(rc, "grouped launch");
-  // one record per issued group; device times are read in finish_timing (timing mode)
-  const int n = disc_cuda_queue_num_records();
-  records_.clear();
-  device_launches_ = 0;
-  for (int i = 0; i < n; ++i) {
-    int level = 0, members = 0, kernel = -1;
-    int64_t bytes = 0;
-    const char* sched = nullptr;
-    float ms = 0.f;
-    if (group_timing_) {
-      // metadata only here (the event query would synchronize): read in finish_timing
-      records_.push_back({i, -1, "", 0, 0.0, 1, -1});
-    } else {
-      cuda_ok(disc_cuda_queue_record(i, &level, &members, &bytes, &kernel, &sched, &ms), "group record");
-      records_.push_back({level, kernel, std::string("group:") + (sched ? sched : ""), bytes, 0.0, members, -1});
-    }
-    device_launches_ += 1;
-  }
-  records_grouped_ = true;
-  timing_pending_ = group_timing_;
-}
-
 void DeviceExecutor::finish_timing() {
   if (!timing_pending_) return;
   timing_pending_ = false;
@@ -495,7 +459,7 @@ void DeviceExecutor::set_stream(void* s) {
 const float* DeviceExecutor::stage_input(int slot, const void* host, int64_t bytes) {
   if (grouped_ && bytes <= kSmallInput) {
     // Small host inputs of a grouped call are packed into pinned arena chunks that go H2D
-    // as one copy per chunk ahead of the group (end_grouped), not one PCIe transfer each.
+    // as one copy per chunk ahead of the group's flush, not one PCIe transfer each.
     for (;;) {
       if (small_cur_ == small_.size()) {
         SmallChunk c;

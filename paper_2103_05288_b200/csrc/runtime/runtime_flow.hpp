@@ -102,19 +102,15 @@ class DeviceExecutor {
   // (SURVEY 8(f) rank 2).  On by default; DISC_GRAPHS=0 or set_graphs(false) disables.
   void set_graphs(bool on) { graphs_ = on; }
   int64_t graph_replays() const { return graph_replays_; }
-  // Grouped execution of independent requests (disc_executor_run_grouped):
-  //   begin_grouped(); { begin_request(); [stage_input...]; run(...); } x n; end_grouped();
-  // Each run() evaluates its request's runtime flow on the host (shapes, buffers,
-  // versions, schedules) while the device work is queued; end_grouped() issues it level
-  // by level with the same plan kernel of all requests fused into grouped launches.
-  // Request outputs stay valid until the next run.
-  void begin_grouped();
-  void begin_request();
-  void end_grouped();
-  // Whole grouped call over raw C-ABI arrays (request r: plans[r], inputs offs[r] ..
-  // offs[r+1]-1).  With host threads > 1 and enough requests, contiguous request ranges
-  // run their host flow on worker threads (each with its own sub-executor: allocator,
-  // scratch, recipe cache, queue); the queues are merged into one grouped flush.
+  // Grouped execution of independent requests (disc_executor_run_grouped), over raw
+  // C-ABI arrays (request r: plans[r], inputs offs[r] .. offs[r+1]-1).  Each request's
+  // runtime flow runs on the host (shapes, buffers, versions, schedules) while its device
+  // work is queued (begin_grouped / begin_request / run); the queues are flushed level by
+  // level with the same plan kernel of all requests fused into grouped launches.  With
+  // host threads > 1 and enough requests, contiguous request ranges run on worker threads
+  // (each with its own sub-executor: allocator, scratch, recipe cache, queue) and their
+  // queues are merged into one flush; calls of >= 128 requests flush in two phases (the
+  // largest eighth first).  Request outputs stay valid until the next run.
   void run_grouped_batch(int n, const CompiledPlan* const* plans, const uint64_t* serials, const int* offs,
                          const char* const* names, const void* const* data, const int64_t* const* dims,
                          const int* ranks, bool on_host);
@@ -171,6 +167,8 @@ class DeviceExecutor {
   bool grouped_ = false;
   bool group_timing_ = false;
   bool records_grouped_ = false;  // records_ describe grouped launches
+  void begin_grouped();
+  void begin_request();
   void run_impl(const CompiledPlan& plan, const std::vector<InputBinding>& inputs, bool append_records,
                 uint64_t plan_serial);
   struct GraphEntry {
