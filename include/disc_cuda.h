@@ -232,7 +232,8 @@ int disc_cuda_gemm(int64_t m, int64_t k, int64_t n, const float* a, const float*
                    void* stream);
 /* Fills n floats with uniform [lo, hi) (counter-based; bench/test input synthesis). */
 int disc_cuda_fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, void* stream);
-/* Writes `bytes` to a scratch buffer to evict L2 between timed iterations. */
+/* Writes `bytes` (>= 2x L2) to a scratch buffer, then reads its first half back, to evict L2
+ * between timed iterations and leave it clean (no write-back inside the next kernel). */
 int disc_cuda_flush_l2(void* scratch, size_t bytes, void* stream);
 /* Occupies `stream` for the given time (bench/profiling aid: lets the host queue a run
  * ahead of the device so per-launch events measure device time only). */

@@ -145,6 +145,16 @@ __global__ void k_flush(uint4* p, int64_t n, uint32_t salt) {
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     p[i] = make_uint4(salt, static_cast<uint32_t>(i), salt, 0u);
 }
+// Read pass over the (long since written back) start of the flush buffer: evicts the
+// dirty lines the write pass left in L2, so their write-back is paid here and not inside
+// the next timed kernel.  The sum goes to p[0].w only if impossible (keeps the loads).
+__global__ void k_flush_read(uint4* p, int64_t n) {
+  uint32_t acc = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    acc ^= __ldcg(p + i).y;
+  if (acc == 0xFFFFFFFFu && n > 0) p[0].w = acc;
+}
 
 // Holds the stream for `ns` nanoseconds (globaltimer), so that host submissions queue up
 // behind it and per-launch events then time device execution only.
@@ -274,6 +284,7 @@ cudaError_t flush(void* p, size_t bytes, cudaStream_t s) {
   const int64_t n = static_cast<int64_t>(bytes / 16);
   if (n <= 0) return cudaSuccess;
   k_flush<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(static_cast<uint4*>(p), n, salt++);
+  k_flush_read<<<grid_for(n / 2, 256, 148 * 32), 256, 0, s>>>(static_cast<uint4*>(p), n / 2);
   return cudaGetLastError();
 }
 
