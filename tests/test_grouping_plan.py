@@ -92,3 +92,14 @@ def test_stream_of_10k_requests_collapses(D):
     fused = sum(a["members"] for a in acts if a["action"] in ("group", "alone"))
     assert fused >= len(reqs)
     assert len(acts) < 600, len(acts)
+
+
+@pytest.mark.parametrize("S,kind,vec", [(1, "loop", 4), (2, "row", 1), (777, "row", 4), (4095, "row", 4), (1024, "row", 4)])
+def test_softmax_schedule_by_width(D, S, kind, vec):
+    """Schedule selection by row width (host only, capture mode): single-element rows become
+    one vectorised elementwise program, odd widths >= 32 the float4 body + scalar head/tail
+    row kernel (vec 4), short odd rows stay scalar."""
+    from paper_2103_05288_b200 import workloads as W
+    plan = D.compile_graph(W.softmax_graph_for(0))
+    recs = D.capture_programs(plan, {"x": [64, S]})
+    assert [(r["kind"], r["vec"]) for r in recs] == [(kind, vec)] * 2
