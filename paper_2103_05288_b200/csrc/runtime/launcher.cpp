@@ -435,6 +435,15 @@ bool unaligned_rows_enabled() {
   return on;
 }
 
+// Narrowest odd row width that takes the float4-body row kernel (DISC_UNALIGNED_MIN, A/B).
+int64_t unaligned_min_width() {
+  static const int64_t w = [] {
+    const char* e = std::getenv("DISC_UNALIGNED_MIN");
+    return int64_t{e ? std::atoi(e) : 16};  // A/B: 16 beats the staged kernel on R = 17, 31 (C1 3897 -> 4122)
+  }();
+  return w;
+}
+
 // DISC_SINGLE_ROWS=0 keeps single-element rows on the row schedule (A/B).
 bool single_rows_enabled() {
   static const bool on = [] {
@@ -1085,7 +1094,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     R.vec = choose_vec({&pre, &post}, R.R);
     // Odd-width rows: float4 body from each row's first 16 B-aligned column + scalar
     // head/tail, when every operand is a 16 B-aligned identity, a row splat or a constant.
-    if (R.vec == 1 && R.R % 4 != 0 && R.R >= 32 && unaligned_rows_enabled()) {
+    if (R.vec == 1 && R.R % 4 != 0 && R.R >= unaligned_min_width() && unaligned_rows_enabled()) {
       bool ok = true;
       for (const Built* b : {&pre, &post}) {
         const disc_program& P = b->prog;
@@ -1127,7 +1136,8 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     // block copies its contiguous span of every identity operand through shared memory,
     // one thread per row.  Only when that layout is bank-conflict-free (odd R for scalar
     // rows, odd R/4 for float4 rows); otherwise rows pack 32/G per warp as usual.
-    if (!empty && !R.wide && row_policy() >= 2 && R.R >= 16 && R.R < 32 && (R.vec == 1 ? (R.R & 1) : ((R.R / 4) & 1))) {
+    if (!empty && !R.wide && !R.unaligned && row_policy() >= 2 && R.R >= 16 && R.R < 32 &&
+        (R.vec == 1 ? (R.R & 1) : ((R.R / 4) & 1))) {
       int n = 0;
       auto slot_of_ptr = [&](const float* ptr, const disc_program& P) -> int {
         for (int l = 0; l < P.n_loads; ++l)
