@@ -361,7 +361,7 @@ __device__ __forceinline__ void copy_span(float* __restrict__ dst, const float* 
   }
 }
 
-template <int VEC, bool WIDE, int KIND, typename Pre, typename Post, int CH, bool STAGED>
+template <int VEC, bool WIDE, int KIND, typename Pre, typename Post, int CH, bool STAGED, bool UNAL>
 __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int bx, const int gx) {
   using RD = Red<KIND>;
   using Acc = typename RD::Acc;
@@ -375,7 +375,9 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
   const int sub = threadIdx.x / G;
   const int rpb = blockDim.x / G;
   // Dynamic smem: [cache_loads slots of slot_stride floats][interpreter slots].
-  const bool unal = VEC == 4 && L.unaligned;  // float4 body + scalar head/tail per row
+  // float4 body + scalar head/tail per row: a separate instantiation (UNAL), so aligned
+  // kernels keep their register budget (30 vs 58 registers for a plain row sum)
+  const bool unal = UNAL && VEC == 4 && L.unaligned;
   const int64_t rrow = unal ? (L.R + 6) / 4 * 4 : L.R;  // row pitch in the row cache
   const int64_t slot_stride = (static_cast<int64_t>(rpb) * rrow + 3) / 4 * 4;
   const int64_t cache_floats = slot_stride * L.cache_loads;
@@ -494,7 +496,7 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
             if (c < nv) *reinterpret_cast<T*>(arg_cache + col0 + c * cstride) = v[c];
         }
       }
-      if constexpr (VEC == 4 && !STAGED) {
+      if constexpr (UNAL && VEC == 4 && !STAGED) {
         if (unal) {  // scalar head [0, h) and tail [Rb, R)
           for (I e = static_cast<I>(lane); e < h + (R - Rb); e += static_cast<I>(G)) {
             const I c = e < h ? e : Rb + (e - h);
@@ -541,7 +543,7 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
             Post::template run<VEC, CH, WIDE>(L.post, Tile<I, false, false, STAGED>{row, col0, R, cstride, nv, row_cache, sst}, v,
                                               slots, blockDim.x, consts[1], result);
         }
-        if constexpr (VEC == 4 && !STAGED) {
+        if constexpr (UNAL && VEC == 4 && !STAGED) {
           if (unal) {
             for (I e = static_cast<I>(lane); e < h + (R - Rb); e += static_cast<I>(G)) {
               const I c = e < h ? e : Rb + (e - h);
@@ -685,16 +687,16 @@ __global__ void __launch_bounds__(kLoopThreads, 4) k_loop_g(const __grid_constan
   loop_body<VEC, WIDE, Prog, CH>(L, b - G.block_off[g], G.block_off[g + 1] - G.block_off[g]);
 }
 
-template <int VEC, bool WIDE, int KIND, typename Pre, typename Post, int CH = kCH, bool STAGED = false>
+template <int VEC, bool WIDE, int KIND, typename Pre, typename Post, int CH = kCH, bool STAGED = false, bool UNAL = false>
 __global__ void __launch_bounds__(1024) k_row(const __grid_constant__ disc_reduce_launch L) {
-  row_body<VEC, WIDE, KIND, Pre, Post, CH, STAGED>(L, blockIdx.x, gridDim.x);
+  row_body<VEC, WIDE, KIND, Pre, Post, CH, STAGED, UNAL>(L, blockIdx.x, gridDim.x);
 }
-template <int VEC, bool WIDE, int KIND, typename Pre, typename Post, int CH = kCH, bool STAGED = false>
+template <int VEC, bool WIDE, int KIND, typename Pre, typename Post, int CH = kCH, bool STAGED = false, bool UNAL = false>
 __global__ void __launch_bounds__(1024) k_row_g(const __grid_constant__ disc_group G) {
   __shared__ __align__(16) unsigned char desc[desc_bytes<disc_reduce_launch>()];
   const int b = blockIdx.x, g = group_of(G, b);
   const disc_reduce_launch& L = group_stage<disc_reduce_launch>(G, g, desc);
-  row_body<VEC, WIDE, KIND, Pre, Post, CH, STAGED>(L, b - G.block_off[g], G.block_off[g + 1] - G.block_off[g]);
+  row_body<VEC, WIDE, KIND, Pre, Post, CH, STAGED, UNAL>(L, b - G.block_off[g], G.block_off[g + 1] - G.block_off[g]);
 }
 
 template <int VEC, bool WIDE, int KIND, typename Pre, int CH = kCH>
@@ -959,16 +961,20 @@ template <typename Pre, typename Post, int CH = kCH, bool ALLOW_WIDE = true>
 inline cudaError_t row_pass(const disc_reduce_launch& L, cudaStream_t s, bool use_slots, const HostGroup* g = nullptr) {
   const bool sum = L.kind == DISC_REDUCE_SUM;
   constexpr int C1 = vec1_ch(CH);
-#define DISC_ROW(V, W, ST, C)                                                                                \
-  (g ? (sum ? launch_row_group<C>(k_row_g<V, W, DISC_REDUCE_SUM, Pre, Post, C, ST>, *g, s, use_slots)        \
-            : launch_row_group<C>(k_row_g<V, W, DISC_REDUCE_MAX, Pre, Post, C, ST>, *g, s, use_slots))       \
-     : (sum ? launch_row_with<C>(k_row<V, W, DISC_REDUCE_SUM, Pre, Post, C, ST>, L, s, use_slots)            \
-            : launch_row_with<C>(k_row<V, W, DISC_REDUCE_MAX, Pre, Post, C, ST>, L, s, use_slots)))
+#define DISC_ROW_U(V, W, ST, C, U)                                                                           \
+  (g ? (sum ? launch_row_group<C>(k_row_g<V, W, DISC_REDUCE_SUM, Pre, Post, C, ST, U>, *g, s, use_slots)     \
+            : launch_row_group<C>(k_row_g<V, W, DISC_REDUCE_MAX, Pre, Post, C, ST, U>, *g, s, use_slots))    \
+     : (sum ? launch_row_with<C>(k_row<V, W, DISC_REDUCE_SUM, Pre, Post, C, ST, U>, L, s, use_slots)         \
+            : launch_row_with<C>(k_row<V, W, DISC_REDUCE_MAX, Pre, Post, C, ST, U>, L, s, use_slots)))
+#define DISC_ROW(V, W, ST, C) DISC_ROW_U(V, W, ST, C, false)
   if constexpr (ALLOW_WIDE)
-    if (L.wide) return L.vec == 4 ? DISC_ROW(4, true, false, CH) : DISC_ROW(1, true, false, C1);
+    if (L.wide) return L.vec == 4 ? (L.unaligned ? DISC_ROW_U(4, true, false, CH, true) : DISC_ROW(4, true, false, CH))
+                                  : DISC_ROW(1, true, false, C1);
   if (L.stage) return L.vec == 4 ? DISC_ROW(4, false, true, CH) : DISC_ROW(1, false, true, CH);
-  return L.vec == 4 ? DISC_ROW(4, false, false, CH) : DISC_ROW(1, false, false, C1);
+  if (L.vec == 4) return L.unaligned ? DISC_ROW_U(4, false, false, CH, true) : DISC_ROW(4, false, false, CH);
+  return DISC_ROW(1, false, false, C1);
 #undef DISC_ROW
+#undef DISC_ROW_U
 }
 
 template <typename Pre, int CH = kCH, bool ALLOW_WIDE = true>
