@@ -212,3 +212,11 @@ def test_grouped_host_threads_identical(gpu, ref, threads):
     assert ex.algorithmic_bytes() == one.algorithmic_bytes()
     key = lambda recs: sorted((r["instr"], r["schedule"], r["bytes"], r["device_kernels"]) for r in recs)
     assert key(ex.launch_records()) == key(one.launch_records())
+
+
+def test_grouped_mixed_alignment_rows(gpu):
+    """Aligned and odd-width rows of one plan in one grouped call: separate kernel
+    instantiations, never one group (odd widths run the float4-body row kernel)."""
+    shapes = [{"S0": b, "S1": s} for s, b in [(64, 50), (255, 40), (1024, 9), (777, 11), (17, 300), (16, 300), (1, 500)]]
+    g, plan, reqs = _workload_requests(gpu, "softmax", shapes, 5)
+    _assert_same(gpu.Executor().run_grouped(reqs), _sequential(gpu, reqs), "mixed alignment")

@@ -103,3 +103,11 @@ def test_softmax_schedule_by_width(D, S, kind, vec):
     plan = D.compile_graph(W.softmax_graph_for(0))
     recs = D.capture_programs(plan, {"x": [64, S]})
     assert [(r["kind"], r["vec"]) for r in recs] == [(kind, vec)] * 2
+
+
+def test_odd_and_aligned_rows_never_share_a_group(D):
+    from paper_2103_05288_b200 import workloads as W
+    g = W.softmax_graph_for(0)
+    plan, reqs = _reqs(D, g, [{"S0": 64, "S1": s} for s in (64, 255, 1024, 777)])
+    acts = [a for a in D.group_dry_run(reqs) if a["action"] == "group" and a["level"] == 0]
+    assert sorted(a["members"] for a in acts) == [2, 2]
