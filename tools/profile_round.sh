@@ -5,7 +5,8 @@
 # there; only the ln_gelu report comes back).  Usage: tools/profile_round.sh <tag>
 tag=$1
 mkdir -p gpurun_out
-timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+# (one flush phase, as in the bench's per-kernel timing pass: traffic per launch matches roofline.bytes_per_launch)
+DISC_GROUP_PHASES=1 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   --csv --log-file gpurun_out/launches_bench_$tag.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/launches_bench_$tag.log 2>&1
 for w in ln_gelu softmax colreduce bert; do
