@@ -2,7 +2,7 @@
 # ncu source-level hot spots of one workload shape's kernels (single request):
 #   tools/prof_shape.sh <workload> <shape> <kernel regex> <out>
 w=$1; shape=$2; re=$3; out=$4
-timeout 600 ncu --section SpeedOfLight --section Occupancy --section LaunchStats --section WarpStateStats --section SourceCounters --import-source on --clock-control none -k "regex:$re" -c 2 -o /tmp/ps python tools/profile_one.py --workload $w --shape $shape --reps 1 > /dev/null 2>&1
+timeout 600 ncu --section SpeedOfLight --section Occupancy --section LaunchStats --section WarpStateStats --section SourceCounters --import-source on --clock-control none -f -k "regex:$re" -c 2 -o /tmp/ps python tools/profile_one.py --workload $w --shape $shape --reps 1 > /dev/null 2>&1
 python tools/ncu_summary.py /tmp/ps.ncu-rep > gpurun_out/${out}_summary.txt 2>&1
 python - <<PY > gpurun_out/${out}_hot.txt 2>&1
 import csv, subprocess, io
