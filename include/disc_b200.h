@@ -62,6 +62,10 @@ const char* disc_plan_output_name(disc_plan p, int i);
 int disc_plan_num_kernels(disc_plan p);
 int64_t disc_plan_eager_op_count(disc_plan p);
 int64_t disc_plan_host_instruction_count(disc_plan p);
+/* PlanInput.declared[d] (runtime_program.hpp:28-160): the graph's declared dim, a
+ * symbol name or a decimal constant (drives the CLI's synthetic inputs, disc_main.cpp:113-136). */
+const char* disc_plan_input_declared(disc_plan p, int i, int d);
+const char* disc_plan_signature(disc_plan p);  /* CompiledPlan.signature_digest */
 /* Evaluate the host shape program for concrete input dims (EvalShape, executor.cpp:303-341):
  * writes the register file (up to cap entries) and each output's dims. */
 int disc_plan_eval_shapes(disc_plan p, int n_inputs, const int64_t* const* dims, const int* ranks,

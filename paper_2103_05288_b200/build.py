@@ -130,7 +130,28 @@ def build(clean: bool = False, verbose: bool = True) -> str:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
         if verbose:
             print(f"built {LIB}")
+    if not _VARIANT:
+        build_cli(inc, verbose)
     return LIB
+
+
+CLI_SRC = os.path.join(PKG, "cli", "disc_main.cpp")
+CLI_BIN = os.path.join(PKG, "disc")
+
+
+def build_cli(inc: list, verbose: bool = True) -> str:
+    """The `disc` command-line tool (cli/disc_main.cpp), linked against the in-tree
+    library with an $ORIGIN rpath so it runs from the package directory."""
+    if os.path.exists(CLI_BIN) and os.path.getmtime(CLI_BIN) >= max(os.path.getmtime(CLI_SRC), os.path.getmtime(LIB)):
+        return CLI_BIN
+    cmd = [CXX, *[f for f in CXXFLAGS if f != "-fPIC"], *[f"-I{i}" for i in inc], CLI_SRC, LIB,
+           "-Wl,-rpath,$ORIGIN", "-o", CLI_BIN]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"cli build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    if verbose:
+        print(f"built {CLI_BIN}")
+    return CLI_BIN
 
 
 if __name__ == "__main__":

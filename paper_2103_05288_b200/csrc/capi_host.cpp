@@ -132,6 +132,12 @@ const char* disc_plan_output_name(disc_plan p, int i) { return p->plan->outputs.
 int disc_plan_num_kernels(disc_plan p) { return static_cast<int>(p->plan->kernels.size()); }
 int64_t disc_plan_eager_op_count(disc_plan p) { return p->plan->eager_op_count; }
 int64_t disc_plan_host_instruction_count(disc_plan p) { return p->plan->host_instruction_count(); }
+const char* disc_plan_input_declared(disc_plan p, int i, int d) {
+  const auto& in = p->plan->inputs;
+  if (i < 0 || i >= static_cast<int>(in.size()) || d < 0 || d >= static_cast<int>(in[i].declared.size())) return nullptr;
+  return in[i].declared[d].c_str();
+}
+const char* disc_plan_signature(disc_plan p) { return p->plan->signature_digest.c_str(); }
 
 int disc_plan_eval_shapes(disc_plan p, int n, const int64_t* const* dims, const int* ranks, int64_t* regs,
                           int cap, int* nregs) {
