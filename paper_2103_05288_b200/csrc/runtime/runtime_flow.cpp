@@ -302,8 +302,19 @@ void DeviceExecutor::run_grouped_batch(int n, const CompiledPlan* const* plans, 
     std::nth_element(w.begin(), w.begin() + k, w.end());
     std::vector<char> first(n, 0);
     for (int i = 0; i < k; ++i) first[w[i].second] = 1;
-    phases.resize(2);
-    for (int r = 0; r < n; ++r) phases[first[r] ? 0 : 1].push_back(r);
+    // the other requests: max_phases - 1 contiguous index ranges of equal count
+    phases.resize(max_phases);
+    const int rest = n - k, per = (rest + max_phases - 2) / (max_phases - 1);
+    int seen = 0;
+    for (int r = 0; r < n; ++r) {
+      if (first[r]) {
+        phases[0].push_back(r);
+      } else {
+        phases[1 + std::min(max_phases - 2, seen / std::max(1, per))].push_back(r);
+        ++seen;
+      }
+    }
+    while (phases.size() > 1 && phases.back().empty()) phases.pop_back();
   } else {
     phases.emplace_back(n);
     std::iota(phases[0].begin(), phases[0].end(), 0);
