@@ -1053,8 +1053,12 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
   auto end_rec = [&] {
     if (timing) cudaEventRecord(t_q.records.back().b, st);
   };
+  static const bool prof_issue = std::getenv("DISC_HOST_PROFILE") != nullptr;
+  double kind_ms[4] = {0, 0, 0, 0};
+  int kind_n[4] = {0, 0, 0, 0};
   for (Action& a : acts) {
     if (rc) break;
+    const auto t_a = prof_issue ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
     begin_rec(a);
     switch (a.kind) {
       case kGroup:
@@ -1095,7 +1099,15 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
       }
     }
     end_rec();
+    if (prof_issue) {
+      const int k = static_cast<int>(a.kind) & 3;
+      kind_ms[k] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_a).count();
+      ++kind_n[k];
+    }
   }
+  if (prof_issue)
+    std::fprintf(stderr, "[disc issue] by action kind (n, ms): 0:%d/%.3f 1:%d/%.3f 2:%d/%.3f 3:%d/%.3f\n", kind_n[0],
+                 kind_ms[0], kind_n[1], kind_ms[1], kind_n[2], kind_ms[2], kind_n[3], kind_ms[3]);
   if (total > 0) {
     std::lock_guard<std::mutex> l2(g_ring_mu);
     if (!rc) rc = check(ring_release(ring, base, total, st), "group tables release");
