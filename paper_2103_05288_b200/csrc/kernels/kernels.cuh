@@ -32,6 +32,7 @@ struct Interp {
   static constexpr bool kSplitFull = false;
   static constexpr int kPipe = 0;  // no load/compute split
   static constexpr bool kXuHeavy = false;
+  static constexpr int kMaxRowMinBlocks = 0;  // see k_row_mb
   template <int VEC, int CH, typename Ctx>
   __device__ __forceinline__ static void prefetch(const disc_program&, const Ctx&) {}
   template <int VEC, int CH, bool WIDE, typename Ctx>
@@ -698,6 +699,22 @@ __global__ void __launch_bounds__(1024) k_row_g(const __grid_constant__ disc_gro
   const disc_reduce_launch& L = group_stage<disc_reduce_launch>(G, g, desc);
   row_body<VEC, WIDE, KIND, Pre, Post, CH, STAGED, UNAL>(L, b - G.block_off[g], G.block_off[g + 1] - G.block_off[g]);
 }
+// Max-reduce rows of generated programs with two or more streamed operands (BERT's scaled +
+// masked scores): <= 256 threads and 6 resident blocks (<= 40 registers).  A/B: that row
+// kernel 5522 -> 6155 GB/s, while the single-stream softmax max row loses (5038 -> 4802),
+// so the choice is per pattern (Pre::kMaxRowMinBlocks) and per launch (block <= 256).
+template <int VEC, bool WIDE, typename Pre, typename Post, int CH, bool STAGED, bool UNAL>
+__global__ void __launch_bounds__(256, 6) k_row_mb(const __grid_constant__ disc_reduce_launch L) {
+  row_body<VEC, WIDE, DISC_REDUCE_MAX, Pre, Post, CH, STAGED, UNAL>(L, blockIdx.x, gridDim.x);
+}
+template <int VEC, bool WIDE, typename Pre, typename Post, int CH, bool STAGED, bool UNAL>
+__global__ void __launch_bounds__(256, 6) k_row_g_mb(const __grid_constant__ disc_group G) {
+  __shared__ __align__(16) unsigned char desc[desc_bytes<disc_reduce_launch>()];
+  const int b = blockIdx.x, g = group_of(G, b);
+  const disc_reduce_launch& L = group_stage<disc_reduce_launch>(G, g, desc);
+  row_body<VEC, WIDE, DISC_REDUCE_MAX, Pre, Post, CH, STAGED, UNAL>(L, b - G.block_off[g],
+                                                                   G.block_off[g + 1] - G.block_off[g]);
+}
 
 template <int VEC, bool WIDE, int KIND, typename Pre, int CH = kCH>
 __global__ void __launch_bounds__(kColThreads, 4) k_col(const __grid_constant__ disc_reduce_launch L) {
@@ -954,6 +971,21 @@ inline cudaError_t loop_pass(const disc_loop_launch& L, cudaStream_t s, bool use
                     : launch_loop_with<C1>(k_loop<1, false, Prog, C1>, L, s, use_slots);
 }
 
+// Max-reduce row kernel for a launch (k_row_mb when the pattern asks for it and the
+// launch's block is <= 256 threads).
+template <int V, bool W, typename Pre, typename Post, int C, bool ST, bool U>
+inline void (*max_row_kernel(const disc_reduce_launch& L))(disc_reduce_launch) {
+  if constexpr (Pre::kMaxRowMinBlocks > 0)
+    if (row_block(L) <= 256) return k_row_mb<V, W, Pre, Post, C, ST, U>;
+  return k_row<V, W, DISC_REDUCE_MAX, Pre, Post, C, ST, U>;
+}
+template <int V, bool W, typename Pre, typename Post, int C, bool ST, bool U>
+inline void (*max_row_group_kernel(const HostGroup& H))(disc_group) {
+  if constexpr (Pre::kMaxRowMinBlocks > 0)
+    if (row_block(H.at<disc_reduce_launch>(0)) <= 256) return k_row_g_mb<V, W, Pre, Post, C, ST, U>;
+  return k_row_g<V, W, DISC_REDUCE_MAX, Pre, Post, C, ST, U>;
+}
+
 // Dispatch on (vec, wide, reduce kind) for a given program functor pair.
 // ALLOW_WIDE = false (generated programs, used only on !wide launches) instantiates no
 // 64-bit-index kernels.
@@ -963,9 +995,9 @@ inline cudaError_t row_pass(const disc_reduce_launch& L, cudaStream_t s, bool us
   constexpr int C1 = vec1_ch(CH);
 #define DISC_ROW_U(V, W, ST, C, U)                                                                           \
   (g ? (sum ? launch_row_group<C>(k_row_g<V, W, DISC_REDUCE_SUM, Pre, Post, C, ST, U>, *g, s, use_slots)     \
-            : launch_row_group<C>(k_row_g<V, W, DISC_REDUCE_MAX, Pre, Post, C, ST, U>, *g, s, use_slots))    \
+            : launch_row_group<C>(max_row_group_kernel<V, W, Pre, Post, C, ST, U>(*g), *g, s, use_slots))    \
      : (sum ? launch_row_with<C>(k_row<V, W, DISC_REDUCE_SUM, Pre, Post, C, ST, U>, L, s, use_slots)         \
-            : launch_row_with<C>(k_row<V, W, DISC_REDUCE_MAX, Pre, Post, C, ST, U>, L, s, use_slots)))
+            : launch_row_with<C>(max_row_kernel<V, W, Pre, Post, C, ST, U>(L), L, s, use_slots)))
 #define DISC_ROW(V, W, ST, C) DISC_ROW_U(V, W, ST, C, false)
   if constexpr (ALLOW_WIDE)
     if (L.wide) return L.vec == 4 ? (L.unaligned ? DISC_ROW_U(4, true, false, CH, true) : DISC_ROW(4, true, false, CH))

@@ -91,9 +91,13 @@ def gen_program(fn, prog, ch=1, early_splat=True):
     early = sorted(ident + splat)
     pf = [f"    prefetch_cls<VEC, CH, 0>(P, t, {code[i][5]});" for i, c in loads if c == 0]
     xu = any(I_UN <= c[0] < I_UN + 4 for c in code)  # exp / tanh (MUFU) in the program
+    # streamed operands (not hoisted constants / per-row splats); max-reduce rows over two
+    # or more streams run register-capped at 6 blocks/SM (kernels.cuh k_row_mb)
+    streams = [i for i, c in loads if code[i][0] != I_LOAD_CONST and c != LC_SPLAT]
     lines = [f"struct {fn} {{",
              "  static constexpr bool kSplitFull = true;",
              f"  static constexpr bool kXuHeavy = {'true' if xu else 'false'};",
+             f"  static constexpr int kMaxRowMinBlocks = {6 if fn.startswith('Pre_row') and len(streams) >= 2 else 0};",
              # pipelined only while the extra tile of loads fits (<= 16 registers at VEC=4)
              f"  static constexpr int kPipe = {len(early) if regs <= 16 else 0};",
              "  template <int VEC, int CH>",
