@@ -1,40 +1,47 @@
 #!/usr/bin/env python
 """disc-b200 benchmark: fused-kernel HBM GB/s across a dynamic-shape sweep, 0 recompiles.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload ln_gelu|softmax|colreduce|bert|stream]
-  python bench.py --impl reference ...     # the reference's own CPU executor, same metric
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload sweep|ln_gelu|softmax|colreduce|bert|stream]
+                  [--verify off|sample|full]
+  python bench.py --impl reference ...     # the reference's own CPU executor, same workload
 
-Workload (BASELINE.json configs[1]): one plan of the LN-like + bias +
-tanh-GELU graph compiled ONCE and run over 192 distinct runtime shapes [T, H] (T
-log-uniform 1..16384, 64 samples x H in {768, 1024, 4096}).  A step = one pass over the
-sweep.  Bytes are the algorithmic boundary bytes of every fused launch (SURVEY §8d:
-4 x (external inputs read + external outputs written), broadcast sources at source size).
-``--workload stream`` is C5: >= 10k distinct (graph, shape) requests over C1-C4 and the
-reference fixtures, one plan per graph, 0 recompiles.
+Headline workload ``sweep`` (BASELINE metric; SURVEY §8(d) C5 over the FULL C1-C4
+ranges): every step is 10 000 distinct (graph, shape) requests, kinds round-robin over
+C1 softmax, C2 LN+bias+GELU, C3 column reduce, C4 BERT non-GEMM and the reference
+fixtures, every dimension drawn log-uniformly over its whole configured range, FRESH
+shapes every step (no shape repeats in the run, so the recipe cache is cold).  One plan
+per graph is compiled once: 0 recompiles.  A step = the step's requests issued through
+disc_executor_run_grouped in chunks of ~--chunk-gb of algorithmic bytes (host flow of
+chunk c+1 overlaps the device work of chunk c).  Inputs are views into a device-resident
+arena of uniform [0.25, 2) f32 (inputs already in HBM when the timed region starts,
+>> L2; the L2 is also flushed before every step).
 
-  value    = bytes / device time of the K timed steps (CUDA events on the executor's
-             stream, inputs resident in HBM, L2 flushed before each step)
-  e2e      = same bytes / wall time through the public C ABI with host inputs: H2D of
-             every request's inputs from pinned memory and D2H of its outputs inside
-             the timed region
-  roofline = the dominant kernel (largest share of device time): its bytes / its mean
-             CUDA-event launch duration (measured in an untimed pass queued behind a spin
-             kernel, so events see device execution), against MEASURED_PEAKS.json hbm_gbs
-  cpu_baseline = the reference executor (oracle/_ref, built from /root/reference) on a
-             bounded sample of the same sweep, 1 host thread
+  value    = algorithmic bytes (4 x (external inputs read + outputs
+             written) per fused launch, broadcast sources at source size) of the K timed
+             steps / their device time (CUDA events on the executor stream, max over ranks)
+  e2e      = the same metric through the public C ABI with HOST buffers: H2D of every
+             request's inputs (pinned) and D2H of its outputs inside the timed region, on
+             a stratified sample of a step (bounded pinned memory)
+  roofline = the dominant kernel, keyed (pattern, plan kernel, schedule): its bytes / its
+             mean CUDA-event duration in per-pattern passes, against MEASURED_PEAKS.json
+  cpu_baseline = the reference executor (oracle/_ref) on a stratified sample of the same
+             step, 1 host thread
+  verify   = B200 outputs of a timed step's exact grouped pass against the reference
+             executor (oracle/verify.py): sample (default) or full (every request with
+             inputs <= 2^22 elements + sampled rows of every larger one)
 
-Multi-GPU (torchrun, one process per GPU): the workload is N distinct sweeps (N x the
-requests; C2 draws each replica with its own seed), sharded across ranks by the
-dispatcher's deterministic LPT partition on algorithmic bytes (paper_2103_05288_b200/
-dispatch.py) -- per-GPU work stays ~fixed (weak scaling) and no collective touches the
-data path; the timed region is bracketed by barriers, the max over ranks is reported and
-value = all ranks' bytes / that time.
+Multi-GPU (torchrun, one process per GPU): ``sweep`` draws an independent 10k-request
+stream per rank (weak scaling); the fixed sweeps are replicated and LPT-sharded on
+algorithmic bytes (paper_2103_05288_b200/dispatch.py).  No collective touches the data
+path; barriers bracket the timed region and the max over ranks is reported.
 """
 from __future__ import annotations
 
 import argparse
 import ctypes as C
+import importlib.util
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -48,124 +55,318 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fused-kernel HBM GB/s (% of peak) across dynamic-shape sweep; 0 recompiles"
+LARGE = 64 << 20  # "large shape": a request moving >= 64 MiB of algorithmic bytes
+MAIN_KINDS = ("softmax", "ln_gelu", "colreduce", "bert")
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-# ---------------------------------------------------------------------------
-# Workloads: (description, {kind: graph}, [(kind, syms)])
+def W():
+    """paper_2103_05288_b200/workloads.py loaded by path: pure Python graph/shape
+    definitions, so the reference arm never imports (or maps) the B200 package."""
+    mod = sys.modules.get("disc_workloads")
+    if mod is None:
+        spec = importlib.util.spec_from_file_location("disc_workloads",
+                                                      os.path.join(ROOT, "paper_2103_05288_b200", "workloads.py"))
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        sys.modules["disc_workloads"] = mod
+    return mod
+
+
+def host_info():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
 
 def load_fixtures():
-    """Reference fixture graphs for the C5 stream (GEMM fixtures excluded: library calls)."""
+    """Reference fixture graphs (GEMM fixtures excluded: library calls, not fused kernels)."""
     fx = json.load(open(os.path.join(ROOT, "tests", "golden", "fixtures.json")))
     return {k: (json.loads(v["graph"]), v["bindings"]) for k, v in sorted(fx.items())
             if k not in ("matmul", "transformer")}
 
 
-def workload(name, replica=0):
-    from paper_2103_05288_b200 import workloads as W
+# ---------------------------------------------------------------------------
+# Workloads
+
+class Workload:
+    """name, description, {kind: graph}; requests(step) -> [(kind, syms)].  Fresh
+    workloads draw new shapes every step; fixed ones repeat one sweep."""
+
+    def __init__(self, name, desc, graphs, fixed=None, draw=None):
+        self.name, self.desc, self.graphs = name, desc, graphs
+        self._fixed, self._draw, self._steps = fixed, draw, []
+        self.fresh = draw is not None
+
+    def requests(self, step):
+        if self._fixed is not None:
+            return self._fixed
+        while len(self._steps) <= step:
+            self._steps.append(self._draw(len(self._steps)))
+        return self._steps[step]
+
+
+def make_workload(name, replica=0, n_requests=10000):
+    w = W()
+    if name == "sweep":
+        fx = load_fixtures()
+        graphs = w.sweep_graphs(fx)
+        return Workload(name, f"C5 full-range sweep: {n_requests} distinct (graph, shape) requests per step, fresh "
+                              "shapes every step, over C1 softmax [B<=2^26/S, S<=4096], C2 LN+bias+GELU [T<=16384, "
+                              "H in {768,1024,4096}], C3 column reduce [N<=2^22, C<=4096], C4 BERT non-GEMM "
+                              "[B<=32, S 8..512] and the reference fixtures (chain, diamond, empty, reshape, "
+                              "softmax, split); dims log-uniform", graphs,
+                        draw=lambda step: w.full_sweep(step, n=n_requests, seed=20261017 + 1000003 * replica,
+                                                       fixtures=fx)[1])
     if name == "ln_gelu":
-        g = W.ln_gelu_graph()
-        return ("C2 LN-like+bias+tanh-GELU [T,H], T log-uniform 1..16384 x H {768,1024,4096}", {name: g},
-                [(name, s) for s in W.ln_shapes(seed=20261017 + replica)])
+        return Workload(name, "C2 LN-like+bias+tanh-GELU [T,H], T log-uniform 1..16384 x H {768,1024,4096}",
+                        {name: w.ln_gelu_graph()}, fixed=[(name, s) for s in w.ln_shapes(seed=20261017 + replica)])
     if name == "softmax":
-        return ("C1 softmax [B,S], S 1..4096, B = 2^26/S", {name: W.softmax_graph_for(0)},
-                [(name, {"S0": s["S0"], "S1": s["_S"]}) for s in W.softmax_shapes()])
+        return Workload(name, "C1 softmax [B,S], S 1..4096, B = 2^26/S", {name: w.softmax_graph_for(0)},
+                        fixed=[(name, {"S0": s["S0"], "S1": s["_S"]}) for s in w.softmax_shapes()])
     if name == "colreduce":
-        return "C3 column reduce with prologue [N,C]", {name: W.colreduce_graph()}, \
-            [(name, s) for s in W.colreduce_shapes()]
+        return Workload(name, "C3 column reduce with prologue [N,C]", {name: w.colreduce_graph()},
+                        fixed=[(name, s) for s in w.colreduce_shapes()])
     if name == "bert":
-        return "C4 BERT-base non-GEMM subgraphs, S 8..512, B {1,8,32}", {name: W.bert_graph()}, \
-            [(name, s) for s in W.bert_shapes()]
+        return Workload(name, "C4 BERT-base non-GEMM subgraphs, S 8..512, B {1,8,32}", {name: w.bert_graph()},
+                        fixed=[(name, s) for s in w.bert_shapes()])
     if name == "stream":
-        graphs, reqs = W.mixed_stream(10000, seed=20261017 + replica, fixtures=load_fixtures())
-        return ("C5 stream: 10000 distinct (graph, shape) requests over C1-C4 + fixtures "
-                "(chain, diamond, empty, reshape, softmax, split), <= 4 MB input each", graphs, reqs)
+        graphs, reqs = w.mixed_stream(10000, seed=20261017 + replica, fixtures=load_fixtures())
+        return Workload(name, "C5 small-shape stream: 10000 distinct (graph, shape) requests over C1-C4 + fixtures, "
+                              "<= 4 MB input each (same shapes every step)", graphs, fixed=reqs)
     raise SystemExit(f"unknown workload {name}")
-
-
-def workload_single(name):
-    """(description, graph, [syms]) of a one-graph workload (tools/)."""
-    wname, graphs, reqs = workload(name)
-    (g,) = graphs.values()
-    return wname, g, [s for _, s in reqs]
-
-
-def const_value(name, syms):
-    from paper_2103_05288_b200 import workloads as W
-    if name == "inv_h":
-        return 1.0 / syms.get("H", 1)
-    return W.CONST_INPUTS.get(name)
 
 
 def input_shape(inp, syms):
     return tuple(syms[d] if isinstance(d, str) else d for d in inp["shape"])
 
 
-class Requests:
-    """Device-resident inputs for every request, bound once; run = one stream pass."""
+def const_value(name, syms):
+    if name == "inv_h":
+        return 1.0 / syms.get("H", 1)
+    return W().CONST_INPUTS.get(name)
 
-    def __init__(self, D, graphs, plans, reqs, seed=0):
-        self.D = D
-        self.bufs = []
-        self.input_bytes = 0
-        names, data, dims, offs, hplans = [], [], [], [0], []
-        self._keep = []
+
+def stratified(items, costs, budget, seed=0):
+    """Systematic sample of `items` (sorted by (kind, cost)) whose cost sums to ~budget:
+    every m-th request from a seeded offset, so every pattern and size class is present
+    in proportion."""
+    total = sum(costs)
+    if total <= budget:
+        return list(range(len(items)))
+    order = sorted(range(len(items)), key=lambda i: (items[i][0], costs[i]))
+    m = max(1, math.ceil(total / max(budget, 1)))
+    start = seed % m
+    return sorted(order[start::m])
+
+
+# ---------------------------------------------------------------------------
+# Device side (B200 arm)
+
+class Arena:
+    """Device-resident synthetic inputs: one buffer of uniform [0.25, 2) f32; every request
+    input is a 256 B-aligned view at a moving cursor (wrapping), so consecutive requests
+    read distinct memory.  [1]-shaped constants (eps, GELU constants, 1/H, ...) come from
+    a small constant table."""
+
+    def __init__(self, D, nbytes, stream, seed=0):
+        self.D, self.L, self.stream = D, D.lib(), stream
+        self.nbytes = nbytes // 256 * 256
+        self.ptr = C.c_void_p()
+        D.api._cuda(self.L.disc_cuda_malloc(self.nbytes, stream, C.byref(self.ptr)), "arena")
+        D.api._cuda(self.L.disc_cuda_fill_uniform(self.ptr, self.nbytes // 4, 0x5EED + seed, 0.25, 2.0, stream), "fill")
+        self.cursor = 0
+        self.consts, self.cvals = {}, []
+        self.cptr = C.c_void_p()
+        D.api._cuda(self.L.disc_cuda_malloc(4096, stream, C.byref(self.cptr)), "const table")
+
+    def const(self, v):
+        v = float(np.float32(v))
+        if v not in self.consts:
+            self.consts[v] = len(self.cvals)
+            self.cvals.append(v)
+            arr = np.array(self.cvals, np.float32)
+            self.D.api._cuda(self.L.disc_cuda_memcpy(self.cptr, arr.ctypes.data, arr.nbytes, 0, self.stream), "h2d")
+            self.D.api._cuda(self.L.disc_cuda_stream_synchronize(self.stream), "sync")
+        return self.cptr.value + 4 * self.consts[v]
+
+    def take(self, nbytes):
+        nbytes = (max(nbytes, 4) + 255) // 256 * 256
+        if nbytes > self.nbytes:
+            raise RuntimeError(f"input of {nbytes} B exceeds the {self.nbytes} B arena")
+        if self.cursor + nbytes > self.nbytes:
+            self.cursor = 0
+        p = self.ptr.value + self.cursor
+        self.cursor += nbytes
+        return p
+
+    def d2h(self, ptr, shape, rows=None):
+        """Host copy of a device tensor (optionally only rows `rows` of its leading dim)."""
+        L, D = self.L, self.D
+        shape = tuple(shape)
+        if rows is None:
+            a = np.empty(shape, np.float32)
+            if a.size:
+                D.api._cuda(L.disc_cuda_memcpy(a.ctypes.data, C.c_void_p(ptr), a.nbytes, 1, self.stream), "d2h")
+            return a
+        row = int(np.prod(shape[1:])) if len(shape) > 1 else 1
+        a = np.empty((len(rows),) + shape[1:], np.float32)
+        for j, r in enumerate(rows):
+            if row:
+                D.api._cuda(L.disc_cuda_memcpy(a.ctypes.data + 4 * row * j, C.c_void_p(ptr + 4 * row * int(r)),
+                                               4 * row, 1, self.stream), "d2h")
+        return a
+
+
+class StepBatch:
+    """One step's requests as flat C-ABI arrays (names / data / dims / ranks / offsets /
+    plans), bound to arena views, split into chunks of ~chunk_bytes algorithmic bytes."""
+
+    _names = {}
+
+    def __init__(self, D, arena, graphs, plans, reqs, costs, chunk_bytes):
+        self.D, self.L = D, D.lib()
+        self.reqs, self.costs, self.graphs = reqs, costs, graphs
+        n_in = sum(len(graphs[k]["inputs"]) for k, _ in reqs)
+        self.names = np.zeros(max(n_in, 1), np.uint64)
+        self.data = np.zeros(max(n_in, 1), np.uint64)
+        self.dimsp = np.zeros(max(n_in, 1), np.uint64)
+        self.ranks = np.zeros(max(n_in, 1), np.int32)
+        self.offs = np.zeros(len(reqs) + 1, np.int32)
+        self.plans = np.array([plans[k]._h.value for k, _ in reqs] or [0], np.uint64)
+        flat = []
+        self.bind = []  # per request: [(input id, ptr, shape)]
+        i = 0
         for r, (kind, syms) in enumerate(reqs):
-            g = graphs[kind]
-            for j, i in enumerate(g["inputs"]):
-                shape = input_shape(i, syms)
-                cv = const_value(i["id"], syms)
-                if cv is not None:
-                    b = D.DeviceBuffer.from_numpy(np.full(shape, cv, np.float32))
-                else:
-                    b = D.DeviceBuffer(shape)
-                    b.fill_uniform(seed * 1000003 + r * 97 + j)
-                self.bufs.append(b)
-                d = np.array(shape, dtype=np.int64)
-                self._keep.append(d)
-                names.append(i["id"].encode())
-                data.append(b.ptr.value)
-                dims.append(d)
-                self.input_bytes += b.nbytes
-            offs.append(len(names))
-            hplans.append(plans[kind]._h)
-        self.n = len(reqs)
-        t = max(len(names), 1)
-        self.c_names = (C.c_char_p * t)(*names)
-        self.c_data = (C.c_void_p * t)(*data)
-        self.c_dims = (C.c_void_p * t)(*[d.ctypes.data for d in dims])
-        self.c_ranks = (C.c_int * t)(*[d.size for d in dims])
-        self.c_offs = (C.c_int * (self.n + 1))(*offs)
-        self.c_plans = (C.c_void_p * max(self.n, 1))(*hplans)
+            b = []
+            for inp in graphs[kind]["inputs"]:
+                shape = input_shape(inp, syms)
+                cv = const_value(inp["id"], syms)
+                p = arena.const(cv) if cv is not None else arena.take(4 * int(np.prod(shape)))
+                nm = StepBatch._names.setdefault(inp["id"], C.create_string_buffer(inp["id"].encode()))
+                self.names[i] = C.addressof(nm)
+                self.data[i] = p
+                self.ranks[i] = len(shape)
+                flat.append((i, shape))
+                b.append((inp["id"], p, shape))
+                i += 1
+            self.offs[r + 1] = i
+            self.bind.append(b)
+        self.dims_flat = np.array([d for _, s in flat for d in s] or [0], np.int64)
+        pos = 0
+        base = self.dims_flat.ctypes.data
+        for k, s in flat:
+            self.dimsp[k] = base + 8 * pos
+            pos += len(s)
+        # chunks: consecutive requests up to chunk_bytes of algorithmic bytes
+        self.chunks, r0, acc = [], 0, 0
+        for r, c in enumerate(costs):
+            acc += c
+            if acc >= chunk_bytes:
+                self.chunks.append((r0, r + 1))
+                r0, acc = r + 1, 0
+        if r0 < len(reqs):
+            self.chunks.append((r0, len(reqs)))
+        self.chunk_offs = [np.ascontiguousarray(self.offs[a:b + 1] - self.offs[a]) for a, b in self.chunks]
+        self.bytes = int(sum(costs))
 
-    def run(self, ex):
-        if self.n == 0:
-            return
-        rc = self.D.lib().disc_executor_run_stream(ex._h, self.n, self.c_plans, self.c_offs, self.c_names,
-                                                    self.c_data, self.c_dims, self.c_ranks, 0)
-        self.D.api._check(rc)
+    def _p(self, arr, k, ctype):
+        return C.cast(C.c_void_p(arr.ctypes.data + arr.itemsize * int(k)), C.POINTER(ctype))
 
-    def run_grouped(self, ex):
-        """One grouped call: every request's runtime flow on the host, then the same plan
-        kernel of all requests as one grouped launch (disc_executor_run_grouped)."""
-        if self.n == 0:
-            return
-        rc = self.D.lib().disc_executor_run_grouped(ex._h, self.n, self.c_plans, self.c_offs, self.c_names,
-                                                     self.c_data, self.c_dims, self.c_ranks, 0)
-        self.D.api._check(rc)
+    def run(self, ex, on_chunk=None):
+        L = self.L
+        for ci, (a, b) in enumerate(self.chunks):
+            i0 = int(self.offs[a])
+            rc = L.disc_executor_run_grouped(ex._h, b - a, self._p(self.plans, a, C.c_void_p),
+                                             self.chunk_offs[ci].ctypes.data_as(C.POINTER(C.c_int)),
+                                             self._p(self.names, i0, C.c_char_p), self._p(self.data, i0, C.c_void_p),
+                                             self._p(self.dimsp, i0, C.c_void_p), self._p(self.ranks, i0, C.c_int), 0)
+            self.D.api._check(rc)
+            if on_chunk is not None:
+                on_chunk(ci, a, b)
 
-    def run_streams(self, exs, which):
-        """Requests interleaved over executors (own stream each): request r on which[r]."""
-        if self.n == 0:
-            return
-        c_exs = (C.c_void_p * len(exs))(*[e._h for e in exs])
-        c_which = (C.c_int * self.n)(*which)
-        rc = self.D.lib().disc_executors_run_interleaved(c_exs, len(exs), self.n, c_which, self.c_plans, self.c_offs,
-                                                          self.c_names, self.c_data, self.c_dims, self.c_ranks, 0)
-        self.D.api._check(rc)
+
+class Bench:
+    """Device state of the B200 arm: executor, arena, plans, events, L2 flush buffer."""
+
+    def __init__(self, D, args, local, workload):
+        self.D, self.L, self.args, self.wl, self.local = D, D.lib(), args, workload, local
+        L = self.L
+        D.api._cuda(L.disc_cuda_set_device(local))
+        st = C.c_void_p()
+        D.api._cuda(L.disc_cuda_stream_create(C.byref(st)))
+        self.stream = st
+        self.ex = D.Executor(local, st.value)
+        self.ex.set_schedule(args.schedule)
+        self.ex.set_host_threads(args.host_threads)
+        self.ex.set_cache_budget(int(args.cache_gb * (1 << 30)))
+        self.compiler = D.Compiler()
+        self.plans = {}
+        sm, l2, hbm = C.c_int(), C.c_int64(), C.c_int64()
+        L.disc_cuda_device_info(local, C.byref(sm), C.byref(l2), C.byref(hbm))
+        self.hbm = hbm.value
+        self.flush_bytes = max(4 * l2.value, 1 << 28)
+        self.flush = C.c_void_p()
+        D.api._cuda(L.disc_cuda_malloc(self.flush_bytes, st, C.byref(self.flush)))
+        arena_bytes = int(min(args.arena_gb * (1 << 30), 0.3 * self.hbm)) if self.hbm else int(args.arena_gb * (1 << 30))
+        self.arena = Arena(D, arena_bytes, st, seed=local)
+        D.api._cuda(L.disc_cuda_stream_synchronize(st))
+
+    def plans_for(self, reqs):
+        for k in {k for k, _ in reqs}:  # one compile per distinct graph (Compiler cache); the handle is kept
+            if k not in self.plans:      # alive for every batch that points at it
+                self.plans[k] = self.compiler.compile(self.wl.graphs[k])
+        return self.plans
+
+    def costs(self, reqs):
+        g = self.wl.graphs
+        return [self.plans[k].algorithmic_bytes({i["id"]: input_shape(i, s) for i in g[k]["inputs"]}) for k, s in reqs]
+
+    def batch(self, reqs, costs=None):
+        self.plans_for(reqs)
+        costs = costs if costs is not None else self.costs(reqs)
+        return StepBatch(self.D, self.arena, self.wl.graphs, self.plans, reqs, costs, self.args.chunk_gb * (1 << 30))
+
+    def event(self):
+        e = C.c_void_p()
+        self.D.api._cuda(self.L.disc_cuda_event_create(C.byref(e)))
+        return e
+
+    def timed_pass(self, batch, flush=True):
+        """Device ms of one pass over `batch` (events on the executor stream)."""
+        L = self.L
+        a, b = self.event(), self.event()
+        if flush:
+            L.disc_cuda_flush_l2(self.flush, self.flush_bytes, self.stream)
+        L.disc_cuda_event_record(a, self.stream)
+        batch.run(self.ex)
+        L.disc_cuda_event_record(b, self.stream)
+        L.disc_cuda_stream_synchronize(self.stream)
+        ms = C.c_float()
+        L.disc_cuda_event_elapsed_ms(a, b, C.byref(ms))
+        L.disc_cuda_event_destroy(a)
+        L.disc_cuda_event_destroy(b)
+        return ms.value
+
+    def record_pass(self, batch):
+        """Per grouped launch records (timing mode: device ms per launch) of one pass."""
+        recs = []
+        self.ex.set_timing(True)
+        self.L.disc_cuda_flush_l2(self.flush, self.flush_bytes, self.stream)
+        self.L.disc_cuda_spin(20000, self.stream)  # queue behind a spin: events see device time
+        batch.run(self.ex, on_chunk=lambda ci, a, b: recs.extend(self.ex.launch_records()))
+        self.ex.set_timing(False)
+        self.L.disc_cuda_stream_synchronize(self.stream)
+        return recs
 
 
 # ---------------------------------------------------------------------------
@@ -173,9 +374,7 @@ class Requests:
 
 class ClockSampler:
     def __init__(self, device):
-        self.samples = []
-        self.proc = None
-        self.device = device
+        self.samples, self.proc, self.device = [], None, device
 
     def __enter__(self):
         try:
@@ -217,31 +416,29 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-# ---------------------------------------------------------------------------
-
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
-        j = json.load(open(p))
-        return float(j["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(json.load(open(p))["hbm_gbs"]), "measured MEASURED_PEAKS.json hbm_gbs"
+    return 6650.0, "fallback B200_PROFILING.md"
 
 
-def ncu_traffic(schedule):
-    """dram bytes per launch for the dominant kernel from the committed ncu summary."""
-    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if not os.path.exists(p):
-        return None
+def ncu_traffic(workload, key):
+    """DRAM bytes per launch of kernel `key` ("pattern:k<artifact>:<schedule>") from the
+    committed same-workload ncu capture (tools/profile_kernels.py -> profiles/ncu_traffic.json),
+    with the algorithmic bytes of the profiled launches for comparison."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        t = json.load(open(p)).get("traffic_per_launch", {})
+        t = json.load(open(p)).get(workload, {}).get(key)
     except Exception:
-        return None
-    while schedule:  # "group:row_fused_cached" -> "group:row_fused" -> "group:row"
-        if schedule in t:
-            return t[schedule]
-        schedule = schedule.rsplit("_", 1)[0] if "_" in schedule else ""
-    return None
+        return None, None
+    if not t:
+        return None, None
+    return t.get("dram_bytes_per_launch"), t
 
+
+# ---------------------------------------------------------------------------
+# Distributed plumbing
 
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -272,7 +469,8 @@ def barrier(dist, local):
         import torch
         t = torch.zeros(1, device=_dev(dist, local))
         dist.all_reduce(t)
-        torch.cuda.synchronize()
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
 
 
 def allreduce(dist, local, v, op="max"):
@@ -284,376 +482,218 @@ def allreduce(dist, local, v, op="max"):
     return float(t.item())
 
 
-def make_inputs(graph, syms, rng):
-    inputs = {}
-    for i in graph["inputs"]:
-        shape = input_shape(i, syms)
-        cv = const_value(i["id"], syms)
-        inputs[i["id"]] = np.full(shape, cv, np.float32) if cv is not None else \
-            rng.uniform(0.25, 2.0, size=shape).astype(np.float32)
-    return inputs
+# ---------------------------------------------------------------------------
+# Reference (CPU) side: cpu_baseline and --impl reference.  Inputs are views into a host
+# pool of uniform [0.25, 2) f32 (the reference executor copies its inputs anyway).
+
+class HostPool:
+    def __init__(self, numel=1 << 27, seed=0):
+        self.a = np.random.default_rng(seed).uniform(0.25, 2.0, size=numel).astype(np.float32)
+        self.cursor = 0
+
+    def inputs(self, graph, syms):
+        out = {}
+        for i in graph["inputs"]:
+            shape = input_shape(i, syms)
+            cv = const_value(i["id"], syms)
+            if cv is not None:
+                out[i["id"]] = np.full(shape, cv, np.float32)
+                continue
+            n = int(np.prod(shape))
+            if self.cursor + n > self.a.size:
+                self.cursor = 0
+            out[i["id"]] = self.a[self.cursor:self.cursor + n].reshape(shape)
+            self.cursor += (n + 63) // 64 * 64
+        return out
 
 
-def cpu_order(costs):
-    """Request indices from the median of the byte distribution outward (bounded samples
-    that stay representative of mid-size requests)."""
-    order = sorted(range(len(costs)), key=lambda i: costs[i])
-    mid = len(order) // 2
-    out = []
-    for d in range(len(order)):
-        for j in ((mid + d, mid - d - 1) if d else (mid,)):
-            if 0 <= j < len(order) and order[j] not in out:
-                out.append(order[j])
-    return out
+def ref_costs(ref_plans_bytes, graphs, reqs):
+    return [ref_plans_bytes[k]({i["id"]: input_shape(i, s) for i in graphs[k]["inputs"]}) for k, s in reqs]
 
 
-def cpu_baseline(graphs, reqs, costs, budget_s=15.0):
-    """Reference executor (oracle/_ref) on a bounded sample of the sweep, 1 thread:
-    requests from the median outward until ~budget_s of CPU time."""
-    from oracle import ref
+def cpu_baseline(workload, reqs, budget_s=15.0):
+    """Reference executor (oracle/_ref) on a stratified sample of one step, 1 thread."""
+    from oracle import plan_bytes, ref
     if not ref.available():
         return None
-    rps = {k: ref.RefPlan(ref.compile(json.dumps(g))) for k, g in graphs.items()}
-    rng = np.random.default_rng(0)
-    total_bytes, total_s, used = 0, 0.0, []
-    t_start = time.perf_counter()
-    for i in cpu_order(costs):
+    rj = {k: ref.compile(json.dumps(g)) for k, g in workload.graphs.items()}
+    pb = {k: plan_bytes.PlanBytes(j) for k, j in rj.items()}
+    costs = ref_costs(pb, workload.graphs, reqs)
+    pick = stratified(reqs, costs, 0.16e9 * budget_s)  # ~0.16 GB/s per reference thread
+    rps = {k: ref.RefPlan(j) for k, j in rj.items()}
+    pool = HostPool()
+    tot_b, tot_s = 0, 0.0
+    for i in pick:
         kind, syms = reqs[i]
-        inputs = make_inputs(graphs[kind], syms, rng)
-        rps[kind].run(inputs)  # warm the reference allocator cache
-        total_s += rps[kind].time(inputs, 1)
-        total_bytes += costs[i]
-        used.append({k: v for k, v in syms.items() if not k.startswith("_")})
-        if total_s > budget_s or time.perf_counter() - t_start > 3 * budget_s:
-            break
-    return {"value": total_bytes / total_s / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference",
-            "sample": f"{len(used)} requests of the same sweep from the median size outward "
-                      f"(e.g. {used[0]}), reference Executor::run, 1 thread, {total_s:.1f}s timed"}
+        x = pool.inputs(workload.graphs[kind], syms)
+        tot_s += rps[kind].time(x, 1)
+        tot_b += costs[i]
+    return {"value": tot_b / max(tot_s, 1e-9) / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference",
+            "sample": f"{len(pick)} of {len(reqs)} requests of the same step (stratified by pattern and size, "
+                      f"{tot_b / 1e9:.2f} GB), reference Executor::run (oracle/_ref), 1 thread, {tot_s:.1f} s",
+            "host": host_info()}
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the reference's CPU executor, all host threads, same metric."""
+    """--impl reference: the reference's own CPU executor (oracle/_ref, built unmodified
+    from /root/reference) on every host thread, over the SAME per-step request lists as the
+    B200 arm (same workload, seeds and steps), each step a stratified bounded sample.
+    Byte accounting comes from the reference's own plan JSON (oracle/plan_bytes.py); the
+    B200 package is never imported."""
     if world > 1 and rank != 0:
         return
-    from oracle import ref
-    import paper_2103_05288_b200 as D
-    wname, graphs, reqs = workload(args.workload)
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import plan_bytes, ref
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    from concurrent.futures import ThreadPoolExecutor
+    wl = make_workload(args.workload, 0, args.requests)
     nthreads = os.cpu_count() or 1
-    plans = {k: D.compile_graph(g) for k, g in graphs.items()}  # byte accounting only (host shape program)
-    costs = [plans[k].algorithmic_bytes({i["id"]: input_shape(i, s) for i in graphs[k]["inputs"]}) for k, s in reqs]
-    # per step: requests from the median outward, ~1 s of single-thread reference work per
-    # host thread (estimated at the reference's ~0.2 GB/s/thread), all threads busy
-    order = cpu_order(costs)
-    budget = 0.2e9 * 1.0 * nthreads
-    pick, acc = [], 0
-    for i in order:
-        pick.append(i)
-        acc += costs[i]
-        if acc >= budget or len(pick) >= 4096:
-            break
-    sample, scost = [reqs[i] for i in pick], [costs[i] for i in pick]
-    rng = np.random.default_rng(0)
-    inputs = [make_inputs(graphs[k], s, rng) for k, s in sample]
-    ref_json = {k: ref.compile(json.dumps(g)) for k, g in graphs.items()}
-    rps = [{k: ref.RefPlan(j) for k, j in ref_json.items()} for _ in range(nthreads)]
-    nbytes = sum(scost)
+    rj = {k: ref.compile(json.dumps(g)) for k, g in wl.graphs.items()}
+    pb = {k: plan_bytes.PlanBytes(j) for k, j in rj.items()}
+    rps = [{k: ref.RefPlan(j) for k, j in rj.items()} for _ in range(nthreads)]
+    pool = HostPool()
+    step_budget = args.ref_step_s * 1.3e9 * nthreads / 16  # ~1.3 GB/s on 16 reference threads
 
-    def step():
+    def step(i, budget):
+        reqs = wl.requests(i)
+        costs = ref_costs(pb, wl.graphs, reqs)
+        pick = stratified(reqs, costs, budget, seed=i)
+        inputs = [pool.inputs(wl.graphs[reqs[j][0]], reqs[j][1]) for j in pick]
+        order = sorted(range(len(pick)), key=lambda j: -costs[pick[j]])  # LPT over the threads
+        lanes = [[] for _ in range(nthreads)]
+        load = [0] * nthreads
+        for j in order:
+            t = load.index(min(load))
+            lanes[t].append(j)
+            load[t] += costs[pick[j]]
+
         def work(t):
-            for i in range(t, len(sample), nthreads):
-                rps[t][sample[i][0]].time(inputs[i], 1)
-        with ThreadPoolExecutor(nthreads) as pool:
-            list(pool.map(work, range(nthreads)))
+            for j in lanes[t]:
+                rps[t][reqs[pick[j]][0]].time(inputs[j], 1)
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(nthreads) as ex:
+            list(ex.map(work, range(nthreads)))
+        return time.perf_counter() - t0, sum(costs[j] for j in pick), len(pick), len(reqs)
 
-    for _ in range(args.warmup):
-        step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    dt = time.perf_counter() - t0
-    v = nbytes * args.steps / dt / 1e9
-    sample_desc = f"{len(sample)} requests of the sweep per step, reference Executor::run, {nthreads} threads"
+    for i in range(args.warmup):
+        step(i, step_budget / 8)
+    secs = nbytes = npick = nreq = 0
+    for i in range(args.warmup, args.warmup + args.steps):
+        s, b, p, n = step(i, step_budget)
+        secs += s
+        nbytes += b
+        npick += p
+        nreq += n
+    v = nbytes / secs / 1e9
+    sample = (f"{npick} of {nreq} requests over {args.steps} steps (the B200 arm's steps {args.warmup}.."
+              f"{args.warmup + args.steps - 1}; stratified by pattern and size), reference Executor::run "
+              f"(oracle/_ref), {nthreads} threads")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": wname, "sample": sample_desc},
-        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": nthreads, "kind": "reference", "sample": sample_desc},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (uniform [0.25, 2) f32)",
+        "config": {"workload": wl.desc, "requests_per_step": len(wl.requests(args.warmup)), "sample": sample},
+        "host": host_info(),
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": nthreads, "kind": "reference", "sample": sample},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="disc", choices=["disc", "reference"])
-    ap.add_argument("--workload", default="ln_gelu")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--schedule", default="auto")
-    ap.add_argument("--e2e-pipes", type=int, default=3, help="executors/streams the e2e pass alternates over")
-    ap.add_argument("--e2e-chunk-mb", type=int, default=256,
-                    help="grouped e2e: boundary bytes per disc_executor_run_grouped call")
-    ap.add_argument("--mode", default="grouped", choices=["grouped", "streams"],
-                    help="grouped: one disc_executor_run_grouped call per step (the same plan kernel of all "
-                         "requests fused into one grouped launch); streams: per-request launches interleaved "
-                         "over --streams executors")
-    ap.add_argument("--host-threads", type=int, default=min(16, os.cpu_count() or 1),
-                    help="grouped mode: host threads running the requests' runtime flows")
-    ap.add_argument("--streams", type=int, default=2,
-                    help="executors/streams per GPU the requests are interleaved over (independent requests overlap)")
-    ap.add_argument("--stream-policy", default="lpt", choices=["size", "lpt"],
-                    help="size: requests >= --big-bytes on stream 0, the rest LPT over the others; lpt: LPT over all")
-    ap.add_argument("--big-bytes", type=float, default=256e6)
-    ap.add_argument("--pdl", type=int, default=1, choices=[0, 1, 2],
-                    help="programmatic dependent launch: 0 off, 1 overlap launch, 2 + early CTA launch")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
+# ---------------------------------------------------------------------------
+# Verification of a timed step's exact grouped pass (outside the timed region)
 
-    world, rank, local, dist = dist_setup(args)
-    if args.impl == "reference":
-        run_reference(args, world, rank)
-        if dist is not None:
-            dist.destroy_process_group()
-        return
-
-    import paper_2103_05288_b200 as D
-    from paper_2103_05288_b200.dispatch import shard
-    D.lib()
-    D.set_pdl(args.pdl)
-    wname, graphs, reqs = workload(args.workload)
-    for r in range(1, world):  # N distinct sweeps, sharded below
-        _, g2, rq2 = workload(args.workload, replica=r)
-        graphs.update(g2)
-        reqs = reqs + rq2
-    D.api._cuda(D.lib().disc_cuda_set_device(local))
-    streams, exs = [], []
-    for _ in range(max(1, args.streams) if args.mode == "streams" else 1):
-        st = C.c_void_p()
-        D.api._cuda(D.lib().disc_cuda_stream_create(C.byref(st)))
-        streams.append(st)
-        exs.append(D.Executor(local, st.value))
-        exs[-1].set_schedule(args.schedule)
-        if args.mode == "grouped":
-            exs[-1].set_host_threads(args.host_threads)
-    stream, ex = streams[0], exs[0]
-    compiler = D.Compiler()
-    plans = {}
-    for k, s in reqs:  # every request asks the cache: 1 compile per distinct graph
-        plans[k] = compiler.compile(graphs[k])
-    costs = [plans[k].algorithmic_bytes({i["id"]: input_shape(i, s) for i in graphs[k]["inputs"]}) for k, s in reqs]
-    mine = shard(costs, world)[rank]
-    my_reqs = [reqs[i] for i in mine]
-    my_bytes = sum(costs[i] for i in mine)
-    which = [0] * len(mine)  # request -> local stream
-    mc = [costs[i] for i in mine]
-    if args.stream_policy == "size" and len(exs) > 1:
-        # large requests serialise on stream 0 (one-wave kernels that fill the GPU);
-        # small/mid ones (latency-bound per kernel) spread over the other streams
-        small = [j for j, c in enumerate(mc) if c < args.big_bytes]
-        for k, part in enumerate(shard([mc[j] for j in small], len(exs) - 1)):
-            for j in part:
-                which[small[j]] = k + 1
+def verify_pass(B, wl, batch, mode, threads, seed=0):
+    """Re-runs a timed step's batch exactly as timed (same arena inputs, chunks, grouped
+    calls, host threads and flush phases), pulls inputs/outputs of the checked requests and
+    hands them to the reference checker (oracle/verify.py)."""
+    from oracle import verify as V
+    rng = np.random.default_rng(seed)
+    reqs, costs = batch.reqs, batch.costs
+    if mode == "sample":  # every large request gets a chance, small ones a stratified share
+        chosen = set(stratified(reqs, costs, 2e9, seed=seed))
+        large_frac = 0.05
     else:
-        for k, part in enumerate(shard(mc, len(exs))):  # balanced by bytes (LPT)
-            for j in part:
-                which[j] = k
-    rq = Requests(D, graphs, plans, my_reqs, seed=rank)
-    D.api._cuda(D.lib().disc_cuda_device_synchronize())
+        chosen = set(range(len(reqs)))
+        large_frac = 1.0
+    checker = V.Checker(wl.graphs, threads=threads)
+    A = B.arena
 
-    sm, l2, hbm = C.c_int(), C.c_int64(), C.c_int64()
-    D.lib().disc_cuda_device_info(local, C.byref(sm), C.byref(l2), C.byref(hbm))
-    flush_bytes = max(4 * l2.value, 1 << 28)
-    flush = C.c_void_p()
-    D.api._cuda(D.lib().disc_cuda_malloc(flush_bytes, stream, C.byref(flush)))
-    ev = [C.c_void_p(), C.c_void_p()]
-    for e in ev:
-        D.api._cuda(D.lib().disc_cuda_event_create(C.byref(e)))
-    join = []
-    for _ in streams:
-        e = C.c_void_p()
-        D.api._cuda(D.lib().disc_cuda_event_create(C.byref(e)))
-        join.append(e)
-    L = D.lib()
+    def on_chunk(ci, a, b):
+        B.L.disc_cuda_stream_synchronize(B.stream)
+        for r in range(a, b):
+            kind, syms = reqs[r]
+            shapes = {name: shape for name, _, shape in batch.bind[r]}
+            small = max((int(np.prod(s)) for s in shapes.values()), default=0) <= V.SMALL_NUMEL
+            if small and r not in chosen:
+                continue
+            if not small and rng.random() >= large_frac:
+                continue
+            plan = V.check_plan(kind, shapes, True, rng)
+            if plan is None:
+                continue
+            views = B.ex.request_output_views(r - a)
+            picks = V.expected_output_rows(kind, plan, len(views))
+            inputs, got = {}, []
+            if plan.mode == "rows":
+                ins, _ = V.ROW_SPEC[kind]
+                for name, p, shape in batch.bind[r]:
+                    inputs[name] = A.d2h(p, shape, plan.pick[ins[name]]) if name in ins else A.d2h(p, shape)
+                for (p, dims), rows in zip(views, picks):
+                    got.append(A.d2h(p, dims, rows))
+            elif plan.mode == "cols":
+                cols = plan.pick["c"]
+                for name, p, shape in batch.bind[r]:
+                    full = A.d2h(p, shape)
+                    ax = V.COL_SPEC[kind][0].get(name)
+                    inputs[name] = np.ascontiguousarray(np.take(full, cols, axis=ax)) if ax is not None else full
+                for (p, dims), _ in zip(views, picks):
+                    got.append(A.d2h(p, dims)[cols])
+            else:
+                for name, p, shape in batch.bind[r]:
+                    inputs[name] = A.d2h(p, shape)
+                for p, dims in views:
+                    got.append(A.d2h(p, dims))
+            B.L.disc_cuda_stream_synchronize(B.stream)
+            checker.submit(f"{kind} {syms}", kind, plan.mode, inputs, got)
 
-    def one_pass():
-        """One pass over this rank's requests, all streams joined back into streams[0]."""
-        if args.mode == "grouped":
-            rq.run_grouped(ex)
-            return
-        if len(exs) == 1:
-            rq.run(ex)
-            return
-        for st in streams[1:]:
-            L.disc_cuda_stream_wait_event(st, ev[0])
-        rq.run_streams(exs, which)
-        for st, e in zip(streams[1:], join[1:]):
-            L.disc_cuda_event_record(e, st)
-            L.disc_cuda_stream_wait_event(stream, e)
-
-    for _ in range(args.warmup):
-        L.disc_cuda_event_record(ev[0], stream)
-        one_pass()
-        L.disc_cuda_stream_synchronize(stream)
-    D.api._cuda(L.disc_cuda_device_synchronize())
-    step_bytes = sum(e.algorithmic_bytes() for e in exs)  # executors' own count for the last pass (this rank)
-    if step_bytes != my_bytes:
-        log(f"warning: executor bytes {step_bytes} != planned {my_bytes}")
-    total_bytes = allreduce(dist, local, step_bytes, "sum")
-
-    # ---- timed region: K steps, device time per step (flush untimed) ----
-    launches0 = D.kernel_launches()
-    step_ms = []
-    step_ev = []
-    for _ in range(2 * args.steps):
-        e = C.c_void_p()
-        D.api._cuda(L.disc_cuda_event_create(C.byref(e)))
-        step_ev.append(e)
-    barrier(dist, local)
-    wall0 = time.perf_counter()
-    with ClockSampler(local) as clk:
-        # K steps issued back to back (the host prepares step i+1 while the device runs
-        # step i); each step's device time is its own event pair, the L2 flush before it
-        # is outside the pair.
-        for i in range(args.steps):
-            L.disc_cuda_flush_l2(flush, flush_bytes, stream)
-            L.disc_cuda_event_record(step_ev[2 * i], stream)
-            if args.mode != "grouped":
-                L.disc_cuda_event_record(ev[0], stream)  # the interleaved streams wait on it
-            one_pass()
-            L.disc_cuda_event_record(step_ev[2 * i + 1], stream)
-        L.disc_cuda_stream_synchronize(stream)
-        for i in range(args.steps):
-            ms = C.c_float()
-            L.disc_cuda_event_elapsed_ms(step_ev[2 * i], step_ev[2 * i + 1], C.byref(ms))
-            step_ms.append(ms.value)
-    wall = time.perf_counter() - wall0
-    flushes = args.steps
-    gpu_launches = D.kernel_launches() - launches0 - flushes
-    barrier(dist, local)
-    total_ms = allreduce(dist, local, sum(step_ms), "max")
-    ms_per_step = total_ms / args.steps
-    value = total_bytes / (ms_per_step / 1e3) / 1e9
-    compile_count = compiler.stats()["compile_count"]
-
-    # ---- per-kernel device time (untimed pass): the pass is queued behind a spin
-    # kernel so per-launch events see device execution, not host submission gaps ----
-    records = []
-    ex.set_timing(True)
-    for _ in range(2):
-        D.lib().disc_cuda_flush_l2(flush, flush_bytes, stream)
-        D.lib().disc_cuda_spin(50000, stream)
-        if args.mode == "grouped":
-            rq.run_grouped(ex)  # one record per grouped launch
-        else:
-            rq.run(ex)
-        D.lib().disc_cuda_stream_synchronize(stream)
-        records.extend(ex.launch_records())
-    ex.set_timing(False)
-    device_ms = sum(r["ms"] for r in records) / 2
-
-    # ---- roofline: dominant kernel ----
-    peak, peak_kind = peaks()
-    by_kernel = {}
-    for r in records:
-        k = (r["kernel"], r["schedule"])
-        b = by_kernel.setdefault(k, [0, 0.0, 0])
-        b[0] += r["bytes"]
-        b[1] += r["ms"]
-        b[2] += 1
-    (dk, dsched), (dbytes, dms, dn) = max(by_kernel.items(), key=lambda kv: kv[1][1])
-    achieved = dbytes / (dms / 1e3) / 1e9 if dms > 0 else 0.0
-    kernel_ms_total = sum(v[1] for v in by_kernel.values())
-    breakdown = {f"k{k}:{s}": {"GB/s": round(b / (ms / 1e3) / 1e9, 1) if ms else None,
-                              "share": round(ms / kernel_ms_total, 3) if kernel_ms_total else None,
-                              "launches_per_step": n // 2}
-                 for (k, s), (b, ms, n) in sorted(by_kernel.items())}
-    if len(breakdown) > 12:  # stream: many artifacts; keep the 12 largest shares
-        breakdown = dict(sorted(breakdown.items(), key=lambda kv: -(kv[1]["share"] or 0))[:12])
-    # large-shape class (the >=70% target applies to large shapes)
-    big = [r for r in records if r["bytes"] >= (64 << 20)]
-    big_gbs = sum(r["bytes"] for r in big) / (sum(r["ms"] for r in big) / 1e3) / 1e9 if big else None
-
-    # ---- e2e through the public API with host buffers ----
-    e2e = None
-    if not args.no_e2e:
-        e2e = measure_e2e(D, graphs, plans, my_reqs, [costs[i] for i in mine], local, stream, pipes=args.e2e_pipes,
-                          grouped=args.mode == "grouped", chunk_bytes=args.e2e_chunk_mb << 20)
-        if e2e is not None and dist is not None:
-            e2e["value"] = round(allreduce(dist, local, e2e["bytes"], "sum") /
-                                 allreduce(dist, local, e2e["seconds"], "max") / 1e9, 2)
-    clocks = clk.summary()
-
-    out = None
-    if rank == 0:
-        cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline(graphs, reqs, costs)
-        out = {
-            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (uniform [0.25, 2) f32, device-generated)",
-            "config": {"workload": wname, "distinct_shapes": len(set((k, tuple(sorted(s.items()))) for k, s in reqs)),
-                       "requests_per_step": len(reqs), "graphs": len(graphs), "bytes_per_step": int(total_bytes),
-                       "l2": "flushed before each step (4x L2 write)",
-                       "parallelism": f"request-sharded x{world} (LPT on algorithmic bytes, no collectives)",
-                       "schedule": args.schedule, "pdl": args.pdl, "mode": args.mode,
-                       "host_threads": args.host_threads if args.mode == "grouped" else 1,
-                       "streams_per_gpu": len(exs),
-                       "stream_policy": args.stream_policy if len(exs) > 1 else None},
-            "frac_of_hbm_peak": round(value / world / peak, 4),
-            "recompiles": compile_count - len(graphs),
-            "compile_count": compile_count,
-            "large_shape_GBps": round(big_gbs, 1) if big_gbs else None,
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dsched),
-                         "kernel": f"artifact {dk} ({dsched})", "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs",
-                         "bytes_per_launch": dbytes // max(dn, 1), "mean_launch_ms": round(dms / max(dn, 1), 5)},
-            "kernel_breakdown": breakdown,
-            "device_ms_per_step": round(device_ms, 4),
-            "host_bound_frac": round(max(0.0, 1 - device_ms / ms_per_step), 3),
-            "cpu_baseline": cpu,
-            "e2e": {k: v for k, v in e2e.items() if k not in ("bytes", "seconds")} if e2e else None,
-            "gpu_launches": gpu_launches,
-            "clocks": clocks,
-            "wall_s_timed": round(wall, 3),
-        }
-        print(json.dumps(out))
-    if dist is not None:
-        dist.destroy_process_group()
+    batch.run(B.ex, on_chunk=on_chunk)
+    out = checker.finish()
+    out["mode"] = mode
+    out["step_requests"] = len(reqs)
+    return out
 
 
-def measure_e2e(D, graphs, plans, reqs, costs, device, stream, max_input_bytes=8 << 30, pipes=3, grouped=True,
-                chunk_bytes=1 << 30):
-    """Public API, host buffers: every request's inputs go H2D from pinned memory inside
-    disc_executor_run(inputs_on_host=1), its outputs D2H into pinned memory
-    (disc_executor_copy_output, async); wall time of one pass.  Requests alternate over
-    `pipes` executors (own stream + allocator each), so one request's D2H overlaps the
-    next one's H2D and compute (PCIe is full duplex).  Requests up to max_input_bytes of
-    pinned input (the whole C2 sweep fits)."""
-    L = D.lib()
+# ---------------------------------------------------------------------------
+# e2e: public C ABI with host buffers
+
+def measure_e2e(B, wl, reqs, costs, budget_bytes, pipes=3, chunk_bytes=256 << 20):
+    """disc_executor_run_grouped(inputs_on_host=1) over a stratified sample of the step
+    (pinned host inputs, ~budget_bytes of input), outputs D2H into pinned host memory with
+    disc_executor_copy_request_output; chunks alternate over `pipes` executors/streams so
+    one chunk's H2D overlaps another's kernels and D2H.  Wall time of one pass."""
+    D, L = B.D, B.L
+    g = wl.graphs
+    in_bytes = [sum(4 * int(np.prod(input_shape(i, s))) for i in g[k]["inputs"]) for k, s in reqs]
+    pick = stratified(reqs, in_bytes, budget_bytes, seed=1)
+    sub = [reqs[i] for i in pick]
+    scost = [costs[i] for i in pick]
+    B.plans_for(sub)
     exs, streams = [], []
     for _ in range(pipes):
         st = C.c_void_p()
         D.api._cuda(L.disc_cuda_stream_create(C.byref(st)))
         streams.append(st)
-        exs.append(D.Executor(device, st.value))
+        e = D.Executor(B.local, st.value)
+        e.set_host_threads(max(1, B.args.host_threads // 2))
+        exs.append(e)
     pinned, work = [], []
-    h2d = d2h = in_bytes = nbytes = 0
     rng = np.random.default_rng(1)
-    for (kind, syms), cost in zip(reqs, costs):
-        g = graphs[kind]
+    h2d = 0
+    for kind, syms in sub:
         ptrs, dims = [], []
-        size = sum(4 * int(np.prod(input_shape(i, syms))) for i in g["inputs"])
-        if in_bytes + size > max_input_bytes:
-            break
-        in_bytes += size
-        for i in g["inputs"]:
+        for i in g[kind]["inputs"]:
             shape = input_shape(i, syms)
             n = int(np.prod(shape))
             p = C.c_void_p()
@@ -665,13 +705,31 @@ def measure_e2e(D, graphs, plans, reqs, costs, device, stream, max_input_bytes=8
             ptrs.append(p.value)
             dims.append(np.array(shape, dtype=np.int64))
             h2d += 4 * n
-        names = [i["id"] for i in g["inputs"]]
-        work.append((plans[kind], (C.c_char_p * len(names))(*[s.encode() for s in names]),
-                     (C.c_void_p * len(ptrs))(*ptrs), dims, (C.c_void_p * len(dims))(*[d.ctypes.data for d in dims]),
-                     (C.c_int * len(dims))(*[d.size for d in dims])))
-        nbytes += cost
-    if not work:
-        return None
+        work.append((B.plans[kind], [i["id"] for i in g[kind]["inputs"]], ptrs, dims))
+    chunks, cur, acc = [], [], 0
+    for r, c in enumerate(scost):
+        cur.append(r)
+        acc += c
+        if acc >= chunk_bytes:
+            chunks.append(cur)
+            cur, acc = [], 0
+    if cur:
+        chunks.append(cur)
+    cargs, keep = [], []
+    for ch in chunks:
+        names, datas, dimsp, ranks, offs, hplans = [], [], [], [], [0], []
+        for r in ch:
+            plan, nm, ptrs, dims = work[r]
+            names += [s.encode() for s in nm]
+            datas += ptrs
+            dimsp += [d.ctypes.data for d in dims]
+            ranks += [d.size for d in dims]
+            offs.append(offs[-1] + len(nm))
+            hplans.append(plan._h)
+        t = max(len(names), 1)
+        a = (len(ch), (C.c_void_p * len(ch))(*hplans), (C.c_int * (len(ch) + 1))(*offs), (C.c_char_p * t)(*names),
+             (C.c_void_p * t)(*datas), (C.c_void_p * t)(*dimsp), (C.c_int * t)(*ranks))
+        cargs.append(a)
     outs = {}
 
     def out_buf(key, n):
@@ -681,36 +739,9 @@ def measure_e2e(D, graphs, plans, reqs, costs, device, stream, max_input_bytes=8
             outs[key] = p
         return outs[key]
 
-    # grouped: consecutive requests in chunks of ~chunk_bytes of boundary traffic, one
-    # disc_executor_run_grouped(inputs_on_host=1) call per chunk, chunks alternating over
-    # the pipes (chunk c's H2D overlaps chunk c-1's kernels and chunk c-2's D2H)
-    chunks, cur, acc = [], [], 0
-    for r, cost in enumerate(costs[:len(work)]):
-        cur.append(r)
-        acc += cost
-        if acc >= chunk_bytes:
-            chunks.append(cur)
-            cur, acc = [], 0
-    if cur:
-        chunks.append(cur)
-    cargs = []
-    for ch in chunks:
-        names, datas, dimsp, ranks, offs, hplans = [], [], [], [], [0], []
-        for r in ch:
-            plan, c_names, data, dims, c_dims, c_ranks = work[r]
-            n = len(dims)
-            names += [c_names[i] for i in range(n)]
-            datas += [data[i] for i in range(n)]
-            dimsp += [c_dims[i] for i in range(n)]
-            ranks += [c_ranks[i] for i in range(n)]
-            offs.append(offs[-1] + n)
-            hplans.append(plan._h)
-        t = max(len(names), 1)
-        cargs.append((len(ch), (C.c_void_p * len(ch))(*hplans), (C.c_int * (len(ch) + 1))(*offs),
-                      (C.c_char_p * t)(*names), (C.c_void_p * t)(*datas), (C.c_void_p * t)(*dimsp),
-                      (C.c_int * t)(*ranks)))
+    d2h = 0
 
-    def one_pass_grouped():
+    def one_pass():
         nonlocal d2h
         d2h = 0
         for c, (ch, a) in enumerate(zip(chunks, cargs)):
@@ -725,42 +756,255 @@ def measure_e2e(D, graphs, plans, reqs, costs, device, stream, max_input_bytes=8
         for ex in exs:
             ex.synchronize()
 
-    def one_pass():
-        nonlocal d2h
-        if grouped:
-            return one_pass_grouped()
-        d2h = 0
-        for r, (plan, c_names, data, dims, c_dims, c_ranks) in enumerate(work):
-            ex = exs[r % pipes]
-            D.api._check(L.disc_executor_run(ex._h, plan._h, len(dims), c_names, data, c_dims, c_ranks, 1))
-            for o, (_, odims) in enumerate(ex.output_views()):
-                n = int(np.prod(odims)) if odims else 1
-                key = (r, o)
-                if key not in outs:
-                    p = C.c_void_p()
-                    D.api._cuda(L.disc_cuda_host_alloc(max(4 * n, 16), C.byref(p)))
-                    outs[key] = p
-                if n:
-                    D.api._check(L.disc_executor_copy_output(ex._h, o, outs[key], 2))
-                d2h += 4 * n
-        for ex in exs:
-            ex.synchronize()
-
-    one_pass()  # warm allocators + staging
+    one_pass()  # warm allocators, staging and recipes
     t0 = time.perf_counter()
     one_pass()
     dt = time.perf_counter() - t0
     for p in pinned + list(outs.values()):
         L.disc_cuda_host_free(p)
     del exs
-    path = (f"disc_executor_run_grouped(inputs_on_host=1) per chunk of requests ({len(chunks)} chunks of "
-            f"~{chunk_bytes >> 20} MB) + disc_executor_copy_request_output(pinned host, async), chunks alternating "
-            f"over {pipes} executors/streams") if grouped else \
-        (f"disc_executor_run(inputs_on_host=1) + disc_executor_copy_output(pinned host, async) per "
-         f"request, requests alternating over {pipes} executors/streams")
+    nbytes = sum(scost)
     return {"value": round(nbytes / dt / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 3), "requests": len(work),
-            "path": path, "bytes": nbytes, "seconds": dt}
+            "d2h_bytes_per_step": d2h, "ms_per_step": round(dt * 1e3, 3), "requests": len(sub),
+            "sample": f"{len(sub)} of {len(reqs)} requests of a timed step (stratified by pattern and size)",
+            "path": f"disc_executor_run_grouped(inputs_on_host=1) per chunk (~{chunk_bytes >> 20} MB of algorithmic "
+                    f"bytes, {len(chunks)} chunks) + disc_executor_copy_request_output(pinned host, async), chunks "
+                    f"alternating over {pipes} executors/streams",
+            "bytes": nbytes, "seconds": dt}
+
+
+# ---------------------------------------------------------------------------
+
+def pattern_of(kind):
+    return kind if kind in MAIN_KINDS else "fixtures"
+
+
+def analyse(B, wl, reqs, costs, peak):
+    """Untimed analysis of one step: per-pattern device GB/s (all and large requests),
+    per-kernel records keyed (pattern, artifact, schedule), the dominant kernel, and the
+    device-only time of the whole step."""
+    pats = {}
+    for i, (k, _) in enumerate(reqs):
+        pats.setdefault(pattern_of(k), []).append(i)
+    per_pattern, records = {}, {}
+    for p, idx in sorted(pats.items()):
+        sub, sc = [reqs[i] for i in idx], [costs[i] for i in idx]
+        ms = B.timed_pass(B.batch(sub, sc))
+        b = sum(sc)
+        ent = {"requests": len(sub), "bytes": b, "GB/s": round(b / ms / 1e6, 1) if ms > 0 else None}
+        ent["frac_of_peak"] = round(ent["GB/s"] / peak, 4) if ent["GB/s"] else None
+        big = [i for i in idx if costs[i] >= LARGE]
+        if big:
+            lb = sum(costs[i] for i in big)
+            lms = B.timed_pass(B.batch([reqs[i] for i in big], [costs[i] for i in big]))
+            ent["large"] = {"requests": len(big), "bytes": lb, "GB/s": round(lb / lms / 1e6, 1) if lms > 0 else None}
+            ent["large"]["frac_of_peak"] = round(ent["large"]["GB/s"] / peak, 4) if ent["large"]["GB/s"] else None
+            ent["large_byte_share"] = round(lb / b, 4) if b else None
+        per_pattern[p] = ent
+        for r in B.record_pass(B.batch(sub, sc)):
+            key = f"{p}:k{r['kernel']}:{r['schedule']}"
+            a = records.setdefault(key, [0, 0.0, 0])
+            a[0] += r["bytes"]
+            a[1] += r["ms"]
+            a[2] += 1
+    full = B.record_pass(B.batch(reqs, costs))
+    device_ms = sum(r["ms"] for r in full)
+    return per_pattern, records, device_ms, len(full)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="disc", choices=["disc", "reference"])
+    ap.add_argument("--workload", default="sweep")
+    ap.add_argument("--requests", type=int, default=10000, help="sweep: distinct requests per step")
+    ap.add_argument("--verify", default="sample", choices=["off", "sample", "full"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-analysis", action="store_true")
+    ap.add_argument("--schedule", default="auto")
+    ap.add_argument("--chunk-gb", type=float, default=32.0, help="algorithmic bytes per grouped call")
+    ap.add_argument("--arena-gb", type=float, default=48.0)
+    ap.add_argument("--cache-gb", type=float, default=8.0, help="executor allocator cache budget")
+    ap.add_argument("--e2e-gb", type=float, default=4.0, help="e2e: pinned host input bytes")
+    ap.add_argument("--ref-step-s", type=float, default=4.0, help="reference arm: seconds of CPU work per step")
+    ap.add_argument("--host-threads", type=int, default=0,
+                    help="host threads per rank for the runtime flows (0: cores / ranks, max 32)")
+    ap.add_argument("--pdl", type=int, default=1, choices=[0, 1, 2])
+    ap.add_argument("--host-only", action="store_true",
+                    help="capture mode (no device): time the host side (runtime flows + flush) of every step")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world, rank, local, dist = dist_setup(args)
+    if args.host_threads <= 0:
+        args.host_threads = max(1, min(32, (os.cpu_count() or 1) // max(1, world)))
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    import paper_2103_05288_b200 as D
+    D.lib()
+    D.set_pdl(args.pdl)
+    if args.host_only:
+        D.lib().disc_cuda_set_capture(2)
+    if args.workload == "sweep":
+        wl = make_workload("sweep", rank, args.requests)
+        shard = None
+    else:
+        from paper_2103_05288_b200.dispatch import shard as lpt
+        wl = make_workload(args.workload, 0)
+        reqs_all = list(wl.requests(0))
+        for r in range(1, world):  # N replicas of the sweep, LPT-sharded below
+            w2 = make_workload(args.workload, r)
+            wl.graphs.update(w2.graphs)
+            reqs_all += w2.requests(0)
+        shard = (lpt, reqs_all)
+    B = Bench(D, args, local, wl)
+    if shard is not None:
+        lpt, reqs_all = shard
+        B.plans_for(reqs_all)
+        costs_all = B.costs(reqs_all)
+        mine = lpt(costs_all, world)[rank]
+        fixed = [reqs_all[i] for i in mine]
+        wl = Workload(wl.name, wl.desc, wl.graphs, fixed=fixed)
+        B.wl = wl
+
+    # all steps' batches are built before the timed region (the request list is the input)
+    t0 = time.perf_counter()
+    batches = []
+    for i in range(args.warmup + args.steps):
+        reqs = wl.requests(i)
+        batches.append(B.batch(reqs))
+        if not wl.fresh:
+            batches += [batches[0]] * (args.warmup + args.steps - 1)
+            break
+    log(f"[bench] {len(batches)} step batches built in {time.perf_counter() - t0:.1f}s "
+        f"({len(wl.requests(0))} requests/step, {batches[0].bytes / 1e9:.1f} GB/step, {len(batches[0].chunks)} chunks)")
+    L = B.L
+    if args.host_only:
+        for i, b in enumerate(batches):
+            t1 = time.perf_counter()
+            b.run(B.ex)
+            log(f"[bench host-only] step {i}: {len(b.reqs)} requests, {len(b.chunks)} chunks, host "
+                f"{(time.perf_counter() - t1) * 1e3:.1f} ms ({(time.perf_counter() - t1) / max(1, len(b.reqs)) * 1e6:.2f} "
+                f"us/request), {b.bytes / 1e9:.1f} GB")
+        return
+    for i in range(args.warmup):
+        batches[i].run(B.ex)
+        L.disc_cuda_stream_synchronize(B.stream)
+    D.api._cuda(L.disc_cuda_device_synchronize())
+
+    # ---- timed region: K steps issued back to back; per step an event pair (the L2 flush
+    # before it outside the pair); host flow of step i+1 overlaps device work of step i ----
+    ev = [B.event() for _ in range(2 * args.steps)]
+    launches0 = D.kernel_launches()
+    barrier(dist, local)
+    wall0 = time.perf_counter()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            L.disc_cuda_flush_l2(B.flush, B.flush_bytes, B.stream)
+            L.disc_cuda_event_record(ev[2 * i], B.stream)
+            batches[args.warmup + i].run(B.ex)
+            L.disc_cuda_event_record(ev[2 * i + 1], B.stream)
+        L.disc_cuda_stream_synchronize(B.stream)
+    wall = time.perf_counter() - wall0
+    step_ms = []
+    for i in range(args.steps):
+        ms = C.c_float()
+        L.disc_cuda_event_elapsed_ms(ev[2 * i], ev[2 * i + 1], C.byref(ms))
+        step_ms.append(ms.value)
+    gpu_launches = D.kernel_launches() - launches0 - args.steps
+    my_bytes = sum(batches[args.warmup + i].bytes for i in range(args.steps))
+    barrier(dist, local)
+    total_ms = allreduce(dist, local, sum(step_ms), "max")
+    total_bytes = allreduce(dist, local, my_bytes, "sum")
+    ms_per_step = total_ms / args.steps
+    value = total_bytes / (total_ms / 1e3) / 1e9
+    compile_count = B.compiler.stats()["compile_count"]
+    distinct = len({(k, tuple(sorted(s.items()))) for i in range(args.warmup + args.steps) for k, s in wl.requests(i)})
+    peak, peak_src = peaks()
+    clocks = clk.summary()
+
+    # ---- untimed: analysis of the first timed step ----
+    reqs0 = wl.requests(args.warmup)
+    costs0 = batches[args.warmup].costs
+    analysis = None
+    if not args.no_analysis:
+        per_pattern, records, device_ms, n_group_launches = analyse(B, wl, reqs0, costs0, peak)
+        (dk, (db, dms, dn)) = max(records.items(), key=lambda kv: kv[1][1])
+        achieved = db / (dms / 1e3) / 1e9 if dms > 0 else 0.0
+        traffic, tinfo = ncu_traffic(wl.name, dk)
+        tot_ms = sum(v[1] for v in records.values())
+        breakdown = {k: {"GB/s": round(b / (ms / 1e3) / 1e9, 1) if ms else None,
+                         "share": round(ms / tot_ms, 3) if tot_ms else None, "launches": n}
+                     for k, (b, ms, n) in sorted(records.items(), key=lambda kv: -kv[1][1])[:16]}
+        analysis = {
+            "per_pattern": per_pattern,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dk,
+                         "peak_source": peak_src, "bytes_per_launch": db // max(dn, 1),
+                         "mean_launch_ms": round(dms / max(dn, 1), 5),
+                         "traffic_source": (f"profiles/ncu_traffic.json[{wl.name}][{dk}]: ncu dram bytes of the same "
+                                            f"kernel, algorithmic {tinfo.get('alg_bytes_per_launch')} B/launch there")
+                         if tinfo else "no committed ncu capture for this (workload, kernel)"},
+            "kernel_breakdown": breakdown,
+            "device_ms_step": round(device_ms, 3),
+            "grouped_launches_step": n_group_launches,
+        }
+
+    out = None
+    ver = None
+    if args.verify != "off" and rank == 0:
+        from oracle import ref as _ref
+        if _ref.available():
+            ver = verify_pass(B, wl, batches[args.warmup], args.verify, threads=max(1, (os.cpu_count() or 2) - 1))
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(B, wl, reqs0, costs0, int(args.e2e_gb * (1 << 30)))
+        if dist is not None:
+            e2e["value"] = round(allreduce(dist, local, e2e["bytes"], "sum") /
+                                 allreduce(dist, local, e2e["seconds"], "max") / 1e9, 2)
+    if rank == 0:
+        cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline(wl, reqs0)
+        big = {p: e.get("large", {}).get("frac_of_peak") for p, e in (analysis or {}).get("per_pattern", {}).items()
+               if p in MAIN_KINDS}
+        out = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (uniform [0.25, 2) f32 device arena; inputs resident in HBM)",
+            "config": {"workload": wl.desc, "workload_name": wl.name,
+                       "distinct_shapes": distinct, "requests_per_step": len(reqs0),
+                       "fresh_shapes_every_step": wl.fresh, "graphs": len(wl.graphs),
+                       "bytes_per_step": int(total_bytes / args.steps),
+                       "l2": "flushed before each step (4x L2 write); inputs >> L2",
+                       "parallelism": f"request-sharded x{world} (no collectives)",
+                       "chunk_gb": args.chunk_gb, "host_threads": args.host_threads, "pdl": args.pdl,
+                       "schedule": args.schedule},
+            "frac_of_hbm_peak": round(value / world / peak, 4),
+            "compile_count": compile_count, "recompiles": compile_count - len(wl.graphs),
+            "large_shape_frac_of_peak": big,
+            "roofline": (analysis or {}).get("roofline"),
+            "per_pattern": (analysis or {}).get("per_pattern"),
+            "kernel_breakdown": (analysis or {}).get("kernel_breakdown"),
+            "device_ms_per_step": (analysis or {}).get("device_ms_step"),
+            "host_bound_frac": round(max(0.0, 1 - analysis["device_ms_step"] / step_ms[0]), 3) if analysis else None,
+            "cpu_baseline": cpu,
+            "e2e": {k: v for k, v in e2e.items() if k not in ("bytes", "seconds")} if e2e else None,
+            "verify": ver,
+            "gpu_launches": gpu_launches,
+            "clocks": clocks,
+            "host": host_info(),
+            "wall_s_timed": round(wall, 3),
+        }
+        print(json.dumps(out))
+    if dist is not None:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

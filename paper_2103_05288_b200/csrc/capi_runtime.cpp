@@ -340,7 +340,7 @@ int disc_plan_group_dry_run(int n_requests, const disc_plan* plans, const int* i
       ps[r] = plans[r]->plan.get();
       serials[r] = plans[r]->serial;
     }
-    disc_cuda_set_capture(1);  // drop the programs recorded so far: only the flush plan
+    disc_cuda_set_capture(2);  // launches unrecorded (mode 2): the output is only the flush plan
     ex.run_grouped_batch(n_requests, ps.data(), serials.data(), input_offsets, names, data.data(), dims, ranks, false);
     disc_cuda_capture_records(json);
   });

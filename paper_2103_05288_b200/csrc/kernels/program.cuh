@@ -47,16 +47,28 @@ __device__ __forceinline__ float bin1(float a, float b) {
 #ifndef DISC_FAST_TANH
 #define DISC_FAST_TANH 1
 #endif
-// tanh(x) = sign(x) (1 - 2 / (2^(2 log2(e) |x|) + 1)) with the MUFU ex2/rcp approximations:
-// 7 instructions instead of libdevice's two-branch ~18.  Absolute error <= 3e-7 over all
-// x (ex2 2^-22.5 relative, rcp 2^-23, final rounding ulp(1)/2; the exponent product's
-// rounding is damped by 2t/(1+t)^2): within the 1e-6 floored rel_err the unfused tests
-// hold exp/tanh to and far inside the north-star 1e-5 (glibc tanhf is the reference).
+// tanh in two ranges, both <= 1 ulp-ish relative (north star: 1e-5 relative, not floored):
+//  * |x| < 0.5: odd minimax polynomial x + x^3 P(x^2), P of degree 3 on the FMA pipe
+//    (<= 0.84 ulp over every f32 in [2^-12, 0.5], coefficients fitted by Lawson-weighted
+//    least squares on the relative error by tools/fit_tanh.py);
+//  * |x| >= 0.5: sign(x) (1 - 2 / (2^(2 log2(e) |x|) + 1)) on the MUFU ex2/rcp units: absolute
+//    error <= 3e-7 and tanh >= 0.46, so relative error <= 7e-7.  (The exp form alone was
+//    only absolute-accurate: ~1e-3 relative just above 2^-12.)
+//  * |x| < 2^-12: tanh(x) rounds to x; returned exactly, sign included.
+// The two branches cost about the same (7-8 instructions); libdevice tanhf is ~18.
 #ifndef DISC_TANH_NEWTON
 #define DISC_TANH_NEWTON 0  // A/B on B200: -6% on the tanh column reduce, -1..3% elsewhere
 #endif
 __device__ __forceinline__ float tanh_fast(float x) {
   const float ax = fabsf(x);
+  if (ax < 0.5f) {
+    const float s = __fmul_rn(x, x);
+    float p = __fmaf_rn(0.01724148355424404f, s, -0.05304549261927605f);
+    p = __fmaf_rn(p, s, 0.13325878977775574f);
+    p = __fmaf_rn(p, s, -0.333331435918808f);
+    const float y = __fmaf_rn(__fmul_rn(s, x), p, x);
+    return ax < 2.44140625e-4f ? x : y;
+  }
   float t, r;
 #if DISC_TANH_NEWTON
   // one MUFU op (ex2) instead of two: 1 / (t + 1) by Newton iterations on the FMA pipe from
@@ -73,9 +85,7 @@ __device__ __forceinline__ float tanh_fast(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(p));
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__fadd_rn(t, 1.0f)));  // t = inf -> r = 0 -> 1
 #endif
-  const float y = __fmaf_rn(-2.0f, r, 1.0f);
-  // |x| < 2^-12: tanh(x) = x (1 - x^2/3 ...) rounds to x; keeps tiny arguments exact and signed
-  return ax < 2.44140625e-4f ? x : copysignf(y, x);
+  return copysignf(__fmaf_rn(-2.0f, r, 1.0f), x);  // NaN: ax < 0.5 false -> NaN propagates
 }
 
 template <int OP>

@@ -528,7 +528,24 @@ int disc_cuda_get_device(int* device) {
 }
 int disc_cuda_set_device(int device) {
   if (g_capture) return 0;
-  return check(cudaSetDevice(device), "cudaSetDevice");
+  if (int rc = check(cudaSetDevice(device), "cudaSetDevice")) return rc;
+  // The stream-ordered pool keeps freed memory (release threshold = max) instead of
+  // returning it to the driver at every synchronisation: a stream of fresh shapes misses
+  // the exact-size cache on every allocation, and cudaMallocAsync from a warm pool is
+  // ~1 us instead of a driver mapping call.
+  static std::mutex mu;
+  static std::vector<char> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (device >= 0 && static_cast<size_t>(device) >= done.size()) done.resize(device + 1, 0);
+  if (device >= 0 && !done[device]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = ~uint64_t{0};
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[device] = 1;
+  }
+  return 0;
 }
 
 int disc_cuda_device_info(int device, int* sm_count, int64_t* l2_bytes, int64_t* hbm_bytes) {
@@ -547,17 +564,25 @@ int disc_cuda_device_info(int device, int* sm_count, int64_t* l2_bytes, int64_t*
 }
 
 int disc_cuda_stream_create(void** stream) {
+  if (g_capture) {  // host-only runs: a distinct fake handle
+    *stream = reinterpret_cast<void*>(g_fake_next.fetch_add(4096));
+    return 0;
+  }
   cudaStream_t s;
   int rc = check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
   *stream = s;
   return rc;
 }
-int disc_cuda_stream_destroy(void* stream) { return check(cudaStreamDestroy(S(stream)), "cudaStreamDestroy"); }
+int disc_cuda_stream_destroy(void* stream) {
+  if (g_capture) return 0;
+  return check(cudaStreamDestroy(S(stream)), "cudaStreamDestroy"); }
 int disc_cuda_stream_synchronize(void* stream) {
   if (g_capture) return 0;
   return check(cudaStreamSynchronize(S(stream)), "cudaStreamSynchronize");
 }
-int disc_cuda_device_synchronize(void) { return check(cudaDeviceSynchronize(), "cudaDeviceSynchronize"); }
+int disc_cuda_device_synchronize(void) {
+  if (g_capture) return 0;
+  return check(cudaDeviceSynchronize(), "cudaDeviceSynchronize"); }
 
 int disc_cuda_malloc(size_t bytes, void* stream, void** dptr) {
   if (g_capture) {
@@ -574,8 +599,20 @@ int disc_cuda_free(void* dptr, void* stream) {
   }
   return check(cudaFreeAsync(dptr, S(stream)), "cudaFreeAsync");
 }
-int disc_cuda_host_alloc(size_t bytes, void** hptr) { return check(cudaMallocHost(hptr, bytes ? bytes : 16), "cudaMallocHost"); }
-int disc_cuda_host_free(void* hptr) { return check(cudaFreeHost(hptr), "cudaFreeHost"); }
+int disc_cuda_host_alloc(size_t bytes, void** hptr) {
+  if (g_capture) {  // host-only runs: pageable memory stands in for pinned
+    *hptr = std::malloc(bytes ? bytes : 16);
+    return *hptr ? 0 : 4;
+  }
+  return check(cudaMallocHost(hptr, bytes ? bytes : 16), "cudaMallocHost");
+}
+int disc_cuda_host_free(void* hptr) {
+  if (g_capture) {
+    std::free(hptr);
+    return 0;
+  }
+  return check(cudaFreeHost(hptr), "cudaFreeHost");
+}
 
 int disc_cuda_memcpy(void* dst, const void* src, size_t bytes, int kind, void* stream) {
   if (!bytes) return 0;
@@ -619,9 +656,14 @@ int disc_cuda_stream_wait_event(void* stream, void* ev) {
   return check(cudaStreamWaitEvent(S(stream), static_cast<cudaEvent_t>(ev), 0), "cudaStreamWaitEvent");
 }
 int disc_cuda_event_synchronize(void* ev) {
+  if (g_capture) return 0;
   return check(cudaEventSynchronize(static_cast<cudaEvent_t>(ev)), "cudaEventSynchronize");
 }
 int disc_cuda_event_elapsed_ms(void* a, void* b, float* ms) {
+  if (g_capture) {
+    *ms = 0.f;
+    return 0;
+  }
   return check(cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(a), static_cast<cudaEvent_t>(b)), "cudaEventElapsedTime");
 }
 
@@ -705,12 +747,15 @@ int disc_cuda_gemm(int64_t m, int64_t k, int64_t n, const float* a, const float*
   return counted(disc_launch::gemm(m, k, n, a, b, c, S(stream)), "launch gemm");
 }
 int disc_cuda_fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, void* stream) {
+  if (g_capture) return 0;
   return counted(disc_launch::fill_uniform(dst, n, seed, lo, hi, S(stream)), "launch fill");
 }
 int disc_cuda_flush_l2(void* scratch, size_t bytes, void* stream) {
+  if (g_capture) return 0;
   return counted(disc_launch::flush(scratch, bytes, S(stream)), "launch flush");
 }
 int disc_cuda_spin(uint64_t microseconds, void* stream) {
+  if (g_capture) return 0;
   return counted(disc_launch::spin(microseconds * 1000ull, S(stream)), "launch spin");
 }
 int64_t disc_cuda_kernel_launches(void) { return g_launches.load(); }

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <unordered_set>
 #include <tuple>
 #include <unordered_map>
 
@@ -1535,7 +1536,20 @@ struct LaunchCache {
   };
   std::unordered_map<uint64_t, std::vector<Entry>> map;
   size_t entries = 0;
+  // Keys seen once (hash only): a recipe is recorded on a key's SECOND launch, so a stream
+  // of fresh shapes lowers each launch once, directly, instead of recording a recipe that
+  // is never replayed.  Both tables are bounded (cleared when full: a new generation).
+  std::unordered_set<uint64_t> seen_once;
+  static constexpr size_t kMaxEntries = 16384, kMaxSeen = 1 << 16;
 };
+
+namespace {
+// True on the first sighting of key hash h (a hash collision only costs one recording).
+bool it_seen_first(LaunchCache* c, uint64_t h) {
+  if (c->seen_once.size() >= LaunchCache::kMaxSeen) c->seen_once.clear();
+  return c->seen_once.insert(h).second;
+}
+}  // namespace
 
 LaunchCache* new_launch_cache() { return new LaunchCache(); }
 void free_launch_cache(LaunchCache* c) { delete c; }
@@ -1573,6 +1587,8 @@ LaunchReport launch_kernel(const KernelArtifact& art, const VersionArtifact& ver
           return e.recipe->rep;
         }
   }
+  bool record = cacheable;
+  if (record && it_seen_first(cache, h)) record = false;  // first sighting: lower directly
 
   std::vector<std::vector<int64_t>> ext_dims;
   for (const auto& e : ext) ext_dims.push_back(e.dims);
@@ -1595,7 +1611,7 @@ LaunchReport launch_kernel(const KernelArtifact& art, const VersionArtifact& ver
     bool done = false;
     if (pref != SchedulePref::kMaterialize) {
       try {
-        if (cacheable) {
+        if (record) {
           // Record with tagged pointers, cache, then replay with the real ones.
           std::vector<DevTensor> text(ext.size());
           for (size_t i = 0; i < ext.size(); ++i) {
@@ -1616,10 +1632,12 @@ LaunchReport launch_kernel(const KernelArtifact& art, const VersionArtifact& ver
           RecordingIssuer rec(*recipe);
           recipe->rep = launch_fused(TB, touts, rec, pref);
           recipe->rep.algorithmic_bytes = algorithmic_bytes(art, ext, B.dims);
-          if (cache->entries < 65536) {
-            cache->map[h].push_back({key, recipe});
-            cache->entries++;
+          if (cache->entries >= LaunchCache::kMaxEntries) {
+            cache->map.clear();
+            cache->entries = 0;
           }
+          cache->map[h].push_back({key, recipe});
+          cache->entries++;
           replay(*recipe, ext, outs, scratch, stream);
           return recipe->rep;
         }
@@ -1628,7 +1646,11 @@ LaunchReport launch_kernel(const KernelArtifact& art, const VersionArtifact& ver
         done = true;
       } catch (const NotFusible& nf) {
         if (pref == SchedulePref::kFusedOnly) throw InternalError(std::string("not fusible: ") + nf.why);
-        if (cacheable && cache->entries < 65536) {
+        if (cacheable) {
+          if (cache->entries >= LaunchCache::kMaxEntries) {
+            cache->map.clear();
+            cache->entries = 0;
+          }
           cache->map[h].push_back({key, nullptr});
           cache->entries++;
         }

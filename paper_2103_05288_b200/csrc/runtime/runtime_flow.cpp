@@ -9,6 +9,9 @@
 #include <mutex>
 #include <numeric>
 #include <thread>
+
+#include <pthread.h>
+#include <sched.h>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -178,9 +181,31 @@ struct DeviceExecutor::Pool {
   uint64_t gen = 0;
   int pending = 0;
   bool stop = false;
+  std::vector<Clock::time_point> wake_at = std::vector<Clock::time_point>(64);
   Pool(int n, int device) {
+    // Workers are pinned one per CPU of the creating thread's affinity set (worker w on the
+    // (w+1)-th CPU; the caller keeps the first).  Unpinned, a wake-up of many short jobs
+    // lands the woken threads on the waker's CPU and they run one after another until the
+    // load balancer spreads them (measured: 7 x 4 ms jobs took 58 ms unpinned, 11 pinned).
+    // DISC_PIN_THREADS=0 disables; a rank's CPU slice is its process affinity mask.
+    std::vector<int> cpus;
+    static const bool pin = [] {
+      const char* e = std::getenv("DISC_PIN_THREADS");
+      return !e || std::atoi(e) != 0;
+    }();
+    cpu_set_t allowed;
+    CPU_ZERO(&allowed);
+    if (pin && sched_getaffinity(0, sizeof allowed, &allowed) == 0)
+      for (int c = 0; c < CPU_SETSIZE; ++c)
+        if (CPU_ISSET(c, &allowed)) cpus.push_back(c);
     for (int w = 0; w < n; ++w)
-      threads.emplace_back([this, w, device] {
+      threads.emplace_back([this, w, device, cpus] {
+        if (cpus.size() > 1) {
+          cpu_set_t one;
+          CPU_ZERO(&one);
+          CPU_SET(cpus[(w + 1) % cpus.size()], &one);
+          pthread_setaffinity_np(pthread_self(), sizeof one, &one);
+        }
         disc_cuda_set_device(device);
         uint64_t seen = 0;
         for (;;) {
@@ -192,6 +217,7 @@ struct DeviceExecutor::Pool {
             seen = gen;
             f = job;
           }
+          wake_at[w] = Clock::now();
           f(w);
           std::lock_guard<std::mutex> l(mu);
           if (--pending == 0) done.notify_all();
@@ -275,10 +301,15 @@ void DeviceExecutor::append_group_records() {
   }
 }
 
+static bool prof_host() {
+  static const bool on = std::getenv("DISC_HOST_PROFILE") != nullptr;
+  return on;
+}
+
 void DeviceExecutor::run_grouped_batch(int n, const CompiledPlan* const* plans, const uint64_t* serials,
                                        const int* offs, const char* const* names, const void* const* data,
                                        const int64_t* const* dims, const int* ranks, bool on_host) {
-  constexpr int kMinPerThread = 64;
+  constexpr int kMinPerThread = 8;
   // Phases: with enough requests, the largest eighth (by input size) is flushed first, so
   // the device starts on the long kernels while the host runs the other flows
   // (DISC_GROUP_PHASES=1: one flush).  Timing mode keeps one flush (per-launch events).
@@ -335,10 +366,13 @@ void DeviceExecutor::run_grouped_batch(int n, const CompiledPlan* const* plans, 
     for (int w = 0; w <= T; ++w) bounds[w] = static_cast<int>(int64_t{m} * w / T);
     std::vector<void*> handles(T, nullptr);
     std::vector<std::exception_ptr> perr(T);
+    std::vector<double> wt(T, 0.0), wl(T, 0.0), ws(T, 0.0);
+    const auto t_phase = Clock::now();
     if (ph > 0) begin_phase();
     if (T > 1) {
       pool_->start([&](int w) {
         if (w + 1 >= T) return;
+        const auto tl = Clock::now();
         DeviceExecutor& ex = *subs_[w];
         try {
           if (!sub_used[w]) {
@@ -349,8 +383,10 @@ void DeviceExecutor::run_grouped_batch(int n, const CompiledPlan* const* plans, 
           } else {
             ex.begin_phase();
           }
+          const auto tw = Clock::now();
           ex.run_requests(P.data() + bounds[w + 1], bounds[w + 2] - bounds[w + 1], plans, serials, offs, names, data,
                           dims, ranks, on_host);
+          wt[w + 1] = std::chrono::duration<double, std::milli>(Clock::now() - tw).count();
         } catch (...) {
           perr[w + 1] = std::current_exception();
         }
@@ -359,14 +395,31 @@ void DeviceExecutor::run_grouped_batch(int n, const CompiledPlan* const* plans, 
         } catch (...) {
           if (!perr[w + 1]) perr[w + 1] = std::current_exception();
         }
+        wl[w + 1] = std::chrono::duration<double, std::milli>(Clock::now() - tl).count();
+        ws[w + 1] = std::chrono::duration<double, std::milli>(tl - t_phase).count();
       });
     }
     try {  // this thread's range, concurrently with the workers
+      const auto tw = Clock::now();
       run_requests(P.data() + bounds[0], bounds[1] - bounds[0], plans, serials, offs, names, data, dims, ranks, on_host);
+      wt[0] = std::chrono::duration<double, std::milli>(Clock::now() - tw).count();
     } catch (...) {
       perr[0] = std::current_exception();
     }
     if (T > 1) pool_->wait();
+    if (prof_host()) {
+      std::fprintf(stderr, "[disc host]   phase %zu: %d requests on %d threads, flows %.3f ms wall; per thread:", ph, m, T,
+                   std::chrono::duration<double, std::milli>(Clock::now() - t_phase).count());
+      for (double x : wt) std::fprintf(stderr, " %.2f", x);
+      std::fprintf(stderr, "; worker lambda:");
+      for (double x : wl) std::fprintf(stderr, " %.2f", x);
+      std::fprintf(stderr, "; start offset:");
+      for (double x : ws) std::fprintf(stderr, " %.2f", x);
+      std::fprintf(stderr, "; wake offset:");
+      for (int w = 0; w + 1 < T; ++w)
+        std::fprintf(stderr, " %.2f", std::chrono::duration<double, std::milli>(pool_->wake_at[w] - t_phase).count());
+      std::fprintf(stderr, "\n");
+    }
     // merged flush of this phase: this thread's queue + the workers' detached ones
     grouped_ = false;
     const int src = issue_small_inputs();

@@ -214,3 +214,98 @@ def mixed_stream(n: int = 10000, seed: int = 20261017, max_bytes: int = 1 << 22,
             reqs.append((kind, syms))
             break
     return graphs, reqs
+
+
+def _logu(rng: random.Random, lo: int, hi: int) -> int:
+    """Integer log-uniform in [lo, hi] (every scale of the range equally likely)."""
+    if hi <= lo:
+        return lo
+    v = int(math.exp(rng.uniform(math.log(lo), math.log(hi + 1))))
+    return max(lo, min(hi, v))
+
+
+SWEEP_KINDS = ("softmax", "ln_gelu", "colreduce", "bert")
+
+
+def sweep_graphs(fixtures: Dict[str, tuple] = None) -> Dict[str, dict]:
+    graphs = {"softmax": softmax_graph_for(0), "ln_gelu": ln_gelu_graph(), "colreduce": colreduce_graph(),
+              "bert": bert_graph()}
+    for name, (g, _) in (fixtures or {}).items():
+        graphs[f"fx_{name}"] = g
+    return graphs
+
+
+def full_sweep(step: int, n: int = 10000, seed: int = 20261017, fixtures: Dict[str, tuple] = None,
+               seen: set = None, fixture_numel_cap: int = 1 << 22):
+    """The headline workload (BASELINE metric; SURVEY §8d C5 over the FULL C1-C4 ranges):
+    n distinct (graph, shape) requests for one step, kinds round-robin over C1-C4 plus the
+    reference fixtures, every dimension drawn log-uniformly over its whole configured range
+    (Python MT19937 seeded with seed + 7919 * step, so each step draws FRESH shapes):
+
+      C1 softmax    [B, S]: S in 1..4096, B in 1..2^26/S   (up to 256 MB per tensor)
+      C2 ln_gelu    [T, H]: T in 1..16384, H in {768, 1024, 4096}
+      C3 colreduce  [N, C]: C in 1..4096, N in 1..min(2^22, 2^26/C)
+      C4 bert       B in 1..32, S in 8..512 (variable-length batches): scores [12BS, S], [BS, 768/3072]
+      fixtures      every symbolic dim log-uniform (2% zero), inputs <= fixture_numel_cap elements
+
+    Shapes are distinct within the step (``seen``, optional, may be shared to make them
+    distinct over several steps -- that biases later steps towards large shapes, since the
+    small end of every range is exhausted first).  Returns (graphs, [(kind, syms)])."""
+    rng = random.Random(seed + 7919 * step)
+    graphs = sweep_graphs(fixtures)
+    ties = {}
+    for name, (g, bindings) in (fixtures or {}).items():
+        tie = {}
+        for b in bindings:
+            for x in b:
+                if x not in tie:
+                    tie[x] = next(y for y in b if all(bb.get(y) == bb.get(x) for bb in bindings))
+        ties[f"fx_{name}"] = tie
+    kinds = list(graphs)
+
+    def draw(kind):
+        if kind == "softmax":
+            s = _logu(rng, 1, 4096)
+            return {"S0": _logu(rng, 1, max(1, (1 << 26) // s)), "S1": s}
+        if kind == "ln_gelu":
+            return {"T": _logu(rng, 1, 16384), "H": rng.choice([768, 1024, 4096])}
+        if kind == "colreduce":
+            c = _logu(rng, 1, 4096)
+            return {"N": _logu(rng, 1, min(1 << 22, (1 << 26) // c)), "C": c}
+        if kind == "bert":
+            b, s = _logu(rng, 1, 32), _logu(rng, 8, 512)
+            return {"R": b * 12 * s, "S": s, "T": b * s, "H": 768, "F": 3072}
+        g = graphs[kind]
+        tie = ties.get(kind, {})
+        roots = sorted({tie.get(d, d) for i in g["inputs"] for d in i["shape"] if isinstance(d, str)})
+        hi = 4096 if len(roots) > 1 else max(1, fixture_numel_cap // 8)
+        syms = {r: (0 if rng.random() < 0.02 else _logu(rng, 1, hi)) for r in roots}
+        for i in g["inputs"]:
+            for d in i["shape"]:
+                if isinstance(d, str):
+                    syms[d] = syms[tie.get(d, d)]
+        for i in g["inputs"]:
+            m = 1
+            for d in i["shape"]:
+                m *= syms[d] if isinstance(d, str) else d
+            if m > fixture_numel_cap:
+                return None
+        return syms
+
+    seen = set() if seen is None else seen
+    reqs = []
+    k = 0
+    while len(reqs) < n:
+        kind = kinds[k % len(kinds)]
+        k += 1
+        for _ in range(64):
+            syms = draw(kind)
+            if syms is None:
+                continue
+            key = (kind, tuple(sorted(syms.items())))
+            if key in seen:
+                continue
+            seen.add(key)
+            reqs.append((kind, syms))
+            break
+    return graphs, reqs

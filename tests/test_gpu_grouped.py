@@ -67,9 +67,13 @@ def test_grouped_ln_gelu_matches_sequential(gpu, host_inputs):
     _assert_same(got, seq, "ln_gelu")
     # 3 plan kernels -> a handful of grouped launches, not 3 x len(shapes)
     assert launched <= 3 * 3, launched
-    want, _, _ = O.Executor().run(plan.to_json(), {k: np.asarray(v) for k, v in
-                                                     _inputs(g, shapes[3], np.random.default_rng(9)).items()})
-    assert want  # oracle runs on this plan
+    # and every request against the numpy oracle (oracle/disc_oracle.py) on its own inputs
+    src = [(p, {k: v.numpy() if hasattr(v, "numpy") else v for k, v in i.items()}) for p, i in reqs]
+    for r, (p, inputs) in enumerate(src):
+        want, _, _ = O.Executor().run(plan.to_json(), {k: np.asarray(v) for k, v in inputs.items()})
+        assert len(want) == len(got[r])
+        for a, b in zip(got[r], want):
+            assert O.rel_err(a, b) <= 1e-5, (r, shapes[r], O.rel_err(a, b))
 
 
 @pytest.mark.parametrize("name,shapes", [

@@ -83,7 +83,8 @@ def test_stream_of_10k_requests_collapses(D):
     """C5: 10 000 distinct (graph, shape) requests over 10 graphs, one compile per graph;
     the flush issues a few hundred actions, not one launch per request kernel."""
     import bench
-    _, graphs, reqs = bench.workload("stream")
+    wl = bench.make_workload("stream")
+    graphs, reqs = wl.graphs, wl.requests(0)
     compiler = D.Compiler()
     plans = {k: compiler.compile(g) for k, g in graphs.items()}
     rq = [(plans[k], {i["id"]: bench.input_shape(i, s) for i in graphs[k]["inputs"]}) for k, s in reqs]
