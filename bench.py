@@ -213,6 +213,8 @@ class Arena:
         """Host copy of a device tensor (optionally only rows `rows` of its leading dim)."""
         L, D = self.L, self.D
         shape = tuple(shape)
+        if not ptr and int(np.prod(shape)):
+            raise RuntimeError(f"d2h: null device pointer for a {shape} tensor")
         if rows is None:
             a = np.empty(shape, np.float32)
             if a.size:
@@ -221,9 +223,11 @@ class Arena:
         row = int(np.prod(shape[1:])) if len(shape) > 1 else 1
         a = np.empty((len(rows),) + shape[1:], np.float32)
         for j, r in enumerate(rows):
+            if not 0 <= int(r) < shape[0]:
+                raise RuntimeError(f"d2h: row {int(r)} outside a {shape} tensor")
             if row:
                 D.api._cuda(L.disc_cuda_memcpy(a.ctypes.data + 4 * row * j, C.c_void_p(ptr + 4 * row * int(r)),
-                                               4 * row, 1, self.stream), "d2h")
+                                               4 * row, 1, self.stream), f"d2h row {int(r)} of {shape} at {ptr:#x}")
         return a
 
 
@@ -320,6 +324,16 @@ class Bench:
         arena_bytes = int(min(args.arena_gb * (1 << 30), 0.3 * self.hbm)) if self.hbm else int(args.arena_gb * (1 << 30))
         self.arena = Arena(D, arena_bytes, st, seed=local)
         D.api._cuda(L.disc_cuda_stream_synchronize(st))
+
+    def close(self):
+        """Releases the executor, arena, flush buffer and stream (tests create several)."""
+        L = self.L
+        L.disc_cuda_stream_synchronize(self.stream)
+        self.ex.close()
+        for p in (self.arena.ptr, self.arena.cptr, self.flush):
+            L.disc_cuda_free(p, self.stream)
+        L.disc_cuda_stream_synchronize(self.stream)
+        L.disc_cuda_stream_destroy(self.stream)
 
     def plans_for(self, reqs):
         for k in {k for k, _ in reqs}:  # one compile per distinct graph (Compiler cache); the handle is kept
@@ -633,30 +647,37 @@ def verify_pass(B, wl, batch, mode, threads, seed=0):
             plan = V.check_plan(kind, shapes, True, rng)
             if plan is None:
                 continue
-            views = B.ex.request_output_views(r - a)
-            picks = V.expected_output_rows(kind, plan, len(views))
-            inputs, got = {}, []
-            if plan.mode == "rows":
-                ins, _ = V.ROW_SPEC[kind]
-                for name, p, shape in batch.bind[r]:
-                    inputs[name] = A.d2h(p, shape, plan.pick[ins[name]]) if name in ins else A.d2h(p, shape)
-                for (p, dims), rows in zip(views, picks):
-                    got.append(A.d2h(p, dims, rows))
-            elif plan.mode == "cols":
-                cols = plan.pick["c"]
-                for name, p, shape in batch.bind[r]:
-                    full = A.d2h(p, shape)
-                    ax = V.COL_SPEC[kind][0].get(name)
-                    inputs[name] = np.ascontiguousarray(np.take(full, cols, axis=ax)) if ax is not None else full
-                for (p, dims), _ in zip(views, picks):
-                    got.append(A.d2h(p, dims)[cols])
-            else:
-                for name, p, shape in batch.bind[r]:
-                    inputs[name] = A.d2h(p, shape)
-                for p, dims in views:
-                    got.append(A.d2h(p, dims))
-            B.L.disc_cuda_stream_synchronize(B.stream)
-            checker.submit(f"{kind} {syms}", kind, plan.mode, inputs, got)
+            try:
+                check_one(r, a, kind, syms, plan)
+            except Exception as ex:
+                raise RuntimeError(f"verify: request {r} ({kind} {syms}, mode {plan.mode}, chunk [{a},{b})): "
+                                   f"{type(ex).__name__}: {ex}") from ex
+
+    def check_one(r, a, kind, syms, plan):
+        views = B.ex.request_output_views(r - a)
+        picks = V.expected_output_rows(kind, plan, len(views))
+        inputs, got = {}, []
+        if plan.mode == "rows":
+            ins, _ = V.ROW_SPEC[kind]
+            for name, p, shape in batch.bind[r]:
+                inputs[name] = A.d2h(p, shape, plan.pick[ins[name]]) if name in ins else A.d2h(p, shape)
+            for (p, dims), rows in zip(views, picks):
+                got.append(A.d2h(p, dims, rows))
+        elif plan.mode == "cols":
+            cols = plan.pick["c"]
+            for name, p, shape in batch.bind[r]:
+                full = A.d2h(p, shape)
+                ax = V.COL_SPEC[kind][0].get(name)
+                inputs[name] = np.ascontiguousarray(np.take(full, cols, axis=ax)) if ax is not None else full
+            for (p, dims), _ in zip(views, picks):
+                got.append(A.d2h(p, dims)[cols])
+        else:
+            for name, p, shape in batch.bind[r]:
+                inputs[name] = A.d2h(p, shape)
+            for p, dims in views:
+                got.append(A.d2h(p, dims))
+        B.L.disc_cuda_stream_synchronize(B.stream)
+        checker.submit(f"{kind} {syms}", kind, plan.mode, inputs, got)
 
     batch.run(B.ex, on_chunk=on_chunk)
     out = checker.finish()
@@ -929,6 +950,8 @@ def main():
     distinct = len({(k, tuple(sorted(s.items()))) for i in range(args.warmup + args.steps) for k, s in wl.requests(i)})
     peak, peak_src = peaks()
     clocks = clk.summary()
+    log(f"[bench] timed: {value:.1f} GB/s ({value / world / peak:.3f} of peak), {ms_per_step:.2f} ms/step, "
+        f"{total_bytes / args.steps / 1e9:.1f} GB/step, {distinct} distinct shapes, clocks {clocks}")
 
     # ---- untimed: analysis of the first timed step ----
     reqs0 = wl.requests(args.warmup)

@@ -422,9 +422,16 @@ class Executor:
         self.stream = stream
         _check(lib().disc_executor_create(device, stream, C.byref(self._h)))
 
+    def close(self) -> None:
+        """Destroys the device executor now (idempotent); needed before the caller's
+        stream is destroyed, since other references may keep this object alive."""
+        h, self._h = self._h, C.c_void_p()
+        if h:
+            lib().disc_executor_destroy(h)
+
     def __del__(self):
         try:
-            lib().disc_executor_destroy(self._h)
+            self.close()
         except Exception:
             pass
 

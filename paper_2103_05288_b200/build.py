@@ -122,9 +122,11 @@ def build(clean: bool = False, verbose: bool = True) -> str:
         path = os.path.join(BUILD, "obj", f)
         if path not in keep:
             os.remove(path)
-    newest = max(os.path.getmtime(o) for o in objs)
+    exports = os.path.join(CSRC, "exports.map")
+    newest = max([os.path.getmtime(o) for o in objs] + [os.path.getmtime(exports)])
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread", "-ldl", "-lrt"]
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lpthread", "-ldl", "-lrt",
+               f"-Xlinker=--version-script={exports}"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

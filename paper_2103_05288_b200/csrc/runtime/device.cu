@@ -589,7 +589,23 @@ int disc_cuda_malloc(size_t bytes, void* stream, void** dptr) {
     *dptr = reinterpret_cast<void*>(g_fake_next.fetch_add((bytes + 4095) / 4096 * 4096 + 4096));
     return 0;
   }
-  return check(cudaMallocAsync(dptr, bytes ? bytes : 16, S(stream)), "cudaMallocAsync");
+  cudaError_t e = cudaMallocAsync(dptr, bytes ? bytes : 16, S(stream));
+  if (e == cudaErrorMemoryAllocation) {
+    // The pool keeps freed memory (release threshold = max): on exhaustion wait for the
+    // stream's pending frees, return the pool's unused memory to the driver and retry once.
+    (void)cudaGetLastError();
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(S(stream), &cs);
+    if (cs == cudaStreamCaptureStatusNone) {
+      int dev = 0;
+      cudaMemPool_t pool;
+      cudaStreamSynchronize(S(stream));
+      if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+        cudaMemPoolTrimTo(pool, 0);
+      e = cudaMallocAsync(dptr, bytes ? bytes : 16, S(stream));
+    }
+  }
+  return check(e, "cudaMallocAsync");
 }
 int disc_cuda_free(void* dptr, void* stream) {
   if (g_capture) return 0;

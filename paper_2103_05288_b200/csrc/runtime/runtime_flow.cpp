@@ -50,6 +50,7 @@ int DeviceCachingAllocator::alloc(int64_t bytes, ExecStats& stats) {
   if (it != free_.end() && !it->second.empty()) {
     int id = it->second.back();
     it->second.pop_back();
+    if (it->second.empty()) free_.erase(it);
     cached_ -= bytes;
     stats.allocator_cache_hits++;
     return id;
@@ -59,6 +60,12 @@ int DeviceCachingAllocator::alloc(int64_t bytes, ExecStats& stats) {
   // 16-byte granularity like the reference; the pool returns 256-byte aligned blocks.
   int64_t cap = (std::max<int64_t>(bytes, 1) + 15) / 16 * 16;
   cuda_ok(disc_cuda_malloc(static_cast<size_t>(cap), stream_, &p), "device allocation");
+  if (!retired_.empty()) {  // ids released by trim() are recycled: blocks_ stays bounded
+    const int id = retired_.back();
+    retired_.pop_back();
+    blocks_[id] = {static_cast<float*>(p), bytes};
+    return id;
+  }
   blocks_.push_back({static_cast<float*>(p), bytes});
   return static_cast<int>(blocks_.size()) - 1;
 }
@@ -82,19 +89,25 @@ void DeviceCachingAllocator::set_defer(bool on) {
 void DeviceCachingAllocator::release(int block) {
   free_[blocks_[block].bytes].push_back(block);
   cached_ += blocks_[block].bytes;
+}
+
+void DeviceCachingAllocator::enforce_budget() {
   if (budget_ > 0 && cached_ > budget_) trim();
 }
 
 void DeviceCachingAllocator::trim() {
-  // Release cached free blocks (largest sizes first) until under budget.  Released ids
-  // are retired, so hit/miss accounting stays exact-size.
-  for (auto it = free_.rbegin(); it != free_.rend() && cached_ > budget_ / 2; ++it) {
+  // Release cached free blocks (largest sizes first) until under half the budget.  Released
+  // ids are retired (reused by later misses), so hit/miss accounting stays exact-size and
+  // neither blocks_ nor free_ grows without bound under a stream of fresh shapes.
+  while (!free_.empty() && cached_ > budget_ / 2) {
+    auto it = std::prev(free_.end());
     for (int id : it->second) {
       disc_cuda_free(blocks_[id].ptr, stream_);
       blocks_[id].ptr = nullptr;
       cached_ -= blocks_[id].bytes;
+      retired_.push_back(id);
     }
-    it->second.clear();
+    free_.erase(it);
   }
 }
 
@@ -258,6 +271,7 @@ void DeviceExecutor::set_host_threads(int n) {
     }
     pool_ = std::make_unique<Pool>(n - 1, device_);
   }
+  set_cache_budget(budget_total_);
 }
 
 void DeviceExecutor::run_requests(const int* ids, int count, const CompiledPlan* const* plans, const uint64_t* serials,
@@ -633,6 +647,9 @@ void DeviceExecutor::run_impl(const CompiledPlan& plan, const std::vector<InputB
   ExecStats stats;
   stats.host_instruction_count = plan.host_instruction_count();
   const auto t_run = Clock::now();
+  // The previous run's outputs (returned to the cache at its end) are dead from here on:
+  // only now may the budget release cached blocks.
+  alloc_.enforce_budget();
   if (!append_records && !grouped_) {
     if (timing_pending_) cuda_ok(disc_cuda_stream_synchronize(stream_), "stream sync");
     timing_pending_ = false;

@@ -3,6 +3,7 @@
 // ExecStats and BufferEvents follow the reference Executor::run (executor.cpp:221-465).
 #pragma once
 
+#include <algorithm>
 #include <chrono>
 #include <map>
 #include <memory>
@@ -43,7 +44,10 @@ class DeviceCachingAllocator {
   float* data(int block) const { return blocks_[block].ptr; }
   int64_t bytes(int block) const { return blocks_[block].bytes; }
   void set_stream(void* s) { stream_ = s; }
+  // The budget is enforced at the start of the next run (enforce_budget): blocks returned
+  // at the end of a run back its outputs, which stay readable until then.
   void set_budget(int64_t b) { budget_ = b; }
+  void enforce_budget();
   // Grouped execution: frees are held back until release_deferred() (work queued for
   // later issue may still use the blocks), so no block is reused inside one group.
   void set_defer(bool on);
@@ -57,6 +61,7 @@ class DeviceCachingAllocator {
   };
   void* stream_;
   std::vector<Block> blocks_;
+  std::vector<int> retired_;
   std::map<int64_t, std::vector<int>> free_;
   int64_t cached_ = 0;
   int64_t budget_ = 0;
@@ -132,9 +137,13 @@ class DeviceExecutor {
     pref_ = p;
     for (auto& x : subs_) x->set_schedule(p);
   }
+  // The byte budget covers the executor and its host-thread sub-executors together: each
+  // allocator caches at most an equal share (a stream of fresh shapes fills every cache).
   void set_cache_budget(int64_t b) {
-    alloc_.set_budget(b);
-    for (auto& x : subs_) x->set_cache_budget(b);
+    budget_total_ = b;
+    const int64_t share = b > 0 ? std::max<int64_t>(1, b / static_cast<int64_t>(1 + subs_.size())) : 0;
+    alloc_.set_budget(share);
+    for (auto& x : subs_) x->alloc_.set_budget(share);
   }
   // Host-staging helper: device copy of host data owned by the executor (not counted in
   // plan allocator stats).
@@ -148,6 +157,7 @@ class DeviceExecutor {
   int device_;
   void* stream_;
   DeviceCachingAllocator alloc_;
+  int64_t budget_total_ = 0;
   Scratch scratch_;
   std::vector<OutputView> outputs_;
   std::vector<float*> passthrough_;  // owned copies for input pass-through outputs

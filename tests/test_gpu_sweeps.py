@@ -27,10 +27,13 @@ def test_benchmarked_sweep_matches_reference(gpu, ref, workload, requests):
     import bench
     wl = bench.make_workload(workload, 0, requests or 10000)
     B = bench.Bench(gpu, _bench_args(), 0, wl)
-    reqs = wl.requests(3)  # a step the bench would time (warmup 3): fresh shapes for the sweep
-    batch = B.batch(reqs)
-    batch.run(B.ex)  # warm pass, as the bench's warmup
-    res = bench.verify_pass(B, wl, batch, "full", threads=max(1, (os.cpu_count() or 2) - 1))
+    try:
+        reqs = wl.requests(3)  # a step the bench would time (warmup 3): fresh shapes for the sweep
+        batch = B.batch(reqs)
+        batch.run(B.ex)  # warm pass, as the bench's warmup
+        res = bench.verify_pass(B, wl, batch, "full", threads=max(1, (os.cpu_count() or 2) - 1))
+    finally:
+        B.close()
     print(f"\n{workload}: {res['requests_checked']} max floored {res['max_rel_err_floored']} true "
           f"{res['max_rel_err_true']} ulp {res['max_ulp']} over1e-5(true) {res['elements_over_1e-5_true']} "
           f"of {res['elements']}; per pattern {res['per_pattern']}")
