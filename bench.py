@@ -231,6 +231,9 @@ class Arena:
         return a
 
 
+call_ms_mallocs = []  # pool-malloc counter after each timed grouped call (diagnostics)
+
+
 class StepBatch:
     """One step's requests as flat C-ABI arrays (names / data / dims / ranks / offsets /
     plans), bound to arena views, split into chunks of ~chunk_bytes algorithmic bytes."""
@@ -286,15 +289,19 @@ class StepBatch:
     def _p(self, arr, k, ctype):
         return C.cast(C.c_void_p(arr.ctypes.data + arr.itemsize * int(k)), C.POINTER(ctype))
 
-    def run(self, ex, on_chunk=None):
+    def run(self, ex, on_chunk=None, call_ms=None):
         L = self.L
         for ci, (a, b) in enumerate(self.chunks):
+            t0 = time.perf_counter()
             i0 = int(self.offs[a])
             rc = L.disc_executor_run_grouped(ex._h, b - a, self._p(self.plans, a, C.c_void_p),
                                              self.chunk_offs[ci].ctypes.data_as(C.POINTER(C.c_int)),
                                              self._p(self.names, i0, C.c_char_p), self._p(self.data, i0, C.c_void_p),
                                              self._p(self.dimsp, i0, C.c_void_p), self._p(self.ranks, i0, C.c_int), 0)
             self.D.api._check(rc)
+            if call_ms is not None:
+                call_ms.append((time.perf_counter() - t0) * 1e3)
+                call_ms_mallocs.append(alloc_stats(self.D)[0])
             if on_chunk is not None:
                 on_chunk(ci, a, b)
 
@@ -313,6 +320,8 @@ class Bench:
         self.ex.set_schedule(args.schedule)
         self.ex.set_host_threads(args.host_threads)
         self.ex.set_cache_budget(int(args.cache_gb * (1 << 30)))
+        if getattr(args, "reserve_gb", 0):
+            self.ex.reserve(int(args.reserve_gb * (1 << 30)))
         self.compiler = D.Compiler()
         self.plans = {}
         sm, l2, hbm = C.c_int(), C.c_int64(), C.c_int64()
@@ -371,6 +380,28 @@ class Bench:
         L.disc_cuda_event_destroy(b)
         return ms.value
 
+    def device_bound_pass(self, batch, spin_us=600000):
+        """Device ms of one pass issued exactly as timed (same chunks, phases, threads) while
+        the stream is held behind a spin kernel, so the host's issue time is hidden: the
+        step's device-bound time (host_bound_frac compares the timed step with it)."""
+        L = self.L
+        a, b = self.event(), self.event()
+        L.disc_cuda_flush_l2(self.flush, self.flush_bytes, self.stream)
+        L.disc_cuda_spin(spin_us, self.stream)
+        L.disc_cuda_event_record(a, self.stream)
+        t0 = time.perf_counter()
+        batch.run(self.ex)
+        host_ms = (time.perf_counter() - t0) * 1e3
+        L.disc_cuda_event_record(b, self.stream)
+        L.disc_cuda_stream_synchronize(self.stream)
+        ms = C.c_float()
+        L.disc_cuda_event_elapsed_ms(a, b, C.byref(ms))
+        L.disc_cuda_event_destroy(a)
+        L.disc_cuda_event_destroy(b)
+        if host_ms > spin_us / 1e3:
+            log(f"[bench] device_bound_pass: host issue {host_ms:.1f} ms exceeded the {spin_us / 1e3:.0f} ms spin")
+        return ms.value, host_ms
+
     def record_pass(self, batch):
         """Per grouped launch records (timing mode: device ms per launch) of one pass."""
         recs = []
@@ -428,6 +459,28 @@ class ClockSampler:
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.samples)}
+
+
+def alloc_stats(D):
+    m, f, o = C.c_int64(), C.c_int64(), C.c_int64()
+    D.lib().disc_cuda_alloc_stats(C.byref(m), C.byref(f), C.byref(o))
+    return m.value, f.value, o.value
+
+
+def cpu_times():
+    try:
+        with open("/proc/stat") as fh:
+            return [int(x) for x in fh.readline().split()[1:]]
+    except OSError:
+        return None
+
+
+def cpu_steal(a, b):
+    """Fraction of CPU time stolen by the hypervisor between two /proc/stat samples."""
+    if not a or not b or len(a) < 8:
+        return None
+    d = [y - x for x, y in zip(a, b)]
+    return round(d[7] / max(1, sum(d[:8])), 4)
 
 
 def peaks():
@@ -801,7 +854,8 @@ def pattern_of(kind):
 
 
 def analyse(B, wl, reqs, costs, peak):
-    """Untimed analysis of one step: per-pattern device GB/s (all and large requests),
+    """Untimed analysis of one step: per-pattern device-bound GB/s (all and large requests;
+    each pass issued behind a spin kernel, so it is the kernels' rate, not the host's),
     per-kernel records keyed (pattern, artifact, schedule), the dominant kernel, and the
     device-only time of the whole step."""
     pats = {}
@@ -810,14 +864,14 @@ def analyse(B, wl, reqs, costs, peak):
     per_pattern, records = {}, {}
     for p, idx in sorted(pats.items()):
         sub, sc = [reqs[i] for i in idx], [costs[i] for i in idx]
-        ms = B.timed_pass(B.batch(sub, sc))
+        ms, _ = B.device_bound_pass(B.batch(sub, sc))
         b = sum(sc)
         ent = {"requests": len(sub), "bytes": b, "GB/s": round(b / ms / 1e6, 1) if ms > 0 else None}
         ent["frac_of_peak"] = round(ent["GB/s"] / peak, 4) if ent["GB/s"] else None
         big = [i for i in idx if costs[i] >= LARGE]
         if big:
             lb = sum(costs[i] for i in big)
-            lms = B.timed_pass(B.batch([reqs[i] for i in big], [costs[i] for i in big]))
+            lms, _ = B.device_bound_pass(B.batch([reqs[i] for i in big], [costs[i] for i in big]))
             ent["large"] = {"requests": len(big), "bytes": lb, "GB/s": round(lb / lms / 1e6, 1) if lms > 0 else None}
             ent["large"]["frac_of_peak"] = round(ent["large"]["GB/s"] / peak, 4) if ent["large"]["GB/s"] else None
             ent["large_byte_share"] = round(lb / b, 4) if b else None
@@ -829,8 +883,8 @@ def analyse(B, wl, reqs, costs, peak):
             a[1] += r["ms"]
             a[2] += 1
     full = B.record_pass(B.batch(reqs, costs))
-    device_ms = sum(r["ms"] for r in full)
-    return per_pattern, records, device_ms, len(full)
+    device_bound_ms, host_issue_ms = B.device_bound_pass(B.batch(reqs, costs))
+    return per_pattern, records, device_bound_ms, host_issue_ms, len(full)
 
 
 def main():
@@ -848,7 +902,8 @@ def main():
     ap.add_argument("--schedule", default="auto")
     ap.add_argument("--chunk-gb", type=float, default=32.0, help="algorithmic bytes per grouped call")
     ap.add_argument("--arena-gb", type=float, default=48.0)
-    ap.add_argument("--cache-gb", type=float, default=8.0, help="executor allocator cache budget")
+    ap.add_argument("--cache-gb", type=float, default=32.0, help="executor idle device-memory budget (caches + arena)")
+    ap.add_argument("--reserve-gb", type=float, default=64.0, help="executor buffer arena reserved up front")
     ap.add_argument("--e2e-gb", type=float, default=4.0, help="e2e: pinned host input bytes")
     ap.add_argument("--ref-step-s", type=float, default=4.0, help="reference arm: seconds of CPU work per step")
     ap.add_argument("--host-threads", type=int, default=0,
@@ -923,6 +978,9 @@ def main():
     # ---- timed region: K steps issued back to back; per step an event pair (the L2 flush
     # before it outside the pair); host flow of step i+1 overlaps device work of step i ----
     ev = [B.event() for _ in range(2 * args.steps)]
+    call_ms = []
+    al0 = alloc_stats(D)
+    cpu0 = cpu_times()
     launches0 = D.kernel_launches()
     barrier(dist, local)
     wall0 = time.perf_counter()
@@ -930,10 +988,21 @@ def main():
         for i in range(args.steps):
             L.disc_cuda_flush_l2(B.flush, B.flush_bytes, B.stream)
             L.disc_cuda_event_record(ev[2 * i], B.stream)
-            batches[args.warmup + i].run(B.ex)
+            batches[args.warmup + i].run(B.ex, call_ms=call_ms)
             L.disc_cuda_event_record(ev[2 * i + 1], B.stream)
         L.disc_cuda_stream_synchronize(B.stream)
     wall = time.perf_counter() - wall0
+    al1 = alloc_stats(D)
+    cpu1 = cpu_times()
+    host_diag = {"grouped_calls": len(call_ms), "call_ms_sum": round(sum(call_ms), 2),
+                 "call_ms_max": round(max(call_ms), 2) if call_ms else None,
+                 "call_ms_p50": round(statistics.median(call_ms), 2) if call_ms else None,
+                 "pool_mallocs": al1[0] - al0[0], "pool_frees": al1[1] - al0[1], "oom_retries": al1[2] - al0[2],
+                 "cpu_steal_frac": cpu_steal(cpu0, cpu1)}
+    mal = [b - a for a, b in zip([al0[0]] + call_ms_mallocs[:-1], call_ms_mallocs)]
+    slow = sorted(range(len(call_ms)), key=lambda k: -call_ms[k])[:6]
+    host_diag["slowest_calls"] = [(k, round(call_ms[k], 1), mal[k]) for k in slow]
+    log(f"[bench] host: {host_diag}")
     step_ms = []
     for i in range(args.steps):
         ms = C.c_float()
@@ -958,7 +1027,7 @@ def main():
     costs0 = batches[args.warmup].costs
     analysis = None
     if not args.no_analysis:
-        per_pattern, records, device_ms, n_group_launches = analyse(B, wl, reqs0, costs0, peak)
+        per_pattern, records, device_ms, host_issue_ms, n_group_launches = analyse(B, wl, reqs0, costs0, peak)
         (dk, (db, dms, dn)) = max(records.items(), key=lambda kv: kv[1][1])
         achieved = db / (dms / 1e3) / 1e9 if dms > 0 else 0.0
         traffic, tinfo = ncu_traffic(wl.name, dk)
@@ -977,6 +1046,7 @@ def main():
                          if tinfo else "no committed ncu capture for this (workload, kernel)"},
             "kernel_breakdown": breakdown,
             "device_ms_step": round(device_ms, 3),
+            "host_issue_ms_step": round(host_issue_ms, 3),
             "grouped_launches_step": n_group_launches,
         }
 
@@ -1016,11 +1086,13 @@ def main():
             "per_pattern": (analysis or {}).get("per_pattern"),
             "kernel_breakdown": (analysis or {}).get("kernel_breakdown"),
             "device_ms_per_step": (analysis or {}).get("device_ms_step"),
-            "host_bound_frac": round(max(0.0, 1 - analysis["device_ms_step"] / step_ms[0]), 3) if analysis else None,
+            "host_issue_ms_per_step": (analysis or {}).get("host_issue_ms_step"),
+            "host_bound_frac": round(max(0.0, 1 - analysis["device_ms_step"] / ms_per_step), 3) if analysis else None,
             "cpu_baseline": cpu,
             "e2e": {k: v for k, v in e2e.items() if k not in ("bytes", "seconds")} if e2e else None,
             "verify": ver,
             "gpu_launches": gpu_launches,
+            "host_diag": host_diag,
             "clocks": clocks,
             "host": host_info(),
             "wall_s_timed": round(wall, 3),

@@ -165,6 +165,9 @@ int disc_executor_set_timing(disc_executor e, int enabled);
 int disc_executor_set_schedule(disc_executor e, const char* schedule);
 /* Allocator byte budget for cached free blocks (0 = unlimited). */
 int disc_executor_set_cache_budget(disc_executor e, int64_t bytes);
+/* Reserves `bytes` of device memory for the executor's buffer arena now (kept for the
+ * executor's lifetime), so a stream of fresh shapes never grows it mid-stream. */
+int disc_executor_reserve(disc_executor e, int64_t bytes);
 
 /* ---- single-kernel entry (run_kernel, executor.cpp:137-219) ------------- */
 /* Runs artifact `kernel` at version `version` on device externals with the given

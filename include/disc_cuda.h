@@ -240,6 +240,9 @@ int disc_cuda_flush_l2(void* scratch, size_t bytes, void* stream);
 int disc_cuda_spin(uint64_t microseconds, void* stream);
 /* Number of kernels this library has launched (process-wide counter). */
 int64_t disc_cuda_kernel_launches(void);
+/* Diagnostics: stream-ordered pool calls made so far (cudaMallocAsync, cudaFreeAsync) and
+ * allocations retried after an out-of-memory (stream sync + pool trim). */
+int64_t disc_cuda_alloc_stats(int64_t* mallocs, int64_t* frees, int64_t* oom_retries);
 
 /* Programmatic dependent launch for fused kernels: 0 plain stream serialisation; 1 (default)
  * each kernel's launch overlaps the previous kernel and its dependency wait; 2 also lets
@@ -297,8 +300,13 @@ int disc_cuda_queue_record(int i, int* level, int* members, int64_t* bytes, int*
                            float* ms);
 
 /* Capture mode (pattern generator, host only): device calls become no-ops, allocations
- * return fake addresses and fused launches are recorded as JSON program structures. */
+ * return fake addresses and fused launches are recorded as JSON program structures.
+ * The mode is per host thread: 0 off, 1 capture + record, 2 capture without recording.
+ * disc_cuda_set_capture(mode) also clears the records; _set_capture_local only sets this
+ * thread's mode (executor host-flow workers inherit their caller's mode per job). */
 int disc_cuda_set_capture(int enabled);
+int disc_cuda_set_capture_local(int mode);
+int disc_cuda_capture_mode(void);
 int disc_cuda_capture_records(char** json);   /* free with disc_free */
 int disc_cuda_capturing(void);
 

@@ -100,6 +100,7 @@ def _declare(L: C.CDLL) -> None:
         "disc_executor_algorithmic_bytes": ([vp], i64),
         "disc_executor_set_schedule": ([vp, cp], i32),
         "disc_executor_set_cache_budget": ([vp, i64], i32),
+        "disc_executor_reserve": ([vp, i64], i32),
         "disc_executor_run_kernel": ([vp, vp, i32, i32, i32, P(vp), P(vp), P(i32), P(i64), i32], i32),
         "disc_guard_passes": ([vp, i32, i32, P(i64), i32], i32),
         "disc_plan_capture_programs": ([vp, i32, P(cp), P(vp), P(i32), P(vp)], i32),
@@ -136,6 +137,7 @@ def _declare(L: C.CDLL) -> None:
         "disc_cuda_set_pdl": ([i32], i32),
         "disc_cuda_pdl_mode": ([], i32),
         "disc_cuda_kernel_launches": ([], i64),
+        "disc_cuda_alloc_stats": ([vp, vp, vp], i64),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -454,6 +456,10 @@ class Executor:
 
     def set_cache_budget(self, nbytes: int) -> None:
         lib().disc_executor_set_cache_budget(self._h, int(nbytes))
+
+    def reserve(self, nbytes: int) -> None:
+        """Reserves device memory for the buffer arena up front (never released)."""
+        _check(lib().disc_executor_reserve(self._h, int(nbytes)))
 
     def _bind(self, inputs: Dict[str, object]):
         names = list(inputs.keys())

@@ -287,6 +287,10 @@ int disc_executor_set_cache_budget(disc_executor e, int64_t bytes) {
   return 0;
 }
 
+int disc_executor_reserve(disc_executor e, int64_t bytes) {
+  return guard([&] { e->ex.reserve(bytes); });
+}
+
 int disc_executor_run_kernel(disc_executor e, disc_plan p, int kernel, int version, int n_ext, const float* const* ext,
                              const int64_t* const* ext_dims, const int* ext_ranks, const int64_t* regs, int n_regs) {
   return guard([&] {

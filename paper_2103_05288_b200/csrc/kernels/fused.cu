@@ -3,6 +3,7 @@
 // accesses, CH chunks in flight per thread, f64 accumulation for reductions (the
 // reference's reduce semantics, kernels.cpp:46-54, 234-259).
 #include <cstdlib>
+#include <mutex>
 #include <unordered_map>
 
 #include "kernels.cuh"
@@ -136,10 +137,31 @@ int group_waves() {
   return w;
 }
 
+namespace {
+struct OccKey {
+  int device;
+  const void* kernel;
+  int block;
+  size_t smem;
+  bool operator==(const OccKey& o) const {
+    return device == o.device && kernel == o.kernel && block == o.block && smem == o.smem;
+  }
+};
+struct OccKeyHash {
+  size_t operator()(const OccKey& k) const {
+    uint64_t h = reinterpret_cast<uintptr_t>(k.kernel) * 0x9E3779B97F4A7C15ull;
+    h ^= (static_cast<uint64_t>(k.block) << 40) ^ (static_cast<uint64_t>(k.device) << 56) ^ k.smem;
+    return static_cast<size_t>(h ^ (h >> 29));
+  }
+};
+}  // namespace
+
+// Resident CTAs per SM for (device, kernel, block, dynamic smem): the full tuple is the key.
 int resident_ctas(const void* kernel, int block, size_t smem) {
-  thread_local std::unordered_map<uint64_t, int> cache;
-  const uint64_t key = (reinterpret_cast<uintptr_t>(kernel) * 0x9E3779B97F4A7C15ull) ^
-                       (static_cast<uint64_t>(block) << 40) ^ static_cast<uint64_t>(smem);
+  thread_local std::unordered_map<OccKey, int, OccKeyHash> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const OccKey key{dev, kernel, block, smem};
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int n = 0;
@@ -147,6 +169,19 @@ int resident_ctas(const void* kernel, int block, size_t smem) {
   if (cache.size() > 4096) cache.clear();
   cache.emplace(key, n);
   return n;
+}
+
+cudaError_t raise_smem_limit(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<OccKey, size_t, OccKeyHash> limit;  // (device, kernel) -> attribute set
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = limit[OccKey{dev, kernel, 0, 0}];
+  if (cur >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (e == cudaSuccess) cur = bytes;
+  return e;
 }
 
 }  // namespace disc_dev

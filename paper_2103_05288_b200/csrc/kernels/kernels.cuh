@@ -734,19 +734,29 @@ __global__ void __launch_bounds__(kColThreads, 4) k_col_g(const __grid_constant_
 
 // ---------------------------------------------------------------------------
 // Host-side launch configuration shared by the interpreter and generated kernels.
+// SM count of the calling thread's current device (cached per thread and device).
 inline int sm_count() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
+  thread_local int dev_cached = -1, n_cached = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return n_cached;
+  if (dev != dev_cached) {
+    int v = 148;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) n_cached = v;
+    dev_cached = dev;
+  }
+  return n_cached;
 }
+
+// Raises `kernel`'s dynamic shared-memory limit on the current device to at least `bytes`
+// (fused.cu).  The attribute is shared by every thread launching the kernel, so it only
+// ever grows (per device and kernel, under a lock): a concurrent launch needing less can
+// never see it lowered under its feet.
+cudaError_t raise_smem_limit(const void* kernel, size_t bytes);
 
 template <typename K>
 inline cudaError_t set_smem(K kernel, size_t bytes, size_t threshold = 40 * 1024) {
   if (bytes <= threshold) return cudaSuccess;
-  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  return raise_smem_limit(reinterpret_cast<const void*>(kernel), bytes);
 }
 
 // Host side of a grouped launch: the members' host descriptors (full layout, for grid and

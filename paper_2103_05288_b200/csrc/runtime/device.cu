@@ -54,14 +54,19 @@ int count();
 namespace {
 thread_local std::string t_err;
 std::atomic<int64_t> g_launches{0};
+std::atomic<int64_t> g_mallocs{0}, g_frees{0}, g_oom_retries{0};  // driver-pool calls (diagnostics)
 std::atomic<int64_t> g_spec_launches{0};
 bool g_spec_enabled = true;
 
 // Capture mode (host-only dry run used by the pattern generator): device calls become
-// no-ops, allocations return fake aligned addresses, launches are recorded.
-bool g_capture = false;
-bool g_capture_record = true;  // capture mode 2: dry run without recording (host timing)
+// no-ops, allocations return fake aligned addresses, launches are recorded.  The mode is
+// per host thread (a dry run must not turn another thread's real executor into a no-op);
+// the executor's host-flow workers inherit their caller's mode for each job
+// (disc_cuda_set_capture_local).
+thread_local bool g_capture = false;
+thread_local bool g_capture_record = true;  // capture mode 2: dry run without recording (host timing)
 std::atomic<uint64_t> g_fake_next{uint64_t{1} << 36};
+std::mutex g_records_mu;
 std::vector<std::string> g_records;
 
 uint64_t mix(uint64_t h, uint64_t v) {
@@ -115,6 +120,7 @@ void record(const std::string& kind, uint64_t key, const std::string& body) {
   if (!g_capture_record) return;
   char hex[32];
   std::snprintf(hex, sizeof hex, "%016llx", static_cast<unsigned long long>(key));
+  std::lock_guard<std::mutex> lock(g_records_mu);
   g_records.push_back("{\"kind\":\"" + kind + "\",\"key\":\"" + hex + "\"," + body + "}");
 }
 
@@ -589,8 +595,10 @@ int disc_cuda_malloc(size_t bytes, void* stream, void** dptr) {
     *dptr = reinterpret_cast<void*>(g_fake_next.fetch_add((bytes + 4095) / 4096 * 4096 + 4096));
     return 0;
   }
+  g_mallocs.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaMallocAsync(dptr, bytes ? bytes : 16, S(stream));
   if (e == cudaErrorMemoryAllocation) {
+    g_oom_retries.fetch_add(1, std::memory_order_relaxed);
     // The pool keeps freed memory (release threshold = max): on exhaustion wait for the
     // stream's pending frees, return the pool's unused memory to the driver and retry once.
     (void)cudaGetLastError();
@@ -613,6 +621,7 @@ int disc_cuda_free(void* dptr, void* stream) {
     t_q.frees.push_back(dptr);
     return 0;
   }
+  g_frees.fetch_add(1, std::memory_order_relaxed);
   return check(cudaFreeAsync(dptr, S(stream)), "cudaFreeAsync");
 }
 int disc_cuda_host_alloc(size_t bytes, void** hptr) {
@@ -775,6 +784,12 @@ int disc_cuda_spin(uint64_t microseconds, void* stream) {
   return counted(disc_launch::spin(microseconds * 1000ull, S(stream)), "launch spin");
 }
 int64_t disc_cuda_kernel_launches(void) { return g_launches.load(); }
+int64_t disc_cuda_alloc_stats(int64_t* mallocs, int64_t* frees, int64_t* oom_retries) {
+  if (mallocs) *mallocs = g_mallocs.load();
+  if (frees) *frees = g_frees.load();
+  if (oom_retries) *oom_retries = g_oom_retries.load();
+  return 0;
+}
 
 int disc_cuda_set_pdl(int mode) {
   disc_launch::set_pdl(mode < 0 ? 0 : (mode > 2 ? 2 : mode));
@@ -1038,6 +1053,7 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
           j += (i ? "," : "") + std::to_string(launch_weight(a.gk.kind == 0 ? 0 : 1, a.ptrs[i]));
         j += "]";
       }
+      std::lock_guard<std::mutex> lock(g_records_mu);
       g_records.push_back(j + "}");
     }
     for (Queue* q : qs) {
@@ -1181,6 +1197,7 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
                  ms(t_start, t_plan), ms(t_plan, t_pack), ms(t_pack, t_end));
   }
   for (Queue* q : qs) {
+    g_frees.fetch_add(static_cast<int64_t>(q->frees.size()), std::memory_order_relaxed);
     for (void* p : q->frees)
       if (!rc) rc = check(cudaFreeAsync(p, st), "cudaFreeAsync");
     q->frees.clear();
@@ -1326,6 +1343,7 @@ int disc_cuda_queue_issue_graph(void* queue, void** graph_exec) {
   }
   if (!done) {
     rc = issue_all();
+    g_frees.fetch_add(static_cast<int64_t>(q->frees.size()), std::memory_order_relaxed);
     for (void* f : q->frees)
       if (!rc) rc = check(cudaFreeAsync(f, st), "cudaFreeAsync");
   }
@@ -1387,12 +1405,22 @@ int disc_cuda_queue_record(int i, int* level, int* members, int64_t* bytes, int*
 int disc_cuda_set_capture(int enabled) {
   g_capture = enabled != 0;
   g_capture_record = enabled == 1;
-  if (g_capture) g_records.clear();
+  if (g_capture) {
+    std::lock_guard<std::mutex> lock(g_records_mu);
+    g_records.clear();
+  }
   return 0;
 }
+int disc_cuda_set_capture_local(int mode) {
+  g_capture = mode != 0;
+  g_capture_record = mode == 1;
+  return 0;
+}
+int disc_cuda_capture_mode(void) { return g_capture ? (g_capture_record ? 1 : 2) : 0; }
 int disc_cuda_capturing(void) { return g_capture ? 1 : 0; }
 
 int disc_cuda_capture_records(char** json) {
+  std::lock_guard<std::mutex> lock(g_records_mu);
   std::string s = "[";
   for (size_t i = 0; i < g_records.size(); ++i) s += (i ? ",\n" : "\n") + g_records[i];
   s += "\n]";

@@ -784,7 +784,12 @@ void fast_div_magic(uint32_t d, uint32_t* magic, uint32_t* shift) {
 }
 
 Scratch::~Scratch() {
-  for (auto& c : chunks_) disc_cuda_free(c.base, stream_);
+  for (auto& c : chunks_) {
+    if (src_)
+      src_->put_chunk(c.base);
+    else
+      disc_cuda_free(c.base, stream_);
+  }
 }
 
 void* Scratch::alloc(int64_t bytes) {
@@ -796,7 +801,10 @@ void* Scratch::alloc(int64_t bytes) {
   if (cur_ == chunks_.size()) {
     int64_t size = std::max<int64_t>(bytes, int64_t{64} << 20);
     void* p = nullptr;
-    cuda_ok(disc_cuda_malloc(static_cast<size_t>(size), stream_, &p), "scratch allocation");
+    if (src_)
+      p = src_->get_chunk(size);
+    else
+      cuda_ok(disc_cuda_malloc(static_cast<size_t>(size), stream_, &p), "scratch allocation");
     chunks_.push_back({static_cast<char*>(p), size});
     used_ = 0;
   }

@@ -27,9 +27,17 @@ struct OutBuf {
 // Stream-ordered bump allocator for per-launch device scratch (reduce results feeding a
 // separate epilogue pass, f64 split-R partials, materialised members).  Chunks are
 // recycled only at reset(), i.e. between launches on the same stream.
+// A device-memory source for large chunks (the executor's DeviceArena); without one,
+// chunks come from the stream-ordered pool.
+struct ChunkSource {
+  virtual void* get_chunk(int64_t bytes) = 0;
+  virtual void put_chunk(void* p) = 0;
+  virtual ~ChunkSource() = default;
+};
+
 class Scratch {
  public:
-  explicit Scratch(void* stream) : stream_(stream) {}
+  explicit Scratch(void* stream, ChunkSource* src = nullptr) : stream_(stream), src_(src) {}
   ~Scratch();
   void set_stream(void* s) { stream_ = s; }
   void* alloc(int64_t bytes);
@@ -41,6 +49,7 @@ class Scratch {
     int64_t size;
   };
   void* stream_;
+  ChunkSource* src_;
   std::vector<Chunk> chunks_;
   size_t cur_ = 0;
   int64_t used_ = 0;

@@ -40,10 +40,150 @@ using Clock = std::chrono::steady_clock;
 
 // ---------------------------------------------------------------------------
 
-DeviceCachingAllocator::~DeviceCachingAllocator() {
-  for (auto& b : blocks_)
-    if (b.ptr) disc_cuda_free(b.ptr, stream_);
+DeviceArena::~DeviceArena() {
+  for (auto& [base, n] : regions_) disc_cuda_free(base, stream_);
 }
+
+char* DeviceArena::region_of(char* p) const {
+  auto it = regions_.upper_bound(p);
+  return it == regions_.begin() ? nullptr : std::prev(it)->first;
+}
+
+void DeviceArena::insert_free(char* p, int64_t n) {
+  free_by_addr_.emplace(p, n);
+  free_by_size_.emplace(n, p);
+}
+
+void DeviceArena::erase_free(std::map<char*, int64_t>::iterator it) {
+  free_by_size_.erase({it->second, it->first});
+  free_by_addr_.erase(it);
+}
+
+void* DeviceArena::alloc(int64_t bytes) {
+  std::lock_guard<std::mutex> lock(mu_);
+  auto fit = free_by_size_.lower_bound({bytes, nullptr});
+  if (fit == free_by_size_.end()) {
+    const int64_t n = std::max(bytes, kRegion);
+    void* q = nullptr;
+    cuda_ok(disc_cuda_malloc(static_cast<size_t>(n), stream_, &q), "device allocation");
+    regions_.emplace(static_cast<char*>(q), n);
+    region_total_ += n;
+    insert_free(static_cast<char*>(q), n);
+    fit = free_by_size_.lower_bound({bytes, nullptr});
+  }
+  const auto [n, p] = *fit;
+  erase_free(free_by_addr_.find(p));
+  if (n > bytes) insert_free(p + bytes, n - bytes);
+  used_.emplace(p, bytes);
+  used_total_ += bytes;
+  return p;
+}
+
+void DeviceArena::free(void* q) {
+  std::lock_guard<std::mutex> lock(mu_);
+  char* p = static_cast<char*>(q);
+  auto u = used_.find(p);
+  if (u == used_.end()) throw InternalError("arena free of an unknown block");
+  int64_t n = u->second;
+  used_.erase(u);
+  used_total_ -= n;
+  char* reg = region_of(p);
+  auto next = free_by_addr_.lower_bound(p);
+  if (next != free_by_addr_.end() && next->first == p + n && region_of(next->first) == reg) {
+    n += next->second;
+    auto after = std::next(next);
+    erase_free(next);
+    next = after;
+  }
+  if (next != free_by_addr_.begin()) {
+    auto prev = std::prev(next);
+    if (prev->first + prev->second == p && region_of(prev->first) == reg) {
+      p = prev->first;
+      n += prev->second;
+      erase_free(prev);
+    }
+  }
+  insert_free(p, n);
+}
+
+void DeviceArena::release_idle(int64_t keep) {
+  std::lock_guard<std::mutex> lock(mu_);
+  for (auto it = regions_.begin(); it != regions_.end() && region_total_ - used_total_ > keep;) {
+    auto f = free_by_addr_.find(it->first);
+    if (f != free_by_addr_.end() && f->second == it->second && !reserved_.count(it->first)) {  // wholly free
+      erase_free(f);
+      disc_cuda_free(it->first, stream_);
+      region_total_ -= it->second;
+      it = regions_.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
+void DeviceArena::reserve(int64_t bytes) {
+  std::lock_guard<std::mutex> lock(mu_);
+  if (region_total_ >= bytes) return;
+  const int64_t n = (bytes - region_total_ + 255) / 256 * 256;
+  void* q = nullptr;
+  cuda_ok(disc_cuda_malloc(static_cast<size_t>(n), stream_, &q), "device reservation");
+  regions_.emplace(static_cast<char*>(q), n);
+  reserved_.insert(static_cast<char*>(q));
+  region_total_ += n;
+  insert_free(static_cast<char*>(q), n);
+}
+
+int64_t DeviceArena::idle_bytes() {
+  std::lock_guard<std::mutex> lock(mu_);
+  return region_total_ - used_total_;
+}
+
+int64_t DeviceArena::region_bytes() {
+  std::lock_guard<std::mutex> lock(mu_);
+  return region_total_;
+}
+
+PhysicalPool::~PhysicalPool() {
+  for (char* p : slabs_) arena_->free(p);
+}
+
+int64_t PhysicalPool::class_of(int64_t bytes) {
+  const int64_t b = std::max<int64_t>(bytes, 256);
+  if (b > kSlabMax) return (b + 255) / 256 * 256;  // arena blocks: 256-byte granularity
+  int e = 63 - __builtin_clzll(static_cast<unsigned long long>(b - 1));  // 2^e < b <= 2^(e+1)
+  const int64_t step = std::max<int64_t>(256, int64_t{1} << std::max(0, e - 2));  // 4 classes per octave
+  return (b + step - 1) / step * step;
+}
+
+void* PhysicalPool::get(int64_t cls) {
+  if (cls > kSlabMax) return arena_->alloc(cls);
+  auto it = free_.find(cls);
+  if (it != free_.end()) {
+    void* p = it->second.back();
+    it->second.pop_back();
+    if (it->second.empty()) free_.erase(it);
+    free_bytes_ -= cls;
+    return p;
+  }
+  if (slab_used_ + cls > kSlab) {  // slabs come from the arena too (reserved memory, no driver call)
+    slabs_.push_back(static_cast<char*>(arena_->alloc(kSlab)));
+    slab_used_ = 0;
+  }
+  void* p = slabs_.back() + slab_used_;
+  slab_used_ += cls;
+  return p;
+}
+
+void PhysicalPool::put(void* p, int64_t cls) {
+  if (cls > kSlabMax) {
+    arena_->free(p);
+    return;
+  }
+  free_[cls].push_back(p);
+  free_bytes_ += cls;
+}
+
+DeviceCachingAllocator::~DeviceCachingAllocator() = default;  // the pool owns the memory
 
 int DeviceCachingAllocator::alloc(int64_t bytes, ExecStats& stats) {
   auto it = free_.find(bytes);
@@ -56,17 +196,16 @@ int DeviceCachingAllocator::alloc(int64_t bytes, ExecStats& stats) {
     return id;
   }
   stats.alloc_calls++;
-  void* p = nullptr;
-  // 16-byte granularity like the reference; the pool returns 256-byte aligned blocks.
-  int64_t cap = (std::max<int64_t>(bytes, 1) + 15) / 16 * 16;
-  cuda_ok(disc_cuda_malloc(static_cast<size_t>(cap), stream_, &p), "device allocation");
+  // 16-byte granularity like the reference; physical blocks are 256-byte aligned classes.
+  const int64_t cls = PhysicalPool::class_of((std::max<int64_t>(bytes, 1) + 15) / 16 * 16);
+  void* p = pool_.get(cls);
   if (!retired_.empty()) {  // ids released by trim() are recycled: blocks_ stays bounded
     const int id = retired_.back();
     retired_.pop_back();
-    blocks_[id] = {static_cast<float*>(p), bytes};
+    blocks_[id] = {static_cast<float*>(p), bytes, cls};
     return id;
   }
-  blocks_.push_back({static_cast<float*>(p), bytes});
+  blocks_.push_back({static_cast<float*>(p), bytes, cls});
   return static_cast<int>(blocks_.size()) - 1;
 }
 
@@ -102,7 +241,7 @@ void DeviceCachingAllocator::trim() {
   while (!free_.empty() && cached_ > budget_ / 2) {
     auto it = std::prev(free_.end());
     for (int id : it->second) {
-      disc_cuda_free(blocks_[id].ptr, stream_);
+      pool_.put(blocks_[id].ptr, blocks_[id].cls);
       blocks_[id].ptr = nullptr;
       cached_ -= blocks_[id].bytes;
       retired_.push_back(id);
@@ -113,8 +252,13 @@ void DeviceCachingAllocator::trim() {
 
 // ---------------------------------------------------------------------------
 
-DeviceExecutor::DeviceExecutor(int device, void* stream)
-    : device_(device), stream_(stream), alloc_(stream), scratch_(stream), cache_(new_launch_cache()) {
+DeviceExecutor::DeviceExecutor(int device, void* stream, std::shared_ptr<DeviceArena> arena)
+    : device_(device),
+      stream_(stream),
+      arena_(arena ? std::move(arena) : std::make_shared<DeviceArena>(stream)),
+      alloc_(stream, arena_),
+      scratch_(stream, arena_.get()),
+      cache_(new_launch_cache()) {
   cuda_ok(disc_cuda_set_device(device), "set device");
 }
 
@@ -238,8 +382,12 @@ struct DeviceExecutor::Pool {
       });
   }
   void start(const std::function<void(int)>& f) {  // f(w) on every worker, asynchronously
+    const int capture = disc_cuda_capture_mode();  // workers run in the caller's capture mode
     std::lock_guard<std::mutex> l(mu);
-    job = f;
+    job = [f, capture](int w) {
+      disc_cuda_set_capture_local(capture);
+      f(w);
+    };
     pending = static_cast<int>(threads.size());
     ++gen;
     cv.notify_all();
@@ -266,7 +414,7 @@ void DeviceExecutor::set_host_threads(int n) {
   host_threads_ = n;
   if (n > 1) {
     for (int w = 1; w < n; ++w) {
-      subs_.push_back(std::make_unique<DeviceExecutor>(device_, stream_));
+      subs_.push_back(std::make_unique<DeviceExecutor>(device_, stream_, arena_));
       subs_.back()->set_schedule(pref_);
     }
     pool_ = std::make_unique<Pool>(n - 1, device_);
@@ -363,6 +511,12 @@ void DeviceExecutor::run_grouped_batch(int n, const CompiledPlan* const* plans, 
   } else {
     phases.emplace_back(n);
     std::iota(phases[0].begin(), phases[0].end(), 0);
+  }
+  // the previous call's outputs are dead: idle memory beyond the budget goes back first
+  if (budget_total_ > 0) {
+    alloc_.enforce_budget();
+    for (auto& x : subs_) x->alloc_.enforce_budget();
+    arena_->release_idle(budget_total_ - budget_total_ / 4);
   }
   // session
   begin_grouped();  // resets outputs, records, scratch; defers frees
@@ -529,9 +683,14 @@ DeviceExecutor::~DeviceExecutor() {
 }
 
 void DeviceExecutor::set_stream(void* s) {
+  // Cached blocks and arena ranges are reused in stream order: work of the old stream must
+  // be done before the new stream may touch them.
+  if (stream_ && s != stream_) disc_cuda_stream_synchronize(stream_);
   stream_ = s;
   alloc_.set_stream(s);
   scratch_.set_stream(s);
+  arena_->set_stream(s);
+  for (auto& x : subs_) x->set_stream(s);
 }
 
 const float* DeviceExecutor::stage_input(int slot, const void* host, int64_t bytes) {
@@ -650,6 +809,7 @@ void DeviceExecutor::run_impl(const CompiledPlan& plan, const std::vector<InputB
   // The previous run's outputs (returned to the cache at its end) are dead from here on:
   // only now may the budget release cached blocks.
   alloc_.enforce_budget();
+  if (budget_total_ > 0 && !grouped_) arena_->release_idle(budget_total_ - budget_total_ / 4);
   if (!append_records && !grouped_) {
     if (timing_pending_) cuda_ok(disc_cuda_stream_synchronize(stream_), "stream sync");
     timing_pending_ = false;

@@ -6,6 +6,9 @@
 #include <algorithm>
 #include <chrono>
 #include <map>
+#include <mutex>
+#include <set>
+#include <unordered_map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -31,19 +34,88 @@ struct BufferEvent {
   int logical = -1, physical = -1, alloc_instr = -1, dealloc_instr = -1;
 };
 
+// Large-block device memory shared by an executor and its host-thread sub-executors:
+// address-ordered best fit with coalescing over big regions taken from the stream-ordered
+// pool, so a stream of fresh shapes allocates without a driver call per buffer.  Every
+// user issues on the same stream, so a freed range can be handed out again at once: the
+// new owner's work is ordered after the old owner's on that stream.
+class DeviceArena : public ChunkSource {
+ public:
+  static constexpr int64_t kRegion = int64_t{2} << 30;
+  explicit DeviceArena(void* stream) : stream_(stream) {}
+  ~DeviceArena() override;
+  void* alloc(int64_t bytes);  // 256-byte multiples
+  void free(void* p);
+  void* get_chunk(int64_t bytes) override { return alloc((bytes + 255) / 256 * 256); }
+  void put_chunk(void* p) override { free(p); }
+  // Returns wholly free regions to the pool while more than `keep` bytes sit idle
+  // (reserved regions are kept).
+  void release_idle(int64_t keep);
+  // Grows the arena to at least `bytes` now, as one region that is never released.
+  void reserve(int64_t bytes);
+  int64_t idle_bytes();
+  int64_t region_bytes();
+  void set_stream(void* s) { stream_ = s; }
+
+ private:
+  void insert_free(char* p, int64_t n);
+  void erase_free(std::map<char*, int64_t>::iterator it);
+  char* region_of(char* p) const;
+  std::mutex mu_;
+  void* stream_;
+  std::map<char*, int64_t> regions_;                 // base -> bytes
+  std::set<char*> reserved_;                         // bases never released
+  std::map<char*, int64_t> free_by_addr_;            // start -> bytes
+  std::set<std::pair<int64_t, char*>> free_by_size_;  // (bytes, start)
+  std::unordered_map<char*, int64_t> used_;          // start -> bytes
+  int64_t region_total_ = 0, used_total_ = 0;
+};
+
+// Physical device memory under the logical allocator.  Blocks up to kSlabMax are rounded up
+// to size classes (four per power of two, <= 25% slack), carved from kSlab slabs and
+// recycled per class across different exact sizes; larger blocks come from the shared
+// DeviceArena.  Nothing here calls the driver per buffer once warm.
+class PhysicalPool {
+ public:
+  static constexpr int64_t kSlab = int64_t{64} << 20;
+  static constexpr int64_t kSlabMax = int64_t{1} << 20;
+  PhysicalPool(void* stream, std::shared_ptr<DeviceArena> arena) : stream_(stream), arena_(std::move(arena)) {}
+  ~PhysicalPool();
+  static int64_t class_of(int64_t bytes);
+  void* get(int64_t cls);
+  void put(void* p, int64_t cls);
+  int64_t free_bytes() const { return free_bytes_; }
+  void set_stream(void* s) { stream_ = s; }
+  void set_arena(std::shared_ptr<DeviceArena> a) { arena_ = std::move(a); }
+  DeviceArena& arena() { return *arena_; }
+
+ private:
+  void* stream_;
+  std::shared_ptr<DeviceArena> arena_;
+  std::map<int64_t, std::vector<void*>> free_;  // small class bytes -> free blocks
+  std::vector<char*> slabs_;
+  int64_t slab_used_ = kSlab;                   // bytes used in slabs_.back()
+  int64_t free_bytes_ = 0;
+};
+
 // Exact-byte-size free-list allocator over device memory (reference CachedAllocator,
-// executor.cpp:53-76, same hit/miss accounting).  Raw memory comes from the stream-
-// ordered pool; an optional byte budget trims cached free blocks (never hit by parity
-// workloads, bounds memory across >=10k distinct shapes).
+// executor.cpp:53-76, same hit/miss accounting).  Physical memory comes from the size-class
+// PhysicalPool; an optional byte budget moves cached free blocks back to it and bounds the
+// pool (never hit by parity workloads, bounds memory across >=10k distinct shapes).
 class DeviceCachingAllocator {
  public:
-  explicit DeviceCachingAllocator(void* stream) : stream_(stream) {}
+  DeviceCachingAllocator(void* stream, std::shared_ptr<DeviceArena> arena)
+      : stream_(stream), pool_(stream, std::move(arena)) {}
   ~DeviceCachingAllocator();
   int alloc(int64_t bytes, ExecStats& stats);
   void free(int block);
   float* data(int block) const { return blocks_[block].ptr; }
   int64_t bytes(int block) const { return blocks_[block].bytes; }
-  void set_stream(void* s) { stream_ = s; }
+  void set_stream(void* s) {
+    stream_ = s;
+    pool_.set_stream(s);
+  }
+  PhysicalPool& pool() { return pool_; }
   // The budget is enforced at the start of the next run (enforce_budget): blocks returned
   // at the end of a run back its outputs, which stay readable until then.
   void set_budget(int64_t b) { budget_ = b; }
@@ -58,8 +130,10 @@ class DeviceCachingAllocator {
   struct Block {
     float* ptr = nullptr;
     int64_t bytes = 0;
+    int64_t cls = 0;  // physical size class
   };
   void* stream_;
+  PhysicalPool pool_;
   std::vector<Block> blocks_;
   std::vector<int> retired_;
   std::map<int64_t, std::vector<int>> free_;
@@ -93,7 +167,8 @@ struct InputBinding {
 
 class DeviceExecutor {
  public:
-  DeviceExecutor(int device, void* stream);
+  // `arena`: the large-block arena to share (host-thread sub-executors get their parent's).
+  DeviceExecutor(int device, void* stream, std::shared_ptr<DeviceArena> arena = nullptr);
   ~DeviceExecutor();
   void set_stream(void* s);
   void* stream() const { return stream_; }
@@ -137,11 +212,14 @@ class DeviceExecutor {
     pref_ = p;
     for (auto& x : subs_) x->set_schedule(p);
   }
-  // The byte budget covers the executor and its host-thread sub-executors together: each
-  // allocator caches at most an equal share (a stream of fresh shapes fills every cache).
+  // The byte budget bounds the idle device memory the executor and its host-thread
+  // sub-executors keep between runs: a quarter for the exact-size caches (an equal share
+  // each; a stream of fresh shapes fills every cache with sizes that never recur), the
+  // rest for idle arena regions (reused across sizes).  Enforced at run start.
+  void reserve(int64_t bytes) { arena_->reserve(bytes); }
   void set_cache_budget(int64_t b) {
     budget_total_ = b;
-    const int64_t share = b > 0 ? std::max<int64_t>(1, b / static_cast<int64_t>(1 + subs_.size())) : 0;
+    const int64_t share = b > 0 ? std::max<int64_t>(1, b / 4 / static_cast<int64_t>(1 + subs_.size())) : 0;
     alloc_.set_budget(share);
     for (auto& x : subs_) x->alloc_.set_budget(share);
   }
@@ -156,6 +234,7 @@ class DeviceExecutor {
  private:
   int device_;
   void* stream_;
+  std::shared_ptr<DeviceArena> arena_;
   DeviceCachingAllocator alloc_;
   int64_t budget_total_ = 0;
   Scratch scratch_;
