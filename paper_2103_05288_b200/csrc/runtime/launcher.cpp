@@ -474,6 +474,15 @@ const float* neg_inf_ptr() {
 }
 
 // DISC_ARG_CACHE=0 disables the reduce-argument cache (A/B).
+// Few long rows without a fused epilogue run on the column machinery (DISC_SPLIT_ROWS=0: off).
+bool split_rows_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DISC_SPLIT_ROWS");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 bool arg_cache_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("DISC_ARG_CACHE");
@@ -1091,6 +1100,16 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
       PL = make_loop(pp, Npost);
       post_pass = Npost > 0;
     }
+  }
+
+  // Few long rows and no fused epilogue (a full reduction [N] -> [1], column sums of
+  // [N, 1], ...): one row per thread group would leave most SMs idle (K CTAs), so the rows
+  // run on the column machinery with C = 1 -- each row's R split across CTAs, f64 partials
+  // joined in a fixed order.
+  if (R.schedule == DISC_SCHED_ROW && !empty && !post_fused && split_rows_enabled() && R.K < sm_count() &&
+      R.R >= 8192) {
+    R.schedule = DISC_SCHED_COL_SINGLE;
+    R.C = 1;
   }
 
   // Bind loads to the schedule's [rows, W] view and pick the vector width.

@@ -463,3 +463,34 @@ def test_odd_width_rows(gpu, ref, fixtures):
         inputs[i["id"]] = (np.full(shape, cv, np.float32) if cv is not None
                            else rng.uniform(0.25, 2.0, size=shape).astype(np.float32))
     check_outputs(gpu.Executor().run(bplan, inputs).outputs, brp.run(inputs).outputs, ctx="bert S=37")
+
+
+SPLIT_ROW_CASES = [
+    # full reduction [N] -> [] / [1]-like, column sums of [N, 1], a handful of long rows, max
+    ('{"name": "full", "inputs": [{"id": "x", "shape": ["N"], "dtype": "f32"}], "outputs": ["r"],'
+     ' "nodes": [{"id": "r", "op": "ReduceSum", "inputs": ["x"], "attrs": {"axes": [0]}}]}', {"N": 3000001}),
+    ('{"name": "col1", "inputs": [{"id": "x", "shape": ["N", "C"], "dtype": "f32"}, {"id": "b", "shape": ["C"]}],'
+     ' "outputs": ["r"], "nodes": [{"id": "bb", "op": "Broadcast", "inputs": ["b"], "attrs": {"shape": ["N", "C"],'
+     ' "broadcast_dims": [1]}}, {"id": "a", "op": "Add", "inputs": ["x", "bb"]},'
+     ' {"id": "t", "op": "Tanh", "inputs": ["a"]}, {"id": "m", "op": "Mul", "inputs": ["t", "x"]},'
+     ' {"id": "r", "op": "ReduceSum", "inputs": ["m"], "attrs": {"axes": [0]}}]}', {"N": 1 << 21, "C": 1}),
+    ('{"name": "rows", "inputs": [{"id": "x", "shape": ["K", "R"], "dtype": "f32"}], "outputs": ["r"],'
+     ' "nodes": [{"id": "e", "op": "Exp", "inputs": ["x"]}, {"id": "r", "op": "ReduceSum", "inputs": ["e"],'
+     ' "attrs": {"axes": [1]}}]}', {"K": 3, "R": 400003}),
+    ('{"name": "rmax", "inputs": [{"id": "x", "shape": ["K", "R"], "dtype": "f32"}], "outputs": ["r"],'
+     ' "nodes": [{"id": "r", "op": "ReduceMax", "inputs": ["x"], "attrs": {"axes": [1]}}]}', {"K": 100, "R": 65536}),
+]
+
+
+@pytest.mark.parametrize("i", range(len(SPLIT_ROW_CASES)))
+def test_few_long_rows_split_across_ctas(gpu, ref, i):
+    """Few long rows without an epilogue run on the column machinery (R split across CTAs,
+    f64 partials joined in order): same results as the reference, and the schedule is not
+    the one-group-per-row kernel."""
+    g, syms = SPLIT_ROW_CASES[i]
+    inputs = ref.make_binding(g, syms, 5)
+    ex = gpu.Executor()
+    got = ex.run(gpu.compile_graph(g), inputs)
+    check_outputs(got.outputs, ref.eval_eager(g, inputs).outputs, ctx=g[:30])
+    scheds = [r["schedule"] for r in ex.launch_records()]
+    assert any(s.startswith("col") for s in scheds), scheds
