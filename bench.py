@@ -981,6 +981,7 @@ def main():
     call_ms = []
     al0 = alloc_stats(D)
     cpu0 = cpu_times()
+    spec0, fused0 = D.lib().disc_cuda_specialized_launches(), D.lib().disc_cuda_fused_launches()
     launches0 = D.kernel_launches()
     barrier(dist, local)
     wall0 = time.perf_counter()
@@ -994,11 +995,13 @@ def main():
     wall = time.perf_counter() - wall0
     al1 = alloc_stats(D)
     cpu1 = cpu_times()
+    spec1, fused1 = D.lib().disc_cuda_specialized_launches(), D.lib().disc_cuda_fused_launches()
     host_diag = {"grouped_calls": len(call_ms), "call_ms_sum": round(sum(call_ms), 2),
                  "call_ms_max": round(max(call_ms), 2) if call_ms else None,
                  "call_ms_p50": round(statistics.median(call_ms), 2) if call_ms else None,
                  "pool_mallocs": al1[0] - al0[0], "pool_frees": al1[1] - al0[1], "oom_retries": al1[2] - al0[2],
-                 "cpu_steal_frac": cpu_steal(cpu0, cpu1)}
+                 "cpu_steal_frac": cpu_steal(cpu0, cpu1),
+                 "fused_launches": fused1 - fused0, "generated_frac": round((spec1 - spec0) / max(1, fused1 - fused0), 4)}
     mal = [b - a for a, b in zip([al0[0]] + call_ms_mallocs[:-1], call_ms_mallocs)]
     slow = sorted(range(len(call_ms)), key=lambda k: -call_ms[k])[:6]
     host_diag["slowest_calls"] = [(k, round(call_ms[k], 1), mal[k]) for k in slow]

@@ -254,6 +254,9 @@ int disc_cuda_pdl_mode(void);
  * the interpreter.  Enabled by default; the counter reports how many launches used one. */
 int disc_cuda_set_specialization(int enabled);
 int64_t disc_cuda_specialized_launches(void);
+/* Fused loop/reduce launches issued (a grouped launch counts its members): with
+ * disc_cuda_specialized_launches, the share that ran generated straight-line code. */
+int64_t disc_cuda_fused_launches(void);
 int disc_cuda_num_specializations(void);
 /* ---- grouped launches and the request queue --------------------------------
  * A grouped launch issues n independent fused launches as ONE kernel per homogeneous

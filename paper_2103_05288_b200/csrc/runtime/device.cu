@@ -56,6 +56,7 @@ thread_local std::string t_err;
 std::atomic<int64_t> g_launches{0};
 std::atomic<int64_t> g_mallocs{0}, g_frees{0}, g_oom_retries{0};  // driver-pool calls (diagnostics)
 std::atomic<int64_t> g_spec_launches{0};
+std::atomic<int64_t> g_fused_launches{0};  // fused launches (grouped: per member), generated or not
 bool g_spec_enabled = true;
 
 // Capture mode (host-only dry run used by the pattern generator): device calls become
@@ -341,6 +342,7 @@ int launch_group(const GroupKey& k, const HostGroup& H, cudaStream_t st) {
   }
   if (rc) return rc;
   g_spec_launches.fetch_add(k.entry ? H.n : 0, std::memory_order_relaxed);
+  g_fused_launches.fetch_add(H.n, std::memory_order_relaxed);
   return 0;
 }
 
@@ -704,6 +706,7 @@ int disc_cuda_launch_loop(const disc_loop_launch* l, void* stream) {
     else if (g_spec_enabled && !l->wide) (void)disc_spec::lookup(0, key);
     return 0;
   }
+  g_fused_launches.fetch_add(1, std::memory_order_relaxed);
   if (g_spec_enabled && !l->wide)
     if (const disc_spec::Entry* e = disc_spec::lookup(0, key)) {
       g_spec_launches.fetch_add(1, std::memory_order_relaxed);
@@ -734,6 +737,7 @@ int disc_cuda_launch_reduce(const disc_reduce_launch* l, void* stream) {
   }
   const disc_spec::Entry* e = (g_spec_enabled && !l->wide && (row || col)) ? disc_spec::lookup(row ? 1 : 2, key) : nullptr;
   if (e) g_spec_launches.fetch_add(1, std::memory_order_relaxed);
+  g_fused_launches.fetch_add(1, std::memory_order_relaxed);
   if (!col) return counted(e ? e->launch(l, l->vec, S(stream), nullptr) : disc_launch::reduce(*l, S(stream)), "launch reduce");
   if (l->K * l->C <= 0) return 0;
   if (l->schedule == DISC_SCHED_COL_ATOMIC) {
@@ -802,6 +806,7 @@ int disc_cuda_set_specialization(int enabled) {
   return 0;
 }
 int64_t disc_cuda_specialized_launches(void) { return g_spec_launches.load(); }
+int64_t disc_cuda_fused_launches(void) { return g_fused_launches.load(); }
 int disc_cuda_num_specializations(void) { return disc_spec::count(); }
 
 int disc_cuda_launch_loop_group(const disc_loop_launch* const* launches, int n, void* stream) {

@@ -474,6 +474,16 @@ const float* neg_inf_ptr() {
 }
 
 // DISC_ARG_CACHE=0 disables the reduce-argument cache (A/B).
+// Shortest rows whose fused epilogue reads the cached reduce argument (DISC_SHORT_ARG_MIN;
+// 32 restores round 1's behaviour: recompute below a warp-width of floats).
+int64_t short_arg_min() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("DISC_SHORT_ARG_MIN");
+    return e ? std::max<int64_t>(2, std::atoll(e)) : int64_t{2};
+  }();
+  return v;
+}
+
 // Few long rows without a fused epilogue run on the column machinery (DISC_SPLIT_ROWS=0: off).
 bool split_rows_enabled() {
   static const bool on = [] {
@@ -1071,9 +1081,11 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     pb.set_fast_div(B.art.tape.size() > 1);
         Lowering lw(B, pb, nullptr, &row);
         // The epilogue reads the reduce argument back from shared memory (written by the
-        // reduce pass) instead of recomputing it; rows up to 4096 keep every cache slot
-        // within 64 KB (never staged: R >= 32).
-        if (arg_cache_enabled() && rarg.kind == TapeRef::Kind::kMember && R.R >= 32 && R.R <= 4096)
+        // reduce pass) instead of recomputing it (softmax: exp once per element); rows up
+        // to 4096 keep every cache slot within 64 KB.  Short rows too (thread per row:
+        // 256 rows x R < 32 floats per slot), where the recompute made the epilogue
+        // issue-bound; such launches are never staged.
+        if (arg_cache_enabled() && rarg.kind == TapeRef::Kind::kMember && R.R >= short_arg_min() && R.R <= 4096)
           lw.substitute(rarg.index, kArgCachePtr);
         for (size_t o = 0; o < art.output_tape_indices.size(); ++o) {
           int t = art.output_tape_indices[o];
@@ -1164,7 +1176,9 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     // block copies its contiguous span of every identity operand through shared memory,
     // one thread per row.  Only when that layout is bank-conflict-free (odd R for scalar
     // rows, odd R/4 for float4 rows); otherwise rows pack 32/G per warp as usual.
-    if (!empty && !R.wide && !R.unaligned && row_policy() >= 2 && R.R >= 16 && R.R < 32 &&
+    bool post_reads_arg = false;
+    for (int q = 0; post_fused && q < R.post.n_loads; ++q) post_reads_arg |= R.post.loads[q].ptr == kArgCachePtr;
+    if (!empty && !R.wide && !R.unaligned && !post_reads_arg && row_policy() >= 2 && R.R >= 16 && R.R < 32 &&
         (R.vec == 1 ? (R.R & 1) : ((R.R / 4) & 1))) {
       int n = 0;
       auto slot_of_ptr = [&](const float* ptr, const disc_program& P) -> int {
