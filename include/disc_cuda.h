@@ -257,6 +257,8 @@ int64_t disc_cuda_specialized_launches(void);
 /* Fused loop/reduce launches issued (a grouped launch counts its members): with
  * disc_cuda_specialized_launches, the share that ran generated straight-line code. */
 int64_t disc_cuda_fused_launches(void);
+/* Profiler capture range (cudaProfilerStart/Stop; ncu --profile-from-start off). */
+int disc_cuda_profiler(int on);
 int disc_cuda_num_specializations(void);
 /* ---- grouped launches and the request queue --------------------------------
  * A grouped launch issues n independent fused launches as ONE kernel per homogeneous

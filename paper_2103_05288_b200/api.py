@@ -109,6 +109,7 @@ def _declare(L: C.CDLL) -> None:
         "disc_cuda_set_specialization": ([i32], i32),
         "disc_cuda_specialized_launches": ([], i64),
         "disc_cuda_fused_launches": ([], i64),
+        "disc_cuda_profiler": ([i32], i32),
         "disc_cuda_num_specializations": ([], i32),
         "disc_cuda_set_capture": ([i32], i32),
         "disc_cuda_capture_records": ([P(vp)], i32),

@@ -17,6 +17,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <cuda_profiler_api.h>
+
 #include "disc_cuda.h"
 #include "../kernels/kernels.cuh"
 #include "../desc_ranges.hpp"
@@ -807,6 +809,10 @@ int disc_cuda_set_specialization(int enabled) {
 }
 int64_t disc_cuda_specialized_launches(void) { return g_spec_launches.load(); }
 int64_t disc_cuda_fused_launches(void) { return g_fused_launches.load(); }
+int disc_cuda_profiler(int on) {
+  if (g_capture) return 0;
+  return check(on ? cudaProfilerStart() : cudaProfilerStop(), "cudaProfiler");
+}
 int disc_cuda_num_specializations(void) { return disc_spec::count(); }
 
 int disc_cuda_launch_loop_group(const disc_loop_launch* const* launches, int n, void* stream) {
