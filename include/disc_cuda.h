@@ -230,6 +230,10 @@ int disc_cuda_launch_concat(const disc_concat_launch* l, void* stream);
 /* C[m,n] = A[m,k] B[k,n], f32 in/out, f64 accumulation (eval_matmul semantics). */
 int disc_cuda_gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c,
                    void* stream);
+/* Same, with the f64 widening workspace supplied by the caller (>= 8*(m*k + k*n + m*n)
+ * bytes, stream-ordered like the operands); ws = NULL allocates it per call. */
+int disc_cuda_gemm_ws(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c, double* ws,
+                      void* stream);
 /* Fills n floats with uniform [lo, hi) (counter-based; bench/test input synthesis). */
 int disc_cuda_fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, void* stream);
 /* Writes `bytes` (>= 2x L2) to a scratch buffer, then reads its first half back, to evict L2
@@ -293,6 +297,9 @@ void* disc_cuda_queue_detach(void);
  * under stream capture (disc_cuda_queue_issue_graph: ops in order, no grouping) and keeps
  * the instantiated graph; graph_exec == nullptr issues the ops directly, no capture. */
 uint64_t disc_cuda_queue_hash(void* queue);
+/* The canonical bytes the hash covers (owned by the queue, valid until it is consumed);
+ * n = 0: not capturable.  Graph caches compare these in full before a replay. */
+int disc_cuda_queue_signature(void* queue, const void** data, size_t* n);
 void disc_cuda_queue_discard(void* queue);
 int disc_cuda_queue_issue_graph(void* queue, void** graph_exec);
 int disc_cuda_graph_launch(void* graph_exec, void* stream);

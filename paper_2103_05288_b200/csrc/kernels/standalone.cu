@@ -246,13 +246,19 @@ Cublas* cublas() {
 
 bool gemm_uses_cublas() { return cublas() != nullptr; }
 
-cudaError_t gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c, cudaStream_t s) {
+// `ws`: f64 workspace of m*k + k*n + m*n doubles (the caller's scratch); null: one
+// stream-ordered allocation, released on every path.
+cudaError_t gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c, double* ws,
+                 cudaStream_t s) {
   if (m <= 0 || n <= 0) return cudaSuccess;
   if (Cublas* cb = cublas(); cb && k > 0 && m < (int64_t{1} << 31) && n < (int64_t{1} << 31) && k < (int64_t{1} << 31)) {
-    double *a64 = nullptr, *b64 = nullptr, *c64 = nullptr;
-    if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&a64), sizeof(double) * m * k, s)) return e;
-    if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&b64), sizeof(double) * k * n, s)) return e;
-    if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&c64), sizeof(double) * m * n, s)) return e;
+    double* own = nullptr;
+    if (!ws) {
+      if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&own), sizeof(double) * (m * k + k * n + m * n), s))
+        return e;
+      ws = own;
+    }
+    double *a64 = ws, *b64 = ws + m * k, *c64 = ws + m * k + k * n;
     k_widen<<<grid_for(m * k, 256, 148 * 16), 256, 0, s>>>(a, a64, m * k);
     k_widen<<<grid_for(k * n, 256, 148 * 16), 256, 0, s>>>(b, b64, k * n);
     // row-major C[m,n] = A[m,k] B[k,n]  ==  column-major C^T = B^T A^T
@@ -262,9 +268,7 @@ cudaError_t gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b
       st = cb->dgemm(cb->handle, 0 /*N*/, 0 /*N*/, static_cast<int>(n), static_cast<int>(m), static_cast<int>(k), &one,
                      b64, static_cast<int>(n), a64, static_cast<int>(k), &zero, c64, static_cast<int>(n));
     k_narrow<<<grid_for(m * n, 256, 148 * 16), 256, 0, s>>>(c64, c, m * n);
-    cudaFreeAsync(a64, s);
-    cudaFreeAsync(b64, s);
-    cudaFreeAsync(c64, s);
+    if (own) cudaFreeAsync(own, s);
     if (st != 0) return cudaErrorUnknown;
     return cudaGetLastError();
   }

@@ -33,7 +33,7 @@ cudaError_t finalize_columns(const disc_reduce_launch& L, cudaStream_t s, const 
 cudaError_t pad(const disc_pad_launch& P, cudaStream_t s);
 cudaError_t concat(const disc_concat_launch& C, cudaStream_t s);
 cudaError_t copy2d_group(const HostGroup& H, cudaStream_t s);
-cudaError_t gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c, cudaStream_t s);
+cudaError_t gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c, double* ws, cudaStream_t s);
 cudaError_t fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, cudaStream_t s);
 cudaError_t flush(void* p, size_t bytes, cudaStream_t s);
 cudaError_t spin(uint64_t ns, cudaStream_t s);
@@ -440,6 +440,7 @@ struct QGemm {
   int64_t m, k, n;
   const float *a, *b;
   float* c;
+  double* ws;
 };
 struct QOp {
   int kind;
@@ -488,6 +489,7 @@ struct Queue {
   std::vector<QRecord> records;
   std::vector<cudaEvent_t> events;  // pool for timing
   size_t next_event = 0;
+  std::string sig;                  // disc_cuda_queue_signature
 };
 thread_local Queue t_q;
 
@@ -769,13 +771,17 @@ int disc_cuda_launch_concat(const disc_concat_launch* l, void* stream) {
   if (g_capture) return 0;
   return counted(disc_launch::concat(*l, S(stream)), "launch concat");
 }
-int disc_cuda_gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c, void* stream) {
+int disc_cuda_gemm_ws(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c, double* ws,
+                      void* stream) {
   if (queued(stream)) {
-    enqueue(kQGemm, QGemm{m, k, n, a, b, c});
+    enqueue(kQGemm, QGemm{m, k, n, a, b, c, ws});
     return 0;
   }
   if (g_capture) return 0;
-  return counted(disc_launch::gemm(m, k, n, a, b, c, S(stream)), "launch gemm");
+  return counted(disc_launch::gemm(m, k, n, a, b, c, ws, S(stream)), "launch gemm");
+}
+int disc_cuda_gemm(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c, void* stream) {
+  return disc_cuda_gemm_ws(m, k, n, a, b, c, nullptr, stream);
 }
 int disc_cuda_fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, void* stream) {
   if (g_capture) return 0;
@@ -1167,7 +1173,7 @@ int flush_queues(const std::vector<Queue*>& qs, int timing) {
           case kQPad: rc = counted(disc_launch::pad(*reinterpret_cast<const disc_pad_launch*>(p), st), "launch pad"); break;
           case kQGemm: {
             const auto& g = *reinterpret_cast<const QGemm*>(p);
-            rc = counted(disc_launch::gemm(g.m, g.k, g.n, g.a, g.b, g.c, st), "launch gemm");
+            rc = counted(disc_launch::gemm(g.m, g.k, g.n, g.a, g.b, g.c, g.ws, st), "launch gemm");
             break;
           }
           case kQMemcpy: {
@@ -1245,31 +1251,62 @@ void* disc_cuda_queue_detach(void) {
 }
 
 // ---- static plans as CUDA graphs ------------------------
-uint64_t disc_cuda_queue_hash(void* queue) {
-  const Queue* q = static_cast<const Queue*>(queue);
-  uint64_t h = 1469598103934665603ull;
-  auto mixb = [&](const void* p, size_t n) {
-    const unsigned char* b = static_cast<const unsigned char*>(p);
-    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
-  };
-  for (const auto& r : q->reqs)
-    for (const QOp& op : r) {
-      mixb(&op.kind, sizeof op.kind);
-      const unsigned char* p = q->arena.data() + op.off;
-      if (op.kind == kQLoop || op.kind == kQReduce) {
-        disc_desc::Range rg[disc_desc::kMaxRanges];
-        const int n = op.kind == kQLoop ? disc_desc::ranges(*reinterpret_cast<const disc_loop_launch*>(p), rg)
-                                        : disc_desc::ranges(*reinterpret_cast<const disc_reduce_launch*>(p), rg);
-        for (int i = 0; i < n; ++i) mixb(p + rg[i].off, rg[i].len);
-      } else {
-        const size_t sz = op.kind == kQPad ? sizeof(disc_pad_launch)
-                          : op.kind == kQConcat ? sizeof(disc_concat_launch)
-                          : op.kind == kQGemm ? sizeof(QGemm)
-                          : op.kind == kQMemcpy ? sizeof(QMemcpy) : sizeof(QMemset);
-        mixb(p, sz);
+// Canonical bytes of a queue's work: per op its kind and the bytes a replay depends on --
+// the used descriptor ranges of fused launches (descriptors are zero-filled when built),
+// the fields (never padding) of copies, memsets and GEMMs.  Empty: not capturable (frees
+// inside the run).  A cached graph is replayed only on an exact match of these bytes.
+int disc_cuda_queue_signature(void* queue, const void** data, size_t* n) {
+  Queue* q = static_cast<Queue*>(queue);
+  std::string& s = q->sig;
+  s.clear();
+  auto put = [&](const void* p, size_t k) { s.append(static_cast<const char*>(p), k); };
+  auto put64 = [&](uint64_t v) { put(&v, sizeof v); };
+  if (q->frees.empty()) {
+    for (const auto& r : q->reqs)
+      for (const QOp& op : r) {
+        put64(static_cast<uint64_t>(op.kind));
+        const unsigned char* p = q->arena.data() + op.off;
+        if (op.kind == kQLoop || op.kind == kQReduce) {
+          disc_desc::Range rg[disc_desc::kMaxRanges];
+          const int k = op.kind == kQLoop ? disc_desc::ranges(*reinterpret_cast<const disc_loop_launch*>(p), rg)
+                                          : disc_desc::ranges(*reinterpret_cast<const disc_reduce_launch*>(p), rg);
+          for (int i = 0; i < k; ++i) put(p + rg[i].off, rg[i].len);
+        } else if (op.kind == kQMemcpy) {
+          const auto& m = *reinterpret_cast<const QMemcpy*>(p);
+          put64(reinterpret_cast<uintptr_t>(m.dst));
+          put64(reinterpret_cast<uintptr_t>(m.src));
+          put64(m.bytes);
+          put64(static_cast<uint64_t>(m.kind));
+        } else if (op.kind == kQMemset) {
+          const auto& m = *reinterpret_cast<const QMemset*>(p);
+          put64(reinterpret_cast<uintptr_t>(m.dst));
+          put64(static_cast<uint64_t>(m.value));
+          put64(m.bytes);
+        } else if (op.kind == kQGemm) {
+          const auto& g = *reinterpret_cast<const QGemm*>(p);
+          put64(g.m), put64(g.k), put64(g.n);
+          put64(reinterpret_cast<uintptr_t>(g.a)), put64(reinterpret_cast<uintptr_t>(g.b));
+          put64(reinterpret_cast<uintptr_t>(g.c));
+          put64(reinterpret_cast<uintptr_t>(g.ws));
+        } else {  // pad / concat descriptors: zero-filled when built (launcher.cpp)
+          put(p, op.kind == kQPad ? sizeof(disc_pad_launch) : sizeof(disc_concat_launch));
+        }
       }
-    }
-  return q->frees.empty() ? h : 0;  // 0: not capturable (frees inside the run)
+  }
+  *data = s.data();
+  *n = s.size();
+  return 0;
+}
+
+uint64_t disc_cuda_queue_hash(void* queue) {
+  const void* d = nullptr;
+  size_t n = 0;
+  disc_cuda_queue_signature(queue, &d, &n);
+  if (!n) return 0;  // not capturable
+  uint64_t h = 1469598103934665603ull;
+  const unsigned char* b = static_cast<const unsigned char*>(d);
+  for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  return h ? h : 1;
 }
 
 void disc_cuda_queue_discard(void* queue) { delete static_cast<Queue*>(queue); }
@@ -1294,7 +1331,7 @@ int disc_cuda_queue_issue_graph(void* queue, void** graph_exec) {
           case kQConcat: rc = disc_cuda_launch_concat(reinterpret_cast<const disc_concat_launch*>(p), st); break;
           case kQGemm: {
             const auto& g = *reinterpret_cast<const QGemm*>(p);
-            rc = disc_cuda_gemm(g.m, g.k, g.n, g.a, g.b, g.c, st);
+            rc = disc_cuda_gemm_ws(g.m, g.k, g.n, g.a, g.b, g.c, g.ws, st);
             break;
           }
           case kQMemcpy: {

@@ -1704,7 +1704,7 @@ LaunchReport launch_kernel(const KernelArtifact& art, const VersionArtifact& ver
 }
 
 void launch_gemm(int64_t m, int64_t k, int64_t n, const DevTensor& a, const DevTensor& b, const OutBuf& c,
-                 void* stream) {
+                 Scratch& scratch, void* stream) {
   if (a.dims.size() != 2 || b.dims.size() != 2) throw RuntimeError("matmul operands must be rank-2");
   if (a.dims[1] != b.dims[0]) throw RuntimeError("matmul inner dim mismatch at runtime");
   if (m * n * 4 > c.capacity_bytes) throw InternalError("kernel output exceeds planned buffer size");
@@ -1713,7 +1713,9 @@ void launch_gemm(int64_t m, int64_t k, int64_t n, const DevTensor& a, const DevT
     cuda_ok(disc_cuda_memset(c.ptr, 0, static_cast<size_t>(m * n * 4), stream), "gemm zero");
     return;
   }
-  cuda_ok(disc_cuda_gemm(m, k, n, a.ptr, b.ptr, c.ptr, stream), "gemm");
+  // f64 widening workspace from the executor's scratch (arena memory, no per-call allocation)
+  double* ws = static_cast<double*>(scratch.alloc(8 * (m * k + k * n + m * n)));
+  cuda_ok(disc_cuda_gemm_ws(m, k, n, a.ptr, b.ptr, c.ptr, ws, stream), "gemm");
 }
 
 }  // namespace disc::rt

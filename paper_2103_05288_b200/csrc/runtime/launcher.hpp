@@ -79,7 +79,7 @@ LaunchReport launch_kernel(const KernelArtifact& art, const VersionArtifact& ver
 
 // Library call (eval_matmul semantics, f64 accumulation).
 void launch_gemm(int64_t m, int64_t k, int64_t n, const DevTensor& a, const DevTensor& b, const OutBuf& c,
-                 void* stream);
+                 Scratch& scratch, void* stream);
 
 // Host-side shape simulation of a tape (exposed for tests): dims of every member.
 std::vector<std::vector<int64_t>> simulate_tape(const KernelArtifact& art, const VersionArtifact& ver,

@@ -770,10 +770,22 @@ void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBindin
   }
   void* q = disc_cuda_queue_detach();
   if (!q) return;
-  const uint64_t h = disc_cuda_queue_hash(q);
+  const void* sig_data = nullptr;
+  size_t sig_n = 0;
+  cuda_ok(disc_cuda_queue_signature(q, &sig_data, &sig_n), "queue signature");
+  std::string h(static_cast<const char*>(sig_data), sig_n);  // empty: not capturable
+  if (!graph_cache_.count(plan_serial) && graph_cache_.size() >= kMaxGraphPlans) {
+    // evict the least recently used plan's graphs (a server compiling many static plans)
+    auto lru = graph_cache_.begin();
+    for (auto it = graph_cache_.begin(); it != graph_cache_.end(); ++it)
+      if (it->second.last_use < lru->second.last_use) lru = it;
+    for (auto& [_, exec] : lru->second.graphs) disc_cuda_graph_destroy(exec);
+    graph_cache_.erase(lru);
+  }
   GraphEntry& g = graph_cache_[plan_serial];
+  g.last_use = ++graph_clock_;
   for (auto& [gh, exec] : g.graphs)
-    if (h && gh == h) {  // same launches, same pointers: replay
+    if (!h.empty() && gh == h) {  // same launches, same pointers (full compare): replay
       disc_cuda_queue_discard(q);
       cuda_ok(disc_cuda_graph_launch(exec, stream_), "graph replay");
       ++graph_replays_;
@@ -781,7 +793,7 @@ void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBindin
       return;
     }
   // capture work seen before (buffer placement can cycle between a few states)
-  const bool repeat = h && std::find(g.seen.begin(), g.seen.end(), h) != g.seen.end();
+  const bool repeat = !h.empty() && std::find(g.seen.begin(), g.seen.end(), h) != g.seen.end();
   if (repeat) {
     void* exec = nullptr;
     cuda_ok(disc_cuda_queue_issue_graph(q, &exec), "graph capture");
@@ -790,13 +802,13 @@ void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBindin
         disc_cuda_graph_destroy(g.graphs.front().second);
         g.graphs.erase(g.graphs.begin());
       }
-      g.graphs.emplace_back(h, exec);
+      g.graphs.emplace_back(std::move(h), exec);
     }
   } else {
     cuda_ok(disc_cuda_queue_issue_graph(q, nullptr), "issue");
-    if (h) {
+    if (!h.empty()) {
       if (g.seen.size() >= 8) g.seen.erase(g.seen.begin());
-      g.seen.push_back(h);
+      g.seen.push_back(std::move(h));
     }
   }
 }
@@ -975,7 +987,7 @@ void DeviceExecutor::run_impl(const CompiledPlan& plan, const std::vector<InputB
         DevTensor a = view(in.arg_bufs[0], {m, k}), b = view(in.arg_bufs[1], {k, n});
         const int ev = timing_ && !grouped_ ? take_event_pair() : -1;
         if (ev >= 0) cuda_ok(disc_cuda_event_record(ev_pool_[ev].first, stream_), "event");
-        launch_gemm(m, k, n, a, b, out_buf(in.out_bufs[0]), stream_);
+        launch_gemm(m, k, n, a, b, out_buf(in.out_bufs[0]), scratch_, stream_);
         if (ev >= 0) cuda_ok(disc_cuda_event_record(ev_pool_[ev].second, stream_), "event");
         stats.library_calls++;
         if (grouped_) {

@@ -261,10 +261,13 @@ class DeviceExecutor {
   void run_impl(const CompiledPlan& plan, const std::vector<InputBinding>& inputs, bool append_records,
                 uint64_t plan_serial);
   struct GraphEntry {
-    std::vector<uint64_t> seen;                      // recent work hashes (capture on a repeat)
-    std::vector<std::pair<uint64_t, void*>> graphs;  // captured graphs by hash (<= 4)
+    std::vector<std::string> seen;                      // recent work signatures (capture on a repeat)
+    std::vector<std::pair<std::string, void*>> graphs;  // captured graphs by exact signature (<= 4)
+    uint64_t last_use = 0;
   };
+  static constexpr size_t kMaxGraphPlans = 64;  // plans with cached graphs per executor (LRU)
   std::map<uint64_t, GraphEntry> graph_cache_;
+  uint64_t graph_clock_ = 0;
   bool graphs_ = true;
   int64_t graph_replays_ = 0;
   // multi-threaded host flow (run_grouped_batch)
