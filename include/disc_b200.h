@@ -53,6 +53,9 @@ int disc_plan_from_json(const char* plan_json, disc_plan* out);
 int disc_plan_to_json(disc_plan p, char** out);
 int disc_plan_check(disc_plan p, char** diagnostics_json);
 void disc_plan_retain(disc_plan p);
+/* Identity of the underlying CompiledPlan: equal for handles the Compiler's cache shared
+ * (codegen.hpp:65-83 returns one shared_ptr per signature). */
+const void* disc_plan_identity(disc_plan p);
 void disc_plan_release(disc_plan p);
 int disc_plan_num_inputs(disc_plan p);
 const char* disc_plan_input_name(disc_plan p, int i);

@@ -101,6 +101,7 @@ def _declare(L: C.CDLL) -> None:
         "disc_executor_set_schedule": ([vp, cp], i32),
         "disc_executor_set_cache_budget": ([vp, i64], i32),
         "disc_executor_reserve": ([vp, i64], i32),
+        "disc_plan_identity": ([vp], vp),
         "disc_executor_run_kernel": ([vp, vp, i32, i32, i32, P(vp), P(vp), P(i32), P(i64), i32], i32),
         "disc_guard_passes": ([vp, i32, i32, P(i64), i32], i32),
         "disc_plan_capture_programs": ([vp, i32, P(cp), P(vp), P(i32), P(vp)], i32),
@@ -206,6 +207,10 @@ class CompiledPlan:
 
     def __init__(self, handle: C.c_void_p):
         self._h = handle
+
+    def identity(self) -> int:
+        """Address of the underlying plan object (shared by Compiler cache hits)."""
+        return lib().disc_plan_identity(self._h) or 0
 
     def __del__(self):
         try:

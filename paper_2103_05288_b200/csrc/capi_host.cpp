@@ -120,6 +120,7 @@ int disc_plan_check(disc_plan p, char** diags) {
 }
 
 void disc_plan_retain(disc_plan p) { p->refs.fetch_add(1); }
+const void* disc_plan_identity(disc_plan p) { return p ? p->plan.get() : nullptr; }
 void disc_plan_release(disc_plan p) {
   if (p && p->refs.fetch_sub(1) == 1) delete p;
 }
