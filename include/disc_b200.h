@@ -199,6 +199,34 @@ int disc_plan_algorithmic_bytes(disc_plan p, int n_inputs, const char* const* na
 /* guard_passes (executor.cpp:78-98) */
 int disc_guard_passes(disc_plan p, int kernel, int version, const int64_t* regs, int n_regs);
 
+/* ---- multi-GPU request dispatcher -------------------------- */
+/* One worker thread per entry of `devices` (a device may repeat), each with its own
+ * executor, stream and host-flow threads (host_threads <= 0: its CPU slice), pinned to a
+ * contiguous slice of the process's CPUs.  A batch is split by greedy LPT on algorithmic
+ * bytes (the rule of dispatch.shard) and each worker runs its share as one grouped call;
+ * no collective touches the data path.  Replaces one Executor::run per request
+ * (executor.cpp:221-465) spread over threads by the caller. */
+typedef struct disc_dispatcher_s* disc_dispatcher;
+int disc_dispatcher_create(int n_workers, const int* devices, int host_threads, disc_dispatcher* out);
+void disc_dispatcher_destroy(disc_dispatcher d);
+int disc_dispatcher_num_workers(disc_dispatcher d);
+int disc_dispatcher_worker_device(disc_dispatcher d, int worker);
+/* Host-only LPT assignment: worker_of[r] for each request (place device inputs with it). */
+int disc_dispatcher_assign(disc_dispatcher d, int n_requests, const disc_plan* plans, const int* input_offsets,
+                           const char* const* names, const int64_t* const* dims, const int* ranks, int* worker_of);
+/* Runs the batch (worker_of = NULL: LPT) and returns when every worker is done.  Inputs are
+ * host pointers (inputs_on_host = 1) or device pointers on the assigned worker's device. */
+int disc_dispatcher_run_grouped(disc_dispatcher d, int n_requests, const disc_plan* plans, const int* input_offsets,
+                                const char* const* names, const void* const* data, const int64_t* const* dims,
+                                const int* ranks, int inputs_on_host, const int* worker_of);
+int disc_dispatcher_request_worker(disc_dispatcher d, int request);
+int disc_dispatcher_num_request_outputs(disc_dispatcher d, int request);
+int disc_dispatcher_request_output(disc_dispatcher d, int request, int i, const float** dptr, const int64_t** dims,
+                                   int* rank, int* device);
+int disc_dispatcher_copy_request_output(disc_dispatcher d, int request, int i, void* dst, int dst_on_host);
+/* Last batch, worker w: requests run, algorithmic bytes, wall ms of its grouped call. */
+int disc_dispatcher_worker_stats(disc_dispatcher d, int worker, int64_t* requests, int64_t* bytes, double* ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -102,6 +102,17 @@ def _declare(L: C.CDLL) -> None:
         "disc_executor_set_cache_budget": ([vp, i64], i32),
         "disc_executor_reserve": ([vp, i64], i32),
         "disc_plan_identity": ([vp], vp),
+        "disc_dispatcher_create": ([i32, P(i32), i32, P(vp)], i32),
+        "disc_dispatcher_destroy": ([vp], None),
+        "disc_dispatcher_num_workers": ([vp], i32),
+        "disc_dispatcher_worker_device": ([vp, i32], i32),
+        "disc_dispatcher_assign": ([vp, i32, P(vp), P(i32), P(cp), P(vp), P(i32), P(i32)], i32),
+        "disc_dispatcher_run_grouped": ([vp, i32, P(vp), P(i32), P(cp), P(vp), P(vp), P(i32), i32, P(i32)], i32),
+        "disc_dispatcher_request_worker": ([vp, i32], i32),
+        "disc_dispatcher_num_request_outputs": ([vp, i32], i32),
+        "disc_dispatcher_request_output": ([vp, i32, i32, P(vp), P(P(i64)), P(i32), P(i32)], i32),
+        "disc_dispatcher_copy_request_output": ([vp, i32, i32, vp, i32], i32),
+        "disc_dispatcher_worker_stats": ([vp, i32, P(i64), P(i64), P(C.c_double)], i32),
         "disc_executor_run_kernel": ([vp, vp, i32, i32, i32, P(vp), P(vp), P(i32), P(i64), i32], i32),
         "disc_guard_passes": ([vp, i32, i32, P(i64), i32], i32),
         "disc_plan_capture_programs": ([vp, i32, P(cp), P(vp), P(i32), P(vp)], i32),

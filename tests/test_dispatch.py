@@ -137,6 +137,18 @@ def test_dispatcher_matches_executor():
     with D.Dispatcher([0]) as disp:
         got = disp.map(work)
         assert disp.assigned == [len(work)]
+    # two native workers sharing the GPU (separate streams, executors, CPU slices): LPT split
+    with D.Dispatcher([0, 0]) as disp2:
+        got2 = disp2.map(work)
+        assert sum(disp2.assigned) == len(work) and min(disp2.assigned) > 0
+        st = disp2.worker_stats()
+        assert sum(w["requests"] for w in st) == len(work)
+        costs = [p.algorithmic_bytes({k: v.shape for k, v in x.items()}) for p, x in work]
+        assert [disp2.worker_of(r) for r in range(len(work))] == [
+            next(w for w, part in enumerate(D.dispatch.shard(costs, 2)) if r in part) for r in range(len(work))]
+    for a_res, b_res in zip(got, got2):
+        for a, b in zip(a_res.outputs, b_res.outputs):
+            np.testing.assert_array_equal(a, b)
     ex = D.Executor()
     for (plan, inputs), r in zip(work, got):
         want = ex.run(plan, inputs).outputs
