@@ -41,6 +41,7 @@ def run(args):
     wl = bench.make_workload(args.workload, 0, args.requests)
     B = bench.Bench(D, a, 0, wl)
     reqs = wl.requests(args.step)
+    B.plans_for(reqs)
     costs = B.costs(reqs)
     pats = {}
     for i, (k, _) in enumerate(reqs):

@@ -8,9 +8,11 @@
 tag=$1
 mkdir -p gpurun_out
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
+if [ -z "$SKIP_LAUNCHES" ]; then
 timeout 1200 ncu --metrics $M --clock-control none --csv --log-file gpurun_out/${tag}_launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --verify off > gpurun_out/${tag}_launches.log 2>&1
 echo "launch list rc=$?"
+fi
 timeout 900 ncu --profile-from-start off --metrics $M --clock-control none --csv --log-file gpurun_out/${tag}_kt.csv \
   python tools/profile_kernels.py run --records gpurun_out/${tag}_kt.json > gpurun_out/${tag}_kt.log 2>&1
 echo "kernel traffic rc=$?"
