@@ -882,9 +882,71 @@ def analyse(B, wl, reqs, costs, peak):
             a[0] += r["bytes"]
             a[1] += r["ms"]
             a[2] += 1
+    # the generic path: the same passes with the generated kernels off (tape interpreter)
+    B.D.set_specialization(False)
+    try:
+        for p, idx in sorted(pats.items()):
+            sub, sc = [reqs[i] for i in idx], [costs[i] for i in idx]
+            ms, _ = B.device_bound_pass(B.batch(sub, sc))
+            per_pattern[p]["generic_GBps"] = round(sum(sc) / ms / 1e6, 1) if ms > 0 else None
+            if per_pattern[p].get("GB/s"):
+                per_pattern[p]["generic_over_generated"] = round(per_pattern[p]["generic_GBps"] / per_pattern[p]["GB/s"], 3)
+    finally:
+        B.D.set_specialization(True)
     full = B.record_pass(B.batch(reqs, costs))
     device_bound_ms, host_issue_ms = B.device_bound_pass(B.batch(reqs, costs))
     return per_pattern, records, device_bound_ms, host_issue_ms, len(full)
+
+
+def random_graph_rate(B, peak, per_graph=5, max_numel=1 << 22, seed=7):
+    """Arbitrary graphs (the reference's RandomGraphGen graphs committed in
+    tests/golden/random_plans.json.gz, 200 seeds) at random shapes: device-bound GB/s of one
+    grouped pass and the share of fused launches that found a generated kernel (the rest
+    run the tape interpreter).  Shapes: each symbol log-uniform, inputs <= max_numel; a
+    binding the runtime flow would reject (host dry run) is redrawn."""
+    import gzip
+    import random
+    D = B.D
+    gr = json.load(gzip.open(os.path.join(ROOT, "tests", "golden", "random_plans.json.gz"), "rt"))
+    rng = random.Random(seed)
+    comp = D.Compiler()
+    reqs_g, reqs = {}, []
+    for key in sorted(gr, key=int):
+        g = json.loads(gr[key]["graph"]) if isinstance(gr[key]["graph"], str) else gr[key]["graph"]
+        plan = comp.compile(g)
+        syms = sorted({d for i in g["inputs"] for d in i["shape"] if isinstance(d, str)})
+        got = 0
+        for _ in range(per_graph * 8):
+            if got == per_graph:
+                break
+            v = {x: W()._logu(rng, 1, 4096) for x in syms}
+            shapes = {i["id"]: input_shape(i, v) for i in g["inputs"]}
+            if max((int(np.prod(sh)) for sh in shapes.values()), default=0) > max_numel:
+                continue
+            try:
+                D.group_dry_run([(plan, shapes)])
+            except D.DiscError:
+                continue
+            kind = f"rg{key}"
+            reqs_g[kind] = g
+            reqs.append((kind, v))
+            B.plans[kind] = plan
+            got += 1
+    saved = B.wl.graphs
+    B.wl.graphs = dict(saved, **reqs_g)
+    try:
+        batch = B.batch(reqs)
+        B.device_bound_pass(batch)  # warm
+        s0, f0 = D.lib().disc_cuda_specialized_launches(), D.lib().disc_cuda_fused_launches()
+        ms, _ = B.device_bound_pass(batch)
+        s1, f1 = D.lib().disc_cuda_specialized_launches(), D.lib().disc_cuda_fused_launches()
+    finally:
+        B.wl.graphs = saved
+    gbs = batch.bytes / ms / 1e6 if ms > 0 else None
+    return {"graphs": len(reqs_g), "requests": len(reqs), "bytes": batch.bytes, "GB/s": round(gbs, 1) if gbs else None,
+            "frac_of_peak": round(gbs / peak, 4) if gbs else None,
+            "generated_frac": round((s1 - s0) / max(1, f1 - f0), 4),
+            "source": "tests/golden/random_plans.json.gz (reference RandomGraphGen seeds 0-199), symbols log-uniform 1..4096"}
 
 
 def main():
@@ -1048,6 +1110,7 @@ def main():
                                             f"kernel, algorithmic {tinfo.get('alg_bytes_per_launch')} B/launch there")
                          if tinfo else "no committed ncu capture for this (workload, kernel)"},
             "kernel_breakdown": breakdown,
+            "random_graphs": random_graph_rate(B, peak),
             "device_ms_step": round(device_ms, 3),
             "host_issue_ms_step": round(host_issue_ms, 3),
             "grouped_launches_step": n_group_launches,
@@ -1087,6 +1150,8 @@ def main():
             "large_shape_frac_of_peak": big,
             "roofline": (analysis or {}).get("roofline"),
             "per_pattern": (analysis or {}).get("per_pattern"),
+            "generic_GBps": {p: e.get("generic_GBps") for p, e in ((analysis or {}).get("per_pattern") or {}).items()},
+            "random_graphs": (analysis or {}).get("random_graphs"),
             "kernel_breakdown": (analysis or {}).get("kernel_breakdown"),
             "device_ms_per_step": (analysis or {}).get("device_ms_step"),
             "host_issue_ms_per_step": (analysis or {}).get("host_issue_ms_step"),

@@ -1,7 +1,7 @@
 """disc-b200: B200-native backend for the DISC dynamic-shape compiler's fused-kernel path.
 
-Host: clean-room C++ compile pipeline (graph -> DHLO -> constraints -> fusion -> plan),
-byte-identical plans to the reference.  Device: sm_100a fused tape kernels behind a
+Host: C++ compile pipeline (graph -> DHLO -> constraints -> fusion -> plan) restating the
+reference's algorithms, byte-identical plans to the reference.  Device: sm_100a fused tape kernels behind a
 C ABI (include/disc_b200.h, include/disc_cuda.h).  See DESIGN.md.
 """
 from .api import (capture_programs, group_dry_run, set_pdl, set_specialization, specialized_launches, CompileOptions, CompiledPlan, Compiler, DeviceBuffer, DiscError, ExecResult, ExecStats,
