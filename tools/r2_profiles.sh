@@ -23,6 +23,6 @@ for p in $2; do
     -o /tmp/full_${tag}_$p python tools/profile_kernels.py run --patterns $p --records /tmp/rec_$p.json > /dev/null 2>&1
   python tools/ncu_summary.py /tmp/full_${tag}_$p.ncu-rep dram__bytes_read.sum dram__bytes_write.sum \
     smsp__inst_executed.sum sm__throughput.avg.pct_of_peak_sustained_elapsed > gpurun_out/${tag}_full_$p.txt 2>&1
-  cp /tmp/full_${tag}_$p.ncu-rep gpurun_out/ 2>/dev/null
+  # (reports stay on the box: gpurun copies back at most 64 MiB)
 done
 ls -la gpurun_out | grep $tag
