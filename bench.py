@@ -303,7 +303,9 @@ class StepBatch:
                 call_ms.append((time.perf_counter() - t0) * 1e3)
                 call_ms_mallocs.append(alloc_stats(self.D)[0])
             if on_chunk is not None:
+                ex.wait_issued()
                 on_chunk(ci, a, b)
+        ex.wait_issued()  # the caller records events / launches on the stream next
 
 
 class Bench:
@@ -320,6 +322,7 @@ class Bench:
         self.ex.set_schedule(args.schedule)
         self.ex.set_host_threads(args.host_threads)
         self.ex.set_cache_budget(int(args.cache_gb * (1 << 30)))
+        self.ex.set_async_flush(bool(getattr(args, "async_flush", 1)))
         if getattr(args, "reserve_gb", 0):
             self.ex.reserve(int(args.reserve_gb * (1 << 30)))
         self.compiler = D.Compiler()
@@ -965,6 +968,8 @@ def main():
     ap.add_argument("--chunk-gb", type=float, default=32.0, help="algorithmic bytes per grouped call")
     ap.add_argument("--arena-gb", type=float, default=48.0)
     ap.add_argument("--cache-gb", type=float, default=32.0, help="executor idle device-memory budget (caches + arena)")
+    ap.add_argument("--async-flush", type=int, default=1, choices=[0, 1],
+                    help="issue grouped launches from a background thread (flows of the next chunk overlap)")
     ap.add_argument("--reserve-gb", type=float, default=64.0, help="executor buffer arena reserved up front")
     ap.add_argument("--e2e-gb", type=float, default=4.0, help="e2e: pinned host input bytes")
     ap.add_argument("--ref-step-s", type=float, default=4.0, help="reference arm: seconds of CPU work per step")
@@ -1144,6 +1149,7 @@ def main():
                        "l2": "flushed before each step (4x L2 write); inputs >> L2",
                        "parallelism": f"request-sharded x{world} (no collectives)",
                        "chunk_gb": args.chunk_gb, "host_threads": args.host_threads, "pdl": args.pdl,
+                       "async_flush": args.async_flush,
                        "schedule": args.schedule},
             "frac_of_hbm_peak": round(value / world / peak, 4),
             "compile_count": compile_count, "recompiles": compile_count - len(wl.graphs),

@@ -171,6 +171,14 @@ int disc_executor_set_cache_budget(disc_executor e, int64_t bytes);
 /* Reserves `bytes` of device memory for the executor's buffer arena now (kept for the
  * executor's lifetime), so a stream of fresh shapes never grows it mid-stream. */
 int disc_executor_reserve(disc_executor e, int64_t bytes);
+/* Asynchronous grouped flush (device inputs, non-timing): disc_executor_run_grouped returns
+ * once the requests' host flows are queued; their grouped launches are issued by a
+ * background thread in call order, so the next call's flows overlap this call's issue.
+ * Outputs (pointers, stats) are known on return; copies, synchronize and other stream work
+ * of the executor wait first.  Call disc_executor_wait_issued before recording your own
+ * events or launching your own work on the executor's stream. */
+int disc_executor_set_async_flush(disc_executor e, int on);
+int disc_executor_wait_issued(disc_executor e);
 
 /* ---- single-kernel entry (run_kernel, executor.cpp:137-219) ------------- */
 /* Runs artifact `kernel` at version `version` on device externals with the given

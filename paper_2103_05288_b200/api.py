@@ -101,6 +101,8 @@ def _declare(L: C.CDLL) -> None:
         "disc_executor_set_schedule": ([vp, cp], i32),
         "disc_executor_set_cache_budget": ([vp, i64], i32),
         "disc_executor_reserve": ([vp, i64], i32),
+        "disc_executor_set_async_flush": ([vp, i32], i32),
+        "disc_executor_wait_issued": ([vp], i32),
         "disc_plan_identity": ([vp], vp),
         "disc_dispatcher_create": ([i32, P(i32), i32, P(vp)], i32),
         "disc_dispatcher_destroy": ([vp], None),
@@ -474,6 +476,12 @@ class Executor:
 
     def set_cache_budget(self, nbytes: int) -> None:
         lib().disc_executor_set_cache_budget(self._h, int(nbytes))
+
+    def set_async_flush(self, on: bool) -> None:
+        _check(lib().disc_executor_set_async_flush(self._h, int(on)))
+
+    def wait_issued(self) -> None:
+        _check(lib().disc_executor_wait_issued(self._h))
 
     def reserve(self, nbytes: int) -> None:
         """Reserves device memory for the buffer arena up front (never released)."""

@@ -145,7 +145,10 @@ int disc_executor_set_graphs(disc_executor e, int on) {
 int64_t disc_executor_graph_replays(disc_executor e) { return e->ex.graph_replays(); }
 
 int disc_executor_set_host_threads(disc_executor e, int n) {
-  return guard([&] { e->ex.set_host_threads(n); });
+  return guard([&] {
+    e->ex.wait_issued();
+    e->ex.set_host_threads(n);
+  });
 }
 
 int disc_executor_num_requests(disc_executor e) { return static_cast<int>(e->ex.request_outputs().size()); }
@@ -166,6 +169,7 @@ int disc_executor_request_output(disc_executor e, int r, int i, const float** dp
 
 int disc_executor_copy_request_output(disc_executor e, int r, int i, void* dst, int dst_on_host) {
   return guard([&] {
+    e->ex.wait_issued();
     const auto& o = e->ex.request_outputs().at(r).at(i);
     int64_t n = 1;
     for (int64_t d : o.dims) n *= d;
@@ -199,6 +203,7 @@ int disc_executor_output(disc_executor e, int i, const float** dptr, const int64
 
 int disc_executor_copy_output(disc_executor e, int i, void* dst, int dst_on_host) {
   return guard([&] {
+    e->ex.wait_issued();
     const auto& o = e->ex.outputs().at(i);
     int64_t n = 1;
     for (int64_t d : o.dims) n *= d;
@@ -212,6 +217,7 @@ int disc_executor_copy_output(disc_executor e, int i, void* dst, int dst_on_host
 
 int disc_executor_synchronize(disc_executor e) {
   return guard([&] {
+    e->ex.wait_issued();
     if (disc_cuda_stream_synchronize(e->ex.stream()) != 0)
       throw RuntimeError(std::string("device error: ") + disc_cuda_last_error());
   });
@@ -264,8 +270,18 @@ int disc_executor_record(disc_executor e, int i, int* instr, int* kernel, int64_
 int64_t disc_executor_algorithmic_bytes(disc_executor e) { return e->ex.algorithmic_bytes(); }
 
 int disc_executor_set_timing(disc_executor e, int enabled) {
-  e->ex.set_timing(enabled != 0);
-  return 0;
+  return guard([&] {
+    e->ex.wait_issued();
+    e->ex.set_timing(enabled != 0);
+  });
+}
+
+int disc_executor_set_async_flush(disc_executor e, int on) {
+  return guard([&] { e->ex.set_async_flush(on != 0); });
+}
+
+int disc_executor_wait_issued(disc_executor e) {
+  return guard([&] { e->ex.wait_issued(); });
 }
 
 int disc_executor_set_schedule(disc_executor e, const char* s) {

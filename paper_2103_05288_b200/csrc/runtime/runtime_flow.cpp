@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <chrono>
 #include <condition_variable>
+#include <deque>
 #include <exception>
 #include <functional>
 #include <mutex>
@@ -406,6 +407,79 @@ struct DeviceExecutor::Pool {
   }
 };
 
+// Background issuer of grouped flushes (set_async_flush): jobs run in submission order.
+struct DeviceExecutor::Flusher {
+  std::thread th;
+  std::mutex mu;
+  std::condition_variable cv, idle;
+  std::deque<std::function<void()>> jobs;
+  int pending = 0;
+  bool stop = false;
+  std::exception_ptr err;
+  explicit Flusher(int device) {
+    th = std::thread([this, device] {
+      disc_cuda_set_device(device);
+      for (;;) {
+        std::function<void()> f;
+        {
+          std::unique_lock<std::mutex> l(mu);
+          cv.wait(l, [&] { return stop || !jobs.empty(); });
+          if (jobs.empty()) return;
+          f = std::move(jobs.front());
+          jobs.pop_front();
+        }
+        try {
+          f();
+        } catch (...) {
+          std::lock_guard<std::mutex> l(mu);
+          if (!err) err = std::current_exception();
+        }
+        std::lock_guard<std::mutex> l(mu);
+        if (--pending == 0) idle.notify_all();
+      }
+    });
+  }
+  void submit(std::function<void()> f) {
+    std::lock_guard<std::mutex> l(mu);
+    jobs.push_back(std::move(f));
+    ++pending;
+    cv.notify_one();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> l(mu);
+    idle.wait(l, [&] { return pending == 0; });
+    if (err) {
+      std::exception_ptr e = err;
+      err = nullptr;
+      std::rethrow_exception(e);
+    }
+  }
+  bool is_idle() {
+    std::lock_guard<std::mutex> l(mu);
+    return pending == 0;
+  }
+  ~Flusher() {
+    {
+      std::lock_guard<std::mutex> l(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    th.join();
+  }
+};
+
+void DeviceExecutor::set_async_flush(bool on) {
+  wait_issued();
+  async_flush_ = on;
+  if (on && !flusher_) flusher_ = std::make_unique<Flusher>(device_);
+}
+
+void DeviceExecutor::wait_issued() {
+  if (flusher_) flusher_->wait();
+}
+
+bool DeviceExecutor::flush_idle() const { return !flusher_ || flusher_->is_idle(); }
+
 void DeviceExecutor::set_host_threads(int n) {
   n = std::max(1, std::min(n, 64));
   if (n == host_threads_) return;
@@ -516,8 +590,14 @@ void DeviceExecutor::run_grouped_batch(int n, const CompiledPlan* const* plans, 
   if (budget_total_ > 0) {
     alloc_.enforce_budget();
     for (auto& x : subs_) x->alloc_.enforce_budget();
-    arena_->release_idle(budget_total_ - budget_total_ / 4);
+    // returning whole regions frees device memory on the stream now: only when no queued
+    // flush (whose kernels may still use them) is pending
+    if (flush_idle()) arena_->release_idle(budget_total_ - budget_total_ / 4);
   }
+  // async flush: device inputs only (host inputs stage through the executor's pinned
+  // chunks, which the next call's flows would overwrite) and never in timing mode
+  const bool async = async_flush_ && !on_host && !timing_;
+  if (!async) wait_issued();
   // session
   begin_grouped();  // resets outputs, records, scratch; defers frees
   req_ids_.clear();
@@ -590,15 +670,27 @@ void DeviceExecutor::run_grouped_batch(int n, const CompiledPlan* const* plans, 
     }
     // merged flush of this phase: this thread's queue + the workers' detached ones
     grouped_ = false;
-    const int src = issue_small_inputs();
     const auto t_flush = Clock::now();
     std::vector<void*> hs;
     for (int w = 1; w < T; ++w)
       if (handles[w]) hs.push_back(handles[w]);
-    const int frc = disc_cuda_queue_flush_detached(hs.data(), static_cast<int>(hs.size()), group_timing_ ? 1 : 0);
-    flush_ms += std::chrono::duration<double, std::milli>(Clock::now() - t_flush).count();
-    if (rc == 0) rc = src ? src : frc;
-    if (rc == 0) append_group_records();
+    if (async) {
+      // issued in the background, in call order; this thread's queue (the first requests)
+      // goes first, as in the synchronous merge
+      if (void* mine = disc_cuda_queue_detach()) hs.insert(hs.begin(), mine);
+      flusher_->submit([hs, capture = disc_cuda_capture_mode()] {
+        disc_cuda_set_capture_local(capture);  // a dry run's flush stays a dry run
+        if (disc_cuda_queue_flush_detached(hs.data(), static_cast<int>(hs.size()), 0) != 0)
+          throw RuntimeError(std::string("grouped launch: ") + disc_cuda_last_error());
+      });
+      flush_ms += std::chrono::duration<double, std::milli>(Clock::now() - t_flush).count();
+    } else {
+      const int src = issue_small_inputs();
+      const int frc = disc_cuda_queue_flush_detached(hs.data(), static_cast<int>(hs.size()), group_timing_ ? 1 : 0);
+      flush_ms += std::chrono::duration<double, std::milli>(Clock::now() - t_flush).count();
+      if (rc == 0) rc = src ? src : frc;
+      if (rc == 0) append_group_records();
+    }
     for (auto& e : perr)
       if (e) errs.push_back(e);
     if (!errs.empty() || rc) break;
@@ -633,6 +725,7 @@ void DeviceExecutor::run_grouped_batch(int n, const CompiledPlan* const* plans, 
 }
 
 void DeviceExecutor::finish_timing() {
+  wait_issued();
   if (!timing_pending_) return;
   timing_pending_ = false;
   if (records_grouped_) {
@@ -663,6 +756,11 @@ void DeviceExecutor::finish_timing() {
 }
 
 DeviceExecutor::~DeviceExecutor() {
+  try {
+    wait_issued();
+  } catch (...) {
+  }
+  flusher_.reset();
   disc_cuda_stream_synchronize(stream_);
   for (auto& [_, g] : graph_cache_)
     for (auto& [h, exec] : g.graphs) disc_cuda_graph_destroy(exec);
@@ -683,6 +781,7 @@ DeviceExecutor::~DeviceExecutor() {
 }
 
 void DeviceExecutor::set_stream(void* s) {
+  wait_issued();
   // Cached blocks and arena ranges are reused in stream order: work of the old stream must
   // be done before the new stream may touch them.
   if (stream_ && s != stream_) disc_cuda_stream_synchronize(stream_);
@@ -734,6 +833,7 @@ const float* DeviceExecutor::stage_input(int slot, const void* host, int64_t byt
 
 void DeviceExecutor::run_kernel(const KernelArtifact& art, const VersionArtifact& ver, const std::vector<DevTensor>& ext,
                                 const std::vector<int64_t>& regs) {
+  wait_issued();
   std::vector<std::vector<int64_t>> ed;
   for (const auto& e : ext) ed.push_back(e.dims);
   auto dims = simulate_tape(art, ver, ed, regs);
@@ -753,6 +853,7 @@ void DeviceExecutor::run_kernel(const KernelArtifact& art, const VersionArtifact
 
 void DeviceExecutor::run(const CompiledPlan& plan, const std::vector<InputBinding>& inputs, bool append_records,
                          uint64_t plan_serial) {
+  if (!grouped_) wait_issued();  // direct launches go behind every queued flush
   static const bool env_on = [] {
     const char* e = std::getenv("DISC_GRAPHS");
     return !e || std::atoi(e) != 0;

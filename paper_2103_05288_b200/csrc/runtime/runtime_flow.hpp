@@ -196,6 +196,13 @@ class DeviceExecutor {
                          const int* ranks, bool on_host);
   void set_host_threads(int n);
   int host_threads() const { return host_threads_; }
+  // Asynchronous flush (grouped calls on device inputs): a call's flows return once queued
+  // and its flushes are issued by a background thread in call order, so the host flows of
+  // the next phase / call overlap the flush of this one.  Stream order = call order, so
+  // every host-side memory reuse stays safe.  Anything that touches the stream from the
+  // caller's thread first waits until all queued flushes are issued (wait_issued).
+  void set_async_flush(bool on);
+  void wait_issued();
   bool grouped() const { return grouped_; }
   const std::vector<std::vector<OutputView>>& request_outputs() const { return req_outputs_; }
   const std::vector<ExecStats>& request_stats() const { return req_stats_; }
@@ -272,6 +279,10 @@ class DeviceExecutor {
   int64_t graph_replays_ = 0;
   // multi-threaded host flow (run_grouped_batch)
   int host_threads_ = 1;
+  struct Flusher;
+  std::unique_ptr<Flusher> flusher_;
+  bool async_flush_ = false;
+  bool flush_idle() const;
   struct Pool;
   std::unique_ptr<Pool> pool_;
   std::vector<std::unique_ptr<DeviceExecutor>> subs_;
