@@ -224,3 +224,35 @@ def test_grouped_mixed_alignment_rows(gpu):
     shapes = [{"S0": b, "S1": s} for s, b in [(64, 50), (255, 40), (1024, 9), (777, 11), (17, 300), (16, 300), (1, 500)]]
     g, plan, reqs = _workload_requests(gpu, "softmax", shapes, 5)
     _assert_same(gpu.Executor().run_grouped(reqs), _sequential(gpu, reqs), "mixed alignment")
+
+
+def test_async_flush_matches_synchronous(gpu):
+    """Grouped calls whose launches are issued by the background flusher (device inputs)
+    give the same bits as synchronous flushes, call after call (memory reused in call
+    order), and ExecStats are unchanged."""
+    from paper_2103_05288_b200 import workloads as W
+    graphs, reqs = W.mixed_stream(600, seed=5)
+    plans = {k: gpu.compile_graph(g) for k, g in graphs.items()}
+    rng = np.random.default_rng(8)
+    batches = []
+    for c in range(3):
+        sub = reqs[c * 200:(c + 1) * 200]
+        batches.append([(plans[k], {i["id"]: gpu.DeviceBuffer.from_numpy(rng.uniform(0.25, 2.0, size=tuple(
+            s[d] if isinstance(d, str) else d for d in i["shape"])).astype(np.float32)) for i in graphs[k]["inputs"]})
+            for k, s in sub])
+    results = {}
+    for mode in (False, True):
+        ex = gpu.Executor()
+        ex.set_host_threads(4)
+        ex.set_async_flush(mode)
+        out = []
+        for b in batches:
+            ex.run_stream(b, grouped=True)
+            out.append((ex.fetch_request_outputs(), [ex.request_stats(r) for r in range(len(b))]))
+        ex.synchronize()
+        results[mode] = out
+    for (oa, sa), (ob, sb) in zip(results[False], results[True]):
+        assert sa == sb
+        for ra, rb in zip(oa, ob):
+            for a, b in zip(ra, rb):
+                np.testing.assert_array_equal(a, b)
