@@ -484,6 +484,15 @@ int64_t short_arg_min() {
   return v;
 }
 
+// Row passes per column-reduce split (DISC_COL_MIN_PASSES; round 1: 8).
+int64_t col_min_passes() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("DISC_COL_MIN_PASSES");
+    return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t{32};
+  }();
+  return v;
+}
+
 // Few long rows without a fused epilogue run on the column machinery (DISC_SPLIT_ROWS=0: off).
 bool split_rows_enabled() {
   static const bool on = [] {
@@ -1267,7 +1276,10 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     const int64_t ctas = R.K * tiles;
     const int64_t rows_per_pass = 8 * (32 / lpc);
     const int64_t want = (int64_t{sm_count()} * 8 + ctas - 1) / ctas;
-    const int64_t max_split = std::max<int64_t>(1, R.R / (rows_per_pass * 8));
+    // each split covers >= col_min_passes() row passes: a CTA's fixed cost (descriptor
+    // staging, the per-column join through shared memory, the partial store) is amortised
+    // over enough rows (grouped launches of many members otherwise run 10^5 tiny CTAs)
+    const int64_t max_split = std::max<int64_t>(1, R.R / (rows_per_pass * col_min_passes()));
     int64_t splits = std::min(want, max_split);
     if (pref == SchedulePref::kTwoPass || pref == SchedulePref::kAtomic) splits = std::max<int64_t>(splits, 2);
     splits = std::min<int64_t>(std::max<int64_t>(splits, 1), 65535);

@@ -41,7 +41,7 @@ def library():
                                    {"S0": 2, "S1": 1}]))
     lib.append(("C2:ln_gelu", W.ln_gelu_graph(), [{"T": 64, "H": 768}, {"T": 1, "H": 1024}, {"T": 7, "H": 4096}]))
     lib.append(("C3:colreduce", W.colreduce_graph(), [{"N": 1000, "C": 36}, {"N": 64, "C": 4096},
-                                                      {"N": 4096, "C": 3}]))
+                                                      {"N": 4096, "C": 3}, {"N": 100000, "C": 1}]))
     lib.append(("C4:bert", W.bert_graph(), [{"R": 96, "S": 8, "T": 8, "H": 768, "F": 3072},
                                             {"R": 12 * 8 * 128, "S": 128, "T": 8 * 128, "H": 768, "F": 3072}]))
     return lib

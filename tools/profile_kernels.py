@@ -78,8 +78,8 @@ def ncu_rows(path):
         v = r[h["Metric Value"]].replace(",", "")
         unit = r[h["Metric Unit"]]
         x = float(v)
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3,
-                 "second": 1e6}.get(unit, 1)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1,
+                 "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(unit, 1)
         ent["m"][r[h["Metric Name"]]] = x * scale
     return [launches[k] for k in sorted(launches)]
 
@@ -92,26 +92,47 @@ def base(name):
 
 def merge(args):
     rec = json.load(open(args.records))
-    rows = [r for r in ncu_rows(args.csv) if base(r["name"]).startswith(KERNEL_PREFIXES)]
-    it = iter(rows)
-    pending = next(it, None)
+    rows = [r for r in ncu_rows(args.csv) if base(r["name"]).startswith(KERNEL_PREFIXES)
+            and not base(r["name"]).startswith("k_col_finalize") or base(r["name"]).startswith("k_col_finalize")]
+    def kinds(sched):
+        """ncu kernel base names a record's grouped launch can have."""
+        s = sched.replace("group:", "")
+        if s == "mixed":
+            return ("k_row_g", "k_row_g_mb", "k_col_g", "k_loop_g")
+        if s.startswith("col"):
+            return ("k_col_g",)
+        if s.startswith("row1_loop") or s.startswith("loop"):
+            return ("k_loop_g",)
+        if s.startswith("row"):
+            return ("k_row_g", "k_row_g_mb")
+        if s.startswith("copy"):
+            return ("k_copy2d_g",)
+        return ()
+    k = 0
     agg = {}
+    unmatched = 0
     for ps in rec["passes"]:
         for r in ps["records"]:
-            if pending is None:
-                raise SystemExit("ncu rows exhausted before the records")
-            dram = pending["m"].get("dram__bytes_read.sum", 0) + pending["m"].get("dram__bytes_write.sum", 0)
-            us = pending["m"].get("gpu__time_duration.sum", 0)
-            pending = next(it, None)
-            while pending is not None and base(pending["name"]).startswith("k_col_finalize"):
-                dram += pending["m"].get("dram__bytes_read.sum", 0) + pending["m"].get("dram__bytes_write.sum", 0)
-                us += pending["m"].get("gpu__time_duration.sum", 0)
-                pending = next(it, None)
+            if k >= len(rows) or base(rows[k]["name"]) not in kinds(r["schedule"]):
+                unmatched += 1  # no kernel for this record (all members empty) or unknown kind
+                continue
+            m = rows[k]["m"]
+            dram = m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
+            us = m.get("gpu__time_duration.sum", 0)
+            k += 1
+            while k < len(rows) and base(rows[k]["name"]).startswith("k_col_finalize"):
+                m = rows[k]["m"]
+                dram += m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
+                us += m.get("gpu__time_duration.sum", 0)
+                k += 1
             a = agg.setdefault(r["key"], {"launches": 0, "dram": 0.0, "alg": 0, "us": 0.0})
             a["launches"] += 1
             a["dram"] += dram
             a["alg"] += r["bytes"]
             a["us"] += us
+    if k != len(rows):
+        raise SystemExit(f"{len(rows) - k} ncu rows left unmatched")
+    print(f"{unmatched} records without a kernel", file=sys.stderr)
     out = json.load(open(args.out)) if os.path.exists(args.out) else {}
     w = {}
     for k, a in sorted(agg.items(), key=lambda kv: -kv[1]["us"]):

@@ -40,17 +40,22 @@ def main():
     ap.add_argument("--bytes", type=float, default=256e6)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--schedule", default="auto")
+    ap.add_argument("--copies-gb", type=float, default=0.0,
+                    help="run each shape as a grouped batch of copies totalling this many GB (grouped rates)")
     a = ap.parse_args()
     import paper_2103_05288_b200 as D
     D.lib()
     var, vals = a.values.split("=")
     vals = [int(x) for x in vals.split(",")]
-    args = types.SimpleNamespace(schedule=a.schedule, host_threads=1, cache_gb=32.0, arena_gb=16.0, chunk_gb=32.0,
-                                 reserve_gb=0)
+    args = types.SimpleNamespace(schedule=a.schedule, host_threads=8, cache_gb=32.0, arena_gb=16.0, chunk_gb=32.0,
+                                 reserve_gb=0, async_flush=0)
     wl = bench.make_workload("sweep", 0, 10)
     B = bench.Bench(D, args, 0, wl)
     for syms in shapes(a.kind, var, vals, a.bytes):
         reqs = [(a.kind, syms)]
+        if a.copies_gb:
+            one = B.costs(B.plans_for(reqs) and reqs)[0]
+            reqs = reqs * max(1, int(a.copies_gb * 1e9 / max(one, 1)))
         batch = B.batch(reqs)
         B.record_pass(batch)
         best = None
@@ -62,7 +67,7 @@ def main():
         tot, recs = best
         ks = " ".join(f"k{r['kernel']}:{r['schedule'].replace('group:', '')}={r['bytes'] / r['ms'] / 1e6:.0f}"
                       for r in recs if r["ms"] > 0)
-        print(f"{a.kind} {var}={syms.get(var)} {syms}: {batch.bytes / 1e6:.0f} MB {tot * 1e3:.1f} us "
+        print(f"{a.kind} {var}={syms.get(var)} x{len(reqs)} {syms}: {batch.bytes / 1e6:.0f} MB {tot * 1e3:.1f} us "
               f"{batch.bytes / tot / 1e6:.0f} GB/s  [{ks}]", flush=True)
     B.close()
 
