@@ -410,7 +410,7 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
       }
       for (int l = 0; l < L.post.n_loads; ++l) {
         const int k = L.post.cache_slot[l];
-        if (k >= 0 && !((pre_slots >> k) & 1)) {
+        if (k >= 0 && k != L.arg_slot && !((pre_slots >> k) & 1)) {  // the arg slot is written, not copied
           pre_slots |= 1u << k;
           copy_span(cache0 + k * slot_stride, L.post.loads[l].ptr + base * L.R, n_el, false);
         }
@@ -475,7 +475,7 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
       }
     } else if (valid) {
       // reduce-argument cache (fused epilogue reads the pre value back from smem)
-      float* const arg_cache = (!STAGED && L.arg_slot >= 0 && row_cache) ? row_cache + L.arg_slot * sst : nullptr;
+      float* const arg_cache = (L.arg_slot >= 0 && row_cache) ? row_cache + L.arg_slot * sst : nullptr;
       for (I col0 = h + static_cast<I>(lane) * VEC; col0 < Rb; col0 += span) {
         const int nv = chunks_in_row<CH>(Rb - col0, cstride);
         T v[CH];

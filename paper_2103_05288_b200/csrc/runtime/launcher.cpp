@@ -493,6 +493,23 @@ int64_t col_min_passes() {
   return v;
 }
 
+// Short rows staged through shared memory from this width (DISC_STAGE_MIN; round 1: 16),
+// scalar rows of even width too (DISC_STAGE_EVEN=0: odd widths only, as round 1).
+int64_t stage_min() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("DISC_STAGE_MIN");
+    return e ? std::max<int64_t>(2, std::atoll(e)) : int64_t{2};
+  }();
+  return v;
+}
+bool stage_even() {
+  static const bool on = [] {
+    const char* e = std::getenv("DISC_STAGE_EVEN");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 // Few long rows without a fused epilogue run on the column machinery (DISC_SPLIT_ROWS=0: off).
 bool split_rows_enabled() {
   static const bool on = [] {
@@ -1185,10 +1202,11 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     // block copies its contiguous span of every identity operand through shared memory,
     // one thread per row.  Only when that layout is bank-conflict-free (odd R for scalar
     // rows, odd R/4 for float4 rows); otherwise rows pack 32/G per warp as usual.
-    bool post_reads_arg = false;
-    for (int q = 0; post_fused && q < R.post.n_loads; ++q) post_reads_arg |= R.post.loads[q].ptr == kArgCachePtr;
-    if (!empty && !R.wide && !R.unaligned && !post_reads_arg && row_policy() >= 2 && R.R >= 16 && R.R < 32 &&
-        (R.vec == 1 ? (R.R & 1) : ((R.R / 4) & 1))) {
+    // Staged short rows (stage_min() <= R < 32): scalar rows of any width (odd R is
+    // bank-conflict-free, even R 2-way), float4 rows when R/4 is odd.  The cached reduce
+    // argument is one more slot.
+    if (!empty && !R.wide && !R.unaligned && row_policy() >= 2 && R.R >= stage_min() && R.R < 32 &&
+        (R.vec == 1 ? ((R.R & 1) || stage_even()) : ((R.R / 4) & 1))) {
       int n = 0;
       auto slot_of_ptr = [&](const float* ptr, const disc_program& P) -> int {
         for (int l = 0; l < P.n_loads; ++l)
@@ -1211,9 +1229,13 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
       for (int o = 0; o < R.pre.n_outs; ++o) R.pre.out_slot[o] = static_cast<int8_t>(n++);
       if (post_fused)
         for (int o = 0; o < R.post.n_outs; ++o) R.post.out_slot[o] = static_cast<int8_t>(n++);
+      int arg = -1;
+      for (int q = 0; post_fused && q < R.post.n_loads; ++q)
+        if (R.post.loads[q].ptr == kArgCachePtr) arg = R.post.cache_slot[q];
       const int64_t slot_bytes = (256 * R.R + 3) / 4 * 4 * 4;
       if (n > 0 && n <= 8 && n * slot_bytes <= 112 * 1024) {
         R.stage = 1;
+        R.arg_slot = arg;  // the reduce pass writes it, the epilogue reads it (never copied in)
         R.cache_loads = n;
         R.pre.cache_mode = DISC_CACHE_READ;
         R.post.cache_mode = DISC_CACHE_READ;
