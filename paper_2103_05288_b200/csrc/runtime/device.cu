@@ -1262,6 +1262,7 @@ int disc_cuda_queue_signature(void* queue, const void** data, size_t* n) {
   auto put = [&](const void* p, size_t k) { s.append(static_cast<const char*>(p), k); };
   auto put64 = [&](uint64_t v) { put(&v, sizeof v); };
   if (q->frees.empty()) {
+    s.push_back('G');  // capturable (also with no ops: an empty graph)
     for (const auto& r : q->reqs)
       for (const QOp& op : r) {
         put64(static_cast<uint64_t>(op.kind));

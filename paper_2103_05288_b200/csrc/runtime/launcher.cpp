@@ -493,12 +493,14 @@ int64_t col_min_passes() {
   return v;
 }
 
-// Short rows staged through shared memory from this width (DISC_STAGE_MIN; round 1: 16),
-// scalar rows of even width too (DISC_STAGE_EVEN=0: odd widths only, as round 1).
+// Short rows staged through shared memory from this width (DISC_STAGE_MIN; round 1: 16).
+// Default 32 = off: on B200 the staged kernel lost at every width (grouped, 4 GB per
+// shape: S=2 2864 -> 1759, S=7 3072 -> 2426, S=20 vs S=24 unstaged 2677 vs 4968 GB/s).
+// Scalar rows of even width too when on (DISC_STAGE_EVEN=0: odd widths only).
 int64_t stage_min() {
   static const int64_t v = [] {
     const char* e = std::getenv("DISC_STAGE_MIN");
-    return e ? std::max<int64_t>(2, std::atoll(e)) : int64_t{2};
+    return e ? std::max<int64_t>(2, std::atoll(e)) : int64_t{32};  // A/B r2s: staging loses at every width
   }();
   return v;
 }
