@@ -165,6 +165,12 @@ typedef struct {
    * float4 body from its first 16 B-aligned column plus a scalar head and tail; row-cache
    * rows are padded to R + 3 and shifted so the body stays aligned in shared memory */
   int32_t unaligned;
+  /* COL, K == 1, C % 4 != 0: rows folded by `fold` into super rows of C = fold * fold_cout
+   * floats (R = full super rows); the finalize joins super-columns c, c + fold_cout, ...
+   * into output c.  fold_tail: rows of a last, partial super row (N mod fold). */
+  int32_t fold;
+  int32_t fold_tail;
+  int64_t fold_cout;
 } disc_reduce_launch;
 
 /* Standalone pad (eval_pad, kernels.cpp:125-147), output-driven gather. */

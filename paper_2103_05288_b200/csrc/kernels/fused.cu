@@ -29,21 +29,36 @@ __device__ __host__ inline int finalize_lanes(int splits) {
   return l;
 }
 
+// Outputs of a column launch: K*C, or K*fold_cout when folded (fold super-columns each).
+__device__ __host__ inline int64_t col_outputs(const disc_reduce_launch& L) {
+  return L.fold > 1 ? L.K * L.fold_cout : L.K * L.C;
+}
+
 __device__ __forceinline__ void finalize_body(const disc_reduce_launch& L, const int bx, const int gx) {
   __shared__ double part[256];
   pdl_enter(L.pre);
-  const int64_t n = L.K * L.C;
-  const int lpo = finalize_lanes(L.splits), opb = 256 / lpo;
+  const int64_t nws = L.K * L.C;  // workspace columns per split
+  const int64_t n = col_outputs(L);
+  const int F = L.fold > 1 ? L.fold : 1;
+  const int64_t cout = F > 1 ? L.fold_cout : 0;
+  const int lpo = finalize_lanes(L.splits * F), opb = 256 / lpo;
   const int ox = threadIdx.x / lpo, sl = threadIdx.x % lpo;
   for (int64_t base = static_cast<int64_t>(bx) * opb; base < n; base += static_cast<int64_t>(gx) * opb) {
     const int64_t o = base + ox;
-    if (L.schedule != DISC_SCHED_COL_TWOPASS) {
-      if (sl == 0 && o < n) L.red_out[o] = static_cast<float>(L.workspace[o]);
+    if (L.schedule != DISC_SCHED_COL_TWOPASS) {  // atomic: one f64 sum per (super-)column
+      if (sl == 0 && o < n) {
+        double t = L.workspace[o];
+        for (int j = 1; j < F; ++j) t = red_join(L.kind, t, L.workspace[o + j * cout]);
+        L.red_out[o] = static_cast<float>(t);
+      }
       continue;
     }
     double t = red_identity(L.kind);
     if (o < n)
-      for (int s = sl; s < L.splits; s += lpo) t = red_join(L.kind, t, L.workspace[static_cast<int64_t>(s) * n + o]);
+      for (int e = sl; e < L.splits * F; e += lpo) {  // (split, fold) pairs in a fixed order
+        const int s = e / F, j = e - s * F;
+        t = red_join(L.kind, t, L.workspace[static_cast<int64_t>(s) * nws + o + j * cout]);
+      }
     part[threadIdx.x] = t;
     __syncthreads();
     for (int w = lpo / 2; w > 0; w >>= 1) {
@@ -200,8 +215,8 @@ cudaError_t loop(const disc_loop_launch& L, cudaStream_t s, const HostGroup* g) 
 cudaError_t col_pass(const disc_reduce_launch& L, cudaStream_t s, const HostGroup* g);
 
 inline int64_t finalize_blocks(const disc_reduce_launch& L) {
-  const int64_t n = L.K * L.C;
-  const int64_t opb = 256 / finalize_lanes(L.splits);
+  const int64_t n = col_outputs(L);
+  const int64_t opb = 256 / finalize_lanes(L.splits * (L.fold > 1 ? L.fold : 1));
   const int64_t want = (n + opb - 1) / opb;
   return want < sm_count() * 8 ? want : sm_count() * 8;
 }

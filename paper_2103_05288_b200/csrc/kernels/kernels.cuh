@@ -466,7 +466,7 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
           if (L.arg_slot >= 0 && row_cache) {
 #pragma unroll
             for (int c = 0; c < CH; ++c)
-              if (c < nv) *reinterpret_cast<T*>(row_cache + L.arg_slot * sst + col0 + c * cstride) = v[c];
+              if (c < nv) st_cache(row_cache + L.arg_slot * sst + col0 + c * cstride, v[c]);
           }
           cur = nxt;
           col0 = ncol;
@@ -494,7 +494,7 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
         if (arg_cache) {
 #pragma unroll
           for (int c = 0; c < CH; ++c)
-            if (c < nv) *reinterpret_cast<T*>(arg_cache + col0 + c * cstride) = v[c];
+            if (c < nv) st_cache(arg_cache + col0 + c * cstride, v[c]);
         }
       }
       if constexpr (UNAL && VEC == 4 && !STAGED) {
@@ -505,7 +505,7 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
             Pre::template run<1, 1, WIDE>(L.pre, Tile<I, false>{row, c, R, 1, 1, row_cache, sst}, vs,
                                           reinterpret_cast<float*>(slots), blockDim.x * 4, consts[0], 0.f);
             part[0] = PA::add(part[0], vs[0]);
-            if (arg_cache) arg_cache[c] = vs[0];
+            if (arg_cache) st_cache(arg_cache + c, vs[0]);
           }
         }
       }
@@ -646,6 +646,21 @@ __device__ __forceinline__ void col_body(const disc_reduce_launch& L, const int 
 #pragma unroll
       for (int c = 0; c < CH; ++c)
         if (c < nv) add(v[c]);
+    }
+    // folded launch (L.fold > 1, K == 1): the partial last super row -- its first
+    // fold_tail * fold_cout columns are real rows -- evaluated element by element, once per
+    // column (the first row slot of warp 0), in the last split
+    if (L.fold > 1 && L.fold_tail > 0 && by == L.splits - 1 && warp == 0 && sub == 0) {
+      const int64_t lim = static_cast<int64_t>(L.fold_tail) * L.fold_cout;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j)
+        if (col0 + j < lim) {
+          float vs[1];
+          Pre::template run<1, 1, WIDE>(
+              L.pre, Tile<I, false, true>{static_cast<I>(L.R), static_cast<I>(col0 + j), static_cast<I>(L.C), 1, 1},
+              vs, reinterpret_cast<float*>(smem_raw) + tid, kColThreads, consts, 0.f);
+          acc[j] = PA::add(acc[j], vs[0]);
+        }
     }
   }
 #pragma unroll

@@ -147,6 +147,49 @@ __device__ __forceinline__ int64_t gather_index(const disc_load& L, int64_t f) {
 
 __device__ __forceinline__ float ldg(const float* p) { return __ldg(p); }
 
+// Stores (and cache reads) the compiler cannot see as memory writes (asm volatile, no
+// memory clobber).  Grouped kernels read their launch descriptor from shared memory; a
+// plain store through a generic pointer may alias it, so every descriptor field used in
+// a loop was re-read (LDS) after each output / row-cache store -- ~10 extra instructions
+// per element in short-row kernels.  These accesses never touch the descriptor (outputs
+// are global, caches are the dynamic shared-memory slots), and volatile asm keeps their
+// order among themselves; __syncthreads() orders them against everything else.
+#ifndef DISC_NC_STORES
+#define DISC_NC_STORES 1
+#endif
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void st_out(float* p, float v) {
+  if constexpr (DISC_NC_STORES) asm volatile("st.global.f32 [%0], %1;" ::"l"(p), "f"(v));
+  else *p = v;
+}
+__device__ __forceinline__ void st_out(float* p, float4 v) {
+  if constexpr (DISC_NC_STORES)
+    asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w));
+  else *reinterpret_cast<float4*>(p) = v;
+}
+__device__ __forceinline__ void st_cache(float* p, float v) {
+  if constexpr (DISC_NC_STORES) asm volatile("st.shared.f32 [%0], %1;" ::"r"(smem_addr(p)), "f"(v));
+  else *p = v;
+}
+__device__ __forceinline__ void st_cache(float* p, float4 v) {
+  if constexpr (DISC_NC_STORES)
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(smem_addr(p)), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w));
+  else *reinterpret_cast<float4*>(p) = v;
+}
+__device__ __forceinline__ void ld_cache(const float* p, float& v) {
+  if constexpr (DISC_NC_STORES) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_addr(p)));
+  else v = *p;
+}
+__device__ __forceinline__ void ld_cache(const float* p, float4& v) {
+  if constexpr (DISC_NC_STORES)
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(smem_addr(p)));
+  else v = *reinterpret_cast<const float4*>(p);
+}
+
 // A tile: CH chunks of VEC elements.  Column tiles (ROWS = false): chunk c at
 // (row, col0 + c*cstride) -- cstride = warp/group width * VEC keeps every access
 // coalesced.  Row tiles (ROWS = true, column reductions): chunk c at (row + c*cstride,
@@ -179,10 +222,7 @@ __device__ __forceinline__ bool cached_load(const disc_program& P, const Ctx& t,
   const float* c0 = t.cache + P.cache_slot[l] * t.slot_stride + t.col0;
 #pragma unroll
   for (int c = 0; c < CH; ++c)
-    if (t.has(c)) {
-      if constexpr (VEC == 1) v[c] = c0[c * t.cstride];
-      else v[c] = *reinterpret_cast<const float4*>(c0 + c * t.cstride);
-    }
+    if (t.has(c)) ld_cache(c0 + c * t.cstride, v[c]);
   return true;
 }
 
@@ -193,10 +233,7 @@ __device__ __forceinline__ void cache_fill(const disc_program& P, const Ctx& t, 
   float* c0 = t.cache + P.cache_slot[l] * t.slot_stride + t.col0;
 #pragma unroll
   for (int c = 0; c < CH; ++c)
-    if (t.has(c)) {
-      if constexpr (VEC == 1) c0[c * t.cstride] = v[c];
-      else *reinterpret_cast<float4*>(c0 + c * t.cstride) = v[c];
-    }
+    if (t.has(c)) st_cache(c0 + c * t.cstride, v[c]);
 }
 
 template <int VEC>
@@ -361,10 +398,7 @@ __device__ __forceinline__ void store_tile(float* out, const Ctx& t, const typen
   const auto step = t.step();
 #pragma unroll
   for (int c = 0; c < CH; ++c)
-    if (t.has(c)) {
-      if constexpr (VEC == 1) o[c * step] = v[c];
-      else *reinterpret_cast<float4*>(o + c * step) = v[c];
-    }
+    if (t.has(c)) st_out(o + c * step, v[c]);
 }
 
 // Output o of a tile: its shared-memory slot in a staged launch, else global memory.
@@ -376,10 +410,7 @@ __device__ __forceinline__ void store_out(const disc_program& P, int o, const Ct
       float* s0 = t.cache + P.out_slot[o] * t.slot_stride + t.col0;
 #pragma unroll
       for (int c = 0; c < CH; ++c)
-        if (t.has(c)) {
-          if constexpr (VEC == 1) s0[c * t.cstride] = v[c];
-          else *reinterpret_cast<float4*>(s0 + c * t.cstride) = v[c];
-        }
+        if (t.has(c)) st_cache(s0 + c * t.cstride, v[c]);
       return;
     }
   }

@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <numeric>
 #include <mutex>
 #include <unordered_set>
 #include <tuple>
@@ -507,6 +508,15 @@ int64_t stage_min() {
 bool stage_even() {
   static const bool on = [] {
     const char* e = std::getenv("DISC_STAGE_EVEN");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+// Column reduces with C % 4 != 0 fold rows into float4-wide super rows (DISC_COL_FOLD=0: off).
+bool fold_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DISC_COL_FOLD");
     return !e || std::atoi(e) != 0;
   }();
   return on;
@@ -1186,8 +1196,61 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     R.g_mask = geo.mask;
     for (int d = 0; d < geo.rank; ++d) R.g_dims[d] = geo.gdims[d];
   } else {
-    bind_view(pre, R.C);
-    R.vec = choose_vec({&pre}, R.C);
+    // Column reduce of [N, C] with C % 4 != 0: fold f = 4 / gcd(C, 4) rows into super rows
+    // of f*C floats (a multiple of 4), so the column kernel runs 128-bit loads instead of
+    // scalar ones; the finalize sums super-columns c, c + C, ... per output.  Operands must
+    // be identity (flat index preserved) or constants, or column broadcasts [N, C] with
+    // row stride 0, which read a tiled copy (f repeats of the C values, built by a small
+    // loop launch).  The last N mod f rows form a partial super row (kernel tail).
+    int64_t fold = 1;
+    std::vector<int> tiled;
+    if (fold_enabled() && R.K == 1 && R.C % 4 != 0 && R.R >= 64 && !empty) {
+      const int64_t f = 4 / std::gcd<int64_t>(R.C, 4);
+      bool ok = true;
+      for (size_t l = 0; l < pre.maps.size() && ok; ++l) {
+        const Map& c = pre.maps[l];
+        if (is_identity(c) || is_const_map(c)) continue;
+        if (c.dims.size() == 2 && c.dims[1] == R.C && c.strides[0] == 0) {
+          tiled.push_back(static_cast<int>(l));
+          continue;
+        }
+        ok = false;
+      }
+      if (ok) fold = f;
+    }
+    if (fold > 1) {
+      const int64_t C0 = R.C, N0 = R.R;
+      R.fold = static_cast<int32_t>(fold);
+      R.fold_cout = C0;
+      R.fold_tail = static_cast<int32_t>(N0 % fold);
+      R.R = N0 / fold;
+      R.C = fold * C0;
+      std::vector<float*> tiles;
+      for (int l : tiled) {  // tile[j*C + c] = src(c), j < f
+        ProgramBuilder tb;
+        const Map& c = pre.maps[l];
+        float* t = static_cast<float*>(issue.scratch(4 * R.C));
+        tb.output(tb.load(pre.prog.loads[l].ptr, canonical(Map{{fold, C0}, {0, c.strides[1]}, c.offset})), t);
+        Built tbb = tb.finish(-1);
+        issue.loop(make_loop(tbb, R.C));
+        rep.device_kernels += 1;
+        tiles.push_back(t);
+      }
+      bind_view(pre, R.C);
+      for (size_t i = 0; i < tiled.size(); ++i) {  // the tiled copy, affine over the folded view
+        disc_load& Ld = pre.prog.loads[tiled[i]];
+        std::memset(&Ld, 0, sizeof Ld);
+        Ld.ptr = tiles[i];
+        Ld.mode = DISC_LOAD_AFFINE;
+        Ld.rs = 0;
+        Ld.cs = 1;
+        pre.prog.code[pre.load_pc[tiled[i]]].op = DISC_I_LOAD_AFF;
+      }
+      R.vec = choose_vec({&pre}, R.C);
+    } else {
+      bind_view(pre, R.C);
+      R.vec = choose_vec({&pre}, R.C);
+    }
   }
   R.pre = pre.prog;
   R.post = post.prog;
@@ -1308,25 +1371,27 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     if (pref == SchedulePref::kTwoPass || pref == SchedulePref::kAtomic) splits = std::max<int64_t>(splits, 2);
     splits = std::min<int64_t>(std::max<int64_t>(splits, 1), 65535);
     R.splits = static_cast<int32_t>(splits);
-    if (splits == 1) {
+    const int64_t nws = R.K * R.C;  // workspace columns (folded: f per output)
+    if (splits == 1 && R.fold <= 1) {
       R.schedule = DISC_SCHED_COL_SINGLE;
       rep.schedule = "col_single";
     } else if (pref == SchedulePref::kAtomic && R.kind == DISC_REDUCE_SUM) {
       R.schedule = DISC_SCHED_COL_ATOMIC;
-      R.workspace = static_cast<double*>(issue.scratch(8 * nout));
+      R.workspace = static_cast<double*>(issue.scratch(8 * nws));
       rep.schedule = "col_atomic";
     } else {
-      R.schedule = DISC_SCHED_COL_TWOPASS;
-      R.workspace = static_cast<double*>(issue.scratch(8 * nout * splits));
+      R.schedule = DISC_SCHED_COL_TWOPASS;  // folded launches always finalize (the fold)
+      R.workspace = static_cast<double*>(issue.scratch(8 * nws * splits));
       rep.schedule = "col_twopass";
     }
+    if (R.fold > 1) rep.schedule += "_fold";
   } else {
     if (!R.red_out) R.red_out = static_cast<float*>(issue.scratch(nout * 4));
     rep.schedule = "generic";
   }
 
   issue.reduce(R);
-  rep.device_kernels = (R.schedule == DISC_SCHED_COL_TWOPASS || R.schedule == DISC_SCHED_COL_ATOMIC) ? 2 : 1;
+  rep.device_kernels += (R.schedule == DISC_SCHED_COL_TWOPASS || R.schedule == DISC_SCHED_COL_ATOMIC) ? 2 : 1;
   if (post_pass) {
     issue.loop(PL);
     rep.device_kernels += 1;

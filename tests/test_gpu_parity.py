@@ -494,3 +494,34 @@ def test_few_long_rows_split_across_ctas(gpu, ref, i):
     check_outputs(got.outputs, ref.eval_eager(g, inputs).outputs, ctx=g[:30])
     scheds = [r["schedule"] for r in ex.launch_records()]
     assert any(s.startswith("col") for s in scheds), scheds
+
+
+COLRED = ('{"name": "colred", "inputs": [{"id": "x", "shape": ["N", "C"], "dtype": "f32"}, {"id": "b", "shape": ["C"]}],'
+          ' "outputs": ["r"], "nodes": [{"id": "bb", "op": "Broadcast", "inputs": ["b"], "attrs": {"shape": ["N", "C"],'
+          ' "broadcast_dims": [1]}}, {"id": "a", "op": "Add", "inputs": ["x", "bb"]},'
+          ' {"id": "t", "op": "Tanh", "inputs": ["a"]}, {"id": "m", "op": "Mul", "inputs": ["t", "x"]},'
+          ' {"id": "r", "op": "ReduceSum", "inputs": ["m"], "attrs": {"axes": [0]}}]}')
+COLMAX = ('{"name": "colmax", "inputs": [{"id": "x", "shape": ["N", "C"], "dtype": "f32"}], "outputs": ["r"],'
+          ' "nodes": [{"id": "e", "op": "Exp", "inputs": ["x"]}, {"id": "r", "op": "ReduceMax", "inputs": ["e"],'
+          ' "attrs": {"axes": [0]}}]}')
+
+
+@pytest.mark.parametrize("g", [COLRED, COLMAX])
+@pytest.mark.parametrize("schedule", ["auto", "atomic"])
+def test_folded_column_reduce(gpu, ref, g, schedule):
+    """Column reduces with C % 4 != 0 fold 2 or 4 rows into float4 super rows (tiled bias,
+    partial last super row, folded finalize): every N mod f tail and both finalize forms
+    against the reference executor."""
+    ex = gpu.Executor()
+    ex.set_schedule(schedule)
+    plan = gpu.compile_graph(g)
+    if schedule == "atomic" and "ReduceMax" in g:
+        pytest.skip("atomic schedules are sum-only")
+    seen = set()
+    for c in (1, 2, 3, 5, 6, 7, 33, 130):
+        for n in (64, 65, 66, 67, 1001, 40003):
+            inputs = ref.make_binding(g, {"N": n, "C": c}, n + c)
+            got = ex.run(plan, inputs)
+            check_outputs(got.outputs, ref.eval_eager(g, inputs).outputs, ctx=f"C={c} N={n}")
+            seen |= {r["schedule"] for r in ex.launch_records()}
+    assert any("fold" in s for s in seen), seen
