@@ -595,12 +595,14 @@ __device__ __forceinline__ void col_body(const disc_reduce_launch& L, const int 
   pdl_enter(L.pre);
   hoist_consts(L.pre, consts);
   __syncthreads();
-  const int lpc = L.group;
-  const int rpw = 32 / lpc;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int sub = lane / lpc, lc = lane & (lpc - 1);
-  const int rows_per_pass = (kColThreads / 32) * rpw;
-  const int64_t span = static_cast<int64_t>(lpc) * VEC;
+  // Q = L.group lanes per row segment (any 1..256): thread tid takes column chunk tid % Q
+  // of row slot tid / Q, so a warp reads consecutive chunks across row boundaries (one
+  // contiguous span when the tile is the whole row); the 256 % Q leftover threads idle.
+  const int Q = L.group;
+  const int rows_per_pass = kColThreads / Q;
+  const int sub = tid / Q, lc = tid - sub * Q;
+  const int warp = sub < rows_per_pass ? 0 : 1;  // 1: an idle leftover thread
+  const int64_t span = static_cast<int64_t>(Q) * VEC;
   const int64_t tiles = (L.C + span - 1) / span;
   const int64_t k = bx / tiles;
   const int64_t tile0 = (bx - k * tiles) * span;
@@ -623,9 +625,9 @@ __device__ __forceinline__ void col_body(const disc_reduce_launch& L, const int 
       acc[3] = PA::add(acc[3], v.w);
     }
   };
-  if (col0 < L.C) {
+  if (col0 < L.C && warp == 0) {
     const int64_t step = static_cast<int64_t>(rows_per_pass) * CH;
-    int64_t r = r0 + warp * rpw + sub;
+    int64_t r = r0 + sub;
     // full steps: all CH rows inside [r0, r1)
     for (; r + (CH - 1) * rows_per_pass < r1; r += step) {
       T v[CH];
@@ -672,8 +674,7 @@ __device__ __forceinline__ void col_body(const disc_reduce_launch& L, const int 
     if (col >= L.C) continue;
     const int jl = j / VEC, e = j % VEC;
     Acc s = RD::identity();
-    for (int w = 0; w < kColThreads / 32; ++w)
-      for (int u = 0; u < rpw; ++u) s = RD::join(s, part[w * 32 + u * lpc + jl][e]);
+    for (int u = 0; u < rows_per_pass; ++u) s = RD::join(s, part[u * Q + jl][e]);  // row slots in order
     const int64_t o = k * L.C + col;
     switch (L.schedule) {
       case DISC_SCHED_COL_SINGLE:

@@ -489,7 +489,7 @@ int64_t short_arg_min() {
 int64_t col_min_passes() {
   static const int64_t v = [] {
     const char* e = std::getenv("DISC_COL_MIN_PASSES");
-    return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t{32};
+    return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t{128};  // A/B r2r: 8/32 -> 128: +10% large
   }();
   return v;
 }
@@ -509,6 +509,14 @@ bool stage_even() {
   static const bool on = [] {
     const char* e = std::getenv("DISC_STAGE_EVEN");
     return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+bool col_pow2() {
+  static const bool on = [] {
+    const char* e = std::getenv("DISC_COL_POW2");
+    return e && std::atoi(e) != 0;
   }();
   return on;
 }
@@ -1352,16 +1360,24 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
                            : post_fused ? (R.cache_loads ? "row_fused_cached" : "row_fused") : "row";
   } else if (R.schedule != DISC_SCHED_GENERIC) {
     if (!R.red_out) R.red_out = static_cast<float*>(issue.scratch(nout * 4));
-    // Lanes per row segment: one VEC-wide column group each, up to a warp (each thread
-    // keeps its columns and walks rows; narrow C packs 32/lpc rows per warp).
+    // Q lanes per row segment, one VEC-wide column chunk each (each thread keeps its
+    // columns and walks rows): the whole row when it has <= 256 chunks (256/Q rows per
+    // pass, consecutive threads on consecutive chunks across rows), else equal tiles of
+    // <= 256 chunks.  Round 1 used a power of two <= 32 (C = 33 floats: a second tile with
+    // one busy lane of 32).  DISC_COL_POW2=1 restores it.
     const int64_t cchunks = (R.C + R.vec - 1) / R.vec;
-    int lpc = 1;
-    while (lpc < cchunks && lpc < 32) lpc <<= 1;
-    R.group = lpc;
-    const int64_t span = int64_t{lpc} * R.vec;
+    int Q = 1;
+    if (col_pow2()) {
+      while (Q < cchunks && Q < 32) Q <<= 1;
+    } else {
+      const int64_t ntile = (cchunks + 255) / 256;
+      Q = static_cast<int>(std::max<int64_t>(1, (cchunks + ntile - 1) / ntile));
+    }
+    R.group = Q;
+    const int64_t span = int64_t{Q} * R.vec;
     const int64_t tiles = (R.C + span - 1) / span;
     const int64_t ctas = R.K * tiles;
-    const int64_t rows_per_pass = 8 * (32 / lpc);
+    const int64_t rows_per_pass = 256 / Q;
     const int64_t want = (int64_t{sm_count()} * 8 + ctas - 1) / ctas;
     // each split covers >= col_min_passes() row passes: a CTA's fixed cost (descriptor
     // staging, the per-column join through shared memory, the partial store) is amortised
