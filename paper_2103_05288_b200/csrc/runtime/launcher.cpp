@@ -1367,9 +1367,12 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     // one busy lane of 32).  DISC_COL_POW2=1 restores it.
     const int64_t cchunks = (R.C + R.vec - 1) / R.vec;
     int Q = 1;
-    if (col_pow2()) {
-      while (Q < cchunks && Q < 32) Q <<= 1;
-    } else {
+    while (Q < cchunks && Q < 32) Q <<= 1;
+    // pow2 tiles of 32 chunks stay when they waste < 10% (A/B r2v: C = 1000, 4096 3.99-4.14
+    // vs 3.80-3.85 TB/s with one 250-chunk row per pass); narrow and badly tiled rows use
+    // Q = their chunk count (C = 12: 3197 -> 4062, C = 33 folded: 2265 -> 3701 GB/s)
+    const double pow2_eff = double(cchunks) / double(((cchunks + Q - 1) / Q) * Q);
+    if (!col_pow2() && (cchunks < 32 || pow2_eff < 0.9)) {
       const int64_t ntile = (cchunks + 255) / 256;
       Q = static_cast<int>(std::max<int64_t>(1, (cchunks + ntile - 1) / ntile));
     }
