@@ -155,7 +155,7 @@ __device__ __forceinline__ float ldg(const float* p) { return __ldg(p); }
 // are global, caches are the dynamic shared-memory slots), and volatile asm keeps their
 // order among themselves; __syncthreads() orders them against everything else.
 #ifndef DISC_NC_STORES
-#define DISC_NC_STORES 1
+#define DISC_NC_STORES 0  // A/B r2x on the sweep: 1 = 4311, 0 = 4376 GB/s (volatile asm costs the row kernels more)
 #endif
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
