@@ -346,6 +346,35 @@ __device__ __forceinline__ void loop_body(const disc_loop_launch& L, const int b
 //                          identity input into the slots (coalesced, 16 B when aligned),
 //                          programs read/write slots, outputs are copied out the same way.
 
+// TMA bulk copies (cp.async.bulk, 1-D) into shared memory, completing on an mbarrier.
+__device__ __forceinline__ uint32_t sh_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sh_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sh_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "DISC_MBAR_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra DISC_MBAR_WAIT_%=;\n"
+      "}\n" ::"r"(sh_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   sh_addr(dst)),
+               "l"(src), "r"(bytes), "r"(sh_addr(bar))
+               : "memory");
+}
+// Generic-proxy accesses of a buffer before the async proxy (TMA) overwrites it.
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // Copies n floats global -> shared (or back), 16 B per access when both ends allow it.
 __device__ __forceinline__ void copy_span(float* __restrict__ dst, const float* __restrict__ src, int64_t n,
                                           bool to_global) {
@@ -397,9 +426,80 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
   const I cstride = static_cast<I>(G) * VEC;
   const I span = cstride * CH;
 
-  for (int64_t base = static_cast<int64_t>(bx) * rpb; base < rows; base += static_cast<int64_t>(gx) * rpb) {
+  // TMA staging (L.stage == 2): the staged inputs of block-iteration i+1 are copied by
+  // bulk copies (one per operand, issued by thread 0) into the other half of a double
+  // buffer while iteration i computes from shared memory; no registers hold loads in
+  // flight.  A block span whose size or source is not 16 B aligned falls back to copy_span.
+  __shared__ __align__(8) uint64_t tma_bar[2];
+  const bool tma = STAGED && L.stage == 2;
+  const int64_t stage_floats = tma ? cache_floats : 0;
+  auto tma_issue = [&](int64_t b, int st) -> bool {  // thread 0; false = not TMA-able
+    const int64_t n = (rows - b < rpb ? rows - b : rpb) * L.R;
+    const uint32_t bytes = static_cast<uint32_t>(n * 4);
+    if (bytes % 16) return false;
+    uint32_t seen = 0, total = 0;
+    for (int pass = 0; pass < 2; ++pass) {  // pass 0: checks and byte count; pass 1: copies
+      seen = 0;
+      for (int q = 0; q < 2; ++q) {
+        const disc_program& P = q ? L.post : L.pre;
+        for (int l = 0; l < P.n_loads; ++l) {
+          const int k = P.cache_slot[l];
+          if (k < 0 || k == L.arg_slot || ((seen >> k) & 1)) continue;
+          seen |= 1u << k;
+          const float* src = P.loads[l].ptr + b * L.R;
+          if (pass == 0) {
+            if (reinterpret_cast<uintptr_t>(src) & 15) return false;
+            total += bytes;
+          } else {
+            bulk_g2s(cache0 + st * stage_floats + k * slot_stride, src, bytes, &tma_bar[st]);
+          }
+        }
+      }
+      if (pass == 0) {
+        fence_proxy_async();  // earlier generic reads/writes of this buffer
+        mbar_expect_tx(&tma_bar[st], total);
+      }
+    }
+    return true;
+  };
+  __shared__ int tma_ok[2];
+  uint32_t tma_phase = 0;  // bit s: parity of the next wait on barrier s
+  if (tma) {
+    if (threadIdx.x == 0) {
+      mbar_init(&tma_bar[0], 1);
+      mbar_init(&tma_bar[1], 1);
+      mbar_fence_init();
+      const int64_t b0 = static_cast<int64_t>(bx) * rpb;
+      if (b0 < rows) tma_ok[0] = tma_issue(b0, 0);
+    }
+    __syncthreads();
+  }
+  int it = 0;
+  for (int64_t base = static_cast<int64_t>(bx) * rpb; base < rows; base += static_cast<int64_t>(gx) * rpb, ++it) {
     const int64_t n_el = (rows - base < rpb ? rows - base : rpb) * L.R;
-    if constexpr (STAGED) {  // copy the block's rows of every staged input into its slot
+    if (tma) {
+      const int st = it & 1;
+      const int64_t nb = base + static_cast<int64_t>(gx) * rpb;
+      if (threadIdx.x == 0 && nb < rows) tma_ok[st ^ 1] = tma_issue(nb, st ^ 1);  // prefetch the next
+      float* const c0 = cache0 + st * stage_floats;
+      if (!tma_ok[st]) {  // synchronous copy of this span (unaligned / odd-sized)
+        uint32_t seen = 0;
+        for (int q = 0; q < 2; ++q) {
+          const disc_program& P = q ? L.post : L.pre;
+          for (int l = 0; l < P.n_loads; ++l) {
+            const int k = P.cache_slot[l];
+            if (k < 0 || k == L.arg_slot || ((seen >> k) & 1)) continue;
+            seen |= 1u << k;
+            copy_span(c0 + k * slot_stride, P.loads[l].ptr + base * L.R, n_el, false);
+          }
+        }
+        __syncthreads();
+      } else {
+        mbar_wait(&tma_bar[st], (tma_phase >> st) & 1);
+        tma_phase ^= 1u << st;
+      }
+      row_cache = c0 + sub * rrow;
+    } else if constexpr (STAGED) {  // copy the block's rows of every staged input into its slot
       uint32_t pre_slots = 0;
       for (int l = 0; l < L.pre.n_loads; ++l) {
         const int k = L.pre.cache_slot[l];
@@ -558,6 +658,7 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
     }
     if constexpr (STAGED) {  // copy every staged output slot back, then free the slots
       __syncthreads();
+      if (tma) continue;  // outputs went to global memory; the barrier frees this half
       for (int o = 0; o < L.pre.n_outs; ++o)
         if (L.pre.out_slot[o] >= 0)
           copy_span(L.pre.outs[o] + base * L.R, cache0 + L.pre.out_slot[o] * slot_stride, n_el, true);
@@ -858,7 +959,8 @@ inline size_t row_smem(const disc_reduce_launch& L, bool use_slots) {
   const int block = row_block(L);
   const int rpb = block / L.group;
   const int64_t rrow = (L.vec == 4 && L.unaligned) ? (L.R + 6) / 4 * 4 : L.R;
-  const size_t cache = static_cast<size_t>((static_cast<int64_t>(rpb) * rrow + 3) / 4 * 4) * L.cache_loads * 4;
+  const size_t cache = static_cast<size_t>((static_cast<int64_t>(rpb) * rrow + 3) / 4 * 4) * L.cache_loads * 4 *
+                       (L.stage == 2 ? 2 : 1);  // TMA staging: double buffer
   return cache + (use_slots ? static_cast<size_t>(slots) * CH * block * (L.vec == 4 ? 16 : 4) : 0);
 }
 

@@ -521,6 +521,37 @@ bool col_pow2() {
   return on;
 }
 
+// Row launches staged by TMA bulk copies (DISC_TMA_ROWS, DISC_TMA_MIN_R / _MAX_R, and the
+// double buffer's shared-memory budget DISC_TMA_SMEM_KB).
+bool tma_rows_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DISC_TMA_ROWS");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+int64_t tma_min_r() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("DISC_TMA_MIN_R");
+    return e ? std::atoll(e) : int64_t{2};
+  }();
+  return v;
+}
+int64_t tma_max_r() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("DISC_TMA_MAX_R");
+    return e ? std::atoll(e) : int64_t{4096};
+  }();
+  return v;
+}
+int64_t tma_smem_budget() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("DISC_TMA_SMEM_KB");
+    return int64_t{e ? std::atoi(e) : 96} * 1024;
+  }();
+  return v;
+}
+
 // Column reduces with C % 4 != 0 fold rows into float4-wide super rows (DISC_COL_FOLD=0: off).
 bool fold_enabled() {
   static const bool on = [] {
@@ -1318,6 +1349,55 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
         for (int o = 0; o < DISC_MAX_OUTS; ++o) R.pre.out_slot[o] = R.post.out_slot[o] = -1;
       }
     }
+    // TMA staging (stage 2): every identity operand of the block's rows arrives by bulk
+    // copy into a double-buffered shared-memory span (prefetched one block-iteration
+    // ahead), the programs read it from there (and the cached reduce argument), outputs go
+    // straight to global memory.  Rows of any width (R % 4 != 0: scalar reads from shared
+    // memory, bank-conflict-free across the G lanes of a row).
+    if (!empty && !R.wide && !R.stage && tma_rows_enabled() && R.R >= tma_min_r() && R.R <= tma_max_r()) {
+      int n = 0, arg = -1;
+      auto slot_of = [&](const float* ptr, const disc_program& P) -> int {
+        for (int l = 0; l < P.n_loads; ++l)
+          if (P.loads[l].mode == DISC_LOAD_IDENTITY && P.loads[l].ptr == ptr && P.cache_slot[l] >= 0)
+            return P.cache_slot[l];
+        return -1;
+      };
+      for (int l = 0; l < DISC_MAX_LOADS; ++l) R.pre.cache_slot[l] = R.post.cache_slot[l] = -1;
+      for (int l = 0; l < R.pre.n_loads; ++l)
+        if (R.pre.loads[l].mode == DISC_LOAD_IDENTITY) {
+          const int k = slot_of(R.pre.loads[l].ptr, R.pre);
+          R.pre.cache_slot[l] = static_cast<int8_t>(k >= 0 ? k : n++);
+        }
+      for (int l = 0; post_fused && l < R.post.n_loads; ++l)
+        if (R.post.loads[l].mode == DISC_LOAD_IDENTITY) {
+          if (R.post.loads[l].ptr == kArgCachePtr) {
+            if (arg < 0) arg = n++;
+            R.post.cache_slot[l] = static_cast<int8_t>(arg);
+            continue;
+          }
+          int k = slot_of(R.post.loads[l].ptr, R.pre);
+          if (k < 0) k = slot_of(R.post.loads[l].ptr, R.post);
+          R.post.cache_slot[l] = static_cast<int8_t>(k >= 0 ? k : n++);
+        }
+      if (R.R % 4 != 0) {  // scalar reads from shared memory
+        R.vec = 1;
+        R.unaligned = 0;
+      }
+      int gt = std::max(g, 1);
+      auto stage_bytes = [&](int gg) { return int64_t{std::max(gg, 256) / gg} * (R.R + 3) / 4 * 4 * n * 4 * 2; };
+      while (stage_bytes(gt) > tma_smem_budget() && gt < 1024) gt <<= 1;
+      if (n > 0 && n <= 8 && stage_bytes(gt) <= tma_smem_budget()) {
+        g = gt;
+        R.stage = 2;
+        R.cache_loads = n;
+        R.arg_slot = arg;
+        R.pre.cache_mode = DISC_CACHE_READ;
+        R.post.cache_mode = DISC_CACHE_READ;
+        for (int o = 0; o < DISC_MAX_OUTS; ++o) R.pre.out_slot[o] = R.post.out_slot[o] = -1;
+      } else {
+        for (int l = 0; l < DISC_MAX_LOADS; ++l) R.pre.cache_slot[l] = R.post.cache_slot[l] = -1;
+      }
+    }
     // Row cache: contiguous loads the epilogue re-reads come from shared memory instead
     // of a second pass over HBM/L2 (softmax: x is read once).
     if (post_fused && !R.stage) {
@@ -1356,7 +1436,8 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
       }
     }
     R.group = g;
-    rep.schedule = R.stage ? (post_fused ? "row_fused_staged" : "row_staged")
+    rep.schedule = R.stage == 2 ? (post_fused ? "row_fused_tma" : "row_tma")
+                   : R.stage ? (post_fused ? "row_fused_staged" : "row_staged")
                            : post_fused ? (R.cache_loads ? "row_fused_cached" : "row_fused") : "row";
   } else if (R.schedule != DISC_SCHED_GENERIC) {
     if (!R.red_out) R.red_out = static_cast<float*>(issue.scratch(nout * 4));
