@@ -186,6 +186,21 @@ int resident_ctas(const void* kernel, int block, size_t smem) {
   return n;
 }
 
+bool sum_row_mb() {
+  static const bool on = [] {
+    const char* e = std::getenv("DISC_SUM_ROW_MB");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+bool col_mb() {
+  static const bool on = [] {
+    const char* e = std::getenv("DISC_COL_MB");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 cudaError_t raise_smem_limit(const void* kernel, size_t bytes) {
   static std::mutex mu;
   static std::unordered_map<OccKey, size_t, OccKeyHash> limit;  // (device, kernel) -> attribute set

@@ -833,6 +833,21 @@ __global__ void __launch_bounds__(256, 6) k_row_g_mb(const __grid_constant__ dis
                                                                    G.block_off[g + 1] - G.block_off[g]);
 }
 
+// Sum rows at <= 256 threads capped at 6 resident blocks (<= 40 registers) -- A/B knob
+// DISC_SUM_ROW_MB (the fused softmax epilogue runs at 64 registers, 50% occupancy).
+template <int VEC, bool WIDE, typename Pre, typename Post, int CH, bool STAGED, bool UNAL>
+__global__ void __launch_bounds__(256, 6) k_row_smb(const __grid_constant__ disc_reduce_launch L) {
+  row_body<VEC, WIDE, DISC_REDUCE_SUM, Pre, Post, CH, STAGED, UNAL>(L, blockIdx.x, gridDim.x);
+}
+template <int VEC, bool WIDE, typename Pre, typename Post, int CH, bool STAGED, bool UNAL>
+__global__ void __launch_bounds__(256, 6) k_row_g_smb(const __grid_constant__ disc_group G) {
+  __shared__ __align__(16) unsigned char desc[desc_bytes<disc_reduce_launch>()];
+  const int b = blockIdx.x, g = group_of(G, b);
+  const disc_reduce_launch& L = group_stage<disc_reduce_launch>(G, g, desc);
+  row_body<VEC, WIDE, DISC_REDUCE_SUM, Pre, Post, CH, STAGED, UNAL>(L, b - G.block_off[g],
+                                                                   G.block_off[g + 1] - G.block_off[g]);
+}
+
 template <int VEC, bool WIDE, int KIND, typename Pre, int CH = kCH>
 __global__ void __launch_bounds__(kColThreads, 4) k_col(const __grid_constant__ disc_reduce_launch L) {
   col_body<VEC, WIDE, KIND, Pre, CH>(L, blockIdx.x, blockIdx.y);
@@ -840,6 +855,17 @@ __global__ void __launch_bounds__(kColThreads, 4) k_col(const __grid_constant__ 
 // Grouped column pass: launch g's 2-D grid (K * col tiles, splits) is flattened x-major.
 template <int VEC, bool WIDE, int KIND, typename Pre, int CH = kCH>
 __global__ void __launch_bounds__(kColThreads, 4) k_col_g(const __grid_constant__ disc_group G) {
+  __shared__ __align__(16) unsigned char desc[desc_bytes<disc_reduce_launch>()];
+  const int b = blockIdx.x, g = group_of(G, b);
+  const disc_reduce_launch& L = group_stage<disc_reduce_launch>(G, g, desc);
+  const int local = b - G.block_off[g];
+  const int64_t span = static_cast<int64_t>(L.group) * L.vec;
+  const int gx = static_cast<int>(L.K * ((L.C + span - 1) / span));
+  col_body<VEC, WIDE, KIND, Pre, CH>(L, local % gx, local / gx);
+}
+// The same at 6 resident blocks (<= 40 registers) -- A/B knob DISC_COL_MB.
+template <int VEC, bool WIDE, int KIND, typename Pre, int CH = kCH>
+__global__ void __launch_bounds__(kColThreads, 6) k_col_g_mb(const __grid_constant__ disc_group G) {
   __shared__ __align__(16) unsigned char desc[desc_bytes<disc_reduce_launch>()];
   const int b = blockIdx.x, g = group_of(G, b);
   const disc_reduce_launch& L = group_stage<disc_reduce_launch>(G, g, desc);
@@ -1099,6 +1125,20 @@ inline cudaError_t loop_pass(const disc_loop_launch& L, cudaStream_t s, bool use
                     : launch_loop_with<C1>(k_loop<1, false, Prog, C1>, L, s, use_slots);
 }
 
+bool sum_row_mb();  // DISC_SUM_ROW_MB (fused.cu)
+bool col_mb();      // DISC_COL_MB
+
+template <int V, bool W, typename Pre, typename Post, int C, bool ST, bool U>
+inline void (*sum_row_kernel(const disc_reduce_launch& L))(disc_reduce_launch) {
+  if (sum_row_mb() && row_block(L) <= 256) return k_row_smb<V, W, Pre, Post, C, ST, U>;
+  return k_row<V, W, DISC_REDUCE_SUM, Pre, Post, C, ST, U>;
+}
+template <int V, bool W, typename Pre, typename Post, int C, bool ST, bool U>
+inline void (*sum_row_group_kernel(const HostGroup& H))(disc_group) {
+  if (sum_row_mb() && row_block(H.at<disc_reduce_launch>(0)) <= 256) return k_row_g_smb<V, W, Pre, Post, C, ST, U>;
+  return k_row_g<V, W, DISC_REDUCE_SUM, Pre, Post, C, ST, U>;
+}
+
 // Max-reduce row kernel for a launch (k_row_mb when the pattern asks for it and the
 // launch's block is <= 256 threads).
 template <int V, bool W, typename Pre, typename Post, int C, bool ST, bool U>
@@ -1122,9 +1162,9 @@ inline cudaError_t row_pass(const disc_reduce_launch& L, cudaStream_t s, bool us
   const bool sum = L.kind == DISC_REDUCE_SUM;
   constexpr int C1 = vec1_ch(CH);
 #define DISC_ROW_U(V, W, ST, C, U)                                                                           \
-  (g ? (sum ? launch_row_group<C>(k_row_g<V, W, DISC_REDUCE_SUM, Pre, Post, C, ST, U>, *g, s, use_slots)     \
+  (g ? (sum ? launch_row_group<C>(sum_row_group_kernel<V, W, Pre, Post, C, ST, U>(*g), *g, s, use_slots)     \
             : launch_row_group<C>(max_row_group_kernel<V, W, Pre, Post, C, ST, U>(*g), *g, s, use_slots))    \
-     : (sum ? launch_row_with<C>(k_row<V, W, DISC_REDUCE_SUM, Pre, Post, C, ST, U>, L, s, use_slots)         \
+     : (sum ? launch_row_with<C>(sum_row_kernel<V, W, Pre, Post, C, ST, U>(L), L, s, use_slots)         \
             : launch_row_with<C>(max_row_kernel<V, W, Pre, Post, C, ST, U>(L), L, s, use_slots)))
 #define DISC_ROW(V, W, ST, C) DISC_ROW_U(V, W, ST, C, false)
   if constexpr (ALLOW_WIDE)
@@ -1141,8 +1181,11 @@ template <typename Pre, int CH = kCH, bool ALLOW_WIDE = true>
 inline cudaError_t col_pass_t(const disc_reduce_launch& L, cudaStream_t s, bool use_slots, const HostGroup* g = nullptr) {
   const bool sum = L.kind == DISC_REDUCE_SUM;
   if (g) {
-#define DISC_COLG(V, W) (sum ? launch_col_group<CH>(k_col_g<V, W, DISC_REDUCE_SUM, Pre, CH>, *g, s, use_slots) \
-                             : launch_col_group<CH>(k_col_g<V, W, DISC_REDUCE_MAX, Pre, CH>, *g, s, use_slots))
+#define DISC_COLG(V, W)                                                                                   \
+  (sum ? launch_col_group<CH>(col_mb() ? k_col_g_mb<V, W, DISC_REDUCE_SUM, Pre, CH> : k_col_g<V, W, DISC_REDUCE_SUM, Pre, CH>, \
+                              *g, s, use_slots)                                                           \
+       : launch_col_group<CH>(col_mb() ? k_col_g_mb<V, W, DISC_REDUCE_MAX, Pre, CH> : k_col_g<V, W, DISC_REDUCE_MAX, Pre, CH>, \
+                              *g, s, use_slots))
     if constexpr (ALLOW_WIDE)
       if (L.wide) return L.vec == 4 ? DISC_COLG(4, true) : DISC_COLG(1, true);
     return L.vec == 4 ? DISC_COLG(4, false) : DISC_COLG(1, false);
