@@ -171,6 +171,9 @@ typedef struct {
   int32_t fold;
   int32_t fold_tail;
   int64_t fold_cout;
+  /* ROW sum with <= 256 threads: 1 = the register-capped kernel (6 resident blocks) */
+  int32_t regcap;
+  int32_t pad2;
 } disc_reduce_launch;
 
 /* Standalone pad (eval_pad, kernels.cpp:125-147), output-driven gather. */

@@ -186,13 +186,6 @@ int resident_ctas(const void* kernel, int block, size_t smem) {
   return n;
 }
 
-bool sum_row_mb() {
-  static const bool on = [] {
-    const char* e = std::getenv("DISC_SUM_ROW_MB");
-    return e && std::atoi(e) != 0;
-  }();
-  return on;
-}
 bool col_mb() {
   static const bool on = [] {
     const char* e = std::getenv("DISC_COL_MB");

@@ -1125,17 +1125,17 @@ inline cudaError_t loop_pass(const disc_loop_launch& L, cudaStream_t s, bool use
                     : launch_loop_with<C1>(k_loop<1, false, Prog, C1>, L, s, use_slots);
 }
 
-bool sum_row_mb();  // DISC_SUM_ROW_MB (fused.cu)
-bool col_mb();      // DISC_COL_MB
+bool col_mb();  // DISC_COL_MB (fused.cu)
 
 template <int V, bool W, typename Pre, typename Post, int C, bool ST, bool U>
 inline void (*sum_row_kernel(const disc_reduce_launch& L))(disc_reduce_launch) {
-  if (sum_row_mb() && row_block(L) <= 256) return k_row_smb<V, W, Pre, Post, C, ST, U>;
+  if (L.regcap && row_block(L) <= 256) return k_row_smb<V, W, Pre, Post, C, ST, U>;
   return k_row<V, W, DISC_REDUCE_SUM, Pre, Post, C, ST, U>;
 }
 template <int V, bool W, typename Pre, typename Post, int C, bool ST, bool U>
 inline void (*sum_row_group_kernel(const HostGroup& H))(disc_group) {
-  if (sum_row_mb() && row_block(H.at<disc_reduce_launch>(0)) <= 256) return k_row_g_smb<V, W, Pre, Post, C, ST, U>;
+  const disc_reduce_launch& L = H.at<disc_reduce_launch>(0);  // the group key includes regcap
+  if (L.regcap && row_block(L) <= 256) return k_row_g_smb<V, W, Pre, Post, C, ST, U>;
   return k_row_g<V, W, DISC_REDUCE_SUM, Pre, Post, C, ST, U>;
 }
 

@@ -256,10 +256,10 @@ cudaError_t ring_release(Ring& r, size_t off, size_t n, cudaStream_t st) {
 struct GroupKey {
   int kind = 0;  // 0 loop, 1 row, 2 column pass
   const disc_spec::Entry* entry = nullptr;
-  int vec = 0, wide = 0, red = 0, stage = 0, block = 0, unaligned = 0;
+  int vec = 0, wide = 0, red = 0, stage = 0, block = 0, unaligned = 0, regcap = 0;
   bool operator<(const GroupKey& o) const {
-    return std::tie(kind, entry, vec, wide, red, stage, block, unaligned) <
-           std::tie(o.kind, o.entry, o.vec, o.wide, o.red, o.stage, o.block, o.unaligned);
+    return std::tie(kind, entry, vec, wide, red, stage, block, unaligned, regcap) <
+           std::tie(o.kind, o.entry, o.vec, o.wide, o.red, o.stage, o.block, o.unaligned, o.regcap);
   }
 };
 
@@ -287,6 +287,7 @@ bool group_key(int kind, const void* l, GroupKey* k) {
   k->stage = row ? R.stage : 0;
   k->block = row ? (R.group > 256 ? R.group : 256) : 256;
   k->unaligned = row ? R.unaligned : 0;  // a separate kernel instantiation
+  k->regcap = row ? R.regcap : 0;        // another (k_row_smb)
   const uint64_t key = row ? launch_key(1, R.pre, &R.post) : launch_key(2, R.pre, nullptr);
   k->entry = (g_spec_enabled && !R.wide) ? disc_spec::lookup(row ? 1 : 2, key) : nullptr;
   return true;

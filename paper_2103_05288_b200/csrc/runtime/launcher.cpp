@@ -513,6 +513,14 @@ bool stage_even() {
   return on;
 }
 
+int sum_row_mb_force() {  // -1: policy
+  static const int v = [] {
+    const char* e = std::getenv("DISC_SUM_ROW_MB");
+    return e ? (std::atoi(e) != 0 ? 1 : 0) : -1;
+  }();
+  return v;
+}
+
 bool col_pow2() {
   static const bool on = [] {
     const char* e = std::getenv("DISC_COL_POW2");
@@ -1436,6 +1444,17 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
       }
     }
     R.group = g;
+    // Register cap (6 resident blocks, <= 40 registers) for sum rows with a fused epilogue
+    // at <= 256 threads when the rows are long or stream several operands (A/B r3a:
+    // softmax S = 1024 epilogue 4480 -> 5143, BERT attention 4492 -> 4928 GB/s; softmax
+    // S = 100 lost 18% and the plain LN sums 8%, so not for those).  DISC_SUM_ROW_MB = 0/1
+    // forces it off/on.
+    if (R.kind == DISC_REDUCE_SUM && post_fused && std::max(g, 256) <= 256) {
+      int streamed = 0;
+      for (int l = 0; l < R.pre.n_loads; ++l) streamed += R.pre.loads[l].mode == DISC_LOAD_IDENTITY;
+      const int force = sum_row_mb_force();
+      R.regcap = force >= 0 ? force : (R.R >= 512 || streamed >= 2) ? 1 : 0;
+    }
     rep.schedule = R.stage == 2 ? (post_fused ? "row_fused_tma" : "row_tma")
                    : R.stage ? (post_fused ? "row_fused_staged" : "row_staged")
                            : post_fused ? (R.cache_loads ? "row_fused_cached" : "row_fused") : "row";
