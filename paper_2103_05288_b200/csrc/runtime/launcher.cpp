@@ -1445,15 +1445,14 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     }
     R.group = g;
     // Register cap (6 resident blocks, <= 40 registers) for sum rows with a fused epilogue
-    // at <= 256 threads when the rows are long or stream several operands (A/B r3a:
-    // softmax S = 1024 epilogue 4480 -> 5143, BERT attention 4492 -> 4928 GB/s; softmax
-    // S = 100 lost 18% and the plain LN sums 8%, so not for those).  DISC_SUM_ROW_MB = 0/1
-    // forces it off/on.
+    // at <= 256 threads, on long rows and row widths that are multiples of 64 (A/B r3a/r3c
+    // on the softmax epilogue, grouped: S = 64 4627 -> 5138, 128 5036 -> 5646, 256 4985 ->
+    // 5586, 1024 4480 -> 5143, BERT S = 128 4111 -> 4513 GB/s; but S = 24 4553 -> 3739,
+    // 48 4656 -> 3944, 200 4621 -> 4349, and the plain LN sums lose 8%).  DISC_SUM_ROW_MB =
+    // 0/1 forces it off/on.
     if (R.kind == DISC_REDUCE_SUM && post_fused && std::max(g, 256) <= 256) {
-      int streamed = 0;
-      for (int l = 0; l < R.pre.n_loads; ++l) streamed += R.pre.loads[l].mode == DISC_LOAD_IDENTITY;
       const int force = sum_row_mb_force();
-      R.regcap = force >= 0 ? force : (R.R >= 512 || streamed >= 2) ? 1 : 0;
+      R.regcap = force >= 0 ? force : (R.R >= 256 || (R.R >= 64 && R.R % 64 == 0)) ? 1 : 0;
     }
     rep.schedule = R.stage == 2 ? (post_fused ? "row_fused_tma" : "row_tma")
                    : R.stage ? (post_fused ? "row_fused_staged" : "row_staged")
