@@ -513,10 +513,10 @@ bool stage_even() {
   return on;
 }
 
-int sum_row_mb_force() {  // -1: policy
+int sum_row_mb_force() {  // 0 off (default), 1 every fused sum row, 2 the width rule
   static const int v = [] {
     const char* e = std::getenv("DISC_SUM_ROW_MB");
-    return e ? (std::atoi(e) != 0 ? 1 : 0) : -1;
+    return e ? std::atoi(e) : 0;
   }();
   return v;
 }
@@ -1448,11 +1448,13 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     // at <= 256 threads, on long rows and row widths that are multiples of 64 (A/B r3a/r3c
     // on the softmax epilogue, grouped: S = 64 4627 -> 5138, 128 5036 -> 5646, 256 4985 ->
     // 5586, 1024 4480 -> 5143, BERT S = 128 4111 -> 4513 GB/s; but S = 24 4553 -> 3739,
-    // 48 4656 -> 3944, 200 4621 -> 4349, and the plain LN sums lose 8%).  DISC_SUM_ROW_MB =
-    // 0/1 forces it off/on.
+    // 48 4656 -> 3944, 200 4621 -> 4349, and the plain LN sums lose 8%).  On the headline
+    // sweep, whose grouped launches mix widths, neither the width rule (4336: it splits the
+    // groups) nor capping every fused sum row (4365-4371) beats none (4388 GB/s, A/B r3d/r3e):
+    // off by default; DISC_SUM_ROW_MB = 1 caps every fused sum row, 2 applies the width rule.
     if (R.kind == DISC_REDUCE_SUM && post_fused && std::max(g, 256) <= 256) {
-      const int force = sum_row_mb_force();
-      R.regcap = force >= 0 ? force : (R.R >= 256 || (R.R >= 64 && R.R % 64 == 0)) ? 1 : 0;
+      const int mode = sum_row_mb_force();
+      R.regcap = mode == 1 ? 1 : (mode == 2 && (R.R >= 256 || (R.R >= 64 && R.R % 64 == 0))) ? 1 : 0;
     }
     rep.schedule = R.stage == 2 ? (post_fused ? "row_fused_tma" : "row_tma")
                    : R.stage ? (post_fused ? "row_fused_staged" : "row_staged")
