@@ -477,6 +477,7 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
   int it = 0;
   for (int64_t base = static_cast<int64_t>(bx) * rpb; base < rows; base += static_cast<int64_t>(gx) * rpb, ++it) {
     const int64_t n_el = (rows - base < rpb ? rows - base : rpb) * L.R;
+
     if (tma) {
       const int st = it & 1;
       const int64_t nb = base + static_cast<int64_t>(gx) * rpb;
@@ -835,12 +836,15 @@ __global__ void __launch_bounds__(256, 6) k_row_g_mb(const __grid_constant__ dis
 
 // Sum rows at <= 256 threads capped at 6 resident blocks (<= 40 registers) -- A/B knob
 // DISC_SUM_ROW_MB (the fused softmax epilogue runs at 64 registers, 50% occupancy).
+#ifndef DISC_SMB_BLOCKS
+#define DISC_SMB_BLOCKS 6
+#endif
 template <int VEC, bool WIDE, typename Pre, typename Post, int CH, bool STAGED, bool UNAL>
-__global__ void __launch_bounds__(256, 6) k_row_smb(const __grid_constant__ disc_reduce_launch L) {
+__global__ void __launch_bounds__(256, DISC_SMB_BLOCKS) k_row_smb(const __grid_constant__ disc_reduce_launch L) {
   row_body<VEC, WIDE, DISC_REDUCE_SUM, Pre, Post, CH, STAGED, UNAL>(L, blockIdx.x, gridDim.x);
 }
 template <int VEC, bool WIDE, typename Pre, typename Post, int CH, bool STAGED, bool UNAL>
-__global__ void __launch_bounds__(256, 6) k_row_g_smb(const __grid_constant__ disc_group G) {
+__global__ void __launch_bounds__(256, DISC_SMB_BLOCKS) k_row_g_smb(const __grid_constant__ disc_group G) {
   __shared__ __align__(16) unsigned char desc[desc_bytes<disc_reduce_launch>()];
   const int b = blockIdx.x, g = group_of(G, b);
   const disc_reduce_launch& L = group_stage<disc_reduce_launch>(G, g, desc);
