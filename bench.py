@@ -972,6 +972,8 @@ def main():
                     help="issue grouped launches from a background thread (flows of the next chunk overlap)")
     ap.add_argument("--reserve-gb", type=float, default=64.0, help="executor buffer arena reserved up front")
     ap.add_argument("--e2e-gb", type=float, default=4.0, help="e2e: pinned host input bytes")
+    ap.add_argument("--e2e-pipes", type=int, default=3, help="e2e: executors/streams the chunks alternate over")
+    ap.add_argument("--e2e-chunk-mb", type=int, default=256, help="e2e: algorithmic MB per grouped call")
     ap.add_argument("--ref-step-s", type=float, default=4.0, help="reference arm: seconds of CPU work per step")
     ap.add_argument("--host-threads", type=int, default=0,
                     help="host threads per rank for the runtime flows (0: cores / ranks, max 32)")
@@ -1129,7 +1131,8 @@ def main():
             ver = verify_pass(B, wl, batches[args.warmup], args.verify, threads=max(1, (os.cpu_count() or 2) - 1))
     e2e = None
     if not args.no_e2e:
-        e2e = measure_e2e(B, wl, reqs0, costs0, int(args.e2e_gb * (1 << 30)))
+        e2e = measure_e2e(B, wl, reqs0, costs0, int(args.e2e_gb * (1 << 30)), pipes=args.e2e_pipes,
+                          chunk_bytes=int(args.e2e_chunk_mb) << 20)
         if dist is not None:
             e2e["value"] = round(allreduce(dist, local, e2e["bytes"], "sum") /
                                  allreduce(dist, local, e2e["seconds"], "max") / 1e9, 2)
