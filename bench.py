@@ -972,8 +972,8 @@ def main():
                     help="issue grouped launches from a background thread (flows of the next chunk overlap)")
     ap.add_argument("--reserve-gb", type=float, default=64.0, help="executor buffer arena reserved up front")
     ap.add_argument("--e2e-gb", type=float, default=4.0, help="e2e: pinned host input bytes")
-    ap.add_argument("--e2e-pipes", type=int, default=3, help="e2e: executors/streams the chunks alternate over")
-    ap.add_argument("--e2e-chunk-mb", type=int, default=256, help="e2e: algorithmic MB per grouped call")
+    ap.add_argument("--e2e-pipes", type=int, default=8, help="e2e: executors/streams the chunks alternate over")
+    ap.add_argument("--e2e-chunk-mb", type=int, default=64, help="e2e: algorithmic MB per grouped call")
     ap.add_argument("--ref-step-s", type=float, default=4.0, help="reference arm: seconds of CPU work per step")
     ap.add_argument("--host-threads", type=int, default=0,
                     help="host threads per rank for the runtime flows (0: cores / ranks, max 32)")
