@@ -8,6 +8,12 @@
 
 #include "kernels.cuh"
 
+// Chunks per thread per interpreter dispatch (the dispatch cost is paid once per
+// instruction per CH*VEC elements); A/B knob at build time.
+#ifndef DISC_INTERP_CH
+#define DISC_INTERP_CH 2
+#endif
+
 
 namespace disc_dev {
 
@@ -217,7 +223,7 @@ void set_pdl(int mode) { g_pdl = mode; }
 int pdl_mode() { return g_pdl; }
 
 cudaError_t loop(const disc_loop_launch& L, cudaStream_t s, const HostGroup* g) {
-  return loop_pass<Interp>(L, s, true, g);
+  return loop_pass<Interp, DISC_INTERP_CH>(L, s, true, g);
 }
 
 cudaError_t col_pass(const disc_reduce_launch& L, cudaStream_t s, const HostGroup* g);
@@ -251,7 +257,7 @@ cudaError_t finalize_columns(const disc_reduce_launch& L, cudaStream_t s, const 
 
 cudaError_t reduce(const disc_reduce_launch& L, cudaStream_t s, const HostGroup* g) {
   if (L.schedule == DISC_SCHED_ROW) {
-    return row_pass<Interp, Interp>(L, s, true, g);
+    return row_pass<Interp, Interp, DISC_INTERP_CH>(L, s, true, g);
   }
   if (L.schedule == DISC_SCHED_GENERIC) {
     if (g) return cudaErrorInvalidValue;  // never grouped (device layer issues these one by one)
@@ -269,7 +275,7 @@ cudaError_t reduce(const disc_reduce_launch& L, cudaStream_t s, const HostGroup*
 }
 
 cudaError_t col_pass(const disc_reduce_launch& L, cudaStream_t s, const HostGroup* g) {
-  return col_pass_t<Interp>(L, s, true, g);
+  return col_pass_t<Interp, DISC_INTERP_CH>(L, s, true, g);
 }
 
 }  // namespace disc_launch
