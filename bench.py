@@ -879,12 +879,16 @@ def analyse(B, wl, reqs, costs, peak):
             ent["large"]["frac_of_peak"] = round(ent["large"]["GB/s"] / peak, 4) if ent["large"]["GB/s"] else None
             ent["large_byte_share"] = round(lb / b, 4) if b else None
         per_pattern[p] = ent
-        for r in B.record_pass(B.batch(sub, sc)):
-            key = f"{p}:k{r['kernel']}:{r['schedule']}"
-            a = records.setdefault(key, [0, 0.0, 0])
-            a[0] += r["bytes"]
-            a[1] += r["ms"]
-            a[2] += 1
+        # per-kernel records keyed (graph, plan kernel, schedule): one timing pass per graph
+        kinds = sorted({reqs[i][0] for i in idx})
+        for kind in kinds:
+            kidx = [i for i in idx if reqs[i][0] == kind]
+            for r in B.record_pass(B.batch([reqs[i] for i in kidx], [costs[i] for i in kidx])):
+                key = f"{kind}:k{r['kernel']}:{r['schedule']}"
+                a = records.setdefault(key, [0, 0.0, 0])
+                a[0] += r["bytes"]
+                a[1] += r["ms"]
+                a[2] += 1
     # the generic path: the same passes with the generated kernels off (tape interpreter)
     B.D.set_specialization(False)
     try:
