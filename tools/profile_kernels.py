@@ -43,13 +43,13 @@ def run(args):
     reqs = wl.requests(args.step)
     B.plans_for(reqs)
     costs = B.costs(reqs)
-    pats = {}
+    pats = {}  # per graph (bench.py's kernel_breakdown keys)
     for i, (k, _) in enumerate(reqs):
-        pats.setdefault(bench.pattern_of(k), []).append(i)
+        pats.setdefault(k, []).append(i)
     out = []
     only = set(args.patterns.split(",")) if args.patterns else None
     for p, idx in sorted(pats.items()):
-        if only and p not in only:
+        if only and p not in only and bench.pattern_of(p) not in only:
             continue
         batch = B.batch([reqs[i] for i in idx], [costs[i] for i in idx])
         B.record_pass(batch)  # warm (recipes, arena)
