@@ -513,6 +513,14 @@ bool stage_even() {
   return on;
 }
 
+int short_rows_g() {  // DISC_SHORT_G: minimum lanes per row for rows of < 32 floats (1 = off)
+  static const int v = [] {
+    const char* e = std::getenv("DISC_SHORT_G");
+    return e ? std::max(1, std::atoi(e)) : 1;
+  }();
+  return v;
+}
+
 int sum_row_mb_force() {  // 0 off (default), 1 every fused sum row, 2 the width rule
   static const int v = [] {
     const char* e = std::getenv("DISC_SUM_ROW_MB");
@@ -1310,6 +1318,12 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
 
   if (R.schedule == DISC_SCHED_ROW) {
     int g = choose_row_group(R.K, R.R, R.vec);
+    if (short_rows_g() > 1 && R.R < 32) {  // A/B: several lanes per short row (coalesced, fewer iterations)
+      const int64_t chunks = (R.R + R.vec - 1) / R.vec;
+      int cap = 1;
+      while (cap < chunks && cap < 32) cap <<= 1;
+      g = std::max(g, std::min(short_rows_g(), cap));
+    }
     // Staged short rows (R < 32 floats: even a whole row is under one 128 B line): the
     // block copies its contiguous span of every identity operand through shared memory,
     // one thread per row.  Only when that layout is bank-conflict-free (odd R for scalar
