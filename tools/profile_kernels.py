@@ -97,7 +97,7 @@ def merge(args):
     def kinds(sched):
         """ncu kernel base names a record's grouped launch can have."""
         s = sched.replace("group:", "")
-        if s == "mixed":
+        if s == "mixed" or "fold" in s:  # a folded column launch issues its tile loop first
             return ("k_row_g", "k_row_g_mb", "k_col_g", "k_loop_g")
         if s.startswith("col"):
             return ("k_col_g",)

@@ -19,7 +19,7 @@ echo "kernel traffic rc=$?"
 python tools/profile_kernels.py merge --records gpurun_out/${tag}_kt.json --csv gpurun_out/${tag}_kt.csv \
   --out gpurun_out/${tag}_ncu_traffic.json > /dev/null 2>&1
 for p in $2; do
-  timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -c 10 \
+  timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -c 10 -k "regex:k_(loop|row|col)" \
     -o /tmp/full_${tag}_$p python tools/profile_kernels.py run --patterns $p --records /tmp/rec_$p.json > /dev/null 2>&1
   python tools/ncu_summary.py /tmp/full_${tag}_$p.ncu-rep dram__bytes_read.sum dram__bytes_write.sum \
     smsp__inst_executed.sum sm__throughput.avg.pct_of_peak_sustained_elapsed > gpurun_out/${tag}_full_$p.txt 2>&1
