@@ -4,6 +4,9 @@
 #include "../desc_ranges.hpp"
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1061,6 +1064,30 @@ class Issuer {
 };
 
 // Issues the fused lowering; throws NotFusible when the tape needs materialisation.
+// Host-cost profile of launch_kernel (DISC_FLOW_PROFILE=1: totals printed at exit).
+namespace {
+struct FlowProf {
+  std::atomic<int64_t> calls{0}, hits{0}, ns_total{0}, ns_key{0}, ns_sim{0}, ns_lower{0}, ns_pre{0}, ns_post{0}, ns_bind{0}, ns_sched{0}, ns_issue{0};
+  ~FlowProf() {
+    if (!std::getenv("DISC_FLOW_PROFILE") || !calls) return;
+    std::fprintf(stderr, "[disc flow] launch_kernel: %lld calls, %lld recipe hits; us/call: total %.2f, key %.2f, "
+                 "simulate %.2f, lower+issue %.2f\n", (long long)calls.load(), (long long)hits.load(),
+                 ns_total / 1e3 / calls, ns_key / 1e3 / calls, ns_sim / 1e3 / calls, ns_lower / 1e3 / calls);
+    std::fprintf(stderr, "[disc flow] reduce lowering us/call: pre %.2f, post %.2f, bind %.2f, schedule %.2f, issue %.2f\n",
+                 ns_pre / 1e3 / calls, ns_post / 1e3 / calls, ns_bind / 1e3 / calls, ns_sched / 1e3 / calls,
+                 ns_issue / 1e3 / calls);
+  }
+};
+FlowProf g_flow_prof;
+bool flow_prof_on() {
+  static const bool on = std::getenv("DISC_FLOW_PROFILE") != nullptr;
+  return on;
+}
+int64_t now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
 LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& issue, SchedulePref pref) {
   const KernelArtifact& art = B.art;
   const int n = static_cast<int>(art.tape.size());
@@ -1087,6 +1114,14 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
   }
 
   // kInput: reduce-rooted.
+  const bool prof = flow_prof_on();
+  int64_t tp = prof ? now_ns() : 0;
+  auto lap = [&](std::atomic<int64_t>& acc) {
+    if (!prof) return;
+    const int64_t t = now_ns();
+    acc += t - tp;
+    tp = t;
+  };
   const TapeInstr& rt = art.tape[B.red];
   const TapeRef& rarg = rt.args[0];
   const std::vector<int64_t>& adims = ref_dims(B, rarg);
@@ -1160,6 +1195,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     return rep;
   }
 
+  lap(g_flow_prof.ns_pre);
   // Post program: fused into the row kernel when every reduce read is row-aligned.
   Built post;
   std::memset(&post.prog, 0, sizeof post.prog);
@@ -1217,6 +1253,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     R.C = 1;
   }
 
+  lap(g_flow_prof.ns_post);
   // Bind loads to the schedule's [rows, W] view and pick the vector width.
   if (empty) {
     bind_view(pre, 1);
@@ -1309,6 +1346,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
   }
   R.pre = pre.prog;
   R.post = post.prog;
+  lap(g_flow_prof.ns_bind);
   if (!empty && R.schedule != DISC_SCHED_GENERIC) {
     const bool row_view = R.schedule == DISC_SCHED_ROW;
     const int64_t vrows = row_view ? R.K : R.K * R.R, vW = row_view ? R.R : R.C;
@@ -1524,7 +1562,9 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     rep.schedule = "generic";
   }
 
+  lap(g_flow_prof.ns_sched);
   issue.reduce(R);
+  lap(g_flow_prof.ns_issue);
   rep.device_kernels += (R.schedule == DISC_SCHED_COL_TWOPASS || R.schedule == DISC_SCHED_COL_ATOMIC) ? 2 : 1;
   if (post_pass) {
     issue.loop(PL);
@@ -1830,9 +1870,26 @@ bool it_seen_first(LaunchCache* c, uint64_t h) {
 LaunchCache* new_launch_cache() { return new LaunchCache(); }
 void free_launch_cache(LaunchCache* c) { delete c; }
 
+LaunchReport launch_kernel_impl(const KernelArtifact& art, const VersionArtifact& ver, const std::vector<DevTensor>& ext,
+                                const std::vector<int64_t>& regs, const std::vector<OutBuf>& outs, Scratch& scratch,
+                                void* stream, SchedulePref pref, LaunchCache* cache, uint64_t plan_serial);
+
 LaunchReport launch_kernel(const KernelArtifact& art, const VersionArtifact& ver, const std::vector<DevTensor>& ext,
                            const std::vector<int64_t>& regs, const std::vector<OutBuf>& outs, Scratch& scratch,
                            void* stream, SchedulePref pref, LaunchCache* cache, uint64_t plan_serial) {
+  if (!flow_prof_on()) return launch_kernel_impl(art, ver, ext, regs, outs, scratch, stream, pref, cache, plan_serial);
+  const int64_t t0 = now_ns();
+  LaunchReport r = launch_kernel_impl(art, ver, ext, regs, outs, scratch, stream, pref, cache, plan_serial);
+  g_flow_prof.ns_total += now_ns() - t0;
+  g_flow_prof.calls++;
+  return r;
+}
+
+LaunchReport launch_kernel_impl(const KernelArtifact& art, const VersionArtifact& ver, const std::vector<DevTensor>& ext,
+                                const std::vector<int64_t>& regs, const std::vector<OutBuf>& outs, Scratch& scratch,
+                                void* stream, SchedulePref pref, LaunchCache* cache, uint64_t plan_serial) {
+  const bool prof = flow_prof_on();
+  int64_t tp = prof ? now_ns() : 0;
   // Recipe cache: everything the lowering depends on is in the key.
   std::vector<int64_t> key;
   uint64_t h = 0;
@@ -1860,8 +1917,14 @@ LaunchReport launch_kernel(const KernelArtifact& art, const VersionArtifact& ver
         if (e.key == key) {
           if (!e.recipe) break;  // known to need the materialised path
           replay(*e.recipe, ext, outs, scratch, stream);
+          if (prof) g_flow_prof.hits++;
           return e.recipe->rep;
         }
+  }
+  if (prof) {
+    const int64_t t = now_ns();
+    g_flow_prof.ns_key += t - tp;
+    tp = t;
   }
   bool record = cacheable;
   if (record && it_seen_first(cache, h)) record = false;  // first sighting: lower directly
@@ -1871,6 +1934,18 @@ LaunchReport launch_kernel(const KernelArtifact& art, const VersionArtifact& ver
   Binding B{art, ver, ext, regs, simulate_tape(art, ver, ext_dims, regs), -1, {}};
   for (size_t o = 0; o < art.output_tape_indices.size(); ++o)
     check_capacity(B.dims.at(art.output_tape_indices[o]), outs.at(o));
+  if (prof) {
+    const int64_t t = now_ns();
+    g_flow_prof.ns_sim += t - tp;
+    tp = t;
+  }
+  struct LowerTimer {
+    bool on;
+    int64_t t0;
+    ~LowerTimer() {
+      if (on) g_flow_prof.ns_lower += now_ns() - t0;
+    }
+  } lower_timer{prof, tp};
 
   LaunchReport rep;
   if (art.standalone) {
