@@ -263,6 +263,14 @@ struct GroupKey {
   }
 };
 
+bool regcap_in_key() {  // DISC_REGCAP_KEY=1: separate groups per register-cap choice
+  static const bool on = [] {
+    const char* e = std::getenv("DISC_REGCAP_KEY");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 bool is_col(int sched) {
   return sched == DISC_SCHED_COL_SINGLE || sched == DISC_SCHED_COL_TWOPASS || sched == DISC_SCHED_COL_ATOMIC;
 }
@@ -287,7 +295,9 @@ bool group_key(int kind, const void* l, GroupKey* k) {
   k->stage = row ? R.stage : 0;
   k->block = row ? (R.group > 256 ? R.group : 256) : 256;
   k->unaligned = row ? R.unaligned : 0;  // a separate kernel instantiation
-  k->regcap = row ? R.regcap : 0;        // another (k_row_smb)
+  // regcap (k_row_smb) is NOT part of the key: a group runs its largest member's choice
+  // (members are issued largest first), so mixed widths never split a group
+  k->regcap = (row && regcap_in_key()) ? R.regcap : 0;
   const uint64_t key = row ? launch_key(1, R.pre, &R.post) : launch_key(2, R.pre, nullptr);
   k->entry = (g_spec_enabled && !R.wide) ? disc_spec::lookup(row ? 1 : 2, key) : nullptr;
   return true;
