@@ -173,7 +173,9 @@ typedef struct {
   int64_t fold_cout;
   /* ROW sum with <= 256 threads: 1 = the register-capped kernel (6 resident blocks) */
   int32_t regcap;
-  int32_t pad2;
+  /* ROW, R < 32, scalar rows, one thread per row: 8 or 32 = the register-resident short-row
+   * kernel (the whole row evaluated at once, one sequential accumulator), 0 = off */
+  int32_t short_rows;
 } disc_reduce_launch;
 
 /* Standalone pad (eval_pad, kernels.cpp:125-147), output-driven gather. */

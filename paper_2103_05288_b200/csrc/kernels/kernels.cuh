@@ -674,6 +674,54 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
 }
 
 // ---------------------------------------------------------------------------
+// Short rows (R < 32 floats, scalar, generated programs): one thread per row evaluates its
+// whole row at once -- MAXR chunks of one element, fully unrolled and predicated (c < R),
+// values in registers -- and reduces them with ONE sequential accumulator (the reference's
+// own order, kernels.cpp:234-259).  No column loop, no per-chunk partials; the fused
+// epilogue reads the cached reduce argument this thread wrote (no barrier).
+template <int KIND, typename Pre, typename Post, int MAXR>
+__device__ __forceinline__ void row_short_body(const disc_reduce_launch& L, const int bx, const int gx) {
+  using RD = Red<KIND>;
+  using Acc = typename RD::Acc;
+  using I = int32_t;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ float consts[2][DISC_MAX_LOADS];
+  const int rpb = blockDim.x;
+  const int64_t slot_stride = (static_cast<int64_t>(rpb) * L.R + 3) / 4 * 4;
+  float* const cache0 = reinterpret_cast<float*>(smem_raw);
+  pdl_enter(L.pre);
+  hoist_consts(L.pre, consts[0]);
+  hoist_consts(L.post, consts[1]);
+  __syncthreads();
+  const I R = static_cast<I>(L.R), sst = static_cast<I>(slot_stride);
+  float* const row_cache = L.cache_loads ? cache0 + threadIdx.x * L.R : nullptr;
+  float* const arg_cache = (L.arg_slot >= 0 && row_cache) ? row_cache + L.arg_slot * slot_stride : nullptr;
+  const bool fuse_post = L.post.n_instr > 0;
+  for (int64_t base = static_cast<int64_t>(bx) * rpb; base < L.K; base += static_cast<int64_t>(gx) * rpb) {
+    const int64_t r64 = base + threadIdx.x;
+    if (r64 >= L.K) continue;
+    const I row = static_cast<I>(r64);
+    float v[MAXR];
+    Pre::template run<1, MAXR, false>(L.pre, Tile<I, false>{row, 0, R, 1, static_cast<int>(R), row_cache, sst}, v,
+                                      nullptr, 0, consts[0], 0.f);
+    Acc acc = RD::identity();
+#pragma unroll
+    for (int c = 0; c < MAXR; ++c)
+      if (c < R) {
+        acc = RD::step(acc, v[c]);
+        if (arg_cache) arg_cache[c] = v[c];
+      }
+    const float result = static_cast<float>(acc);
+    if (L.red_out) L.red_out[row] = result;
+    if (fuse_post) {
+      float w[MAXR];
+      Post::template run<1, MAXR, false>(L.post, Tile<I, false>{row, 0, R, 1, static_cast<int>(R), row_cache, sst}, w,
+                                         nullptr, 0, consts[1], result);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Column schedule: reduce arg collapsed to [K, R, C], reduce over R, C contiguous; viewed
 // as rows k*R + r of width C.  A thread owns VEC columns; lpc = L.group lanes span a row
 // segment of lpc*VEC columns and a warp covers 32/lpc rows (narrow C packs many rows per
@@ -832,6 +880,18 @@ __global__ void __launch_bounds__(256, 6) k_row_g_mb(const __grid_constant__ dis
   const disc_reduce_launch& L = group_stage<disc_reduce_launch>(G, g, desc);
   row_body<VEC, WIDE, DISC_REDUCE_MAX, Pre, Post, CH, STAGED, UNAL>(L, b - G.block_off[g],
                                                                    G.block_off[g + 1] - G.block_off[g]);
+}
+
+template <int KIND, typename Pre, typename Post, int MAXR>
+__global__ void __launch_bounds__(256) k_row_short(const __grid_constant__ disc_reduce_launch L) {
+  row_short_body<KIND, Pre, Post, MAXR>(L, blockIdx.x, gridDim.x);
+}
+template <int KIND, typename Pre, typename Post, int MAXR>
+__global__ void __launch_bounds__(256) k_row_short_g(const __grid_constant__ disc_group G) {
+  __shared__ __align__(16) unsigned char desc[desc_bytes<disc_reduce_launch>()];
+  const int b = blockIdx.x, g = group_of(G, b);
+  const disc_reduce_launch& L = group_stage<disc_reduce_launch>(G, g, desc);
+  row_short_body<KIND, Pre, Post, MAXR>(L, b - G.block_off[g], G.block_off[g + 1] - G.block_off[g]);
 }
 
 // Sum rows at <= 256 threads capped at 6 resident blocks (<= 40 registers) -- A/B knob
@@ -1174,6 +1234,17 @@ inline cudaError_t row_pass(const disc_reduce_launch& L, cudaStream_t s, bool us
   if constexpr (ALLOW_WIDE)
     if (L.wide) return L.vec == 4 ? (L.unaligned ? DISC_ROW_U(4, true, false, CH, true) : DISC_ROW(4, true, false, CH))
                                   : DISC_ROW(1, true, false, C1);
+  if constexpr (!std::is_same<Pre, Interp>::value) {  // register-resident short rows (generated programs)
+    if (L.short_rows) {
+#define DISC_ROWS(M)                                                                                              \
+  (g ? (sum ? launch_row_group<1>(k_row_short_g<DISC_REDUCE_SUM, Pre, Post, M>, *g, s, false)                     \
+            : launch_row_group<1>(k_row_short_g<DISC_REDUCE_MAX, Pre, Post, M>, *g, s, false))                    \
+     : (sum ? launch_row_with<1>(k_row_short<DISC_REDUCE_SUM, Pre, Post, M>, L, s, false)                         \
+            : launch_row_with<1>(k_row_short<DISC_REDUCE_MAX, Pre, Post, M>, L, s, false)))
+      return L.short_rows <= 8 ? DISC_ROWS(8) : DISC_ROWS(32);
+#undef DISC_ROWS
+    }
+  }
   if (L.stage) return L.vec == 4 ? DISC_ROW(4, false, true, CH) : DISC_ROW(1, false, true, CH);
   if (L.vec == 4) return L.unaligned ? DISC_ROW_U(4, false, false, CH, true) : DISC_ROW(4, false, false, CH);
   return DISC_ROW(1, false, false, C1);

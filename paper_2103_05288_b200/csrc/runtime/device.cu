@@ -256,10 +256,10 @@ cudaError_t ring_release(Ring& r, size_t off, size_t n, cudaStream_t st) {
 struct GroupKey {
   int kind = 0;  // 0 loop, 1 row, 2 column pass
   const disc_spec::Entry* entry = nullptr;
-  int vec = 0, wide = 0, red = 0, stage = 0, block = 0, unaligned = 0, regcap = 0;
+  int vec = 0, wide = 0, red = 0, stage = 0, block = 0, unaligned = 0, regcap = 0, short_rows = 0;
   bool operator<(const GroupKey& o) const {
-    return std::tie(kind, entry, vec, wide, red, stage, block, unaligned, regcap) <
-           std::tie(o.kind, o.entry, o.vec, o.wide, o.red, o.stage, o.block, o.unaligned, o.regcap);
+    return std::tie(kind, entry, vec, wide, red, stage, block, unaligned, regcap, short_rows) <
+           std::tie(o.kind, o.entry, o.vec, o.wide, o.red, o.stage, o.block, o.unaligned, o.regcap, o.short_rows);
   }
 };
 
@@ -298,6 +298,7 @@ bool group_key(int kind, const void* l, GroupKey* k) {
   // regcap (k_row_smb) is NOT part of the key: a group runs its largest member's choice
   // (members are issued largest first), so mixed widths never split a group
   k->regcap = (row && regcap_in_key()) ? R.regcap : 0;
+  k->short_rows = row ? R.short_rows : 0;  // another kernel (k_row_short)
   const uint64_t key = row ? launch_key(1, R.pre, &R.post) : launch_key(2, R.pre, nullptr);
   k->entry = (g_spec_enabled && !R.wide) ? disc_spec::lookup(row ? 1 : 2, key) : nullptr;
   return true;

@@ -524,6 +524,14 @@ int short_rows_g() {  // DISC_SHORT_G: minimum lanes per row for rows of < 32 fl
   return v;
 }
 
+bool short_rows_enabled() {  // DISC_SHORT_ROWS=0: the looped row kernel for short rows too
+  static const bool on = [] {
+    const char* e = std::getenv("DISC_SHORT_ROWS");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 int sum_row_mb_force() {  // 0 off (default), 1 every fused sum row, 2 the width rule
   static const int v = [] {
     const char* e = std::getenv("DISC_SUM_ROW_MB");
@@ -1496,6 +1504,11 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
       }
     }
     R.group = g;
+    // Short scalar rows, one thread per row: the register-resident kernel (whole row at
+    // once, one sequential accumulator) when the programs are generated ones.
+    if (short_rows_enabled() && g == 1 && R.vec == 1 && !R.wide && !R.stage && !R.unaligned && R.R >= 2 &&
+        R.R < 32)
+      R.short_rows = R.R <= 8 ? 8 : 32;
     // Register cap (6 resident blocks, <= 40 registers) for sum rows with a fused epilogue
     // at <= 256 threads, on long rows and row widths that are multiples of 64 (A/B r3a/r3c
     // on the softmax epilogue, grouped: S = 64 4627 -> 5138, 128 5036 -> 5646, 256 4985 ->
@@ -1508,7 +1521,8 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
       const int mode = sum_row_mb_force();
       R.regcap = mode == 1 ? 1 : (mode == 2 && (R.R >= 256 || (R.R >= 64 && R.R % 64 == 0))) ? 1 : 0;
     }
-    rep.schedule = R.stage == 2 ? (post_fused ? "row_fused_tma" : "row_tma")
+    rep.schedule = R.short_rows ? (post_fused ? "row_fused_short" : "row_short")
+                   : R.stage == 2 ? (post_fused ? "row_fused_tma" : "row_tma")
                    : R.stage ? (post_fused ? "row_fused_staged" : "row_staged")
                            : post_fused ? (R.cache_loads ? "row_fused_cached" : "row_fused") : "row";
   } else if (R.schedule != DISC_SCHED_GENERIC) {
