@@ -524,6 +524,14 @@ int short_rows_g() {  // DISC_SHORT_G: minimum lanes per row for rows of < 32 fl
   return v;
 }
 
+bool short_vec4() {  // DISC_SHORT_VEC4=1: rows of 4k floats (< 32) take the short kernel too
+  static const bool on = [] {
+    const char* e = std::getenv("DISC_SHORT_VEC4");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 bool short_rows_enabled() {  // DISC_SHORT_ROWS=0: the looped row kernel for short rows too
   static const bool on = [] {
     const char* e = std::getenv("DISC_SHORT_ROWS");
@@ -1272,7 +1280,14 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     R.vec = choose_vec({&pre, &post}, R.R);
     // Odd-width rows: float4 body from each row's first 16 B-aligned column + scalar
     // head/tail, when every operand is a 16 B-aligned identity, a row splat or a constant.
-    if (R.vec == 1 && R.R % 4 != 0 && R.R >= unaligned_min_width() && unaligned_rows_enabled()) {
+    // Short rows (R < 32) run the register-resident thread-per-row kernel (see below):
+    // scalar, never the unaligned float4 body; rows of 4k floats too with DISC_SHORT_VEC4.
+    const bool short_row = short_rows_enabled() && !R.wide && R.R >= 2 && R.R < 32 && (R.vec == 1 || short_vec4());
+    if (short_row) {
+      R.vec = 1;
+      R.short_rows = 1;  // pending: confirmed (or dropped) with the row group below
+    }
+    if (!short_row && R.vec == 1 && R.R % 4 != 0 && R.R >= unaligned_min_width() && unaligned_rows_enabled()) {
       bool ok = true;
       for (const Built* b : {&pre, &post}) {
         const disc_program& P = b->prog;
@@ -1364,6 +1379,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
 
   if (R.schedule == DISC_SCHED_ROW) {
     int g = choose_row_group(R.K, R.R, R.vec);
+    if (R.short_rows) g = 1;  // thread per row
     if (short_rows_g() > 1 && R.R < 32) {  // A/B: several lanes per short row (coalesced, fewer iterations)
       const int64_t chunks = (R.R + R.vec - 1) / R.vec;
       int cap = 1;
@@ -1490,10 +1506,11 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
       }();
       const int64_t rrow = R.unaligned ? (R.R + 6) / 4 * 4 : R.R;  // padded rows (kernels.cuh row_body)
       auto bytes = [&](int gg) { return int64_t{std::max(gg, 256) / gg} * nc * rrow * 4; };
-      while (nc && bytes(g) > budget && g < 1024) g <<= 1;
       // the epilogue of an argument-cached launch reads the cache: it must fit (one row of
-      // up to 3 slots of 4100 floats), so such launches may exceed the budget up to 64 KB
+      // up to 3 slots of 4100 floats), so such launches may exceed the budget up to 64 KB;
+      // short rows stay one thread per row within that limit
       const int64_t limit = R.arg_slot >= 0 ? std::max<int64_t>(budget, 64 * 1024) : budget;
+      while (nc && bytes(g) > (R.short_rows ? limit : budget) && g < 1024) g <<= 1;
       if (nc && bytes(g) <= limit) {
         R.cache_loads = nc;
         R.pre.cache_mode = DISC_CACHE_FILL;
@@ -1506,9 +1523,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     R.group = g;
     // Short scalar rows, one thread per row: the register-resident kernel (whole row at
     // once, one sequential accumulator) when the programs are generated ones.
-    if (short_rows_enabled() && g == 1 && R.vec == 1 && !R.wide && !R.stage && !R.unaligned && R.R >= 2 &&
-        R.R < 32)
-      R.short_rows = R.R <= 8 ? 8 : 32;
+    if (R.short_rows) R.short_rows = (g == 1 && !R.stage && !R.unaligned) ? (R.R <= 8 ? 8 : 32) : 0;
     // Register cap (6 resident blocks, <= 40 registers) for sum rows with a fused epilogue
     // at <= 256 threads, on long rows and row widths that are multiples of 64 (A/B r3a/r3c
     // on the softmax epilogue, grouped: S = 64 4627 -> 5138, 128 5036 -> 5646, 256 4985 ->
