@@ -176,6 +176,10 @@ typedef struct {
   /* ROW, R < 32, scalar rows, one thread per row: 8 or 32 = the register-resident short-row
    * kernel (the whole row evaluated at once, one sequential accumulator), 0 = off */
   int32_t short_rows;
+  /* ROW with a row cache: floats between consecutive rows in a cache slot (0 = R, or
+   * R + 3 rounded to 4 for unaligned rows); padded so that the rows one shared-memory
+   * wavefront touches fall in distinct banks */
+  int32_t row_pitch;
 } disc_reduce_launch;
 
 /* Standalone pad (eval_pad, kernels.cpp:125-147), output-driven gather. */

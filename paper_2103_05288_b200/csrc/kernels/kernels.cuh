@@ -408,7 +408,7 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
   // float4 body + scalar head/tail per row: a separate instantiation (UNAL), so aligned
   // kernels keep their register budget (30 vs 58 registers for a plain row sum)
   const bool unal = UNAL && VEC == 4 && L.unaligned;
-  const int64_t rrow = unal ? (L.R + 6) / 4 * 4 : L.R;  // row pitch in the row cache
+  const int64_t rrow = L.row_pitch ? L.row_pitch : unal ? (L.R + 6) / 4 * 4 : L.R;  // row pitch in the row cache
   const int64_t slot_stride = (static_cast<int64_t>(rpb) * rrow + 3) / 4 * 4;
   const int64_t cache_floats = slot_stride * L.cache_loads;
   float* const cache0 = reinterpret_cast<float*>(smem_raw);
@@ -1048,7 +1048,7 @@ inline size_t row_smem(const disc_reduce_launch& L, bool use_slots) {
   const int slots = L.pre.n_slots > L.post.n_slots ? L.pre.n_slots : L.post.n_slots;
   const int block = row_block(L);
   const int rpb = block / L.group;
-  const int64_t rrow = (L.vec == 4 && L.unaligned) ? (L.R + 6) / 4 * 4 : L.R;
+  const int64_t rrow = L.row_pitch ? L.row_pitch : (L.vec == 4 && L.unaligned) ? (L.R + 6) / 4 * 4 : L.R;
   const size_t cache = static_cast<size_t>((static_cast<int64_t>(rpb) * rrow + 3) / 4 * 4) * L.cache_loads * 4 *
                        (L.stage == 2 ? 2 : 1);  // TMA staging: double buffer
   return cache + (use_slots ? static_cast<size_t>(slots) * CH * block * (L.vec == 4 ? 16 : 4) : 0);

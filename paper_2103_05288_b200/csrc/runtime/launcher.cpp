@@ -540,6 +540,23 @@ bool short_rows_enabled() {  // DISC_SHORT_ROWS=0: the looped row kernel for sho
   return on;
 }
 
+int row_pad_mode() {  // DISC_ROW_PAD: 0 row-cache rows at pitch R, 1 padded within budget, 2 padded (A/B)
+  static const int v = [] {
+    const char* e = std::getenv("DISC_ROW_PAD");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+bool row_pad_enabled() { return row_pad_mode() != 0; }
+
+int short_rows_max() {  // rows narrower than this run one thread per row (DISC_SHORT_MAX)
+  static const int v = [] {
+    const char* e = std::getenv("DISC_SHORT_MAX");
+    return e ? std::max(2, std::min(32, std::atoi(e))) : 8;
+  }();
+  return v;
+}
+
 int sum_row_mb_force() {  // 0 off (default), 1 every fused sum row, 2 the width rule
   static const int v = [] {
     const char* e = std::getenv("DISC_SUM_ROW_MB");
@@ -640,7 +657,11 @@ int choose_row_group(int64_t K, int64_t R, int vec) {
     while (g < x && g < 1024) g <<= 1;
     return g;
   };
-  int g = np2((chunks + 31) / 32);
+  static const int cpt = [] {  // target chunks per thread (DISC_ROW_CPT, A/B)
+    const char* e = std::getenv("DISC_ROW_CPT");
+    return e ? std::max(1, std::atoi(e)) : 32;
+  }();
+  int g = np2((chunks + cpt - 1) / cpt);
   if (row_policy() == 0) {
     const int64_t need = (int64_t{sm_count()} * 1024 + K - 1) / K;
     while (g < need && g < 1024 && int64_t{g} * 4 <= chunks) g <<= 1;
@@ -1282,7 +1303,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     // head/tail, when every operand is a 16 B-aligned identity, a row splat or a constant.
     // Short rows (R < 32) run the register-resident thread-per-row kernel (see below):
     // scalar, never the unaligned float4 body; rows of 4k floats too with DISC_SHORT_VEC4.
-    const bool short_row = short_rows_enabled() && !R.wide && R.R >= 2 && R.R < 32 && (R.vec == 1 || short_vec4());
+    const bool short_row = short_rows_enabled() && !R.wide && R.R >= 2 && R.R < short_rows_max() && (R.vec == 1 || short_vec4());
     if (short_row) {
       R.vec = 1;
       R.short_rows = 1;  // pending: confirmed (or dropped) with the row group below
@@ -1505,7 +1526,21 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
         return int64_t{e ? std::atoi(e) : 32} * 1024;  // A/B: 48 -> 32 KB: BERT 5336 -> 5572 GB/s, C1/C2 flat
       }();
       const int64_t rrow = R.unaligned ? (R.R + 6) / 4 * 4 : R.R;  // padded rows (kernels.cuh row_body)
-      auto bytes = [&](int gg) { return int64_t{std::max(gg, 256) / gg} * nc * rrow * 4; };
+      // Row pitch: the 8 (float4) or 32 (scalar) threads of one shared-memory wavefront
+      // are 8/G or 32/G rows x G lanes; with a pitch of G x an odd number of bank units
+      // they hit distinct banks (thread-per-row float4 rows of 16 or 32 floats were 4- and
+      // 8-way conflicted).
+      auto pitch = [&](int gg) -> int64_t {
+        const int unit = R.vec == 4 ? 4 : 1, phase = R.vec == 4 ? 8 : 32;
+        if (!row_pad_enabled() || R.short_rows || gg >= phase) return rrow;
+        int64_t p = (rrow + unit - 1) / unit;
+        while (p % gg != 0 || (p / gg) % 2 == 0) ++p;
+        return p * unit;
+      };
+      // The pitch never changes the lane count nor exceeds the budget (DISC_ROW_PAD=2: it
+      // may, A/B): grouped launches share the largest member's shared memory.
+      auto bytes_at = [&](int gg, int64_t p) { return int64_t{std::max(gg, 256) / gg} * nc * p * 4; };
+      auto bytes = [&](int gg) { return bytes_at(gg, row_pad_mode() == 2 ? pitch(gg) : rrow); };
       // the epilogue of an argument-cached launch reads the cache: it must fit (one row of
       // up to 3 slots of 4100 floats), so such launches may exceed the budget up to 64 KB;
       // short rows stay one thread per row within that limit
@@ -1513,6 +1548,8 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
       while (nc && bytes(g) > (R.short_rows ? limit : budget) && g < 1024) g <<= 1;
       if (nc && bytes(g) <= limit) {
         R.cache_loads = nc;
+        if (pitch(g) != rrow && bytes_at(g, pitch(g)) <= std::max(bytes(g), R.short_rows ? limit : budget))
+          R.row_pitch = static_cast<int32_t>(pitch(g));
         R.pre.cache_mode = DISC_CACHE_FILL;
         R.post.cache_mode = DISC_CACHE_READ;
       } else {
