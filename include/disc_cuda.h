@@ -150,7 +150,8 @@ typedef struct {
   int32_t group;            /* ROW: threads per row (power of two) */
   int32_t splits;           /* COL: number of R splits */
   int32_t cache_loads;      /* ROW: number of shared-memory slots (0 = no cache) */
-  int32_t stage;            /* ROW: 1 = staged block tiles (see disc_program.out_slot) */
+  int32_t stage;            /* ROW: 1 = staged block tiles (see disc_program.out_slot), 2 = TMA-staged,
+                               3 = warp-staged short rows */
   float* red_out;           /* f32 reduce result [K*C] */
   double* workspace;        /* COL two-pass/atomic: f64 [splits or 1][K*C] */
   /* GENERIC: arg dims and reduced-axis mask */

@@ -679,7 +679,34 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
 // values in registers -- and reduces them with ONE sequential accumulator (the reference's
 // own order, kernels.cpp:234-259).  No column loop, no per-chunk partials; the fused
 // epilogue reads the cached reduce argument this thread wrote (no barrier).
-template <int KIND, typename Pre, typename Post, int MAXR>
+//
+// Warp-staged variant (STG, L.stage == 3): a thread-per-row warp reads 32 rows whose
+// elements sit R floats apart -- every load instruction touches ~R different lines, so
+// the L1 replays it ~R times and the kernel is issue/L1-bound (ncu: DRAM 33-42%, issue
+// slots 82-88%).  Instead each warp copies its 32 rows' contiguous span of every identity
+// operand into shared memory with 128-bit coalesced loads (all of a lane's loads issued
+// before any store: up to MAXR/4 x 16 B in flight per thread), the rows are evaluated
+// from shared memory (odd R: bank-conflict-free), staged outputs are copied back the same
+// way.  Only __syncwarp between the phases: no block barrier, warps stay independent.
+template <int U>
+__device__ __forceinline__ void warp_copy(float* __restrict__ dst, const float* __restrict__ src, int n, int lane,
+                                          bool to_global) {
+  const int n4 = n >> 2;
+  float4 r[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int i = lane + 32 * u;
+    if (i < n4) r[u] = to_global ? reinterpret_cast<const float4*>(src)[i] : __ldg(reinterpret_cast<const float4*>(src) + i);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int i = lane + 32 * u;
+    if (i < n4) reinterpret_cast<float4*>(dst)[i] = r[u];
+  }
+  for (int i = (n4 << 2) + lane; i < n; i += 32) dst[i] = to_global ? src[i] : __ldg(src + i);
+}
+
+template <int KIND, typename Pre, typename Post, int MAXR, bool STG = false>
 __device__ __forceinline__ void row_short_body(const disc_reduce_launch& L, const int bx, const int gx) {
   using RD = Red<KIND>;
   using Acc = typename RD::Acc;
@@ -697,26 +724,58 @@ __device__ __forceinline__ void row_short_body(const disc_reduce_launch& L, cons
   float* const row_cache = L.cache_loads ? cache0 + threadIdx.x * L.R : nullptr;
   float* const arg_cache = (L.arg_slot >= 0 && row_cache) ? row_cache + L.arg_slot * slot_stride : nullptr;
   const bool fuse_post = L.post.n_instr > 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t wofs = static_cast<int64_t>(threadIdx.x & ~31) * L.R;  // this warp's rows in a slot
   for (int64_t base = static_cast<int64_t>(bx) * rpb; base < L.K; base += static_cast<int64_t>(gx) * rpb) {
     const int64_t r64 = base + threadIdx.x;
-    if (r64 >= L.K) continue;
-    const I row = static_cast<I>(r64);
-    float v[MAXR];
-    Pre::template run<1, MAXR, false>(L.pre, Tile<I, false>{row, 0, R, 1, static_cast<int>(R), row_cache, sst}, v,
-                                      nullptr, 0, consts[0], 0.f);
-    Acc acc = RD::identity();
-#pragma unroll
-    for (int c = 0; c < MAXR; ++c)
-      if (c < R) {
-        acc = RD::step(acc, v[c]);
-        if (arg_cache) arg_cache[c] = v[c];
+    int nw = 0;  // this warp's element count (warp-uniform)
+    if constexpr (STG) {
+      const int64_t w0 = base + (threadIdx.x & ~31);
+      const int64_t nr = L.K - w0 < 32 ? L.K - w0 : 32;
+      if (nr <= 0) continue;  // the whole warp is past the end
+      nw = static_cast<int>(nr * L.R);
+      uint32_t seen = 0;
+      for (int q = 0; q < 2; ++q) {
+        const disc_program& P = q ? L.post : L.pre;
+        for (int l = 0; l < P.n_loads; ++l) {
+          const int k = P.cache_slot[l];
+          if (k < 0 || k == L.arg_slot || P.loads[l].mode != DISC_LOAD_IDENTITY || ((seen >> k) & 1)) continue;
+          seen |= 1u << k;
+          warp_copy<MAXR / 4>(cache0 + k * slot_stride + wofs, P.loads[l].ptr + w0 * L.R, nw, lane, false);
+        }
       }
-    const float result = static_cast<float>(acc);
-    if (L.red_out) L.red_out[row] = result;
-    if (fuse_post) {
-      float w[MAXR];
-      Post::template run<1, MAXR, false>(L.post, Tile<I, false>{row, 0, R, 1, static_cast<int>(R), row_cache, sst}, w,
-                                         nullptr, 0, consts[1], result);
+      __syncwarp();
+    }
+    if (r64 < L.K) {
+      const I row = static_cast<I>(r64);
+      float v[MAXR];
+      Pre::template run<1, MAXR, false>(L.pre, Tile<I, false, false, STG>{row, 0, R, 1, static_cast<int>(R), row_cache, sst},
+                                        v, nullptr, 0, consts[0], 0.f);
+      Acc acc = RD::identity();
+#pragma unroll
+      for (int c = 0; c < MAXR; ++c)
+        if (c < R) {
+          acc = RD::step(acc, v[c]);
+          if (arg_cache) arg_cache[c] = v[c];
+        }
+      const float result = static_cast<float>(acc);
+      if (L.red_out) L.red_out[row] = result;
+      if (fuse_post) {
+        float w[MAXR];
+        Post::template run<1, MAXR, false>(L.post, Tile<I, false, false, STG>{row, 0, R, 1, static_cast<int>(R), row_cache, sst},
+                                           w, nullptr, 0, consts[1], result);
+      }
+    }
+    if constexpr (STG) {
+      __syncwarp();
+      const int64_t w0 = base + (threadIdx.x & ~31);
+      for (int q = 0; q < 2; ++q) {
+        const disc_program& P = q ? L.post : L.pre;
+        for (int o = 0; o < P.n_outs; ++o)
+          if (P.out_slot[o] >= 0)
+            warp_copy<MAXR / 4>(P.outs[o] + w0 * L.R, cache0 + P.out_slot[o] * slot_stride + wofs, nw, lane, true);
+      }
+      __syncwarp();
     }
   }
 }
@@ -730,6 +789,9 @@ __device__ __forceinline__ void row_short_body(const disc_reduce_launch& L, cons
 // ceil(C / (lpc*VEC)), grid.y = R splits.  Per-thread partials are joined per column
 // through shared memory in a fixed order (deterministic).
 constexpr int kColThreads = 256;
+#ifndef DISC_COL_PIPE
+#define DISC_COL_PIPE 0  // software-pipelined full steps in the column pass (A/B s2 on B200: 3144 vs 3858 GB/s, off)
+#endif
 
 template <int VEC, bool WIDE, int KIND, typename Pre, int CH>
 __device__ __forceinline__ void col_body(const disc_reduce_launch& L, const int bx, const int by) {
@@ -778,6 +840,35 @@ __device__ __forceinline__ void col_body(const disc_reduce_launch& L, const int 
   if (col0 < L.C && warp == 0) {
     const int64_t step = static_cast<int64_t>(rows_per_pass) * CH;
     int64_t r = r0 + sub;
+#if DISC_COL_PIPE
+    if constexpr (Pre::kPipe > 0) {
+      // Software pipeline over full steps: the next step's streaming loads are issued
+      // before the current step computes (CH x VEC floats in flight per thread while the
+      // prologue math runs -- the tanh prologue of C3 is long).
+      using LD = typename Pre::template Loads<VEC, CH>;
+      auto tile = [&](int64_t rr) {
+        return Tile<I, true, true>{static_cast<I>(k * L.R + rr), static_cast<I>(col0), static_cast<I>(L.C),
+                                   static_cast<I>(rows_per_pass), CH};
+      };
+      if (r + (CH - 1) * rows_per_pass < r1) {
+        LD cur;
+        Pre::template load<VEC, CH, WIDE>(L.pre, tile(r), cur);
+        for (;;) {
+          const int64_t rn = r + step;
+          const bool more = rn + (CH - 1) * rows_per_pass < r1;
+          LD nxt;
+          if (more) Pre::template load<VEC, CH, WIDE>(L.pre, tile(rn), nxt);
+          T v[CH];
+          Pre::template run_loaded<VEC, CH, WIDE>(L.pre, tile(r), cur, v, slots, kColThreads, consts, 0.f);
+#pragma unroll
+          for (int c = 0; c < CH; ++c) add(v[c]);
+          r = rn;
+          if (!more) break;
+          cur = nxt;
+        }
+      }
+    }
+#endif
     // full steps: all CH rows inside [r0, r1)
     for (; r + (CH - 1) * rows_per_pass < r1; r += step) {
       T v[CH];
@@ -882,16 +973,16 @@ __global__ void __launch_bounds__(256, 6) k_row_g_mb(const __grid_constant__ dis
                                                                    G.block_off[g + 1] - G.block_off[g]);
 }
 
-template <int KIND, typename Pre, typename Post, int MAXR>
+template <int KIND, typename Pre, typename Post, int MAXR, bool STG = false>
 __global__ void __launch_bounds__(256) k_row_short(const __grid_constant__ disc_reduce_launch L) {
-  row_short_body<KIND, Pre, Post, MAXR>(L, blockIdx.x, gridDim.x);
+  row_short_body<KIND, Pre, Post, MAXR, STG>(L, blockIdx.x, gridDim.x);
 }
-template <int KIND, typename Pre, typename Post, int MAXR>
+template <int KIND, typename Pre, typename Post, int MAXR, bool STG = false>
 __global__ void __launch_bounds__(256) k_row_short_g(const __grid_constant__ disc_group G) {
   __shared__ __align__(16) unsigned char desc[desc_bytes<disc_reduce_launch>()];
   const int b = blockIdx.x, g = group_of(G, b);
   const disc_reduce_launch& L = group_stage<disc_reduce_launch>(G, g, desc);
-  row_short_body<KIND, Pre, Post, MAXR>(L, b - G.block_off[g], G.block_off[g + 1] - G.block_off[g]);
+  row_short_body<KIND, Pre, Post, MAXR, STG>(L, b - G.block_off[g], G.block_off[g + 1] - G.block_off[g]);
 }
 
 // Sum rows at <= 256 threads capped at 6 resident blocks (<= 40 registers) -- A/B knob
@@ -917,8 +1008,11 @@ __global__ void __launch_bounds__(kColThreads, 4) k_col(const __grid_constant__ 
   col_body<VEC, WIDE, KIND, Pre, CH>(L, blockIdx.x, blockIdx.y);
 }
 // Grouped column pass: launch g's 2-D grid (K * col tiles, splits) is flattened x-major.
+#ifndef DISC_COL_MINB
+#define DISC_COL_MINB 4  // resident blocks of the grouped column pass (4: <= 64 registers)
+#endif
 template <int VEC, bool WIDE, int KIND, typename Pre, int CH = kCH>
-__global__ void __launch_bounds__(kColThreads, 4) k_col_g(const __grid_constant__ disc_group G) {
+__global__ void __launch_bounds__(kColThreads, DISC_COL_MINB) k_col_g(const __grid_constant__ disc_group G) {
   __shared__ __align__(16) unsigned char desc[desc_bytes<disc_reduce_launch>()];
   const int b = blockIdx.x, g = group_of(G, b);
   const disc_reduce_launch& L = group_stage<disc_reduce_launch>(G, g, desc);
@@ -1236,12 +1330,13 @@ inline cudaError_t row_pass(const disc_reduce_launch& L, cudaStream_t s, bool us
                                   : DISC_ROW(1, true, false, C1);
   if constexpr (!std::is_same<Pre, Interp>::value) {  // register-resident short rows (generated programs)
     if (L.short_rows) {
-#define DISC_ROWS(M)                                                                                              \
-  (g ? (sum ? launch_row_group<1>(k_row_short_g<DISC_REDUCE_SUM, Pre, Post, M>, *g, s, false)                     \
-            : launch_row_group<1>(k_row_short_g<DISC_REDUCE_MAX, Pre, Post, M>, *g, s, false))                    \
-     : (sum ? launch_row_with<1>(k_row_short<DISC_REDUCE_SUM, Pre, Post, M>, L, s, false)                         \
-            : launch_row_with<1>(k_row_short<DISC_REDUCE_MAX, Pre, Post, M>, L, s, false)))
-      return L.short_rows <= 8 ? DISC_ROWS(8) : DISC_ROWS(32);
+#define DISC_ROWS(M, ST)                                                                                          \
+  (g ? (sum ? launch_row_group<1>(k_row_short_g<DISC_REDUCE_SUM, Pre, Post, M, ST>, *g, s, false)                 \
+            : launch_row_group<1>(k_row_short_g<DISC_REDUCE_MAX, Pre, Post, M, ST>, *g, s, false))                \
+     : (sum ? launch_row_with<1>(k_row_short<DISC_REDUCE_SUM, Pre, Post, M, ST>, L, s, false)                     \
+            : launch_row_with<1>(k_row_short<DISC_REDUCE_MAX, Pre, Post, M, ST>, L, s, false)))
+      if (L.stage == 3) return L.short_rows <= 8 ? DISC_ROWS(8, true) : DISC_ROWS(32, true);
+      return L.short_rows <= 8 ? DISC_ROWS(8, false) : DISC_ROWS(32, false);
 #undef DISC_ROWS
     }
   }

@@ -293,6 +293,10 @@ __host__ __device__ inline int load_class(const disc_load& L) {
   }
 }
 
+#ifndef DISC_COL_BCAST1
+#define DISC_COL_BCAST1 1  // column tiles load a row-broadcast operand once, not once per row chunk
+#endif
+
 // One load of a tile with its binding class known at compile time.  Index math in the
 // tile's index type (32-bit for !wide launches: one wide multiply-add per pointer).
 template <int VEC, int CH, bool WIDE, int CLS, typename Ctx>
@@ -332,6 +336,17 @@ __device__ __forceinline__ void load_cls(const disc_program& P, const Ctx& t, co
   } else if constexpr (CLS == kLcContig || CLS == kLcContigU) {
     const I rs = static_cast<I>(L.rs);
     const float* base = L.ptr + (static_cast<I>(L.offset) + t.row * rs + t.col0);
+    if constexpr (ROWS && DISC_COL_BCAST1) {
+      if (rs == 0) {  // column tile of a row-broadcast operand (C3's bias): one load for all chunks
+        typename Vec<VEC>::T x;
+        if constexpr (VEC == 1) x = ldg(base);
+        else if constexpr (CLS == kLcContig) x = __ldg(reinterpret_cast<const float4*>(base));
+        else x = make_float4(ldg(base), ldg(base + 1), ldg(base + 2), ldg(base + 3));
+#pragma unroll
+        for (int c = 0; c < CH; ++c) v[c] = x;
+        return;
+      }
+    }
     const I step = ROWS ? t.cstride * rs : t.cstride;
 #pragma unroll
     for (int c = 0; c < CH; ++c)

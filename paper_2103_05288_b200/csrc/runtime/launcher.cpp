@@ -557,6 +557,16 @@ int short_rows_max() {  // rows narrower than this run one thread per row (DISC_
   return v;
 }
 
+// Scalar rows narrower than this run the warp-staged short-row kernel (stage 3) when
+// their operands are 16 B aligned (DISC_WARP_STAGE_MAX; <= 2 = off, max 32).
+int warp_stage_max() {
+  static const int v = [] {
+    const char* e = std::getenv("DISC_WARP_STAGE_MAX");
+    return e ? std::min(32, std::atoi(e)) : 32;
+  }();
+  return v;
+}
+
 int sum_row_mb_force() {  // 0 off (default), 1 every fused sum row, 2 the width rule
   static const int v = [] {
     const char* e = std::getenv("DISC_SUM_ROW_MB");
@@ -1303,7 +1313,8 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     // head/tail, when every operand is a 16 B-aligned identity, a row splat or a constant.
     // Short rows (R < 32) run the register-resident thread-per-row kernel (see below):
     // scalar, never the unaligned float4 body; rows of 4k floats too with DISC_SHORT_VEC4.
-    const bool short_row = short_rows_enabled() && !R.wide && R.R >= 2 && R.R < short_rows_max() && (R.vec == 1 || short_vec4());
+    const bool short_row = short_rows_enabled() && !R.wide && R.R >= 2 &&
+                           (R.R < short_rows_max() || (R.vec == 1 && R.R < warp_stage_max())) && (R.vec == 1 || short_vec4());
     if (short_row) {
       R.vec = 1;
       R.short_rows = 1;  // pending: confirmed (or dropped) with the row group below
@@ -1414,8 +1425,21 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     // Staged short rows (stage_min() <= R < 32): scalar rows of any width (odd R is
     // bank-conflict-free, even R 2-way), float4 rows when R/4 is odd.  The cached reduce
     // argument is one more slot.
-    if (!empty && !R.wide && !R.unaligned && row_policy() >= 2 && R.R >= stage_min() && R.R < 32 &&
-        (R.vec == 1 ? ((R.R & 1) || stage_even()) : ((R.R / 4) & 1))) {
+    bool warp_stage = false;
+    // Warp-staged short rows (stage 3, generated programs): every identity operand and
+    // output of a warp's 32 rows goes through shared memory with 128-bit coalesced copies
+    // (kernels.cuh row_short_body); slots as below, 16 B-aligned operands only.
+    if (!empty && R.short_rows && g == 1 && !R.wide && warp_stage_max() > 2) {
+      bool ok = true;
+      for (const disc_program* P : {&R.pre, &R.post}) {
+        for (int l = 0; l < P->n_loads && ok; ++l)
+          if (P->loads[l].mode == DISC_LOAD_IDENTITY && P->loads[l].ptr != kArgCachePtr) ok = aligned16(P->loads[l].ptr);
+        for (int o = 0; o < P->n_outs && ok; ++o) ok = aligned16(P->outs[o]);
+      }
+      if (ok) warp_stage = true;
+    }
+    if (!empty && !R.wide && !R.unaligned && row_policy() >= 2 && R.R < 32 &&
+        (warp_stage || (R.R >= stage_min() && (R.vec == 1 ? ((R.R & 1) || stage_even()) : ((R.R / 4) & 1))))) {
       int n = 0;
       auto slot_of_ptr = [&](const float* ptr, const disc_program& P) -> int {
         for (int l = 0; l < P.n_loads; ++l)
@@ -1443,7 +1467,7 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
         if (R.post.loads[q].ptr == kArgCachePtr) arg = R.post.cache_slot[q];
       const int64_t slot_bytes = (256 * R.R + 3) / 4 * 4 * 4;
       if (n > 0 && n <= 8 && n * slot_bytes <= 112 * 1024) {
-        R.stage = 1;
+        R.stage = warp_stage ? 3 : 1;
         R.arg_slot = arg;  // the reduce pass writes it, the epilogue reads it (never copied in)
         R.cache_loads = n;
         R.pre.cache_mode = DISC_CACHE_READ;
@@ -1560,7 +1584,9 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     R.group = g;
     // Short scalar rows, one thread per row: the register-resident kernel (whole row at
     // once, one sequential accumulator) when the programs are generated ones.
-    if (R.short_rows) R.short_rows = (g == 1 && !R.stage && !R.unaligned) ? (R.R <= 8 ? 8 : 32) : 0;
+    if (R.short_rows)
+      R.short_rows = (g == 1 && (!R.stage || R.stage == 3) && !R.unaligned) ? (R.R <= 8 ? 8 : 32) : 0;
+    if (R.stage == 3 && !R.short_rows) throw InternalError("warp-staged rows without the short-row kernel");
     // Register cap (6 resident blocks, <= 40 registers) for sum rows with a fused epilogue
     // at <= 256 threads, on long rows and row widths that are multiples of 64 (A/B r3a/r3c
     // on the softmax epilogue, grouped: S = 64 4627 -> 5138, 128 5036 -> 5646, 256 4985 ->
@@ -1573,7 +1599,8 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
       const int mode = sum_row_mb_force();
       R.regcap = mode == 1 ? 1 : (mode == 2 && (R.R >= 256 || (R.R >= 64 && R.R % 64 == 0))) ? 1 : 0;
     }
-    rep.schedule = R.short_rows ? (post_fused ? "row_fused_short" : "row_short")
+    rep.schedule = R.short_rows ? (R.stage == 3 ? (post_fused ? "row_fused_short_ws" : "row_short_ws")
+                                             : (post_fused ? "row_fused_short" : "row_short"))
                    : R.stage == 2 ? (post_fused ? "row_fused_tma" : "row_tma")
                    : R.stage ? (post_fused ? "row_fused_staged" : "row_staged")
                            : post_fused ? (R.cache_loads ? "row_fused_cached" : "row_fused") : "row";

