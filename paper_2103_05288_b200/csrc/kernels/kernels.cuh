@@ -706,6 +706,15 @@ __device__ __forceinline__ void warp_copy(float* __restrict__ dst, const float* 
   for (int i = (n4 << 2) + lane; i < n; i += 32) dst[i] = to_global ? src[i] : __ldg(src + i);
 }
 
+// Rows per thread of the narrowest short rows (MAXR 8, unstaged): RPT rows' loads are
+// issued before any of them is reduced, so a thread keeps RPT x R loads in flight instead
+// of R (2-7 floats).  Shared memory (the argument cache) holds RPT x blockDim rows.
+#ifndef DISC_SHORT_RPT
+#define DISC_SHORT_RPT 4
+#endif
+template <int MAXR, bool STG>
+constexpr int short_rpt() { return (!STG && MAXR <= 8) ? DISC_SHORT_RPT : 1; }
+
 template <int KIND, typename Pre, typename Post, int MAXR, bool STG = false>
 __device__ __forceinline__ void row_short_body(const disc_reduce_launch& L, const int bx, const int gx) {
   using RD = Red<KIND>;
@@ -713,8 +722,53 @@ __device__ __forceinline__ void row_short_body(const disc_reduce_launch& L, cons
   using I = int32_t;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ float consts[2][DISC_MAX_LOADS];
+  constexpr int RPT = short_rpt<MAXR, STG>();
   const int rpb = blockDim.x;
-  const int64_t slot_stride = (static_cast<int64_t>(rpb) * L.R + 3) / 4 * 4;
+  const int64_t slot_stride = (static_cast<int64_t>(rpb) * RPT * L.R + 3) / 4 * 4;
+  if constexpr (RPT > 1) {
+    pdl_enter(L.pre);
+    hoist_consts(L.pre, consts[0]);
+    hoist_consts(L.post, consts[1]);
+    __syncthreads();
+    float* const cache0 = reinterpret_cast<float*>(smem_raw);
+    const I R = static_cast<I>(L.R), sst = static_cast<I>(slot_stride);
+    const bool fuse_post = L.post.n_instr > 0;
+    const int64_t span = static_cast<int64_t>(rpb) * RPT;
+    for (int64_t base = static_cast<int64_t>(bx) * span; base < L.K; base += static_cast<int64_t>(gx) * span) {
+      float v[RPT][MAXR];
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int64_t r64 = base + u * rpb + threadIdx.x;
+        float* const rc = L.cache_loads ? cache0 + (u * rpb + threadIdx.x) * L.R : nullptr;
+        if (r64 < L.K)
+          Pre::template run<1, MAXR, false>(L.pre, Tile<I, false>{static_cast<I>(r64), 0, R, 1, static_cast<int>(R), rc, sst},
+                                            v[u], nullptr, 0, consts[0], 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int64_t r64 = base + u * rpb + threadIdx.x;
+        if (r64 >= L.K) continue;
+        const I row = static_cast<I>(r64);
+        float* const rc = L.cache_loads ? cache0 + (u * rpb + threadIdx.x) * L.R : nullptr;
+        float* const ac = (L.arg_slot >= 0 && rc) ? rc + L.arg_slot * slot_stride : nullptr;
+        Acc acc = RD::identity();
+#pragma unroll
+        for (int c = 0; c < MAXR; ++c)
+          if (c < R) {
+            acc = RD::step(acc, v[u][c]);
+            if (ac) ac[c] = v[u][c];
+          }
+        const float result = static_cast<float>(acc);
+        if (L.red_out) L.red_out[row] = result;
+        if (fuse_post) {
+          float w[MAXR];
+          Post::template run<1, MAXR, false>(L.post, Tile<I, false>{row, 0, R, 1, static_cast<int>(R), rc, sst}, w,
+                                             nullptr, 0, consts[1], result);
+        }
+      }
+    }
+    return;
+  }
   float* const cache0 = reinterpret_cast<float*>(smem_raw);
   pdl_enter(L.pre);
   hoist_consts(L.pre, consts[0]);
@@ -1143,7 +1197,8 @@ inline size_t row_smem(const disc_reduce_launch& L, bool use_slots) {
   const int block = row_block(L);
   const int rpb = block / L.group;
   const int64_t rrow = L.row_pitch ? L.row_pitch : (L.vec == 4 && L.unaligned) ? (L.R + 6) / 4 * 4 : L.R;
-  const size_t cache = static_cast<size_t>((static_cast<int64_t>(rpb) * rrow + 3) / 4 * 4) * L.cache_loads * 4 *
+  const int rpt = (L.short_rows && L.short_rows <= 8 && L.stage != 3) ? short_rpt<8, false>() : 1;  // row_short_body
+  const size_t cache = static_cast<size_t>((static_cast<int64_t>(rpb) * rpt * rrow + 3) / 4 * 4) * L.cache_loads * 4 *
                        (L.stage == 2 ? 2 : 1);  // TMA staging: double buffer
   return cache + (use_slots ? static_cast<size_t>(slots) * CH * block * (L.vec == 4 ? 16 : 4) : 0);
 }

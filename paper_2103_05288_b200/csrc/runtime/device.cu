@@ -748,7 +748,7 @@ int disc_cuda_launch_reduce(const disc_reduce_launch* l, void* stream) {
     if (row || col)
       record(row ? "row" : "col", key,
              "\"vec\":" + std::to_string(l->vec) + ",\"stage\":" + std::to_string(row ? l->stage : 0) +
-                 ",\"short\":" + std::to_string(row ? l->short_rows : 0) + ",\"pre\":" + program_text(l->pre) +
+                 ",\"short\":" + std::to_string(row ? l->short_rows : 0) + ",\"regcap\":" + std::to_string(row ? l->regcap : 0) + ",\"pre\":" + program_text(l->pre) +
                  (row ? ",\"post\":" + program_text(l->post) : std::string()));
     return 0;
   }

@@ -558,16 +558,19 @@ int short_rows_max() {  // rows narrower than this run one thread per row (DISC_
 }
 
 // Scalar rows narrower than this run the warp-staged short-row kernel (stage 3) when
-// their operands are 16 B aligned (DISC_WARP_STAGE_MAX; <= 2 = off, max 32).
+// their operands are 16 B aligned (DISC_WARP_STAGE_MAX; <= 2 = off, max 32).  Off: A/B s3
+// on B200 (grouped softmax, 2 GB per width): S=2 2457 -> 995, S=7 5170 -> 2497, S=17
+// 2917 -> 1487, S=31 3032 -> 2208 GB/s -- 64-128 registers (the staging copies, MAXR
+// unrolled) and ~1 KB per warp in flight per round trip.
 int warp_stage_max() {
   static const int v = [] {
     const char* e = std::getenv("DISC_WARP_STAGE_MAX");
-    return e ? std::min(32, std::atoi(e)) : 32;
+    return e ? std::min(32, std::atoi(e)) : 2;
   }();
   return v;
 }
 
-int sum_row_mb_force() {  // 0 off (default), 1 every fused sum row, 2 the width rule
+int sum_row_mb_force() {  // 0 off (default), 1 every fused sum row, 2 the width rule, 3 argument-only epilogues
   static const int v = [] {
     const char* e = std::getenv("DISC_SUM_ROW_MB");
     return e ? std::atoi(e) : 0;
@@ -1597,7 +1600,13 @@ LaunchReport launch_fused(Binding& B, const std::vector<OutBuf>& outs, Issuer& i
     // off by default; DISC_SUM_ROW_MB = 1 caps every fused sum row, 2 applies the width rule.
     if (R.kind == DISC_REDUCE_SUM && post_fused && std::max(g, 256) <= 256) {
       const int mode = sum_row_mb_force();
-      R.regcap = mode == 1 ? 1 : (mode == 2 && (R.R >= 256 || (R.R >= 64 && R.R % 64 == 0))) ? 1 : 0;
+      // mode 3: epilogues that only read the cached reduce argument (softmax-like: y =
+      // arg * 1/sum) -- the pattern that gains -- not LN-like ones that re-read operands
+      bool arg_only = R.arg_slot >= 0 && R.post.n_loads >= 1;
+      for (int q = 0; q < R.post.n_loads && arg_only; ++q) arg_only = R.post.loads[q].ptr == kArgCachePtr;
+      R.regcap = mode == 1 ? 1
+                 : (mode == 2 && (R.R >= 256 || (R.R >= 64 && R.R % 64 == 0))) ? 1
+                 : (mode == 3 && arg_only && R.R >= 32) ? 1 : 0;
     }
     rep.schedule = R.short_rows ? (R.stage == 3 ? (post_fused ? "row_fused_short_ws" : "row_short_ws")
                                              : (post_fused ? "row_fused_short" : "row_short"))
