@@ -710,7 +710,7 @@ __device__ __forceinline__ void warp_copy(float* __restrict__ dst, const float* 
 // issued before any of them is reduced, so a thread keeps RPT x R loads in flight instead
 // of R (2-7 floats).  Shared memory (the argument cache) holds RPT x blockDim rows.
 #ifndef DISC_SHORT_RPT
-#define DISC_SHORT_RPT 4
+#define DISC_SHORT_RPT 1  // A/B s4 on B200 at 4: S=2 2457 -> 1735, S=7 5170 -> 4076 GB/s (56 vs 31 registers, 4x argument cache)
 #endif
 template <int MAXR, bool STG>
 constexpr int short_rpt() { return (!STG && MAXR <= 8) ? DISC_SHORT_RPT : 1; }

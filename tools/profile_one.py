@@ -19,17 +19,18 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--schedule", default="auto")
     a = ap.parse_args()
+    import types
     import paper_2103_05288_b200 as D
-    _, graph, _ = bench.workload_single(a.workload)
+    D.lib()
     syms = {k: int(v) for k, v in (kv.split("=") for kv in a.shape.split(","))}
-    plan = D.compile_graph(graph)
-    reqs = bench.Requests(D, {"g": graph}, {"g": plan}, [("g", syms)])
-    ex = D.Executor()
-    ex.set_schedule(a.schedule)
+    args = types.SimpleNamespace(schedule=a.schedule, host_threads=8, cache_gb=32.0, arena_gb=16.0, chunk_gb=32.0,
+                                 reserve_gb=0, async_flush=0)
+    B = bench.Bench(D, args, 0, bench.make_workload("sweep", 0, 10))
+    batch = B.batch([(a.workload, syms)])
     for _ in range(a.reps):
-        reqs.run(ex)
-    ex.synchronize()
-    print("records", ex.launch_records())
+        recs = B.record_pass(batch)
+    print("records", recs)
+    B.close()
 
 
 if __name__ == "__main__":

@@ -8,7 +8,7 @@ timeout 300 python tools/shape_scan.py softmax "$S" --copies-gb 2 > gpurun_out/$
 DISC_WARP_STAGE_MAX=2 timeout 300 python tools/shape_scan.py softmax "$S" --copies-gb 2 > gpurun_out/${t}_scan_sm_nows.txt 2>&1
 timeout 200 python tools/shape_scan.py bert "S=8,16,24,32" --copies-gb 2 > gpurun_out/${t}_scan_bert_ws.txt 2>&1
 DISC_WARP_STAGE_MAX=2 timeout 200 python tools/shape_scan.py bert "S=8,16,24,32" --copies-gb 2 > gpurun_out/${t}_scan_bert_nows.txt 2>&1
-bash tools/r4_ab.sh $t "main col3 col2" "colreduce" 0
+bash tools/r4_ab.sh $t "main col3" "colreduce" 0
 bash tools/r4_ab.sh $t "main" "softmax" 0
 DISC_WARP_STAGE_MAX=2 bash tools/r4_ab.sh ${t}nows "main" "softmax" 0
 timeout 1500 python -m pytest tests -m gpu -q -x --timeout 600 > gpurun_out/${t}_tests.log 2>&1
