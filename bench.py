@@ -969,12 +969,14 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-analysis", action="store_true")
     ap.add_argument("--schedule", default="auto")
-    ap.add_argument("--chunk-gb", type=float, default=32.0, help="algorithmic bytes per grouped call")
+    # A/B s7 on B200 (sweep): 32 GB 4441, 64 GB 4675, 128 GB 4818 GB/s -- fewer grouped calls,
+    # fewer level boundaries (kernel tails) per step
+    ap.add_argument("--chunk-gb", type=float, default=128.0, help="algorithmic bytes per grouped call")
     ap.add_argument("--arena-gb", type=float, default=48.0)
     ap.add_argument("--cache-gb", type=float, default=32.0, help="executor idle device-memory budget (caches + arena)")
     ap.add_argument("--async-flush", type=int, default=1, choices=[0, 1],
                     help="issue grouped launches from a background thread (flows of the next chunk overlap)")
-    ap.add_argument("--reserve-gb", type=float, default=64.0, help="executor buffer arena reserved up front")
+    ap.add_argument("--reserve-gb", type=float, default=120.0, help="executor buffer arena reserved up front")
     ap.add_argument("--e2e-gb", type=float, default=4.0, help="e2e: pinned host input bytes")
     ap.add_argument("--e2e-pipes", type=int, default=8, help="e2e: executors/streams the chunks alternate over")
     ap.add_argument("--e2e-chunk-mb", type=int, default=64, help="e2e: algorithmic MB per grouped call")

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 def _bench_args(**kw):
     a = types.SimpleNamespace(schedule="auto", host_threads=min(16, os.cpu_count() or 1), cache_gb=8.0,
-                              arena_gb=48.0, chunk_gb=32.0)
+                              arena_gb=48.0, chunk_gb=128.0)
     a.__dict__.update(kw)
     return a
 

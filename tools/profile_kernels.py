@@ -37,7 +37,7 @@ def run(args):
     import paper_2103_05288_b200 as D
     D.lib()
     a = types.SimpleNamespace(schedule="auto", host_threads=min(16, os.cpu_count() or 1), cache_gb=32.0,
-                              arena_gb=48.0, chunk_gb=32.0, reserve_gb=64.0)
+                              arena_gb=48.0, chunk_gb=128.0, reserve_gb=120.0)
     wl = bench.make_workload(args.workload, 0, args.requests)
     B = bench.Bench(D, a, 0, wl)
     reqs = wl.requests(args.step)
