@@ -112,6 +112,35 @@ struct PartAcc<DISC_REDUCE_SUM, true> {
   __device__ __forceinline__ static T add(T a, float4 v) { return add(add(add(add(a, v.x), v.y), v.z), v.w); }
   __device__ __forceinline__ static double to(T a) { return static_cast<double>(a.s) + static_cast<double>(a.c); }
 };
+// f32 -> f64 on the integer pipe (XU-bound column passes: the XU executes both the tanh
+// prologue's MUFU ops and F2F.F64.F32, ncu s9: XU 75.6% of peak, ALU 28%).  Exact for
+// normal floats (the f64 exponent is the f32 one rebiased, the mantissa shifted); zeros,
+// subnormals, infinities and NaNs (exponent field 0 or 255) take the hardware conversion,
+// for the whole warp when any lane has one, so the result is bit-identical to (double)v.
+#ifndef DISC_INT_CVT
+#define DISC_INT_CVT 0  // A/B s10 on B200: column reduce 4181 -> 3556 GB/s (the ALU work and the vote cost more than the XU relief); off
+#endif
+__device__ __forceinline__ double f2d_bits(float v, bool& special) {
+  const uint32_t u = __float_as_uint(v);
+  const uint32_t e = u & 0x7f800000u;
+  special |= (e == 0u) | (e == 0x7f800000u);
+  const uint32_t hi = (((u & 0x7fffffffu) >> 3) + 0x38000000u) | (u & 0x80000000u);
+  return __hiloint2double(static_cast<int>(hi), static_cast<int>(u << 29));
+}
+__device__ __forceinline__ void f2d4(const float4& v, double (&d)[4]) {
+  bool sp = false;
+  d[0] = f2d_bits(v.x, sp);
+  d[1] = f2d_bits(v.y, sp);
+  d[2] = f2d_bits(v.z, sp);
+  d[3] = f2d_bits(v.w, sp);
+  if (__any_sync(__activemask(), sp)) {
+    d[0] = static_cast<double>(v.x);
+    d[1] = static_cast<double>(v.y);
+    d[2] = static_cast<double>(v.z);
+    d[3] = static_cast<double>(v.w);
+  }
+}
+
 template <typename Prog>
 constexpr bool comp_sum() {
   if constexpr (DISC_COMP_SUM == 0) return false;
@@ -881,9 +910,17 @@ __device__ __forceinline__ void col_body(const disc_reduce_launch& L, const int 
   typename PA::T acc[VEC];
 #pragma unroll
   for (int i = 0; i < VEC; ++i) acc[i] = PA::identity();
+  constexpr bool kIntCvt = DISC_INT_CVT && VEC == 4 && KIND == DISC_REDUCE_SUM && Pre::kXuHeavy && !comp_sum<Pre>();
   auto add = [&](const T& v) {
     if constexpr (VEC == 1) {
       acc[0] = PA::add(acc[0], v);
+    } else if constexpr (kIntCvt) {
+      double d[4];
+      f2d4(v, d);
+      acc[0] += d[0];
+      acc[1] += d[1];
+      acc[2] += d[2];
+      acc[3] += d[3];
     } else {
       acc[0] = PA::add(acc[0], v.x);
       acc[1] = PA::add(acc[1], v.y);

@@ -525,3 +525,32 @@ def test_folded_column_reduce(gpu, ref, g, schedule):
             check_outputs(got.outputs, ref.eval_eager(g, inputs).outputs, ctx=f"C={c} N={n}")
             seen |= {r["schedule"] for r in ex.launch_records()}
     assert any("fold" in s for s in seen), seen
+
+
+def test_column_reduce_special_values(gpu, ref):
+    """The XU-heavy column pass converts f32 -> f64 on the integer pipe (kernels.cuh
+    f2d_bits); zeros, signed zeros, subnormals, infinities and NaNs must take the hardware
+    conversion: every output equals the reference's (NaN where the reference has NaN,
+    matching infinities), for columns with and without special values in one warp."""
+    import numpy as np
+    ex = gpu.Executor()
+    plan = gpu.compile_graph(COLRED)
+    rng = np.random.default_rng(11)
+    for n, c in ((4096, 256), (777, 1024), (20000, 64)):
+        x = rng.uniform(0.25, 2.0, size=(n, c)).astype(np.float32)
+        b = rng.uniform(0.25, 2.0, size=(c,)).astype(np.float32)
+        x[:, 1] = 0.0
+        x[::7, 2] = -0.0
+        x[::5, 3] = 1e-40  # subnormal
+        x[3, 4] = np.inf
+        x[5, 5] = -np.inf
+        x[9, 6] = np.nan
+        x[:, 8] = -x[:, 8]
+        x[::3, 9] = np.float32(1e-39) * -1
+        inputs = {"x": x, "b": b}
+        got = ex.run(plan, inputs).outputs[0]
+        want = ref.eval_eager(COLRED, inputs).outputs[0]
+        assert np.array_equal(np.isnan(got), np.isnan(want)), (n, c)
+        fin = np.isfinite(want)
+        assert np.array_equal(got[~fin & ~np.isnan(want)], want[~fin & ~np.isnan(want)]), (n, c)
+        check_outputs([np.where(fin, got, 0)], [np.where(fin, want, 0)], ctx=f"special N={n} C={c}")
