@@ -98,13 +98,13 @@ def merge(args):
         """ncu kernel base names a record's grouped launch can have."""
         s = sched.replace("group:", "")
         if s == "mixed" or "fold" in s:  # a folded column launch issues its tile loop first
-            return ("k_row_g", "k_row_g_mb", "k_col_g", "k_loop_g")
+            return ("k_row_g", "k_row_g_mb", "k_row_g_smb", "k_row_short_g", "k_col_g", "k_loop_g")
         if s.startswith("col"):
             return ("k_col_g",)
         if s.startswith("row1_loop") or s.startswith("loop"):
             return ("k_loop_g",)
         if s.startswith("row"):
-            return ("k_row_g", "k_row_g_mb")
+            return ("k_row_g", "k_row_g_mb", "k_row_g_smb", "k_row_short_g")
         if s.startswith("copy"):
             return ("k_copy2d_g",)
         return ()
