@@ -404,16 +404,38 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // Generic-proxy accesses of a buffer before the async proxy (TMA) overwrites it.
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+#ifndef DISC_COPY_BATCH
+#define DISC_COPY_BATCH 1  // A/B s13 (4): staged short rows stay 2-3x slower than unstaged; off
+#endif
 // Copies n floats global -> shared (or back), 16 B per access when both ends allow it.
 __device__ __forceinline__ void copy_span(float* __restrict__ dst, const float* __restrict__ src, int64_t n,
                                           bool to_global) {
   const int tid = threadIdx.x, nt = blockDim.x;
   if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
     const int64_t n4 = n >> 2;
+#if DISC_COPY_BATCH > 1
+    // DISC_COPY_BATCH float4 loads per thread issued before any store (memory-level
+    // parallelism: the plain loop waits for each load before its store)
+    constexpr int U = DISC_COPY_BATCH;
+    for (int64_t i0 = tid; i0 < n4; i0 += static_cast<int64_t>(nt) * U) {
+      float4 r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + static_cast<int64_t>(u) * nt;
+        if (i < n4) r[u] = to_global ? reinterpret_cast<const float4*>(src)[i] : __ldg(reinterpret_cast<const float4*>(src) + i);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + static_cast<int64_t>(u) * nt;
+        if (i < n4) reinterpret_cast<float4*>(dst)[i] = r[u];
+      }
+    }
+#else
     for (int64_t i = tid; i < n4; i += nt) {
       const float4 v = to_global ? reinterpret_cast<const float4*>(src)[i] : __ldg(reinterpret_cast<const float4*>(src) + i);
       reinterpret_cast<float4*>(dst)[i] = v;
     }
+#endif
     for (int64_t i = (n4 << 2) + tid; i < n; i += nt) dst[i] = to_global ? src[i] : __ldg(src + i);
   } else {
     for (int64_t i = tid; i < n; i += nt) dst[i] = to_global ? src[i] : __ldg(src + i);
