@@ -114,11 +114,38 @@ __device__ __forceinline__ float tanh_poly(float x) {  // |x| < 0.5
   const float y = __fmaf_rn(__fmul_rn(s, x), p, x);
   return fabsf(x) < 2.44140625e-4f ? x : y;
 }
+// 2^p on the FMA pipe for p in [0, 30] (DISC_TANH_EXP_POLY): p = n + f with n the nearest
+// integer (magic-number rounding, no F2I), 2^f by its degree-7 Taylor polynomial on
+// |f| <= 0.5 (relative error ~1e-9), n added to the exponent field.
+#ifndef DISC_TANH_EXP_POLY
+#define DISC_TANH_EXP_POLY 0
+#endif
+__device__ __forceinline__ float exp2_fma(float p) {
+  const float j = __fadd_rn(p, 12582912.0f);  // 1.5 * 2^23
+  const float f = __fsub_rn(p, __fsub_rn(j, 12582912.0f));
+  float q = 1.5252734e-5f;
+  q = __fmaf_rn(q, f, 1.5403530e-4f);
+  q = __fmaf_rn(q, f, 1.3333558e-3f);
+  q = __fmaf_rn(q, f, 9.6181291e-3f);
+  q = __fmaf_rn(q, f, 5.5504109e-2f);
+  q = __fmaf_rn(q, f, 2.4022651e-1f);
+  q = __fmaf_rn(q, f, 6.9314718e-1f);
+  q = __fmaf_rn(q, f, 1.0f);
+  return __int_as_float(__float_as_int(q) + ((__float_as_int(j) - 0x4B400000) << 23));
+}
 __device__ __forceinline__ float tanh_exp(float x) {  // |x| >= 0.5 (and NaN)
   float t, r;
+#if DISC_TANH_EXP_POLY
+  const float p = __fmul_rn(fabsf(x), 2.8853900817779268f);
+  t = exp2_fma(p < 30.0f ? p : 30.0f);  // tanh rounds to 1 from 2^30 on; NaN -> handled below
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__fadd_rn(t, 1.0f)));
+  const float y = copysignf(__fmaf_rn(-2.0f, r, 1.0f), x);
+  return x != x ? x : y;
+#else
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(__fmul_rn(fabsf(x), 2.8853900817779268f)));
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__fadd_rn(t, 1.0f)));
   return copysignf(__fmaf_rn(-2.0f, r, 1.0f), x);
+#endif
 }
 // Warp-uniform range dispatch (DISC_TANH_VOTE): when no active lane has an argument below
 // 0.5 (the column reduce's x + b) only the exp path runs; otherwise (GELU on normalised
