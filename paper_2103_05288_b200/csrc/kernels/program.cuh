@@ -157,6 +157,9 @@ __device__ __forceinline__ float tanh_exp(float x) {  // |x| >= 0.5 (and NaN)
 #ifndef DISC_TANH_VOTE
 #define DISC_TANH_VOTE 1
 #endif
+#ifndef DISC_TANH_TILE_VOTE
+#define DISC_TANH_TILE_VOTE 1  // generated programs: one vote per tile (un_tile), not per float4
+#endif
 __device__ __forceinline__ float tanh_vote(float x) {
   const bool small = fabsf(x) < 0.5f;
   const unsigned m = __activemask();
@@ -171,6 +174,25 @@ __device__ __forceinline__ float4 tanh_vote(float4 a) {
   const float4 y = make_float4(tanh_poly(a.x), tanh_poly(a.y), tanh_poly(a.z), tanh_poly(a.w));
   const float4 e = make_float4(tanh_exp(a.x), tanh_exp(a.y), tanh_exp(a.z), tanh_exp(a.w));
   return make_float4(sx ? y.x : e.x, sy ? y.y : e.y, sz ? y.z : e.z, sw ? y.w : e.w);
+}
+
+// A unary op over a tile's CH chunks (generated programs).  tanh: ONE warp vote for the
+// whole tile, so the exp-only path of every chunk is straight-line code the compiler can
+// interleave (per-float4 votes left 4 branch-separated chains per step).
+__device__ __forceinline__ bool tanh_small(float x) { return fabsf(x) < 0.5f; }
+__device__ __forceinline__ bool tanh_small(float4 a) {
+  return tanh_small(a.x) || tanh_small(a.y) || tanh_small(a.z) || tanh_small(a.w);
+}
+__device__ __forceinline__ float tanh_exp_v(float x) { return tanh_exp(x); }
+__device__ __forceinline__ float4 tanh_exp_v(float4 a) {
+  return make_float4(tanh_exp(a.x), tanh_exp(a.y), tanh_exp(a.z), tanh_exp(a.w));
+}
+__device__ __forceinline__ float tanh_both(float x) {
+  const float y = tanh_poly(x), e = tanh_exp(x);
+  return fabsf(x) < 0.5f ? y : e;
+}
+__device__ __forceinline__ float4 tanh_both(float4 a) {
+  return make_float4(tanh_both(a.x), tanh_both(a.y), tanh_both(a.z), tanh_both(a.w));
 }
 
 template <int OP>
@@ -201,6 +223,26 @@ __device__ __forceinline__ float4 un(float4 a) {
   if constexpr (OP == 1) return tanh_vote(a);
 #endif
   return make_float4(un1<OP>(a.x), un1<OP>(a.y), un1<OP>(a.z), un1<OP>(a.w));
+}
+template <int OP, typename T, int CH>
+__device__ __forceinline__ void un_tile(const T (&a)[CH], T (&o)[CH]) {
+#if DISC_FAST_TANH && DISC_TANH_VOTE && DISC_TANH_TILE_VOTE
+  if constexpr (OP == 1) {
+    bool sm = false;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) sm |= tanh_small(a[c]);
+    if (!__any_sync(__activemask(), sm)) {
+#pragma unroll
+      for (int c = 0; c < CH; ++c) o[c] = tanh_exp_v(a[c]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < CH; ++c) o[c] = tanh_both(a[c]);
+    }
+    return;
+  }
+#endif
+#pragma unroll
+  for (int c = 0; c < CH; ++c) o[c] = un<OP>(a[c]);
 }
 
 __device__ __forceinline__ float splat(float v, float) { return v; }

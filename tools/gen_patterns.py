@@ -143,7 +143,7 @@ def gen_program(fn, prog, ch=1, early_splat=True):
             lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = bin<{k}>({x}[c], {y}[c]);")
         else:
             k, mode = divmod(op - I_UN, 2)
-            lines.append(f"    _Pragma(\"unroll\") for (int c = 0; c < CH; ++c) {v}[c] = un<{k}>({src(mode == 1, a)}[c]);")
+            lines.append(f"    un_tile<{k}>({src(mode == 1, a)}, {v});")
         if flags & 1:
             slot_val[dst] = i
         if flags & 2:
