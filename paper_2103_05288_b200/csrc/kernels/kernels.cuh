@@ -442,6 +442,9 @@ __device__ __forceinline__ void copy_span(float* __restrict__ dst, const float* 
   }
 }
 
+#ifndef DISC_UNAL_HT_TILES
+#define DISC_UNAL_HT_TILES 0  // A/B s17 on B200: S=17 2935 -> 3233 GB/s but S=65 3443 -> 3338, C1 and the sweep flat; off
+#endif
 template <int VEC, bool WIDE, int KIND, typename Pre, typename Post, int CH, bool STAGED, bool UNAL>
 __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int bx, const int gx) {
   using RD = Red<KIND>;
@@ -650,7 +653,30 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
         }
       }
       if constexpr (UNAL && VEC == 4 && !STAGED) {
-        if (unal) {  // scalar head [0, h) and tail [Rb, R)
+        if (unal && DISC_UNAL_HT_TILES && Pre::kSplitFull && G == 1) {
+          // thread per row (generated programs): head [0, h) and tail [Rb, R) as two scalar
+          // tiles of <= 3 elements, each with its loads issued together (2 dependent round
+          // trips instead of up to 6); same accumulation order as the element loop below
+          float hv[4], tv[4];
+          if (h > 0)
+            Pre::template run<1, 4, WIDE>(L.pre, Tile<I, false>{row, 0, R, 1, static_cast<int>(h), row_cache, sst}, hv,
+                                          nullptr, 0, consts[0], 0.f);
+          if (R > Rb)
+            Pre::template run<1, 4, WIDE>(L.pre, Tile<I, false>{row, Rb, R, 1, static_cast<int>(R - Rb), row_cache, sst},
+                                          tv, nullptr, 0, consts[0], 0.f);
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            if (c < h) {
+              part[0] = PA::add(part[0], hv[c]);
+              if (arg_cache) st_cache(arg_cache + c, hv[c]);
+            }
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            if (c < R - Rb) {
+              part[0] = PA::add(part[0], tv[c]);
+              if (arg_cache) st_cache(arg_cache + Rb + c, tv[c]);
+            }
+        } else if (unal) {  // scalar head [0, h) and tail [Rb, R)
           for (I e = static_cast<I>(lane); e < h + (R - Rb); e += static_cast<I>(G)) {
             const I c = e < h ? e : Rb + (e - h);
             float vs[1];
@@ -697,7 +723,15 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
                                               slots, blockDim.x, consts[1], result);
         }
         if constexpr (UNAL && VEC == 4 && !STAGED) {
-          if (unal) {
+          if (unal && DISC_UNAL_HT_TILES && Post::kSplitFull && G == 1) {
+            float hv[4], tv[4];
+            if (h > 0)
+              Post::template run<1, 4, WIDE>(L.post, Tile<I, false>{row, 0, R, 1, static_cast<int>(h), row_cache, sst}, hv,
+                                             nullptr, 0, consts[1], result);
+            if (R > Rb)
+              Post::template run<1, 4, WIDE>(L.post, Tile<I, false>{row, Rb, R, 1, static_cast<int>(R - Rb), row_cache, sst},
+                                             tv, nullptr, 0, consts[1], result);
+          } else if (unal) {
             for (I e = static_cast<I>(lane); e < h + (R - Rb); e += static_cast<I>(G)) {
               const I c = e < h ? e : Rb + (e - h);
               float vs[1];
