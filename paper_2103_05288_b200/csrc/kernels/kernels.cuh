@@ -442,6 +442,9 @@ __device__ __forceinline__ void copy_span(float* __restrict__ dst, const float* 
   }
 }
 
+#ifndef DISC_ROW_L2PF
+#define DISC_ROW_L2PF 0  // A/B s18/s19: fused softmax epilogue +4%, but the code alone costs plain rows 20-30% (ptxas allocation); off
+#endif
 #ifndef DISC_UNAL_HT_TILES
 #define DISC_UNAL_HT_TILES 0  // A/B s17 on B200: S=17 2935 -> 3233 GB/s but S=65 3443 -> 3338, C1 and the sweep flat; off
 #endif
@@ -531,6 +534,23 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
   int it = 0;
   for (int64_t base = static_cast<int64_t>(bx) * rpb; base < rows; base += static_cast<int64_t>(gx) * rpb, ++it) {
     const int64_t n_el = (rows - base < rpb ? rows - base : rpb) * L.R;
+#if DISC_ROW_L2PF
+    if constexpr (!STAGED) {
+      // L2 prefetch of this block's NEXT rows (grid stride) for every streamed operand of the
+      // reduce pass: one prefetch per 128 B line, no registers held, so the next iteration's
+      // loads hit L2 while this one's epilogue runs (fused rows load nothing in pass 2)
+      const int64_t nb = base + static_cast<int64_t>(gx) * rpb;
+      if (nb < rows && L.post.n_instr > 0 && L.arg_slot >= 0) {  // argument-cached epilogues only (A/B s18)
+        const int64_t nn = (rows - nb < rpb ? rows - nb : rpb) * L.R;
+        for (int l = 0; l < L.pre.n_loads; ++l) {
+          if (L.pre.loads[l].mode != DISC_LOAD_IDENTITY) continue;
+          const float* p = L.pre.loads[l].ptr + nb * L.R;
+          for (int64_t i = static_cast<int64_t>(threadIdx.x) * 32; i < nn; i += static_cast<int64_t>(blockDim.x) * 32)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p + i));
+        }
+      }
+    }
+#endif
 
     if (tma) {
       const int st = it & 1;

@@ -1,0 +1,12 @@
+#!/bin/bash
+# L2 prefetch of the next rows in row kernels (variant pf)
+mkdir -p gpurun_out
+t=s18
+bash tools/r4_ab.sh $t "main pf" "softmax bert ln_gelu" 0
+for v in main pf; do
+  if [ $v = main ]; then unset DISC_LIB_VARIANT; else export DISC_LIB_VARIANT=$v; fi
+  timeout 600 python bench.py --no-cpu-baseline --no-e2e --verify off > gpurun_out/${t}_sweep_$v.json 2>> gpurun_out/${t}_err.log
+  python -c "import json; j=json.load(open('gpurun_out/${t}_sweep_$v.json')); print('sweep $v', j['value'], j['large_shape_frac_of_peak'], {k: v['GB/s'] for k, v in j['per_pattern'].items()})"
+done
+unset DISC_LIB_VARIANT
+DISC_LIB_VARIANT=pf timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "random_graphs_oracle or odd_width or edge" > gpurun_out/${t}_tests_pf.log 2>&1; tail -1 gpurun_out/${t}_tests_pf.log
