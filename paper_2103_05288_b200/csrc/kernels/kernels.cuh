@@ -443,7 +443,7 @@ __device__ __forceinline__ void copy_span(float* __restrict__ dst, const float* 
 }
 
 #ifndef DISC_ROW_L2PF
-#define DISC_ROW_L2PF 0  // A/B s18/s19: fused softmax epilogue +4%, but the code alone costs plain rows 20-30% (ptxas allocation); off
+#define DISC_ROW_L2PF 1  // A/B s20 on B200 (rows with exp/tanh in the reduce pass only): sweep 4947 -> 4976, softmax 4112 -> 4238, BERT 5444 -> 5480-5526 GB/s
 #endif
 #ifndef DISC_UNAL_HT_TILES
 #define DISC_UNAL_HT_TILES 0  // A/B s17 on B200: S=17 2935 -> 3233 GB/s but S=65 3443 -> 3338, C1 and the sweep flat; off
@@ -535,7 +535,9 @@ __device__ __forceinline__ void row_body(const disc_reduce_launch& L, const int 
   for (int64_t base = static_cast<int64_t>(bx) * rpb; base < rows; base += static_cast<int64_t>(gx) * rpb, ++it) {
     const int64_t n_el = (rows - base < rpb ? rows - base : rpb) * L.R;
 #if DISC_ROW_L2PF
-    if constexpr (!STAGED) {
+    // only compiled into rows whose reduce pass evaluates exp/tanh (softmax-like fused
+    // epilogues): the code alone changes ptxas's allocation of the plain row kernels
+    if constexpr (!STAGED && Pre::kXuHeavy) {
       // L2 prefetch of this block's NEXT rows (grid stride) for every streamed operand of the
       // reduce pass: one prefetch per 128 B line, no registers held, so the next iteration's
       // loads hit L2 while this one's epilogue runs (fused rows load nothing in pass 2)

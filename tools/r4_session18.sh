@@ -1,6 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
-t=s19
+t=s20
 bash tools/r4_ab.sh $t "pf" "softmax bert ln_gelu" 0
 for v in pf main pf; do
   if [ $v = main ]; then unset DISC_LIB_VARIANT; else export DISC_LIB_VARIANT=$v; fi
