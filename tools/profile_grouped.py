@@ -18,14 +18,17 @@ def main():
     ap.add_argument("--workload", default="ln_gelu")
     ap.add_argument("--reps", type=int, default=2)
     a = ap.parse_args()
+    import types
     import paper_2103_05288_b200 as D
-    _, graphs, reqs = bench.workload(a.workload)
-    plans = {k: D.compile_graph(g) for k, g in graphs.items()}
-    rq = bench.Requests(D, graphs, plans, reqs)
-    ex = D.Executor()
+    D.lib()
+    args = types.SimpleNamespace(schedule="auto", host_threads=8, cache_gb=32.0, arena_gb=16.0, chunk_gb=128.0,
+                                 reserve_gb=0, async_flush=0)
+    wl = bench.make_workload(a.workload, 0, 10000)
+    B = bench.Bench(D, args, 0, wl)
+    batch = B.batch(wl.requests(0))
     for _ in range(a.reps):
-        rq.run_grouped(ex)
-    ex.synchronize()
+        batch.run(B.ex)
+    B.close()
 
 
 if __name__ == "__main__":

@@ -2,7 +2,7 @@
 # Final evidence of the round: the driver's bench command and reference arm, smoke, the
 # per-key ncu traffic (profiles/ncu_traffic.json) and the ncu launch list / full sets.
 mkdir -p gpurun_out
-t=r4f
+t=r4g
 timeout 1800 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/${t}_tests.log 2>&1; tail -2 gpurun_out/${t}_tests.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${t}_smoke.log 2>&1; tail -1 gpurun_out/${t}_smoke.log
 timeout 900 python bench.py > gpurun_out/${t}_bench.json 2> gpurun_out/${t}_bench.err
